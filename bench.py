@@ -1,0 +1,424 @@
+"""Benchmark of the B200 state-vector engine on BASELINE.json's configs.
+
+Default workload (N=1): config 2 -- 28-qubit random brickwork, depth 20
+(830 gates: 560 Haar-random U3 + 270 CNOT), complex128, from |0...0>.
+One step = evolve(prepare("0"*28), circuit) on resident HBM state.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+                    [--extra ucc12,expect30,ucc32]
+
+Prints ONE JSON line (rank 0).  value = amplitude-updates/s (sum over the 830
+gates of 2^n, per second, whole job); e2e = the same metric through the public
+backend API with host buffers (gate arrays in, full amplitude vector out to
+pinned host memory) inside the timed region.  roofline = the dominant kernel
+(tile_pass_kernel): algorithmic 32 B x 2^n per launch over its average launch
+duration (CUDA events on the library's stream), vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline = the reference (oracle/_ref: vqekit + Cython kernels, 1 thread --
+the reference evolve is single-threaded) on a bounded sample of the same
+circuit.  For N > 1 each rank runs an independent replica (the sharded 36q
+path is config 5, not this line): scaling "weak".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_QUBITS = 28
+LAYERS = 20
+SEED = 0
+REF_SAMPLE_GATES = 6  # reference arm: first gates of the circuit per step (~1.2-2.5 s each)
+
+
+def load_peaks() -> tuple[float, str]:
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# reference / CPU baseline
+# ---------------------------------------------------------------------------
+
+
+def _reference_modules():
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "vqekit")):
+        sys.path.insert(0, ref)
+        try:
+            import vqekit.circuit as RC
+            import vqekit.kernels as RK
+            import vqekit.statevector as RSV
+            if RK.IMPLEMENTATION == "cython":
+                return "reference", RC, RSV
+        except Exception:
+            pass
+    return "port", None, None
+
+
+def cpu_sample_run(circuit, n_gates: int):
+    """Time the reference evolve of the first n_gates gates on a 2^n state.
+    Returns (seconds, kind, description)."""
+    import numpy as np
+
+    kind, RC, RSV = _reference_modules()
+    n = circuit.n_qubits
+    gates = circuit.gates[:n_gates]
+    if kind == "reference":
+        rgates = tuple(RC.Gate(g.kind, g.qubits, tuple(RC.Constant(p.value) for p in g.params))
+                       for g in gates)
+        rc = RC.Circuit(n, rgates, 0)
+        amps = np.zeros(1 << n, dtype=np.complex128)
+        amps[0] = 1.0
+        s0 = RSV.StateVector(n, amps)
+        t0 = time.perf_counter()
+        RSV.evolve(s0, rc)  # includes the reference's own state copy (statevector.py:71)
+        dt = time.perf_counter() - t0
+        desc = (f"first {n_gates} of {len(circuit.gates)} gates of the {n}q brickwork via "
+                "vqekit.statevector.evolve (oracle/_ref, Cython kernels, 1 thread)")
+        return dt, kind, desc
+    from oracle import oracle as O
+
+    amps = np.zeros(1 << n, dtype=np.complex128)
+    amps[0] = 1.0
+    t0 = time.perf_counter()
+    O.evolve(amps, gates)
+    dt = time.perf_counter() - t0
+    return dt, "port", f"first {n_gates} gates via oracle/oracle.c (C restatement, 1 thread)"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2208_10978_b200 import workloads as W
+
+    circ = W.brickwork(N_QUBITS, LAYERS, SEED)
+    for _ in range(args.warmup):
+        cpu_sample_run(circ, REF_SAMPLE_GATES)
+    times = []
+    kind = desc = None
+    for _ in range(args.steps):
+        dt, kind, desc = cpu_sample_run(circ, REF_SAMPLE_GATES)
+        times.append(dt)
+    per = sum(times) / len(times)
+    value = REF_SAMPLE_GATES * (1 << N_QUBITS) / per
+    line = {
+        "impl": "reference", "metric": "amplitude-updates/s", "value": value,
+        "unit": "amplitude-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic",
+        "config": {"workload": "config2: 28q random brickwork depth 20 (830 gates), seed 0",
+                   "sample": f"first {REF_SAMPLE_GATES} gates per step"},
+        "cpu_baseline": {"value": value, "unit": "amplitude-updates/s", "cores": 1, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "amplitude-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# engine
+# ---------------------------------------------------------------------------
+
+
+def extra_ucc12(steps=20):
+    import torch
+
+    from paper_2208_10978_b200 import engine
+    from paper_2208_10978_b200 import statevector as sv
+    from paper_2208_10978_b200 import workloads as W
+
+    cfg = W.config1(seed=0)
+    be = engine.StateVectorBackend()
+    s0 = be.prepare(cfg["reference"])
+    for _ in range(3):
+        be.expectation(be.evolve(s0, cfg["circuit"]), cfg["hamiltonian"])
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        e = be.expectation(be.evolve(s0, cfg["circuit"]), cfg["hamiltonian"])
+    dt = (time.perf_counter() - t0) / steps
+    return {"workload": "config1: 12q UCCSD-shaped (1,872 rotations = 37,824 gates) + 500-term H",
+            "metric": "energy evals/s", "value": 1.0 / dt, "ms_per_eval": dt * 1e3, "energy": e,
+            "passes": sv.last_plan_stats()["n_passes"]}
+
+
+def extra_expect30(steps=3):
+    import torch
+
+    from paper_2208_10978_b200 import statevector as sv
+    from paper_2208_10978_b200 import workloads as W
+
+    n = 30
+    h = W.config3_hamiltonian(seed=0)
+    s = sv.StateVector._empty(n)
+    view = torch.as_tensor(s, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(0)
+    view.copy_(torch.randn(view.shape, dtype=torch.float64, device="cuda", generator=g))
+    view /= torch.linalg.vector_norm(view)
+    torch.cuda.synchronize()
+    sv.expectation_terms(s, h)  # plan + warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        re, im, _ = sv.expectation_terms(s, h)
+    dt = (time.perf_counter() - t0) / steps
+    st = sv.last_plan_stats()
+    prods = len(h) * (1 << n)
+    return {"workload": "config3: 30q expectation, 10,000 strings (30% Z-only), random state "
+                        "(torch-generated on device)",
+            "metric": "expectations/s", "value": 1.0 / dt, "ms_per_eval": dt * 1e3,
+            "sweeps": st["n_passes"], "term_amplitude_products_per_s": prods / dt,
+            "hbm_gbs_sweeps": st["n_passes"] * 16 * (1 << n) / dt / 1e9}
+
+
+def extra_ucc32(steps=1):
+    from paper_2208_10978_b200 import engine
+    from paper_2208_10978_b200 import statevector as sv
+    from paper_2208_10978_b200 import workloads as W
+
+    cfg = W.config4(seed=0)
+    be = engine.StateVectorBackend()
+    s0 = be.prepare(cfg["reference"])
+    psi = be.evolve(s0, cfg["circuit"])
+    e = be.expectation(psi, cfg["hamiltonian"])
+    del psi
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        psi = be.evolve(s0, cfg["circuit"])
+        st_ev = sv.last_plan_stats()
+        e = be.expectation(psi, cfg["hamiltonian"])
+        del psi
+    dt = (time.perf_counter() - t0) / steps
+    return {"workload": "config4: 32q UCC (16,512 rotations) + 5,000-term H",
+            "metric": "energy evals/s", "value": 1.0 / dt, "s_per_eval": dt, "energy": e,
+            "evolve_passes": st_ev["n_passes"]}
+
+
+def run_engine(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    from paper_2208_10978_b200 import engine
+    from paper_2208_10978_b200 import statevector as sv
+    from paper_2208_10978_b200 import workloads as W
+    from paper_2208_10978_b200 import _lib
+    from paper_2208_10978_b200.circuit import flatten_bound
+
+    torch.cuda.set_device(local)
+    dev = local
+    circ = W.brickwork(N_QUBITS, LAYERS, SEED)
+    G = len(circ.gates)
+    dim = 1 << N_QUBITS
+    be = engine.StateVectorBackend(device=dev)
+
+    # library stream -> torch events
+    probe = sv.init_state("0" * N_QUBITS, dev)
+    probe._ensure()
+    import ctypes
+    sp = ctypes.c_void_p()
+    _lib.check(_lib.lib().qsv_get_stream(probe.handle, ctypes.byref(sp)))
+    stream = torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", dev))
+    del probe
+
+    def step():
+        return sv.evolve(be.prepare("0" * N_QUBITS), circ)
+
+    for _ in range(args.warmup):
+        psi = step()
+        del psi
+    stats = sv.last_plan_stats()
+    passes = stats["n_passes"]
+    torch.cuda.synchronize(dev)
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize(dev)
+        start.record(stream)
+        for _ in range(args.steps):
+            psi = step()
+            del psi
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    t_step = start.elapsed_time(end) / 1e3 / args.steps
+
+    # set_basis share of a step (one elementwise write of 16 B x 2^n)
+    tmp = sv.StateVector._empty(N_QUBITS, dev)
+    b0 = torch.cuda.Event(enable_timing=True)
+    b1 = torch.cuda.Event(enable_timing=True)
+    b0.record(stream)
+    for _ in range(args.steps):
+        _lib.check(_lib.lib().qsv_set_basis(tmp.handle, 0))
+    b1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_basis = b0.elapsed_time(b1) / 1e3 / args.steps
+    del tmp
+    t_pass = (t_step - t_basis) / passes
+
+    t_max = t_step
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+
+    value = world * G * dim / t_max
+
+    # e2e: public API with host buffers (gate arrays in, full state out to pinned host)
+    host_out = torch.empty(dim, dtype=torch.complex128, pin_memory=True).numpy()
+    kinds, qubits, values = flatten_bound(circ)
+    h2d = kinds.nbytes + qubits.nbytes + values.nbytes
+    e2e_steps = max(1, min(args.steps, 3))
+    psi = be.evolve(be.prepare("0" * N_QUBITS), circ)
+    psi.download_into(host_out)
+    del psi
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sv._FLAT_CACHE.clear()  # re-read the gate list from the host objects every step
+        psi = be.evolve(be.prepare("0" * N_QUBITS), circ)
+        psi.download_into(host_out)
+        del psi
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    e2e_val = world * G * dim / t_e2e
+    if rank == 0:
+        assert abs(np.linalg.norm(host_out) - 1.0) < 1e-9
+
+    peak, peak_kind = load_peaks()
+    achieved = 32.0 * dim / t_pass / 1e9
+    line = {
+        "metric": "amplitude-updates/s", "value": value, "unit": "amplitude-updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic",
+        "config": {"workload": "config2: 28q random brickwork depth 20 (830 gates: 560 U3 + 270 CNOT), "
+                               "seed 0, from |0...0>", "n_qubits": N_QUBITS, "gates": G,
+                   "hbm_passes_per_step": passes, "l2": "state 4 GiB >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"replica x{world}"},
+        "e2e": {"value": e2e_val, "unit": "amplitude-updates/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": 16 * dim, "ms_per_step": t_e2e * 1e3},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "tile_pass_kernel",
+                     "ms_per_launch": t_pass * 1e3, "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": 32 * dim},
+        "gpu_launches": args.steps * (passes + 1),
+        "clocks": clocks.summary(),
+    }
+
+    extras = [e for e in (args.extra or "").split(",") if e]
+    if rank == 0 and extras:
+        line["extra"] = {}
+        for e in extras:
+            fn = {"ucc12": extra_ucc12, "expect30": extra_expect30, "ucc32": extra_ucc32}[e]
+            line["extra"][e] = fn()
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dt, kind, desc = cpu_sample_run(circ, REF_SAMPLE_GATES)
+        line["cpu_baseline"] = {"value": REF_SAMPLE_GATES * dim / dt, "unit": "amplitude-updates/s",
+                                "cores": 1, "kind": kind, "sample": desc, "seconds": dt}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--extra", default="")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    run_engine(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * qsv.h -- C ABI of the B200 (sm_100a) state-vector engine (libqsv.so).
+ *
+ * Drop-in boundary for the state-vector hot path of vqekit
+ * (/root/reference/pkg/src/vqekit).  Every entry point names the reference
+ * interface it replaces (file:line, relative to /root/reference/pkg/src/vqekit).
+ *
+ * Conventions
+ *  - A state is 2^n complex128 amplitudes; basis-index bit k is qubit k
+ *    (statevector.py:1-6).  Host buffers are interleaved (re, im) doubles in
+ *    index order -- the little-endian <c16 layout of dump_state
+ *    (statevector.py:214-216).  Pin host buffers for full PCIe speed.
+ *  - Device memory is owned by the handle; host pointers are borrowed for
+ *    the duration of the call only.  All calls are ordered on the handle's
+ *    CUDA stream; calls that return host values synchronise that stream.
+ *  - Every call returns QSV_OK (0) or an error code; qsv_last_error() gives a
+ *    thread-local message.  The Python layer maps codes to the reference's
+ *    exception types (errors.py:9-22; ValueError / ArithmeticError).
+ *  - Gate kinds are the reference's closed gate set (circuit.py:27-34):
+ *    H=0 HY=1 X=2 CNOT=3 SWAP=4 RZ=5 RY=6 U3=7 CU3=8.  For two-qubit gates the
+ *    first qubit is the control / most-significant bit of the 4x4 matrix
+ *    (circuit.py:5-6).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    call fails with QSV_ERR_CUDA.
+ */
+#ifndef QSV_H
+#define QSV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSV_ABI_VERSION 1
+
+#define QSV_OK 0
+#define QSV_ERR_INVALID 1  /* bad argument (ValueError) */
+#define QSV_ERR_CUDA 2     /* CUDA runtime failure / no device */
+#define QSV_ERR_NOMEM 3    /* device or pinned allocation failed */
+#define QSV_ERR_RESOURCE 4 /* request exceeds a hard cap (ResourceLimitError) */
+
+typedef struct qsv_state qsv_state;
+
+/* Plan statistics of the last qsv_apply_gates / qsv_apply_pauli_rotations /
+ * qsv_expectation call on the calling thread. */
+typedef struct qsv_plan_stats {
+    int64_t n_input_ops;   /* gates or rotations or terms passed in */
+    int64_t n_rotations;   /* evolution blocks recognised as Pauli rotations */
+    int64_t n_items;       /* scheduled items (gates + rotation groups / term groups) */
+    int64_t n_passes;      /* HBM passes launched (each reads + writes, or reads, every amplitude) */
+    int64_t n_fallback;    /* passes that had to use the global (non-tile) kernel */
+    int32_t tile_bits;     /* qubits resident per shared-memory tile */
+    int32_t cache_hit;     /* 1 if the structural plan came from the cache */
+} qsv_plan_stats;
+
+int qsv_abi_version(void);
+const char *qsv_last_error(void);
+int qsv_device_count(int *out);
+
+/* Handle lifetime.  qsv_create allocates 16 * 2^n bytes on `device` and
+ * leaves the amplitudes uninitialised.  (StateVector, statevector.py:26-39) */
+int qsv_create(qsv_state **out, int n_qubits, int device);
+int qsv_destroy(qsv_state *s);
+int qsv_n_qubits(const qsv_state *s, int *out);
+int qsv_set_stream(qsv_state *s, void *cuda_stream); /* NULL -> library-owned stream */
+int qsv_get_stream(const qsv_state *s, void **cuda_stream);
+int qsv_device_ptr(const qsv_state *s, void **ptr);   /* zero-copy view (DLPack/torch) */
+int qsv_synchronize(qsv_state *s);
+
+/* StateVector.copy (statevector.py:38-39) / the copy in evolve (statevector.py:71). */
+int qsv_copy(qsv_state *dst, const qsv_state *src);
+/* init_state (statevector.py:42-54): |index>. */
+int qsv_set_basis(qsv_state *s, uint64_t index);
+/* Host <-> device in dump_state layout (statevector.py:214-216). */
+int qsv_upload(qsv_state *s, const double *host);
+int qsv_download(const qsv_state *s, double *host);
+
+/* kernels.apply_1q (kernels/__init__.py:21; _cykernels.pyx:19-38): m = 2x2 row-major complex128. */
+int qsv_apply_1q(qsv_state *s, const double *m, int qubit);
+/* kernels.apply_2q (kernels/__init__.py:22; _cykernels.pyx:41-73): m = 4x4, rows 2*bit(q0)+bit(q1). */
+int qsv_apply_2q(qsv_state *s, const double *m, int q0, int q1);
+/* kernels.apply_pauli (kernels/__init__.py:23; _cykernels.pyx:76-102): dst = P src. */
+int qsv_apply_pauli(const qsv_state *src, qsv_state *dst, uint64_t x, uint64_t y, uint64_t z);
+
+/* evolve's gate loop (statevector.py:65-74 via _apply_gate :57-62) for a bound
+ * circuit: kinds[g], qubits[2g..2g+1] (second = -1 for 1q gates),
+ * values[3g..3g+2] (bound parameter values, circuit.py:106-109).  The engine
+ * recognises pauli_evolution blocks (circuit.py:271-281) as direct Pauli
+ * rotations, fuses everything into shared-memory tile passes and applies it
+ * in place.  stats may be NULL. */
+int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                    const double *values, qsv_plan_stats *stats);
+
+/* Product of exp(-i theta_r / 2 P_r), r = 0..n-1 in order (P_r given by X/Y/Z
+ * bit masks as in statevector._string_masks, statevector.py:77-88).  Equals
+ * evolve() of pauli_evolution(P_r, -theta_r/2) blocks (circuit.py:254-281). */
+int qsv_apply_pauli_rotations(qsv_state *s, int64_t n, const uint64_t *x, const uint64_t *y,
+                              const uint64_t *z, const double *theta, qsv_plan_stats *stats);
+
+/* expectation (statevector.py:98-110): out = sum_t c_t <psi|P_t|psi>.
+ * out_re receives the real part, out_im the imaginary residue contributed by
+ * Im(c_t) (the caller raises above 1e-10, statevector.py:108-109).
+ * per_term (nullable, n_terms doubles) receives <psi|P_t|psi> (real). */
+int qsv_expectation(const qsv_state *s, int64_t n_terms, const uint64_t *x, const uint64_t *y,
+                    const uint64_t *z, const double *coef_re, const double *coef_im,
+                    double *out_re, double *out_im, double *per_term, qsv_plan_stats *stats);
+
+/* apply_operator (statevector.py:113-121): dst = sum_t c_t P_t src. */
+int qsv_apply_operator(const qsv_state *src, qsv_state *dst, int64_t n_terms, const uint64_t *x,
+                       const uint64_t *y, const uint64_t *z, const double *coef_re,
+                       const double *coef_im);
+
+/* np.vdot(a, b) (engine.py:74-75, statevector.py:107): out2 = {re, im}. */
+int qsv_vdot(const qsv_state *a, const qsv_state *b, double *out2);
+/* StateVector.norm (statevector.py:35-36). */
+int qsv_norm(const qsv_state *s, double *out);
+/* y = alpha*y + beta*x (axpy of apply_operator, statevector.py:120). */
+int qsv_axpby(qsv_state *y, const qsv_state *x, double alpha_re, double alpha_im, double beta_re,
+              double beta_im);
+
+/* Planner only (no device work; usable without a GPU): the plan that
+ * qsv_apply_gates / qsv_expectation would execute for these inputs. */
+int qsv_plan_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                   qsv_plan_stats *out);
+int qsv_plan_expectation(int n_qubits, int64_t n_terms, const uint64_t *x, const uint64_t *y,
+                         const uint64_t *z, qsv_plan_stats *out);
+
+/* Statistics of the last plan on the calling thread (see qsv_plan_stats). */
+int qsv_last_plan_stats(qsv_plan_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSV_H */

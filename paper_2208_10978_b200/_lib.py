@@ -1,0 +1,142 @@
+"""ctypes binding of libqsv.so (include/qsv.h).
+
+The CUDA library is the only compute path of this package: if it is missing
+or no sm_100 device is visible, the first call raises -- there is no CPU
+fallback.  ctypes releases the GIL for the duration of each call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ResourceLimitError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqsv.so")
+
+QSV_OK = 0
+QSV_ERR_INVALID = 1
+QSV_ERR_CUDA = 2
+QSV_ERR_NOMEM = 3
+QSV_ERR_RESOURCE = 4
+
+# Gate kind codes of the C ABI (reference gate set, circuit.py:27-34).
+KIND_CODES = {"H": 0, "HY": 1, "X": 2, "CNOT": 3, "SWAP": 4, "RZ": 5, "RY": 6, "U3": 7, "CU3": 8}
+
+
+class QsvCudaError(RuntimeError):
+    """The CUDA runtime failed (no device, launch failure, ...)."""
+
+
+class PlanStats(ctypes.Structure):
+    _fields_ = [
+        ("n_input_ops", ctypes.c_int64),
+        ("n_rotations", ctypes.c_int64),
+        ("n_items", ctypes.c_int64),
+        ("n_passes", ctypes.c_int64),
+        ("n_fallback", ctypes.c_int64),
+        ("tile_bits", ctypes.c_int32),
+        ("cache_hit", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+# Every symbol include/qsv.h declares (checked by tests/test_abi_cpu.py).
+EXPORTED = (
+    "qsv_abi_version", "qsv_last_error", "qsv_device_count", "qsv_create", "qsv_destroy",
+    "qsv_n_qubits", "qsv_set_stream", "qsv_get_stream", "qsv_device_ptr", "qsv_synchronize",
+    "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_apply_1q", "qsv_apply_2q",
+    "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
+    "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
+    "qsv_plan_expectation", "qsv_last_plan_stats",
+)
+
+_lib = None
+
+
+def _declare(L):
+    vp, dp, i64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64
+    u64, u64p = ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    sp = ctypes.POINTER(PlanStats)
+    sig = {
+        "qsv_abi_version": ([], ctypes.c_int),
+        "qsv_last_error": ([], ctypes.c_char_p),
+        "qsv_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "qsv_create": ([ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "qsv_destroy": ([vp], ctypes.c_int),
+        "qsv_n_qubits": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "qsv_set_stream": ([vp, vp], ctypes.c_int),
+        "qsv_get_stream": ([vp, ctypes.POINTER(vp)], ctypes.c_int),
+        "qsv_device_ptr": ([vp, ctypes.POINTER(vp)], ctypes.c_int),
+        "qsv_synchronize": ([vp], ctypes.c_int),
+        "qsv_copy": ([vp, vp], ctypes.c_int),
+        "qsv_set_basis": ([vp, u64], ctypes.c_int),
+        "qsv_upload": ([vp, vp], ctypes.c_int),
+        "qsv_download": ([vp, vp], ctypes.c_int),
+        "qsv_apply_1q": ([vp, dp, ctypes.c_int], ctypes.c_int),
+        "qsv_apply_2q": ([vp, dp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "qsv_apply_pauli": ([vp, vp, u64, u64, u64], ctypes.c_int),
+        "qsv_apply_gates": ([vp, i64, i32p, i32p, dp, sp], ctypes.c_int),
+        "qsv_apply_pauli_rotations": ([vp, i64, u64p, u64p, u64p, dp, sp], ctypes.c_int),
+        "qsv_expectation": ([vp, i64, u64p, u64p, u64p, dp, dp, dp, dp, dp, sp], ctypes.c_int),
+        "qsv_apply_operator": ([vp, vp, i64, u64p, u64p, u64p, dp, dp], ctypes.c_int),
+        "qsv_vdot": ([vp, vp, dp], ctypes.c_int),
+        "qsv_norm": ([vp, dp], ctypes.c_int),
+        "qsv_axpby": ([vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                       ctypes.c_double], ctypes.c_int),
+        "qsv_plan_gates": ([ctypes.c_int, i64, i32p, i32p, sp], ctypes.c_int),
+        "qsv_plan_expectation": ([ctypes.c_int, i64, u64p, u64p, u64p, sp], ctypes.c_int),
+        "qsv_last_plan_stats": ([sp], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib():
+    """Load libqsv.so; raises ImportError if the extension was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        _declare(L)
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == QSV_OK:
+        return
+    msg = lib().qsv_last_error().decode("utf-8", "replace")
+    if rc == QSV_ERR_INVALID:
+        raise ValueError(msg)
+    if rc in (QSV_ERR_RESOURCE, QSV_ERR_NOMEM):
+        raise ResourceLimitError(msg)
+    raise QsvCudaError(msg)
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    rc = lib().qsv_device_count(ctypes.byref(n))
+    return n.value if rc == QSV_OK else 0
+
+
+def dptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def u64ptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+
+
+def i32ptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))

@@ -1,0 +1,248 @@
+"""Gate-level circuit IR consumed by the engine.
+
+Mirrors the input contract of the reference's circuit module
+(circuit.py:27-156): the closed gate set {H, HY, X, CNOT, SWAP, RZ, RY, U3,
+CU3}; the first qubit of a two-qubit gate is the control and the
+most-significant bit of its 4x4 matrix (circuit.py:5-6); parameters are
+``Constant`` or ``Affine`` (scale * theta[index] + offset) and ``bind``
+evaluates them.  The engine consumes circuits duck-typed (``gate.kind``,
+``gate.qubits``, ``gate.params``/``gate.bound_values()``), so reference
+``Circuit`` objects work unchanged; these classes let the engine run without
+the reference.  ``pauli_evolution`` reproduces the gate pattern of
+circuit.py:254-281 exactly -- that pattern is what the native planner
+recognises and turns back into one direct Pauli rotation.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+
+GATE_QUBITS = {"H": 1, "HY": 1, "X": 1, "RZ": 1, "RY": 1, "U3": 1, "CNOT": 2, "SWAP": 2, "CU3": 2}
+GATE_PARAMS = {"H": 0, "HY": 0, "X": 0, "CNOT": 0, "SWAP": 0, "RZ": 1, "RY": 1, "U3": 3, "CU3": 3}
+
+
+@dataclass(frozen=True)
+class Constant:
+    value: float
+
+    def evaluate(self, theta) -> float:
+        return self.value
+
+
+@dataclass(frozen=True)
+class Affine:
+    index: int
+    scale: float
+    offset: float = 0.0
+
+    def __post_init__(self):
+        if self.index < 0:
+            raise ValueError("negative parameter index")
+        if not math.isfinite(self.scale) or self.scale == 0.0:
+            raise ValueError("affine scale must be finite and non-zero")
+
+    def evaluate(self, theta) -> float:
+        return self.scale * theta[self.index] + self.offset
+
+
+@dataclass(frozen=True)
+class Gate:
+    kind: str
+    qubits: tuple[int, ...]
+    params: tuple = ()
+
+    def __post_init__(self):
+        if self.kind not in GATE_QUBITS:
+            raise ValueError(f"unknown gate kind {self.kind!r}")
+        object.__setattr__(self, "qubits", tuple(self.qubits))
+        object.__setattr__(self, "params", tuple(self.params))
+        if len(self.qubits) != GATE_QUBITS[self.kind]:
+            raise ValueError(f"{self.kind} expects {GATE_QUBITS[self.kind]} qubits")
+        if len(set(self.qubits)) != len(self.qubits):
+            raise ValueError("gate qubit indices must be distinct")
+        if any(q < 0 for q in self.qubits):
+            raise ValueError("negative qubit index")
+        if len(self.params) != GATE_PARAMS[self.kind]:
+            raise ValueError(f"{self.kind} expects {GATE_PARAMS[self.kind]} parameters")
+
+    def is_bound(self) -> bool:
+        return all(isinstance(p, Constant) for p in self.params)
+
+    def bound_values(self) -> tuple[float, ...]:
+        if not self.is_bound():
+            raise RuntimeError(f"gate {self.kind} has unbound parameters")
+        return tuple(p.value for p in self.params)
+
+
+@dataclass(frozen=True)
+class Circuit:
+    n_qubits: int
+    gates: tuple[Gate, ...] = ()
+    n_params: int = 0
+
+    def __post_init__(self):
+        object.__setattr__(self, "gates", tuple(self.gates))
+        for g in self.gates:
+            if any(q >= self.n_qubits for q in g.qubits):
+                raise ValueError(f"gate {g.kind} addresses qubit outside 0..{self.n_qubits - 1}")
+            for p in g.params:
+                if isinstance(p, Affine) and p.index >= self.n_params:
+                    raise ValueError(f"parameter index {p.index} out of range")
+
+    def is_bound(self) -> bool:
+        return all(g.is_bound() for g in self.gates)
+
+    def __len__(self) -> int:
+        return len(self.gates)
+
+
+def bind(c, theta: Sequence[float]) -> Circuit:
+    theta = np.asarray(theta, dtype=float)
+    if theta.shape != (c.n_params,):
+        raise ValueError(f"expected {c.n_params} parameter values, got {theta.shape}")
+    if not np.all(np.isfinite(theta)):
+        raise ValueError("parameter values must be finite")
+    gates = tuple(Gate(g.kind, g.qubits, tuple(Constant(float(p.evaluate(theta))) for p in g.params))
+                  for g in c.gates)
+    return Circuit(c.n_qubits, gates, 0)
+
+
+def gate_matrix(kind: str, values: Sequence[float] = ()) -> np.ndarray:
+    """Dense gate matrix (row-major complex128); same convention as the native
+    planner's restatement of circuit.py:198-223."""
+    code = _lib.KIND_CODES[kind]
+    if kind in ("X", "CNOT", "SWAP"):
+        return {
+            "X": np.array([[0, 1], [1, 0]], dtype=complex),
+            "CNOT": np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]], dtype=complex),
+            "SWAP": np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=complex),
+        }[kind]
+    v = list(values) + [0.0] * (3 - len(values))
+    r = math.sqrt(0.5)
+    if code == 0:
+        return np.array([[r, r], [r, -r]], dtype=complex)
+    if code == 1:
+        return np.array([[r, -1j * r], [1j * r, -r]], dtype=complex)
+    if kind == "RZ":
+        return np.diag([np.exp(-0.5j * v[0]), np.exp(0.5j * v[0])])
+    if kind == "RY":
+        c, s = math.cos(v[0] / 2), math.sin(v[0] / 2)
+        return np.array([[c, -s], [s, c]], dtype=complex)
+    c, s = math.cos(v[0] / 2), math.sin(v[0] / 2)
+    u = np.array([[c, -np.exp(1j * v[2]) * s], [np.exp(1j * v[1]) * s, np.exp(1j * (v[1] + v[2])) * c]])
+    if kind == "U3":
+        return u
+    out = np.eye(4, dtype=complex)
+    out[2:, 2:] = u
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Pauli exponentials (gate pattern of circuit.py:254-281)
+# ---------------------------------------------------------------------------
+
+
+def _scaled(expr, factor: float):
+    if isinstance(expr, (int, float)):
+        return Constant(float(expr) * factor)
+    if isinstance(expr, Constant):
+        return Constant(expr.value * factor)
+    return Affine(expr.index, expr.scale * factor, expr.offset * factor)
+
+
+def evolution_gates(string, angle) -> list[Gate]:
+    """Gates of exp(i * angle * P): basis layer (H for X, HY for Y, ascending
+    qubit order), CNOT ladder down the support, RZ(-2 angle) on the last
+    support qubit, then the mirror image."""
+    support = tuple(q for q, _ in string.factors)
+    if not support:
+        raise ValueError("cannot build an evolution circuit for the identity string")
+    basis = [Gate("H" if a == "X" else "HY", (q,)) for q, a in string.factors if a in ("X", "Y")]
+    ladder = [Gate("CNOT", (support[k], support[k + 1])) for k in range(len(support) - 1)]
+    rz = Gate("RZ", (support[-1],), (_scaled(angle, -2.0),))
+    return basis + ladder + [rz] + ladder[::-1] + basis
+
+
+def pauli_evolution(string, angle, n_qubits: int) -> Circuit:
+    if string.max_index() >= n_qubits:
+        raise ValueError("string support exceeds qubit count")
+    if isinstance(angle, (int, float)):
+        angle = Constant(float(angle))
+    n_params = angle.index + 1 if isinstance(angle, Affine) else 0
+    return Circuit(n_qubits, tuple(evolution_gates(string, angle)), n_params)
+
+
+def rotation_circuit(n_qubits: int, rotations: Iterable[tuple[object, float]]) -> Circuit:
+    """Bound circuit applying exp(-i theta/2 P) for each (P, theta) in order
+    (pauli_evolution(P, -theta/2))."""
+    gates: list[Gate] = []
+    for string, theta in rotations:
+        gates.extend(evolution_gates(string, Constant(-0.5 * float(theta))))
+    return Circuit(n_qubits, tuple(gates), 0)
+
+
+# ---------------------------------------------------------------------------
+# Flattening for the C ABI, and the reference's JSON interchange
+# (circuit.py:539-579)
+# ---------------------------------------------------------------------------
+
+
+def flatten_bound(c) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Bound circuit -> (kinds int32[G], qubits int32[2G], values float64[3G])."""
+    gates = c.gates
+    G = len(gates)
+    codes = _lib.KIND_CODES
+    kinds = np.empty(G, dtype=np.int32)
+    qubits = np.full(2 * G, -1, dtype=np.int32)
+    values = np.zeros(3 * G, dtype=np.float64)
+    for i, g in enumerate(gates):
+        kinds[i] = codes[g.kind]
+        qs = g.qubits
+        qubits[2 * i] = qs[0]
+        if len(qs) == 2:
+            qubits[2 * i + 1] = qs[1]
+        ps = g.params
+        if ps:
+            for k, p in enumerate(ps):
+                v = getattr(p, "value", None)
+                if v is None:
+                    raise RuntimeError(f"gate {g.kind} has unbound parameters")
+                values[3 * i + k] = v
+    return kinds, qubits, values
+
+
+def _expr_json(e) -> dict:
+    if isinstance(e, Constant):
+        return {"type": "const", "value": e.value}
+    return {"type": "affine", "index": e.index, "scale": e.scale, "offset": e.offset}
+
+
+def circuit_to_json(c) -> str:
+    return json.dumps({
+        "n_qubits": c.n_qubits,
+        "n_params": c.n_params,
+        "gates": [{"kind": g.kind, "qubits": list(g.qubits), "params": [_expr_json(p) for p in g.params]}
+                  for g in c.gates],
+    }, separators=(",", ":"))
+
+
+def circuit_from_json(text: str) -> Circuit:
+    d = json.loads(text)
+
+    def expr(o):
+        if o["type"] == "const":
+            return Constant(float(o["value"]))
+        if o["type"] == "affine":
+            return Affine(int(o["index"]), float(o["scale"]), float(o.get("offset", 0.0)))
+        raise ValueError(f"unknown parameter expression type {o['type']!r}")
+
+    gates = tuple(Gate(g["kind"], tuple(g["qubits"]), tuple(expr(p) for p in g["params"]))
+                  for g in d["gates"])
+    return Circuit(int(d["n_qubits"]), gates, int(d["n_params"]))

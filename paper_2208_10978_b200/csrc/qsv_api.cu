@@ -1,0 +1,784 @@
+// qsv_api.cu -- the C ABI (include/qsv.h): handles, validation, program
+// staging and launch sequencing.  Every compute entry point runs on the GPU;
+// there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <list>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qsv.h"
+#include "qsv_internal.h"
+#include "qsv_planner.h"
+
+namespace qsv {
+
+namespace {
+
+thread_local std::string g_err;
+thread_local qsv_plan_stats g_last_stats{};
+
+std::recursive_mutex g_mu;
+
+struct DeviceCtx {
+    bool init = false;
+    cudaStream_t stream = nullptr;
+    void *d_work = nullptr;
+    size_t d_bytes = 0;
+    void *h_stage = nullptr;
+    size_t h_bytes = 0;
+    cudaEvent_t stage_ev = nullptr;
+    bool stage_pending = false;
+};
+DeviceCtx g_dev[64];
+
+#define QSV_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (call);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            return fail_code(QSV_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+int fail_code(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+int ctx_for(int device, DeviceCtx **out)
+{
+    if (device < 0 || device >= 64) return fail_code(QSV_ERR_INVALID, "device index out of range");
+    DeviceCtx &c = g_dev[device];
+    QSV_CUDA(cudaSetDevice(device));
+    if (!c.init) {
+        QSV_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        QSV_CUDA(cudaEventCreateWithFlags(&c.stage_ev, cudaEventDisableTiming));
+        c.init = true;
+    }
+    *out = &c;
+    return QSV_OK;
+}
+
+int ensure_work(DeviceCtx &c, cudaStream_t st, size_t bytes)
+{
+    if (c.d_bytes >= bytes) return QSV_OK;
+    QSV_CUDA(cudaStreamSynchronize(st));
+    if (c.d_work) QSV_CUDA(cudaFree(c.d_work));
+    c.d_work = nullptr;
+    size_t want = std::max<size_t>(bytes + bytes / 2, (size_t)1 << 20);
+    if (cudaMalloc(&c.d_work, want) != cudaSuccess) {
+        cudaGetLastError();
+        c.d_bytes = 0;
+        return fail_code(QSV_ERR_NOMEM, "device workspace allocation failed");
+    }
+    c.d_bytes = want;
+    return QSV_OK;
+}
+
+int ensure_stage(DeviceCtx &c, size_t bytes)
+{
+    if (c.stage_pending) {
+        QSV_CUDA(cudaEventSynchronize(c.stage_ev));
+        c.stage_pending = false;
+    }
+    if (c.h_bytes >= bytes) return QSV_OK;
+    if (c.h_stage) QSV_CUDA(cudaFreeHost(c.h_stage));
+    c.h_stage = nullptr;
+    size_t want = std::max<size_t>(bytes + bytes / 2, (size_t)1 << 20);
+    if (cudaMallocHost(&c.h_stage, want) != cudaSuccess) {
+        cudaGetLastError();
+        c.h_bytes = 0;
+        return fail_code(QSV_ERR_NOMEM, "pinned staging allocation failed");
+    }
+    c.h_bytes = want;
+    return QSV_OK;
+}
+
+// Host blob assembled from several arrays; uploaded with one H2D copy.
+struct Blob {
+    std::vector<char> bytes;
+    size_t add(const void *p, size_t n)
+    {
+        size_t off = (bytes.size() + 255) & ~(size_t)255;
+        bytes.resize(off + n);
+        if (n) std::memcpy(bytes.data() + off, p, n);
+        return off;
+    }
+    size_t reserve(size_t n)
+    {
+        size_t off = (bytes.size() + 255) & ~(size_t)255;
+        bytes.resize(off + n);
+        return off;
+    }
+};
+
+// Upload blob into the head of the device workspace; extra = trailing scratch.
+int upload_blob(DeviceCtx &c, cudaStream_t st, const Blob &b, size_t extra, char **d_base,
+                size_t *scratch_off)
+{
+    const size_t head = (b.bytes.size() + 255) & ~(size_t)255;
+    int rc = ensure_work(c, st, head + extra + 256);
+    if (rc) return rc;
+    if (!b.bytes.empty()) {
+        rc = ensure_stage(c, b.bytes.size());
+        if (rc) return rc;
+        std::memcpy(c.h_stage, b.bytes.data(), b.bytes.size());
+        QSV_CUDA(cudaMemcpyAsync(c.d_work, c.h_stage, b.bytes.size(), cudaMemcpyHostToDevice, st));
+        QSV_CUDA(cudaEventRecord(c.stage_ev, st));
+        c.stage_pending = true;
+    }
+    *d_base = (char *)c.d_work;
+    *scratch_off = head;
+    return QSV_OK;
+}
+
+int check_state(const qsv_state *s)
+{
+    if (!s || !s->amps) return fail_code(QSV_ERR_INVALID, "null or destroyed state handle");
+    return QSV_OK;
+}
+
+// Cache of structural gate plans.
+struct CacheEntry {
+    uint64_t hash;
+    int n;
+    std::vector<int32_t> kinds, qubits;
+    ProgramTemplate tpl;
+};
+std::list<CacheEntry> g_cache;
+constexpr size_t kCacheMax = 8;
+
+struct ExpCacheEntry {
+    uint64_t hash;
+    int n;
+    std::vector<uint64_t> x, y, z;
+    std::vector<SweepPlan> plan;
+};
+std::list<ExpCacheEntry> g_exp_cache;
+
+uint64_t hash_masks(int n, int64_t S, const uint64_t *x, const uint64_t *y, const uint64_t *z)
+{
+    uint64_t h = 0xcbf29ce484222325ull ^ (uint64_t)n;
+    for (int64_t t = 0; t < S; ++t) {
+        uint64_t v[3] = {x[t], y[t], z[t]};
+        for (uint64_t w : v) {
+            h ^= w + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+            h *= 1099511628211ull;
+        }
+    }
+    return h;
+}
+
+int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params)
+{
+    DeviceCtx *c = nullptr;
+    int rc = ctx_for(s->device, &c);
+    if (rc) return rc;
+    Blob b;
+    const size_t o_ops = b.add(t.ops.data(), t.ops.size() * sizeof(OpRec));
+    const size_t o_rots = b.add(t.rots.data(), t.rots.size() * sizeof(RotRec));
+    const size_t o_par = b.add(params.data(), params.size() * sizeof(double));
+    std::vector<size_t> o_off(t.passes.size()), o_comp(t.passes.size());
+    {
+        std::vector<uint64_t> offhi;
+        std::vector<int32_t> comp;
+        for (size_t k = 0; k < t.passes.size(); ++k) {
+            if (t.passes[k].global) continue;
+            geom_tables(t.passes[k].geom, offhi, comp);
+            o_off[k] = b.add(offhi.data(), offhi.size() * sizeof(uint64_t));
+            o_comp[k] = b.add(comp.data(), comp.size() * sizeof(int32_t));
+        }
+    }
+    char *d = nullptr;
+    size_t scratch = 0;
+    rc = upload_blob(*c, s->stream, b, 0, &d, &scratch);
+    if (rc) return rc;
+    const OpRec *d_ops = (const OpRec *)(d + o_ops);
+    const RotRec *d_rots = (const RotRec *)(d + o_rots);
+    const double *d_par = (const double *)(d + o_par);
+    for (size_t k = 0; k < t.passes.size(); ++k) {
+        const PassPlan &p = t.passes[k];
+        if (p.op_end <= p.op_begin) continue;
+        if (p.global) {
+            for (int k = p.op_begin; k < p.op_end; ++k) {
+                const OpRec &op = t.ops[k];
+                QSV_CUDA(launch_rot_global(s->amps, s->n, p.flip, d_rots + op.r0, op.r1 - op.r0,
+                                           s->stream));
+            }
+        } else {
+            QSV_CUDA(launch_tile_pass(s->amps, dims_of(p.geom), (const uint64_t *)(d + o_off[k]),
+                                      (const int32_t *)(d + o_comp[k]), d_ops + p.op_begin,
+                                      p.op_end - p.op_begin, d_rots, d_par, s->stream));
+        }
+    }
+    return QSV_OK;
+}
+
+void fill_stats(const ProgramTemplate &t, bool hit, qsv_plan_stats *out)
+{
+    qsv_plan_stats st{};
+    st.n_input_ops = t.n_input;
+    st.n_rotations = t.n_rotations;
+    st.n_items = t.n_items;
+    st.n_passes = (int64_t)t.passes.size();
+    st.n_fallback = t.n_fallback;
+    st.tile_bits = t.m;
+    st.cache_hit = hit ? 1 : 0;
+    g_last_stats = st;
+    if (out) *out = st;
+}
+
+}  // namespace
+
+void set_error(const std::string &msg) { g_err = msg; }
+int fail(const std::string &msg) { return fail_code(QSV_ERR_INVALID, msg); }
+
+}  // namespace qsv
+
+using namespace qsv;
+
+extern "C" {
+
+int qsv_abi_version(void) { return QSV_ABI_VERSION; }
+
+const char *qsv_last_error(void) { return g_err.c_str(); }
+
+int qsv_device_count(int *out)
+{
+    if (!out) return fail_code(QSV_ERR_INVALID, "null output");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        *out = 0;
+        return fail_code(QSV_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *out = n;
+    return QSV_OK;
+}
+
+int qsv_create(qsv_state **out, int n_qubits, int device)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!out) return fail_code(QSV_ERR_INVALID, "null output");
+    *out = nullptr;
+    if (n_qubits < 1 || n_qubits > kMaxQubits)
+        return fail_code(QSV_ERR_RESOURCE, "qubit count out of range 1.." + std::to_string(kMaxQubits));
+    DeviceCtx *c = nullptr;
+    int rc = ctx_for(device, &c);
+    if (rc) return rc;
+    qsv_state *s = new qsv_state();
+    s->n = n_qubits;
+    s->device = device;
+    s->dim = 1ull << n_qubits;
+    s->stream = c->stream;
+    const size_t bytes = (size_t)16 * s->dim;
+    if (cudaMalloc((void **)&s->amps, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        delete s;
+        return fail_code(QSV_ERR_NOMEM, "cannot allocate " + std::to_string(bytes) +
+                                            " bytes of device memory for the state");
+    }
+    *out = s;
+    return QSV_OK;
+}
+
+int qsv_destroy(qsv_state *s)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!s) return QSV_OK;
+    if (s->amps) {
+        cudaSetDevice(s->device);
+        cudaStreamSynchronize(s->stream);
+        cudaFree(s->amps);
+        s->amps = nullptr;
+    }
+    delete s;
+    return QSV_OK;
+}
+
+int qsv_n_qubits(const qsv_state *s, int *out)
+{
+    if (int rc = check_state(s)) return rc;
+    *out = s->n;
+    return QSV_OK;
+}
+
+int qsv_set_stream(qsv_state *s, void *stream)
+{
+    if (int rc = check_state(s)) return rc;
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(s->device, &c)) return rc;
+    s->stream = stream ? (cudaStream_t)stream : c->stream;
+    return QSV_OK;
+}
+
+int qsv_get_stream(const qsv_state *s, void **stream)
+{
+    if (int rc = check_state(s)) return rc;
+    *stream = (void *)s->stream;
+    return QSV_OK;
+}
+
+int qsv_device_ptr(const qsv_state *s, void **ptr)
+{
+    if (int rc = check_state(s)) return rc;
+    *ptr = (void *)s->amps;
+    return QSV_OK;
+}
+
+int qsv_synchronize(qsv_state *s)
+{
+    if (int rc = check_state(s)) return rc;
+    QSV_CUDA(cudaSetDevice(s->device));
+    QSV_CUDA(cudaStreamSynchronize(s->stream));
+    return QSV_OK;
+}
+
+int qsv_copy(qsv_state *dst, const qsv_state *src)
+{
+    if (int rc = check_state(dst)) return rc;
+    if (int rc = check_state(src)) return rc;
+    if (dst->n != src->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
+    QSV_CUDA(cudaSetDevice(dst->device));
+    if (dst == src) return QSV_OK;
+    QSV_CUDA(cudaMemcpyAsync(dst->amps, src->amps, 16 * dst->dim, cudaMemcpyDeviceToDevice,
+                             dst->stream));
+    return QSV_OK;
+}
+
+int qsv_set_basis(qsv_state *s, uint64_t index)
+{
+    if (int rc = check_state(s)) return rc;
+    if (index >= s->dim) return fail_code(QSV_ERR_INVALID, "basis index out of range");
+    QSV_CUDA(cudaSetDevice(s->device));
+    QSV_CUDA(launch_set_basis(s->amps, s->dim, index, s->stream));
+    return QSV_OK;
+}
+
+int qsv_upload(qsv_state *s, const double *host)
+{
+    if (int rc = check_state(s)) return rc;
+    if (!host) return fail_code(QSV_ERR_INVALID, "null host buffer");
+    QSV_CUDA(cudaSetDevice(s->device));
+    QSV_CUDA(cudaMemcpyAsync(s->amps, host, 16 * s->dim, cudaMemcpyHostToDevice, s->stream));
+    QSV_CUDA(cudaStreamSynchronize(s->stream));
+    return QSV_OK;
+}
+
+int qsv_download(const qsv_state *s, double *host)
+{
+    if (int rc = check_state(s)) return rc;
+    if (!host) return fail_code(QSV_ERR_INVALID, "null host buffer");
+    QSV_CUDA(cudaSetDevice(s->device));
+    QSV_CUDA(cudaMemcpyAsync(host, s->amps, 16 * s->dim, cudaMemcpyDeviceToHost, s->stream));
+    QSV_CUDA(cudaStreamSynchronize(s->stream));
+    return QSV_OK;
+}
+
+static int validate_gates(const qsv_state *s, int64_t n, const int32_t *kinds,
+                          const int32_t *qubits)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        const int k = kinds[i];
+        if (k < 0 || k >= K_COUNT)
+            return fail_code(QSV_ERR_INVALID, "unknown gate kind code " + std::to_string(k));
+        const bool two = (k == K_CNOT || k == K_SWAP || k == K_CU3);
+        const int a = qubits[2 * i], b = qubits[2 * i + 1];
+        if (a < 0 || a >= s->n || (two && (b < 0 || b >= s->n)))
+            return fail_code(QSV_ERR_INVALID, "gate " + std::to_string(i) +
+                                                  " addresses a qubit outside the state");
+        if (two && a == b)
+            return fail_code(QSV_ERR_INVALID, "gate qubit indices must be distinct");
+        if (!two && b != -1)
+            return fail_code(QSV_ERR_INVALID, "one-qubit gate with a second qubit index");
+    }
+    return QSV_OK;
+}
+
+int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                    const double *values, qsv_plan_stats *stats)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (n_gates < 0) return fail_code(QSV_ERR_INVALID, "negative gate count");
+    if (n_gates == 0) {
+        ProgramTemplate empty;
+        fill_stats(empty, false, stats);
+        return QSV_OK;
+    }
+    if (!kinds || !qubits || !values) return fail_code(QSV_ERR_INVALID, "null gate arrays");
+    if (int rc = validate_gates(s, n_gates, kinds, qubits)) return rc;
+    for (int64_t i = 0; i < 3 * n_gates; ++i)
+        if (!std::isfinite(values[i])) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
+    QSV_CUDA(cudaSetDevice(s->device));
+    const uint64_t h = hash_structure(s->n, n_gates, kinds, qubits);
+    ProgramTemplate *tpl = nullptr;
+    bool hit = false;
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+        if (it->hash == h && it->n == s->n && (int64_t)it->kinds.size() == n_gates &&
+            std::memcmp(it->kinds.data(), kinds, n_gates * 4) == 0 &&
+            std::memcmp(it->qubits.data(), qubits, n_gates * 8) == 0) {
+            g_cache.splice(g_cache.begin(), g_cache, it);
+            tpl = &g_cache.front().tpl;
+            hit = true;
+            break;
+        }
+    }
+    if (!tpl) {
+        CacheEntry e;
+        e.hash = h;
+        e.n = s->n;
+        e.kinds.assign(kinds, kinds + n_gates);
+        e.qubits.assign(qubits, qubits + 2 * n_gates);
+        plan_gates(s->n, n_gates, kinds, qubits, e.tpl);
+        g_cache.push_front(std::move(e));
+        if (g_cache.size() > kCacheMax) g_cache.pop_back();
+        tpl = &g_cache.front().tpl;
+    }
+    materialize_gates(*tpl, values);
+    std::vector<double> params(tpl->n_params);
+    for (const ParamFill &f : tpl->fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, &params[f.offset]);
+    fill_stats(*tpl, hit, stats);
+    return run_template(s, *tpl, params);
+}
+
+static int validate_masks(int n, int64_t S, const uint64_t *x, const uint64_t *y,
+                          const uint64_t *z)
+{
+    const uint64_t allowed = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+    for (int64_t t = 0; t < S; ++t) {
+        if ((x[t] | y[t] | z[t]) & ~allowed)
+            return fail_code(QSV_ERR_INVALID, "string index out of range for " + std::to_string(n) +
+                                                  " qubits");
+        if ((x[t] & y[t]) | (x[t] & z[t]) | (y[t] & z[t]))
+            return fail_code(QSV_ERR_INVALID, "X/Y/Z masks of a string overlap");
+    }
+    return QSV_OK;
+}
+
+int qsv_apply_pauli_rotations(qsv_state *s, int64_t n, const uint64_t *x, const uint64_t *y,
+                              const uint64_t *z, const double *theta, qsv_plan_stats *stats)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (n < 0) return fail_code(QSV_ERR_INVALID, "negative rotation count");
+    if (n == 0) return QSV_OK;
+    if (!x || !y || !z || !theta) return fail_code(QSV_ERR_INVALID, "null rotation arrays");
+    if (int rc = validate_masks(s->n, n, x, y, z)) return rc;
+    for (int64_t r = 0; r < n; ++r)
+        if (!std::isfinite(theta[r])) return fail_code(QSV_ERR_INVALID, "non-finite rotation angle");
+    QSV_CUDA(cudaSetDevice(s->device));
+    std::vector<Rot> R;
+    R.reserve(n);
+    for (int64_t r = 0; r < n; ++r) {
+        if ((x[r] | y[r] | z[r]) == 0) continue;  // identity: global phase exp(-i t/2)
+        R.push_back(Rot{x[r], y[r], z[r], (int)r});
+    }
+    ProgramTemplate t;
+    plan_rotations(s->n, R, n, t);
+    materialize_rotations(t, theta);
+    std::vector<double> params;
+    fill_stats(t, false, stats);
+    int rc = run_template(s, t, params);
+    if (rc) return rc;
+    // identity strings contribute a global phase exp(-i theta/2)
+    double ph_re = 1.0, ph_im = 0.0;
+    bool any = false;
+    for (int64_t r = 0; r < n; ++r) {
+        if ((x[r] | y[r] | z[r]) != 0) continue;
+        const double c = std::cos(0.5 * theta[r]), sn = -std::sin(0.5 * theta[r]);
+        const double nr = ph_re * c - ph_im * sn, ni = ph_re * sn + ph_im * c;
+        ph_re = nr;
+        ph_im = ni;
+        any = true;
+    }
+    if (any) QSV_CUDA(launch_axpby(s->amps, s->amps, s->dim, ph_re, ph_im, 0.0, 0.0, s->stream));
+    return QSV_OK;
+}
+
+int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint64_t *y,
+                    const uint64_t *z, const double *coef_re, const double *coef_im,
+                    double *out_re, double *out_im, double *per_term, qsv_plan_stats *stats)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (!out_re || !out_im) return fail_code(QSV_ERR_INVALID, "null outputs");
+    *out_re = 0.0;
+    *out_im = 0.0;
+    if (S < 0) return fail_code(QSV_ERR_INVALID, "negative term count");
+    if (S == 0) return QSV_OK;
+    if (!x || !y || !z || !coef_re) return fail_code(QSV_ERR_INVALID, "null term arrays");
+    if (int rc = validate_masks(s->n, S, x, y, z)) return rc;
+    QSV_CUDA(cudaSetDevice(s->device));
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(s->device, &c)) return rc;
+
+    const uint64_t h = hash_masks(s->n, S, x, y, z);
+    std::vector<SweepPlan> *plan = nullptr;
+    bool hit = false;
+    for (auto it = g_exp_cache.begin(); it != g_exp_cache.end(); ++it) {
+        if (it->hash == h && it->n == s->n && (int64_t)it->x.size() == S &&
+            std::memcmp(it->x.data(), x, S * 8) == 0 && std::memcmp(it->y.data(), y, S * 8) == 0 &&
+            std::memcmp(it->z.data(), z, S * 8) == 0) {
+            g_exp_cache.splice(g_exp_cache.begin(), g_exp_cache, it);
+            plan = &g_exp_cache.front().plan;
+            hit = true;
+            break;
+        }
+    }
+    if (!plan) {
+        ExpCacheEntry e;
+        e.hash = h;
+        e.n = s->n;
+        e.x.assign(x, x + S);
+        e.y.assign(y, y + S);
+        e.z.assign(z, z + S);
+        plan_expectation(s->n, S, x, y, z, e.plan);
+        g_exp_cache.push_front(std::move(e));
+        if (g_exp_cache.size() > 4) g_exp_cache.pop_back();
+        plan = &g_exp_cache.front().plan;
+    }
+    // blob: per sweep groups / terms / map / gflip
+    Blob b;
+    struct Off { size_t g, t, m, f, off, comp; int rows; };
+    std::vector<Off> offs;
+    size_t max_partial = 0;
+    for (const SweepPlan &sp : *plan) {
+        Off o;
+        o.g = b.add(sp.groups.data(), sp.groups.size() * sizeof(GroupRec));
+        o.t = b.add(sp.terms.data(), sp.terms.size() * sizeof(TermRec));
+        o.m = b.add(sp.map.data(), sp.map.size() * sizeof(int32_t));
+        o.f = b.add(sp.gflip.data(), sp.gflip.size() * sizeof(uint64_t));
+        o.off = o.comp = 0;
+        if (!sp.global) {
+            std::vector<uint64_t> offhi;
+            std::vector<int32_t> comp;
+            geom_tables(sp.geom, offhi, comp);
+            o.off = b.add(offhi.data(), offhi.size() * sizeof(uint64_t));
+            o.comp = b.add(comp.data(), comp.size() * sizeof(int32_t));
+        }
+        o.rows = sp.global ? expect_global_grid(s->n)
+                           : expect_sweep_grid(dims_of(sp.geom), (int)sp.terms.size());
+        max_partial = std::max(max_partial, (size_t)o.rows * sp.terms.size());
+        offs.push_back(o);
+    }
+    const size_t per_term_bytes = ((size_t)S * 8 + 255) & ~(size_t)255;
+    char *d = nullptr;
+    size_t scratch = 0;
+    if (int rc = upload_blob(*c, s->stream, b, per_term_bytes + max_partial * 8 + 256, &d, &scratch))
+        return rc;
+    double *d_per_term = (double *)(d + scratch);
+    double *d_partial = (double *)(d + scratch + per_term_bytes);
+    for (size_t k = 0; k < plan->size(); ++k) {
+        const SweepPlan &sp = (*plan)[k];
+        const Off &o = offs[k];
+        const int nterms = (int)sp.terms.size();
+        if (nterms == 0) continue;
+        int rows = 0;
+        if (sp.global) {
+            QSV_CUDA(launch_expect_global(s->amps, s->n, (const GroupRec *)(d + o.g),
+                                          (const uint64_t *)(d + o.f), (int)sp.groups.size(),
+                                          (const TermRec *)(d + o.t), nterms, d_partial, &rows,
+                                          s->stream));
+        } else {
+            QSV_CUDA(launch_expect_sweep(s->amps, dims_of(sp.geom), (const uint64_t *)(d + o.off),
+                                         (const int32_t *)(d + o.comp), (const GroupRec *)(d + o.g),
+                                         (int)sp.groups.size(), (const TermRec *)(d + o.t), nterms,
+                                         sp.ndiag, d_partial, &rows, s->stream));
+        }
+        QSV_CUDA(launch_reduce_columns(d_partial, rows, nterms, (const int32_t *)(d + o.m),
+                                       d_per_term, s->stream));
+    }
+    std::vector<double> vals(S);
+    if (int rc = ensure_stage(*c, (size_t)S * 8)) return rc;
+    QSV_CUDA(cudaMemcpyAsync(c->h_stage, d_per_term, (size_t)S * 8, cudaMemcpyDeviceToHost, s->stream));
+    QSV_CUDA(cudaStreamSynchronize(s->stream));
+    std::memcpy(vals.data(), c->h_stage, (size_t)S * 8);
+    // term-order accumulation, as statevector.py:104-107
+    double re = 0.0, im = 0.0;
+    for (int64_t t = 0; t < S; ++t) {
+        re += coef_re[t] * vals[t];
+        if (coef_im) im += coef_im[t] * vals[t];
+    }
+    *out_re = re;
+    *out_im = im;
+    if (per_term) std::memcpy(per_term, vals.data(), (size_t)S * 8);
+    qsv_plan_stats st{};
+    st.n_input_ops = S;
+    st.n_items = (int64_t)plan->size();
+    st.n_passes = (int64_t)plan->size();
+    for (const SweepPlan &sp : *plan) st.n_fallback += sp.global ? 1 : 0;
+    st.tile_bits = plan->empty() ? 0 : plan->front().geom.m;
+    st.cache_hit = hit ? 1 : 0;
+    g_last_stats = st;
+    if (stats) *stats = st;
+    return QSV_OK;
+}
+
+int qsv_apply_pauli(const qsv_state *src, qsv_state *dst, uint64_t x, uint64_t y, uint64_t z)
+{
+    if (int rc = check_state(src)) return rc;
+    if (int rc = check_state(dst)) return rc;
+    if (src->n != dst->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
+    if (src == dst) return fail_code(QSV_ERR_INVALID, "apply_pauli needs distinct src and dst");
+    if (int rc = validate_masks(src->n, 1, &x, &y, &z)) return rc;
+    QSV_CUDA(cudaSetDevice(src->device));
+    QSV_CUDA(launch_apply_pauli(src->amps, dst->amps, src->dim, x, y, z, 1.0, 0.0, 0, src->stream));
+    return QSV_OK;
+}
+
+int qsv_apply_operator(const qsv_state *src, qsv_state *dst, int64_t S, const uint64_t *x,
+                       const uint64_t *y, const uint64_t *z, const double *coef_re,
+                       const double *coef_im)
+{
+    if (int rc = check_state(src)) return rc;
+    if (int rc = check_state(dst)) return rc;
+    if (src->n != dst->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
+    if (src == dst) return fail_code(QSV_ERR_INVALID, "apply_operator needs distinct src and dst");
+    if (S < 0 || (S > 0 && (!x || !y || !z || !coef_re)))
+        return fail_code(QSV_ERR_INVALID, "bad term arrays");
+    if (int rc = validate_masks(src->n, S, x, y, z)) return rc;
+    QSV_CUDA(cudaSetDevice(src->device));
+    if (S == 0) {
+        QSV_CUDA(cudaMemsetAsync(dst->amps, 0, 16 * dst->dim, src->stream));
+        return QSV_OK;
+    }
+    for (int64_t t = 0; t < S; ++t) {
+        QSV_CUDA(launch_apply_pauli(src->amps, dst->amps, src->dim, x[t], y[t], z[t], coef_re[t],
+                                    coef_im ? coef_im[t] : 0.0, t > 0 ? 1 : 0, src->stream));
+    }
+    return QSV_OK;
+}
+
+static int dot_common(const qsv_state *a, const qsv_state *b, int mode, double *out2)
+{
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(a->device, &c)) return rc;
+    const size_t part = (size_t)num_sms(a->device) * 4 * 2 * sizeof(double);
+    if (int rc = ensure_work(*c, a->stream, part + 256)) return rc;
+    double *d_part = (double *)c->d_work;
+    double *d_out = (double *)((char *)c->d_work + ((part + 255) & ~(size_t)255));
+    QSV_CUDA(launch_dot(a->amps, b ? b->amps : nullptr, a->dim, d_part, d_out, mode, a->stream));
+    if (int rc = ensure_stage(*c, 16)) return rc;
+    QSV_CUDA(cudaMemcpyAsync(c->h_stage, d_out, 16, cudaMemcpyDeviceToHost, a->stream));
+    QSV_CUDA(cudaStreamSynchronize(a->stream));
+    std::memcpy(out2, c->h_stage, 16);
+    return QSV_OK;
+}
+
+int qsv_vdot(const qsv_state *a, const qsv_state *b, double *out2)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(a)) return rc;
+    if (int rc = check_state(b)) return rc;
+    if (!out2) return fail_code(QSV_ERR_INVALID, "null output");
+    if (a->n != b->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
+    QSV_CUDA(cudaSetDevice(a->device));
+    return dot_common(a, b, 0, out2);
+}
+
+int qsv_norm(const qsv_state *s, double *out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (!out) return fail_code(QSV_ERR_INVALID, "null output");
+    QSV_CUDA(cudaSetDevice(s->device));
+    double v[2];
+    if (int rc = dot_common(s, nullptr, 1, v)) return rc;
+    *out = std::sqrt(v[0]);
+    return QSV_OK;
+}
+
+int qsv_axpby(qsv_state *y, const qsv_state *x, double are, double aim, double bre, double bim)
+{
+    if (int rc = check_state(y)) return rc;
+    if (int rc = check_state(x)) return rc;
+    if (x->n != y->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
+    QSV_CUDA(cudaSetDevice(y->device));
+    QSV_CUDA(launch_axpby(y->amps, x->amps, y->dim, are, aim, bre, bim, y->stream));
+    return QSV_OK;
+}
+
+int qsv_apply_1q(qsv_state *s, const double *m, int qubit)
+{
+    if (int rc = check_state(s)) return rc;
+    if (!m) return fail_code(QSV_ERR_INVALID, "null matrix");
+    if (qubit < 0 || qubit >= s->n) return fail_code(QSV_ERR_INVALID, "qubit out of range");
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    QSV_CUDA(cudaSetDevice(s->device));
+    ProgramTemplate t;
+    int32_t kind = K_U3, q[2] = {qubit, -1};
+    plan_gates(s->n, 1, &kind, q, t);
+    // plan for a U3 gate: one OP_U1 whose params are the supplied matrix
+    std::vector<double> params(t.n_params);
+    std::memcpy(params.data(), m, 8 * sizeof(double));
+    fill_stats(t, false, nullptr);
+    return run_template(s, t, params);
+}
+
+int qsv_apply_2q(qsv_state *s, const double *m, int q0, int q1)
+{
+    if (int rc = check_state(s)) return rc;
+    if (!m) return fail_code(QSV_ERR_INVALID, "null matrix");
+    if (q0 < 0 || q0 >= s->n || q1 < 0 || q1 >= s->n || q0 == q1)
+        return fail_code(QSV_ERR_INVALID, "bad qubit pair");
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    QSV_CUDA(cudaSetDevice(s->device));
+    ProgramTemplate t;
+    int32_t kind = K_CU3, q[2] = {q0, q1};
+    plan_gates(s->n, 1, &kind, q, t);
+    std::vector<double> params(t.n_params);
+    std::memcpy(params.data(), m, 32 * sizeof(double));
+    fill_stats(t, false, nullptr);
+    return run_template(s, t, params);
+}
+
+int qsv_plan_gates(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                   qsv_plan_stats *out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!out) return fail_code(QSV_ERR_INVALID, "null output");
+    if (n < 1 || n > kMaxQubits) return fail_code(QSV_ERR_RESOURCE, "qubit count out of range");
+    if (n_gates < 0 || (n_gates > 0 && (!kinds || !qubits)))
+        return fail_code(QSV_ERR_INVALID, "bad gate arrays");
+    qsv_state fake;
+    fake.n = n;
+    if (int rc = validate_gates(&fake, n_gates, kinds, qubits)) return rc;
+    ProgramTemplate t;
+    plan_gates(n, n_gates, kinds, qubits, t);
+    fill_stats(t, false, out);
+    return QSV_OK;
+}
+
+int qsv_plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y,
+                         const uint64_t *z, qsv_plan_stats *out)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!out) return fail_code(QSV_ERR_INVALID, "null output");
+    if (n < 1 || n > kMaxQubits) return fail_code(QSV_ERR_RESOURCE, "qubit count out of range");
+    if (S < 0 || (S > 0 && (!x || !y || !z))) return fail_code(QSV_ERR_INVALID, "bad term arrays");
+    if (int rc = validate_masks(n, S, x, y, z)) return rc;
+    std::vector<SweepPlan> plan;
+    plan_expectation(n, S, x, y, z, plan);
+    qsv_plan_stats st{};
+    st.n_input_ops = S;
+    st.n_items = (int64_t)plan.size();
+    st.n_passes = (int64_t)plan.size();
+    for (const SweepPlan &sp : plan) st.n_fallback += sp.global ? 1 : 0;
+    st.tile_bits = plan.empty() ? 0 : plan.front().geom.m;
+    *out = st;
+    return QSV_OK;
+}
+
+int qsv_last_plan_stats(qsv_plan_stats *out)
+{
+    if (!out) return fail_code(QSV_ERR_INVALID, "null output");
+    *out = g_last_stats;
+    return QSV_OK;
+}
+
+}  // extern "C"

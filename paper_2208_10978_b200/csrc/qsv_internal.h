@@ -1,0 +1,131 @@
+// qsv_internal.h -- shared definitions between the sm_100a kernels, the C++
+// pass planner and the C-ABI (include/qsv.h).
+//
+// Data layout in HBM: one state = 2^n complex128 amplitudes stored as
+// double2 {re, im} in basis-index order; index bit k is qubit k
+// (reference: statevector.py:1-6, dump_state layout statevector.py:214-216).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace qsv {
+
+// Largest tile (in qubits) a CTA keeps resident in shared memory: 2^12
+// amplitudes x 16 B = 64 KiB, so three CTAs fit one SM's 228 KiB.
+constexpr int kMaxTileBits = 12;
+// Low physical bits that every tile always contains: 2^5 amplitudes = 512 B
+// contiguous segments, so every warp-wide 16 B load is fully coalesced.
+constexpr int kMinContig = 5;
+constexpr int kMaxQubits = 40;
+
+// ---- fused tile-pass program -------------------------------------------
+enum OpType : int32_t {
+    OP_U1 = 1,     // dense 2x2 on local bit a; params[p..p+8)
+    OP_U2 = 2,     // dense 4x4, rows = 2*bit(a) + bit(b); params[p..p+32)
+    OP_CX = 3,     // CNOT control a, target b (permutation, no flops)
+    OP_SWAP = 4,   // SWAP a, b
+    OP_X = 5,      // Pauli X on a
+    OP_DIAG1 = 6,  // diag(d0, d1) on a; params[p..p+4)
+    OP_ROTG = 7,   // rotations exp(-i t/2 P) sharing local flip mask f (highest bit h), rots[r0..r1)
+    OP_ROTD = 8,   // diagonal (Z-only) rotations, rots[r0..r1)
+};
+
+struct OpRec {  // 32 B
+    int32_t type;
+    int32_t a, b, h;
+    int32_t r0, r1, p;
+    uint32_t f;
+};
+
+struct RotRec {     // 32 B
+    uint64_t s_hi;  // sign bits outside the tile (per-tile constant parity)
+    uint32_t s_loc; // sign bits inside the tile, in local bit order
+    int32_t q;      // low 2 bits: kappa = i^q ; bit 2: |y| odd
+    double c, s;    // cos(theta/2), sin(theta/2)
+};
+
+// Tile geometry of one pass (host side): local bit i <-> physical bit pos[i]; pos[i] = i
+// for i < c (contiguous low block).  The tile index enumerates the n - m
+// complement bits comp[] in ascending order.
+struct TileGeom {
+    int32_t n, m, c, ncomp;
+    int32_t pos[kMaxTileBits];
+    int32_t comp[kMaxQubits];
+};
+
+// What the kernels see of a TileGeom (the position tables travel as device
+// arrays: offhi[2^(m-c)] and comp[32]).
+struct TileDims {
+    int32_t n, m, c, ncomp;
+};
+
+// ---- expectation sweep --------------------------------------------------
+struct GroupRec {   // a flip group evaluated by one warp
+    uint32_t f_loc;
+    int32_t h;
+    int32_t t0, t1;  // term range (sweep-local indices)
+};
+
+struct TermRec {    // 24 B
+    uint64_t s_hi;
+    uint32_t s_loc;
+    int32_t use_im;
+    double scale;
+};
+
+}  // namespace qsv
+
+// ---- state handle -------------------------------------------------------
+struct qsv_state {
+    int n = 0;
+    int device = 0;
+    uint64_t dim = 0;
+    double2 *amps = nullptr;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // per-state workspace (lazily grown)
+    void *d_work = nullptr;
+    size_t d_work_bytes = 0;
+    void *h_stage = nullptr;  // pinned staging for host->device programs
+    size_t h_stage_bytes = 0;
+    cudaEvent_t stage_done = nullptr;
+    bool stage_pending = false;
+};
+
+namespace qsv {
+
+void set_error(const std::string &msg);
+int fail(const std::string &msg);
+
+// kernels (qsv_kernels.cu)
+int num_sms(int device);
+cudaError_t launch_tile_pass(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
+                             const int32_t *d_comp, const OpRec *d_ops, int nops,
+                             const RotRec *d_rots, const double *d_params, cudaStream_t st);
+cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
+                                const int32_t *d_comp, const GroupRec *d_groups,
+                                int ngroups, const TermRec *d_terms, int nterms, int ndiag,
+                                double *d_partial, int *grid_out, cudaStream_t st);
+cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
+                                  double *out, cudaStream_t st);
+cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStream_t st);
+cudaError_t launch_apply_pauli(const double2 *src, double2 *dst, uint64_t dim, uint64_t x,
+                               uint64_t y, uint64_t z, double cre, double cim, int accumulate,
+                               cudaStream_t st);
+cudaError_t launch_dot(const double2 *a, const double2 *b, uint64_t dim, double *d_partial,
+                       double *d_out2, int mode, cudaStream_t st);
+cudaError_t launch_rot_global(double2 *psi, int n, uint64_t flip, const RotRec *d_rots, int nrot,
+                              cudaStream_t st);
+cudaError_t launch_expect_global(const double2 *psi, int n, const GroupRec *d_groups,
+                                 const uint64_t *d_gflip, int ngroups, const TermRec *d_terms,
+                                 int nterms, double *d_partial, int *grid_out, cudaStream_t st);
+int expect_global_grid(int n);
+int expect_sweep_grid(const TileDims &g, int nterms);
+cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,
+                         double bre, double bim, cudaStream_t st);
+
+}  // namespace qsv

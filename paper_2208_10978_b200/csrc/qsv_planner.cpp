@@ -1,0 +1,710 @@
+// qsv_planner.cpp -- native fusion planner (see qsv_planner.h).
+#include "qsv_planner.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unordered_map>
+
+namespace qsv {
+
+namespace {
+
+inline int popc64(uint64_t v) { return __builtin_popcountll(v); }
+
+inline int highest_bit(uint64_t v) { return 63 - __builtin_clzll(v); }
+
+// Local (tile) image of a physical mask: bit i of the result = bit pos[i] of mask.
+inline uint32_t compress(uint64_t mask, const TileGeom &g)
+{
+    uint32_t out = 0;
+    for (int i = 0; i < g.m; ++i)
+        if ((mask >> g.pos[i]) & 1ull) out |= 1u << i;
+    return out;
+}
+
+inline uint64_t tile_mask(const TileGeom &g)
+{
+    uint64_t t = 0;
+    for (int i = 0; i < g.m; ++i) t |= 1ull << g.pos[i];
+    return t;
+}
+
+inline int local_of(const TileGeom &g, int q)
+{
+    for (int i = 0; i < g.m; ++i)
+        if (g.pos[i] == q) return i;
+    return -1;
+}
+
+void choose_tile(int n, int &m, int &c)
+{
+    m = n < kMaxTileBits ? n : kMaxTileBits;
+    if (m == n) {
+        c = n;
+    } else {
+        c = kMinContig;
+        if (c > m - 4) c = m - 4;
+        if (c < 0) c = 0;
+    }
+}
+
+// Tile = low c bits + hi bits, topped up with the lowest unused bits.
+TileGeom make_geom(int n, int m, int c, uint64_t hi)
+{
+    TileGeom g;
+    std::memset(&g, 0, sizeof(g));
+    g.n = n;
+    g.m = m;
+    uint64_t t = (c >= 64 ? ~0ull : ((1ull << c) - 1ull)) | hi;
+    for (int q = 0; popc64(t) < m && q < n; ++q) t |= 1ull << q;
+    int k = 0;
+    for (int q = 0; q < n; ++q)
+        if ((t >> q) & 1ull) g.pos[k++] = q;
+    int cc = 0;
+    while (cc < m && g.pos[cc] == cc) ++cc;
+    g.c = cc;
+    g.ncomp = 0;
+    for (int q = 0; q < n; ++q)
+        if (!((t >> q) & 1ull)) g.comp[g.ncomp++] = q;
+    return g;
+}
+
+// One Pauli rotation / string in symplectic form.
+struct Sym {
+    uint64_t a;  // flip bits x|y
+    uint64_t b;  // sign bits y|z
+};
+
+inline bool anticommute(const Sym &p, const Sym &q)
+{
+    return ((popc64(p.a & q.b) + popc64(p.b & q.a)) & 1) != 0;
+}
+
+struct Item {
+    bool rot = false;
+    int gate = -1;            // gate index (gate items)
+    std::vector<int> rots;    // indices into the rotation list (rot items)
+    uint64_t supp = 0;        // all touched qubits
+    uint64_t req = 0;         // qubits that must be tile-local
+    uint64_t a_union = 0, b_union = 0;
+};
+
+bool conflict(const Item &A, const Item &B, const std::vector<Rot> &R)
+{
+    if (!A.rot || !B.rot) return (A.supp & B.supp) != 0;
+    if (((A.a_union & B.b_union) | (A.b_union & B.a_union)) == 0) return false;
+    for (int i : A.rots) {
+        const Sym p{R[i].x | R[i].y, R[i].y | R[i].z};
+        for (int j : B.rots) {
+            const Sym q{R[j].x | R[j].y, R[j].y | R[j].z};
+            if (anticommute(p, q)) return true;
+        }
+    }
+    return false;
+}
+
+struct Schedule {
+    std::vector<std::vector<int>> pass_items;
+    std::vector<uint64_t> pass_hi;
+    std::vector<bool> pass_global;
+};
+
+Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int n, int m, int c)
+{
+    Schedule S;
+    const uint64_t low = c >= 64 ? ~0ull : ((1ull << c) - 1ull);
+    const int free_slots = m - c;
+    std::vector<int> item_pass(items.size(), 0);
+    for (size_t i = 0; i < items.size(); ++i) {
+        const Item &it = items[i];
+        const uint64_t need = it.req & ~low;
+        const bool fits = popc64(need) <= free_slots;
+        int earliest = 0;
+        const int last = (int)S.pass_items.size() - 1;
+        for (size_t jj = i; jj-- > 0;) {
+            if (item_pass[jj] <= earliest) continue;
+            if (conflict(items[jj], it, R)) {
+                earliest = std::max(earliest, item_pass[jj]);
+                if (earliest == last) break;
+            }
+        }
+        int placed = -1;
+        if (fits) {
+            for (int p = earliest; p <= last; ++p) {
+                if (S.pass_global[p]) continue;
+                if (popc64(S.pass_hi[p] | need) <= free_slots) {
+                    placed = p;
+                    break;
+                }
+            }
+        }
+        if (placed < 0) {
+            // a new pass at the end; a global pass must also come after every
+            // conflicting item, which `earliest <= last` already guarantees.
+            S.pass_items.emplace_back();
+            S.pass_hi.push_back(0);
+            S.pass_global.push_back(!fits);
+            placed = (int)S.pass_items.size() - 1;
+        }
+        S.pass_items[placed].push_back((int)i);
+        S.pass_hi[placed] |= need;
+        item_pass[i] = placed;
+    }
+    return S;
+}
+
+// Pattern match of circuit.py:271-281 `_evolution_gates` at position i.
+bool match_block(const int32_t *kinds, const int32_t *qubits, int64_t N, int64_t i, Rot &out,
+                 int64_t &len)
+{
+    int64_t j = i;
+    int bq[64], bk[64], nb = 0;
+    while (j < N && (kinds[j] == K_H || kinds[j] == K_HY)) {
+        const int q = qubits[2 * j];
+        if (nb > 0 && q <= bq[nb - 1]) break;
+        if (nb >= 64) return false;
+        bq[nb] = q;
+        bk[nb] = kinds[j];
+        ++nb;
+        ++j;
+    }
+    int s[66], ns = 0;
+    while (j < N && kinds[j] == K_CNOT) {
+        const int a = qubits[2 * j], b = qubits[2 * j + 1];
+        if (ns == 0) {
+            if (!(a < b)) break;
+            s[0] = a;
+            s[1] = b;
+            ns = 2;
+        } else {
+            if (a != s[ns - 1] || !(b > a) || ns >= 64) break;
+            s[ns++] = b;
+        }
+        ++j;
+    }
+    if (j >= N || kinds[j] != K_RZ) return false;
+    const int rzq = qubits[2 * j];
+    if (ns == 0) {
+        s[0] = rzq;
+        ns = 1;
+    } else if (rzq != s[ns - 1]) {
+        return false;
+    }
+    const int64_t rz_index = j;
+    ++j;
+    for (int k = ns - 2; k >= 0; --k) {
+        if (j >= N || kinds[j] != K_CNOT || qubits[2 * j] != s[k] || qubits[2 * j + 1] != s[k + 1])
+            return false;
+        ++j;
+    }
+    for (int k = 0; k < nb; ++k) {
+        if (j >= N || kinds[j] != bk[k] || qubits[2 * j] != bq[k]) return false;
+        ++j;
+    }
+    uint64_t supp = 0;
+    for (int k = 0; k < ns; ++k) supp |= 1ull << s[k];
+    uint64_t x = 0, y = 0;
+    for (int k = 0; k < nb; ++k) {
+        const uint64_t bit = 1ull << bq[k];
+        if (!(supp & bit)) return false;
+        if (bk[k] == K_H) x |= bit;
+        else y |= bit;
+    }
+    out.x = x;
+    out.y = y;
+    out.z = supp & ~x & ~y;
+    out.src = (int)rz_index;
+    len = j - i;
+    return true;
+}
+
+void build_items_from_rots(const std::vector<Rot> &R, std::vector<Item> &items)
+{
+    for (size_t r = 0; r < R.size(); ++r) {
+        const uint64_t a = R[r].x | R[r].y, b = R[r].y | R[r].z;
+        if (!items.empty() && items.back().rot && items.back().a_union == a &&
+            (items.back().req == a)) {
+            Item &g = items.back();
+            g.rots.push_back((int)r);
+            g.b_union |= b;
+            g.supp |= a | b;
+            continue;
+        }
+        Item it;
+        it.rot = true;
+        it.rots.push_back((int)r);
+        it.a_union = a;
+        it.b_union = b;
+        it.supp = a | b;
+        it.req = a;
+        items.push_back(std::move(it));
+    }
+}
+
+int param_count(int kind)
+{
+    switch (kind) {
+        case K_H: case K_HY: case K_RY: case K_U3: return 8;
+        case K_RZ: return 4;
+        case K_CU3: return 32;
+        default: return 0;
+    }
+}
+
+void emit_program(int n, int m, int c, const std::vector<Item> &items, const std::vector<Rot> &R,
+                  const int32_t *kinds, const int32_t *qubits, const Schedule &S,
+                  ProgramTemplate &t)
+{
+    t.n = n;
+    t.m = m;
+    t.c = c;
+    for (size_t p = 0; p < S.pass_items.size(); ++p) {
+        PassPlan pp;
+        if (S.pass_global[p]) {
+            // single rotation group, applied over the whole state
+            std::memset(&pp.geom, 0, sizeof(pp.geom));
+            pp.geom.n = n;
+            pp.global = true;
+            pp.op_begin = (int)t.ops.size();
+            for (int ii : S.pass_items[p]) {
+                const Item &it = items[ii];
+                OpRec op{};
+                op.type = OP_ROTG;
+                op.r0 = (int)t.rots.size();
+                for (int r : it.rots) {
+                    RotRec rr{};
+                    rr.s_hi = R[r].y | R[r].z;
+                    rr.s_loc = 0;
+                    const int ny = popc64(R[r].y);
+                    rr.q = ((ny + 3) & 3) | ((ny & 1) << 2);
+                    t.rots.push_back(rr);
+                    t.rot_src.push_back(R[r].src);
+                }
+                op.r1 = (int)t.rots.size();
+                pp.flip = it.a_union;
+                t.ops.push_back(op);
+            }
+            pp.op_end = (int)t.ops.size();
+            t.passes.push_back(pp);
+            ++t.n_fallback;
+            continue;
+        }
+        pp.geom = make_geom(n, m, c, S.pass_hi[p]);
+        const TileGeom &g = pp.geom;
+        const uint64_t tm = tile_mask(g);
+        pp.op_begin = (int)t.ops.size();
+        for (int ii : S.pass_items[p]) {
+            const Item &it = items[ii];
+            OpRec op{};
+            if (it.rot) {
+                const uint64_t a = it.a_union;
+                op.r0 = (int)t.rots.size();
+                for (int r : it.rots) {
+                    RotRec rr{};
+                    const uint64_t b = R[r].y | R[r].z;
+                    rr.s_hi = b & ~tm;
+                    rr.s_loc = compress(b, g);
+                    const int ny = popc64(R[r].y);
+                    rr.q = ((ny + 3) & 3) | ((ny & 1) << 2);
+                    t.rots.push_back(rr);
+                    t.rot_src.push_back(R[r].src);
+                }
+                op.r1 = (int)t.rots.size();
+                if (a == 0) {
+                    op.type = OP_ROTD;
+                } else {
+                    op.type = OP_ROTG;
+                    op.f = compress(a, g);
+                    op.h = highest_bit(op.f);
+                }
+            } else {
+                const int gi = it.gate, kind = kinds[gi];
+                const int a = local_of(g, qubits[2 * gi]);
+                const int b = (kind == K_CNOT || kind == K_SWAP || kind == K_CU3)
+                                  ? local_of(g, qubits[2 * gi + 1])
+                                  : -1;
+                op.a = a;
+                op.b = b;
+                switch (kind) {
+                    case K_X: op.type = OP_X; break;
+                    case K_CNOT: op.type = OP_CX; break;
+                    case K_SWAP: op.type = OP_SWAP; break;
+                    case K_RZ: op.type = OP_DIAG1; break;
+                    case K_CU3: op.type = OP_U2; break;
+                    default: op.type = OP_U1; break;
+                }
+                const int np = param_count(kind);
+                if (np) {
+                    op.p = (int)t.n_params;
+                    t.fills.push_back(ParamFill{(int)t.n_params, gi, kind});
+                    t.n_params += np;
+                }
+            }
+            t.ops.push_back(op);
+        }
+        pp.op_end = (int)t.ops.size();
+        t.passes.push_back(pp);
+    }
+    t.n_items = (int64_t)items.size();
+}
+
+}  // namespace
+
+int gate_matrix(int kind, const double *v, double *o)
+{
+    // circuit.py:36-45 (fixed), :164-171 (_u3_matrix), :198-223 (gate_matrix)
+    const double r = std::sqrt(0.5);
+    auto set = [&](int i, double re, double im) {
+        o[2 * i] = re;
+        o[2 * i + 1] = im;
+    };
+    switch (kind) {
+        case K_H: set(0, r, 0); set(1, r, 0); set(2, r, 0); set(3, -r, 0); return 8;
+        case K_HY: set(0, r, 0); set(1, 0, -r); set(2, 0, r); set(3, -r, 0); return 8;
+        case K_RZ: {
+            const double c = std::cos(0.5 * v[0]), s = std::sin(0.5 * v[0]);
+            set(0, c, -s);
+            set(1, c, s);
+            return 4;
+        }
+        case K_RY: {
+            const double c = std::cos(v[0] / 2), s = std::sin(v[0] / 2);
+            set(0, c, 0); set(1, -s, 0); set(2, s, 0); set(3, c, 0);
+            return 8;
+        }
+        case K_U3:
+        case K_CU3: {
+            const double th = v[0], ph = v[1], la = v[2];
+            const double c = std::cos(th / 2), s = std::sin(th / 2);
+            double u[8];
+            u[0] = c; u[1] = 0;
+            u[2] = -std::cos(la) * s; u[3] = -std::sin(la) * s;
+            u[4] = std::cos(ph) * s; u[5] = std::sin(ph) * s;
+            u[6] = std::cos(ph + la) * c; u[7] = std::sin(ph + la) * c;
+            if (kind == K_U3) {
+                std::memcpy(o, u, sizeof(u));
+                return 8;
+            }
+            for (int i = 0; i < 32; ++i) o[i] = 0.0;
+            o[0] = 1.0;            // (0,0)
+            o[2 * 5] = 1.0;        // (1,1)
+            o[2 * 10] = u[0]; o[2 * 10 + 1] = u[1];   // (2,2)
+            o[2 * 11] = u[2]; o[2 * 11 + 1] = u[3];   // (2,3)
+            o[2 * 14] = u[4]; o[2 * 14 + 1] = u[5];   // (3,2)
+            o[2 * 15] = u[6]; o[2 * 15 + 1] = u[7];   // (3,3)
+            return 32;
+        }
+        default: return 0;
+    }
+}
+
+TileDims dims_of(const TileGeom &g)
+{
+    TileDims d;
+    d.n = g.n;
+    d.m = g.m;
+    d.c = g.c;
+    d.ncomp = g.ncomp;
+    return d;
+}
+
+void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<int32_t> &comp32)
+{
+    const int nhi = 1 << (g.m - g.c);
+    offhi.assign(nhi, 0);
+    for (int i = 0; i < nhi; ++i) {
+        uint64_t off = 0;
+        for (int b = 0; b < g.m - g.c; ++b)
+            if ((i >> b) & 1) off |= 1ull << g.pos[g.c + b];
+        offhi[i] = off;
+    }
+    comp32.assign(32, 0);
+    for (int i = 0; i < g.ncomp && i < 32; ++i) comp32[i] = g.comp[i];
+}
+
+uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits)
+{
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)n_qubits;
+    auto mix = [&](uint64_t v) {
+        h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+        h *= 1099511628211ull;
+    };
+    mix((uint64_t)n_gates);
+    for (int64_t i = 0; i < n_gates; ++i) {
+        mix(((uint64_t)(uint32_t)kinds[i] << 40) ^ ((uint64_t)(uint32_t)qubits[2 * i] << 20) ^
+            (uint64_t)(uint32_t)qubits[2 * i + 1]);
+    }
+    return h;
+}
+
+void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, ProgramTemplate &t)
+{
+    t = ProgramTemplate();
+    int m, c;
+    choose_tile(n, m, c);
+    std::vector<Rot> R;
+    std::vector<Item> items;
+    int64_t i = 0;
+    while (i < N) {
+        Rot rot;
+        int64_t len = 0;
+        if (match_block(kinds, qubits, N, i, rot, len)) {
+            const uint64_t a = rot.x | rot.y, b = rot.y | rot.z;
+            R.push_back(rot);
+            const int r = (int)R.size() - 1;
+            if (!items.empty() && items.back().rot && items.back().req == a) {
+                Item &g = items.back();
+                g.rots.push_back(r);
+                g.b_union |= b;
+                g.supp |= a | b;
+            } else {
+                Item it;
+                it.rot = true;
+                it.rots.push_back(r);
+                it.a_union = a;
+                it.b_union = b;
+                it.supp = a | b;
+                it.req = a;
+                items.push_back(std::move(it));
+            }
+            i += len;
+        } else {
+            Item it;
+            it.gate = (int)i;
+            uint64_t s = 1ull << qubits[2 * i];
+            if (qubits[2 * i + 1] >= 0) s |= 1ull << qubits[2 * i + 1];
+            it.supp = s;
+            it.req = s;
+            items.push_back(std::move(it));
+            ++i;
+        }
+    }
+    Schedule S = schedule(items, R, n, m, c);
+    emit_program(n, m, c, items, R, kinds, qubits, S, t);
+    t.n_input = N;
+    t.n_rotations = (int64_t)R.size();
+}
+
+void plan_rotations(int n, const std::vector<Rot> &R, int64_t n_input, ProgramTemplate &t)
+{
+    t = ProgramTemplate();
+    int m, c;
+    choose_tile(n, m, c);
+    std::vector<Item> items;
+    build_items_from_rots(R, items);
+    Schedule S = schedule(items, R, n, m, c);
+    emit_program(n, m, c, items, R, nullptr, nullptr, S, t);
+    t.n_input = n_input;
+    t.n_rotations = (int64_t)R.size();
+}
+
+void materialize_gates(ProgramTemplate &t, const double *values)
+{
+    for (size_t r = 0; r < t.rots.size(); ++r) {
+        const double th = values[3 * (size_t)t.rot_src[r]];
+        t.rots[r].c = std::cos(0.5 * th);
+        t.rots[r].s = std::sin(0.5 * th);
+    }
+}
+
+void materialize_rotations(ProgramTemplate &t, const double *theta)
+{
+    for (size_t r = 0; r < t.rots.size(); ++r) {
+        const double th = theta[t.rot_src[r]];
+        t.rots[r].c = std::cos(0.5 * th);
+        t.rots[r].s = std::sin(0.5 * th);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Expectation sweeps
+// ---------------------------------------------------------------------------
+
+void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, const uint64_t *z,
+                      std::vector<SweepPlan> &out)
+{
+    out.clear();
+    int m, c;
+    choose_tile(n, m, c);
+    const uint64_t low = c >= 64 ? ~0ull : ((1ull << c) - 1ull);
+    const int free_slots = m - c;
+    const int kCap = 2048;  // terms per sweep (shared-memory accumulators)
+
+    std::vector<int32_t> diag;
+    std::unordered_map<uint64_t, int> flip_index;
+    std::vector<uint64_t> flips;
+    std::vector<std::vector<int32_t>> members;
+    for (int64_t t = 0; t < S; ++t) {
+        const uint64_t f = x[t] | y[t];
+        if (f == 0) {
+            diag.push_back((int32_t)t);
+            continue;
+        }
+        auto it = flip_index.find(f);
+        if (it == flip_index.end()) {
+            flip_index.emplace(f, (int)flips.size());
+            flips.push_back(f);
+            members.emplace_back();
+            members.back().push_back((int32_t)t);
+        } else {
+            members[it->second].push_back((int32_t)t);
+        }
+    }
+    // order groups: most high bits first (hardest to place), then by first term
+    std::vector<int> order(flips.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return popc64(flips[a] & ~low) > popc64(flips[b] & ~low);
+    });
+    struct Bin {
+        uint64_t hi = 0;
+        int nterms = 0;
+        std::vector<int> groups;
+    };
+    std::vector<Bin> bins;
+    std::vector<int> global_groups;
+    for (int gi : order) {
+        const uint64_t need = flips[gi] & ~low;
+        const int nt = (int)members[gi].size();
+        if (popc64(need) > free_slots) {
+            global_groups.push_back(gi);
+            continue;
+        }
+        int placed = -1;
+        for (size_t b = 0; b < bins.size(); ++b) {
+            if (bins[b].nterms + nt > kCap && bins[b].nterms > 0) continue;
+            if (popc64(bins[b].hi | need) <= free_slots) {
+                placed = (int)b;
+                break;
+            }
+        }
+        if (placed < 0) {
+            bins.emplace_back();
+            placed = (int)bins.size() - 1;
+        }
+        bins[placed].hi |= need;
+        bins[placed].nterms += nt;
+        bins[placed].groups.push_back(gi);
+    }
+    // diagonal terms: spread over sweeps with spare capacity, new sweeps as needed
+    size_t dpos = 0;
+    std::vector<int> bin_ndiag(bins.size(), 0);
+    for (size_t b = 0; b < bins.size() && dpos < diag.size(); ++b) {
+        const int room = kCap - bins[b].nterms;
+        const int take = (int)std::min<size_t>(room > 0 ? room : 0, diag.size() - dpos);
+        bin_ndiag[b] = take;
+        bins[b].nterms += take;
+        dpos += take;
+    }
+    while (dpos < diag.size()) {
+        bins.emplace_back();
+        const int take = (int)std::min<size_t>(kCap, diag.size() - dpos);
+        bin_ndiag.push_back(take);
+        bins.back().nterms = take;
+        dpos += take;
+    }
+
+    auto term_scale = [&](int64_t t, bool is_diag) {
+        if (is_diag) return 1.0;
+        const int ny = popc64(y[t]);
+        if ((ny & 1) == 0) return ((ny / 2) & 1) ? -2.0 : 2.0;
+        return (((ny + 1) / 2) & 1) ? 2.0 : -2.0;
+    };
+
+    dpos = 0;
+    for (size_t b = 0; b < bins.size(); ++b) {
+        SweepPlan sp;
+        sp.geom = make_geom(n, m, c, bins[b].hi);
+        const uint64_t tm = tile_mask(sp.geom);
+        sp.ndiag = bin_ndiag[b];
+        for (int k = 0; k < sp.ndiag; ++k) {
+            const int64_t t = diag[dpos++];
+            TermRec tr{};
+            const uint64_t bb = y[t] | z[t];
+            tr.s_hi = bb & ~tm;
+            tr.s_loc = compress(bb, sp.geom);
+            tr.use_im = 0;
+            tr.scale = 1.0;
+            sp.terms.push_back(tr);
+            sp.map.push_back((int32_t)t);
+        }
+        for (int gi : bins[b].groups) {
+            GroupRec gr{};
+            gr.f_loc = compress(flips[gi], sp.geom);
+            gr.h = highest_bit(gr.f_loc);
+            gr.t0 = (int)sp.terms.size();
+            for (int32_t t : members[gi]) {
+                TermRec tr{};
+                const uint64_t bb = y[t] | z[t];
+                tr.s_hi = bb & ~tm;
+                tr.s_loc = compress(bb, sp.geom);
+                tr.use_im = popc64(y[t]) & 1;
+                tr.scale = term_scale(t, false);
+                sp.terms.push_back(tr);
+                sp.map.push_back(t);
+            }
+            gr.t1 = (int)sp.terms.size();
+            sp.groups.push_back(gr);
+        }
+        out.push_back(std::move(sp));
+    }
+    // global fallback sweeps (flip too wide for a tile): chunks of groups
+    size_t gpos = 0;
+    while (gpos < global_groups.size()) {
+        SweepPlan sp;
+        sp.global = true;
+        std::memset(&sp.geom, 0, sizeof(sp.geom));
+        sp.geom.n = n;
+        while (gpos < global_groups.size() &&
+               (int)sp.terms.size() + (int)members[global_groups[gpos]].size() <= kCap) {
+            const int gi = global_groups[gpos++];
+            GroupRec gr{};
+            gr.f_loc = 0;
+            gr.h = highest_bit(flips[gi]);
+            gr.t0 = (int)sp.terms.size();
+            for (int32_t t : members[gi]) {
+                TermRec tr{};
+                tr.s_hi = y[t] | z[t];
+                tr.s_loc = 0;
+                tr.use_im = popc64(y[t]) & 1;
+                tr.scale = term_scale(t, false);
+                sp.terms.push_back(tr);
+                sp.map.push_back(t);
+            }
+            gr.t1 = (int)sp.terms.size();
+            sp.groups.push_back(gr);
+            sp.gflip.push_back(flips[gi]);
+        }
+        if (sp.groups.empty()) {  // a single group larger than the cap: split its terms
+            const int gi = global_groups[gpos++];
+            const auto &mem = members[gi];
+            for (size_t k0 = 0; k0 < mem.size(); k0 += kCap) {
+                SweepPlan s2;
+                s2.global = true;
+                std::memset(&s2.geom, 0, sizeof(s2.geom));
+                s2.geom.n = n;
+                GroupRec gr{};
+                gr.h = highest_bit(flips[gi]);
+                gr.t0 = 0;
+                for (size_t k = k0; k < std::min(mem.size(), k0 + kCap); ++k) {
+                    const int32_t t = mem[k];
+                    TermRec tr{};
+                    tr.s_hi = y[t] | z[t];
+                    tr.use_im = popc64(y[t]) & 1;
+                    tr.scale = term_scale(t, false);
+                    s2.terms.push_back(tr);
+                    s2.map.push_back(t);
+                }
+                gr.t1 = (int)s2.terms.size();
+                s2.groups.push_back(gr);
+                s2.gflip.push_back(flips[gi]);
+                out.push_back(std::move(s2));
+            }
+            continue;
+        }
+        out.push_back(std::move(sp));
+    }
+}
+
+}  // namespace qsv

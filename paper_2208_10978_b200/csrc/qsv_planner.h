@@ -1,0 +1,95 @@
+// qsv_planner.h -- host-side (native C++) fusion planner of the engine.
+//
+// Turns a bound gate list (the reference's Circuit, circuit.py:48-156) into a
+// short sequence of HBM passes:
+//   1. recognise pauli_evolution blocks (circuit.py:271-281: basis layer,
+//      CNOT ladder, RZ, mirror) and replace each by one direct Pauli rotation
+//      exp(-i theta/2 P) (theta = the RZ's bound value);
+//   2. group consecutive rotations that share a flip mask (they act on the
+//      same amplitude pairs, so one register sweep applies all of them);
+//   3. schedule gates / rotation groups into shared-memory tile passes by a
+//      dependency-aware first-fit: an item may move into an earlier pass past
+//      anything it commutes with (disjoint qubits for gates, even symplectic
+//      product for Pauli rotations), and a pass accepts it if its tile (low
+//      contiguous bits + up to m - c other qubits) covers the qubits the item
+//      must see (gate qubits / rotation flip bits; Z bits outside the tile are
+//      a per-tile sign).
+// Structural plans are cached by a hash of (n, kinds, qubits) so repeated
+// energy evaluations only refresh angles and matrices.
+#pragma once
+
+#include <stdint.h>
+
+#include <vector>
+
+#include "qsv_internal.h"
+
+namespace qsv {
+
+enum GateKind : int32_t {
+    K_H = 0, K_HY = 1, K_X = 2, K_CNOT = 3, K_SWAP = 4, K_RZ = 5, K_RY = 6, K_U3 = 7, K_CU3 = 8,
+    K_COUNT = 9
+};
+
+struct PassPlan {
+    TileGeom geom;
+    int op_begin = 0, op_end = 0;
+    bool global = false;  // fallback: single rotation group applied pairwise over HBM
+    uint64_t flip = 0;
+};
+
+struct ParamFill {
+    int offset;  // into params
+    int src;     // gate index
+    int kind;    // gate kind
+};
+
+struct ProgramTemplate {
+    int n = 0, m = 0, c = 0;
+    std::vector<PassPlan> passes;
+    std::vector<OpRec> ops;
+    std::vector<RotRec> rots;      // c/s refreshed per call
+    std::vector<int> rot_src;      // theta source index per RotRec
+    std::vector<ParamFill> fills;  // matrices refreshed per call
+    size_t n_params = 0;
+    // global-fallback rotation records (full 64-bit masks), per pass: rots[r0..r1)
+    int64_t n_input = 0, n_rotations = 0, n_items = 0, n_fallback = 0;
+};
+
+struct Rot {
+    uint64_t x, y, z;
+    int src;
+};
+
+// Build a template from a gate list (kinds/qubits as in qsv_apply_gates).
+void plan_gates(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                ProgramTemplate &out);
+// Build a template from an explicit rotation list.
+void plan_rotations(int n, const std::vector<Rot> &rots, int64_t n_input, ProgramTemplate &out);
+// Refresh angle-dependent data.  theta_of(src) gives the rotation angle.
+void materialize_gates(ProgramTemplate &t, const double *values);
+void materialize_rotations(ProgramTemplate &t, const double *theta);
+// Gate matrix restatement of circuit.py:198-223 (row-major complex128).
+int gate_matrix(int kind, const double *v, double *out);
+
+// ---- expectation sweep plan ----
+struct SweepPlan {
+    TileGeom geom;
+    bool global = false;  // fallback: groups evaluated pairwise over HBM
+    std::vector<GroupRec> groups;
+    std::vector<TermRec> terms;
+    std::vector<int32_t> map;  // sweep-local term -> input term index
+    int ndiag = 0;
+    std::vector<uint64_t> gflip;  // global fallback: full flip masks per group
+};
+
+void plan_expectation(int n, int64_t n_terms, const uint64_t *x, const uint64_t *y,
+                      const uint64_t *z, std::vector<SweepPlan> &out);
+
+// Device-side geometry tables of a tile (see TileDims).
+TileDims dims_of(const TileGeom &g);
+void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<int32_t> &comp32);
+
+uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits);
+
+}  // namespace qsv

@@ -1,0 +1,354 @@
+"""Device-resident dense state-vector simulation on B200 (sm_100a).
+
+Mirror of the reference's statevector module (statevector.py:26-216) for the
+hot path: the same names, argument meaning and error behaviour, with the
+amplitudes living in HBM behind a libqsv handle instead of a NumPy array.
+
+* ``StateVector`` -- (n_qubits, device amplitudes); ``.amplitudes`` downloads
+  a NumPy copy (the reference's attribute), ``.norm()`` / ``.copy()`` run on
+  the GPU.  A state made by ``init_state`` stays a lazy basis state until it
+  is first needed, so ``evolve`` writes |index> straight into its output
+  instead of copying 16 * 2^n bytes (hard part 1).
+* ``evolve`` returns a new state and leaves the input untouched
+  (statevector.py:65-74); gates run as fused shared-memory tile passes.
+* ``expectation`` keeps the Hermitian check and the 1e-10 imaginary-residue
+  check (statevector.py:98-110).
+
+Layout: basis-index bit k is qubit k (statevector.py:4-5).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .circuit import flatten_bound
+from .errors import ResourceLimitError
+from .pauli import term_arrays
+
+# One B200 holds 2^33 complex128 amplitudes (128 GiB) next to its workspace;
+# larger states need the multi-GPU path (distributed.py).
+QUBIT_CAP = 33
+
+_POOL: dict[tuple[int, int], list[int]] = {}
+_POOL_MAX = 2
+
+
+def _alloc(n: int, device: int) -> int:
+    key = (n, device)
+    bucket = _POOL.get(key)
+    if bucket:
+        return bucket.pop()
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().qsv_create(ctypes.byref(h), n, device))
+    return h.value
+
+
+def _release(n: int, device: int, h: int) -> None:
+    if not h:
+        return
+    L = _lib._lib
+    if L is None:
+        return
+    bucket = _POOL.setdefault((n, device), [])
+    if len(bucket) < _POOL_MAX and n < 30:
+        bucket.append(h)
+    else:
+        L.qsv_destroy(ctypes.c_void_p(h))
+
+
+def release_pool() -> None:
+    """Free every pooled device buffer."""
+    L = _lib._lib
+    for bucket in _POOL.values():
+        while bucket:
+            h = bucket.pop()
+            if L is not None:
+                L.qsv_destroy(ctypes.c_void_p(h))
+
+
+class _Handle:
+    __slots__ = ("value", "n", "device", "__weakref__")
+
+    def __init__(self, n: int, device: int, value: int):
+        self.value = value
+        self.n = n
+        self.device = device
+        weakref.finalize(self, _release, n, device, value)
+
+
+class StateVector:
+    """Dense 2^n complex128 state in device memory (statevector.py:26-39)."""
+
+    __slots__ = ("n_qubits", "device", "_h", "_basis")
+
+    def __init__(self, n_qubits: int, amplitudes=None, device: int = 0):
+        self.n_qubits = int(n_qubits)
+        self.device = device
+        self._h: Optional[_Handle] = None
+        self._basis: Optional[int] = None
+        if amplitudes is not None:
+            amps = np.ascontiguousarray(amplitudes, dtype=np.complex128)
+            if amps.shape != (1 << self.n_qubits,):
+                raise ValueError("amplitude vector length must be 2^n_qubits")
+            self._ensure()
+            _lib.check(_lib.lib().qsv_upload(self.handle, amps.ctypes.data_as(ctypes.c_void_p)))
+
+    # -- handle management ---------------------------------------------------
+    @classmethod
+    def _empty(cls, n: int, device: int = 0) -> "StateVector":
+        s = cls.__new__(cls)
+        s.n_qubits = n
+        s.device = device
+        s._h = None
+        s._basis = None
+        s._ensure()
+        return s
+
+    @classmethod
+    def _basis_state(cls, n: int, index: int, device: int = 0) -> "StateVector":
+        s = cls.__new__(cls)
+        s.n_qubits = n
+        s.device = device
+        s._h = None
+        s._basis = index
+        return s
+
+    def _ensure(self) -> None:
+        if self._h is None:
+            self._h = _Handle(self.n_qubits, self.device, _alloc(self.n_qubits, self.device))
+            if self._basis is not None:
+                _lib.check(_lib.lib().qsv_set_basis(self.handle, self._basis))
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        self._ensure()
+        return ctypes.c_void_p(self._h.value)
+
+    @property
+    def basis_index(self) -> Optional[int]:
+        """Index of the basis state if this is an untouched init_state() result."""
+        return self._basis if self._h is None else None
+
+    # -- reference attributes -----------------------------------------------
+    @property
+    def amplitudes(self) -> np.ndarray:
+        """Host copy of the amplitudes (NumPy complex128, index order)."""
+        out = np.empty(1 << self.n_qubits, dtype=np.complex128)
+        self.download_into(out)
+        return out
+
+    def download_into(self, out: np.ndarray) -> None:
+        if out.dtype != np.complex128 or out.size != (1 << self.n_qubits) or not out.flags.c_contiguous:
+            raise ValueError("output must be a contiguous complex128 array of length 2^n")
+        _lib.check(_lib.lib().qsv_download(self.handle, out.ctypes.data_as(ctypes.c_void_p)))
+
+    def norm(self) -> float:
+        if self.basis_index is not None:
+            return 1.0
+        v = ctypes.c_double()
+        _lib.check(_lib.lib().qsv_norm(self.handle, ctypes.byref(v)))
+        return v.value
+
+    def copy(self) -> "StateVector":
+        if self.basis_index is not None:
+            return StateVector._basis_state(self.n_qubits, self._basis, self.device)
+        out = StateVector._empty(self.n_qubits, self.device)
+        _lib.check(_lib.lib().qsv_copy(out.handle, self.handle))
+        return out
+
+    def device_ptr(self) -> int:
+        p = ctypes.c_void_p()
+        _lib.check(_lib.lib().qsv_device_ptr(self.handle, ctypes.byref(p)))
+        return p.value
+
+    @property
+    def __cuda_array_interface__(self) -> dict:
+        """Zero-copy view as (2^n, 2) float64 for torch.as_tensor / CuPy."""
+        return {"shape": (1 << self.n_qubits, 2), "typestr": "<f8",
+                "data": (self.device_ptr(), False), "version": 3, "strides": None}
+
+    def synchronize(self) -> None:
+        _lib.check(_lib.lib().qsv_synchronize(self.handle))
+
+
+def _check_cap(n: int) -> None:
+    if n > QUBIT_CAP:
+        raise ResourceLimitError(
+            f"{n} qubits exceeds the single-GPU dense cap of {QUBIT_CAP}; use distributed.py"
+        )
+
+
+def init_state(bitstring: str, device: int = 0) -> StateVector:
+    """Computational basis state; character k of the bitstring is qubit k
+    (statevector.py:42-54)."""
+    n = len(bitstring)
+    if n == 0 or any(c not in "01" for c in bitstring):
+        raise ValueError(f"invalid bitstring {bitstring!r}")
+    _check_cap(n)
+    index = sum(1 << k for k, c in enumerate(bitstring) if c == "1")
+    return StateVector._basis_state(n, index, device)
+
+
+def from_amplitudes(amplitudes, device: int = 0) -> StateVector:
+    amps = np.ascontiguousarray(amplitudes, dtype=np.complex128)
+    n = int(amps.size).bit_length() - 1
+    if amps.ndim != 1 or (1 << n) != amps.size:
+        raise ValueError("amplitude vector length must be a power of two")
+    return StateVector(n, amps, device)
+
+
+# Per-circuit flattening cache: bound circuits are immutable, so repeated
+# evolutions of the same object skip the Python walk over its gates.
+_FLAT_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_last_stats = _lib.PlanStats()
+
+
+def _flat(c):
+    try:
+        hit = _FLAT_CACHE.get(c)
+    except TypeError:
+        hit = None
+    if hit is not None:
+        return hit
+    flat = flatten_bound(c)
+    try:
+        _FLAT_CACHE[c] = flat
+    except TypeError:
+        pass
+    return flat
+
+
+def apply_circuit_inplace(s: StateVector, c) -> None:
+    """Apply a bound circuit to s in place (the loop of statevector.py:72-73)."""
+    kinds, qubits, values = _flat(c)
+    _lib.check(_lib.lib().qsv_apply_gates(s.handle, len(kinds), _lib.i32ptr(kinds),
+                                          _lib.i32ptr(qubits), _lib.dptr(values),
+                                          ctypes.byref(_last_stats)))
+
+
+def evolve(s: StateVector, c) -> StateVector:
+    """Apply a bound circuit; returns a new state (statevector.py:65-74)."""
+    if c.n_qubits != s.n_qubits:
+        raise ValueError("circuit and state qubit counts differ")
+    if not c.is_bound():
+        raise RuntimeError("circuit must be bound before evolution")
+    out = StateVector._empty(s.n_qubits, s.device)
+    if s.basis_index is not None:
+        _lib.check(_lib.lib().qsv_set_basis(out.handle, s.basis_index))
+    else:
+        _lib.check(_lib.lib().qsv_copy(out.handle, s.handle))
+    apply_circuit_inplace(out, c)
+    return out
+
+
+def apply_rotations(s: StateVector, x, y, z, theta) -> StateVector:
+    """New state = prod_r exp(-i theta_r/2 P_r) s (direct Pauli-rotation path)."""
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    y = np.ascontiguousarray(y, dtype=np.uint64)
+    z = np.ascontiguousarray(z, dtype=np.uint64)
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    out = s.copy()
+    _lib.check(_lib.lib().qsv_apply_pauli_rotations(out.handle, len(theta), _lib.u64ptr(x),
+                                                    _lib.u64ptr(y), _lib.u64ptr(z),
+                                                    _lib.dptr(theta), ctypes.byref(_last_stats)))
+    return out
+
+
+def last_plan_stats() -> dict:
+    """Planner statistics of the last evolve / apply_rotations / expectation."""
+    st = _lib.PlanStats()
+    _lib.check(_lib.lib().qsv_last_plan_stats(ctypes.byref(st)))
+    return st.as_dict()
+
+
+_H_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _hamiltonian(h, n: int):
+    key = (n,)
+    try:
+        hit = _H_CACHE.get(h)
+    except TypeError:
+        hit = None
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    arrays = term_arrays(h, n)
+    try:
+        _H_CACHE[h] = (key, arrays)
+    except TypeError:
+        pass
+    return arrays
+
+
+def expectation_terms(s: StateVector, h) -> tuple[float, float, np.ndarray]:
+    """(Re, Im residue, per-term <P_t>) of <s|H|s>; no Hermitian checks."""
+    x, y, z, cr, ci = _hamiltonian(h, s.n_qubits)
+    re, im = ctypes.c_double(), ctypes.c_double()
+    per = np.zeros(len(cr), dtype=np.float64)
+    if len(cr):
+        _lib.check(_lib.lib().qsv_expectation(s.handle, len(cr), _lib.u64ptr(x), _lib.u64ptr(y),
+                                              _lib.u64ptr(z), _lib.dptr(cr), _lib.dptr(ci),
+                                              ctypes.byref(re), ctypes.byref(im), _lib.dptr(per),
+                                              None))
+    return re.value, im.value, per
+
+
+def expectation(s: StateVector, h) -> float:
+    """<s|H|s> (statevector.py:98-110)."""
+    if not h.is_hermitian():
+        raise ValueError("expectation requires a Hermitian operator (real coefficients)")
+    re, im, _ = expectation_terms(s, h)
+    if abs(im) > 1e-10:
+        raise ArithmeticError(f"expectation has imaginary residue {im:.3e}")
+    return float(re)
+
+
+def apply_pauli_string(s: StateVector, p) -> StateVector:
+    """P|s> (statevector.py:91-95)."""
+    x, y, z = _masks(p, s.n_qubits)
+    out = StateVector._empty(s.n_qubits, s.device)
+    _lib.check(_lib.lib().qsv_apply_pauli(s.handle, out.handle, x, y, z))
+    return out
+
+
+def _masks(p, n: int) -> tuple[int, int, int]:
+    x = y = zm = 0
+    for q, axis in p.factors:
+        if q >= n:
+            raise ValueError(f"string index {q} out of range for {n} qubits")
+        if axis == "X":
+            x |= 1 << q
+        elif axis == "Y":
+            y |= 1 << q
+        else:
+            zm |= 1 << q
+    return x, y, zm
+
+
+def apply_operator(s: StateVector, h) -> StateVector:
+    """H|s> as a dense (unnormalised) vector (statevector.py:113-121)."""
+    x, y, z, cr, ci = _hamiltonian(h, s.n_qubits)
+    out = StateVector._empty(s.n_qubits, s.device)
+    _lib.check(_lib.lib().qsv_apply_operator(s.handle, out.handle, len(cr), _lib.u64ptr(x),
+                                             _lib.u64ptr(y), _lib.u64ptr(z), _lib.dptr(cr),
+                                             _lib.dptr(ci)))
+    return out
+
+
+def vdot(a: StateVector, b: StateVector) -> complex:
+    """np.vdot(a, b) = sum conj(a) b (engine.py:74-75)."""
+    if a.n_qubits != b.n_qubits:
+        raise ValueError("state qubit counts differ")
+    out = np.zeros(2, dtype=np.float64)
+    _lib.check(_lib.lib().qsv_vdot(a.handle, b.handle, _lib.dptr(out)))
+    return complex(out[0], out[1])
+
+
+def dump_state(s: StateVector) -> bytes:
+    """Little-endian complex-double amplitude dump (statevector.py:214-216)."""
+    return s.amplitudes.astype("<c16").tobytes()

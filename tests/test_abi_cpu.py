@@ -1,0 +1,105 @@
+"""The C-ABI library loads without a GPU and exports every symbol that
+include/qsv.h declares; the native planner (no device work) is exercised on
+the BASELINE configs."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import REPO
+from paper_2208_10978_b200 import _lib
+from paper_2208_10978_b200 import workloads as W
+from paper_2208_10978_b200.circuit import Circuit, Constant, Gate, evolution_gates, flatten_bound
+from paper_2208_10978_b200.pauli import PauliString, term_arrays
+
+
+def header_symbols():
+    text = open(os.path.join(REPO, "include", "qsv.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(qsv_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+    assert L.qsv_abi_version() == 1
+
+
+def plan(circ):
+    k, q, _ = flatten_bound(circ)
+    st = _lib.PlanStats()
+    _lib.check(_lib.lib().qsv_plan_gates(circ.n_qubits, len(k), _lib.i32ptr(k), _lib.i32ptr(q),
+                                         ctypes.byref(st)))
+    return st.as_dict()
+
+
+def test_planner_config1_single_pass():
+    st = plan(W.config1()["circuit"])
+    assert st["n_input_ops"] == 37824
+    assert st["n_rotations"] == 1872
+    assert st["n_items"] == 261  # same-flip groups
+    assert st["n_passes"] == 1   # 12 qubits = one shared-memory tile
+
+
+def test_planner_config2_fuses_brickwork():
+    st = plan(W.config2()["circuit"])
+    assert st["n_input_ops"] == 830
+    assert st["n_rotations"] == 0
+    assert st["n_passes"] <= 60
+
+
+def test_pattern_matcher_recognises_every_block():
+    rng = np.random.default_rng(0)
+    n = 20
+    gates = []
+    for _ in range(50):
+        w = int(rng.integers(1, 8))
+        pos = rng.choice(n, size=w, replace=False)
+        axes = rng.choice(list("XYZ"), size=w)
+        s = PauliString(tuple(zip((int(p) for p in pos), axes)))
+        gates.extend(evolution_gates(s, Constant(float(rng.uniform(-1, 1)))))
+        if rng.random() < 0.3:  # a stray gate between blocks must stay a gate
+            gates.append(Gate("H", (int(rng.integers(n)),)))
+    st = plan(Circuit(n, tuple(gates), 0))
+    assert st["n_rotations"] == 50
+
+
+def test_planner_rejects_bad_gates():
+    k = np.array([3], dtype=np.int32)
+    q = np.array([2, 2], dtype=np.int32)
+    st = _lib.PlanStats()
+    with pytest.raises(ValueError):
+        _lib.check(_lib.lib().qsv_plan_gates(4, 1, _lib.i32ptr(k), _lib.i32ptr(q), ctypes.byref(st)))
+    q = np.array([1, 7], dtype=np.int32)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.lib().qsv_plan_gates(4, 1, _lib.i32ptr(k), _lib.i32ptr(q), ctypes.byref(st)))
+
+
+def test_expectation_planner_config3():
+    h = W.config3_hamiltonian()
+    x, y, z, _, _ = term_arrays(h, 30)
+    st = _lib.PlanStats()
+    _lib.check(_lib.lib().qsv_plan_expectation(30, len(x), _lib.u64ptr(x), _lib.u64ptr(y),
+                                               _lib.u64ptr(z), ctypes.byref(st)))
+    assert st.n_fallback == 0
+    assert 1 <= st.n_passes <= 300
+    # a flip wider than a tile needs the global fallback sweep
+    x2 = np.array([(1 << 20) - 1], dtype=np.uint64)
+    zz = np.zeros(1, dtype=np.uint64)
+    _lib.check(_lib.lib().qsv_plan_expectation(30, 1, _lib.u64ptr(x2), _lib.u64ptr(zz),
+                                               _lib.u64ptr(zz), ctypes.byref(st)))
+    assert st.n_fallback == 1
+
+
+def test_no_gpu_compute_fails_loudly():
+    if _lib.device_count() > 0:
+        pytest.skip("a GPU is present")
+    h = ctypes.c_void_p()
+    with pytest.raises(_lib.QsvCudaError):
+        _lib.check(_lib.lib().qsv_create(ctypes.byref(h), 4, 0))

@@ -1,0 +1,256 @@
+"""CUDA engine vs the reference golden vectors and the CPU oracle.
+
+Tolerances (north_star): amplitudes within 1e-10 max-abs, energies within
+1e-10 relative, FP64 throughout."""
+
+import numpy as np
+import pytest
+
+from conftest import parse_h, random_state
+from oracle import oracle as O
+from paper_2208_10978_b200 import engine, kernels
+from paper_2208_10978_b200 import statevector as sv
+from paper_2208_10978_b200 import workloads as W
+from paper_2208_10978_b200.circuit import (Circuit, Constant, Gate, bind, circuit_from_json,
+                                           evolution_gates, gate_matrix)
+from paper_2208_10978_b200.errors import ResourceLimitError
+from paper_2208_10978_b200.pauli import PauliString, PauliSum, PauliTerm
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-10
+REL_TOL = 1e-10
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def test_kernels_implementation_is_cuda():
+    assert kernels.IMPLEMENTATION == "cuda-sm_100a"
+
+
+@pytest.mark.parametrize("n", [5, 9])
+def test_golden_mixed_circuits(golden, n):
+    circ = circuit_from_json(str(golden[f"mixed_n{n}_circuit"]))
+    s0 = sv.from_amplitudes(golden[f"mixed_n{n}_in"])
+    s1 = sv.evolve(s0, circ)
+    assert np.abs(s1.amplitudes - golden[f"mixed_n{n}_out"]).max() <= AMP_TOL
+    # input untouched (statevector.py:71)
+    assert np.array_equal(s0.amplitudes, golden[f"mixed_n{n}_in"])
+
+
+@pytest.mark.parametrize("n", [6, 10])
+def test_golden_brickwork(golden, n):
+    circ = circuit_from_json(str(golden[f"brick_n{n}_circuit"]))
+    out = sv.evolve(sv.init_state("0" * n), circ).amplitudes
+    assert np.abs(out - golden[f"brick_n{n}_out"]).max() <= AMP_TOL
+
+
+def test_golden_apply_pauli(golden):
+    s = sv.from_amplitudes(golden["pauli_in"])
+    for (x, y, z), ref in zip(golden["pauli_masks"], golden["pauli_out"]):
+        out = sv.StateVector._empty(s.n_qubits)
+        kernels.apply_pauli(s, int(x), int(y), int(z), out)
+        assert np.abs(out.amplitudes - ref).max() <= 1e-15
+
+
+def test_golden_expectation(golden):
+    s = sv.from_amplitudes(golden["expect_state"])
+    h = parse_h(golden["expect_h"])
+    e = sv.expectation(s, h)
+    assert rel(e, float(golden["expect_value"])) <= REL_TOL
+    _, _, per = sv.expectation_terms(s, h)
+    assert np.abs(per - golden["expect_per_term"].real).max() <= 1e-12
+    out = sv.apply_operator(s, h).amplitudes
+    assert np.abs(out - golden["apply_operator_out"]).max() <= AMP_TOL
+
+
+def test_golden_uccsd8(golden):
+    circ = circuit_from_json(str(golden["uccsd8_circuit"]))
+    be = engine.StateVectorBackend()
+    psi = be.evolve(be.prepare(str(golden["uccsd8_reference"])), circ)
+    assert np.abs(psi.amplitudes - golden["uccsd8_out"]).max() <= AMP_TOL
+    e = be.expectation(psi, parse_h(golden["uccsd8_h"]))
+    assert rel(e, float(golden["uccsd8_energy"])) <= REL_TOL
+
+
+def test_h2_fixture_energies(h2_fixtures):
+    be = engine.StateVectorBackend()
+    for name, fx in h2_fixtures.items():
+        h = parse_h(fx["hamiltonian"])
+        s0 = be.prepare(fx["reference"])
+        assert rel(be.expectation(s0, h), fx["fixture_hf_energy"]) <= REL_TOL, name
+        ansatz = circuit_from_json(fx["ansatz"])
+        psi = be.evolve(s0, bind(ansatz, fx["theta_opt"]))
+        assert rel(be.expectation(psi, h), fx["fixture_fci_energy"]) <= REL_TOL, name
+        assert abs(be.overlap(psi, psi) - 1.0) <= 1e-12
+
+
+def test_config1_full(config1_golden):
+    cfg = W.config1(seed=0)
+    psi = sv.evolve(sv.init_state(cfg["reference"]), cfg["circuit"])
+    st = sv.last_plan_stats()
+    assert st["n_rotations"] == 1872 and st["n_passes"] == 1
+    assert np.abs(psi.amplitudes - config1_golden["amplitudes"]).max() <= AMP_TOL
+    assert rel(sv.expectation(psi, cfg["hamiltonian"]), float(config1_golden["energy"])) <= REL_TOL
+
+
+@pytest.mark.parametrize("n", [3, 7, 12, 13, 15])
+def test_apply_1q_2q_every_position(n):
+    rng = np.random.default_rng(n)
+    st = random_state(n, rng)
+    s = sv.from_amplitudes(st)
+    ref = st.copy()
+    for q in range(n):
+        m = O.gate_matrix("U3", tuple(rng.uniform(-3, 3, size=3)))
+        kernels.apply_1q(s, m, q)
+        O.apply_1q(ref, m, q)
+    for _ in range(2 * n):
+        q0, q1 = (int(v) for v in rng.choice(n, size=2, replace=False))
+        m = O.gate_matrix("CU3", tuple(rng.uniform(-3, 3, size=3)))
+        kernels.apply_2q(s, m, q0, q1)
+        O.apply_2q(ref, m, q0, q1)
+    assert np.abs(s.amplitudes - ref).max() <= AMP_TOL
+
+
+def random_mixed(n, n_gates, rng):
+    kinds = ["H", "HY", "X", "CNOT", "SWAP", "RZ", "RY", "U3", "CU3"]
+    nparams = {"RZ": 1, "RY": 1, "U3": 3, "CU3": 3}
+    gates = []
+    for _ in range(n_gates):
+        k = kinds[rng.integers(len(kinds))]
+        nq = 2 if k in ("CNOT", "SWAP", "CU3") else 1
+        qs = tuple(int(q) for q in rng.choice(n, size=nq, replace=False))
+        ps = tuple(Constant(float(v)) for v in rng.uniform(-3, 3, size=nparams.get(k, 0)))
+        gates.append(Gate(k, qs, ps))
+    return Circuit(n, tuple(gates), 0)
+
+
+@pytest.mark.parametrize("n,g", [(14, 300), (17, 400)])
+def test_random_mixed_multi_tile(n, g):
+    rng = np.random.default_rng(100 + n)
+    circ = random_mixed(n, g, rng)
+    st = random_state(n, rng)
+    out = sv.evolve(sv.from_amplitudes(st), circ).amplitudes
+    ref = O.evolve(st, circ.gates)
+    assert np.abs(out - ref).max() <= AMP_TOL
+
+
+def random_rotations(n, count, rng, max_w=6):
+    strings, thetas = [], []
+    for _ in range(count):
+        w = int(rng.integers(1, max_w + 1))
+        pos = rng.choice(n, size=w, replace=False)
+        axes = rng.choice(list("XYZ"), size=w)
+        strings.append(PauliString(tuple(zip((int(p) for p in pos), axes))))
+        thetas.append(float(rng.uniform(-1, 1)))
+    return strings, thetas
+
+
+@pytest.mark.parametrize("n", [13, 18])
+def test_rotations_vs_decomposed_oracle(n):
+    rng = np.random.default_rng(7 * n)
+    strings, thetas = random_rotations(n, 120, rng)
+    # repeat flips to exercise same-flip groups
+    strings += strings[:10]
+    thetas += thetas[:10]
+    circ = W.rotations_circuit(n, strings, thetas)
+    st = random_state(n, rng)
+    out = sv.evolve(sv.from_amplitudes(st), circ)
+    assert sv.last_plan_stats()["n_rotations"] == len(strings)
+    ref = O.evolve(st, circ.gates)
+    assert np.abs(out.amplitudes - ref).max() <= AMP_TOL
+    # direct rotation API agrees too
+    x, y, z = W.string_masks(strings)
+    out2 = sv.apply_rotations(sv.from_amplitudes(st), x, y, z, np.array(thetas))
+    assert np.abs(out2.amplitudes - ref).max() <= AMP_TOL
+
+
+def test_wide_flip_global_fallback():
+    n = 18
+    rng = np.random.default_rng(3)
+    s = PauliString(tuple((q, "XY"[q % 2]) for q in range(2, 16)) + ((17, "Z"),))
+    circ = W.rotations_circuit(n, [s, s], [0.7, -0.2])
+    st = random_state(n, rng)
+    out = sv.evolve(sv.from_amplitudes(st), circ)
+    assert sv.last_plan_stats()["n_fallback"] >= 1
+    ref = O.evolve(st, circ.gates)
+    assert np.abs(out.amplitudes - ref).max() <= AMP_TOL
+    h = PauliSum((PauliTerm(0.8, s), PauliTerm(-1.1, PauliString.from_label("X3 Y9 Z17"))))
+    e = sv.expectation(sv.from_amplitudes(ref), h)
+    assert rel(e, O.expectation(ref, h, n)) <= REL_TOL
+
+
+@pytest.mark.parametrize("n,S", [(12, 400), (16, 600), (20, 300)])
+def test_expectation_vs_oracle(n, S):
+    rng = np.random.default_rng(n * 31 + S)
+    h = W.sparse_random_hamiltonian(n, S, rng, z_only=S // 3)
+    h = PauliSum(h.terms + (PauliTerm(0.5, PauliString()),))  # identity term
+    st = random_state(n, rng)
+    s = sv.from_amplitudes(st)
+    e = sv.expectation(s, h)
+    ref, per_ref = O.expectation(st, h, n, per_term=True)
+    assert rel(e, ref) <= REL_TOL
+    _, _, per = sv.expectation_terms(s, h)
+    assert np.abs(per - per_ref[:, 0]).max() <= 1e-12
+
+
+def test_dense_hamiltonian_config1_shape():
+    rng = np.random.default_rng(11)
+    h = W.dense_random_hamiltonian(12, 500, rng)
+    st = random_state(12, rng)
+    assert rel(sv.expectation(sv.from_amplitudes(st), h), O.expectation(st, h, 12)) <= REL_TOL
+
+
+def test_brickwork_vs_oracle_20q():
+    circ = W.brickwork(20, 6, seed=5)
+    out = sv.evolve(sv.init_state("0" * 20), circ).amplitudes
+    ref = O.evolve(O.init_state("0" * 20), circ.gates)
+    assert np.abs(out - ref).max() <= AMP_TOL
+
+
+def inverse(circ):
+    gates = []
+    for g in reversed(circ.gates):
+        if g.kind == "U3":
+            th, ph, la = g.bound_values()
+            gates.append(Gate("U3", g.qubits, (Constant(-th), Constant(-la), Constant(-ph))))
+        else:
+            gates.append(g)
+    return Circuit(circ.n_qubits, tuple(gates), 0)
+
+
+@pytest.mark.parametrize("n,layers", [(26, 6), (28, 20)])
+def test_brickwork_mirror_large(n, layers):
+    circ = W.brickwork(n, layers, seed=0)
+    psi = sv.evolve(sv.init_state("0" * n), circ)
+    assert abs(psi.norm() - 1.0) <= 1e-12
+    back = sv.evolve(psi, inverse(circ))
+    a = back.amplitudes
+    assert abs(a[0] - 1.0) <= 1e-10
+    a[0] = 0
+    assert np.abs(a).max() <= 1e-10
+
+
+def test_backend_protocol_and_errors():
+    be = engine.StateVectorBackend()
+    assert be.name == "sv-b200" and be.supports_reverse_gradient is False
+    s0 = be.prepare("1100")
+    assert s0.amplitudes[3] == 1.0
+    circ = Circuit(4, (Gate("H", (0,)),), 0)
+    with pytest.raises(ValueError):
+        be.evolve(be.prepare("110"), circ)
+    from paper_2208_10978_b200.circuit import Affine
+    with pytest.raises(RuntimeError):
+        be.evolve(s0, Circuit(4, (Gate("RZ", (0,), (Affine(0, 1.0),)),), 1))
+    with pytest.raises(ValueError):
+        be.expectation(s0, PauliSum((PauliTerm(1j, PauliString.from_label("Z0")),)))
+    with pytest.raises(ValueError):
+        be.expectation(s0, PauliSum((PauliTerm(1.0, PauliString.from_label("Z7")),)))
+    with pytest.raises(ValueError):
+        sv.init_state("01x")
+    with pytest.raises(ResourceLimitError):
+        sv.init_state("0" * 40)
+    psi = be.evolve(s0, circ)
+    assert abs(be.overlap(psi, s0) - np.sqrt(0.5)) <= 1e-15

@@ -1,0 +1,101 @@
+"""Host-side logic without a GPU: IR, interchange formats, JW generator,
+workload determinism, LPT partition semantics."""
+
+import io
+
+import numpy as np
+import pytest
+
+from conftest import parse_h
+from paper_2208_10978_b200 import engine
+from paper_2208_10978_b200 import workloads as W
+from paper_2208_10978_b200.circuit import (Affine, Circuit, Constant, Gate, bind, circuit_from_json,
+                                           circuit_to_json, flatten_bound, gate_matrix,
+                                           pauli_evolution)
+from paper_2208_10978_b200.errors import FormatError
+from paper_2208_10978_b200.pauli import PauliString, PauliSum, read_pauli_sum, write_pauli_sum
+
+
+def test_pauli_text_roundtrip(golden):
+    h = parse_h(golden["expect_h"])
+    buf = io.StringIO()
+    write_pauli_sum(h, buf)
+    assert buf.getvalue() == str(golden["expect_h"])
+    with pytest.raises(FormatError):
+        read_pauli_sum(io.StringIO("1.0 X0 X0\n"))
+    with pytest.raises(FormatError):
+        read_pauli_sum(io.StringIO("abc X0\n"))
+
+
+def test_circuit_json_roundtrip(golden):
+    text = str(golden["uccsd8_circuit"])
+    assert circuit_to_json(circuit_from_json(text)) == text
+
+
+def test_gate_validation():
+    with pytest.raises(ValueError):
+        Gate("CNOT", (1, 1))
+    with pytest.raises(ValueError):
+        Gate("RZ", (0,))
+    with pytest.raises(ValueError):
+        Circuit(2, (Gate("H", (2,)),))
+    c = Circuit(2, (Gate("RZ", (0,), (Affine(0, 2.0, 0.5),)),), 1)
+    with pytest.raises(RuntimeError):
+        flatten_bound(c)
+    b = bind(c, [0.25])
+    assert b.gates[0].bound_values() == (1.0,)
+    with pytest.raises(ValueError):
+        bind(c, [np.nan])
+
+
+def test_gate_matrices_unitary():
+    for kind, vals in [("H", ()), ("HY", ()), ("RZ", (0.3,)), ("RY", (1.1,)), ("U3", (0.4, 1.3, -2.0)),
+                       ("CU3", (0.4, 1.3, -2.0)), ("CNOT", ()), ("SWAP", ()), ("X", ())]:
+        m = gate_matrix(kind, vals)
+        assert np.allclose(m.conj().T @ m, np.eye(m.shape[0]), atol=1e-14)
+    hy = gate_matrix("HY")
+    y = np.array([[0, -1j], [1j, 0]])
+    z = np.diag([1, -1])
+    assert np.allclose(hy @ z @ hy, y)  # HY rotates the Y eigenbasis onto Z
+
+
+def test_pauli_evolution_gate_pattern():
+    p = PauliString.from_label("X0 Z2 Y5")
+    c = pauli_evolution(p, 0.3, 6)
+    kinds = [g.kind for g in c.gates]
+    assert kinds == ["H", "HY", "CNOT", "CNOT", "RZ", "CNOT", "CNOT", "H", "HY"]
+    assert c.gates[4].bound_values() == (-0.6,)
+    assert c.gates[4].qubits == (5,)
+
+
+def test_workload_shapes():
+    c1 = W.config1()
+    assert len(c1["strings"]) == 1872 and c1["reference"] == "111111000000"
+    assert len(c1["hamiltonian"]) == 500 and c1["hamiltonian"].is_hermitian()
+    c2 = W.config2()
+    assert len(c2["circuit"].gates) == 830
+    assert sum(g.kind == "CNOT" for g in c2["circuit"].gates) == 270
+    h3 = W.config3_hamiltonian()
+    assert len(h3) == 10_000
+    zonly = [all(a == "Z" for _, a in t.string.factors) for t in h3.terms]
+    assert all(zonly[:3000]) and not any(zonly[3000:])
+    assert all(1 <= t.string.weight <= 4 for t in h3.terms)
+
+
+def test_workload_determinism():
+    a = W.brickwork(8, 3, seed=7)
+    b = W.brickwork(8, 3, seed=7)
+    assert circuit_to_json(a) == circuit_to_json(b)
+    s = W.config3_state(seed=1, n_qubits=12, chunk_bits=8)
+    assert abs(np.linalg.norm(s) - 1) < 1e-12
+
+
+def test_plan_partition_lpt():
+    h = PauliSum.from_terms([(1.0, PauliString.from_label(lbl)) for lbl in
+                             ["X0", "X0 X1 X2", "Z3", "Y1 Y2", "Z0 Z1 Z2 Z3", ""]])
+    plan = engine.plan_partition(h, 2)
+    seen = sorted(i for p in plan.partitions for i in p)
+    assert seen == list(range(6))
+    loads = [sum(plan.costs[i] for i in p) for p in plan.partitions]
+    assert max(loads) <= sum(plan.costs) / 2 + max(plan.costs)
+    assert plan.partitions == engine.plan_partition(h, 2).partitions  # deterministic
