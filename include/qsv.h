@@ -126,6 +126,12 @@ int qsv_plan_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const in
 int qsv_plan_expectation(int n_qubits, int64_t n_terms, const uint64_t *x, const uint64_t *y,
                          const uint64_t *z, qsv_plan_stats *out);
 
+/* Debug: the compiled tile program for a gate list as JSON (planner output
+ * consumed by the CPU emulator in tests/).  needed receives the buffer size. */
+int qsv_debug_plan_json(int n_qubits, int64_t n_gates, const int32_t *kinds,
+                        const int32_t *qubits, const double *values, char *out, int64_t cap,
+                        int64_t *needed);
+
 /* Statistics of the last plan on the calling thread (see qsv_plan_stats). */
 int qsv_last_plan_stats(qsv_plan_stats *out);
 

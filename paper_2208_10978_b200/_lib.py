@@ -51,7 +51,7 @@ EXPORTED = (
     "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_apply_1q", "qsv_apply_2q",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
-    "qsv_plan_expectation", "qsv_last_plan_stats",
+    "qsv_plan_expectation", "qsv_debug_plan_json", "qsv_last_plan_stats",
 )
 
 _lib = None
@@ -90,6 +90,8 @@ def _declare(L):
                        ctypes.c_double], ctypes.c_int),
         "qsv_plan_gates": ([ctypes.c_int, i64, i32p, i32p, sp], ctypes.c_int),
         "qsv_plan_expectation": ([ctypes.c_int, i64, u64p, u64p, u64p, sp], ctypes.c_int),
+        "qsv_debug_plan_json": ([ctypes.c_int, i64, i32p, i32p, dp, ctypes.c_char_p, i64,
+                                 ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_last_plan_stats": ([sp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -128,6 +130,19 @@ def device_count() -> int:
     n = ctypes.c_int(0)
     rc = lib().qsv_device_count(ctypes.byref(n))
     return n.value if rc == QSV_OK else 0
+
+
+def debug_plan(n_qubits: int, kinds, qubits, values) -> dict:
+    """Compiled tile program of a flattened gate list (planner debug export)."""
+    import json
+
+    need = ctypes.c_int64(0)
+    check(lib().qsv_debug_plan_json(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits),
+                                    dptr(values), None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(lib().qsv_debug_plan_json(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits),
+                                    dptr(values), buf, need.value, ctypes.byref(need)))
+    return json.loads(buf.value.decode())
 
 
 def dptr(a):

@@ -182,13 +182,14 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     const size_t o_ops = b.add(t.ops.data(), t.ops.size() * sizeof(OpRec));
     const size_t o_rots = b.add(t.rots.data(), t.rots.size() * sizeof(RotRec));
     const size_t o_par = b.add(params.data(), params.size() * sizeof(double));
+    const size_t o_blk = b.add(t.blocks.data(), t.blocks.size() * sizeof(BlockRec));
     std::vector<size_t> o_off(t.passes.size()), o_comp(t.passes.size());
     {
         std::vector<uint64_t> offhi;
         std::vector<int32_t> comp;
         for (size_t k = 0; k < t.passes.size(); ++k) {
             if (t.passes[k].global) continue;
-            geom_tables(t.passes[k].geom, offhi, comp);
+            geom_tables(t.passes[k].geom, offhi, comp, &t.passes[k]);
             o_off[k] = b.add(offhi.data(), offhi.size() * sizeof(uint64_t));
             o_comp[k] = b.add(comp.data(), comp.size() * sizeof(int32_t));
         }
@@ -202,13 +203,21 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     const double *d_par = (const double *)(d + o_par);
     for (size_t k = 0; k < t.passes.size(); ++k) {
         const PassPlan &p = t.passes[k];
-        if (p.op_end <= p.op_begin) continue;
+        // a pass made only of permutation gates has no blocks but a permuted
+        // store map: it still has to run (load -> store through the map)
+        if (p.op_end <= p.op_begin && !p.map_permuted) continue;
         if (p.global) {
             for (int k = p.op_begin; k < p.op_end; ++k) {
                 const OpRec &op = t.ops[k];
                 QSV_CUDA(launch_rot_global(s->amps, s->n, p.flip, d_rots + op.r0, op.r1 - op.r0,
                                            s->stream));
             }
+        } else if (p.geom.m >= 4) {
+            QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o_off[k]),
+                                        (const int32_t *)(d + o_comp[k]),
+                                        (const BlockRec *)(d + o_blk) + p.block_begin,
+                                        p.block_end - p.block_begin, d_ops, d_rots, d_par,
+                                        s->stream));
         } else {
             QSV_CUDA(launch_tile_pass(s->amps, dims_of(p.geom), (const uint64_t *)(d + o_off[k]),
                                       (const int32_t *)(d + o_comp[k]), d_ops + p.op_begin,
@@ -771,6 +780,75 @@ int qsv_plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y,
     for (const SweepPlan &sp : plan) st.n_fallback += sp.global ? 1 : 0;
     st.tile_bits = plan.empty() ? 0 : plan.front().geom.m;
     *out = st;
+    return QSV_OK;
+}
+
+// Debug export of the compiled tile program (JSON) for the CPU emulator in
+// tests/ -- lets the planner and its encoding be verified without a GPU.
+int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                        const double *values, char *out, int64_t cap, int64_t *needed)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (n < 1 || n > kMaxQubits) return fail_code(QSV_ERR_RESOURCE, "qubit count out of range");
+    qsv_state fake;
+    fake.n = n;
+    if (int rc = validate_gates(&fake, n_gates, kinds, qubits)) return rc;
+    ProgramTemplate t;
+    plan_gates(n, n_gates, kinds, qubits, t);
+    materialize_gates(t, values);
+    std::vector<double> params(t.n_params);
+    for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, &params[f.offset]);
+    std::string j = "{\"n\":" + std::to_string(n) + ",\"passes\":[";
+    char buf[256];
+    for (size_t k = 0; k < t.passes.size(); ++k) {
+        const PassPlan &p = t.passes[k];
+        if (k) j += ",";
+        j += "{\"global\":" + std::to_string(p.global ? 1 : 0);
+        snprintf(buf, sizeof(buf), ",\"flip\":%llu", (unsigned long long)p.flip);
+        j += buf;
+        j += ",\"m\":" + std::to_string(p.geom.m) + ",\"c\":" + std::to_string(p.geom.c);
+        j += ",\"pos\":[";
+        for (int i = 0; i < p.geom.m; ++i) j += (i ? "," : "") + std::to_string(p.geom.pos[i]);
+        j += "],\"comp\":[";
+        for (int i = 0; i < p.geom.ncomp; ++i) j += (i ? "," : "") + std::to_string(p.geom.comp[i]);
+        j += "],\"store_cols\":[";
+        for (int i = 0; i < 12; ++i) j += (i ? "," : "") + std::to_string(p.store_cols[i]);
+        j += "],\"store_t\":" + std::to_string(p.store_t);
+        j += ",\"op_begin\":" + std::to_string(p.op_begin) + ",\"op_end\":" + std::to_string(p.op_end);
+        j += ",\"blocks\":[";
+        for (int b = p.block_begin; b < p.block_end; ++b) {
+            const BlockRec &br = t.blocks[b];
+            if (b > p.block_begin) j += ",";
+            j += "{\"kind\":" + std::to_string(br.kind) + ",\"op0\":" + std::to_string(br.op0) +
+                 ",\"op1\":" + std::to_string(br.op1) + ",\"tswz\":" + std::to_string(br.tswz) +
+                 ",\"cols\":[";
+            for (int i = 0; i < 12; ++i) j += (i ? "," : "") + std::to_string(br.cols[i]);
+            j += "]}";
+        }
+        j += "]}";
+    }
+    j += "],\"ops\":[";
+    for (size_t k = 0; k < t.ops.size(); ++k) {
+        const OpRec &o = t.ops[k];
+        snprintf(buf, sizeof(buf), "%s[%d,%d,%d,%d,%d,%d,%d,%u]", k ? "," : "", o.type, o.a, o.b, o.h,
+                 o.r0, o.r1, o.p, o.f);
+        j += buf;
+    }
+    j += "],\"rots\":[";
+    for (size_t k = 0; k < t.rots.size(); ++k) {
+        const RotRec &r = t.rots[k];
+        snprintf(buf, sizeof(buf), "%s[%llu,%u,%d,%.17g,%.17g]", k ? "," : "",
+                 (unsigned long long)r.s_hi, r.s_loc, r.q, r.c, r.s);
+        j += buf;
+    }
+    j += "],\"params\":[";
+    for (size_t k = 0; k < params.size(); ++k) {
+        snprintf(buf, sizeof(buf), "%s%.17g", k ? "," : "", params[k]);
+        j += buf;
+    }
+    j += "]}";
+    if (needed) *needed = (int64_t)j.size() + 1;
+    if (out && cap > (int64_t)j.size()) std::memcpy(out, j.c_str(), j.size() + 1);
     return QSV_OK;
 }
 

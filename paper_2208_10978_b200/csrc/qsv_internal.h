@@ -48,6 +48,24 @@ struct RotRec {     // 32 B
     double c, s;    // cos(theta/2), sin(theta/2)
 };
 
+// A block of the tile kernel.  The SMEM tile is addressed through a
+// GF(2)-affine map slot(L) = swz(A L ^ t) of the logical tile index L, so
+// permutation gates (CNOT, SWAP, X) cost nothing on the device: the planner
+// folds them into (A, t).  cols[] hold swizzled map columns:
+//   kind 0 (register block, <= 4 logical bits B): cols[0..7] = columns of the
+//          non-B bits in ascending order (= thread-index bits), cols[8..11] =
+//          columns of B (block-local bits 0..3); ops[op0..op1) use
+//          block-local bit indices.
+//   kind 1 (wide-flip rotation group on SMEM): cols[b] = column of tile bit b.
+struct BlockRec {  // 48 B
+    int32_t kind;
+    int32_t op0, op1;
+    uint16_t cols[12];
+    uint16_t tswz;
+    uint16_t pad0;
+    int32_t pad[2];
+};
+
 // Tile geometry of one pass (host side): local bit i <-> physical bit pos[i]; pos[i] = i
 // for i < c (contiguous low block).  The tile index enumerates the n - m
 // complement bits comp[] in ascending order.
@@ -106,6 +124,10 @@ int num_sms(int device);
 cudaError_t launch_tile_pass(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                              const int32_t *d_comp, const OpRec *d_ops, int nops,
                              const RotRec *d_rots, const double *d_params, cudaStream_t st);
+cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
+                               const int32_t *d_comp, const BlockRec *d_blocks, int nblocks,
+                               const OpRec *d_ops, const RotRec *d_rots, const double *d_params,
+                               cudaStream_t st);
 cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                                 const int32_t *d_comp, const GroupRec *d_groups,
                                 int ngroups, const TermRec *d_terms, int nterms, int ndiag,

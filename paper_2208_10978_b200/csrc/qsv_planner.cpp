@@ -252,6 +252,8 @@ int param_count(int kind)
     }
 }
 
+void block_pass(ProgramTemplate &t, PassPlan &pp);
+
 void emit_program(int n, int m, int c, const std::vector<Item> &items, const std::vector<Rot> &R,
                   const int32_t *kinds, const int32_t *qubits, const Schedule &S,
                   ProgramTemplate &t)
@@ -344,9 +346,171 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
             t.ops.push_back(op);
         }
         pp.op_end = (int)t.ops.size();
+        if (g.m >= 4) block_pass(t, pp);
         t.passes.push_back(pp);
     }
     t.n_items = (int64_t)items.size();
+}
+
+inline uint16_t swz16(uint32_t l) { return (uint16_t)(l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u)); }
+
+// Group a pass's tile-local ops into register blocks of <= 4 logical tile
+// bits, fold the permutation gates (CNOT / SWAP / X) into the pass's
+// GF(2)-affine SMEM map, and rewrite ops to the block encoding (see BlockRec).
+void block_pass(ProgramTemplate &t, PassPlan &pp)
+{
+    const int m = pp.geom.m;
+    std::vector<OpRec> src(t.ops.begin() + pp.op_begin, t.ops.begin() + pp.op_end);
+    std::vector<OpRec> out;
+    pp.block_begin = (int)t.blocks.size();
+    uint32_t A[12];   // map columns (unswizzled slot vectors) of the logical tile bits
+    uint32_t tr = 0;  // map translation
+    for (int b = 0; b < 12; ++b) A[b] = 1u << b;
+    auto is_perm = [](int type) { return type == OP_CX || type == OP_SWAP || type == OP_X; };
+    auto rot_signs = [&](const OpRec &op) {
+        uint32_t u = 0;
+        for (int r = op.r0; r < op.r1; ++r) u |= t.rots[r].s_loc;
+        return u;
+    };
+    auto supp = [&](const OpRec &op) -> uint32_t {
+        switch (op.type) {
+            case OP_U1: case OP_X: case OP_DIAG1: return 1u << op.a;
+            case OP_U2: case OP_CX: case OP_SWAP: return (1u << op.a) | (1u << op.b);
+            case OP_ROTG: return op.f | rot_signs(op);
+            case OP_ROTD: return rot_signs(op);
+            default: return 0u;
+        }
+    };
+    auto req = [](const OpRec &op) -> uint32_t {
+        switch (op.type) {
+            case OP_U1: return 1u << op.a;
+            case OP_U2: return (1u << op.a) | (1u << op.b);
+            case OP_ROTG: return op.f;
+            default: return 0u;  // diagonal ops fit any block
+        }
+    };
+    auto apply_perm = [&](const OpRec &op) {
+        // psi'(L) = psi(P L) with P an involution, data unmoved: map' = map o P
+        if (op.type == OP_CX) A[op.a] ^= A[op.b];
+        else if (op.type == OP_SWAP) std::swap(A[op.a], A[op.b]);
+        else tr ^= A[op.a];
+    };
+    std::vector<OpRec> pending, perms;
+    uint32_t cur = 0, D = 0;
+    uint32_t Ab[12], tb = 0;  // map at block start
+    auto start_block = [&]() {
+        std::copy(A, A + 12, Ab);
+        tb = tr;
+    };
+    auto flush = [&]() {
+        if (!pending.empty()) {
+            uint32_t bits = cur;
+            for (int b = m - 1; b >= 0 && __builtin_popcount(bits) < 4; --b) bits |= 1u << b;
+            int pos[4], nb[12], k = 0, kn = 0;
+            for (int b = 0; b < m; ++b) {
+                if ((bits >> b) & 1u) pos[k++] = b;
+                else nb[kn++] = b;
+            }
+            auto local = [&](int b) {
+                for (int j = 0; j < 4; ++j)
+                    if (pos[j] == b) return j;
+                return -1;
+            };
+            auto thread_index = [&](int b) {
+                for (int i = 0; i < kn; ++i)
+                    if (nb[i] == b) return i;
+                return -1;
+            };
+            auto comp_b = [&](uint32_t mask) {
+                uint32_t o = 0;
+                for (int j = 0; j < 4; ++j)
+                    if ((mask >> pos[j]) & 1u) o |= 1u << j;
+                return o;
+            };
+            auto comp_t = [&](uint32_t mask) {
+                uint32_t o = 0;
+                for (int i = 0; i < kn; ++i)
+                    if ((mask >> nb[i]) & 1u) o |= 1u << i;
+                return o;
+            };
+            BlockRec br{};
+            br.kind = 0;
+            for (int i = 0; i < kn && i < 8; ++i) br.cols[i] = swz16(Ab[nb[i]]);
+            for (int j = 0; j < 4; ++j) br.cols[8 + j] = swz16(Ab[pos[j]]);
+            br.tswz = swz16(tb);
+            br.op0 = (int)out.size();
+            for (OpRec op : pending) {
+                switch (op.type) {
+                    case OP_U1: op.a = local(op.a); break;
+                    case OP_U2: op.a = local(op.a); op.b = local(op.b); break;
+                    case OP_DIAG1: {
+                        const int j = local(op.a);
+                        op.b = j >= 0 ? 0 : thread_index(op.a);
+                        op.a = j;
+                        break;
+                    }
+                    case OP_ROTG: op.f = comp_b(op.f); break;
+                    default: break;
+                }
+                if (op.type == OP_ROTG || op.type == OP_ROTD)
+                    for (int r = op.r0; r < op.r1; ++r)
+                        t.rots[r].q = (t.rots[r].q & 0xff) | (int32_t)(comp_b(t.rots[r].s_loc) << 8) |
+                                      (int32_t)(comp_t(t.rots[r].s_loc) << 12);
+                out.push_back(op);
+            }
+            br.op1 = (int)out.size();
+            t.blocks.push_back(br);
+        }
+        for (const OpRec &op : perms) apply_perm(op);
+        pending.clear();
+        perms.clear();
+        cur = 0;
+        D = 0;
+    };
+    for (const OpRec &op : src) {
+        if (is_perm(op.type)) {
+            if (pending.empty()) {
+                apply_perm(op);  // free: only the map changes
+            } else {
+                perms.push_back(op);
+                D |= supp(op);
+            }
+            continue;
+        }
+        const uint32_t s = supp(op), r = req(op);
+        if (s & D) flush();
+        if (op.type == OP_ROTG && __builtin_popcount(op.f) > 4) {
+            flush();
+            BlockRec br{};
+            br.kind = 1;
+            for (int b = 0; b < 12; ++b) br.cols[b] = swz16(A[b]);
+            br.tswz = swz16(tr);
+            br.op0 = (int)out.size();
+            out.push_back(op);
+            br.op1 = (int)out.size();
+            t.blocks.push_back(br);
+            continue;
+        }
+        if (!pending.empty() && __builtin_popcount(cur | r) > 4) flush();
+        if (pending.empty()) start_block();
+        cur |= r;
+        pending.push_back(op);
+    }
+    flush();
+    pp.block_end = (int)t.blocks.size();
+    for (int b = pp.block_begin; b < pp.block_end; ++b) {
+        t.blocks[b].op0 += pp.op_begin;
+        t.blocks[b].op1 += pp.op_begin;
+    }
+    std::copy(out.begin(), out.end(), t.ops.begin() + pp.op_begin);
+    pp.op_end = pp.op_begin + (int)out.size();
+    pp.map_permuted = tr != 0;
+    for (int b = 0; b < 12; ++b) {
+        pp.store_cols[b] = swz16(A[b]);
+        if (b < m && A[b] != (1u << b)) pp.map_permuted = true;
+    }
+    pp.store_t = swz16(tr);
+    t.n_blocks += pp.block_end - pp.block_begin;
 }
 
 }  // namespace
@@ -409,7 +573,8 @@ TileDims dims_of(const TileGeom &g)
     return d;
 }
 
-void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<int32_t> &comp32)
+void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<int32_t> &comp32,
+                 const PassPlan *pp)
 {
     const int nhi = 1 << (g.m - g.c);
     offhi.assign(nhi, 0);
@@ -419,8 +584,13 @@ void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<in
             if ((i >> b) & 1) off |= 1ull << g.pos[g.c + b];
         offhi[i] = off;
     }
-    comp32.assign(32, 0);
+    comp32.assign(64, 0);
     for (int i = 0; i < g.ncomp && i < 32; ++i) comp32[i] = g.comp[i];
+    for (int b = 0; b < 12; ++b) {
+        const uint32_t l = 1u << b;
+        comp32[32 + b] = pp ? pp->store_cols[b] : (int32_t)(l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u));
+    }
+    comp32[44] = pp ? pp->store_t : 0;
 }
 
 uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits)

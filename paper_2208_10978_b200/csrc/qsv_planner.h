@@ -36,6 +36,10 @@ struct PassPlan {
     int op_begin = 0, op_end = 0;
     bool global = false;  // fallback: single rotation group applied pairwise over HBM
     uint64_t flip = 0;
+    int block_begin = 0, block_end = 0;  // register blocks (m >= 4)
+    uint16_t store_cols[12] = {0};       // final SMEM map of the pass (swizzled)
+    uint16_t store_t = 0;
+    bool map_permuted = false;           // final map differs from the identity
 };
 
 struct ParamFill {
@@ -48,12 +52,13 @@ struct ProgramTemplate {
     int n = 0, m = 0, c = 0;
     std::vector<PassPlan> passes;
     std::vector<OpRec> ops;
+    std::vector<BlockRec> blocks;
     std::vector<RotRec> rots;      // c/s refreshed per call
     std::vector<int> rot_src;      // theta source index per RotRec
     std::vector<ParamFill> fills;  // matrices refreshed per call
     size_t n_params = 0;
     // global-fallback rotation records (full 64-bit masks), per pass: rots[r0..r1)
-    int64_t n_input = 0, n_rotations = 0, n_items = 0, n_fallback = 0;
+    int64_t n_input = 0, n_rotations = 0, n_items = 0, n_fallback = 0, n_blocks = 0;
 };
 
 struct Rot {
@@ -88,7 +93,10 @@ void plan_expectation(int n, int64_t n_terms, const uint64_t *x, const uint64_t 
 
 // Device-side geometry tables of a tile (see TileDims).
 TileDims dims_of(const TileGeom &g);
-void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<int32_t> &comp32);
+// comp table: [0..31] tile-index bit positions, [32..43] final map columns,
+// [44] final map translation (identity unless a PassPlan is given).
+void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<int32_t> &comp64,
+                 const PassPlan *pp = nullptr);
 
 uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits);
 

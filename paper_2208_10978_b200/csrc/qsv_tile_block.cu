@@ -1,0 +1,437 @@
+// qsv_tile_block.cu -- K1/K2 v2: register-blocked tile pass (sm_100a).
+//
+// One launch = one HBM pass: every CTA streams 2^m-amplitude tiles (m <= 12,
+// 64 KiB) of the state through shared memory and applies a planner-built
+// program of *blocks*.  A block names <= 4 tile bits B; each thread gathers
+// the 16 amplitudes of one coset of B from SMEM into registers, applies all
+// of the block's ops there (dense 1q/2q gates, diagonal phases, same-flip
+// Pauli-rotation groups), and scatters them back: one SMEM round trip and
+// one barrier per block instead of per gate.  Permutation gates (CNOT, SWAP,
+// X) never touch data: the planner folds them into a GF(2)-affine map from
+// logical tile index to SMEM slot, and every gather / scatter / store goes
+// through that map.  SMEM slots are XOR-swizzled (granule ^= fold3(slot)) so
+// the strided coset gathers stay close to conflict-free.
+//
+// Reference semantics: the per-gate loops of _cykernels.pyx:19-73 driven by
+// statevector.py:65-74; Pauli rotations exp(-i t/2 P) with P as in
+// _cykernels.pyx:76-102.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "qsv_internal.h"
+
+namespace qsv {
+
+namespace {
+
+constexpr int kT = 256;     // threads per CTA
+constexpr int kRB = 4;      // register bits per block
+constexpr int kR = 1 << kRB;
+
+__device__ __forceinline__ uint32_t ins0(uint32_t i, int b)
+{
+    return ((i >> b) << (b + 1)) | (i & ((1u << b) - 1u));
+}
+
+// GF(2)-linear swizzle: XOR the 16 B granule index (low 3 bits) with the
+// fold of all higher 3-bit chunks.  Bijective on [0, 4096).
+__device__ __forceinline__ uint32_t swz(uint32_t l)
+{
+    return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
+}
+
+__device__ __forceinline__ double2 cfma2(double2 m0, double2 x, double2 m1, double2 y)
+{
+    double re = fma(m0.x, x.x, fma(-m0.y, x.y, fma(m1.x, y.x, -m1.y * y.y)));
+    double im = fma(m0.x, x.y, fma(m0.y, x.x, fma(m1.x, y.y, m1.y * y.x)));
+    return make_double2(re, im);
+}
+
+__device__ __forceinline__ double2 ld2(const double *p) { return make_double2(__ldg(p), __ldg(p + 1)); }
+
+// volatile (non-hoistable) variant: re-read from L1 instead of pinning a whole
+// 4x4 complex matrix in registers
+__device__ __forceinline__ double2 ld2v(const double *p)
+{
+    double2 v;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint64_t tbase(uint64_t tile, int lane, int ncomp, int comp_lane)
+{
+    uint64_t bit = (lane < ncomp && ((tile >> lane) & 1ull)) ? (1ull << comp_lane) : 0ull;
+    uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)bit);
+    uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(bit >> 32));
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// ---- register ops on a[16] (block-local bit indices are template args) ----
+
+template <int J>
+__device__ __forceinline__ void r_u1(double2 (&a)[kR], const double *P)
+{
+    const double2 m00 = ld2(P), m01 = ld2(P + 2), m10 = ld2(P + 4), m11 = ld2(P + 6);
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        if (r & (1 << J)) continue;
+        const double2 x = a[r], y = a[r | (1 << J)];
+        a[r] = cfma2(m00, x, m01, y);
+        a[r | (1 << J)] = cfma2(m10, x, m11, y);
+    }
+}
+
+template <int JA, int JB>
+__device__ __forceinline__ void r_u2(double2 (&a)[kR], const double *P)
+{
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        if (r & ((1 << JA) | (1 << JB))) continue;
+        const int i00 = r, i01 = r | (1 << JB), i10 = r | (1 << JA), i11 = r | (1 << JA) | (1 << JB);
+        const double2 x0 = a[i00], x1 = a[i01], x2 = a[i10], x3 = a[i11];
+        double2 o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double *R = P + 8 * k;
+            const double2 p = cfma2(ld2v(R), x0, ld2v(R + 2), x1);
+            const double2 q = cfma2(ld2v(R + 4), x2, ld2v(R + 6), x3);
+            o[k] = make_double2(p.x + q.x, p.y + q.y);
+        }
+        a[i00] = o[0];
+        a[i01] = o[1];
+        a[i10] = o[2];
+        a[i11] = o[3];
+    }
+}
+
+__device__ __forceinline__ double2 cmulc(double2 d, double2 x)
+{
+    return make_double2(fma(d.x, x.x, -d.y * x.y), fma(d.x, x.y, d.y * x.x));
+}
+
+template <int J>
+__device__ __forceinline__ void r_diag_in(double2 (&a)[kR], double2 d0, double2 d1)
+{
+#pragma unroll
+    for (int r = 0; r < kR; ++r) a[r] = cmulc((r & (1 << J)) ? d1 : d0, a[r]);
+}
+
+// a0' = c a0 + k1 a1 where k1 = +-(i^q s) ; q odd -> imaginary
+__device__ __forceinline__ double2 rot_mix(double c, double2 a0, double k, bool imag, double2 a1)
+{
+    if (imag) return make_double2(fma(c, a0.x, -k * a1.y), fma(c, a0.y, k * a1.x));
+    return make_double2(fma(c, a0.x, k * a1.x), fma(c, a0.y, k * a1.y));
+}
+
+// Same-flip rotation group on the block-local flip F.  The sign of amplitude
+// r is tpar ^ parity(r & sB) ^ thread parity (bits outside the block).
+template <int F>
+__device__ __forceinline__ void r_rotg(double2 (&a)[kR], const RotRec *rots, int r0, int r1,
+                                       uint64_t base, uint32_t tid)
+{
+    constexpr int H = 31 - __builtin_clz(F);
+#pragma unroll 1
+    for (int k = r0; k < r1; ++k) {
+        const uint64_t s_hi = __ldg(&rots[k].s_hi);
+        const int q = __ldg(&rots[k].q);
+        const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
+        const uint32_t sB = (q >> 8) & 15u;
+        const uint32_t par = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
+        const uint32_t yodd = (q >> 2) & 1u;
+        const bool imag = q & 1;
+        const double kk = (q & 2) ? -s : s;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            if (r & (1 << H)) continue;
+            const int r1i = r ^ F;
+            const uint32_t s1 = par ^ (__popc((uint32_t)r1i & sB) & 1u);
+            const uint32_t s0 = s1 ^ yodd;
+            const double k1 = s1 ? -kk : kk, k0 = s0 ? -kk : kk;
+            const double2 x = a[r], y = a[r1i];
+            a[r] = rot_mix(c, x, k1, imag, y);
+            a[r1i] = rot_mix(c, y, k0, imag, x);
+        }
+    }
+}
+
+__device__ __forceinline__ void r_rotd(double2 (&a)[kR], const RotRec *rots, int r0, int r1,
+                                       uint64_t base, uint32_t tid)
+{
+#pragma unroll 1
+    for (int k = r0; k < r1; ++k) {
+        const uint64_t s_hi = __ldg(&rots[k].s_hi);
+        const int q = __ldg(&rots[k].q);
+        const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
+        const uint32_t sB = (q >> 8) & 15u;
+        const uint32_t par = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
+        // diagonal: a *= c + kappa sg, kappa = -i s (q = 3)
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            const uint32_t sg = par ^ (__popc((uint32_t)r & sB) & 1u);
+            const double ks = sg ? s : -s;  // imaginary part of (c - i s sg)
+            const double2 x = a[r];
+            a[r] = make_double2(fma(c, x.x, -ks * x.y), fma(c, x.y, ks * x.x));
+        }
+    }
+}
+
+__device__ __forceinline__ void dispatch_rotg(int F, double2 (&a)[kR], const RotRec *rots, int r0,
+                                              int r1, uint64_t base, uint32_t tid)
+{
+    switch (F) {
+#define QSV_ROTG_CASE(f) case f: r_rotg<f>(a, rots, r0, r1, base, tid); break;
+        QSV_ROTG_CASE(1) QSV_ROTG_CASE(2) QSV_ROTG_CASE(3) QSV_ROTG_CASE(4) QSV_ROTG_CASE(5)
+        QSV_ROTG_CASE(6) QSV_ROTG_CASE(7) QSV_ROTG_CASE(8) QSV_ROTG_CASE(9) QSV_ROTG_CASE(10)
+        QSV_ROTG_CASE(11) QSV_ROTG_CASE(12) QSV_ROTG_CASE(13) QSV_ROTG_CASE(14) QSV_ROTG_CASE(15)
+#undef QSV_ROTG_CASE
+        default: break;
+    }
+}
+
+__device__ __forceinline__ void dispatch_u1(int j, double2 (&a)[kR], const double *P)
+{
+    switch (j) {
+        case 0: r_u1<0>(a, P); break;
+        case 1: r_u1<1>(a, P); break;
+        case 2: r_u1<2>(a, P); break;
+        default: r_u1<3>(a, P); break;
+    }
+}
+
+template <template <int, int> class OPW>
+__device__ __forceinline__ void dispatch_pair(int ja, int jb, double2 (&a)[kR], const double *P)
+{
+    switch (ja * 4 + jb) {
+        case 1: OPW<0, 1>::run(a, P); break;
+        case 2: OPW<0, 2>::run(a, P); break;
+        case 3: OPW<0, 3>::run(a, P); break;
+        case 4: OPW<1, 0>::run(a, P); break;
+        case 6: OPW<1, 2>::run(a, P); break;
+        case 7: OPW<1, 3>::run(a, P); break;
+        case 8: OPW<2, 0>::run(a, P); break;
+        case 9: OPW<2, 1>::run(a, P); break;
+        case 11: OPW<2, 3>::run(a, P); break;
+        case 12: OPW<3, 0>::run(a, P); break;
+        case 13: OPW<3, 1>::run(a, P); break;
+        case 14: OPW<3, 2>::run(a, P); break;
+        default: break;
+    }
+}
+
+template <int A, int B> struct W_u2 { __device__ static void run(double2 (&a)[kR], const double *P) { r_u2<A, B>(a, P); } };
+
+// Slot of logical tile index l under the block's affine map (kind-1 blocks).
+__device__ __forceinline__ uint32_t map_slot(uint32_t l, int m, uint32_t tswz, const uint16_t *cols)
+{
+    uint32_t o = tswz;
+    for (int b = 0; b < m; ++b)
+        if ((l >> b) & 1u) o ^= cols[b];
+    return o;
+}
+
+// Wide-flip rotation group (flip with more than 4 in-tile bits) straight on SMEM.
+__device__ void smem_rotg(double2 *sm, int m, uint32_t f, int h, const RotRec *rots, int r0,
+                          int r1, uint64_t base, uint32_t tswz, const uint16_t *cols)
+{
+    const int npairs = 1 << (m - 1);
+    for (int i = threadIdx.x; i < npairs; i += kT) {
+        const uint32_t l0 = ins0(i, h), l1 = l0 ^ f;
+        const uint32_t p0 = map_slot(l0, m, tswz, cols), p1 = map_slot(l1, m, tswz, cols);
+        double2 a0 = sm[p0], a1 = sm[p1];
+        for (int k = r0; k < r1; ++k) {
+            const uint64_t s_hi = __ldg(&rots[k].s_hi);
+            const uint32_t s_loc = __ldg(&rots[k].s_loc);
+            const int q = __ldg(&rots[k].q);
+            const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
+            const uint32_t s1 = (__popcll(base & s_hi) + __popc(l1 & s_loc)) & 1u;
+            const uint32_t s0 = s1 ^ ((q >> 2) & 1u);
+            const double kk = (q & 2) ? -s : s;
+            const bool imag = q & 1;
+            const double2 x = a0, y = a1;
+            a0 = rot_mix(c, x, s1 ? -kk : kk, imag, y);
+            a1 = rot_mix(c, y, s0 ? -kk : kk, imag, x);
+        }
+        sm[p0] = a0;
+        sm[p1] = a1;
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc)
+{
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issue the asynchronous (LDGSTS) loads of one tile into a swizzled SMEM buffer.
+__device__ __forceinline__ void issue_tile_load(double2 *buf, const double2 *src, const uint64_t *offhi,
+                                                int tsize, int c, uint32_t cmask)
+{
+#pragma unroll 4
+    for (int l = threadIdx.x; l < tsize; l += kT) cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
+}
+
+// Persistent CTA (one per SM): double-buffered tiles -- while the register
+// blocks run on tile i, the LDGSTS copies of tile i+1 stream into the other
+// buffer, so HBM traffic overlaps the DFMA / SMEM work.  g_geo[0..31] are the
+// tile-index bit positions, g_geo[32..43] the swizzled columns of the pass's
+// final map and g_geo[44] its swizzled translation (used by the store).
+__global__ void __launch_bounds__(kT, 1)
+tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__restrict__ g_offhi,
+                  const int32_t *__restrict__ g_geo, const BlockRec *__restrict__ blocks, int nblocks,
+                  const OpRec *__restrict__ ops, const RotRec *__restrict__ rots,
+                  const double *__restrict__ params)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int m = g.m, c = g.c;
+    const int tsize = 1 << m;
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);  // 2 x tsize
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + 2 * tsize);
+    for (int i = threadIdx.x; i < (1 << (m - c)); i += kT) offhi[i] = __ldg(g_offhi + i);
+    const uint32_t tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int comp_lane = __ldg(g_geo + lane);
+    const uint32_t cmask = (1u << c) - 1u;
+    const int ncos = tsize >> kRB;  // cosets per block (m >= 4)
+    const int tbits = m - kRB;      // thread-index bits of a block
+    // store map: slot of logical l = tid + k*kT
+    uint32_t st_base = (uint32_t)__ldg(g_geo + 44);
+    for (int i = 0; i < 8 && i < m; ++i)
+        if ((tid >> i) & 1u) st_base ^= (uint32_t)__ldg(g_geo + 32 + i);
+    __syncthreads();
+    const uint64_t ntiles = 1ull << g.ncomp;
+    uint64_t tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
+    issue_tile_load(bufs, psi + base, offhi, tsize, c, cmask);
+    cp_async_commit();
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        double2 *sm = bufs + (it & 1) * tsize;
+        const uint64_t next = tile + gridDim.x;
+        if (next < ntiles) {
+            const uint64_t nb = tbase(next, lane, g.ncomp, comp_lane);
+            issue_tile_load(bufs + ((it + 1) & 1) * tsize, psi + nb, offhi, tsize, c, cmask);
+        }
+        cp_async_commit();
+        cp_async_wait<1>();  // this tile's copies have landed (the next tile's may be in flight)
+        __syncthreads();
+        for (int bi = 0; bi < nblocks; ++bi) {
+            const BlockRec *B = blocks + bi;
+            const int kind = __ldg(&B->kind);
+            const int op0 = __ldg(&B->op0), op1 = __ldg(&B->op1);
+            if (kind == 0) {
+                if ((int)tid < ncos) {
+                    uint32_t sb = __ldg(&B->tswz);
+                    for (int i = 0; i < tbits; ++i)
+                        if ((tid >> i) & 1u) sb ^= __ldg(&B->cols[i]);
+                    const uint32_t e0 = __ldg(&B->cols[8]), e1 = __ldg(&B->cols[9]);
+                    const uint32_t e2 = __ldg(&B->cols[10]), e3 = __ldg(&B->cols[11]);
+                    double2 a[kR];
+#pragma unroll
+                    for (int r = 0; r < kR; ++r) {
+                        const uint32_t o = ((r & 1) ? e0 : 0u) ^ ((r & 2) ? e1 : 0u) ^
+                                           ((r & 4) ? e2 : 0u) ^ ((r & 8) ? e3 : 0u);
+                        a[r] = sm[sb ^ o];
+                    }
+#pragma unroll 1
+                    for (int k = op0; k < op1; ++k) {
+                        const int4 w0 = __ldg(reinterpret_cast<const int4 *>(ops + k));
+                        const int4 w1 = __ldg(reinterpret_cast<const int4 *>(ops + k) + 1);
+                        const int type = w0.x, oa = w0.y, ob = w0.z;
+                        switch (type) {
+                            case OP_U1: dispatch_u1(oa, a, params + w1.z); break;
+                            case OP_U2: dispatch_pair<W_u2>(oa, ob, a, params + w1.z); break;
+                            case OP_DIAG1: {
+                                const double *P = params + w1.z;
+                                const double2 d0 = ld2(P), d1 = ld2(P + 2);
+                                if (oa >= 0) {
+                                    switch (oa) {
+                                        case 0: r_diag_in<0>(a, d0, d1); break;
+                                        case 1: r_diag_in<1>(a, d0, d1); break;
+                                        case 2: r_diag_in<2>(a, d0, d1); break;
+                                        default: r_diag_in<3>(a, d0, d1); break;
+                                    }
+                                } else {
+                                    const double2 d = ((tid >> ob) & 1u) ? d1 : d0;
+#pragma unroll
+                                    for (int r = 0; r < kR; ++r) a[r] = cmulc(d, a[r]);
+                                }
+                                break;
+                            }
+                            case OP_ROTG: dispatch_rotg(w1.w, a, rots, w1.x, w1.y, base, tid); break;
+                            case OP_ROTD: r_rotd(a, rots, w1.x, w1.y, base, tid); break;
+                            default: break;
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < kR; ++r) {
+                        const uint32_t o = ((r & 1) ? e0 : 0u) ^ ((r & 2) ? e1 : 0u) ^
+                                           ((r & 4) ? e2 : 0u) ^ ((r & 8) ? e3 : 0u);
+                        sm[sb ^ o] = a[r];
+                    }
+                }
+            } else {
+                uint16_t cols[12];
+#pragma unroll
+                for (int b = 0; b < 12; ++b) cols[b] = __ldg(&B->cols[b]);
+                smem_rotg(sm, m, __ldg(&ops[op0].f), __ldg(&ops[op0].h), rots, __ldg(&ops[op0].r0),
+                          __ldg(&ops[op0].r1), base, __ldg(&B->tswz), cols);
+            }
+            __syncthreads();
+        }
+        // ---- store through the pass's final map (streaming STG) ----
+        double2 *dst = psi + base;
+        if (tsize >= kT) {
+#pragma unroll 4
+            for (int k = 0; k < (tsize >> 8); ++k) {
+                uint32_t sk = 0;
+                for (int j = 0; j < 4; ++j)
+                    if ((k >> j) & 1) sk ^= (uint32_t)__ldg(g_geo + 40 + j);
+                const uint32_t l = tid + k * kT;
+                __stcs(dst + (l & cmask) + offhi[l >> c], sm[st_base ^ sk]);
+            }
+        } else if ((int)tid < tsize) {
+            __stcs(dst + (tid & cmask) + offhi[tid >> c], sm[st_base]);
+        }
+        __syncthreads();
+        if (next < ntiles) base = tbase(next, lane, g.ncomp, comp_lane);
+    }
+    cp_async_wait<0>();
+}
+
+}  // namespace
+
+cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
+                               const int32_t *d_geo, const BlockRec *d_blocks, int nblocks,
+                               const OpRec *d_ops, const RotRec *d_rots, const double *d_params,
+                               cudaStream_t st)
+{
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(tile_block_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(((size_t)32 << kMaxTileBits) + 8192));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t smem = ((size_t)32 << g.m) + ((size_t)8 << (g.m - g.c));
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_block_kernel, kT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t ntiles = 1ull << g.ncomp;
+    uint64_t cap = (uint64_t)num_sms(dev) * per_sm;
+    static const char *env_grid = getenv("QSV_TILE_GRID");  // debug: cap the persistent grid
+    if (env_grid && atoi(env_grid) > 0) cap = (uint64_t)atoi(env_grid);
+    const int grid = (int)(ntiles < cap ? ntiles : cap);
+    tile_block_kernel<<<grid, kT, smem, st>>>(psi, g, d_offhi, d_geo, d_blocks, nblocks, d_ops,
+                                              d_rots, d_params);
+    return cudaGetLastError();
+}
+
+}  // namespace qsv

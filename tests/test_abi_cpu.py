@@ -10,6 +10,8 @@ import numpy as np
 import pytest
 
 from conftest import REPO
+import sys
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from paper_2208_10978_b200 import _lib
 from paper_2208_10978_b200 import workloads as W
 from paper_2208_10978_b200.circuit import Circuit, Constant, Gate, evolution_gates, flatten_bound
@@ -103,3 +105,45 @@ def test_no_gpu_compute_fails_loudly():
     h = ctypes.c_void_p()
     with pytest.raises(_lib.QsvCudaError):
         _lib.check(_lib.lib().qsv_create(ctypes.byref(h), 4, 0))
+
+
+# ---- planner + encoding checked on CPU through the kernel emulator ----
+
+def _emulate(circ, psi0):
+    import emulator
+    k, q, v = flatten_bound(circ)
+    prog = _lib.debug_plan(circ.n_qubits, k, q, v)
+    return emulator.run_program(prog, psi0), prog
+
+
+@pytest.mark.parametrize("n,layers", [(9, 5), (14, 4), (20, 6)])
+def test_emulated_brickwork_matches_oracle(n, layers):
+    from oracle import oracle as O
+    circ = W.brickwork(n, layers, seed=5)
+    psi0 = O.init_state("0" * n)
+    out, prog = _emulate(circ, psi0)
+    assert np.abs(out - O.evolve(psi0, circ.gates)).max() <= 1e-12
+
+
+@pytest.mark.parametrize("n", [6, 13, 16])
+def test_emulated_mixed_and_rotations_match_oracle(n):
+    from oracle import oracle as O
+    rng = np.random.default_rng(n)
+    kinds = ["H", "HY", "X", "CNOT", "SWAP", "RZ", "RY", "U3", "CU3"]
+    gates = []
+    for _ in range(150):
+        kd = kinds[rng.integers(len(kinds))]
+        nq = 2 if kd in ("CNOT", "SWAP", "CU3") else 1
+        qs = tuple(int(x) for x in rng.choice(n, size=nq, replace=False))
+        npar = {"RZ": 1, "RY": 1, "U3": 3, "CU3": 3}.get(kd, 0)
+        gates.append(Gate(kd, qs, tuple(Constant(float(x)) for x in rng.uniform(-3, 3, size=npar))))
+        if rng.random() < 0.3:
+            w = int(rng.integers(1, min(n, 7) + 1))
+            pos = rng.choice(n, size=w, replace=False)
+            s = PauliString(tuple(zip((int(p) for p in pos), rng.choice(list("XYZ"), size=w))))
+            gates.extend(evolution_gates(s, Constant(float(rng.uniform(-1, 1)))))
+    circ = Circuit(n, tuple(gates), 0)
+    a = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi0 = a / np.linalg.norm(a)
+    out, _ = _emulate(circ, psi0)
+    assert np.abs(out - O.evolve(psi0, circ.gates)).max() <= 1e-12

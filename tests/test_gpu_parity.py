@@ -253,4 +253,4 @@ def test_backend_protocol_and_errors():
     with pytest.raises(ResourceLimitError):
         sv.init_state("0" * 40)
     psi = be.evolve(s0, circ)
-    assert abs(be.overlap(psi, s0) - np.sqrt(0.5)) <= 1e-15
+    assert abs(be.overlap(psi, s0) + np.sqrt(0.5)) <= 1e-15  # H|1> = (|0> - |1>)/sqrt2 on qubit 0
