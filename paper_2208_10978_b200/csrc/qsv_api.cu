@@ -212,7 +212,7 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                 QSV_CUDA(launch_rot_global(s->amps, s->n, p.flip, d_rots + op.r0, op.r1 - op.r0,
                                            s->stream));
             }
-        } else if (p.geom.m >= 4) {
+        } else if (p.geom.m >= kBlockBits + 1) {
             QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o_off[k]),
                                         (const int32_t *)(d + o_comp[k]),
                                         (const BlockRec *)(d + o_blk) + p.block_begin,
@@ -571,7 +571,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
             o.comp = b.add(comp.data(), comp.size() * sizeof(int32_t));
         }
         o.rows = sp.global ? expect_global_grid(s->n)
-                           : expect_sweep_grid(dims_of(sp.geom), (int)sp.terms.size());
+                           : expect_sweep_grid(dims_of(sp.geom), (int)sp.terms.size(), sp.ndiag);
         max_partial = std::max(max_partial, (size_t)o.rows * sp.terms.size());
         offs.push_back(o);
     }
@@ -798,7 +798,8 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     materialize_gates(t, values);
     std::vector<double> params(t.n_params);
     for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, &params[f.offset]);
-    std::string j = "{\"n\":" + std::to_string(n) + ",\"passes\":[";
+    std::string j = "{\"n\":" + std::to_string(n) + ",\"block_bits\":" +
+                    std::to_string(kBlockBits) + ",\"passes\":[";
     char buf[256];
     for (size_t k = 0; k < t.passes.size(); ++k) {
         const PassPlan &p = t.passes[k];

@@ -21,6 +21,12 @@ constexpr int kMaxTileBits = 12;
 // contiguous segments, so every warp-wide 16 B load is fully coalesced.
 constexpr int kMinContig = 5;
 constexpr int kMaxQubits = 40;
+// Register bits of a tile-kernel block: each thread holds 2^kBlockBits
+// amplitudes (8 -> 512 threads per 4096-amplitude tile, 16 warps per SM).
+#ifndef QSV_BLOCK_BITS
+#define QSV_BLOCK_BITS 3
+#endif
+constexpr int kBlockBits = QSV_BLOCK_BITS;
 
 // ---- fused tile-pass program -------------------------------------------
 enum OpType : int32_t {
@@ -52,10 +58,10 @@ struct RotRec {     // 32 B
 // GF(2)-affine map slot(L) = swz(A L ^ t) of the logical tile index L, so
 // permutation gates (CNOT, SWAP, X) cost nothing on the device: the planner
 // folds them into (A, t).  cols[] hold swizzled map columns:
-//   kind 0 (register block, <= 4 logical bits B): cols[0..7] = columns of the
-//          non-B bits in ascending order (= thread-index bits), cols[8..11] =
-//          columns of B (block-local bits 0..3); ops[op0..op1) use
-//          block-local bit indices.
+//   kind 0 (register block, <= kBlockBits logical bits B): cols[0..11-kBlockBits]
+//          = columns of the non-B bits in ascending order (= thread-index
+//          bits), cols[12-kBlockBits..11] = columns of B (block-local bits);
+//          ops[op0..op1) use block-local bit indices.
 //   kind 1 (wide-flip rotation group on SMEM): cols[b] = column of tile bit b.
 struct BlockRec {  // 48 B
     int32_t kind;
@@ -82,10 +88,11 @@ struct TileDims {
 };
 
 // ---- expectation sweep --------------------------------------------------
-struct GroupRec {   // a flip group evaluated by one warp
+struct GroupRec {   // a flip group of an expectation sweep (32 B)
     uint32_t f_loc;
     int32_t h;
-    int32_t t0, t1;  // term range (sweep-local indices)
+    int32_t t0, t_im, t1;  // terms [t0, t_im) use Re w, [t_im, t1) use Im w
+    int32_t pad[3];
 };
 
 struct TermRec {    // 24 B
@@ -129,9 +136,9 @@ cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *
                                const OpRec *d_ops, const RotRec *d_rots, const double *d_params,
                                cudaStream_t st);
 cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
-                                const int32_t *d_comp, const GroupRec *d_groups,
-                                int ngroups, const TermRec *d_terms, int nterms, int ndiag,
-                                double *d_partial, int *grid_out, cudaStream_t st);
+                                const int32_t *d_comp, const GroupRec *d_groups, int ngroups,
+                                const TermRec *d_terms, int nterms, int ndiag, double *d_partial,
+                                int *grid_out, cudaStream_t st);
 cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
                                   double *out, cudaStream_t st);
 cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStream_t st);
@@ -146,7 +153,7 @@ cudaError_t launch_expect_global(const double2 *psi, int n, const GroupRec *d_gr
                                  const uint64_t *d_gflip, int ngroups, const TermRec *d_terms,
                                  int nterms, double *d_partial, int *grid_out, cudaStream_t st);
 int expect_global_grid(int n);
-int expect_sweep_grid(const TileDims &g, int nterms);
+int expect_sweep_grid(const TileDims &g, int nterms, int ndiag);
 cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,
                          double bre, double bim, cudaStream_t st);
 

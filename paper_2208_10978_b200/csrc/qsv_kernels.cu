@@ -10,10 +10,8 @@
 //                             Replaces the per-gate loops of
 //                             _cykernels.pyx:19-73 (apply_1q/apply_2q) driven by
 //                             statevector.py:65-74 (evolve).
-//  K3     expect_sweep_kernel one read-only pass evaluating a batch of Pauli
-//                             strings <psi|P|psi> (flip groups per warp, the
-//                             Z-only group through an in-SMEM Walsh-Hadamard
-//                             transform).  Replaces statevector.py:98-110.
+//  K3     see qsv_expect.cu (batched expectation sweep); here only the
+//                             global fallback for flips wider than a tile.
 //  K4     apply_pauli_kernel  out (+)= c * P psi  (_cykernels.pyx:76-102,
 //                             statevector.py:91-95, 113-121).
 //  K5     dot kernels         vdot / norm with a deterministic two-stage
@@ -372,123 +370,11 @@ __global__ void __launch_bounds__(T, 2) tile_pass_kernel(double2 *__restrict__ p
     }
 }
 
-// ---- expectation sweep ----------------------------------------------------
-
 __device__ __forceinline__ double warp_sum(double v)
 {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
-}
-
-template <int T>
-__global__ void __launch_bounds__(T, 2) expect_sweep_kernel(const double2 *__restrict__ psi,
-                                                         const TileDims g,
-                                                         const uint64_t *__restrict__ g_offhi,
-                                                         const int32_t *__restrict__ g_comp,
-                                                         const GroupRec *__restrict__ groups,
-                                                         int ngroups,
-                                                         const TermRec *__restrict__ terms,
-                                                         int nterms, int ndiag,
-                                                         double *__restrict__ partial)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *sm = reinterpret_cast<double2 *>(smem_raw);
-    const int m = g.m, c = g.c;
-    const int tsize = 1 << m;
-    uint64_t *offhi = reinterpret_cast<uint64_t *>(sm + tsize);
-    double *acc = reinterpret_cast<double *>(offhi + (1 << (m - c)));
-    load_geom(offhi, g_offhi, 1 << (m - c));
-    for (int t = threadIdx.x; t < nterms; t += T) acc[t] = 0.0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int comp_lane = __ldg(g_comp + lane);
-    __syncthreads();
-    const uint64_t ntiles = 1ull << g.ncomp;
-    const int npairs = tsize >> 1;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t base = tile_base(tile, lane, g.ncomp, comp_lane);
-        load_tile<T>(sm, offhi, psi, base, m, c);
-        __syncthreads();
-        // flip groups: one warp per group, terms in chunks held in registers
-        for (int gi = warp; gi < ngroups; gi += T / 32) {
-            const uint32_t f = __ldg(&groups[gi].f_loc);
-            const int h = __ldg(&groups[gi].h);
-            const int t0g = __ldg(&groups[gi].t0), t1g = __ldg(&groups[gi].t1);
-            for (int t0 = t0g; t0 < t1g; t0 += kTermChunk) {
-                const int nt = min(kTermChunk, t1g - t0);
-                uint32_t sl[kTermChunk];
-                int ui[kTermChunk];
-                double a8[kTermChunk];
-#pragma unroll
-                for (int k = 0; k < kTermChunk; ++k) {
-                    sl[k] = k < nt ? __ldg(&terms[t0 + k].s_loc) : 0u;
-                    ui[k] = k < nt ? __ldg(&terms[t0 + k].use_im) : 0;
-                    a8[k] = 0.0;
-                }
-                for (int i = lane; i < npairs; i += 32) {
-                    const uint32_t l0 = insert0(i, h), l1 = l0 ^ f;
-                    const double2 x = sm[l0], y = sm[l1];
-                    const double re = fma(x.x, y.x, x.y * y.y);
-                    const double im = fma(x.x, y.y, -x.y * y.x);
-#pragma unroll
-                    for (int k = 0; k < kTermChunk; ++k) {
-                        if (k < nt) {
-                            const double v = ui[k] ? im : re;
-                            a8[k] += (__popc(l0 & sl[k]) & 1u) ? -v : v;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < kTermChunk; ++k) {
-                    if (k < nt) {
-                        const double sum = warp_sum(a8[k]);
-                        if (lane == 0) {
-                            const uint32_t tp = __popcll(base & __ldg(&terms[t0 + k].s_hi)) & 1u;
-                            const double sc = __ldg(&terms[t0 + k].scale);
-                            acc[t0 + k] += tp ? -sc * sum : sc * sum;
-                        }
-                    }
-                }
-            }
-        }
-        if (ndiag > 0) {
-            // Z-only strings: <Z_s> over the tile = WHT(|psi|^2)[s_loc] * tile parity.
-            double p[kMaxPer];
-#pragma unroll
-            for (int k = 0; k < kMaxPer; ++k) {
-                const int l = threadIdx.x + k * T;
-                if (l < tsize) {
-                    const double2 a = sm[l];
-                    p[k] = fma(a.x, a.x, a.y * a.y);
-                }
-            }
-            __syncthreads();
-            double *pw = reinterpret_cast<double *>(sm);
-#pragma unroll
-            for (int k = 0; k < kMaxPer; ++k) {
-                const int l = threadIdx.x + k * T;
-                if (l < tsize) pw[l] = p[k];
-            }
-            __syncthreads();
-            for (int b = 0; b < m; ++b) {
-                for (int i = threadIdx.x; i < npairs; i += T) {
-                    const uint32_t l0 = insert0(i, b), l1 = l0 | (1u << b);
-                    const double u = pw[l0], v = pw[l1];
-                    pw[l0] = u + v;
-                    pw[l1] = u - v;
-                }
-                __syncthreads();
-            }
-            for (int t = threadIdx.x; t < ndiag; t += T) {
-                const double v = pw[__ldg(&terms[t].s_loc)];
-                const uint32_t tp = __popcll(base & __ldg(&terms[t].s_hi)) & 1u;
-                const double sc = __ldg(&terms[t].scale);
-                acc[t] += tp ? -sc * v : sc * v;
-            }
-        }
-        __syncthreads();
-    }
-    for (int t = threadIdx.x; t < nterms; t += T) partial[(size_t)blockIdx.x * nterms + t] = acc[t];
 }
 
 __global__ void reduce_columns_kernel(const double *__restrict__ partial, int rows, int cols,
@@ -741,36 +627,6 @@ cudaError_t launch_tile_pass(double2 *psi, const TileDims &g, const uint64_t *d_
     return cudaGetLastError();
 }
 
-cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
-                                const int32_t *d_comp, const GroupRec *d_groups,
-                                int ngroups, const TermRec *d_terms, int nterms, int ndiag,
-                                double *d_partial, int *grid_out, cudaStream_t st)
-{
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(expect_sweep_kernel<kTileThreads>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const size_t smem = tile_smem_bytes(g) + (size_t)8 * nterms;
-    int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, expect_sweep_kernel<kTileThreads>, kTileThreads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t ntiles = 1ull << g.ncomp;
-    const uint64_t cap = (uint64_t)num_sms(dev) * per_sm;
-    const int grid = (int)(ntiles < cap ? ntiles : cap);
-    *grid_out = grid;
-    expect_sweep_kernel<kTileThreads><<<grid, kTileThreads, smem, st>>>(
-        psi, g, d_offhi, d_comp, d_groups, ngroups, d_terms, nterms, ndiag, d_partial);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
                                   double *out, cudaStream_t st)
 {
@@ -861,21 +717,6 @@ cudaError_t launch_expect_global(const double2 *psi, int n, const GroupRec *d_gr
     expect_global_kernel<256><<<grid, 256, 0, st>>>(psi, n, d_groups, d_gflip, ngroups, d_terms,
                                                     nterms, d_partial);
     return cudaGetLastError();
-}
-
-int expect_sweep_grid(const TileDims &g, int nterms)
-{
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const size_t smem = tile_smem_bytes(g) + (size_t)8 * nterms;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expect_sweep_kernel<kTileThreads>,
-                                                      kTileThreads, smem) != cudaSuccess)
-        per_sm = 1;
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t ntiles = 1ull << g.ncomp;
-    const uint64_t cap = (uint64_t)num_sms(dev) * per_sm;
-    return (int)(ntiles < cap ? ntiles : cap);
 }
 
 }  // namespace qsv

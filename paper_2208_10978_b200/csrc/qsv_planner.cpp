@@ -346,7 +346,7 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
             t.ops.push_back(op);
         }
         pp.op_end = (int)t.ops.size();
-        if (g.m >= 4) block_pass(t, pp);
+        if (g.m >= kBlockBits + 1) block_pass(t, pp);
         t.passes.push_back(pp);
     }
     t.n_items = (int64_t)items.size();
@@ -404,15 +404,16 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
     };
     auto flush = [&]() {
         if (!pending.empty()) {
+            constexpr int RB = kBlockBits, TB = kMaxTileBits - kBlockBits;
             uint32_t bits = cur;
-            for (int b = m - 1; b >= 0 && __builtin_popcount(bits) < 4; --b) bits |= 1u << b;
-            int pos[4], nb[12], k = 0, kn = 0;
+            for (int b = m - 1; b >= 0 && __builtin_popcount(bits) < RB; --b) bits |= 1u << b;
+            int pos[RB], nb[12], k = 0, kn = 0;
             for (int b = 0; b < m; ++b) {
                 if ((bits >> b) & 1u) pos[k++] = b;
                 else nb[kn++] = b;
             }
             auto local = [&](int b) {
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < RB; ++j)
                     if (pos[j] == b) return j;
                 return -1;
             };
@@ -423,7 +424,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
             };
             auto comp_b = [&](uint32_t mask) {
                 uint32_t o = 0;
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < RB; ++j)
                     if ((mask >> pos[j]) & 1u) o |= 1u << j;
                 return o;
             };
@@ -435,8 +436,8 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
             };
             BlockRec br{};
             br.kind = 0;
-            for (int i = 0; i < kn && i < 8; ++i) br.cols[i] = swz16(Ab[nb[i]]);
-            for (int j = 0; j < 4; ++j) br.cols[8 + j] = swz16(Ab[pos[j]]);
+            for (int i = 0; i < kn && i < TB; ++i) br.cols[i] = swz16(Ab[nb[i]]);
+            for (int j = 0; j < RB; ++j) br.cols[TB + j] = swz16(Ab[pos[j]]);
             br.tswz = swz16(tb);
             br.op0 = (int)out.size();
             for (OpRec op : pending) {
@@ -479,7 +480,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
         }
         const uint32_t s = supp(op), r = req(op);
         if (s & D) flush();
-        if (op.type == OP_ROTG && __builtin_popcount(op.f) > 4) {
+        if (op.type == OP_ROTG && __builtin_popcount(op.f) > kBlockBits) {
             flush();
             BlockRec br{};
             br.kind = 1;
@@ -491,7 +492,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
             t.blocks.push_back(br);
             continue;
         }
-        if (!pending.empty() && __builtin_popcount(cur | r) > 4) flush();
+        if (!pending.empty() && __builtin_popcount(cur | r) > kBlockBits) flush();
         if (pending.empty()) start_block();
         cur |= r;
         pending.push_back(op);
@@ -721,29 +722,35 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
             members[it->second].push_back((int32_t)t);
         }
     }
-    // order groups: most high bits first (hardest to place), then by first term
+    // Bin flip groups into sweeps: a sweep's tile must hold every group's
+    // flip bits.  First-fit decreasing on the high-bit need; capacity is
+    // bounded by the shared-memory accumulators (kFlipCap strings).
+    const int kFlipCap = 1024, kDiagCap = 4096, kGroupCap = 256;
     std::vector<int> order(flips.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        return popc64(flips[a] & ~low) > popc64(flips[b] & ~low);
+        const int pa = popc64(flips[a] & ~low), pb = popc64(flips[b] & ~low);
+        if (pa != pb) return pa > pb;
+        return members[a].size() > members[b].size();
     });
     struct Bin {
         uint64_t hi = 0;
         int nterms = 0;
         std::vector<int> groups;
+        std::vector<int32_t> diag;
     };
     std::vector<Bin> bins;
     std::vector<int> global_groups;
     for (int gi : order) {
         const uint64_t need = flips[gi] & ~low;
         const int nt = (int)members[gi].size();
-        if (popc64(need) > free_slots) {
+        if (popc64(need) > free_slots || nt > kFlipCap) {
             global_groups.push_back(gi);
             continue;
         }
         int placed = -1;
         for (size_t b = 0; b < bins.size(); ++b) {
-            if (bins[b].nterms + nt > kCap && bins[b].nterms > 0) continue;
+            if (bins[b].nterms + nt > kFlipCap || (int)bins[b].groups.size() >= kGroupCap) continue;
             if (popc64(bins[b].hi | need) <= free_slots) {
                 placed = (int)b;
                 break;
@@ -757,39 +764,24 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
         bins[placed].nterms += nt;
         bins[placed].groups.push_back(gi);
     }
-    // diagonal terms: spread over sweeps with spare capacity, new sweeps as needed
-    size_t dpos = 0;
-    std::vector<int> bin_ndiag(bins.size(), 0);
-    for (size_t b = 0; b < bins.size() && dpos < diag.size(); ++b) {
-        const int room = kCap - bins[b].nterms;
-        const int take = (int)std::min<size_t>(room > 0 ? room : 0, diag.size() - dpos);
-        bin_ndiag[b] = take;
-        bins[b].nterms += take;
-        dpos += take;
-    }
-    while (dpos < diag.size()) {
-        bins.emplace_back();
-        const int take = (int)std::min<size_t>(kCap, diag.size() - dpos);
-        bin_ndiag.push_back(take);
-        bins.back().nterms = take;
-        dpos += take;
+    // Z-only strings ride along with the first sweeps (any tile works)
+    for (size_t d0 = 0, b = 0; d0 < diag.size(); d0 += kDiagCap, ++b) {
+        if (b >= bins.size()) bins.emplace_back();
+        bins[b].diag.assign(diag.begin() + d0, diag.begin() + std::min(diag.size(), d0 + kDiagCap));
     }
 
-    auto term_scale = [&](int64_t t, bool is_diag) {
-        if (is_diag) return 1.0;
+    auto term_scale = [&](int64_t t) {
         const int ny = popc64(y[t]);
         if ((ny & 1) == 0) return ((ny / 2) & 1) ? -2.0 : 2.0;
         return (((ny + 1) / 2) & 1) ? 2.0 : -2.0;
     };
 
-    dpos = 0;
-    for (size_t b = 0; b < bins.size(); ++b) {
+    for (Bin &bin : bins) {
         SweepPlan sp;
-        sp.geom = make_geom(n, m, c, bins[b].hi);
+        sp.geom = make_geom(n, m, c, bin.hi);
         const uint64_t tm = tile_mask(sp.geom);
-        sp.ndiag = bin_ndiag[b];
-        for (int k = 0; k < sp.ndiag; ++k) {
-            const int64_t t = diag[dpos++];
+        sp.ndiag = (int)bin.diag.size();
+        for (int32_t t : bin.diag) {
             TermRec tr{};
             const uint64_t bb = y[t] | z[t];
             tr.s_hi = bb & ~tm;
@@ -797,22 +789,32 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
             tr.use_im = 0;
             tr.scale = 1.0;
             sp.terms.push_back(tr);
-            sp.map.push_back((int32_t)t);
+            sp.map.push_back(t);
         }
-        for (int gi : bins[b].groups) {
+        // heavier groups first so the two warp halves stay balanced
+        std::stable_sort(bin.groups.begin(), bin.groups.end(),
+                         [&](int a, int b) { return members[a].size() > members[b].size(); });
+        for (int gi : bin.groups) {
             GroupRec gr{};
             gr.f_loc = compress(flips[gi], sp.geom);
             gr.h = highest_bit(gr.f_loc);
+            const uint32_t lowmask_h = (1u << gr.h) - 1u;
             gr.t0 = (int)sp.terms.size();
-            for (int32_t t : members[gi]) {
-                TermRec tr{};
-                const uint64_t bb = y[t] | z[t];
-                tr.s_hi = bb & ~tm;
-                tr.s_loc = compress(bb, sp.geom);
-                tr.use_im = popc64(y[t]) & 1;
-                tr.scale = term_scale(t, false);
-                sp.terms.push_back(tr);
-                sp.map.push_back(t);
+            for (int pass = 0; pass < 2; ++pass) {  // Re-w strings, then Im-w strings
+                if (pass == 1) gr.t_im = (int)sp.terms.size();
+                for (int32_t t : members[gi]) {
+                    if ((popc64(y[t]) & 1) != pass) continue;
+                    TermRec tr{};
+                    const uint64_t bb = y[t] | z[t];
+                    const uint32_t sl = compress(bb, sp.geom);
+                    tr.s_hi = bb & ~tm;
+                    // sign mask in pair-index coordinates (bit h removed)
+                    tr.s_loc = (sl & lowmask_h) | ((sl >> (gr.h + 1)) << gr.h);
+                    tr.use_im = pass;
+                    tr.scale = term_scale(t);
+                    sp.terms.push_back(tr);
+                    sp.map.push_back(t);
+                }
             }
             gr.t1 = (int)sp.terms.size();
             sp.groups.push_back(gr);
@@ -838,7 +840,7 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
                 tr.s_hi = y[t] | z[t];
                 tr.s_loc = 0;
                 tr.use_im = popc64(y[t]) & 1;
-                tr.scale = term_scale(t, false);
+                tr.scale = term_scale(t);
                 sp.terms.push_back(tr);
                 sp.map.push_back(t);
             }
@@ -862,7 +864,7 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
                     TermRec tr{};
                     tr.s_hi = y[t] | z[t];
                     tr.use_im = popc64(y[t]) & 1;
-                    tr.scale = term_scale(t, false);
+                    tr.scale = term_scale(t);
                     s2.terms.push_back(tr);
                     s2.map.push_back(t);
                 }

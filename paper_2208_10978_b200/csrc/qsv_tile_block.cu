@@ -25,9 +25,10 @@ namespace qsv {
 
 namespace {
 
-constexpr int kT = 256;     // threads per CTA
-constexpr int kRB = 4;      // register bits per block
-constexpr int kR = 1 << kRB;
+constexpr int kRB = kBlockBits;              // register bits per block (qsv_internal.h)
+constexpr int kR = 1 << kRB;                  // amplitudes per thread
+constexpr int kT = (1 << kMaxTileBits) / kR;  // threads per CTA: one coset each
+constexpr int kTB = kMaxTileBits - kRB;       // thread-index bits of a full tile
 
 __device__ __forceinline__ uint32_t ins0(uint32_t i, int b)
 {
@@ -136,7 +137,7 @@ __device__ __forceinline__ void r_rotg(double2 (&a)[kR], const RotRec *rots, int
         const uint64_t s_hi = __ldg(&rots[k].s_hi);
         const int q = __ldg(&rots[k].q);
         const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
-        const uint32_t sB = (q >> 8) & 15u;
+        const uint32_t sB = (q >> 8) & (kR - 1u);
         const uint32_t par = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
         const uint32_t yodd = (q >> 2) & 1u;
         const bool imag = q & 1;
@@ -163,7 +164,7 @@ __device__ __forceinline__ void r_rotd(double2 (&a)[kR], const RotRec *rots, int
         const uint64_t s_hi = __ldg(&rots[k].s_hi);
         const int q = __ldg(&rots[k].q);
         const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
-        const uint32_t sB = (q >> 8) & 15u;
+        const uint32_t sB = (q >> 8) & (kR - 1u);
         const uint32_t par = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
         // diagonal: a *= c + kappa sg, kappa = -i s (q = 3)
 #pragma unroll
@@ -182,8 +183,11 @@ __device__ __forceinline__ void dispatch_rotg(int F, double2 (&a)[kR], const Rot
     switch (F) {
 #define QSV_ROTG_CASE(f) case f: r_rotg<f>(a, rots, r0, r1, base, tid); break;
         QSV_ROTG_CASE(1) QSV_ROTG_CASE(2) QSV_ROTG_CASE(3) QSV_ROTG_CASE(4) QSV_ROTG_CASE(5)
-        QSV_ROTG_CASE(6) QSV_ROTG_CASE(7) QSV_ROTG_CASE(8) QSV_ROTG_CASE(9) QSV_ROTG_CASE(10)
+        QSV_ROTG_CASE(6) QSV_ROTG_CASE(7)
+#if QSV_BLOCK_BITS > 3
+        QSV_ROTG_CASE(8) QSV_ROTG_CASE(9) QSV_ROTG_CASE(10)
         QSV_ROTG_CASE(11) QSV_ROTG_CASE(12) QSV_ROTG_CASE(13) QSV_ROTG_CASE(14) QSV_ROTG_CASE(15)
+#endif
 #undef QSV_ROTG_CASE
         default: break;
     }
@@ -194,8 +198,12 @@ __device__ __forceinline__ void dispatch_u1(int j, double2 (&a)[kR], const doubl
     switch (j) {
         case 0: r_u1<0>(a, P); break;
         case 1: r_u1<1>(a, P); break;
+#if QSV_BLOCK_BITS > 3
         case 2: r_u1<2>(a, P); break;
         default: r_u1<3>(a, P); break;
+#else
+        default: r_u1<2>(a, P); break;
+#endif
     }
 }
 
@@ -205,16 +213,18 @@ __device__ __forceinline__ void dispatch_pair(int ja, int jb, double2 (&a)[kR], 
     switch (ja * 4 + jb) {
         case 1: OPW<0, 1>::run(a, P); break;
         case 2: OPW<0, 2>::run(a, P); break;
-        case 3: OPW<0, 3>::run(a, P); break;
         case 4: OPW<1, 0>::run(a, P); break;
         case 6: OPW<1, 2>::run(a, P); break;
-        case 7: OPW<1, 3>::run(a, P); break;
         case 8: OPW<2, 0>::run(a, P); break;
         case 9: OPW<2, 1>::run(a, P); break;
+#if QSV_BLOCK_BITS > 3
+        case 3: OPW<0, 3>::run(a, P); break;
+        case 7: OPW<1, 3>::run(a, P); break;
         case 11: OPW<2, 3>::run(a, P); break;
         case 12: OPW<3, 0>::run(a, P); break;
         case 13: OPW<3, 1>::run(a, P); break;
         case 14: OPW<3, 2>::run(a, P); break;
+#endif
         default: break;
     }
 }
@@ -299,7 +309,7 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
     const int tbits = m - kRB;      // thread-index bits of a block
     // store map: slot of logical l = tid + k*kT
     uint32_t st_base = (uint32_t)__ldg(g_geo + 44);
-    for (int i = 0; i < 8 && i < m; ++i)
+    for (int i = 0; i < kTB && i < m; ++i)
         if ((tid >> i) & 1u) st_base ^= (uint32_t)__ldg(g_geo + 32 + i);
     __syncthreads();
     const uint64_t ntiles = 1ull << g.ncomp;
@@ -327,13 +337,15 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
                     uint32_t sb = __ldg(&B->tswz);
                     for (int i = 0; i < tbits; ++i)
                         if ((tid >> i) & 1u) sb ^= __ldg(&B->cols[i]);
-                    const uint32_t e0 = __ldg(&B->cols[8]), e1 = __ldg(&B->cols[9]);
-                    const uint32_t e2 = __ldg(&B->cols[10]), e3 = __ldg(&B->cols[11]);
+                    uint32_t e[kRB];
+#pragma unroll
+                    for (int j = 0; j < kRB; ++j) e[j] = __ldg(&B->cols[kTB + j]);
                     double2 a[kR];
 #pragma unroll
                     for (int r = 0; r < kR; ++r) {
-                        const uint32_t o = ((r & 1) ? e0 : 0u) ^ ((r & 2) ? e1 : 0u) ^
-                                           ((r & 4) ? e2 : 0u) ^ ((r & 8) ? e3 : 0u);
+                        uint32_t o = 0;
+#pragma unroll
+                        for (int j = 0; j < kRB; ++j) o ^= ((r >> j) & 1) ? e[j] : 0u;
                         a[r] = sm[sb ^ o];
                     }
 #pragma unroll 1
@@ -351,8 +363,12 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
                                     switch (oa) {
                                         case 0: r_diag_in<0>(a, d0, d1); break;
                                         case 1: r_diag_in<1>(a, d0, d1); break;
+#if QSV_BLOCK_BITS > 3
                                         case 2: r_diag_in<2>(a, d0, d1); break;
                                         default: r_diag_in<3>(a, d0, d1); break;
+#else
+                                        default: r_diag_in<2>(a, d0, d1); break;
+#endif
                                     }
                                 } else {
                                     const double2 d = ((tid >> ob) & 1u) ? d1 : d0;
@@ -368,8 +384,9 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
                     }
 #pragma unroll
                     for (int r = 0; r < kR; ++r) {
-                        const uint32_t o = ((r & 1) ? e0 : 0u) ^ ((r & 2) ? e1 : 0u) ^
-                                           ((r & 4) ? e2 : 0u) ^ ((r & 8) ? e3 : 0u);
+                        uint32_t o = 0;
+#pragma unroll
+                        for (int j = 0; j < kRB; ++j) o ^= ((r >> j) & 1) ? e[j] : 0u;
                         sm[sb ^ o] = a[r];
                     }
                 }
@@ -386,10 +403,10 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
         double2 *dst = psi + base;
         if (tsize >= kT) {
 #pragma unroll 4
-            for (int k = 0; k < (tsize >> 8); ++k) {
+            for (int k = 0; k < (tsize >> kTB); ++k) {
                 uint32_t sk = 0;
-                for (int j = 0; j < 4; ++j)
-                    if ((k >> j) & 1) sk ^= (uint32_t)__ldg(g_geo + 40 + j);
+                for (int j = 0; j < kRB; ++j)
+                    if ((k >> j) & 1) sk ^= (uint32_t)__ldg(g_geo + 32 + kTB + j);
                 const uint32_t l = tid + k * kT;
                 __stcs(dst + (l & cmask) + offhi[l >> c], sm[st_base ^ sk]);
             }

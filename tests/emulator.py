@@ -39,14 +39,15 @@ def _mix(c, a0, k, imag, a1):
     return c * a0 + (1j * k if imag else k) * a1
 
 
-def run_block(a, ops, rots, params, tid, base, blk_ops):
-    """a: (ncos, 16) complex; tid: (ncos,) thread indices; base: tile base index."""
+def run_block(a, ops, rots, params, tid, base, blk_ops, RB):
+    """a: (ncos, 2^RB) complex; tid: (ncos,) thread indices; base: tile base index."""
+    R = 1 << RB
     for op in blk_ops:
         typ, oa, ob, oh, r0, r1, p, f = op
         if typ == OP_U1:
             J = 1 << oa
             m00, m01, m10, m11 = (_c(params, p, k) for k in range(4))
-            for r in range(16):
+            for r in range(R):
                 if r & J:
                     continue
                 x, y = a[:, r].copy(), a[:, r | J].copy()
@@ -55,7 +56,7 @@ def run_block(a, ops, rots, params, tid, base, blk_ops):
         elif typ == OP_U2:
             JA, JB = 1 << oa, 1 << ob
             M = np.array([[_c(params, p + 8 * k, i) for i in range(4)] for k in range(4)])
-            for r in range(16):
+            for r in range(R):
                 if r & (JA | JB):
                     continue
                 idx = [r, r | JB, r | JA, r | JA | JB]
@@ -64,7 +65,7 @@ def run_block(a, ops, rots, params, tid, base, blk_ops):
         elif typ == OP_DIAG1:
             d0, d1 = _c(params, p, 0), _c(params, p, 1)
             if oa >= 0:
-                for r in range(16):
+                for r in range(R):
                     a[:, r] *= d1 if (r >> oa) & 1 else d0
             else:
                 bit = (tid >> ob) & 1
@@ -72,12 +73,12 @@ def run_block(a, ops, rots, params, tid, base, blk_ops):
         elif typ in (OP_ROTG, OP_ROTD):
             for k in range(r0, r1):
                 s_hi, s_loc, q, c, kk, imag = _rot_coeffs(rots[k])
-                sB = (q >> 8) & 15
+                sB = (q >> 8) & (R - 1)
                 s_thr = (q >> 12)
                 par = (popc(base & s_hi) + popc(tid & s_thr)) & 1
                 if typ == OP_ROTD:
                     s = rots[k][4]
-                    for r in range(16):
+                    for r in range(R):
                         sg = par ^ (bin(r & sB).count("1") & 1)
                         ks = np.where(sg, s, -s)
                         a[:, r] = a[:, r] * (c + 1j * ks)
@@ -85,7 +86,7 @@ def run_block(a, ops, rots, params, tid, base, blk_ops):
                     F = f
                     H = F.bit_length() - 1
                     yodd = (q >> 2) & 1
-                    for r in range(16):
+                    for r in range(R):
                         if r & (1 << H):
                             continue
                         r1i = r ^ F
@@ -110,6 +111,8 @@ def run_program(prog: dict, psi: np.ndarray) -> np.ndarray:
     psi = psi.copy()
     ops, rots, params = prog["ops"], prog["rots"], prog["params"]
     n = prog["n"]
+    RB = prog.get("block_bits", 4)
+    R, TB = 1 << RB, 12 - RB
     for ps in prog["passes"]:
         if ps["global"]:
             flip = ps["flip"]
@@ -131,7 +134,7 @@ def run_program(prog: dict, psi: np.ndarray) -> np.ndarray:
         loc = np.zeros(tsize, dtype=np.int64)
         for b in range(m):
             loc |= ((np.arange(tsize) >> b) & 1) << pos[b]
-        ncos = tsize >> 4
+        ncos = tsize >> RB
         tid = np.arange(ncos, dtype=np.int64)
         for tile in range(1 << len(comp)):
             base = 0
@@ -145,14 +148,17 @@ def run_program(prog: dict, psi: np.ndarray) -> np.ndarray:
                 cols = blk["cols"]
                 if blk["kind"] == 0:
                     sb = np.full(ncos, blk["tswz"], dtype=np.int64)
-                    for i in range(m - 4):
+                    for i in range(m - RB):
                         sb ^= np.where((tid >> i) & 1, cols[i], 0)
-                    e = cols[8:12]
-                    off = np.array([(e[0] if r & 1 else 0) ^ (e[1] if r & 2 else 0) ^
-                                    (e[2] if r & 4 else 0) ^ (e[3] if r & 8 else 0) for r in range(16)])
+                    e = cols[TB:TB + RB]
+                    off = np.zeros(R, dtype=np.int64)
+                    for r in range(R):
+                        for j in range(RB):
+                            if (r >> j) & 1:
+                                off[r] ^= e[j]
                     slots = sb[:, None] ^ off[None, :]
                     a = sm[slots]
-                    run_block(a, ops, rots, params, tid, base, bops)
+                    run_block(a, ops, rots, params, tid, base, bops, RB)
                     sm[slots] = a
                 else:
                     typ, oa, ob, oh, r0, r1, p, f = bops[0]
