@@ -451,6 +451,7 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
     materialize_gates(*tpl, values);
     std::vector<double> params(tpl->n_params);
     for (const ParamFill &f : tpl->fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, &params[f.offset]);
+    materialize_gmats(*tpl, params.data());
     fill_stats(*tpl, hit, stats);
     return run_template(s, *tpl, params);
 }
@@ -490,7 +491,8 @@ int qsv_apply_pauli_rotations(qsv_state *s, int64_t n, const uint64_t *x, const 
     ProgramTemplate t;
     plan_rotations(s->n, R, n, t);
     materialize_rotations(t, theta);
-    std::vector<double> params;
+    std::vector<double> params(t.n_params);
+    materialize_gmats(t, params.data());
     fill_stats(t, false, stats);
     int rc = run_template(s, t, params);
     if (rc) return rc;
@@ -798,6 +800,7 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     materialize_gates(t, values);
     std::vector<double> params(t.n_params);
     for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, &params[f.offset]);
+    materialize_gmats(t, params.data());
     std::string j = "{\"n\":" + std::to_string(n) + ",\"block_bits\":" +
                     std::to_string(kBlockBits) + ",\"passes\":[";
     char buf[256];

@@ -24,7 +24,7 @@ constexpr int kMaxQubits = 40;
 // Register bits of a tile-kernel block: each thread holds 2^kBlockBits
 // amplitudes (8 -> 512 threads per 4096-amplitude tile, 16 warps per SM).
 #ifndef QSV_BLOCK_BITS
-#define QSV_BLOCK_BITS 3
+#define QSV_BLOCK_BITS 4
 #endif
 constexpr int kBlockBits = QSV_BLOCK_BITS;
 
@@ -38,6 +38,8 @@ enum OpType : int32_t {
     OP_DIAG1 = 6,  // diag(d0, d1) on a; params[p..p+4)
     OP_ROTG = 7,   // rotations exp(-i t/2 P) sharing local flip mask f (highest bit h), rots[r0..r1)
     OP_ROTD = 8,   // diagonal (Z-only) rotations, rots[r0..r1)
+    OP_GMAT = 9,   // fused same-flip group: per pair one 2x2 from params[p..], selected by
+                   // (common sign parity, flip-bit pattern); rots[r0] holds the common masks
 };
 
 struct OpRec {  // 32 B

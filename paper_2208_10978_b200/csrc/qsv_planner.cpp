@@ -428,6 +428,12 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
                     if ((mask >> pos[j]) & 1u) o |= 1u << j;
                 return o;
             };
+            auto expand_b = [&](uint32_t loc) {
+                uint32_t o = 0;
+                for (int j = 0; j < RB; ++j)
+                    if ((loc >> j) & 1u) o |= 1u << pos[j];
+                return o;
+            };
             auto comp_t = [&](uint32_t mask) {
                 uint32_t o = 0;
                 for (int i = 0; i < kn; ++i)
@@ -457,6 +463,39 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
                     for (int r = op.r0; r < op.r1; ++r)
                         t.rots[r].q = (t.rots[r].q & 0xff) | (int32_t)(comp_b(t.rots[r].s_loc) << 8) |
                                       (int32_t)(comp_t(t.rots[r].s_loc) << 12);
+                if (op.type == OP_ROTG && op.r1 - op.r0 >= 2) {
+                    // fuse when every string shares the sign bits off the flip
+                    // (JW Z-chain): one 2x2 per pair instead of r1-r0 rotations
+                    const uint32_t fl = expand_b(op.f);
+                    const uint32_t zc = t.rots[op.r0].s_loc & ~fl;
+                    const uint64_t zh = t.rots[op.r0].s_hi;
+                    bool ok = true;
+                    for (int r = op.r0 + 1; r < op.r1 && ok; ++r)
+                        ok = (t.rots[r].s_loc & ~fl) == zc && t.rots[r].s_hi == zh;
+                    if (ok) {
+                        GmatFill gf;
+                        gf.r0 = op.r0;
+                        gf.r1 = op.r1;
+                        gf.F = (int)op.f;
+                        gf.H = 31 - __builtin_clz(op.f);
+                        gf.w = __builtin_popcount(op.f);
+                        for (int r = op.r0; r < op.r1; ++r)
+                            gf.yF.push_back((uint8_t)comp_b(t.rots[r].s_loc & fl));
+                        gf.offset = (int)t.n_params;
+                        t.n_params += (size_t)8 * (2u << (gf.w - 1));
+                        t.gfills.push_back(gf);
+                        // common masks live in a dedicated record
+                        RotRec cr = t.rots[op.r0];
+                        cr.q = (int32_t)(comp_b(zc) << 8) | (int32_t)(comp_t(zc) << 12);
+                        cr.s_loc = zc;
+                        t.rots.push_back(cr);
+                        t.rot_src.push_back(t.rot_src[op.r0]);
+                        op.type = OP_GMAT;
+                        op.p = gf.offset;
+                        op.r0 = (int)t.rots.size() - 1;
+                        op.r1 = op.r0 + 1;
+                    }
+                }
                 out.push_back(op);
             }
             br.op1 = (int)out.size();
@@ -685,6 +724,62 @@ void materialize_rotations(ProgramTemplate &t, const double *theta)
         const double th = theta[t.rot_src[r]];
         t.rots[r].c = std::cos(0.5 * th);
         t.rots[r].s = std::sin(0.5 * th);
+    }
+}
+
+void materialize_gmats(const ProgramTemplate &t, double *params)
+{
+    for (const GmatFill &g : t.gfills) {
+        const int ncfg = 1 << (g.w - 1);
+        int fpos[8], k = 0;
+        for (int j = 0; j < 8; ++j)
+            if ((g.F >> j) & 1) fpos[k++] = j;
+        for (int cp = 0; cp < 2; ++cp) {
+            for (int cfg = 0; cfg < ncfg; ++cfg) {
+                // r1's bits on F: bit H set, the others from cfg (ascending, H skipped)
+                uint32_t r1 = 1u << g.H;
+                for (int i = 0, c = 0; i < g.w; ++i) {
+                    if (fpos[i] == g.H) continue;
+                    if ((cfg >> c) & 1) r1 |= 1u << fpos[i];
+                    ++c;
+                }
+                double M[8] = {1, 0, 0, 0, 0, 0, 1, 0};  // identity, row-major complex
+                for (int r = g.r0; r < g.r1; ++r) {
+                    const RotRec &R = t.rots[r];
+                    const int yodd = (R.q >> 2) & 1;
+                    const int q = R.q & 3;
+                    const int s1 = (cp + __builtin_popcount(r1 & g.yF[r - g.r0])) & 1;
+                    const int s0 = s1 ^ yodd;
+                    // kappa = i^q sin; R = [[c, kappa sg1], [kappa sg0, c]]
+                    double kre = 0, kim = 0;
+                    switch (q) {
+                        case 0: kre = R.s; break;
+                        case 1: kim = R.s; break;
+                        case 2: kre = -R.s; break;
+                        default: kim = -R.s; break;
+                    }
+                    const double b_re = s1 ? -kre : kre, b_im = s1 ? -kim : kim;
+                    const double c_re = s0 ? -kre : kre, c_im = s0 ? -kim : kim;
+                    const double Rm[8] = {R.c, 0, b_re, b_im, c_re, c_im, R.c, 0};
+                    double N[8];
+                    for (int i = 0; i < 2; ++i)
+                        for (int j = 0; j < 2; ++j) {
+                            double re = 0, im = 0;
+                            for (int l = 0; l < 2; ++l) {
+                                const double ar = Rm[2 * (2 * i + l)], ai = Rm[2 * (2 * i + l) + 1];
+                                const double br = M[2 * (2 * l + j)], bi = M[2 * (2 * l + j) + 1];
+                                re += ar * br - ai * bi;
+                                im += ar * bi + ai * br;
+                            }
+                            N[2 * (2 * i + j)] = re;
+                            N[2 * (2 * i + j) + 1] = im;
+                        }
+                    for (int i = 0; i < 8; ++i) M[i] = N[i];
+                }
+                double *dst = params + g.offset + 8 * (cp * ncfg + cfg);
+                for (int i = 0; i < 8; ++i) dst[i] = M[i];
+            }
+        }
     }
 }
 

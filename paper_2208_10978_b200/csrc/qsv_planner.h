@@ -48,6 +48,15 @@ struct ParamFill {
     int kind;    // gate kind
 };
 
+// A fused same-flip rotation group (OP_GMAT): the table of 2 x 2^(w-1)
+// complex 2x2 matrices is rebuilt from the angles on every call.
+struct GmatFill {
+    int offset;        // params offset of the table
+    int r0, r1;        // rotations (in order) of the group
+    int F, H, w;       // block-local flip, its highest bit, popcount
+    std::vector<uint8_t> yF;  // block-local Y bits of each rotation
+};
+
 struct ProgramTemplate {
     int n = 0, m = 0, c = 0;
     std::vector<PassPlan> passes;
@@ -56,6 +65,7 @@ struct ProgramTemplate {
     std::vector<RotRec> rots;      // c/s refreshed per call
     std::vector<int> rot_src;      // theta source index per RotRec
     std::vector<ParamFill> fills;  // matrices refreshed per call
+    std::vector<GmatFill> gfills;  // fused group tables refreshed per call
     size_t n_params = 0;
     // global-fallback rotation records (full 64-bit masks), per pass: rots[r0..r1)
     int64_t n_input = 0, n_rotations = 0, n_items = 0, n_fallback = 0, n_blocks = 0;
@@ -74,6 +84,8 @@ void plan_rotations(int n, const std::vector<Rot> &rots, int64_t n_input, Progra
 // Refresh angle-dependent data.  theta_of(src) gives the rotation angle.
 void materialize_gates(ProgramTemplate &t, const double *values);
 void materialize_rotations(ProgramTemplate &t, const double *theta);
+// Fused group tables (after rots[].c/s are refreshed) into params.
+void materialize_gmats(const ProgramTemplate &t, double *params);
 // Gate matrix restatement of circuit.py:198-223 (row-major complex128).
 int gate_matrix(int kind, const double *v, double *out);
 

@@ -177,6 +177,65 @@ __device__ __forceinline__ void r_rotd(double2 (&a)[kR], const RotRec *rots, int
     }
 }
 
+__host__ __device__ constexpr int popc_c(int v) { return v ? (v & 1) + popc_c(v >> 1) : 0; }
+
+// index of r1's flip-bit pattern (bits of F except H, compressed ascending);
+// folds to a constant inside the unrolled pair loops
+template <int F, int H>
+__device__ __forceinline__ int cfg_of(int r1)
+{
+    int out = 0, k = 0;
+#pragma unroll
+    for (int b = 0; b < kRB; ++b) {
+        if (((F >> b) & 1) && b != H) {
+            out |= ((r1 >> b) & 1) << k;
+            ++k;
+        }
+    }
+    return out;
+}
+
+// Fused same-flip group (OP_GMAT): per pair, the product of the group's
+// rotations is one 2x2 picked by (common sign parity cp, flip pattern cfg).
+template <int F>
+__device__ __forceinline__ void r_gmat(double2 (&a)[kR], const double *T, const RotRec *rc,
+                                       uint64_t base, uint32_t tid)
+{
+    constexpr int H = 31 - __builtin_clz(F);
+    constexpr int NCFG = 1 << (popc_c(F) - 1);
+    const uint64_t s_hi = __ldg(&rc->s_hi);
+    const int q = __ldg(&rc->q);
+    const uint32_t zB = (q >> 8) & (kR - 1u);
+    const uint32_t par0 = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        if (r & (1 << H)) continue;
+        const int r1 = r ^ F;
+        const uint32_t cp = par0 ^ (__popc((uint32_t)r1 & zB) & 1u);
+        const double *M = T + 8 * ((int)cp * NCFG + cfg_of<F, H>(r1));
+        const double2 m00 = ld2(M), m01 = ld2(M + 2), m10 = ld2(M + 4), m11 = ld2(M + 6);
+        const double2 x = a[r], y = a[r1];
+        a[r] = cfma2(m00, x, m01, y);
+        a[r1] = cfma2(m10, x, m11, y);
+    }
+}
+
+__device__ __forceinline__ void dispatch_gmat(int F, double2 (&a)[kR], const double *T,
+                                              const RotRec *rc, uint64_t base, uint32_t tid)
+{
+    switch (F) {
+#define QSV_GMAT_CASE(f) case f: r_gmat<f>(a, T, rc, base, tid); break;
+        QSV_GMAT_CASE(1) QSV_GMAT_CASE(2) QSV_GMAT_CASE(3) QSV_GMAT_CASE(4) QSV_GMAT_CASE(5)
+        QSV_GMAT_CASE(6) QSV_GMAT_CASE(7)
+#if QSV_BLOCK_BITS > 3
+        QSV_GMAT_CASE(8) QSV_GMAT_CASE(9) QSV_GMAT_CASE(10)
+        QSV_GMAT_CASE(11) QSV_GMAT_CASE(12) QSV_GMAT_CASE(13) QSV_GMAT_CASE(14) QSV_GMAT_CASE(15)
+#endif
+#undef QSV_GMAT_CASE
+        default: break;
+    }
+}
+
 __device__ __forceinline__ void dispatch_rotg(int F, double2 (&a)[kR], const RotRec *rots, int r0,
                                               int r1, uint64_t base, uint32_t tid)
 {
@@ -379,6 +438,9 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
                             }
                             case OP_ROTG: dispatch_rotg(w1.w, a, rots, w1.x, w1.y, base, tid); break;
                             case OP_ROTD: r_rotd(a, rots, w1.x, w1.y, base, tid); break;
+                            case OP_GMAT:
+                                dispatch_gmat(w1.w, a, params + w1.z, rots + w1.x, base, tid);
+                                break;
                             default: break;
                         }
                     }

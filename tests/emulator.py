@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-OP_U1, OP_U2, OP_CX, OP_SWAP, OP_X, OP_DIAG1, OP_ROTG, OP_ROTD = 1, 2, 3, 4, 5, 6, 7, 8
+OP_U1, OP_U2, OP_CX, OP_SWAP, OP_X, OP_DIAG1, OP_ROTG, OP_ROTD, OP_GMAT = 1, 2, 3, 4, 5, 6, 7, 8, 9
 
 
 def swz(l):
@@ -70,6 +70,31 @@ def run_block(a, ops, rots, params, tid, base, blk_ops, RB):
             else:
                 bit = (tid >> ob) & 1
                 a *= np.where(bit, d1, d0)[:, None]
+        elif typ == OP_GMAT:
+            F = f
+            H = F.bit_length() - 1
+            w = bin(F).count("1")
+            ncfg = 1 << (w - 1)
+            s_hi, s_loc, q, c, kk, imag = _rot_coeffs(rots[r0])
+            zB = (q >> 8) & (R - 1)
+            par0 = (popc(base & s_hi) + popc(tid & (q >> 12))) & 1
+            fpos = [j for j in range(RB) if (F >> j) & 1]
+            for r in range(R):
+                if r & (1 << H):
+                    continue
+                r1 = r ^ F
+                cfg, k = 0, 0
+                for j in fpos:
+                    if j == H:
+                        continue
+                    cfg |= ((r1 >> j) & 1) << k
+                    k += 1
+                cp = par0 ^ (bin(r1 & zB).count("1") & 1)
+                idx = p + 8 * (cp * ncfg + cfg)
+                m = [np.array([params[i + 2 * e] + 1j * params[i + 2 * e + 1] for i in idx]) for e in range(4)]
+                x, y = a[:, r].copy(), a[:, r1].copy()
+                a[:, r] = m[0] * x + m[1] * y
+                a[:, r1] = m[2] * x + m[3] * y
         elif typ in (OP_ROTG, OP_ROTD):
             for k in range(r0, r1):
                 s_hi, s_loc, q, c, kk, imag = _rot_coeffs(rots[k])

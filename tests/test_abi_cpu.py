@@ -147,3 +147,23 @@ def test_emulated_mixed_and_rotations_match_oracle(n):
     psi0 = a / np.linalg.norm(a)
     out, _ = _emulate(circ, psi0)
     assert np.abs(out - O.evolve(psi0, circ.gates)).max() <= 1e-12
+
+
+@pytest.mark.parametrize("n,ne,ndoubles", [(8, 4, None), (14, 6, 40)])
+def test_emulated_ucc_groups_match_oracle(n, ne, ndoubles):
+    """Same-flip UCC groups take the fused 2x2-table path (OP_GMAT)."""
+    import itertools
+
+    from oracle import oracle as O
+    occ, vir = range(ne), range(ne, n)
+    doubles = [(ij, ab) for ij in itertools.combinations(occ, 2) for ab in itertools.combinations(vir, 2)]
+    if ndoubles is not None:
+        rng = np.random.default_rng(1)
+        doubles = [doubles[k] for k in rng.choice(len(doubles), size=ndoubles, replace=False)]
+    strings = W.ucc_rotation_strings(n, ne, doubles)
+    thetas = np.random.default_rng(2).uniform(-0.3, 0.3, size=len(strings))
+    circ = W.rotations_circuit(n, strings, thetas)
+    psi0 = O.init_state(W.hf_bitstring(ne, n))
+    out, prog = _emulate(circ, psi0)
+    assert any(op[0] == 9 for op in prog["ops"])  # fused groups present
+    assert np.abs(out - O.evolve(psi0, circ.gates)).max() <= 1e-12
