@@ -11,7 +11,7 @@ Prints ONE JSON line (rank 0).  value = amplitude-updates/s (sum over the 830
 gates of 2^n, per second, whole job); e2e = the same metric through the public
 backend API with host buffers (gate arrays in, full amplitude vector out to
 pinned host memory) inside the timed region.  roofline = the dominant kernel
-(tile_pass_kernel): algorithmic 32 B x 2^n per launch over its average launch
+(tile_block_kernel): algorithmic 32 B x 2^n per launch over its average launch
 duration (CUDA events on the library's stream), vs MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline = the reference (oracle/_ref: vqekit + Cython kernels, 1 thread --
 the reference evolve is single-threaded) on a bounded sample of the same
@@ -373,7 +373,7 @@ def run_engine(args, rank, world, local):
         "e2e": {"value": e2e_val, "unit": "amplitude-updates/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": 16 * dim, "ms_per_step": t_e2e * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "tile_pass_kernel",
+                     "frac": achieved / peak, "traffic": None, "kernel": "tile_block_kernel",
                      "ms_per_launch": t_pass * 1e3, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": 32 * dim},
         "gpu_launches": args.steps * (passes + 1),

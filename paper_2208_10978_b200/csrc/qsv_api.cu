@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <list>
@@ -173,25 +174,82 @@ uint64_t hash_masks(int n, int64_t S, const uint64_t *x, const uint64_t *y, cons
     return h;
 }
 
+// Parameter doubles an op reads (for pass-local rebasing).
+int op_param_count(const OpRec &op)
+{
+    switch (op.type) {
+        case OP_U1: return 8;
+        case OP_U2: return 32;
+        case OP_DIAG1: return 4;
+        case OP_GMAT: return 16 << (__builtin_popcount(op.f) - 1);
+        default: return 0;
+    }
+}
+
 int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params)
 {
     DeviceCtx *c = nullptr;
     int rc = ctx_for(s->device, &c);
     if (rc) return rc;
     Blob b;
+    // global (shared) arrays for the legacy / fallback kernels
     const size_t o_ops = b.add(t.ops.data(), t.ops.size() * sizeof(OpRec));
     const size_t o_rots = b.add(t.rots.data(), t.rots.size() * sizeof(RotRec));
     const size_t o_par = b.add(params.data(), params.size() * sizeof(double));
-    const size_t o_blk = b.add(t.blocks.data(), t.blocks.size() * sizeof(BlockRec));
-    std::vector<size_t> o_off(t.passes.size()), o_comp(t.passes.size());
+    struct PassOff { size_t off, comp, blk, ops, rots, par; int nblk, nops, nrots, npar; };
+    std::vector<PassOff> po(t.passes.size());
     {
         std::vector<uint64_t> offhi;
         std::vector<int32_t> comp;
+        std::vector<OpRec> lops;
+        std::vector<BlockRec> lblk;
         for (size_t k = 0; k < t.passes.size(); ++k) {
-            if (t.passes[k].global) continue;
-            geom_tables(t.passes[k].geom, offhi, comp, &t.passes[k]);
-            o_off[k] = b.add(offhi.data(), offhi.size() * sizeof(uint64_t));
-            o_comp[k] = b.add(comp.data(), comp.size() * sizeof(int32_t));
+            const PassPlan &p = t.passes[k];
+            PassOff &o = po[k];
+            o = PassOff{};
+            if (p.global) continue;
+            geom_tables(p.geom, offhi, comp, &t.passes[k]);
+            o.off = b.add(offhi.data(), offhi.size() * sizeof(uint64_t));
+            o.comp = b.add(comp.data(), comp.size() * sizeof(int32_t));
+            if (p.geom.m < kBlockBits + 1) continue;
+            // pass-local program: rebase op/rot/param indices
+            int r_lo = INT32_MAX, r_hi = 0, p_lo = INT32_MAX, p_hi = 0;
+            for (int i = p.op_begin; i < p.op_end; ++i) {
+                const OpRec &op = t.ops[i];
+                if (op.r1 > op.r0) {
+                    r_lo = std::min(r_lo, op.r0);
+                    r_hi = std::max(r_hi, op.r1);
+                }
+                const int np = op_param_count(op);
+                if (np) {
+                    p_lo = std::min(p_lo, op.p);
+                    p_hi = std::max(p_hi, op.p + np);
+                }
+            }
+            if (r_lo == INT32_MAX) r_lo = r_hi = 0;
+            if (p_lo == INT32_MAX) p_lo = p_hi = 0;
+            p_lo &= ~3;  // keep 32 B alignment of matrices
+            lops.assign(t.ops.begin() + p.op_begin, t.ops.begin() + p.op_end);
+            for (OpRec &op : lops) {
+                if (op.r1 > op.r0) {
+                    op.r0 -= r_lo;
+                    op.r1 -= r_lo;
+                }
+                if (op_param_count(op)) op.p -= p_lo;
+            }
+            lblk.assign(t.blocks.begin() + p.block_begin, t.blocks.begin() + p.block_end);
+            for (BlockRec &bl : lblk) {
+                bl.op0 -= p.op_begin;
+                bl.op1 -= p.op_begin;
+            }
+            o.nblk = (int)lblk.size();
+            o.nops = (int)lops.size();
+            o.nrots = r_hi - r_lo;
+            o.npar = p_hi - p_lo;
+            o.blk = b.add(lblk.data(), lblk.size() * sizeof(BlockRec));
+            o.ops = b.add(lops.data(), lops.size() * sizeof(OpRec));
+            o.rots = b.add(t.rots.data() + r_lo, (size_t)o.nrots * sizeof(RotRec));
+            o.par = b.add(params.data() + p_lo, (size_t)o.npar * sizeof(double));
         }
     }
     char *d = nullptr;
@@ -203,24 +261,25 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     const double *d_par = (const double *)(d + o_par);
     for (size_t k = 0; k < t.passes.size(); ++k) {
         const PassPlan &p = t.passes[k];
+        const PassOff &o = po[k];
         // a pass made only of permutation gates has no blocks but a permuted
         // store map: it still has to run (load -> store through the map)
         if (p.op_end <= p.op_begin && !p.map_permuted) continue;
         if (p.global) {
-            for (int k = p.op_begin; k < p.op_end; ++k) {
-                const OpRec &op = t.ops[k];
+            for (int i = p.op_begin; i < p.op_end; ++i) {
+                const OpRec &op = t.ops[i];
                 QSV_CUDA(launch_rot_global(s->amps, s->n, p.flip, d_rots + op.r0, op.r1 - op.r0,
                                            s->stream));
             }
         } else if (p.geom.m >= kBlockBits + 1) {
-            QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o_off[k]),
-                                        (const int32_t *)(d + o_comp[k]),
-                                        (const BlockRec *)(d + o_blk) + p.block_begin,
-                                        p.block_end - p.block_begin, d_ops, d_rots, d_par,
-                                        s->stream));
+            QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
+                                        (const int32_t *)(d + o.comp), (const BlockRec *)(d + o.blk),
+                                        o.nblk, (const OpRec *)(d + o.ops), o.nops,
+                                        (const RotRec *)(d + o.rots), o.nrots,
+                                        (const double *)(d + o.par), o.npar, s->stream));
         } else {
-            QSV_CUDA(launch_tile_pass(s->amps, dims_of(p.geom), (const uint64_t *)(d + o_off[k]),
-                                      (const int32_t *)(d + o_comp[k]), d_ops + p.op_begin,
+            QSV_CUDA(launch_tile_pass(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
+                                      (const int32_t *)(d + o.comp), d_ops + p.op_begin,
                                       p.op_end - p.op_begin, d_rots, d_par, s->stream));
         }
     }

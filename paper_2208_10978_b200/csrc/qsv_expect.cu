@@ -6,7 +6,7 @@
 //
 //  * flip groups (strings sharing f = x|y): the group's 2^(m-1) amplitude
 //    pairs (l0, l0 ^ f) are cut into quarters of 512; one warp takes a
-//    quarter, each lane 16 consecutive pair indices.  A lane forms
+//    quarter, each lane the 16 pair indices lane + 32 r.  A lane forms
 //    w = conj(psi_l0) psi_l1 for its 16 pairs, runs a 16-point Walsh-Hadamard
 //    transform of Re w / Im w in registers, and every string of the group
 //    then costs one shared-memory lookup + one warp reduction instead of a
@@ -49,6 +49,15 @@ __device__ __forceinline__ uint64_t tbase(uint64_t tile, int lane, int ncomp, in
     return ((uint64_t)hi << 32) | lo;
 }
 
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc)
+{
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ double wsum(double v)
 {
 #pragma unroll
@@ -71,6 +80,8 @@ __device__ __forceinline__ void wht16(double (&v)[16])
 }
 
 // Strings [t_a, t_b) of one group against the lane's WHT16 vector in scratch.
+// The lane's pairs are p = pbase + 32 r (r = 0..15): the WHT runs over pair
+// bits 5..8, the lane's own bits enter as a sign.
 __device__ __forceinline__ void eval_terms(const double *scr, int lane, uint32_t pbase,
                                            uint64_t base, const TermRec *terms, int t_a, int t_b,
                                            double *acc, int ndiag, int slot)
@@ -78,8 +89,8 @@ __device__ __forceinline__ void eval_terms(const double *scr, int lane, uint32_t
     for (int t = t_a; t < t_b; ++t) {
         const uint32_t sp = __ldg(&terms[t].s_loc);
         const uint64_t s_hi = __ldg(&terms[t].s_hi);
-        const uint32_t sg = (__popc(pbase & sp & ~15u) + __popcll(base & s_hi)) & 1u;
-        const double v = scr[(sp & 15u) * 32 + lane];
+        const uint32_t sg = (__popc(pbase & sp & ~(15u << 5)) + __popcll(base & s_hi)) & 1u;
+        const double v = scr[((sp >> 5) & 15u) * 32 + lane];
         const double sum = wsum(sg ? -v : v);
         if (lane == 0) acc[(t - ndiag) * kSlots + slot] += __ldg(&terms[t].scale) * sum;
     }
@@ -96,8 +107,8 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
     const int m = g.m, c = g.c;
     const int tsize = 1 << m;
     const int npairs = tsize >> 1;
-    double2 *sm = reinterpret_cast<double2 *>(smem_raw);
-    double *scr = reinterpret_cast<double *>(sm + tsize);      // [kW][16][32]
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);    // 2 x tsize (double-buffered)
+    double *scr = reinterpret_cast<double *>(bufs + 2 * tsize);  // [kW][16][32]
     double *acc = scr + kW * 16 * 32;                           // flip: [nflip][kSlots], then diag
     const int nflip = nterms - ndiag;
     double *accd = acc + nflip * kSlots;
@@ -112,11 +123,26 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
     double *wscr = scr + warp * 16 * 32;
     __syncthreads();
     const uint64_t ntiles = 1ull << g.ncomp;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
+    uint64_t tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
+    {
         const double2 *src = psi + base;
 #pragma unroll 4
-        for (int l = threadIdx.x; l < tsize; l += kT) sm[l] = __ldcs(src + (l & cmask) + offhi[l >> c]);
+        for (int l = threadIdx.x; l < tsize; l += kT) cp_async16(bufs + l, src + (l & cmask) + offhi[l >> c]);
+        cp_async_commit();
+    }
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        double2 *sm = bufs + (it & 1) * tsize;
+        const uint64_t next = tile + gridDim.x;
+        if (next < ntiles) {  // prefetch the next tile into the other buffer
+            const double2 *src = psi + tbase(next, lane, g.ncomp, comp_lane);
+            double2 *dstb = bufs + ((it + 1) & 1) * tsize;
+#pragma unroll 4
+            for (int l = threadIdx.x; l < tsize; l += kT) cp_async16(dstb + l, src + (l & cmask) + offhi[l >> c]);
+        }
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncthreads();
         // ---- flip groups: items (group, quarter) round-robin over warps ----
         for (int item = warp; item < ngroups * items_per_group; item += kW) {
@@ -125,11 +151,11 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
             const int h = __ldg(&groups[gi].h);
             const int t0 = __ldg(&groups[gi].t0), tim = __ldg(&groups[gi].t_im),
                       t1 = __ldg(&groups[gi].t1);
-            const uint32_t pbase = slot * qsize + lane * 16;
+            const uint32_t pbase = slot * qsize + lane;  // lanes on consecutive pairs
             double vr[16], vi[16];
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
-                const uint32_t p = pbase + r;
+                const uint32_t p = pbase + 32 * r;
                 double re = 0.0, im = 0.0;
                 if (p < (uint32_t)npairs) {
                     const uint32_t l0 = ins0(p, h), l1 = l0 ^ f;
@@ -192,7 +218,9 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
             }
         }
         __syncthreads();
+        if (next < ntiles) base = tbase(next, lane, g.ncomp, comp_lane);
     }
+    cp_async_wait<0>();
     // per-CTA partial sums, fixed slot order
     for (int t = threadIdx.x; t < nterms; t += kT) {
         double v;
@@ -208,7 +236,7 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
 
 size_t sweep2_smem(const TileDims &g, int nterms, int ndiag)
 {
-    return ((size_t)16 << g.m) + (size_t)8 * kW * 16 * 32 +
+    return ((size_t)32 << g.m) + (size_t)8 * kW * 16 * 32 +
            (size_t)8 * ((nterms - ndiag) * kSlots + ndiag) + ((size_t)8 << (g.m - g.c));
 }
 

@@ -820,7 +820,7 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     // Bin flip groups into sweeps: a sweep's tile must hold every group's
     // flip bits.  First-fit decreasing on the high-bit need; capacity is
     // bounded by the shared-memory accumulators (kFlipCap strings).
-    const int kFlipCap = 1024, kDiagCap = 4096, kGroupCap = 256;
+    const int kFlipCap = 512, kDiagCap = 2048, kGroupCap = 256;
     std::vector<int> order(flips.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {

@@ -49,14 +49,14 @@ __device__ __forceinline__ double2 cfma2(double2 m0, double2 x, double2 m1, doub
     return make_double2(re, im);
 }
 
-__device__ __forceinline__ double2 ld2(const double *p) { return make_double2(__ldg(p), __ldg(p + 1)); }
+__device__ __forceinline__ double2 ld2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 
 // volatile (non-hoistable) variant: re-read from L1 instead of pinning a whole
 // 4x4 complex matrix in registers
 __device__ __forceinline__ double2 ld2v(const double *p)
 {
     double2 v;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    asm volatile("ld.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));  // generic: SMEM or global
     return v;
 }
 
@@ -134,9 +134,9 @@ __device__ __forceinline__ void r_rotg(double2 (&a)[kR], const RotRec *rots, int
     constexpr int H = 31 - __builtin_clz(F);
 #pragma unroll 1
     for (int k = r0; k < r1; ++k) {
-        const uint64_t s_hi = __ldg(&rots[k].s_hi);
-        const int q = __ldg(&rots[k].q);
-        const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
+        const uint64_t s_hi = (rots[k].s_hi);
+        const int q = (rots[k].q);
+        const double c = (rots[k].c), s = (rots[k].s);
         const uint32_t sB = (q >> 8) & (kR - 1u);
         const uint32_t par = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
         const uint32_t yodd = (q >> 2) & 1u;
@@ -161,9 +161,9 @@ __device__ __forceinline__ void r_rotd(double2 (&a)[kR], const RotRec *rots, int
 {
 #pragma unroll 1
     for (int k = r0; k < r1; ++k) {
-        const uint64_t s_hi = __ldg(&rots[k].s_hi);
-        const int q = __ldg(&rots[k].q);
-        const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
+        const uint64_t s_hi = (rots[k].s_hi);
+        const int q = (rots[k].q);
+        const double c = (rots[k].c), s = (rots[k].s);
         const uint32_t sB = (q >> 8) & (kR - 1u);
         const uint32_t par = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
         // diagonal: a *= c + kappa sg, kappa = -i s (q = 3)
@@ -203,8 +203,8 @@ __device__ __forceinline__ void r_gmat(double2 (&a)[kR], const double *T, const 
 {
     constexpr int H = 31 - __builtin_clz(F);
     constexpr int NCFG = 1 << (popc_c(F) - 1);
-    const uint64_t s_hi = __ldg(&rc->s_hi);
-    const int q = __ldg(&rc->q);
+    const uint64_t s_hi = (rc->s_hi);
+    const int q = (rc->q);
     const uint32_t zB = (q >> 8) & (kR - 1u);
     const uint32_t par0 = (__popcll(base & s_hi) + __popc(tid & ((uint32_t)q >> 12))) & 1u;
 #pragma unroll
@@ -309,10 +309,10 @@ __device__ void smem_rotg(double2 *sm, int m, uint32_t f, int h, const RotRec *r
         const uint32_t p0 = map_slot(l0, m, tswz, cols), p1 = map_slot(l1, m, tswz, cols);
         double2 a0 = sm[p0], a1 = sm[p1];
         for (int k = r0; k < r1; ++k) {
-            const uint64_t s_hi = __ldg(&rots[k].s_hi);
-            const uint32_t s_loc = __ldg(&rots[k].s_loc);
-            const int q = __ldg(&rots[k].q);
-            const double c = __ldg(&rots[k].c), s = __ldg(&rots[k].s);
+            const uint64_t s_hi = (rots[k].s_hi);
+            const uint32_t s_loc = (rots[k].s_loc);
+            const int q = (rots[k].q);
+            const double c = (rots[k].c), s = (rots[k].s);
             const uint32_t s1 = (__popcll(base & s_hi) + __popc(l1 & s_loc)) & 1u;
             const uint32_t s0 = s1 ^ ((q >> 2) & 1u);
             const double kk = (q & 2) ? -s : s;
@@ -348,11 +348,20 @@ __device__ __forceinline__ void issue_tile_load(double2 *buf, const double2 *src
 // buffer, so HBM traffic overlaps the DFMA / SMEM work.  g_geo[0..31] are the
 // tile-index bit positions, g_geo[32..43] the swizzled columns of the pass's
 // final map and g_geo[44] its swizzled translation (used by the store).
+// Program of one pass (pass-local indices).  STAGED: copied into shared
+// memory once per CTA so every per-tile decode is an LDS.
+struct PassProgram {
+    const BlockRec *blocks;
+    const OpRec *ops;
+    const RotRec *rots;
+    const double *params;
+    int nblocks, nops, nrots, nparams;
+};
+
+template <bool STAGED>
 __global__ void __launch_bounds__(kT, 1)
 tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__restrict__ g_offhi,
-                  const int32_t *__restrict__ g_geo, const BlockRec *__restrict__ blocks, int nblocks,
-                  const OpRec *__restrict__ ops, const RotRec *__restrict__ rots,
-                  const double *__restrict__ params)
+                  const int32_t *__restrict__ g_geo, const PassProgram prog)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = g.m, c = g.c;
@@ -360,6 +369,29 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);  // 2 x tsize
     uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + 2 * tsize);
     for (int i = threadIdx.x; i < (1 << (m - c)); i += kT) offhi[i] = __ldg(g_offhi + i);
+    const BlockRec *blocks = prog.blocks;
+    const OpRec *ops = prog.ops;
+    const RotRec *rots = prog.rots;
+    const double *params = prog.params;
+    const int nblocks = prog.nblocks;
+    if (STAGED) {
+        // layout after offhi (16 B aligned): params | rots | ops | blocks
+        double *sp = reinterpret_cast<double *>(offhi + (1 << (m - c)) + ((1 << (m - c)) & 1));
+        RotRec *sr = reinterpret_cast<RotRec *>(sp + ((prog.nparams + 1) & ~1));
+        OpRec *so = reinterpret_cast<OpRec *>(sr + prog.nrots);
+        BlockRec *sb = reinterpret_cast<BlockRec *>(so + prog.nops);
+        for (int i = threadIdx.x; i < prog.nparams; i += kT) sp[i] = __ldg(prog.params + i);
+        const int4 *gs = reinterpret_cast<const int4 *>(prog.rots);
+        for (int i = threadIdx.x; i < prog.nrots * 2; i += kT) reinterpret_cast<int4 *>(sr)[i] = __ldg(gs + i);
+        gs = reinterpret_cast<const int4 *>(prog.ops);
+        for (int i = threadIdx.x; i < prog.nops * 2; i += kT) reinterpret_cast<int4 *>(so)[i] = __ldg(gs + i);
+        gs = reinterpret_cast<const int4 *>(prog.blocks);
+        for (int i = threadIdx.x; i < prog.nblocks * 3; i += kT) reinterpret_cast<int4 *>(sb)[i] = __ldg(gs + i);
+        params = sp;
+        rots = sr;
+        ops = so;
+        blocks = sb;
+    }
     const uint32_t tid = threadIdx.x;
     const int lane = tid & 31;
     const int comp_lane = __ldg(g_geo + lane);
@@ -389,16 +421,16 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
         __syncthreads();
         for (int bi = 0; bi < nblocks; ++bi) {
             const BlockRec *B = blocks + bi;
-            const int kind = __ldg(&B->kind);
-            const int op0 = __ldg(&B->op0), op1 = __ldg(&B->op1);
+            const int kind = B->kind;
+            const int op0 = B->op0, op1 = B->op1;
             if (kind == 0) {
                 if ((int)tid < ncos) {
-                    uint32_t sb = __ldg(&B->tswz);
+                    uint32_t sb = B->tswz;
                     for (int i = 0; i < tbits; ++i)
-                        if ((tid >> i) & 1u) sb ^= __ldg(&B->cols[i]);
+                        if ((tid >> i) & 1u) sb ^= B->cols[i];
                     uint32_t e[kRB];
 #pragma unroll
-                    for (int j = 0; j < kRB; ++j) e[j] = __ldg(&B->cols[kTB + j]);
+                    for (int j = 0; j < kRB; ++j) e[j] = B->cols[kTB + j];
                     double2 a[kR];
 #pragma unroll
                     for (int r = 0; r < kR; ++r) {
@@ -409,8 +441,8 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
                     }
 #pragma unroll 1
                     for (int k = op0; k < op1; ++k) {
-                        const int4 w0 = __ldg(reinterpret_cast<const int4 *>(ops + k));
-                        const int4 w1 = __ldg(reinterpret_cast<const int4 *>(ops + k) + 1);
+                        const int4 w0 = reinterpret_cast<const int4 *>(ops + k)[0];
+                        const int4 w1 = reinterpret_cast<const int4 *>(ops + k)[1];
                         const int type = w0.x, oa = w0.y, ob = w0.z;
                         switch (type) {
                             case OP_U1: dispatch_u1(oa, a, params + w1.z); break;
@@ -455,9 +487,9 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
             } else {
                 uint16_t cols[12];
 #pragma unroll
-                for (int b = 0; b < 12; ++b) cols[b] = __ldg(&B->cols[b]);
-                smem_rotg(sm, m, __ldg(&ops[op0].f), __ldg(&ops[op0].h), rots, __ldg(&ops[op0].r0),
-                          __ldg(&ops[op0].r1), base, __ldg(&B->tswz), cols);
+                for (int b = 0; b < 12; ++b) cols[b] = B->cols[b];
+                smem_rotg(sm, m, ops[op0].f, ops[op0].h, rots, ops[op0].r0, ops[op0].r1, base,
+                          B->tswz, cols);
             }
             __syncthreads();
         }
@@ -485,31 +517,38 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
 
 cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                                const int32_t *d_geo, const BlockRec *d_blocks, int nblocks,
-                               const OpRec *d_ops, const RotRec *d_rots, const double *d_params,
-                               cudaStream_t st)
+                               const OpRec *d_ops, int nops, const RotRec *d_rots, int nrots,
+                               const double *d_params, int nparams, cudaStream_t st)
 {
     static bool configured = false;
+    const int max_smem = 227 * 1024;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tile_block_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(((size_t)32 << kMaxTileBits) + 8192));
+        cudaError_t e = cudaFuncSetAttribute(tile_block_kernel<true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(tile_block_kernel<false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     int dev = 0;
     cudaGetDevice(&dev);
-    const size_t smem = ((size_t)32 << g.m) + ((size_t)8 << (g.m - g.c));
-    int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_block_kernel, kT, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
+    const size_t nhi = (size_t)1 << (g.m - g.c);
+    const size_t base_smem = ((size_t)32 << g.m) + 8 * (nhi + (nhi & 1));
+    const size_t prog_bytes = 8 * (size_t)((nparams + 1) & ~1) + sizeof(RotRec) * nrots +
+                              sizeof(OpRec) * nops + sizeof(BlockRec) * nblocks;
+    const bool staged = base_smem + prog_bytes <= (size_t)max_smem;
+    const size_t smem = staged ? base_smem + prog_bytes : base_smem;
+    PassProgram prog{d_blocks, d_ops, d_rots, d_params, nblocks, nops, nrots, nparams};
     const uint64_t ntiles = 1ull << g.ncomp;
-    uint64_t cap = (uint64_t)num_sms(dev) * per_sm;
+    uint64_t cap = (uint64_t)num_sms(dev);  // one persistent CTA per SM
     static const char *env_grid = getenv("QSV_TILE_GRID");  // debug: cap the persistent grid
     if (env_grid && atoi(env_grid) > 0) cap = (uint64_t)atoi(env_grid);
     const int grid = (int)(ntiles < cap ? ntiles : cap);
-    tile_block_kernel<<<grid, kT, smem, st>>>(psi, g, d_offhi, d_geo, d_blocks, nblocks, d_ops,
-                                              d_rots, d_params);
+    if (staged)
+        tile_block_kernel<true><<<grid, kT, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+    else
+        tile_block_kernel<false><<<grid, kT, smem, st>>>(psi, g, d_offhi, d_geo, prog);
     return cudaGetLastError();
 }
 
