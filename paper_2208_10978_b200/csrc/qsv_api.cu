@@ -196,7 +196,7 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     const size_t o_ops = b.add(t.ops.data(), t.ops.size() * sizeof(OpRec));
     const size_t o_rots = b.add(t.rots.data(), t.rots.size() * sizeof(RotRec));
     const size_t o_par = b.add(params.data(), params.size() * sizeof(double));
-    struct PassOff { size_t off, comp, blk, ops, rots, par; int nblk, nops, nrots, npar; };
+    struct PassOff { size_t off, comp, blk, ops, rots, par; int nblk, nops, nrots, npar; bool lite; };
     std::vector<PassOff> po(t.passes.size());
     {
         std::vector<uint64_t> offhi;
@@ -242,6 +242,11 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                 bl.op0 -= p.op_begin;
                 bl.op1 -= p.op_begin;
             }
+            o.lite = true;
+            for (const OpRec &op : lops)
+                if (op.type == OP_U2) o.lite = false;
+            for (const BlockRec &bl : lblk)
+                if (bl.kind != 0) o.lite = false;
             o.nblk = (int)lblk.size();
             o.nops = (int)lops.size();
             o.nrots = r_hi - r_lo;
@@ -276,7 +281,7 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                                         (const int32_t *)(d + o.comp), (const BlockRec *)(d + o.blk),
                                         o.nblk, (const OpRec *)(d + o.ops), o.nops,
                                         (const RotRec *)(d + o.rots), o.nrots,
-                                        (const double *)(d + o.par), o.npar, s->stream));
+                                        (const double *)(d + o.par), o.npar, o.lite, s->stream));
         } else {
             QSV_CUDA(launch_tile_pass(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
                                       (const int32_t *)(d + o.comp), d_ops + p.op_begin,

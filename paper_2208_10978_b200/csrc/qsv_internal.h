@@ -136,7 +136,7 @@ cudaError_t launch_tile_pass(double2 *psi, const TileDims &g, const uint64_t *d_
 cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                                const int32_t *d_geo, const BlockRec *d_blocks, int nblocks,
                                const OpRec *d_ops, int nops, const RotRec *d_rots, int nrots,
-                               const double *d_params, int nparams, cudaStream_t st);
+                               const double *d_params, int nparams, bool lite, cudaStream_t st);
 cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                                 const int32_t *d_comp, const GroupRec *d_groups, int ngroups,
                                 const TermRec *d_terms, int nterms, int ndiag, double *d_partial,

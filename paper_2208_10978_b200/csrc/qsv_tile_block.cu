@@ -358,16 +358,20 @@ struct PassProgram {
     int nblocks, nops, nrots, nparams;
 };
 
-template <bool STAGED>
-__global__ void __launch_bounds__(kT, 1)
+// LITE: passes without U2 / wide-flip groups -> <= 128 registers, a single
+// SMEM tile buffer, two CTAs per SM (16 warps) that overlap each other's
+// loads and compute.  Otherwise one CTA per SM with a double-buffered tile.
+template <bool STAGED, bool LITE>
+__global__ void __launch_bounds__(kT, LITE ? 2 : 1)
 tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__restrict__ g_offhi,
                   const int32_t *__restrict__ g_geo, const PassProgram prog)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int NBUF = LITE ? 1 : 2;
     const int m = g.m, c = g.c;
     const int tsize = 1 << m;
-    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);  // 2 x tsize
-    uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + 2 * tsize);
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);  // NBUF x tsize
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + NBUF * tsize);
     for (int i = threadIdx.x; i < (1 << (m - c)); i += kT) offhi[i] = __ldg(g_offhi + i);
     const BlockRec *blocks = prog.blocks;
     const OpRec *ops = prog.ops;
@@ -410,14 +414,18 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
     issue_tile_load(bufs, psi + base, offhi, tsize, c, cmask);
     cp_async_commit();
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-        double2 *sm = bufs + (it & 1) * tsize;
+        double2 *sm = bufs + (NBUF == 2 ? (it & 1) * tsize : 0);
         const uint64_t next = tile + gridDim.x;
-        if (next < ntiles) {
-            const uint64_t nb = tbase(next, lane, g.ncomp, comp_lane);
-            issue_tile_load(bufs + ((it + 1) & 1) * tsize, psi + nb, offhi, tsize, c, cmask);
+        if (NBUF == 2) {
+            if (next < ntiles) {
+                const uint64_t nb = tbase(next, lane, g.ncomp, comp_lane);
+                issue_tile_load(bufs + ((it + 1) & 1) * tsize, psi + nb, offhi, tsize, c, cmask);
+            }
+            cp_async_commit();
+            cp_async_wait<1>();  // this tile's copies have landed (the next tile's may be in flight)
+        } else {
+            cp_async_wait<0>();
         }
-        cp_async_commit();
-        cp_async_wait<1>();  // this tile's copies have landed (the next tile's may be in flight)
         __syncthreads();
         for (int bi = 0; bi < nblocks; ++bi) {
             const BlockRec *B = blocks + bi;
@@ -446,7 +454,9 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
                         const int type = w0.x, oa = w0.y, ob = w0.z;
                         switch (type) {
                             case OP_U1: dispatch_u1(oa, a, params + w1.z); break;
-                            case OP_U2: dispatch_pair<W_u2>(oa, ob, a, params + w1.z); break;
+                            case OP_U2:
+                                if (!LITE) dispatch_pair<W_u2>(oa, ob, a, params + w1.z);
+                                break;
                             case OP_DIAG1: {
                                 const double *P = params + w1.z;
                                 const double2 d0 = ld2(P), d1 = ld2(P + 2);
@@ -484,7 +494,7 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
                         sm[sb ^ o] = a[r];
                     }
                 }
-            } else {
+            } else if (!LITE) {
                 uint16_t cols[12];
 #pragma unroll
                 for (int b = 0; b < 12; ++b) cols[b] = B->cols[b];
@@ -508,7 +518,13 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
             __stcs(dst + (tid & cmask) + offhi[tid >> c], sm[st_base]);
         }
         __syncthreads();
-        if (next < ntiles) base = tbase(next, lane, g.ncomp, comp_lane);
+        if (next < ntiles) {
+            base = tbase(next, lane, g.ncomp, comp_lane);
+            if (NBUF == 1) {  // single buffer: the next tile's load starts after the store
+                issue_tile_load(bufs, psi + base, offhi, tsize, c, cmask);
+                cp_async_commit();
+            }
+        }
     }
     cp_async_wait<0>();
 }
@@ -518,37 +534,51 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
 cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                                const int32_t *d_geo, const BlockRec *d_blocks, int nblocks,
                                const OpRec *d_ops, int nops, const RotRec *d_rots, int nrots,
-                               const double *d_params, int nparams, cudaStream_t st)
+                               const double *d_params, int nparams, bool lite, cudaStream_t st)
 {
     static bool configured = false;
     const int max_smem = 227 * 1024;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tile_block_kernel<true>,
+        cudaError_t e = cudaFuncSetAttribute(tile_block_kernel<true, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(tile_block_kernel<false>,
+        e = cudaFuncSetAttribute(tile_block_kernel<false, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(tile_block_kernel<true, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t nhi = (size_t)1 << (g.m - g.c);
-    const size_t base_smem = ((size_t)32 << g.m) + 8 * (nhi + (nhi & 1));
     const size_t prog_bytes = 8 * (size_t)((nparams + 1) & ~1) + sizeof(RotRec) * nrots +
                               sizeof(OpRec) * nops + sizeof(BlockRec) * nblocks;
-    const bool staged = base_smem + prog_bytes <= (size_t)max_smem;
-    const size_t smem = staged ? base_smem + prog_bytes : base_smem;
+    const size_t lite_base = ((size_t)16 << g.m) + 8 * (nhi + (nhi & 1));
+    const size_t full_base = ((size_t)32 << g.m) + 8 * (nhi + (nhi & 1));
     PassProgram prog{d_blocks, d_ops, d_rots, d_params, nblocks, nops, nrots, nparams};
     const uint64_t ntiles = 1ull << g.ncomp;
-    uint64_t cap = (uint64_t)num_sms(dev);  // one persistent CTA per SM
     static const char *env_grid = getenv("QSV_TILE_GRID");  // debug: cap the persistent grid
-    if (env_grid && atoi(env_grid) > 0) cap = (uint64_t)atoi(env_grid);
-    const int grid = (int)(ntiles < cap ? ntiles : cap);
+    auto grid_for = [&](int per_sm) {
+        uint64_t cap = (uint64_t)num_sms(dev) * (per_sm > 0 ? per_sm : 1);
+        if (env_grid && atoi(env_grid) > 0) cap = (uint64_t)atoi(env_grid);
+        return (int)(ntiles < cap ? ntiles : cap);
+    };
+    // two CTAs per SM need <= ~113 KB each: single tile buffer + staged program
+    if (lite && lite_base + prog_bytes <= (size_t)112 * 1024) {
+        const size_t smem = lite_base + prog_bytes;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_block_kernel<true, true>, kT, smem);
+        tile_block_kernel<true, true><<<grid_for(per_sm), kT, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+        return cudaGetLastError();
+    }
+    const bool staged = full_base + prog_bytes <= (size_t)max_smem;
+    const size_t smem = staged ? full_base + prog_bytes : full_base;
     if (staged)
-        tile_block_kernel<true><<<grid, kT, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+        tile_block_kernel<true, false><<<grid_for(1), kT, smem, st>>>(psi, g, d_offhi, d_geo, prog);
     else
-        tile_block_kernel<false><<<grid, kT, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+        tile_block_kernel<false, false><<<grid_for(1), kT, smem, st>>>(psi, g, d_offhi, d_geo, prog);
     return cudaGetLastError();
 }
 
