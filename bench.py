@@ -15,8 +15,13 @@ pinned host memory) inside the timed region.  roofline = the dominant kernel
 duration (CUDA events on the library's stream), vs MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline = the reference (oracle/_ref: vqekit + Cython kernels, 1 thread --
 the reference evolve is single-threaded) on a bounded sample of the same
-circuit.  For N > 1 each rank runs an independent replica (the sharded 36q
-path is config 5, not this line): scaling "weak".
+circuit.
+
+For N > 1 (torchrun, one rank per GPU, NCCL) the line measures the SHARDED
+engine (distributed.py): the same brickwork family on n = 28 + log2(N)
+qubits, so every GPU holds 2^28 amplitudes (weak scaling, SURVEY.md 8(e));
+gates on the top log2(N) (global) qubits trigger batched qubit-swap
+relayouts over NCCL.  value = total amplitude-updates/s of the whole job.
 """
 
 from __future__ import annotations
@@ -395,6 +400,105 @@ def run_engine(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def run_engine_dist(args, rank, world, local):
+    """Sharded brickwork, weak scaling: 2^28 amplitudes per GPU."""
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2208_10978_b200 import _lib
+    from paper_2208_10978_b200 import distributed as D
+    from paper_2208_10978_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    g = world.bit_length() - 1
+    n = N_QUBITS + g
+    circ = W.brickwork(n, LAYERS, SEED)
+    G = len(circ.gates)
+    comm = D.ProcessGroupComm()
+    be = D.DistributedBackend(comm, D.CudaEngine(local))
+
+    def step():
+        return be.evolve(be.prepare("0" * n), circ)
+
+    for _ in range(args.warmup):
+        psi = step()
+        del psi
+    torch.cuda.synchronize(local)
+    stats0 = None
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    with ClockSampler(local) as clocks:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        relayout_s = 0.0
+        relayouts = 0
+        sent = 0
+        for _ in range(args.steps):
+            psi = step()
+            for sh in psi.shards.values():
+                sh.synchronize()
+            relayout_s += psi.stats["relayout_seconds"]
+            relayouts += psi.stats["relayouts"]
+            sent += psi.stats["relayout_bytes_sent"]
+            del psi
+        end.record()
+        torch.cuda.synchronize(local)
+    t_step = start.elapsed_time(end) / 1e3 / args.steps
+    tt = torch.tensor([t_step, relayout_s / args.steps], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max, t_swap = float(tt[0].item()), float(tt[1].item())
+    value = G * (1 << n) / t_max
+
+    # e2e: public API, gate arrays in, every rank's shard out to pinned host memory
+    n_local = n - g
+    host_out = torch.empty(1 << n_local, dtype=torch.complex128, pin_memory=True).numpy()
+    e2e_steps = max(1, min(args.steps, 2))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        psi = step()
+        for sh in psi.shards.values():
+            sh.download_into(host_out)
+        del psi
+    t_e2e = time.perf_counter() - t0
+    te = torch.tensor([t_e2e / e2e_steps], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te.item())
+
+    peak, peak_kind = load_peaks()
+    passes = None
+    if rank == 0:
+        line = {
+            "metric": "amplitude-updates/s", "value": value, "unit": "amplitude-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": f"config2/5 family: {n}q random brickwork depth {LAYERS} "
+                                   f"({G} gates), seed {SEED}, sharded over {world} GPUs "
+                                   f"(2^{n_local} amplitudes per GPU, {g} global qubits)",
+                       "n_qubits": n, "gates": G, "parallelism": f"state sharded x{world} (global qubits)",
+                       "l2": "shard 4 GiB >> 126 MB L2 (no flush needed)"},
+            "e2e": {"value": G * (1 << n) / t_e2e, "unit": "amplitude-updates/s",
+                    "h2d_bytes_per_step": int(G * 24),
+                    "d2h_bytes_per_step": int(16 * (1 << n)), "ms_per_step": t_e2e * 1e3},
+            "swap": {"relayouts_per_step": relayouts / args.steps,
+                     "bytes_sent_per_gpu_per_step": sent / args.steps,
+                     "seconds_per_step": t_swap,
+                     "GB_per_s": (sent / args.steps) / max(t_swap, 1e-12) / 1e9,
+                     "nvlink_frac": (sent / args.steps) / max(t_swap, 1e-12) / 900e9},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
+                         "frac": None, "traffic": None, "kernel": "tile pass (see N=1 line)",
+                         "peak_source": peak_kind},
+            "gpu_launches": None,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -413,7 +517,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    run_engine(args, rank, world, local)
+    if world > 1:
+        run_engine_dist(args, rank, world, local)
+    else:
+        run_engine(args, rank, world, local)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -512,10 +512,8 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
         if (g_cache.size() > kCacheMax) g_cache.pop_back();
         tpl = &g_cache.front().tpl;
     }
-    materialize_gates(*tpl, values);
     std::vector<double> params(tpl->n_params);
-    for (const ParamFill &f : tpl->fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, &params[f.offset]);
-    materialize_gmats(*tpl, params.data());
+    materialize_params(*tpl, values, params.data());
     fill_stats(*tpl, hit, stats);
     return run_template(s, *tpl, params);
 }
@@ -861,10 +859,8 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     if (int rc = validate_gates(&fake, n_gates, kinds, qubits)) return rc;
     ProgramTemplate t;
     plan_gates(n, n_gates, kinds, qubits, t);
-    materialize_gates(t, values);
     std::vector<double> params(t.n_params);
-    for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, &params[f.offset]);
-    materialize_gmats(t, params.data());
+    materialize_params(t, values, params.data());
     std::string j = "{\"n\":" + std::to_string(n) + ",\"block_bits\":" +
                     std::to_string(kBlockBits) + ",\"passes\":[";
     char buf[256];

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <unordered_map>
 
 namespace qsv {
@@ -88,6 +89,7 @@ struct Item {
     uint64_t supp = 0;        // all touched qubits
     uint64_t req = 0;         // qubits that must be tile-local
     uint64_t a_union = 0, b_union = 0;
+    int cluster = -1;         // dense-fused gate cluster (index into ProgramTemplate::cfills)
 };
 
 bool conflict(const Item &A, const Item &B, const std::vector<Rot> &R)
@@ -252,6 +254,208 @@ int param_count(int kind)
     }
 }
 
+// FP64 work of a gate in complex multiply-adds per amplitude: dense 2x2 = 2,
+// diagonal = 1, permutation = 0 (folded into the tile map), dense 4x4 = 4.
+int gate_cost(int kind)
+{
+    switch (kind) {
+        case K_X: case K_CNOT: case K_SWAP: return 0;
+        case K_RZ: return 1;
+        case K_CU3: return 4;
+        default: return 2;
+    }
+}
+
+// Dense gate fusion (north star (1), k <= 2): walk the items in order and
+// grow clusters of consecutive gates confined to <= 2 qubits.  A gate joins
+// the open clusters on its qubits when their union stays within 2 qubits;
+// otherwise the clusters that would widen it are closed (emitted) first.
+// A closed cluster becomes one dense 2x2 / 4x4 item when that is cheaper than
+// its gates (e.g. U3 U3 CNOT U3 U3: 8 -> 4 complex FMAs per amplitude).
+// Emitting at close time is order-safe: everything emitted while a cluster is
+// open acts on disjoint qubits and commutes with it.
+void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t *qubits,
+                   ProgramTemplate &t)
+{
+    struct Open {
+        std::vector<int> gates;
+        uint64_t qs = 0;
+        int cost = 0;
+        bool live = false;
+    };
+    std::vector<Open> cl;
+    static const char *env_fuse = getenv("QSV_FUSE_QUBITS");  // 0 / 1 / 2 (default 2)
+    const int max_q = env_fuse ? std::max(0, std::min(2, atoi(env_fuse))) : 2;
+    int open_of[kMaxQubits];
+    for (int q = 0; q < kMaxQubits; ++q) open_of[q] = -1;
+    std::vector<Item> out;
+    out.reserve(items.size());
+    auto gate_item = [&](int gi) {
+        Item it;
+        it.gate = gi;
+        uint64_t s = 1ull << qubits[2 * gi];
+        if (qubits[2 * gi + 1] >= 0) s |= 1ull << qubits[2 * gi + 1];
+        it.supp = s;
+        it.req = s;
+        return it;
+    };
+    auto close = [&](int ci) {
+        Open &C = cl[ci];
+        if (!C.live) return;
+        C.live = false;
+        for (int q = 0; q < kMaxQubits; ++q)
+            if (((C.qs >> q) & 1ull) && open_of[q] == ci) open_of[q] = -1;
+        const int nq = popc64(C.qs);
+        const int fused_cost = nq == 2 ? 4 : 2;
+        if (C.gates.size() >= 2 && C.cost > fused_cost) {
+            ClusterFill cf;
+            cf.offset = -1;
+            cf.qa = 63 - __builtin_clzll(C.qs);
+            cf.qb = nq == 2 ? __builtin_ctzll(C.qs) : -1;
+            cf.gates = C.gates;
+            t.n_fused_gates += (int64_t)C.gates.size();
+            Item it;
+            it.cluster = (int)t.cfills.size();
+            it.supp = C.qs;
+            it.req = C.qs;
+            t.cfills.push_back(std::move(cf));
+            out.push_back(std::move(it));
+        } else {
+            for (int gi : C.gates) out.push_back(gate_item(gi));
+        }
+    };
+    auto close_touching = [&](uint64_t mask) {
+        // close in creation order (deterministic)
+        int ids[kMaxQubits], k = 0;
+        for (int q = 0; q < kMaxQubits; ++q)
+            if (((mask >> q) & 1ull) && open_of[q] >= 0) {
+                bool dup = false;
+                for (int j = 0; j < k; ++j) dup |= ids[j] == open_of[q];
+                if (!dup) ids[k++] = open_of[q];
+            }
+        std::sort(ids, ids + k);
+        for (int j = 0; j < k; ++j) close(ids[j]);
+    };
+    for (Item &it : items) {
+        if (it.rot || it.gate < 0 || popc64(it.supp) > max_q) {
+            close_touching(it.supp);
+            out.push_back(std::move(it));
+            continue;
+        }
+        const int gi = it.gate;
+        const uint64_t Q = it.supp;
+        // clusters on Q that carry a qubit outside Q cannot absorb a 2q gate
+        int ids[2], k = 0;
+        for (int q = 0; q < kMaxQubits; ++q)
+            if (((Q >> q) & 1ull) && open_of[q] >= 0 && (k == 0 || ids[0] != open_of[q])) ids[k++] = open_of[q];
+        uint64_t uni = Q;
+        for (int j = 0; j < k; ++j) uni |= cl[ids[j]].qs;
+        if (popc64(uni) > max_q) {
+            for (int j = 0; j < k; ++j)
+                if (cl[ids[j]].qs & ~Q) close(ids[j]);
+            int kk = 0;
+            for (int j = 0; j < k; ++j)
+                if (cl[ids[j]].live) ids[kk++] = ids[j];
+            k = kk;
+        }
+        int target;
+        if (k == 0) {
+            cl.emplace_back();
+            target = (int)cl.size() - 1;
+            cl[target].live = true;
+        } else {
+            target = std::min(ids[0], k > 1 ? ids[1] : ids[0]);
+            if (k == 2) {  // merge the other (disjoint qubits: the two commute)
+                const int other = ids[0] == target ? ids[1] : ids[0];
+                Open &O = cl[other];
+                cl[target].gates.insert(cl[target].gates.end(), O.gates.begin(), O.gates.end());
+                cl[target].qs |= O.qs;
+                cl[target].cost += O.cost;
+                O.live = false;
+                O.gates.clear();
+            }
+        }
+        Open &T = cl[target];
+        T.gates.push_back(gi);
+        T.qs |= Q;
+        T.cost += gate_cost(kinds[gi]);
+        for (int q = 0; q < kMaxQubits; ++q)
+            if ((T.qs >> q) & 1ull) open_of[q] = target;
+    }
+    for (size_t ci = 0; ci < cl.size(); ++ci) close((int)ci);
+    items.swap(out);
+}
+
+// Fixed 2x2 / 4x4 matrices of the permutation gates (circuit.py:36-45).
+void perm_matrix(int kind, double *o)
+{
+    const int n = kind == K_X ? 2 : 4;
+    for (int i = 0; i < 2 * n * n; ++i) o[i] = 0.0;
+    auto one = [&](int r, int c) { o[2 * (r * n + c)] = 1.0; };
+    if (kind == K_X) { one(0, 1); one(1, 0); }
+    else if (kind == K_CNOT) { one(0, 0); one(1, 1); one(2, 3); one(3, 2); }
+    else { one(0, 0); one(1, 2); one(2, 1); one(3, 3); }
+}
+
+void cluster_matrix(const ClusterFill &cf, const int32_t *kinds, const int32_t *qubits,
+                    const double *values, double *out)
+{
+    const int n = cf.qb >= 0 ? 4 : 2;
+    double M[32], G[32], N[32], g[32];
+    for (int i = 0; i < 2 * n * n; ++i) M[i] = 0.0;
+    for (int i = 0; i < n; ++i) M[2 * (i * n + i)] = 1.0;
+    for (int gi : cf.gates) {
+        const int kind = kinds[gi];
+        const int q0 = qubits[2 * gi], q1 = qubits[2 * gi + 1];
+        if (kind == K_X || kind == K_CNOT || kind == K_SWAP) perm_matrix(kind, g);
+        else gate_matrix(kind, values + 3 * (size_t)gi, g);
+        if (kind == K_RZ) {  // diag(d0, d1) -> dense 2x2
+            const double d0r = g[0], d0i = g[1], d1r = g[2], d1i = g[3];
+            for (int i = 0; i < 8; ++i) g[i] = 0.0;
+            g[0] = d0r; g[1] = d0i; g[6] = d1r; g[7] = d1i;
+        }
+        for (int i = 0; i < 2 * n * n; ++i) G[i] = 0.0;
+        const bool two = q1 >= 0;
+        if (n == 2) {
+            for (int i = 0; i < 8; ++i) G[i] = g[i];
+        } else if (!two) {
+            // 1q gate on qa (MSB, bit 1 of the 4x4 index) or qb (bit 0)
+            const int sh = q0 == cf.qa ? 1 : 0;
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) {
+                    const int other = 1 - sh;
+                    if (((r >> other) & 1) != ((c >> other) & 1)) continue;
+                    const int rr = (r >> sh) & 1, cc = (c >> sh) & 1;
+                    G[2 * (r * 4 + c)] = g[2 * (rr * 2 + cc)];
+                    G[2 * (r * 4 + c) + 1] = g[2 * (rr * 2 + cc) + 1];
+                }
+        } else {
+            // 4x4 in (bit q0, bit q1) order; re-index to (bit qa, bit qb)
+            const bool same = q0 == cf.qa;
+            auto idx = [&](int r) { return same ? r : ((r & 1) << 1) | (r >> 1); };
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) {
+                    G[2 * (r * 4 + c)] = g[2 * (idx(r) * 4 + idx(c))];
+                    G[2 * (r * 4 + c) + 1] = g[2 * (idx(r) * 4 + idx(c)) + 1];
+                }
+        }
+        for (int r = 0; r < n; ++r)
+            for (int c = 0; c < n; ++c) {
+                double re = 0, im = 0;
+                for (int l = 0; l < n; ++l) {
+                    const double ar = G[2 * (r * n + l)], ai = G[2 * (r * n + l) + 1];
+                    const double br = M[2 * (l * n + c)], bi = M[2 * (l * n + c) + 1];
+                    re += ar * br - ai * bi;
+                    im += ar * bi + ai * br;
+                }
+                N[2 * (r * n + c)] = re;
+                N[2 * (r * n + c) + 1] = im;
+            }
+        for (int i = 0; i < 2 * n * n; ++i) M[i] = N[i];
+    }
+    for (int i = 0; i < 2 * n * n; ++i) out[i] = M[i];
+}
+
 void block_pass(ProgramTemplate &t, PassPlan &pp);
 
 void emit_program(int n, int m, int c, const std::vector<Item> &items, const std::vector<Rot> &R,
@@ -320,6 +524,14 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
                     op.f = compress(a, g);
                     op.h = highest_bit(op.f);
                 }
+            } else if (it.cluster >= 0) {
+                ClusterFill &cf = t.cfills[it.cluster];
+                op.a = local_of(g, cf.qa);
+                op.b = cf.qb >= 0 ? local_of(g, cf.qb) : -1;
+                op.type = cf.qb >= 0 ? OP_U2 : OP_U1;
+                op.p = (int)t.n_params;
+                cf.offset = (int)t.n_params;
+                t.n_params += cf.qb >= 0 ? 32 : 8;
             } else {
                 const int gi = it.gate, kind = kinds[gi];
                 const int a = local_of(g, qubits[2 * gi]);
@@ -690,9 +902,12 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
             ++i;
         }
     }
+    fuse_clusters(items, kinds, qubits, t);
     Schedule S = schedule(items, R, n, m, c);
     emit_program(n, m, c, items, R, kinds, qubits, S, t);
     t.n_input = N;
+    t.src_kinds.assign(kinds, kinds + N);
+    t.src_qubits.assign(qubits, qubits + 2 * N);
     t.n_rotations = (int64_t)R.size();
 }
 
@@ -716,6 +931,16 @@ void materialize_gates(ProgramTemplate &t, const double *values)
         t.rots[r].c = std::cos(0.5 * th);
         t.rots[r].s = std::sin(0.5 * th);
     }
+}
+
+void materialize_params(ProgramTemplate &t, const double *values, double *params)
+{
+    materialize_gates(t, values);
+    for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, params + f.offset);
+    for (const ClusterFill &cf : t.cfills)
+        if (cf.offset >= 0)
+            cluster_matrix(cf, t.src_kinds.data(), t.src_qubits.data(), values, params + cf.offset);
+    materialize_gmats(t, params);
 }
 
 void materialize_rotations(ProgramTemplate &t, const double *theta)

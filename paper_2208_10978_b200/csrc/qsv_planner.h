@@ -57,6 +57,15 @@ struct GmatFill {
     std::vector<uint8_t> yF;  // block-local Y bits of each rotation
 };
 
+// A dense-fused gate cluster: a run of gates confined to <= 2 qubits whose
+// product is applied as one 2x2 (qb < 0) or 4x4 (rows = 2*bit(qa) + bit(qb))
+// matrix, recomputed from the bound values on every call.
+struct ClusterFill {
+    int offset;               // params offset of the fused matrix
+    int qa, qb;               // physical qubits (qb = -1: single-qubit cluster)
+    std::vector<int> gates;   // source gate indices, in application order
+};
+
 struct ProgramTemplate {
     int n = 0, m = 0, c = 0;
     std::vector<PassPlan> passes;
@@ -66,9 +75,12 @@ struct ProgramTemplate {
     std::vector<int> rot_src;      // theta source index per RotRec
     std::vector<ParamFill> fills;  // matrices refreshed per call
     std::vector<GmatFill> gfills;  // fused group tables refreshed per call
+    std::vector<ClusterFill> cfills;  // dense-fused gate clusters refreshed per call
     size_t n_params = 0;
     // global-fallback rotation records (full 64-bit masks), per pass: rots[r0..r1)
     int64_t n_input = 0, n_rotations = 0, n_items = 0, n_fallback = 0, n_blocks = 0;
+    int64_t n_fused_gates = 0;  // gates absorbed into dense clusters
+    std::vector<int32_t> src_kinds, src_qubits;  // the gate list (cluster materialisation)
 };
 
 struct Rot {
@@ -86,6 +98,10 @@ void materialize_gates(ProgramTemplate &t, const double *values);
 void materialize_rotations(ProgramTemplate &t, const double *theta);
 // Fused group tables (after rots[].c/s are refreshed) into params.
 void materialize_gmats(const ProgramTemplate &t, double *params);
+// Every angle-dependent parameter of a gate-list template (gate matrices,
+// fused cluster matrices, fused group tables) into params[t.n_params];
+// refreshes t.rots first.
+void materialize_params(ProgramTemplate &t, const double *values, double *params);
 // Gate matrix restatement of circuit.py:198-223 (row-major complex128).
 int gate_matrix(int kind, const double *v, double *out);
 

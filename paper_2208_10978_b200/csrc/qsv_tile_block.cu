@@ -86,23 +86,20 @@ __device__ __forceinline__ void r_u1(double2 (&a)[kR], const double *P)
 template <int JA, int JB>
 __device__ __forceinline__ void r_u2(double2 (&a)[kR], const double *P)
 {
+    // quad by quad; only the four inputs are copied, each output row goes
+    // straight back into a[], matrix rows re-read from SMEM (broadcast LDS)
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
         if (r & ((1 << JA) | (1 << JB))) continue;
         const int i00 = r, i01 = r | (1 << JB), i10 = r | (1 << JA), i11 = r | (1 << JA) | (1 << JB);
         const double2 x0 = a[i00], x1 = a[i01], x2 = a[i10], x3 = a[i11];
-        double2 o[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const double *R = P + 8 * k;
             const double2 p = cfma2(ld2v(R), x0, ld2v(R + 2), x1);
             const double2 q = cfma2(ld2v(R + 4), x2, ld2v(R + 6), x3);
-            o[k] = make_double2(p.x + q.x, p.y + q.y);
+            a[k == 0 ? i00 : k == 1 ? i01 : k == 2 ? i10 : i11] = make_double2(p.x + q.x, p.y + q.y);
         }
-        a[i00] = o[0];
-        a[i01] = o[1];
-        a[i10] = o[2];
-        a[i11] = o[3];
     }
 }
 
@@ -301,10 +298,10 @@ __device__ __forceinline__ uint32_t map_slot(uint32_t l, int m, uint32_t tswz, c
 
 // Wide-flip rotation group (flip with more than 4 in-tile bits) straight on SMEM.
 __device__ void smem_rotg(double2 *sm, int m, uint32_t f, int h, const RotRec *rots, int r0,
-                          int r1, uint64_t base, uint32_t tswz, const uint16_t *cols)
+                          int r1, uint64_t base, uint32_t tswz, const uint16_t *cols, uint32_t tid)
 {
     const int npairs = 1 << (m - 1);
-    for (int i = threadIdx.x; i < npairs; i += kT) {
+    for (int i = tid; i < npairs; i += kT) {
         const uint32_t l0 = ins0(i, h), l1 = l0 ^ f;
         const uint32_t p0 = map_slot(l0, m, tswz, cols), p1 = map_slot(l1, m, tswz, cols);
         double2 a0 = sm[p0], a1 = sm[p1];
@@ -341,6 +338,103 @@ __device__ __forceinline__ void issue_tile_load(double2 *buf, const double2 *src
 {
 #pragma unroll 4
     for (int l = threadIdx.x; l < tsize; l += kT) cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
+}
+
+// Consumer barrier: BAR = 0 -> whole CTA; otherwise named barrier BAR over
+// the kT compute threads (warp-specialised kernel).
+template <int BAR>
+__device__ __forceinline__ void block_sync(int bar_id)
+{
+    if (BAR == 0) __syncthreads();
+    else if (BAR > 0) asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(kT) : "memory");
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kT) : "memory");
+}
+
+// Run a pass's register blocks on one SMEM tile (all kT compute threads).
+template <bool LITE, int BAR>
+__device__ __forceinline__ void run_blocks(double2 *sm, const BlockRec *blocks, int nblocks,
+                                           const OpRec *ops, const RotRec *rots,
+                                           const double *params, uint64_t base, uint32_t tid, int m,
+                                           int bar_id = 0)
+{
+    const int ncos = (1 << m) >> kRB;  // cosets per block (m >= 4)
+    const int tbits = m - kRB;         // thread-index bits of a block
+    for (int bi = 0; bi < nblocks; ++bi) {
+        const BlockRec *B = blocks + bi;
+        const int kind = B->kind;
+        const int op0 = B->op0, op1 = B->op1;
+        if (kind == 0) {
+            if ((int)tid < ncos) {
+                uint32_t sb = B->tswz;
+                for (int i = 0; i < tbits; ++i)
+                    if ((tid >> i) & 1u) sb ^= B->cols[i];
+                uint32_t e[kRB];
+#pragma unroll
+                for (int j = 0; j < kRB; ++j) e[j] = B->cols[kTB + j];
+                double2 a[kR];
+#pragma unroll
+                for (int r = 0; r < kR; ++r) {
+                    uint32_t o = 0;
+#pragma unroll
+                    for (int j = 0; j < kRB; ++j) o ^= ((r >> j) & 1) ? e[j] : 0u;
+                    a[r] = sm[sb ^ o];
+                }
+#pragma unroll 1
+                for (int k = op0; k < op1; ++k) {
+                    const int4 w0 = reinterpret_cast<const int4 *>(ops + k)[0];
+                    const int4 w1 = reinterpret_cast<const int4 *>(ops + k)[1];
+                    const int type = w0.x, oa = w0.y, ob = w0.z;
+                    switch (type) {
+                        case OP_U1: dispatch_u1(oa, a, params + w1.z); break;
+                        case OP_U2:
+                            if (!LITE) dispatch_pair<W_u2>(oa, ob, a, params + w1.z);
+                            break;
+                        case OP_DIAG1: {
+                            const double *P = params + w1.z;
+                            const double2 d0 = ld2(P), d1 = ld2(P + 2);
+                            if (oa >= 0) {
+                                switch (oa) {
+                                    case 0: r_diag_in<0>(a, d0, d1); break;
+                                    case 1: r_diag_in<1>(a, d0, d1); break;
+#if QSV_BLOCK_BITS > 3
+                                    case 2: r_diag_in<2>(a, d0, d1); break;
+                                    default: r_diag_in<3>(a, d0, d1); break;
+#else
+                                    default: r_diag_in<2>(a, d0, d1); break;
+#endif
+                                }
+                            } else {
+                                const double2 d = ((tid >> ob) & 1u) ? d1 : d0;
+#pragma unroll
+                                for (int r = 0; r < kR; ++r) a[r] = cmulc(d, a[r]);
+                            }
+                            break;
+                        }
+                        case OP_ROTG: dispatch_rotg(w1.w, a, rots, w1.x, w1.y, base, tid); break;
+                        case OP_ROTD: r_rotd(a, rots, w1.x, w1.y, base, tid); break;
+                        case OP_GMAT:
+                            dispatch_gmat(w1.w, a, params + w1.z, rots + w1.x, base, tid);
+                            break;
+                        default: break;
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < kR; ++r) {
+                    uint32_t o = 0;
+#pragma unroll
+                    for (int j = 0; j < kRB; ++j) o ^= ((r >> j) & 1) ? e[j] : 0u;
+                    sm[sb ^ o] = a[r];
+                }
+            }
+        } else if (!LITE) {
+            uint16_t cols[12];
+#pragma unroll
+            for (int b = 0; b < 12; ++b) cols[b] = B->cols[b];
+            smem_rotg(sm, m, ops[op0].f, ops[op0].h, rots, ops[op0].r0, ops[op0].r1, base,
+                      B->tswz, cols, tid);
+        }
+        block_sync<BAR>(bar_id);
+    }
 }
 
 // Persistent CTA (one per SM): double-buffered tiles -- while the register
@@ -400,8 +494,6 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
     const int lane = tid & 31;
     const int comp_lane = __ldg(g_geo + lane);
     const uint32_t cmask = (1u << c) - 1u;
-    const int ncos = tsize >> kRB;  // cosets per block (m >= 4)
-    const int tbits = m - kRB;      // thread-index bits of a block
     // store map: slot of logical l = tid + k*kT
     uint32_t st_base = (uint32_t)__ldg(g_geo + 44);
     for (int i = 0; i < kTB && i < m; ++i)
@@ -427,82 +519,7 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
             cp_async_wait<0>();
         }
         __syncthreads();
-        for (int bi = 0; bi < nblocks; ++bi) {
-            const BlockRec *B = blocks + bi;
-            const int kind = B->kind;
-            const int op0 = B->op0, op1 = B->op1;
-            if (kind == 0) {
-                if ((int)tid < ncos) {
-                    uint32_t sb = B->tswz;
-                    for (int i = 0; i < tbits; ++i)
-                        if ((tid >> i) & 1u) sb ^= B->cols[i];
-                    uint32_t e[kRB];
-#pragma unroll
-                    for (int j = 0; j < kRB; ++j) e[j] = B->cols[kTB + j];
-                    double2 a[kR];
-#pragma unroll
-                    for (int r = 0; r < kR; ++r) {
-                        uint32_t o = 0;
-#pragma unroll
-                        for (int j = 0; j < kRB; ++j) o ^= ((r >> j) & 1) ? e[j] : 0u;
-                        a[r] = sm[sb ^ o];
-                    }
-#pragma unroll 1
-                    for (int k = op0; k < op1; ++k) {
-                        const int4 w0 = reinterpret_cast<const int4 *>(ops + k)[0];
-                        const int4 w1 = reinterpret_cast<const int4 *>(ops + k)[1];
-                        const int type = w0.x, oa = w0.y, ob = w0.z;
-                        switch (type) {
-                            case OP_U1: dispatch_u1(oa, a, params + w1.z); break;
-                            case OP_U2:
-                                if (!LITE) dispatch_pair<W_u2>(oa, ob, a, params + w1.z);
-                                break;
-                            case OP_DIAG1: {
-                                const double *P = params + w1.z;
-                                const double2 d0 = ld2(P), d1 = ld2(P + 2);
-                                if (oa >= 0) {
-                                    switch (oa) {
-                                        case 0: r_diag_in<0>(a, d0, d1); break;
-                                        case 1: r_diag_in<1>(a, d0, d1); break;
-#if QSV_BLOCK_BITS > 3
-                                        case 2: r_diag_in<2>(a, d0, d1); break;
-                                        default: r_diag_in<3>(a, d0, d1); break;
-#else
-                                        default: r_diag_in<2>(a, d0, d1); break;
-#endif
-                                    }
-                                } else {
-                                    const double2 d = ((tid >> ob) & 1u) ? d1 : d0;
-#pragma unroll
-                                    for (int r = 0; r < kR; ++r) a[r] = cmulc(d, a[r]);
-                                }
-                                break;
-                            }
-                            case OP_ROTG: dispatch_rotg(w1.w, a, rots, w1.x, w1.y, base, tid); break;
-                            case OP_ROTD: r_rotd(a, rots, w1.x, w1.y, base, tid); break;
-                            case OP_GMAT:
-                                dispatch_gmat(w1.w, a, params + w1.z, rots + w1.x, base, tid);
-                                break;
-                            default: break;
-                        }
-                    }
-#pragma unroll
-                    for (int r = 0; r < kR; ++r) {
-                        uint32_t o = 0;
-#pragma unroll
-                        for (int j = 0; j < kRB; ++j) o ^= ((r >> j) & 1) ? e[j] : 0u;
-                        sm[sb ^ o] = a[r];
-                    }
-                }
-            } else if (!LITE) {
-                uint16_t cols[12];
-#pragma unroll
-                for (int b = 0; b < 12; ++b) cols[b] = B->cols[b];
-                smem_rotg(sm, m, ops[op0].f, ops[op0].h, rots, ops[op0].r0, ops[op0].r1, base,
-                          B->tswz, cols);
-            }
-            __syncthreads();
-        }
+        run_blocks<LITE, 0>(sm, blocks, nblocks, ops, rots, params, base, tid, m);
         // ---- store through the pass's final map (streaming STG) ----
         double2 *dst = psi + base;
         if (tsize >= kT) {
@@ -529,6 +546,286 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
     cp_async_wait<0>();
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-specialised full-tile pass (m = 12): one persistent CTA per SM with a
+// 3-stage ring of 64 KiB SMEM tiles.  Warps 0-7 (kT threads) run the register
+// blocks; warps 8-11 (kIo threads) stream tiles in with LDGSTS and out with
+// streaming STG.  While the compute warps work on tile i, the I/O warps load
+// tile i+1 and write back tile i-1, so HBM traffic overlaps the FP64 work
+// instead of alternating with it.  Hand-off by mbarriers:
+//   full[s]     -- cp.async completion of every I/O thread (noinc arrive)
+//   computed[s] -- every compute thread finished its last block on stage s
+// The I/O warps order "store tile i-3 from stage s" before "load tile i into
+// stage s" with a named barrier among themselves.
+constexpr int kIo = 128;
+constexpr int kStages = 3;
+constexpr int kWsThreads = kT + kIo;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "QSV_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra QSV_WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *b)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void io_sync()
+{
+    asm volatile("bar.sync 2, %0;" ::"n"(kIo) : "memory");
+}
+
+template <bool STAGED>
+__global__ void __launch_bounds__(kWsThreads, 1)
+tile_ws_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__restrict__ g_offhi,
+               const int32_t *__restrict__ g_geo, const PassProgram prog)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int m = kMaxTileBits;
+    constexpr int tsize = 1 << m;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);  // [kStages]
+    uint64_t *computed = full + kStages;                      // [kStages]
+    uint32_t *st_k = reinterpret_cast<uint32_t *>(computed + kStages);  // [32]
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);        // kStages x tsize
+    const int c = g.c;
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + kStages * tsize);
+    const int nhi = 1 << (m - c);
+    const uint32_t tid = threadIdx.x;
+    for (int i = tid; i < nhi; i += kWsThreads) offhi[i] = __ldg(g_offhi + i);
+    const BlockRec *blocks = prog.blocks;
+    const OpRec *ops = prog.ops;
+    const RotRec *rots = prog.rots;
+    const double *params = prog.params;
+    if (STAGED) {
+        double *sp = reinterpret_cast<double *>(offhi + nhi + (nhi & 1));
+        RotRec *sr = reinterpret_cast<RotRec *>(sp + ((prog.nparams + 1) & ~1));
+        OpRec *so = reinterpret_cast<OpRec *>(sr + prog.nrots);
+        BlockRec *sb = reinterpret_cast<BlockRec *>(so + prog.nops);
+        for (int i = tid; i < prog.nparams; i += kWsThreads) sp[i] = __ldg(prog.params + i);
+        const int4 *gs = reinterpret_cast<const int4 *>(prog.rots);
+        for (int i = tid; i < prog.nrots * 2; i += kWsThreads) reinterpret_cast<int4 *>(sr)[i] = __ldg(gs + i);
+        gs = reinterpret_cast<const int4 *>(prog.ops);
+        for (int i = tid; i < prog.nops * 2; i += kWsThreads) reinterpret_cast<int4 *>(so)[i] = __ldg(gs + i);
+        gs = reinterpret_cast<const int4 *>(prog.blocks);
+        for (int i = tid; i < prog.nblocks * 3; i += kWsThreads) reinterpret_cast<int4 *>(sb)[i] = __ldg(gs + i);
+        params = sp;
+        rots = sr;
+        ops = so;
+        blocks = sb;
+    }
+    // store map of logical l = io_tid + kIo * k: bits 0..6 from io_tid, 7..11 from k
+    if (tid < 32) {
+        uint32_t v = 0;
+        for (int j = 0; j < 5; ++j)
+            if ((tid >> j) & 1u) v ^= (uint32_t)__ldg(g_geo + 32 + 7 + j);
+        st_k[tid] = v;
+    }
+    if (tid == 0) {
+        for (int st = 0; st < kStages; ++st) {
+            mbar_init(full + st, kIo);
+            mbar_init(computed + st, kT);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint64_t ntiles = 1ull << g.ncomp;
+    if ((uint64_t)blockIdx.x >= ntiles) return;
+    const int ntile_cta = (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1;
+    const int lane = tid & 31;
+    const int comp_lane = __ldg(g_geo + lane);
+    const uint32_t cmask = (1u << c) - 1u;
+
+    if (tid >= (uint32_t)kT) {
+        // ---------------- I/O warps ----------------
+        const uint32_t io = tid - kT;
+        uint32_t st_base = (uint32_t)__ldg(g_geo + 44);
+        for (int i = 0; i < 7; ++i)
+            if ((io >> i) & 1u) st_base ^= (uint32_t)__ldg(g_geo + 32 + i);
+        auto load = [&](int it) {
+            const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
+            const uint64_t b = tbase(tile, lane, g.ncomp, comp_lane);
+            double2 *buf = bufs + (it % kStages) * tsize;
+            const double2 *src = psi + b;
+#pragma unroll 8
+            for (int k = 0; k < tsize / kIo; ++k) {
+                const uint32_t l = io + k * kIo;
+                cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
+            }
+            cp_async_mbar_arrive(full + (it % kStages));
+        };
+        load(0);
+        for (int it = 0; it < ntile_cta; ++it) {
+            if (it + 1 < ntile_cta) {
+                io_sync();  // every I/O thread is done reading stage (it+1)%3 (tile it-2)
+                load(it + 1);
+            }
+            const int st = it % kStages;
+            mbar_wait(computed + st, (uint32_t)((it / kStages) & 1));
+            const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
+            const uint64_t b = tbase(tile, lane, g.ncomp, comp_lane);
+            const double2 *sm = bufs + st * tsize;
+            double2 *dst = psi + b;
+#pragma unroll 8
+            for (int k = 0; k < tsize / kIo; ++k) {
+                const uint32_t l = io + k * kIo;
+                __stcs(dst + (l & cmask) + offhi[l >> c], sm[st_base ^ st_k[k]]);
+            }
+        }
+        cp_async_wait<0>();
+    } else {
+        // ---------------- compute warps ----------------
+        for (int it = 0; it < ntile_cta; ++it) {
+            const int st = it % kStages;
+            const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
+            const uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
+            mbar_wait(full + st, (uint32_t)((it / kStages) & 1));
+            run_blocks<false, 1>(bufs + st * tsize, blocks, prog.nblocks, ops, rots, params, base,
+                                 tid, m);
+            mbar_arrive(computed + st);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two-group ring pass (m = 12, no U2 / wide-flip blocks): one persistent CTA
+// per SM, 512 threads = two groups of 8 warps at <= 128 registers (the whole
+// register file), sharing a 3-stage ring of 64 KiB tiles.  Group g takes the
+// CTA's tiles it = g, g+2, ...; tile it lives in stage it % 3.  After
+// computing and storing tile it, the group refills that stage with tile it+3
+// (which the *other* group will compute), so one tile load is always in
+// flight while both groups run FP64 work: HBM streaming overlaps compute.
+// full[s] is completed by the 256 noinc cp.async arrivals of the loading
+// group; each group syncs its own blocks on named barrier 1 + g.
+constexpr int kRingThreads = 2 * kT;
+
+template <bool STAGED>
+__global__ void __launch_bounds__(kRingThreads, 1)
+tile_ring_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__restrict__ g_offhi,
+                 const int32_t *__restrict__ g_geo, const PassProgram prog)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int m = kMaxTileBits;
+    constexpr int tsize = 1 << m;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);            // [kStages]
+    uint32_t *st_k = reinterpret_cast<uint32_t *>(full + kStages);      // [16]
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);        // kStages x tsize
+    const int c = g.c;
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + kStages * tsize);
+    const int nhi = 1 << (m - c);
+    const uint32_t tid_all = threadIdx.x;
+    for (int i = tid_all; i < nhi; i += kRingThreads) offhi[i] = __ldg(g_offhi + i);
+    const BlockRec *blocks = prog.blocks;
+    const OpRec *ops = prog.ops;
+    const RotRec *rots = prog.rots;
+    const double *params = prog.params;
+    if (STAGED) {
+        double *sp = reinterpret_cast<double *>(offhi + nhi + (nhi & 1));
+        RotRec *sr = reinterpret_cast<RotRec *>(sp + ((prog.nparams + 1) & ~1));
+        OpRec *so = reinterpret_cast<OpRec *>(sr + prog.nrots);
+        BlockRec *sb = reinterpret_cast<BlockRec *>(so + prog.nops);
+        for (int i = tid_all; i < prog.nparams; i += kRingThreads) sp[i] = __ldg(prog.params + i);
+        const int4 *gs = reinterpret_cast<const int4 *>(prog.rots);
+        for (int i = tid_all; i < prog.nrots * 2; i += kRingThreads) reinterpret_cast<int4 *>(sr)[i] = __ldg(gs + i);
+        gs = reinterpret_cast<const int4 *>(prog.ops);
+        for (int i = tid_all; i < prog.nops * 2; i += kRingThreads) reinterpret_cast<int4 *>(so)[i] = __ldg(gs + i);
+        gs = reinterpret_cast<const int4 *>(prog.blocks);
+        for (int i = tid_all; i < prog.nblocks * 3; i += kRingThreads) reinterpret_cast<int4 *>(sb)[i] = __ldg(gs + i);
+        params = sp;
+        rots = sr;
+        ops = so;
+        blocks = sb;
+    }
+    // store map of logical l = tid + kT * k: bits 0..7 from tid, 8..11 from k
+    if (tid_all < 16) {
+        uint32_t v = 0;
+        for (int j = 0; j < 4; ++j)
+            if ((tid_all >> j) & 1u) v ^= (uint32_t)__ldg(g_geo + 32 + kTB + j);
+        st_k[tid_all] = v;
+    }
+    if (tid_all == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(full + st, kT);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint64_t ntiles = 1ull << g.ncomp;
+    if ((uint64_t)blockIdx.x >= ntiles) return;
+    const int T = (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1;
+    const int grp = (int)(tid_all / kT);
+    const uint32_t tid = tid_all % kT;
+    const int bar_id = 1 + grp;
+    const int lane = tid & 31;
+    const int comp_lane = __ldg(g_geo + lane);
+    const uint32_t cmask = (1u << c) - 1u;
+    uint32_t st_base = (uint32_t)__ldg(g_geo + 44);
+    for (int i = 0; i < kTB; ++i)
+        if ((tid >> i) & 1u) st_base ^= (uint32_t)__ldg(g_geo + 32 + i);
+
+    auto load = [&](int it) {
+        const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
+        const uint64_t b = tbase(tile, lane, g.ncomp, comp_lane);
+        double2 *buf = bufs + (it % kStages) * tsize;
+        const double2 *src = psi + b;
+#pragma unroll 4
+        for (int k = 0; k < tsize / kT; ++k) {
+            const uint32_t l = tid + k * kT;
+            cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
+        }
+        cp_async_mbar_arrive(full + (it % kStages));
+    };
+    // prologue: group 0 loads tiles 0 and 2, group 1 loads tile 1
+    if (grp == 0) {
+        load(0);
+        if (T > 2) load(2);
+    } else if (T > 1) {
+        load(1);
+    }
+    for (int it = grp; it < T; it += 2) {
+        const int st = it % kStages;
+        const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
+        const uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
+        // The other group may still be on tile it - 3 of this stage (its load
+        // may not even have landed): a parity wait only distinguishes the
+        // current phase from the previous one, so first wait for tile it - 3's
+        // phase, then for tile it's.
+        if (it >= kStages) mbar_wait(full + st, (uint32_t)(((it / kStages) - 1) & 1));
+        mbar_wait(full + st, (uint32_t)((it / kStages) & 1));
+        double2 *sm = bufs + st * tsize;
+        run_blocks<true, -1>(sm, blocks, prog.nblocks, ops, rots, params, base, tid, m, bar_id);
+        // run_blocks ends with a group barrier: the tile is final in SMEM
+        double2 *dst = psi + base;
+#pragma unroll 4
+        for (int k = 0; k < tsize / kT; ++k) {
+            const uint32_t l = tid + k * kT;
+            __stcs(dst + (l & cmask) + offhi[l >> c], sm[st_base ^ st_k[k]]);
+        }
+        if (it + kStages < T) {
+            block_sync<-1>(bar_id);  // every thread of the group is done reading stage st
+            load(it + kStages);
+        }
+    }
+    cp_async_wait<0>();
+}
 }  // namespace
 
 cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *d_offhi,
@@ -565,6 +862,49 @@ cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *
         if (env_grid && atoi(env_grid) > 0) cap = (uint64_t)atoi(env_grid);
         return (int)(ntiles < cap ? ntiles : cap);
     };
+    static const char *env_ring = getenv("QSV_TILE_RING");  // 0: disable the ring kernel
+    if (lite && g.m == kMaxTileBits && !(env_ring && env_ring[0] == '0')) {
+        static bool ring_configured = false;
+        if (!ring_configured) {
+            cudaError_t e = cudaFuncSetAttribute(tile_ring_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+            if (e != cudaSuccess) return e;
+            e = cudaFuncSetAttribute(tile_ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     max_smem);
+            if (e != cudaSuccess) return e;
+            ring_configured = true;
+        }
+        const size_t rb = 256 + ((size_t)kStages * 16 << g.m) + 8 * (nhi + (nhi & 1));
+        const bool rs = rb + prog_bytes <= (size_t)max_smem;
+        const size_t smem = rs ? rb + prog_bytes : rb;
+        if (rs)
+            tile_ring_kernel<true><<<grid_for(1), kRingThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+        else
+            tile_ring_kernel<false><<<grid_for(1), kRingThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+        return cudaGetLastError();
+    }
+    static const char *env_ws = getenv("QSV_TILE_WS");  // 1: enable the warp-specialised kernel
+    const bool ws_ok = g.m == kMaxTileBits && env_ws && env_ws[0] == '1';
+    if (ws_ok) {
+        static bool ws_configured = false;
+        if (!ws_configured) {
+            cudaError_t e = cudaFuncSetAttribute(tile_ws_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+            if (e != cudaSuccess) return e;
+            e = cudaFuncSetAttribute(tile_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     max_smem);
+            if (e != cudaSuccess) return e;
+            ws_configured = true;
+        }
+        const size_t ws_base = 256 + ((size_t)kStages * 16 << g.m) + 8 * (nhi + (nhi & 1));
+        const bool ws_staged = ws_base + prog_bytes <= (size_t)max_smem;
+        const size_t smem = ws_staged ? ws_base + prog_bytes : ws_base;
+        if (ws_staged)
+            tile_ws_kernel<true><<<grid_for(1), kWsThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+        else
+            tile_ws_kernel<false><<<grid_for(1), kWsThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
+        return cudaGetLastError();
+    }
     // two CTAs per SM need <= ~113 KB each: single tile buffer + staged program
     if (lite && lite_base + prog_bytes <= (size_t)112 * 1024) {
         const size_t smem = lite_base + prog_bytes;

@@ -1,0 +1,663 @@
+"""Multi-GPU state vector: global-qubit sharding with batched qubit-swap
+relayouts.
+
+The reference has no sharded state (SPEC.md:398 lists it as a non-goal; its
+only parallelism is the fork pool of engine.py:169-199).  This module is the
+B200 analogue: one process per GPU, ``torch.distributed`` (NCCL over NVLink /
+NVSwitch) for the plumbing, the single-GPU engine (libqsv) for every local
+pass.
+
+Layout.  With P = 2^g ranks and n qubits, rank r holds the contiguous slice
+of 2^(n-g) amplitudes whose *physical* index bits [n_local, n) equal r.  A
+logical->physical qubit map ``perm`` says where each logical qubit lives;
+physical positions >= n_local are global (rank bits).
+
+Gates.  ``plan_segments`` walks the gate list and emits local segments (gates
+whose qubits are all local, remapped to physical positions) separated by
+relayouts.  When a gate needs a global qubit, ONE relayout brings in that
+qubit plus other global qubits needed before the evicted ones (Belady-style
+lookahead), so several global-qubit gates share one exchange.  A relayout
+first moves the evicted local qubits to the top k local positions with SWAP
+gates (free inside the engine's tile passes: the planner folds permutations
+into the shared-memory map), then swaps those k top local bits with k global
+bits: every rank exchanges 2^k - 1 contiguous chunks of 2^(n_local-k)
+amplitudes pairwise with its partners (in place, through a bounded staging
+buffer).  The map is updated and never swapped back.
+
+Expectation.  Strings whose flip avoids the global bits are evaluated on
+every shard by the engine's batched sweep (a Z bit on a global position is a
+per-rank sign).  The remaining strings are localised by further relayouts of
+the state (logically read-only).  Per-rank partials are gathered and summed in
+ascending rank order -- the reduction order of engine.py:199 -- so the energy
+is deterministic and independent of P up to rounding.
+
+Communicators: ``ProcessGroupComm`` (one shard per process; NCCL on GPUs,
+gloo on CPU for tests) and ``LoopbackComm`` (all P shards in one process,
+exchanges are device copies -- SURVEY.md 4's single-device loopback).  Local
+compute goes through a ``LocalEngine``; ``CudaEngine`` is the product one.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+K_SWAP = 4  # gate-kind code of SWAP (include/qsv.h)
+
+
+# ---------------------------------------------------------------------------
+# local engine (product: libqsv on the process's GPU)
+# ---------------------------------------------------------------------------
+
+
+class CudaEngine:
+    """Local shard operations on libqsv device states."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+
+    def zeros(self, n_local: int):
+        from . import statevector as sv
+
+        s = sv.StateVector._empty(n_local, self.device)
+        self.tensor(s).zero_()
+        return s
+
+    def basis(self, n_local: int, index: int):
+        from . import _lib
+        from . import statevector as sv
+
+        s = sv.StateVector._empty(n_local, self.device)
+        _lib.check(_lib.lib().qsv_set_basis(s.handle, int(index)))
+        return s
+
+    def copy(self, shard):
+        return shard.copy()
+
+    def apply_gates(self, shard, kinds, qubits, values) -> None:
+        from . import _lib
+
+        if len(kinds) == 0:
+            return
+        _lib.check(_lib.lib().qsv_apply_gates(shard.handle, len(kinds), _lib.i32ptr(kinds),
+                                              _lib.i32ptr(qubits), _lib.dptr(values), None))
+
+    def expectation_terms(self, shard, x, y, z) -> np.ndarray:
+        """Per-string Re<P_t> summed over this shard only."""
+        from . import _lib
+
+        S = len(x)
+        per = np.zeros(S, dtype=np.float64)
+        if S == 0:
+            return per
+        ones = np.ones(S, dtype=np.float64)
+        zeros = np.zeros(S, dtype=np.float64)
+        re, im = ctypes.c_double(), ctypes.c_double()
+        _lib.check(_lib.lib().qsv_expectation(shard.handle, S, _lib.u64ptr(x), _lib.u64ptr(y),
+                                              _lib.u64ptr(z), _lib.dptr(ones), _lib.dptr(zeros),
+                                              ctypes.byref(re), ctypes.byref(im), _lib.dptr(per),
+                                              None))
+        return per
+
+    def apply_pauli(self, src, dst, x: int, y: int, z: int) -> None:
+        """dst = P src (kernels.apply_pauli, _cykernels.pyx:76-102)."""
+        from . import _lib
+
+        _lib.check(_lib.lib().qsv_apply_pauli(src.handle, dst.handle, int(x), int(y), int(z)))
+
+    def vdot(self, a, b) -> complex:
+        from . import statevector as sv
+
+        return sv.vdot(a, b)
+
+    def tensor(self, shard):
+        """Zero-copy torch view (2^n_local, 2) float64 of the shard."""
+        import torch
+
+        return torch.as_tensor(shard, device=f"cuda:{self.device}")
+
+    def synchronize(self, shard) -> None:
+        shard.synchronize()
+
+    def download(self, shard) -> np.ndarray:
+        return shard.amplitudes
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+
+
+class LoopbackComm:
+    """All P shards live in this process; exchanges are device copies."""
+
+    def __init__(self, world: int):
+        if world < 1 or world & (world - 1):
+            raise ValueError("world size must be a power of two")
+        self.world = world
+        self.owned = list(range(world))
+
+    def gather_partials(self, partials: dict) -> list:
+        return [partials[r] for r in range(self.world)]
+
+    def gather_arrays(self, arrays: dict) -> list:
+        return [arrays[r] for r in range(self.world)]
+
+    def barrier(self) -> None:
+        pass
+
+
+class ProcessGroupComm:
+    """One shard per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None, piece_bytes: int = 256 << 20):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        if self.world & (self.world - 1):
+            raise ValueError("world size must be a power of two")
+        self.rank = dist.get_rank(group)
+        self.owned = [self.rank]
+        self.piece_bytes = piece_bytes
+
+    def _device(self, like):
+        return like.device
+
+    def gather_partials(self, partials: dict) -> list:
+        import torch
+
+        v = partials[self.rank]
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor(v, dtype=torch.float64, device=dev).reshape(-1)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
+    def gather_arrays(self, arrays: dict) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, arrays[self.rank], group=self.group)
+        return out
+
+    def barrier(self) -> None:
+        self.dist.barrier(group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# planner (pure host logic, identical on every rank)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Relayout:
+    """Swap the top k local physical bits with global bits S[0..k-1]
+    (rank-bit indices): top local bit n_local - k + i <-> global bit S[i]."""
+    S: tuple[int, ...]
+
+    @property
+    def k(self) -> int:
+        return len(self.S)
+
+
+@dataclass
+class Segment:
+    src: np.ndarray        # source gate index per local gate (-1: inserted SWAP)
+    qubits: np.ndarray     # int32 [2 * L] physical local qubits
+    relayout: Optional[Relayout]
+
+
+def _gate_qubits(qubits, i):
+    a, b = int(qubits[2 * i]), int(qubits[2 * i + 1])
+    return (a,) if b < 0 else (a, b)
+
+
+class _NextUse:
+    def __init__(self, n, kinds, qubits):
+        self.uses = [[] for _ in range(n)]
+        for i in range(len(kinds)):
+            for q in _gate_qubits(qubits, i):
+                self.uses[q].append(i)
+        self.ptr = [0] * n
+
+    def __call__(self, q, i):
+        u, p = self.uses[q], self.ptr[q]
+        while p < len(u) and u[p] < i:
+            p += 1
+        self.ptr[q] = p
+        return u[p] if p < len(u) else math.inf
+
+
+def _apply_relayout_to_map(perm, inv, bring, victims, n_local):
+    k = len(bring)
+    for j in range(k):
+        b, v = bring[j], victims[j]
+        T = n_local - k + j
+        Gp = perm[b]
+        perm[b], perm[v] = T, Gp
+        inv[T], inv[Gp] = b, v
+
+
+def _move_victims(perm, inv, victims, n_local, swaps):
+    """SWAP gates (physical) bringing victims[j] to position n_local - k + j."""
+    k = len(victims)
+    for j, v in enumerate(victims):
+        T = n_local - k + j
+        p = perm[v]
+        if p != T:
+            other = inv[T]
+            swaps.append((p, T))
+            perm[v], perm[other] = T, p
+            inv[T], inv[p] = v, other
+
+
+def plan_segments(kinds, qubits, n: int, n_local: int, perm):
+    """Split a gate list into local segments and relayouts.
+    Returns (segments, final_perm)."""
+    g = n - n_local
+    perm = list(perm)
+    inv = [0] * n
+    for q, p in enumerate(perm):
+        inv[p] = q
+    nxt = _NextUse(n, kinds, qubits)
+    segs = []
+    src, qs = [], []
+    for i in range(len(kinds)):
+        gq = _gate_qubits(qubits, i)
+        if all(perm[q] < n_local for q in gq):
+            src.append(i)
+            qs.extend([perm[gq[0]], perm[gq[1]] if len(gq) == 2 else -1])
+            continue
+        need = [q for q in gq if perm[q] >= n_local]
+        glob = [inv[p] for p in range(n_local, n) if inv[p] not in need]
+        extra = sorted(glob, key=lambda q: (nxt(q, i), q))
+        cand = sorted((inv[p] for p in range(n_local) if inv[p] not in gq),
+                      key=lambda q: (-nxt(q, i), q))
+        if len(cand) < g:
+            raise ValueError("too few local qubits for a relayout")
+        bring = list(need)
+        for q in extra:
+            if len(bring) >= g:
+                break
+            if nxt(q, i) < nxt(cand[len(bring)], i):
+                bring.append(q)
+        victims = cand[:len(bring)]
+        swaps = []
+        _move_victims(perm, inv, victims, n_local, swaps)
+        for a, b in swaps:
+            src.append(-1)
+            qs.extend([a, b])
+        S = tuple(perm[b] - n_local for b in bring)
+        segs.append(Segment(np.array(src, dtype=np.int64), np.array(qs, dtype=np.int32),
+                            Relayout(S)))
+        _apply_relayout_to_map(perm, inv, bring, victims, n_local)
+        src = [i]
+        qs = [perm[gq[0]], perm[gq[1]] if len(gq) == 2 else -1]
+    segs.append(Segment(np.array(src, dtype=np.int64), np.array(qs, dtype=np.int32), None))
+    return segs, perm
+
+
+def plan_localize(flips: list[int], n: int, n_local: int, perm):
+    """Relayout that makes flips[0] (logical mask) local, evicting the local
+    qubits least used by the other flips.  Returns (swaps, Relayout, new perm)."""
+    perm = list(perm)
+    inv = [0] * n
+    for q, p in enumerate(perm):
+        inv[p] = q
+    f0 = flips[0]
+    bring = [q for q in range(n) if (f0 >> q) & 1 and perm[q] >= n_local]
+    freq = [0] * n
+    for f in flips:
+        for q in range(n):
+            if (f >> q) & 1:
+                freq[q] += 1
+    cand = sorted((inv[p] for p in range(n_local) if not (f0 >> inv[p]) & 1),
+                  key=lambda q: (freq[q], q))
+    if len(cand) < len(bring):
+        raise ValueError("Pauli string wider than the local qubits of a shard")
+    victims = cand[:len(bring)]
+    swaps = []
+    _move_victims(perm, inv, victims, n_local, swaps)
+    S = tuple(perm[b] - n_local for b in bring)
+    _apply_relayout_to_map(perm, inv, bring, victims, n_local)
+    return swaps, Relayout(S), perm
+
+
+# ---------------------------------------------------------------------------
+# the distributed state
+# ---------------------------------------------------------------------------
+
+
+def _log2(p: int) -> int:
+    g = p.bit_length() - 1
+    if p < 1 or (1 << g) != p:
+        raise ValueError("world size must be a power of two")
+    return g
+
+
+class DistStateVector:
+    """Logical n-qubit state sharded over comm.world ranks."""
+
+    def __init__(self, n_qubits: int, comm, engine, shards: dict, perm):
+        self.n_qubits = n_qubits
+        self.comm = comm
+        self.engine = engine
+        self.g = _log2(comm.world)
+        self.n_local = n_qubits - self.g
+        self.shards = shards
+        self.perm = list(perm)
+        self.stats = {"relayouts": 0, "relayout_bytes_sent": 0, "relayout_seconds": 0.0}
+
+    # -- construction --------------------------------------------------------
+    @classmethod
+    def basis(cls, n_qubits: int, index: int, comm, engine) -> "DistStateVector":
+        g = _log2(comm.world)
+        n_local = n_qubits - g
+        if n_local < 1:
+            raise ValueError("more ranks than amplitudes per shard allow")
+        owner, local = index >> n_local, index & ((1 << n_local) - 1)
+        shards = {r: (engine.basis(n_local, local) if r == owner else engine.zeros(n_local))
+                  for r in comm.owned}
+        return cls(n_qubits, comm, engine, shards, range(n_qubits))
+
+    def copy(self) -> "DistStateVector":
+        out = DistStateVector(self.n_qubits, self.comm, self.engine,
+                              {r: self.engine.copy(s) for r, s in self.shards.items()}, self.perm)
+        return out
+
+    # -- exchange ------------------------------------------------------------
+    def _relayout(self, rl: Relayout) -> None:
+        """Swap the top k local bits with global bits rl.S, pairwise in place."""
+        import time
+
+        k = rl.k
+        if k == 0:
+            return
+        t0 = time.perf_counter()
+        n_local = self.n_local
+        chunk = 1 << (n_local - k)
+        views = {}
+        for r, s in self.shards.items():
+            self.engine.synchronize(s)
+            views[r] = self.engine.tensor(s)
+
+        def s_value(r):
+            return sum(((r >> rl.S[i]) & 1) << i for i in range(k))
+
+        def partner(r, c):
+            p = r
+            for i in range(k):
+                p = (p & ~(1 << rl.S[i])) | (((c >> i) & 1) << rl.S[i])
+            return p
+
+        remote = {}
+        for r in self.comm.owned:
+            rs = s_value(r)
+            for c in range(1 << k):
+                if c == rs:
+                    continue
+                p = partner(r, c)
+                # (r, chunk c) <-> (p, chunk rs)
+                if p in views:
+                    if r < p:
+                        a = views[r][c * chunk:(c + 1) * chunk]
+                        b = views[p][rs * chunk:(rs + 1) * chunk]
+                        tmp = a.clone()
+                        a.copy_(b)
+                        b.copy_(tmp)
+                else:
+                    remote.setdefault(r, []).append((c, p))
+        if remote:
+            self._p2p_exchange(views, remote, chunk)
+        self._sync_after(views)
+        self.stats["relayouts"] += 1
+        self.stats["relayout_bytes_sent"] += 16 * (((1 << k) - 1) * chunk)  # per rank
+        self.stats["relayout_seconds"] += time.perf_counter() - t0
+
+    def _p2p_exchange(self, views, remote, chunk):
+        import torch
+
+        dist = self.comm.dist
+        group = self.comm.group
+        for r, lst in remote.items():
+            t = views[r]
+            row_bytes = t.element_size() * (t.shape[1] if t.dim() > 1 else 1)
+            piece = max(1, min(chunk, self.comm.piece_bytes // row_bytes))
+            staging = torch.empty((len(lst), piece) + tuple(t.shape[1:]), dtype=t.dtype,
+                                  device=t.device)
+            for off in range(0, chunk, piece):
+                w = min(piece, chunk - off)
+                ops = []
+                for j, (c, p) in enumerate(lst):
+                    src = t[c * chunk + off: c * chunk + off + w]
+                    ops.append(dist.P2POp(dist.isend, src.contiguous(), p, group))
+                    ops.append(dist.P2POp(dist.irecv, staging[j, :w], p, group))
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+                for j, (c, p) in enumerate(lst):
+                    t[c * chunk + off: c * chunk + off + w].copy_(staging[j, :w])
+
+    def _sync_after(self, views):
+        import torch
+
+        for t in views.values():
+            if t.is_cuda:
+                torch.cuda.current_stream(t.device).synchronize()
+                break
+
+    # -- gates ---------------------------------------------------------------
+    def apply_flat(self, kinds, qubits, values) -> None:
+        """Apply a flattened bound gate list (logical qubits) in place."""
+        segs, perm = plan_segments(kinds, qubits, self.n_qubits, self.n_local, self.perm)
+        for seg in segs:
+            L = len(seg.src)
+            if L:
+                sk = np.empty(L, dtype=np.int32)
+                sv_ = np.zeros(3 * L, dtype=np.float64)
+                for j, i in enumerate(seg.src):
+                    if i < 0:
+                        sk[j] = K_SWAP
+                    else:
+                        sk[j] = kinds[i]
+                        sv_[3 * j:3 * j + 3] = values[3 * i:3 * i + 3]
+                for r in self.comm.owned:
+                    self.engine.apply_gates(self.shards[r], sk, seg.qubits, sv_)
+            if seg.relayout is not None:
+                self._relayout(seg.relayout)
+        self.perm = perm
+
+    def _apply_swaps(self, swaps) -> None:
+        if not swaps:
+            return
+        L = len(swaps)
+        sk = np.full(L, K_SWAP, dtype=np.int32)
+        sq = np.array([q for ab in swaps for q in ab], dtype=np.int32)
+        sv_ = np.zeros(3 * L, dtype=np.float64)
+        for r in self.comm.owned:
+            self.engine.apply_gates(self.shards[r], sk, sq, sv_)
+
+    # -- expectation ---------------------------------------------------------
+    def _phys(self, mask: int) -> int:
+        out = 0
+        for q in range(self.n_qubits):
+            if (mask >> q) & 1:
+                out |= 1 << self.perm[q]
+        return out
+
+    def expectation_terms(self, x, y, z, cr, ci) -> tuple[float, float]:
+        """(Re, Im) of sum_t c_t <P_t>, reduced over ranks in ascending order."""
+        S = len(cr)
+        lmask = (1 << self.n_local) - 1
+        part = {r: np.zeros(2) for r in self.comm.owned}
+        wide = [t for t in range(S) if bin(int(x[t]) | int(y[t])).count("1") > self.n_local]
+        if wide:
+            self._pairwise_terms(wide, x, y, z, cr, ci, part)
+        wset = set(wide)
+        remaining = [t for t in range(S) if t not in wset]
+        while remaining:
+            px = [self._phys(int(x[t])) for t in remaining]
+            py = [self._phys(int(y[t])) for t in remaining]
+            pz = [self._phys(int(z[t])) for t in remaining]
+            loc = [j for j in range(len(remaining)) if ((px[j] | py[j]) >> self.n_local) == 0]
+            if loc:
+                lx = np.array([px[j] & lmask for j in loc], dtype=np.uint64)
+                ly = np.array([py[j] & lmask for j in loc], dtype=np.uint64)
+                lz = np.array([pz[j] & lmask for j in loc], dtype=np.uint64)
+                gz = [pz[j] >> self.n_local for j in loc]
+                c_re = np.array([cr[remaining[j]] for j in loc])
+                c_im = np.array([ci[remaining[j]] for j in loc])
+                for r in self.comm.owned:
+                    per = self.engine.expectation_terms(self.shards[r], lx, ly, lz)
+                    sign = np.array([-1.0 if bin(gzj & r).count("1") & 1 else 1.0 for gzj in gz])
+                    v = per * sign
+                    part[r][0] += float(np.dot(c_re, v))
+                    part[r][1] += float(np.dot(c_im, v))
+            keep = set(loc)
+            remaining = [remaining[j] for j in range(len(remaining)) if j not in keep]
+            if remaining:
+                flips = [int(x[t]) | int(y[t]) for t in remaining]
+                swaps, rl, perm = plan_localize(flips, self.n_qubits, self.n_local, self.perm)
+                self._apply_swaps(swaps)
+                self._relayout(rl)
+                self.perm = perm
+        parts = self.comm.gather_partials({r: part[r] for r in self.comm.owned})
+        re = 0.0
+        im = 0.0
+        for p in parts:  # ascending rank order (engine.py:199)
+            re += float(p[0])
+            im += float(p[1])
+        return re, im
+
+
+    def _pairwise_terms(self, terms, x, y, z, cr, ci, part) -> None:
+        """Strings wider than a shard's local qubits: for each global flip
+        pattern fg, every rank r fetches the shard of r ^ fg and evaluates
+        sum_j conj(psi_j) (P psi)_j over its own slice (one pairwise shard
+        exchange per pattern)."""
+        n_local = self.n_local
+        lmask = (1 << n_local) - 1
+        by_fg = {}
+        for t in terms:
+            px, py, pz = self._phys(int(x[t])), self._phys(int(y[t])), self._phys(int(z[t]))
+            by_fg.setdefault((px | py) >> n_local, []).append((t, px, py, pz))
+        for fg in sorted(by_fg):
+            partners = self._fetch_partners(fg)
+            scratch = {r: self.engine.zeros(n_local) for r in self.comm.owned}
+            for t, px, py, pz in by_fg[fg]:
+                yg = py >> n_local
+                yzg = (py | pz) >> n_local
+                ph = (1j) ** (bin(yg).count("1") & 3)
+                c = complex(cr[t], ci[t])
+                for r in self.comm.owned:
+                    p = r ^ fg
+                    sg = -1.0 if bin(p & yzg).count("1") & 1 else 1.0
+                    self.engine.apply_pauli(partners[r], scratch[r], px & lmask, py & lmask,
+                                            pz & lmask)
+                    v = c * ph * sg * self.engine.vdot(self.shards[r], scratch[r])
+                    part[r][0] += v.real
+                    part[r][1] += v.imag
+
+    def _fetch_partners(self, fg: int) -> dict:
+        """{r: copy of rank (r ^ fg)'s shard} for every owned rank r."""
+        out = {}
+        remote = []
+        for r in self.comm.owned:
+            p = r ^ fg
+            if p in self.shards:
+                out[r] = self.shards[p]
+            else:
+                remote.append((r, p))
+        if remote:
+            import torch
+
+            dist = self.comm.dist
+            for r, p in remote:
+                buf = self.engine.zeros(self.n_local)
+                self.engine.synchronize(self.shards[r])
+                mine = self.engine.tensor(self.shards[r])
+                theirs = self.engine.tensor(buf)
+                ops = [dist.P2POp(dist.isend, mine, p, self.comm.group),
+                       dist.P2POp(dist.irecv, theirs, p, self.comm.group)]
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+                if theirs.is_cuda:
+                    torch.cuda.current_stream(theirs.device).synchronize()
+                out[r] = buf
+        return out
+
+    # -- host view -------------------------------------------------------------
+    def amplitudes(self) -> np.ndarray:
+        """Logical amplitude vector on the host (small states; test helper)."""
+        arrays = self.comm.gather_arrays({r: self.engine.download(self.shards[r])
+                                          for r in self.comm.owned})
+        phys = np.concatenate([np.asarray(a) for a in arrays])
+        n = self.n_qubits
+        idx = np.arange(1 << n, dtype=np.int64)
+        pidx = np.zeros_like(idx)
+        for q in range(n):
+            pidx |= ((idx >> q) & 1) << self.perm[q]
+        return phys[pidx]
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped API
+# ---------------------------------------------------------------------------
+
+
+def init_state(bitstring: str, comm, engine=None) -> DistStateVector:
+    """init_state (statevector.py:42-54) on a sharded state."""
+    n = len(bitstring)
+    if n == 0 or any(c not in "01" for c in bitstring):
+        raise ValueError(f"invalid bitstring {bitstring!r}")
+    index = sum(1 << k for k, c in enumerate(bitstring) if c == "1")
+    return DistStateVector.basis(n, index, comm, engine or CudaEngine())
+
+
+def evolve(s: DistStateVector, c) -> DistStateVector:
+    """evolve (statevector.py:65-74): new sharded state, input untouched."""
+    from .circuit import flatten_bound
+
+    if c.n_qubits != s.n_qubits:
+        raise ValueError("circuit and state qubit counts differ")
+    if not c.is_bound():
+        raise RuntimeError("circuit must be bound before evolution")
+    out = s.copy()
+    out.apply_flat(*flatten_bound(c))
+    return out
+
+
+def expectation(s: DistStateVector, h) -> float:
+    """expectation (statevector.py:98-110) over the shards."""
+    from .pauli import term_arrays
+
+    if not h.is_hermitian():
+        raise ValueError("expectation requires a Hermitian operator (real coefficients)")
+    x, y, z, cr, ci = term_arrays(h, s.n_qubits)
+    re, im = s.expectation_terms(x, y, z, cr, ci)
+    if abs(im) > 1e-10:
+        raise ArithmeticError(f"expectation has imaginary residue {im:.3e}")
+    return re
+
+
+class DistributedBackend:
+    """Backend protocol (engine.py:59-75) over a sharded state."""
+
+    name = "sv-b200-dist"
+    supports_reverse_gradient = False
+
+    def __init__(self, comm, engine=None):
+        self.comm = comm
+        self.engine = engine or CudaEngine()
+
+    def prepare(self, bitstring: str) -> DistStateVector:
+        return init_state(bitstring, self.comm, self.engine)
+
+    def evolve(self, state: DistStateVector, bound) -> DistStateVector:
+        return evolve(state, bound)
+
+    def expectation(self, state: DistStateVector, h) -> float:
+        return expectation(state, h)
