@@ -132,6 +132,13 @@ int qsv_debug_plan_json(int n_qubits, int64_t n_gates, const int32_t *kinds,
                         const int32_t *qubits, const double *values, char *out, int64_t cap,
                         int64_t *needed);
 
+/* Run-time specialised tile passes (NVRTC-compiled per pass structure):
+ * available = 1 if NVRTC + the driver API could be loaded, launches = number
+ * of specialised pass launches so far in this process.  Env: QSV_JIT=0
+ * disables, QSV_JIT_MIN_QUBITS (default 22) sets the state size from which
+ * passes are specialised. */
+int qsv_jit_info(int *available, int64_t *launches);
+
 /* Statistics of the last plan on the calling thread (see qsv_plan_stats). */
 int qsv_last_plan_stats(qsv_plan_stats *out);
 

@@ -51,7 +51,7 @@ EXPORTED = (
     "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_apply_1q", "qsv_apply_2q",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
-    "qsv_plan_expectation", "qsv_debug_plan_json", "qsv_last_plan_stats",
+    "qsv_plan_expectation", "qsv_debug_plan_json", "qsv_jit_info", "qsv_last_plan_stats",
 )
 
 _lib = None
@@ -92,6 +92,7 @@ def _declare(L):
         "qsv_plan_expectation": ([ctypes.c_int, i64, u64p, u64p, u64p, sp], ctypes.c_int),
         "qsv_debug_plan_json": ([ctypes.c_int, i64, i32p, i32p, dp, ctypes.c_char_p, i64,
                                  ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_jit_info": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_last_plan_stats": ([sp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -143,6 +144,13 @@ def debug_plan(n_qubits: int, kinds, qubits, values) -> dict:
     check(lib().qsv_debug_plan_json(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits),
                                     dptr(values), buf, need.value, ctypes.byref(need)))
     return json.loads(buf.value.decode())
+
+
+def jit_info() -> tuple[bool, int]:
+    """(specialised passes available, specialised pass launches so far)."""
+    av, n = ctypes.c_int(0), ctypes.c_int64(0)
+    check(lib().qsv_jit_info(ctypes.byref(av), ctypes.byref(n)))
+    return bool(av.value), int(n.value)
 
 
 def dptr(a):

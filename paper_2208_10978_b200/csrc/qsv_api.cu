@@ -2,6 +2,8 @@
 // staging and launch sequencing.  Every compute entry point runs on the GPU;
 // there is no CPU path.
 #include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <climits>
@@ -22,6 +24,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local qsv_plan_stats g_last_stats{};
+int64_t g_jit_launches = 0;  // specialised pass launches (debug / tests)
 
 std::recursive_mutex g_mu;
 
@@ -198,6 +201,8 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     const size_t o_par = b.add(params.data(), params.size() * sizeof(double));
     struct PassOff { size_t off, comp, blk, ops, rots, par; int nblk, nops, nrots, npar; bool lite; };
     std::vector<PassOff> po(t.passes.size());
+    const bool jit = jit_enabled(s->n);
+    std::vector<std::string> jit_src(jit ? t.passes.size() : 0);
     {
         std::vector<uint64_t> offhi;
         std::vector<int32_t> comp;
@@ -251,6 +256,7 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
             o.nops = (int)lops.size();
             o.nrots = r_hi - r_lo;
             o.npar = p_hi - p_lo;
+            if (jit) jit_source(p.geom, lblk.data(), o.nblk, lops.data(), o.npar, jit_src[k]);
             o.blk = b.add(lblk.data(), lblk.size() * sizeof(BlockRec));
             o.ops = b.add(lops.data(), lops.size() * sizeof(OpRec));
             o.rots = b.add(t.rots.data() + r_lo, (size_t)o.nrots * sizeof(RotRec));
@@ -261,6 +267,14 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     size_t scratch = 0;
     rc = upload_blob(*c, s->stream, b, 0, &d, &scratch);
     if (rc) return rc;
+    if (jit) {
+        std::vector<const std::string *> srcs;
+        for (const std::string &src : jit_src)
+            if (!src.empty()) srcs.push_back(&src);
+        std::string err;
+        if (!srcs.empty() && jit_prepare(s->device, srcs, err) && getenv("QSV_JIT_VERBOSE"))
+            fprintf(stderr, "qsv jit: %s\n", err.c_str());
+    }
     const OpRec *d_ops = (const OpRec *)(d + o_ops);
     const RotRec *d_rots = (const RotRec *)(d + o_rots);
     const double *d_par = (const double *)(d + o_par);
@@ -276,6 +290,13 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                 QSV_CUDA(launch_rot_global(s->amps, s->n, p.flip, d_rots + op.r0, op.r1 - op.r0,
                                            s->stream));
             }
+        } else if (jit && !jit_src[k].empty() &&
+                   jit_launch(s->device, jit_src[k], s->amps, dims_of(p.geom),
+                              (const uint64_t *)(d + o.off), (const int32_t *)(d + o.comp),
+                              (const double *)(d + o.par), o.npar,
+                              (int)std::min<uint64_t>(1ull << p.geom.ncomp, (uint64_t)num_sms(s->device)),
+                              s->stream)) {
+            ++g_jit_launches;
         } else if (p.geom.m >= kBlockBits + 1) {
             QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
                                         (const int32_t *)(d + o.comp), (const BlockRec *)(d + o.blk),
@@ -786,6 +807,8 @@ int qsv_apply_1q(qsv_state *s, const double *m, int qubit)
     ProgramTemplate t;
     int32_t kind = K_U3, q[2] = {qubit, -1};
     plan_gates(s->n, 1, &kind, q, t);
+    for (OpRec &op : t.ops)
+        if (op.type == OP_U1) op.h = 0;  // arbitrary caller matrix: general class
     // plan for a U3 gate: one OP_U1 whose params are the supplied matrix
     std::vector<double> params(t.n_params);
     std::memcpy(params.data(), m, 8 * sizeof(double));
@@ -913,6 +936,14 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     j += "]}";
     if (needed) *needed = (int64_t)j.size() + 1;
     if (out && cap > (int64_t)j.size()) std::memcpy(out, j.c_str(), j.size() + 1);
+    return QSV_OK;
+}
+
+int qsv_jit_info(int *available, int64_t *launches)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (available) *available = jit_enabled(64) ? 1 : 0;
+    if (launches) *launches = g_jit_launches;
     return QSV_OK;
 }
 

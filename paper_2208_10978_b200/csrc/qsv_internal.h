@@ -44,7 +44,7 @@ enum OpType : int32_t {
 
 struct OpRec {  // 32 B
     int32_t type;
-    int32_t a, b, h;
+    int32_t a, b, h;  // h: highest flip bit (ROTG) / matrix class (U1: 0 general, 1 m00 real, 2 real)
     int32_t r0, r1, p;
     uint32_t f;
 };
@@ -156,6 +156,15 @@ cudaError_t launch_expect_global(const double2 *psi, int n, const GroupRec *d_gr
                                  int nterms, double *d_partial, int *grid_out, cudaStream_t st);
 int expect_global_grid(int n);
 int expect_sweep_grid(const TileDims &g, int nterms, int ndiag);
+// run-time specialised tile passes (qsv_jit.cpp)
+bool jit_enabled(int n_qubits);
+const char *jit_unavailable_reason();
+bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const OpRec *ops, int nparams,
+                std::string &src);
+int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::string &err);
+bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims &g,
+                const uint64_t *d_offhi, const int32_t *d_geo, const double *d_params, int nparams,
+                int grid, cudaStream_t st);
 cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,
                          double bre, double bim, cudaStream_t st);
 

@@ -1,0 +1,490 @@
+// qsv_jit.cpp -- run-time specialised tile passes (NVRTC -> sm_100a cubin).
+//
+// The interpreted tile kernel (qsv_tile_block.cu) decodes each pass's block
+// program at run time: a switch per op, matrices re-read from shared memory,
+// and -- because the register array a[16] must sit in the same registers at
+// every loop back-edge -- register moves after every in-place 2x2 update.
+// ncu on the config-2 brickwork shows the FP64 pipe only ~38 % busy with
+// ~1.5 non-FP64 instructions issued per FP64 one.  A dense-gate pass is pure
+// data-independent straight-line code once the planner has fixed its
+// structure, so this module generates that code: every block's gather /
+// scatter offsets become immediates, every op a template instantiation whose
+// matrix entries are __constant__ operands of the DFMA/DMUL instructions (no
+// loads, no registers), and the whole block is one basic block the compiler
+// schedules freely.  Structure-identical passes share a module (cache keyed by
+// the generated source); the angle-dependent matrices are copied into the
+// module's __constant__ bank before each launch (stream-ordered DtoD copy).
+//
+// The tile skeleton is the two-group ring pipeline of tile_ring_kernel:
+// 512 threads = 2 groups x 8 warps, 3 x 64 KiB SMEM stages, LDGSTS loads with
+// mbarrier completion, named-barrier block syncs, streaming stores.
+//
+// NVRTC and the driver API are dlopen'ed on first use, so libqsv.so still
+// loads (and its planner entry points work) on machines without a GPU driver.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "qsv_internal.h"
+
+namespace qsv {
+
+namespace {
+
+// ---- minimal driver / NVRTC API surface ----------------------------------
+typedef int CUresult;
+typedef void *CUmodule;
+typedef void *CUfunction;
+typedef unsigned long long CUdeviceptr;
+typedef int nvrtcResult;
+typedef void *nvrtcProgram;
+
+struct Api {
+    bool tried = false, ok = false;
+    std::string why;
+    // nvrtc
+    nvrtcResult (*CreateProgram)(nvrtcProgram *, const char *, const char *, int, const char *const *,
+                                 const char *const *) = nullptr;
+    nvrtcResult (*CompileProgram)(nvrtcProgram, int, const char *const *) = nullptr;
+    nvrtcResult (*GetCUBINSize)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*GetCUBIN)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*GetProgramLogSize)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*GetProgramLog)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*DestroyProgram)(nvrtcProgram *) = nullptr;
+    // driver
+    CUresult (*ModuleLoadData)(CUmodule *, const void *) = nullptr;
+    CUresult (*ModuleGetFunction)(CUfunction *, CUmodule, const char *) = nullptr;
+    CUresult (*ModuleGetGlobal)(CUdeviceptr *, size_t *, CUmodule, const char *) = nullptr;
+    CUresult (*FuncSetAttribute)(CUfunction, int, int) = nullptr;
+    CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             unsigned, cudaStream_t, void **, void **) = nullptr;
+    CUresult (*MemcpyDtoDAsync)(CUdeviceptr, CUdeviceptr, size_t, cudaStream_t) = nullptr;
+};
+Api g_api;
+
+template <typename F>
+bool sym(void *h, const char *name, F &out)
+{
+    out = reinterpret_cast<F>(dlsym(h, name));
+    return out != nullptr;
+}
+
+bool load_api()
+{
+    if (g_api.tried) return g_api.ok;
+    g_api.tried = true;
+    void *nv = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!nv) nv = dlopen("libnvrtc.so", RTLD_NOW | RTLD_LOCAL);
+    void *cu = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (!nv || !cu) {
+        g_api.why = !nv ? "libnvrtc not found" : "libcuda.so.1 not found";
+        return false;
+    }
+    bool ok = sym(nv, "nvrtcCreateProgram", g_api.CreateProgram) &&
+              sym(nv, "nvrtcCompileProgram", g_api.CompileProgram) &&
+              sym(nv, "nvrtcGetCUBINSize", g_api.GetCUBINSize) && sym(nv, "nvrtcGetCUBIN", g_api.GetCUBIN) &&
+              sym(nv, "nvrtcGetProgramLogSize", g_api.GetProgramLogSize) &&
+              sym(nv, "nvrtcGetProgramLog", g_api.GetProgramLog) &&
+              sym(nv, "nvrtcDestroyProgram", g_api.DestroyProgram) &&
+              sym(cu, "cuModuleLoadData", g_api.ModuleLoadData) &&
+              sym(cu, "cuModuleGetFunction", g_api.ModuleGetFunction) &&
+              sym(cu, "cuModuleGetGlobal_v2", g_api.ModuleGetGlobal) &&
+              sym(cu, "cuFuncSetAttribute", g_api.FuncSetAttribute) &&
+              sym(cu, "cuLaunchKernel", g_api.LaunchKernel) &&
+              sym(cu, "cuMemcpyDtoDAsync_v2", g_api.MemcpyDtoDAsync);
+    if (!ok) g_api.why = "missing NVRTC / driver symbols";
+    g_api.ok = ok;
+    return ok;
+}
+
+// ---- device-side skeleton (compiled by NVRTC) ------------------------------
+const char *kSkeleton = R"QSV(
+typedef unsigned long long u64;
+typedef unsigned int u32;
+#define KT 256
+#define KSTAGES 3
+#define TSIZE 4096
+__constant__ double C[QSV_NPARAMS];
+
+__device__ __forceinline__ double2 cmul(double ar, double ai, double2 x)
+{
+    return make_double2(fma(ar, x.x, -ai * x.y), fma(ar, x.y, ai * x.x));
+}
+
+// dense 2x2 on register bit J; K = 0 general, 1 m00 real, 2 all real
+template <int J, int K, int P>
+__device__ __forceinline__ void u1(double2 (&a)[16])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if (r & (1 << J)) continue;
+        const double2 x = a[r], y = a[r | (1 << J)];
+        double2 o0, o1;
+        if (K == 2) {
+            o0.x = fma(C[P], x.x, C[P + 2] * y.x);
+            o0.y = fma(C[P], x.y, C[P + 2] * y.y);
+            o1.x = fma(C[P + 4], x.x, C[P + 6] * y.x);
+            o1.y = fma(C[P + 4], x.y, C[P + 6] * y.y);
+        } else {
+            if (K == 1) {
+                o0.x = fma(C[P], x.x, fma(C[P + 2], y.x, -C[P + 3] * y.y));
+                o0.y = fma(C[P], x.y, fma(C[P + 2], y.y, C[P + 3] * y.x));
+            } else {
+                o0.x = fma(C[P], x.x, fma(-C[P + 1], x.y, fma(C[P + 2], y.x, -C[P + 3] * y.y)));
+                o0.y = fma(C[P], x.y, fma(C[P + 1], x.x, fma(C[P + 2], y.y, C[P + 3] * y.x)));
+            }
+            o1.x = fma(C[P + 4], x.x, fma(-C[P + 5], x.y, fma(C[P + 6], y.x, -C[P + 7] * y.y)));
+            o1.y = fma(C[P + 4], x.y, fma(C[P + 5], x.x, fma(C[P + 6], y.y, C[P + 7] * y.x)));
+        }
+        a[r] = o0;
+        a[r | (1 << J)] = o1;
+    }
+}
+
+// dense 4x4 on register bits (JA = MSB of the row index, JB)
+template <int JA, int JB, int P>
+__device__ __forceinline__ void u2(double2 (&a)[16])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if (r & ((1 << JA) | (1 << JB))) continue;
+        const int i0 = r, i1 = r | (1 << JB), i2 = r | (1 << JA), i3 = r | (1 << JA) | (1 << JB);
+        const double2 x0 = a[i0], x1 = a[i1], x2 = a[i2], x3 = a[i3];
+        double2 o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int R = P + 8 * k;
+            o[k].x = fma(C[R], x0.x, fma(-C[R + 1], x0.y, fma(C[R + 2], x1.x, fma(-C[R + 3], x1.y,
+                     fma(C[R + 4], x2.x, fma(-C[R + 5], x2.y, fma(C[R + 6], x3.x, -C[R + 7] * x3.y)))))));
+            o[k].y = fma(C[R], x0.y, fma(C[R + 1], x0.x, fma(C[R + 2], x1.y, fma(C[R + 3], x1.x,
+                     fma(C[R + 4], x2.y, fma(C[R + 5], x2.x, fma(C[R + 6], x3.y, C[R + 7] * x3.x)))))));
+        }
+        a[i0] = o[0];
+        a[i1] = o[1];
+        a[i2] = o[2];
+        a[i3] = o[3];
+    }
+}
+
+// diag(d0, d1) on register bit J
+template <int J, int P>
+__device__ __forceinline__ void dg(double2 (&a)[16])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+        a[r] = (r & (1 << J)) ? cmul(C[P + 2], C[P + 3], a[r]) : cmul(C[P], C[P + 1], a[r]);
+}
+
+// diag(d0, d1) on a thread-index bit
+template <int P>
+__device__ __forceinline__ void dgt(double2 (&a)[16], bool bit)
+{
+    const double dr = bit ? C[P + 2] : C[P], di = bit ? C[P + 3] : C[P + 1];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) a[r] = cmul(dr, di, a[r]);
+}
+
+__device__ __forceinline__ u32 swz(u32 l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+__device__ __forceinline__ u32 tb(u32 tid, int i, u32 col) { return (0u - ((tid >> i) & 1u)) & col; }
+__device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+
+__device__ __forceinline__ u64 tbase(u64 tile, int lane, int ncomp, int comp_lane)
+{
+    u64 bit = (lane < ncomp && ((tile >> lane) & 1ull)) ? (1ull << comp_lane) : 0ull;
+    u32 lo = __reduce_or_sync(0xffffffffu, (u32)bit);
+    u32 hi = __reduce_or_sync(0xffffffffu, (u32)(bit >> 32));
+    return ((u64)hi << 32) | lo;
+}
+__device__ __forceinline__ u32 saddr(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void *d, const void *s)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr(d)), "l"(s) : "memory");
+}
+__device__ __forceinline__ void mbar_init(u64 *b, int n)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *b, u32 parity)
+{
+    asm volatile("{\n\t.reg .pred p;\nQJ_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra QJ_WAIT_%=;\n\t}" ::"r"(saddr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(u64 *b)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ int ring_bar(int it) { return it % KSTAGES + KSTAGES * ((it / KSTAGES) & 1); }
+
+__device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar);
+
+extern "C" __global__ void __launch_bounds__(2 * KT, 1)
+qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_offhi,
+         const int *__restrict__ g_geo)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    u64 *full = reinterpret_cast<u64 *>(smem_raw);
+    u32 *st_k = reinterpret_cast<u32 *>(full + 2 * KSTAGES);
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);
+    u64 *offhi = reinterpret_cast<u64 *>(bufs + KSTAGES * TSIZE);
+    const int nhi = 1 << (12 - c);
+    const u32 tid_all = threadIdx.x;
+    for (int i = tid_all; i < nhi; i += 2 * KT) offhi[i] = __ldg(g_offhi + i);
+    if (tid_all < 16) {
+        u32 v = 0;
+        for (int j = 0; j < 4; ++j)
+            if ((tid_all >> j) & 1u) v ^= (u32)__ldg(g_geo + 40 + j);
+        st_k[tid_all] = v;
+    }
+    if (tid_all == 0) {
+        for (int s = 0; s < 2 * KSTAGES; ++s) mbar_init(full + s, KT);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const u64 ntiles = 1ull << ncomp;
+    if ((u64)blockIdx.x >= ntiles) return;
+    const int T = (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1;
+    const int grp = (int)(tid_all / KT);
+    const u32 tid = tid_all % KT;
+    const int bar = 1 + grp;
+    const int lane = tid & 31;
+    const int comp_lane = __ldg(g_geo + lane);
+    const u32 cmask = (1u << c) - 1u;
+    u32 st_base = (u32)__ldg(g_geo + 44);
+    for (int i = 0; i < 8; ++i)
+        if ((tid >> i) & 1u) st_base ^= (u32)__ldg(g_geo + 32 + i);
+    auto load = [&](int it) {
+        const u64 tile = blockIdx.x + (u64)it * gridDim.x;
+        const u64 b = tbase(tile, lane, ncomp, comp_lane);
+        double2 *buf = bufs + (it % KSTAGES) * TSIZE;
+        const double2 *src = psi + b;
+#pragma unroll 4
+        for (int k = 0; k < TSIZE / KT; ++k) {
+            const u32 l = tid + k * KT;
+            cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
+        }
+        cp_async_mbar_arrive(full + ring_bar(it));
+    };
+    if (grp == 0) {
+        load(0);
+        if (T > 2) load(2);
+    } else if (T > 1) {
+        load(1);
+    }
+    for (int it = grp; it < T; it += 2) {
+        const int st = it % KSTAGES;
+        const u64 tile = blockIdx.x + (u64)it * gridDim.x;
+        const u64 base = tbase(tile, lane, ncomp, comp_lane);
+        mbar_wait(full + ring_bar(it), (u32)((it / (2 * KSTAGES)) & 1));
+        double2 *sm = bufs + st * TSIZE;
+        apply_tile(sm, tid, bar);
+        double2 *dst = psi + base;
+#pragma unroll 4
+        for (int k = 0; k < TSIZE / KT; ++k) {
+            const u32 l = tid + k * KT;
+            __stcs(dst + (l & cmask) + offhi[l >> c], sm[st_base ^ st_k[k]]);
+        }
+        if (it + KSTAGES < T) {
+            gsync(bar);
+            load(it + KSTAGES);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+)QSV";
+
+struct Module {
+    CUmodule mod = nullptr;
+    CUfunction fn = nullptr;
+    CUdeviceptr cparams = 0;
+    size_t cbytes = 0;
+    bool failed = false;
+    std::vector<char> cubin;
+    std::string log;
+};
+
+// device -> source -> module
+std::unordered_map<std::string, Module> g_mods[64];
+
+bool compile(const std::string &src, Module &m)
+{
+    nvrtcProgram prog = nullptr;
+    if (g_api.CreateProgram(&prog, src.c_str(), "qsv_pass.cu", 0, nullptr, nullptr) != 0) {
+        m.log = "nvrtcCreateProgram failed";
+        return false;
+    }
+    const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                          "--fmad=true"};
+    const int rc = g_api.CompileProgram(prog, 4, opts);
+    size_t ls = 0;
+    g_api.GetProgramLogSize(prog, &ls);
+    if (ls > 1) {
+        m.log.resize(ls);
+        g_api.GetProgramLog(prog, &m.log[0]);
+    }
+    bool ok = rc == 0;
+    if (ok) {
+        size_t n = 0;
+        ok = g_api.GetCUBINSize(prog, &n) == 0 && n > 0;
+        if (ok) {
+            m.cubin.resize(n);
+            ok = g_api.GetCUBIN(prog, m.cubin.data()) == 0;
+        }
+    }
+    g_api.DestroyProgram(&prog);
+    return ok;
+}
+
+bool jit_wanted(int n)
+{
+    const char *e = getenv("QSV_JIT");
+    if (e && e[0] == '0') return false;
+    const char *mq = getenv("QSV_JIT_MIN_QUBITS");
+    const int min_q = mq ? atoi(mq) : 22;
+    return n >= min_q;
+}
+
+}  // namespace
+
+bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const OpRec *ops, int nparams,
+                std::string &src)
+{
+    if (g.m != kMaxTileBits || kBlockBits != 4 || nparams > 8192) return false;
+    constexpr int TB = kMaxTileBits - kBlockBits;  // 8 thread-index bits
+    std::string body;
+    body.reserve(4096 + 160 * nblocks);
+    char buf[256];
+    for (int bi = 0; bi < nblocks; ++bi) {
+        const BlockRec &B = blocks[bi];
+        if (B.kind != 0) return false;
+        for (int k = B.op0; k < B.op1; ++k) {
+            const int t = ops[k].type;
+            if (t != OP_U1 && t != OP_U2 && t != OP_DIAG1) return false;
+        }
+        snprintf(buf, sizeof(buf), "  {\n    const u32 sb = %uu", (unsigned)B.tswz);
+        body += buf;
+        for (int i = 0; i < TB; ++i) {
+            snprintf(buf, sizeof(buf), " ^ tb(tid, %d, %uu)", i, (unsigned)B.cols[i]);
+            body += buf;
+        }
+        body += ";\n    double2 a[16];\n";
+        unsigned E[16];
+        for (int r = 0; r < 16; ++r) {
+            unsigned o = 0;
+            for (int j = 0; j < 4; ++j)
+                if ((r >> j) & 1) o ^= B.cols[TB + j];
+            E[r] = o;
+            snprintf(buf, sizeof(buf), "    a[%d] = sm[sb ^ %uu];\n", r, o);
+            body += buf;
+        }
+        for (int k = B.op0; k < B.op1; ++k) {
+            const OpRec &op = ops[k];
+            if (op.type == OP_U1) {
+                const int cls = (op.h >= 0 && op.h <= 2) ? op.h : 0;
+                snprintf(buf, sizeof(buf), "    u1<%d, %d, %d>(a);\n", op.a, cls, op.p);
+            } else if (op.type == OP_U2) {
+                snprintf(buf, sizeof(buf), "    u2<%d, %d, %d>(a);\n", op.a, op.b, op.p);
+            } else if (op.a >= 0) {
+                snprintf(buf, sizeof(buf), "    dg<%d, %d>(a);\n", op.a, op.p);
+            } else {
+                snprintf(buf, sizeof(buf), "    dgt<%d>(a, (tid >> %d) & 1u);\n", op.p, op.b);
+            }
+            body += buf;
+        }
+        for (int r = 0; r < 16; ++r) {
+            snprintf(buf, sizeof(buf), "    sm[sb ^ %uu] = a[%d];\n", E[r], r);
+            body += buf;
+        }
+        body += "  }\n  gsync(bar);\n";
+    }
+    snprintf(buf, sizeof(buf), "#define QSV_NPARAMS %d\n", std::max(1, nparams));
+    src = buf;
+    src += kSkeleton;
+    src += "__device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar)\n{\n";
+    src += body;
+    src += "}\n";
+    return true;
+}
+
+bool jit_enabled(int n) { return jit_wanted(n) && load_api(); }
+
+const char *jit_unavailable_reason() { return g_api.why.c_str(); }
+
+// Compile every not-yet-cached source in parallel (NVRTC is thread-safe),
+// then load the cubins into the current context.
+int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::string &err)
+{
+    if (!load_api()) {
+        err = g_api.why;
+        return 1;
+    }
+    auto &mods = g_mods[device];
+    std::vector<std::pair<const std::string *, Module *>> todo;
+    for (const std::string *s : srcs) {
+        auto it = mods.find(*s);
+        if (it != mods.end()) continue;
+        Module &m = mods[*s];
+        todo.push_back({s, &m});
+    }
+    if (todo.empty()) return 0;
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    size_t next = 0;
+    std::vector<char> ok(todo.size(), 0);
+    auto worker = [&](unsigned w) {
+        for (size_t i = w; i < todo.size(); i += hw) ok[i] = compile(*todo[i].first, *todo[i].second);
+    };
+    (void)next;
+    for (unsigned w = 0; w < hw && w < todo.size(); ++w) pool.emplace_back(worker, w);
+    for (auto &t : pool) t.join();
+    for (size_t i = 0; i < todo.size(); ++i) {
+        Module &m = *todo[i].second;
+        if (!ok[i]) {
+            m.failed = true;
+            err = "NVRTC: " + m.log.substr(0, 2000);
+            continue;
+        }
+        if (g_api.ModuleLoadData(&m.mod, m.cubin.data()) != 0 ||
+            g_api.ModuleGetFunction(&m.fn, m.mod, "qsv_pass") != 0 ||
+            g_api.ModuleGetGlobal(&m.cparams, &m.cbytes, m.mod, "C") != 0) {
+            m.failed = true;
+            err = "cuModuleLoadData / GetFunction failed";
+            continue;
+        }
+        const int smem = 256 + 3 * (16 << kMaxTileBits) + 8 * 128;
+        g_api.FuncSetAttribute(m.fn, 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */, smem);
+        m.cubin.clear();
+        m.cubin.shrink_to_fit();
+    }
+    return 0;
+}
+
+// Launch a prepared pass; returns false if its module is unavailable.
+bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims &g,
+                const uint64_t *d_offhi, const int32_t *d_geo, const double *d_params, int nparams,
+                int grid, cudaStream_t st)
+{
+    auto &mods = g_mods[device];
+    auto it = mods.find(src);
+    if (it == mods.end() || it->second.failed || !it->second.fn) return false;
+    Module &m = it->second;
+    if (nparams > 0)
+        if (g_api.MemcpyDtoDAsync(m.cparams, (CUdeviceptr)d_params, (size_t)nparams * 8, st) != 0)
+            return false;
+    int ncomp = g.ncomp, c = g.c;
+    void *args[] = {&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo};
+    const unsigned smem = 256 + 3 * (16u << kMaxTileBits) + 8u * (1u << (kMaxTileBits - g.c));
+    return g_api.LaunchKernel(m.fn, (unsigned)grid, 1, 1, 512, 1, 1, smem, st, args, nullptr) == 0;
+}
+
+}  // namespace qsv

@@ -90,6 +90,7 @@ struct Item {
     uint64_t req = 0;         // qubits that must be tile-local
     uint64_t a_union = 0, b_union = 0;
     int cluster = -1;         // dense-fused gate cluster (index into ProgramTemplate::cfills)
+    int cost = 2;             // FP64 work (complex FMAs per amplitude) -- bounds a pass
 };
 
 bool conflict(const Item &A, const Item &B, const std::vector<Rot> &R)
@@ -110,6 +111,7 @@ struct Schedule {
     std::vector<std::vector<int>> pass_items;
     std::vector<uint64_t> pass_hi;
     std::vector<bool> pass_global;
+    std::vector<int> pass_cost;
 };
 
 Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int n, int m, int c)
@@ -118,6 +120,11 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
     const uint64_t low = c >= 64 ? ~0ull : ((1ull << c) - 1ull);
     const int free_slots = m - c;
     std::vector<int> item_pass(items.size(), 0);
+    // FP64 budget of one pass (complex FMAs per amplitude).  A pass much
+    // heavier than the HBM time of a pass only grows the specialised kernel
+    // past the instruction cache; the excess is better spent in later passes.
+    const char *env_cap = getenv("QSV_PASS_COST_CAP");
+    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 40;
     for (size_t i = 0; i < items.size(); ++i) {
         const Item &it = items[i];
         const uint64_t need = it.req & ~low;
@@ -135,7 +142,8 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
         if (fits) {
             for (int p = earliest; p <= last; ++p) {
                 if (S.pass_global[p]) continue;
-                if (popc64(S.pass_hi[p] | need) <= free_slots) {
+                if (popc64(S.pass_hi[p] | need) <= free_slots &&
+                    (S.pass_cost[p] + it.cost <= cost_cap || it.cost == 0)) {
                     placed = p;
                     break;
                 }
@@ -147,10 +155,12 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
             S.pass_items.emplace_back();
             S.pass_hi.push_back(0);
             S.pass_global.push_back(!fits);
+            S.pass_cost.push_back(0);
             placed = (int)S.pass_items.size() - 1;
         }
         S.pass_items[placed].push_back((int)i);
         S.pass_hi[placed] |= need;
+        S.pass_cost[placed] += it.cost;
         item_pass[i] = placed;
     }
     return S;
@@ -235,6 +245,7 @@ void build_items_from_rots(const std::vector<Rot> &R, std::vector<Item> &items)
         }
         Item it;
         it.rot = true;
+        it.cost = 0;
         it.rots.push_back((int)r);
         it.a_union = a;
         it.b_union = b;
@@ -284,7 +295,7 @@ void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t
         bool live = false;
     };
     std::vector<Open> cl;
-    static const char *env_fuse = getenv("QSV_FUSE_QUBITS");  // 0 / 1 / 2 (default 2)
+    const char *env_fuse = getenv("QSV_FUSE_QUBITS");  // 0 / 1 / 2 (default 2)
     const int max_q = env_fuse ? std::max(0, std::min(2, atoi(env_fuse))) : 2;
     int open_of[kMaxQubits];
     for (int q = 0; q < kMaxQubits; ++q) open_of[q] = -1;
@@ -297,6 +308,7 @@ void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t
         if (qubits[2 * gi + 1] >= 0) s |= 1ull << qubits[2 * gi + 1];
         it.supp = s;
         it.req = s;
+        it.cost = gate_cost(kinds[gi]);
         return it;
     };
     auto close = [&](int ci) {
@@ -318,6 +330,7 @@ void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t
             it.cluster = (int)t.cfills.size();
             it.supp = C.qs;
             it.req = C.qs;
+            it.cost = fused_cost;
             t.cfills.push_back(std::move(cf));
             out.push_back(std::move(it));
         } else {
@@ -548,6 +561,11 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
                     case K_CU3: op.type = OP_U2; break;
                     default: op.type = OP_U1; break;
                 }
+                // matrix class of a U1 (lets specialised passes drop zero
+                // imaginary parts): 2 = all entries real (H, RY),
+                // 1 = m00 real (U3: m00 = cos(theta/2); HY)
+                if (op.type == OP_U1)
+                    op.h = (kind == K_H || kind == K_RY) ? 2 : (kind == K_U3 || kind == K_HY) ? 1 : 0;
                 const int np = param_count(kind);
                 if (np) {
                     op.p = (int)t.n_params;
@@ -883,6 +901,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
             } else {
                 Item it;
                 it.rot = true;
+            it.cost = 0;  // rotation groups run in the interpreted kernel: no pass budget
                 it.rots.push_back(r);
                 it.a_union = a;
                 it.b_union = b;
@@ -898,6 +917,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
             if (qubits[2 * i + 1] >= 0) s |= 1ull << qubits[2 * i + 1];
             it.supp = s;
             it.req = s;
+            it.cost = gate_cost(kinds[i]);
             items.push_back(std::move(it));
             ++i;
         }

@@ -714,9 +714,17 @@ tile_ws_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__re
 // computing and storing tile it, the group refills that stage with tile it+3
 // (which the *other* group will compute), so one tile load is always in
 // flight while both groups run FP64 work: HBM streaming overlaps compute.
-// full[s] is completed by the 256 noinc cp.async arrivals of the loading
-// group; each group syncs its own blocks on named barrier 1 + g.
+// Tile it's arrival barrier is full[it % 3 + 3 * ((it / 3) & 1)], completed
+// by the 256 noinc cp.async arrivals of the loading group.  Two barriers per
+// stage: a group may reach tile it before the other group's tile it - 3 of
+// the same stage has landed, or after tile it's own load already landed, and a
+// parity wait can only tell the current phase from the previous one -- with
+// the barrier reused every 6 tiles (always by the same group) the phase being
+// waited on is always the current or the just-completed one.  Each group syncs
+// its own blocks on named barrier 1 + g.
 constexpr int kRingThreads = 2 * kT;
+
+__device__ __forceinline__ int ring_bar(int it) { return it % kStages + kStages * ((it / kStages) & 1); }
 
 template <bool STAGED>
 __global__ void __launch_bounds__(kRingThreads, 1)
@@ -726,8 +734,8 @@ tile_ring_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int m = kMaxTileBits;
     constexpr int tsize = 1 << m;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);            // [kStages]
-    uint32_t *st_k = reinterpret_cast<uint32_t *>(full + kStages);      // [16]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);            // [2 * kStages]
+    uint32_t *st_k = reinterpret_cast<uint32_t *>(full + 2 * kStages);  // [16]
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);        // kStages x tsize
     const int c = g.c;
     uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + kStages * tsize);
@@ -763,7 +771,7 @@ tile_ring_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__
         st_k[tid_all] = v;
     }
     if (tid_all == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(full + st, kT);
+        for (int st = 0; st < 2 * kStages; ++st) mbar_init(full + st, kT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -791,7 +799,7 @@ tile_ring_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__
             const uint32_t l = tid + k * kT;
             cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
         }
-        cp_async_mbar_arrive(full + (it % kStages));
+        cp_async_mbar_arrive(full + ring_bar(it));
     };
     // prologue: group 0 loads tiles 0 and 2, group 1 loads tile 1
     if (grp == 0) {
@@ -804,12 +812,7 @@ tile_ring_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__
         const int st = it % kStages;
         const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
         const uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
-        // The other group may still be on tile it - 3 of this stage (its load
-        // may not even have landed): a parity wait only distinguishes the
-        // current phase from the previous one, so first wait for tile it - 3's
-        // phase, then for tile it's.
-        if (it >= kStages) mbar_wait(full + st, (uint32_t)(((it / kStages) - 1) & 1));
-        mbar_wait(full + st, (uint32_t)((it / kStages) & 1));
+        mbar_wait(full + ring_bar(it), (uint32_t)((it / (2 * kStages)) & 1));
         double2 *sm = bufs + st * tsize;
         run_blocks<true, -1>(sm, blocks, prog.nblocks, ops, rots, params, base, tid, m, bar_id);
         // run_blocks ends with a group barrier: the tile is final in SMEM

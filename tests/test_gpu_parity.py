@@ -254,3 +254,39 @@ def test_backend_protocol_and_errors():
         sv.init_state("0" * 40)
     psi = be.evolve(s0, circ)
     assert abs(be.overlap(psi, s0) + np.sqrt(0.5)) <= 1e-15  # H|1> = (|0> - |1>)/sqrt2 on qubit 0
+
+
+@pytest.fixture
+def jit_from_14(monkeypatch):
+    """Specialise (NVRTC) tile passes from 14 qubits so the JIT path is
+    checked against the oracle at sizes the oracle finishes quickly."""
+    from paper_2208_10978_b200 import _lib
+
+    monkeypatch.setenv("QSV_JIT_MIN_QUBITS", "14")
+    available, _ = _lib.jit_info()
+    assert available, "NVRTC / driver API not loadable on the GPU box"
+    return _lib
+
+
+@pytest.mark.parametrize("fuse", ["0", "1", "2"])
+def test_jit_brickwork_vs_oracle(jit_from_14, monkeypatch, fuse):
+    monkeypatch.setenv("QSV_FUSE_QUBITS", fuse)
+    _, before = jit_from_14.jit_info()
+    circ = W.brickwork(16, 8, seed=12 + int(fuse))  # distinct structure per setting (plan cache)
+    out = sv.evolve(sv.init_state("0" * 16), circ).amplitudes
+    ref = O.evolve(O.init_state("0" * 16), circ.gates)
+    assert np.abs(out - ref).max() <= AMP_TOL
+    _, after = jit_from_14.jit_info()
+    assert after > before  # the specialised kernels ran
+
+
+@pytest.mark.parametrize("n,g", [(14, 400), (17, 500)])
+def test_jit_random_mixed_vs_oracle(jit_from_14, n, g):
+    # every gate kind: H HY X CNOT SWAP RZ RY U3 CU3 -> U1 classes, U2, diagonals,
+    # permutations folded into the tile map
+    rng = np.random.default_rng(300 + n)
+    circ = random_mixed(n, g, rng)
+    st = random_state(n, rng)
+    out = sv.evolve(sv.from_amplitudes(st), circ).amplitudes
+    ref = O.evolve(st, circ.gates)
+    assert np.abs(out - ref).max() <= AMP_TOL
