@@ -42,6 +42,9 @@ N_QUBITS = 28
 LAYERS = 20
 SEED = 0
 REF_SAMPLE_GATES = 6  # reference arm: first gates of the circuit per step (~1.2-2.5 s each)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2
+# dram__bytes_read.sum + dram__bytes_write.sum of one config-2 pass (ncu --set full, r01)
+TRAFFIC_PER_LAUNCH = 4.295412e9 + 4.238421e9
 
 
 def load_peaks() -> tuple[float, str]:
@@ -344,6 +347,7 @@ def run_engine(args, rank, world, local):
         t_max = float(tt.item())
 
     value = world * G * dim / t_max
+    n_u1 = sum(1 for g in circ.gates if len(g.qubits) == 1)
 
     # e2e: public API with host buffers (gate arrays in, full state out to pinned host)
     host_out = torch.empty(dim, dtype=torch.complex128, pin_memory=True).numpy()
@@ -378,9 +382,17 @@ def run_engine(args, rank, world, local):
         "e2e": {"value": e2e_val, "unit": "amplitude-updates/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": 16 * dim, "ms_per_step": t_e2e * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "tile_block_kernel",
+                     "frac": achieved / peak, "traffic": TRAFFIC_PER_LAUNCH,
+                     "kernel": "qsv_pass (NVRTC-specialised tile pass)",
                      "ms_per_launch": t_pass * 1e3, "peak_source": peak_kind,
-                     "algorithmic_bytes_per_launch": 32 * dim},
+                     "algorithmic_bytes_per_launch": 32 * dim,
+                     "traffic_source": "ncu dram__bytes_read+write of one pass (profiles/r01_jit_pass_ncu.txt)"},
+        # the pass is FP64-bound as much as HBM-bound: 560 dense 2x2 complex
+        # gates x 2^28 amplitudes x 8 real FMAs = 1.2e12 DFMA per step
+        "fp64": {"dfma_per_step": n_u1 * dim * 8, "achieved_tflops": 2 * n_u1 * dim * 8 / t_step / 1e12,
+                 "peak_tflops": FP64_PEAK_TFLOPS,
+                 "frac": 2 * n_u1 * dim * 8 / t_step / 1e12 / FP64_PEAK_TFLOPS,
+                 "peak_source": "148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200 FP64 vector)"},
         "gpu_launches": args.steps * (passes + 1),
         "clocks": clocks.summary(),
     }

@@ -124,7 +124,7 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
     // heavier than the HBM time of a pass only grows the specialised kernel
     // past the instruction cache; the excess is better spent in later passes.
     const char *env_cap = getenv("QSV_PASS_COST_CAP");
-    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 40;
+    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 48;
     for (size_t i = 0; i < items.size(); ++i) {
         const Item &it = items[i];
         const uint64_t need = it.req & ~low;
@@ -283,6 +283,9 @@ int gate_cost(int kind)
 // otherwise the clusters that would widen it are closed (emitted) first.
 // A closed cluster becomes one dense 2x2 / 4x4 item when that is cheaper than
 // its gates (e.g. U3 U3 CNOT U3 U3: 8 -> 4 complex FMAs per amplitude).
+// Default width is 1 (runs of single-qubit gates): measured on B200, the
+// 4x4 form is slower in the specialised passes than the m00-real U3 form it
+// replaces (config-2: 103 vs 97 ms), so QSV_FUSE_QUBITS=2 is opt-in.
 // Emitting at close time is order-safe: everything emitted while a cluster is
 // open acts on disjoint qubits and commutes with it.
 void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t *qubits,
@@ -295,8 +298,8 @@ void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t
         bool live = false;
     };
     std::vector<Open> cl;
-    const char *env_fuse = getenv("QSV_FUSE_QUBITS");  // 0 / 1 / 2 (default 2)
-    const int max_q = env_fuse ? std::max(0, std::min(2, atoi(env_fuse))) : 2;
+    const char *env_fuse = getenv("QSV_FUSE_QUBITS");  // 0 / 1 / 2 (default 1)
+    const int max_q = env_fuse ? std::max(0, std::min(2, atoi(env_fuse))) : 1;
     int open_of[kMaxQubits];
     for (int q = 0; q < kMaxQubits; ++q) open_of[q] = -1;
     std::vector<Item> out;
