@@ -256,7 +256,9 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
             o.nops = (int)lops.size();
             o.nrots = r_hi - r_lo;
             o.npar = p_hi - p_lo;
-            if (jit) jit_source(p.geom, lblk.data(), o.nblk, lops.data(), o.npar, jit_src[k]);
+            if (jit)
+                jit_source(p.geom, lblk.data(), o.nblk, lops.data(), t.rots.data() + r_lo, o.npar,
+                           jit_src[k]);
             o.blk = b.add(lblk.data(), lblk.size() * sizeof(BlockRec));
             o.ops = b.add(lops.data(), lops.size() * sizeof(OpRec));
             o.rots = b.add(t.rots.data() + r_lo, (size_t)o.nrots * sizeof(RotRec));

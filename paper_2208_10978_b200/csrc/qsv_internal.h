@@ -159,8 +159,8 @@ int expect_sweep_grid(const TileDims &g, int nterms, int ndiag);
 // run-time specialised tile passes (qsv_jit.cpp)
 bool jit_enabled(int n_qubits);
 const char *jit_unavailable_reason();
-bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const OpRec *ops, int nparams,
-                std::string &src);
+bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const OpRec *ops,
+                const RotRec *rots, int nparams, std::string &src);
 int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::string &err);
 bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims &g,
                 const uint64_t *d_offhi, const int32_t *d_geo, const double *d_params, int nparams,

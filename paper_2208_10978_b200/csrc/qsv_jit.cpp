@@ -194,6 +194,50 @@ __device__ __forceinline__ void dgt(double2 (&a)[16], bool bit)
     for (int r = 0; r < 16; ++r) a[r] = cmul(dr, di, a[r]);
 }
 
+// fused same-flip rotation group on block-local flip F (highest bit H): per
+// pair one 2x2 from the cp = 0 half of the table, selected by the flip
+// pattern of r ^ F; the other parity uses Z M Z (negated off-diagonals),
+// applied as sign flips of y and of the second output.
+__host__ __device__ constexpr int hbit(int v) { return v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
+__host__ __device__ constexpr int par4(int v) { return (v ^ (v >> 1) ^ (v >> 2) ^ (v >> 3)) & 1; }
+template <int F>
+__device__ __forceinline__ constexpr int gm_cfg(int r1)
+{
+    int out = 0, k = 0;
+    const int H = hbit(F);
+    for (int b = 0; b < 4; ++b)
+        if (((F >> b) & 1) && b != H) {
+            out |= ((r1 >> b) & 1) << k;
+            ++k;
+        }
+    return out;
+}
+__device__ __forceinline__ double negif(double v, u32 s)
+{
+    return __longlong_as_double(__double_as_longlong(v) ^ ((long long)s << 63));
+}
+template <int F, int P, int ZB>
+__device__ __forceinline__ void gm(double2 (&a)[16], u32 par0)
+{
+    constexpr int H = hbit(F);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if (r & (1 << H)) continue;
+        const int r1 = r ^ F;
+        const u32 cp = par0 ^ (u32)par4(r1 & ZB);
+        const int M = P + 8 * gm_cfg<F>(r1);
+        const double2 x = a[r], yy = a[r1];
+        const double2 y = make_double2(negif(yy.x, cp), negif(yy.y, cp));
+        double2 o0, o1;
+        o0.x = fma(C[M], x.x, fma(-C[M + 1], x.y, fma(C[M + 2], y.x, -C[M + 3] * y.y)));
+        o0.y = fma(C[M], x.y, fma(C[M + 1], x.x, fma(C[M + 2], y.y, C[M + 3] * y.x)));
+        o1.x = fma(C[M + 4], x.x, fma(-C[M + 5], x.y, fma(C[M + 6], y.x, -C[M + 7] * y.y)));
+        o1.y = fma(C[M + 4], x.y, fma(C[M + 5], x.x, fma(C[M + 6], y.y, C[M + 7] * y.x)));
+        a[r] = o0;
+        a[r1] = make_double2(negif(o1.x, cp), negif(o1.y, cp));
+    }
+}
+
 __device__ __forceinline__ u32 swz(u32 l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
 __device__ __forceinline__ u32 tb(u32 tid, int i, u32 col) { return (0u - ((tid >> i) & 1u)) & col; }
 __device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
@@ -226,7 +270,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive(u64 *b)
 }
 __device__ __forceinline__ int ring_bar(int it) { return it % KSTAGES + KSTAGES * ((it / KSTAGES) & 1); }
 
-__device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar);
+__device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar, u64 base);
 
 extern "C" __global__ void __launch_bounds__(2 * KT, 1)
 qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_offhi,
@@ -287,7 +331,7 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
         const u64 base = tbase(tile, lane, ncomp, comp_lane);
         mbar_wait(full + ring_bar(it), (u32)((it / (2 * KSTAGES)) & 1));
         double2 *sm = bufs + st * TSIZE;
-        apply_tile(sm, tid, bar);
+        apply_tile(sm, tid, bar, base);
         double2 *dst = psi + base;
 #pragma unroll 4
         for (int k = 0; k < TSIZE / KT; ++k) {
@@ -356,8 +400,8 @@ bool jit_wanted(int n)
 
 }  // namespace
 
-bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const OpRec *ops, int nparams,
-                std::string &src)
+bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const OpRec *ops,
+                const RotRec *rots, int nparams, std::string &src)
 {
     if (g.m != kMaxTileBits || kBlockBits != 4 || nparams > 8192) return false;
     constexpr int TB = kMaxTileBits - kBlockBits;  // 8 thread-index bits
@@ -369,7 +413,7 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
         if (B.kind != 0) return false;
         for (int k = B.op0; k < B.op1; ++k) {
             const int t = ops[k].type;
-            if (t != OP_U1 && t != OP_U2 && t != OP_DIAG1) return false;
+            if (t != OP_U1 && t != OP_U2 && t != OP_DIAG1 && t != OP_GMAT) return false;
         }
         snprintf(buf, sizeof(buf), "  {\n    const u32 sb = %uu", (unsigned)B.tswz);
         body += buf;
@@ -394,6 +438,13 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
                 snprintf(buf, sizeof(buf), "    u1<%d, %d, %d>(a);\n", op.a, cls, op.p);
             } else if (op.type == OP_U2) {
                 snprintf(buf, sizeof(buf), "    u2<%d, %d, %d>(a);\n", op.a, op.b, op.p);
+            } else if (op.type == OP_GMAT) {
+                // common sign masks of the group (qsv_planner.cpp block_pass)
+                const RotRec &rc = rots[op.r0];
+                const unsigned zb = ((unsigned)rc.q >> 8) & 15u, zt = (unsigned)rc.q >> 12;
+                snprintf(buf, sizeof(buf),
+                         "    gm<%u, %d, %u>(a, (u32)((__popcll(base & %lluull) + __popc(tid & %uu)) & 1));\n",
+                         op.f, op.p, zb, (unsigned long long)rc.s_hi, zt);
             } else if (op.a >= 0) {
                 snprintf(buf, sizeof(buf), "    dg<%d, %d>(a);\n", op.a, op.p);
             } else {
@@ -410,7 +461,7 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
     snprintf(buf, sizeof(buf), "#define QSV_NPARAMS %d\n", std::max(1, nparams));
     src = buf;
     src += kSkeleton;
-    src += "__device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar)\n{\n";
+    src += "__device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar, u64 base)\n{\n";
     src += body;
     src += "}\n";
     return true;
@@ -461,7 +512,7 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
             err = "cuModuleLoadData / GetFunction failed";
             continue;
         }
-        const int smem = 256 + 3 * (16 << kMaxTileBits) + 8 * 128;
+        const int smem = 256 + 3 * (16 << kMaxTileBits) + 8 * (1 << (kMaxTileBits - 1));  // any c >= 1
         g_api.FuncSetAttribute(m.fn, 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */, smem);
         m.cubin.clear();
         m.cubin.shrink_to_fit();

@@ -44,7 +44,8 @@ void choose_tile(int n, int &m, int &c)
     if (m == n) {
         c = n;
     } else {
-        c = kMinContig;
+        const char *env_c = getenv("QSV_MIN_CONTIG");  // low contiguous tile bits (default 3: 128 B segments)
+        c = env_c ? std::max(1, std::min(kMinContig, atoi(env_c))) : 3;
         if (c > m - 4) c = m - 4;
         if (c < 0) c = 0;
     }

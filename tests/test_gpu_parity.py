@@ -290,3 +290,30 @@ def test_jit_random_mixed_vs_oracle(jit_from_14, n, g):
     out = sv.evolve(sv.from_amplitudes(st), circ).amplitudes
     ref = O.evolve(st, circ.gates)
     assert np.abs(out - ref).max() <= AMP_TOL
+
+
+@pytest.mark.parametrize("n,ne", [(14, 6), (16, 8)])
+def test_jit_ucc_groups_vs_oracle(jit_from_14, n, ne):
+    # UCC-shaped circuits: fused same-flip groups (OP_GMAT) in specialised passes
+    cfg = W.config1(seed=n, n_qubits=n, n_electrons=ne, n_terms=200)
+    _, before = jit_from_14.jit_info()
+    psi = sv.evolve(sv.init_state(cfg["reference"]), cfg["circuit"])
+    _, after = jit_from_14.jit_info()
+    ref = O.evolve(O.init_state(cfg["reference"]), cfg["circuit"].gates)
+    assert np.abs(psi.amplitudes - ref).max() <= AMP_TOL
+    assert after > before
+    e = sv.expectation(psi, cfg["hamiltonian"])
+    assert rel(e, O.expectation(ref, cfg["hamiltonian"], n)) <= REL_TOL
+
+
+def test_jit_rotations_mixed_vs_oracle(jit_from_14):
+    n = 16
+    rng = np.random.default_rng(77)
+    strings, thetas = random_rotations(n, 150, rng, max_w=4)
+    strings += strings[:20]
+    thetas += thetas[:20]
+    circ = W.rotations_circuit(n, strings, thetas)
+    st = random_state(n, rng)
+    out = sv.evolve(sv.from_amplitudes(st), circ).amplitudes
+    ref = O.evolve(st, circ.gates)
+    assert np.abs(out - ref).max() <= AMP_TOL
