@@ -159,6 +159,8 @@ constexpr size_t kCacheMax = 8;
 struct ExpCacheEntry {
     uint64_t hash;
     int n;
+    bool jit = false;
+    std::vector<std::string> jit_src;  // per sweep ("" = interpreted)
     std::vector<uint64_t> x, y, z;
     std::vector<SweepPlan> plan;
 };
@@ -614,14 +616,17 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
     if (int rc = ctx_for(s->device, &c)) return rc;
 
     const uint64_t h = hash_masks(s->n, S, x, y, z);
+    const bool jit = jit_enabled(s->n);
     std::vector<SweepPlan> *plan = nullptr;
+    std::vector<std::string> *jsrc = nullptr;
     bool hit = false;
     for (auto it = g_exp_cache.begin(); it != g_exp_cache.end(); ++it) {
-        if (it->hash == h && it->n == s->n && (int64_t)it->x.size() == S &&
+        if (it->hash == h && it->n == s->n && it->jit == jit && (int64_t)it->x.size() == S &&
             std::memcmp(it->x.data(), x, S * 8) == 0 && std::memcmp(it->y.data(), y, S * 8) == 0 &&
             std::memcmp(it->z.data(), z, S * 8) == 0) {
             g_exp_cache.splice(g_exp_cache.begin(), g_exp_cache, it);
             plan = &g_exp_cache.front().plan;
+            jsrc = &g_exp_cache.front().jit_src;
             hit = true;
             break;
         }
@@ -633,10 +638,23 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
         e.x.assign(x, x + S);
         e.y.assign(y, y + S);
         e.z.assign(z, z + S);
-        plan_expectation(s->n, S, x, y, z, e.plan);
+        e.jit = jit;
+        plan_expectation(s->n, S, x, y, z, e.plan, jit);
+        e.jit_src.resize(e.plan.size());
+        if (jit)
+            for (size_t k = 0; k < e.plan.size(); ++k) jit_sweep_source(e.plan[k], e.jit_src[k]);
         g_exp_cache.push_front(std::move(e));
         if (g_exp_cache.size() > 4) g_exp_cache.pop_back();
         plan = &g_exp_cache.front().plan;
+        jsrc = &g_exp_cache.front().jit_src;
+    }
+    if (jit) {
+        std::vector<const std::string *> srcs;
+        for (const std::string &src : *jsrc)
+            if (!src.empty()) srcs.push_back(&src);
+        std::string err;
+        if (!srcs.empty() && jit_prepare(s->device, srcs, err) && getenv("QSV_JIT_VERBOSE"))
+            fprintf(stderr, "qsv jit: %s\n", err.c_str());
     }
     // blob: per sweep groups / terms / map / gflip
     Blob b;
@@ -659,7 +677,8 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
         }
         o.rows = sp.global ? expect_global_grid(s->n)
                            : expect_sweep_grid(dims_of(sp.geom), (int)sp.terms.size(), sp.ndiag);
-        max_partial = std::max(max_partial, (size_t)o.rows * sp.terms.size());
+        max_partial = std::max(max_partial, (size_t)std::max(o.rows, 16 * num_sms(s->device)) *
+                                                sp.terms.size());
         offs.push_back(o);
     }
     const size_t per_term_bytes = ((size_t)S * 8 + 255) & ~(size_t)255;
@@ -680,6 +699,15 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
                                           (const uint64_t *)(d + o.f), (int)sp.groups.size(),
                                           (const TermRec *)(d + o.t), nterms, d_partial, &rows,
                                           s->stream));
+        } else if (jit && !(*jsrc)[k].empty() &&
+                   jit_sweep_launch(s->device, (*jsrc)[k], s->amps, dims_of(sp.geom),
+                                    (const uint64_t *)(d + o.off), (const int32_t *)(d + o.comp),
+                                    d_partial,
+                                    (int)std::min<uint64_t>(1ull << sp.geom.ncomp,
+                                                            (uint64_t)num_sms(s->device)),
+                                    s->stream)) {
+            rows = 16 * (int)std::min<uint64_t>(1ull << sp.geom.ncomp, (uint64_t)num_sms(s->device));
+            ++g_jit_launches;
         } else {
             QSV_CUDA(launch_expect_sweep(s->amps, dims_of(sp.geom), (const uint64_t *)(d + o.off),
                                          (const int32_t *)(d + o.comp), (const GroupRec *)(d + o.g),

@@ -165,6 +165,11 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
 bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims &g,
                 const uint64_t *d_offhi, const int32_t *d_geo, const double *d_params, int nparams,
                 int grid, cudaStream_t st);
+struct SweepPlan;
+bool jit_sweep_source(const SweepPlan &sp, std::string &src);
+bool jit_sweep_launch(int device, const std::string &src, const double2 *psi, const TileDims &g,
+                      const uint64_t *d_offhi, const int32_t *d_geo, double *d_partial, int grid,
+                      cudaStream_t st);
 cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,
                          double bre, double bim, cudaStream_t st);
 

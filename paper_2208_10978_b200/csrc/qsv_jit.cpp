@@ -36,6 +36,7 @@
 #include <vector>
 
 #include "qsv_internal.h"
+#include "qsv_planner.h"
 
 namespace qsv {
 
@@ -347,7 +348,159 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
 }
 )QSV";
 
+
+// ---- expectation sweep skeleton (read-only ring; per-lane term accumulators) ----
+const char *kSweepSkeleton = R"QSV(
+typedef unsigned long long u64;
+typedef unsigned int u32;
+#define KT 256
+#define KSTAGES 3
+#define TSIZE 4096
+__device__ __forceinline__ u32 swz(u32 l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+__device__ __forceinline__ u32 ins0(u32 i, int b) { return ((i >> b) << (b + 1)) | (i & ((1u << b) - 1u)); }
+__device__ __forceinline__ double wsum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double sgn(u32 lane, u32 sl, u64 base, u64 sh)
+{
+    return ((__popc(lane & sl) + __popcll(base & sh)) & 1) ? -1.0 : 1.0;
+}
+// Pair products w = conj(psi_l0) psi_l0^F for the thread's 8 pairs
+// p = pl + 256 j (pl = lane + 32 warp; pair index = l0 with bit H removed),
+// then an 8-point Walsh-Hadamard transform over j: W[m] = sum_j (-1)^{|j & m|} w_j,
+// so a string whose sign mask has pair bits 8..10 = m reads W[m].  All eight
+// warps of a tile group run the same group code on disjoint pairs (one
+// instruction stream -> no I-cache pressure).
+template <bool RE, bool IM, int H>
+__device__ __forceinline__ void wht8(const double2 *sm, u32 pl, u32 sF, double (&Wr)[8], double (&Wi)[8])
+{
+    const u32 b0 = swz(ins0(pl, H));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const u32 a0 = b0 ^ swz(ins0(256u * j, H));
+        const double2 x = sm[a0], y = sm[a0 ^ sF];
+        if (RE) Wr[j] = fma(x.x, y.x, x.y * y.y);
+        if (IM) Wi[j] = fma(x.x, y.y, -x.y * y.x);
+    }
+#pragma unroll
+    for (int b = 1; b < 8; b <<= 1) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (r & b) continue;
+            if (RE) { const double u = Wr[r], v = Wr[r | b]; Wr[r] = u + v; Wr[r | b] = u - v; }
+            if (IM) { const double u = Wi[r], v = Wi[r | b]; Wi[r] = u + v; Wi[r | b] = u - v; }
+        }
+    }
+}
+__device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ u64 tbase(u64 tile, int lane, int ncomp, int comp_lane)
+{
+    u64 bit = (lane < ncomp && ((tile >> lane) & 1ull)) ? (1ull << comp_lane) : 0ull;
+    u32 lo = __reduce_or_sync(0xffffffffu, (u32)bit);
+    u32 hi = __reduce_or_sync(0xffffffffu, (u32)(bit >> 32));
+    return ((u64)hi << 32) | lo;
+}
+__device__ __forceinline__ u32 saddr(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void *d, const void *s)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr(d)), "l"(s) : "memory");
+}
+__device__ __forceinline__ void mbar_init(u64 *b, int n)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *b, u32 parity)
+{
+    asm volatile("{\n\t.reg .pred p;\nQS_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra QS_WAIT_%=;\n\t}" ::"r"(saddr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(u64 *b)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ int ring_bar(int it) { return it % KSTAGES + KSTAGES * ((it / KSTAGES) & 1); }
+
+// generated: every flip group of the sweep on one tile (acc[] persists across tiles)
+__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT]);
+
+extern "C" __global__ void __launch_bounds__(2 * KT, 1)
+qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_offhi,
+          const int *__restrict__ g_geo, double *__restrict__ partial)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    u64 *full = reinterpret_cast<u64 *>(smem_raw);
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);
+    u64 *offhi = reinterpret_cast<u64 *>(bufs + KSTAGES * TSIZE);
+    const int nhi = 1 << (12 - c);
+    const u32 tid_all = threadIdx.x;
+    for (int i = tid_all; i < nhi; i += 2 * KT) offhi[i] = __ldg(g_offhi + i);
+    if (tid_all == 0) {
+        for (int s = 0; s < 2 * KSTAGES; ++s) mbar_init(full + s, KT);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const u64 ntiles = 1ull << ncomp;
+    const int grp = (int)(tid_all / KT);
+    const u32 tid = tid_all % KT;
+    const int bar = 1 + grp;
+    const u32 lane = tid & 31;
+    const int warp = (int)(tid >> 5);
+    double acc[MAXT];
+#pragma unroll
+    for (int i = 0; i < MAXT; ++i) acc[i] = 0.0;
+    if ((u64)blockIdx.x < ntiles) {
+        const int T = (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1;
+        const int comp_lane = __ldg(g_geo + lane);
+        const u32 cmask = (1u << c) - 1u;
+        auto load = [&](int it) {
+            const u64 tile = blockIdx.x + (u64)it * gridDim.x;
+            const u64 b = tbase(tile, lane, ncomp, comp_lane);
+            double2 *buf = bufs + (it % KSTAGES) * TSIZE;
+            const double2 *src = psi + b;
+#pragma unroll 4
+            for (int k = 0; k < TSIZE / KT; ++k) {
+                const u32 l = tid + k * KT;
+                cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
+            }
+            cp_async_mbar_arrive(full + ring_bar(it));
+        };
+        if (grp == 0) {
+            load(0);
+            if (T > 2) load(2);
+        } else if (T > 1) {
+            load(1);
+        }
+        for (int it = grp; it < T; it += 2) {
+            const u64 tile = blockIdx.x + (u64)it * gridDim.x;
+            const u64 base = tbase(tile, lane, ncomp, comp_lane);
+            mbar_wait(full + ring_bar(it), (u32)((it / (2 * KSTAGES)) & 1));
+            sweep_tile(bufs + (it % KSTAGES) * TSIZE, tid, base, acc);
+            if (it + KSTAGES < T) {
+                gsync(bar);
+                load(it + KSTAGES);
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    // one row per (CTA, warp): reduce_columns sums rows in a fixed order
+    double *row = partial + (size_t)(blockIdx.x * 16 + grp * 8 + warp) * MAXT;
+#pragma unroll
+    for (int i = 0; i < MAXT; ++i) {
+        const double v = wsum(acc[i]);
+        if (lane == 0) row[i] = v;
+    }
+}
+)QSV";
+
+inline uint32_t h_swz(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+inline uint32_t h_ins0(uint32_t i, int b) { return ((i >> b) << (b + 1)) | (i & ((1u << b) - 1u)); }
+
 struct Module {
+    bool sweep = false;
     CUmodule mod = nullptr;
     CUfunction fn = nullptr;
     CUdeviceptr cparams = 0;
@@ -467,6 +620,45 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
     return true;
 }
 
+
+// Specialised expectation sweep: flip groups only (Z-only strings stay on the
+// interpreted sweep, whose in-tile Walsh-Hadamard transform serves thousands
+// of them at once).  Groups go to the 8 warps of a tile group by
+// longest-processing-time on cost = pairs x (2 + 2 + terms); each warp keeps
+// one per-lane accumulator per string across all of its tiles, so the warp
+// reduction happens once per kernel instead of once per (tile, string).
+bool jit_sweep_source(const SweepPlan &sp, std::string &src)
+{
+    if (sp.global || sp.geom.m != kMaxTileBits || sp.ndiag != 0 || sp.groups.empty()) return false;
+    const int nterms = (int)sp.terms.size();
+    if (nterms > 24) return false;
+    std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";
+    char buf[512];
+    for (const GroupRec &G : sp.groups) {
+        const bool need_re = G.t_im > G.t0, need_im = G.t1 > G.t_im;
+        snprintf(buf, sizeof(buf),
+                 "  { double Wr[8], Wi[8];\n    wht8<%s, %s, %d>(sm, pl, %uu, Wr, Wi);\n",
+                 need_re ? "true" : "false", need_im ? "true" : "false", G.h, h_swz(G.f_loc));
+        fn += buf;
+        for (int t = G.t0; t < G.t1; ++t) {
+            const TermRec &tr = sp.terms[t];
+            // scale folded in: the term's sweep total is scale * sum_p sign(p) w_p
+            snprintf(buf, sizeof(buf),
+                     "    acc[%d] = fma(((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g, %s[%u], acc[%d]);\n",
+                     t, tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale,
+                     tr.use_im ? "Wi" : "Wr", (tr.s_loc >> 8) & 7u, t);
+            fn += buf;
+        }
+        fn += "  }\n";
+    }
+    fn += "}\n";
+    snprintf(buf, sizeof(buf), "#define MAXT %d\n", nterms);
+    src = buf;
+    src += kSweepSkeleton;
+    src += fn;
+    return true;
+}
+
 bool jit_enabled(int n) { return jit_wanted(n) && load_api(); }
 
 const char *jit_unavailable_reason() { return g_api.why.c_str(); }
@@ -485,6 +677,7 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
         auto it = mods.find(*s);
         if (it != mods.end()) continue;
         Module &m = mods[*s];
+        m.sweep = s->find("qsv_sweep(") != std::string::npos;
         todo.push_back({s, &m});
     }
     if (todo.empty()) return 0;
@@ -506,8 +699,8 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
             continue;
         }
         if (g_api.ModuleLoadData(&m.mod, m.cubin.data()) != 0 ||
-            g_api.ModuleGetFunction(&m.fn, m.mod, "qsv_pass") != 0 ||
-            g_api.ModuleGetGlobal(&m.cparams, &m.cbytes, m.mod, "C") != 0) {
+            g_api.ModuleGetFunction(&m.fn, m.mod, m.sweep ? "qsv_sweep" : "qsv_pass") != 0 ||
+            (!m.sweep && g_api.ModuleGetGlobal(&m.cparams, &m.cbytes, m.mod, "C") != 0)) {
             m.failed = true;
             err = "cuModuleLoadData / GetFunction failed";
             continue;
@@ -534,6 +727,22 @@ bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims
             return false;
     int ncomp = g.ncomp, c = g.c;
     void *args[] = {&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo};
+    const unsigned smem = 256 + 3 * (16u << kMaxTileBits) + 8u * (1u << (kMaxTileBits - g.c));
+    return g_api.LaunchKernel(m.fn, (unsigned)grid, 1, 1, 512, 1, 1, smem, st, args, nullptr) == 0;
+}
+
+
+// Launch a prepared expectation sweep; partial gets 16 * grid rows of nterms.
+bool jit_sweep_launch(int device, const std::string &src, const double2 *psi, const TileDims &g,
+                      const uint64_t *d_offhi, const int32_t *d_geo, double *d_partial, int grid,
+                      cudaStream_t st)
+{
+    auto &mods = g_mods[device];
+    auto it = mods.find(src);
+    if (it == mods.end() || it->second.failed || !it->second.fn) return false;
+    Module &m = it->second;
+    int ncomp = g.ncomp, c = g.c;
+    void *args[] = {(void *)&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo, (void *)&d_partial};
     const unsigned smem = 256 + 3 * (16u << kMaxTileBits) + 8u * (1u << (kMaxTileBits - g.c));
     return g_api.LaunchKernel(m.fn, (unsigned)grid, 1, 1, 512, 1, 1, smem, st, args, nullptr) == 0;
 }

@@ -1037,7 +1037,7 @@ void materialize_gmats(const ProgramTemplate &t, double *params)
 // ---------------------------------------------------------------------------
 
 void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, const uint64_t *z,
-                      std::vector<SweepPlan> &out)
+                      std::vector<SweepPlan> &out, bool jit_layout)
 {
     out.clear();
     int m, c;
@@ -1069,7 +1069,7 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     // Bin flip groups into sweeps: a sweep's tile must hold every group's
     // flip bits.  First-fit decreasing on the high-bit need; capacity is
     // bounded by the shared-memory accumulators (kFlipCap strings).
-    const int kFlipCap = 512, kDiagCap = 2048, kGroupCap = 256;
+    const int kFlipCap = jit_layout ? 24 : 512, kDiagCap = 2048, kGroupCap = 256;
     std::vector<int> order(flips.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
@@ -1088,12 +1088,13 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     for (int gi : order) {
         const uint64_t need = flips[gi] & ~low;
         const int nt = (int)members[gi].size();
-        if (popc64(need) > free_slots || nt > kFlipCap) {
+        if (popc64(need) > free_slots || nt > 512) {
             global_groups.push_back(gi);
             continue;
         }
         int placed = -1;
-        for (size_t b = 0; b < bins.size(); ++b) {
+        // a group above the (specialised-sweep) cap gets an interpreted sweep of its own
+        for (size_t b = 0; b < bins.size() && nt <= kFlipCap; ++b) {
             if (bins[b].nterms + nt > kFlipCap || (int)bins[b].groups.size() >= kGroupCap) continue;
             if (popc64(bins[b].hi | need) <= free_slots) {
                 placed = (int)b;
@@ -1108,8 +1109,10 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
         bins[placed].nterms += nt;
         bins[placed].groups.push_back(gi);
     }
-    // Z-only strings ride along with the first sweeps (any tile works)
-    for (size_t d0 = 0, b = 0; d0 < diag.size(); d0 += kDiagCap, ++b) {
+    // Z-only strings ride along with the first sweeps (any tile works), or
+    // get sweeps of their own for the specialised flip-only kernel
+    const size_t first_diag_bin = jit_layout ? bins.size() : 0;
+    for (size_t d0 = 0, b = first_diag_bin; d0 < diag.size(); d0 += kDiagCap, ++b) {
         if (b >= bins.size()) bins.emplace_back();
         bins[b].diag.assign(diag.begin() + d0, diag.begin() + std::min(diag.size(), d0 + kDiagCap));
     }

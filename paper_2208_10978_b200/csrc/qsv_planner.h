@@ -116,8 +116,10 @@ struct SweepPlan {
     std::vector<uint64_t> gflip;  // global fallback: full flip masks per group
 };
 
+// jit_layout: Z-only strings get sweeps of their own (the specialised sweep
+// kernel handles flip groups only) and flip sweeps hold at most 24 strings.
 void plan_expectation(int n, int64_t n_terms, const uint64_t *x, const uint64_t *y,
-                      const uint64_t *z, std::vector<SweepPlan> &out);
+                      const uint64_t *z, std::vector<SweepPlan> &out, bool jit_layout = false);
 
 // Device-side geometry tables of a tile (see TileDims).
 TileDims dims_of(const TileGeom &g);

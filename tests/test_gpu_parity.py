@@ -317,3 +317,20 @@ def test_jit_rotations_mixed_vs_oracle(jit_from_14):
     out = sv.evolve(sv.from_amplitudes(st), circ).amplitudes
     ref = O.evolve(st, circ.gates)
     assert np.abs(out - ref).max() <= AMP_TOL
+
+
+@pytest.mark.parametrize("n,S,zq", [(16, 400, 120), (18, 300, 0)])
+def test_jit_expectation_sweeps_vs_oracle(jit_from_14, n, S, zq):
+    # specialised flip-group sweeps + interpreted Z-only sweeps
+    rng = np.random.default_rng(500 + n)
+    h = W.sparse_random_hamiltonian(n, S, rng, z_only=zq)
+    st = random_state(n, rng)
+    s = sv.from_amplitudes(st)
+    _, before = jit_from_14.jit_info()
+    re, im, per = sv.expectation_terms(s, h)
+    _, after = jit_from_14.jit_info()
+    assert after > before
+    _, ref_per = O.expectation(st, h, n, per_term=True)
+    assert np.abs(per - ref_per[:, 0]).max() <= 1e-12
+    e_ref = O.expectation(st, h, n)
+    assert rel(re, e_ref) <= REL_TOL
