@@ -144,6 +144,44 @@ def gate_matrix(kind: str, values: Sequence[float] = ()) -> np.ndarray:
     return out
 
 
+def _u3_derivative(theta: float, phi: float, lam: float, slot: int) -> np.ndarray:
+    c, s = math.cos(theta / 2), math.sin(theta / 2)
+    if slot == 0:
+        return 0.5 * np.array([[-s, -np.exp(1j * lam) * c],
+                               [np.exp(1j * phi) * c, -np.exp(1j * (phi + lam)) * s]])
+    if slot == 1:
+        return np.array([[0, 0], [1j * np.exp(1j * phi) * s, 1j * np.exp(1j * (phi + lam)) * c]])
+    return np.array([[0, -1j * np.exp(1j * lam) * s], [0, 1j * np.exp(1j * (phi + lam)) * c]])
+
+
+def gate_derivative(kind: str, values: Sequence[float], slot: int) -> np.ndarray:
+    """d(gate matrix)/d(angle in parameter slot) (circuit.py:226-243); generally non-unitary."""
+    if kind == "RZ":
+        lam = values[0]
+        return np.array([[-0.5j * np.exp(-0.5j * lam), 0], [0, 0.5j * np.exp(0.5j * lam)]])
+    if kind == "RY":
+        c, s = math.cos(values[0] / 2), math.sin(values[0] / 2)
+        return 0.5 * np.array([[-s, -c], [c, -s]], dtype=complex)
+    if kind == "U3":
+        return _u3_derivative(*values, slot)
+    if kind == "CU3":
+        out = np.zeros((4, 4), dtype=complex)
+        out[2:, 2:] = _u3_derivative(*values, slot)
+        return out
+    raise ValueError(f"gate kind {kind!r} is not differentiable")
+
+
+def dagger_gate(g: Gate) -> Gate:
+    """Bound gate implementing g^dagger: H, HY, X, CNOT, SWAP are Hermitian;
+    RZ/RY negate the angle; U3(t, p, l)^dagger = U3(-t, -l, -p) (same for CU3)."""
+    if g.kind in ("H", "HY", "X", "CNOT", "SWAP"):
+        return g
+    v = g.bound_values()
+    if g.kind in ("RZ", "RY"):
+        return Gate(g.kind, g.qubits, (Constant(-v[0]),))
+    return Gate(g.kind, g.qubits, (Constant(-v[0]), Constant(-v[2]), Constant(-v[1])))
+
+
 # ---------------------------------------------------------------------------
 # Pauli exponentials (gate pattern of circuit.py:254-281)
 # ---------------------------------------------------------------------------

@@ -40,6 +40,13 @@ class StateVectorBackend:
     def overlap(self, a: sv.StateVector, b: sv.StateVector) -> complex:
         return sv.vdot(a, b)
 
+    def reverse_gradient(self, circuit, theta, h, state0: sv.StateVector):
+        """Device reverse-mode gradient (statevector.py:153-163 semantics).
+        Callers that want it use this method explicitly: the reference's
+        vqe_minimize would route supports_reverse_gradient=True to its own CPU
+        statevector.reverse_gradient (engine.py:463-464)."""
+        return sv.reverse_gradient(circuit, theta, h, state0)
+
 
 @dataclass(frozen=True)
 class ExpectationPlan:

@@ -356,6 +356,84 @@ def vdot(a: StateVector, b: StateVector) -> complex:
     return complex(out[0], out[1])
 
 
+def reverse_gradient(c, theta, h, s0: StateVector) -> np.ndarray:
+    """Gradient of <psi(theta)|H|psi(theta)> over all parameters in one
+    backward sweep with a single application of H (statevector.py:153-163)."""
+    if not h.is_hermitian():
+        raise ValueError("reverse-mode gradient requires a Hermitian operator")
+    return reverse_gradient_general(c, theta, lambda s: apply_operator(s, h), s0)
+
+
+def reverse_gradient_general(c, theta, apply_h, s0: StateVector) -> np.ndarray:
+    """Reverse-mode sweep (Algorithm 1, statevector.py:166-211) on device states.
+
+    Forward evolve to |psi>, |psi_l> = H|psi>, |psi_r> = |psi>; walking the
+    gates backwards, each Affine slot contributes scale * 2 Re <psi_l| dU |psi_r>
+    with psi_r the state before the gate and psi_l the back-propagated H|psi>
+    after it (psi_l is not renormalised).  B200 form: runs of gates without
+    Affine parameters are un-applied as ONE fused gate list per state (the
+    planner's tile passes), and RZ / RY slots use dU = -i/2 P U with U, P
+    commuting, i.e. 2 Re <psi_l|dU|psi_before> = Im <U^dag psi_l| P |psi_before>:
+    one apply_pauli + one vdot instead of a copy, a derivative pass and a vdot.
+    """
+    from .circuit import Affine, Circuit, bind, dagger_gate, gate_derivative
+    from . import kernels
+
+    theta = np.asarray(theta, dtype=float)
+    for gate in c.gates:
+        if gate.params and gate.kind not in ("RZ", "RY", "U3", "CU3"):
+            raise ValueError(f"gate kind {gate.kind} is not differentiable")
+    n = c.n_qubits
+    bound = bind(c, theta)
+    psi = evolve(s0, bound)
+    psi_l = apply_h(psi)
+    psi_r = psi
+    grad = np.zeros(c.n_params)
+    pend_r: list = []
+    pend_l: list = []
+    scratch = None
+
+    def flush(state, pend):
+        if pend:
+            apply_circuit_inplace(state, Circuit(n, tuple(pend), 0))
+            pend.clear()
+
+    for gate, bg in zip(reversed(c.gates), reversed(bound.gates)):
+        slots = [(k, e) for k, e in enumerate(gate.params) if isinstance(e, Affine)]
+        d = dagger_gate(bg)
+        if not slots:
+            pend_r.append(d)
+            pend_l.append(d)
+            continue
+        pend_r.append(d)  # psi_r -> state before the gate
+        if gate.kind in ("RZ", "RY"):
+            pend_l.append(d)  # psi_l -> U^dag psi_l (U commutes with its generator)
+            flush(psi_r, pend_r)
+            flush(psi_l, pend_l)
+            if scratch is None:
+                scratch = StateVector._empty(n, psi_r.device)
+            q = gate.qubits[0]
+            pm = (0, 0, 1 << q) if gate.kind == "RZ" else (0, 1 << q, 0)
+            _lib.check(_lib.lib().qsv_apply_pauli(psi_r.handle, scratch.handle, *pm))
+            v = vdot(psi_l, scratch)
+            for k, e in slots:
+                grad[e.index] += e.scale * v.imag
+        else:
+            flush(psi_r, pend_r)
+            flush(psi_l, pend_l)
+            values = bg.bound_values()
+            for k, e in slots:
+                work = psi_r.copy()
+                dm = np.ascontiguousarray(gate_derivative(gate.kind, values, k))
+                if len(gate.qubits) == 1:
+                    kernels.apply_1q(work, dm, gate.qubits[0])
+                else:
+                    kernels.apply_2q(work, dm, gate.qubits[0], gate.qubits[1])
+                grad[e.index] += e.scale * 2.0 * vdot(psi_l, work).real
+            pend_l.append(d)
+    return grad
+
+
 def dump_state(s: StateVector) -> bytes:
     """Little-endian complex-double amplitude dump (statevector.py:214-216)."""
     return s.amplitudes.astype("<c16").tobytes()

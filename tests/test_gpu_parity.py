@@ -334,3 +334,31 @@ def test_jit_expectation_sweeps_vs_oracle(jit_from_14, n, S, zq):
     assert np.abs(per - ref_per[:, 0]).max() <= 1e-12
     e_ref = O.expectation(st, h, n)
     assert rel(re, e_ref) <= REL_TOL
+
+
+@pytest.mark.parametrize("case,n", [("ucc", 8), ("mixed", 7)])
+def test_reverse_gradient_golden(case, n):
+    """Device reverse-mode gradient (statevector.reverse_gradient) vs the
+    reference's gradients (tests/golden/gradient_golden.npz)."""
+    g = np.load(f"{__import__('conftest').GOLDEN}/gradient_golden.npz")
+    circ = circuit_from_json(str(g[f"{case}_circuit"]))
+    h = parse_h(g[f"{case}_h"])
+    grad = sv.reverse_gradient(circ, g[f"{case}_theta"], h, sv.init_state(str(g[f"{case}_ref"])))
+    assert np.abs(grad - g[f"{case}_grad"]).max() <= 1e-10
+
+
+def test_reverse_gradient_ucc_vs_oracle_14q():
+    from paper_2208_10978_b200.circuit import Affine, Circuit, evolution_gates
+    n = 14
+    rng = np.random.default_rng(8)
+    strings = W.ucc_rotation_strings(n, 6)[:120]
+    gates = []
+    for k, s in enumerate(strings):
+        gates.extend(evolution_gates(s, Affine(k, -0.5)))
+    circ = Circuit(n, tuple(gates), len(strings))
+    theta = rng.uniform(-0.2, 0.2, len(strings))
+    h = W.sparse_random_hamiltonian(n, 80, rng)
+    ref = W.hf_bitstring(6, n)
+    grad = sv.reverse_gradient(circ, theta, h, sv.init_state(ref))
+    grad_ref = O.reverse_gradient(circ, theta, h, O.init_state(ref), n)
+    assert np.abs(grad - grad_ref).max() <= 1e-10

@@ -2,10 +2,12 @@
 (tests/golden/make_golden.py) and the reference's own H2 fixtures
 (pkg/tests/fixtures/reference.json, copied into h2_sto3g.json)."""
 
+import os
+
 import numpy as np
 import pytest
 
-from conftest import parse_h, random_state
+from conftest import GOLDEN, parse_h, random_state
 from oracle import oracle as O
 from paper_2208_10978_b200.circuit import bind, circuit_from_json
 
@@ -99,3 +101,18 @@ def test_numpy_twins_match_c_oracle():
         O.apply_2q(a, m2, q0, q1)
         O.np_apply_2q(b, m2, q0, q1)
         assert np.abs(a - b).max() <= 1e-15
+
+
+@pytest.mark.parametrize("case,n", [("ucc", 8), ("mixed", 7)])
+def test_oracle_reverse_gradient_golden(case, n):
+    """oracle.reverse_gradient (restating statevector.py:153-211) vs the
+    reference's own gradients (tests/golden/make_gradient_golden.py)."""
+    from conftest import parse_h
+    from paper_2208_10978_b200.circuit import circuit_from_json
+
+    g = np.load(os.path.join(GOLDEN, "gradient_golden.npz"))
+    circ = circuit_from_json(str(g[f"{case}_circuit"]))
+    h = parse_h(g[f"{case}_h"])
+    s0 = O.init_state(str(g[f"{case}_ref"]))
+    grad = O.reverse_gradient(circ, g[f"{case}_theta"], h, s0, n)
+    assert np.abs(grad - g[f"{case}_grad"]).max() <= 1e-12
