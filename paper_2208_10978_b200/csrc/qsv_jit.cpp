@@ -239,6 +239,32 @@ __device__ __forceinline__ void gm(double2 (&a)[16], u32 par0)
     }
 }
 
+// in-register permutations: pure relabelings in straight-line code
+template <int A, int B>
+__device__ __forceinline__ void pcx(double2 (&a)[16])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+        if ((r & (1 << A)) && !(r & (1 << B))) { const double2 t = a[r]; a[r] = a[r | (1 << B)]; a[r | (1 << B)] = t; }
+}
+template <int A, int B>
+__device__ __forceinline__ void pswap(double2 (&a)[16])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+        if ((r & (1 << A)) && !(r & (1 << B))) {
+            const int q = r ^ (1 << A) ^ (1 << B);
+            const double2 t = a[r]; a[r] = a[q]; a[q] = t;
+        }
+}
+template <int J>
+__device__ __forceinline__ void px(double2 (&a)[16])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+        if (!(r & (1 << J))) { const double2 t = a[r]; a[r] = a[r | (1 << J)]; a[r | (1 << J)] = t; }
+}
+
 __device__ __forceinline__ u32 swz(u32 l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
 __device__ __forceinline__ u32 tb(u32 tid, int i, u32 col) { return (0u - ((tid >> i) & 1u)) & col; }
 __device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
@@ -566,7 +592,9 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
         if (B.kind != 0) return false;
         for (int k = B.op0; k < B.op1; ++k) {
             const int t = ops[k].type;
-            if (t != OP_U1 && t != OP_U2 && t != OP_DIAG1 && t != OP_GMAT) return false;
+            if (t != OP_U1 && t != OP_U2 && t != OP_DIAG1 && t != OP_GMAT && t != OP_CX &&
+                t != OP_SWAP && t != OP_X)
+                return false;
         }
         snprintf(buf, sizeof(buf), "  {\n    const u32 sb = %uu", (unsigned)B.tswz);
         body += buf;
@@ -591,6 +619,12 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
                 snprintf(buf, sizeof(buf), "    u1<%d, %d, %d>(a);\n", op.a, cls, op.p);
             } else if (op.type == OP_U2) {
                 snprintf(buf, sizeof(buf), "    u2<%d, %d, %d>(a);\n", op.a, op.b, op.p);
+            } else if (op.type == OP_CX) {
+                snprintf(buf, sizeof(buf), "    pcx<%d, %d>(a);\n", op.a, op.b);
+            } else if (op.type == OP_SWAP) {
+                snprintf(buf, sizeof(buf), "    pswap<%d, %d>(a);\n", op.a, op.b);
+            } else if (op.type == OP_X) {
+                snprintf(buf, sizeof(buf), "    px<%d>(a);\n", op.a);
             } else if (op.type == OP_GMAT) {
                 // common sign masks of the group (qsv_planner.cpp block_pass)
                 const RotRec &rc = rots[op.r0];

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
 #include <cstdlib>
 #include <unordered_map>
 
@@ -691,6 +692,8 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
                         break;
                     }
                     case OP_ROTG: op.f = comp_b(op.f); break;
+                    case OP_CX: case OP_SWAP: op.a = local(op.a); op.b = local(op.b); break;
+                    case OP_X: op.a = local(op.a); break;
                     default: break;
                 }
                 if (op.type == OP_ROTG || op.type == OP_ROTD)
@@ -741,10 +744,19 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
         cur = 0;
         D = 0;
     };
+    // Permutations inside an open block whose bits fit the block become
+    // register relabelings (free in specialised passes) instead of being
+    // deferred to the SMEM map, which would force a new block as soon as a
+    // later op touches their qubits (every brickwork CNOT would split blocks).
+    const char *env_inreg = getenv("QSV_INREG_PERMS");
+    const bool inreg_perms = !(env_inreg && env_inreg[0] == '0');
     for (const OpRec &op : src) {
         if (is_perm(op.type)) {
             if (pending.empty()) {
                 apply_perm(op);  // free: only the map changes
+            } else if (inreg_perms && !(supp(op) & D) && (supp(op) & ~cur) == 0) {
+                cur |= supp(op);
+                pending.push_back(op);
             } else {
                 perms.push_back(op);
                 D |= supp(op);

@@ -287,6 +287,44 @@ __device__ __forceinline__ void dispatch_pair(int ja, int jb, double2 (&a)[kR], 
 
 template <int A, int B> struct W_u2 { __device__ static void run(double2 (&a)[kR], const double *P) { r_u2<A, B>(a, P); } };
 
+// in-register permutations (block-local bits): CNOT control A target B, SWAP, X
+template <int A, int B> struct W_cx {
+    __device__ static void run(double2 (&a)[kR], const double *)
+    {
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+            if ((r & (1 << A)) && !(r & (1 << B))) {
+                const double2 t = a[r];
+                a[r] = a[r | (1 << B)];
+                a[r | (1 << B)] = t;
+            }
+    }
+};
+template <int A, int B> struct W_swap {
+    __device__ static void run(double2 (&a)[kR], const double *)
+    {
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+            if ((r & (1 << A)) && !(r & (1 << B))) {
+                const int q = r ^ (1 << A) ^ (1 << B);
+                const double2 t = a[r];
+                a[r] = a[q];
+                a[q] = t;
+            }
+    }
+};
+template <int J>
+__device__ __forceinline__ void r_x(double2 (&a)[kR])
+{
+#pragma unroll
+    for (int r = 0; r < kR; ++r)
+        if (!(r & (1 << J))) {
+            const double2 t = a[r];
+            a[r] = a[r | (1 << J)];
+            a[r | (1 << J)] = t;
+        }
+}
+
 // Slot of logical tile index l under the block's affine map (kind-1 blocks).
 __device__ __forceinline__ uint32_t map_slot(uint32_t l, int m, uint32_t tswz, const uint16_t *cols)
 {
@@ -388,6 +426,16 @@ __device__ __forceinline__ void run_blocks(double2 *sm, const BlockRec *blocks, 
                         case OP_U1: dispatch_u1(oa, a, params + w1.z); break;
                         case OP_U2:
                             if (!LITE) dispatch_pair<W_u2>(oa, ob, a, params + w1.z);
+                            break;
+                        case OP_CX: dispatch_pair<W_cx>(oa, ob, a, params); break;
+                        case OP_SWAP: dispatch_pair<W_swap>(oa, ob, a, params); break;
+                        case OP_X:
+                            switch (oa) {
+                                case 0: r_x<0>(a); break;
+                                case 1: r_x<1>(a); break;
+                                case 2: r_x<2>(a); break;
+                                default: r_x<3>(a); break;
+                            }
                             break;
                         case OP_DIAG1: {
                             const double *P = params + w1.z;

@@ -70,6 +70,19 @@ def run_block(a, ops, rots, params, tid, base, blk_ops, RB):
             else:
                 bit = (tid >> ob) & 1
                 a *= np.where(bit, d1, d0)[:, None]
+        elif typ in (OP_CX, OP_SWAP, OP_X):
+            # in-register permutation on block-local bits
+            perm = []
+            for r in range(R):
+                if typ == OP_CX:
+                    q = r ^ (1 << ob) if (r >> oa) & 1 else r
+                elif typ == OP_SWAP:
+                    ba, bb = (r >> oa) & 1, (r >> ob) & 1
+                    q = r ^ ((ba ^ bb) * ((1 << oa) | (1 << ob)))
+                else:
+                    q = r ^ (1 << oa)
+                perm.append(q)
+            a[:, :] = a[:, perm]
         elif typ == OP_GMAT:
             F = f
             H = F.bit_length() - 1
