@@ -63,8 +63,12 @@ class CudaEngine:
     def zeros(self, n_local: int):
         from . import statevector as sv
 
+        import torch
+
         s = sv.StateVector._empty(n_local, self.device)
         self.tensor(s).zero_()
+        # zero_ ran on torch's stream; libqsv works on the handle's own stream
+        torch.cuda.current_stream(torch.device("cuda", self.device)).synchronize()
         return s
 
     def basis(self, n_local: int, index: int):
