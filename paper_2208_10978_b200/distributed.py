@@ -14,9 +14,10 @@ physical positions >= n_local are global (rank bits).
 
 Gates.  ``plan_segments`` walks the gate list and emits local segments (gates
 whose qubits are all local, remapped to physical positions) separated by
-relayouts.  When a gate needs a global qubit, ONE relayout brings in that
-qubit plus other global qubits needed before the evicted ones (Belady-style
-lookahead), so several global-qubit gates share one exchange.  A relayout
+relayouts, scheduling local-first inside the light cone: gates needing a
+global qubit (and everything behind them on the same qubits) are deferred
+while all other gates run, so one relayout serves many global-qubit gates --
+the 20-layer brickwork needs ONE exchange at any P.  A relayout
 first moves the evicted local qubits to the top k local positions with SWAP
 gates (free inside the engine's tile passes: the planner folds permutations
 into the shared-memory map), then swaps those k top local bits with k global
@@ -220,22 +221,6 @@ def _gate_qubits(qubits, i):
     return (a,) if b < 0 else (a, b)
 
 
-class _NextUse:
-    def __init__(self, n, kinds, qubits):
-        self.uses = [[] for _ in range(n)]
-        for i in range(len(kinds)):
-            for q in _gate_qubits(qubits, i):
-                self.uses[q].append(i)
-        self.ptr = [0] * n
-
-    def __call__(self, q, i):
-        u, p = self.uses[q], self.ptr[q]
-        while p < len(u) and u[p] < i:
-            p += 1
-        self.ptr[q] = p
-        return u[p] if p < len(u) else math.inf
-
-
 def _apply_relayout_to_map(perm, inv, bring, victims, n_local):
     k = len(bring)
     for j in range(k):
@@ -261,34 +246,51 @@ def _move_victims(perm, inv, victims, n_local, swaps):
 
 def plan_segments(kinds, qubits, n: int, n_local: int, perm):
     """Split a gate list into local segments and relayouts.
-    Returns (segments, final_perm)."""
+    Returns (segments, final_perm).
+
+    Local-first light-cone scheduling: a gate that needs a global qubit is
+    deferred, and so is every later gate sharing a qubit with a deferred one;
+    all other gates run now (gates on disjoint qubits commute).  Only when
+    every remaining gate is blocked does a relayout happen, bringing in the
+    global qubits the deferred gates need first (up to g) and evicting the
+    local qubits used latest among the remaining gates.  On a brickwork the
+    local qubits run many layers ahead inside the light cone before an
+    exchange is needed."""
     g = n - n_local
     perm = list(perm)
     inv = [0] * n
     for q, p in enumerate(perm):
         inv[p] = q
-    nxt = _NextUse(n, kinds, qubits)
     segs = []
     src, qs = [], []
-    for i in range(len(kinds)):
-        gq = _gate_qubits(qubits, i)
-        if all(perm[q] < n_local for q in gq):
-            src.append(i)
-            qs.extend([perm[gq[0]], perm[gq[1]] if len(gq) == 2 else -1])
-            continue
-        need = [q for q in gq if perm[q] >= n_local]
-        glob = [inv[p] for p in range(n_local, n) if inv[p] not in need]
-        extra = sorted(glob, key=lambda q: (nxt(q, i), q))
-        cand = sorted((inv[p] for p in range(n_local) if inv[p] not in gq),
-                      key=lambda q: (-nxt(q, i), q))
-        if len(cand) < g:
+    remaining = list(range(len(kinds)))
+    while True:
+        blocked = set()
+        deferred = []
+        for i in remaining:
+            gq = _gate_qubits(qubits, i)
+            if any(q in blocked for q in gq) or any(perm[q] >= n_local for q in gq):
+                deferred.append(i)
+                blocked.update(gq)
+            else:
+                src.append(i)
+                qs.extend([perm[gq[0]], perm[gq[1]] if len(gq) == 2 else -1])
+        remaining = deferred
+        if not remaining:
+            break
+        # global qubits in order of first use by the deferred gates
+        bring = []
+        first_use = {}
+        for pos, i in enumerate(remaining):
+            for q in _gate_qubits(qubits, i):
+                first_use.setdefault(q, pos)
+                if perm[q] >= n_local and q not in bring and len(bring) < g:
+                    bring.append(q)
+        head = set(_gate_qubits(qubits, remaining[0]))
+        cand = sorted((inv[p] for p in range(n_local) if inv[p] not in head and inv[p] not in bring),
+                      key=lambda q: (-first_use.get(q, math.inf), q))
+        if len(cand) < len(bring):
             raise ValueError("too few local qubits for a relayout")
-        bring = list(need)
-        for q in extra:
-            if len(bring) >= g:
-                break
-            if nxt(q, i) < nxt(cand[len(bring)], i):
-                bring.append(q)
         victims = cand[:len(bring)]
         swaps = []
         _move_victims(perm, inv, victims, n_local, swaps)
@@ -299,8 +301,7 @@ def plan_segments(kinds, qubits, n: int, n_local: int, perm):
         segs.append(Segment(np.array(src, dtype=np.int64), np.array(qs, dtype=np.int32),
                             Relayout(S)))
         _apply_relayout_to_map(perm, inv, bring, victims, n_local)
-        src = [i]
-        qs = [perm[gq[0]], perm[gq[1]] if len(gq) == 2 else -1]
+        src, qs = [], []
     segs.append(Segment(np.array(src, dtype=np.int64), np.array(qs, dtype=np.int32), None))
     return segs, perm
 

@@ -108,9 +108,16 @@ def test_plan_segments_only_local_gates(P):
         seen.extend(int(i) for i in s.src if i >= 0)
         if s.relayout is not None:
             assert 1 <= s.relayout.k <= g
-    assert seen == list(range(len(kinds)))  # every gate once, in order
-    # batching: fewer relayouts than gates that touch a global qubit at issue time
-    assert sum(s.relayout is not None for s in segs) < len(kinds) // 4
+    assert sorted(seen) == list(range(len(kinds)))  # every gate exactly once
+    # gates sharing a qubit keep their relative order (only commuting gates move)
+    last = {}
+    for i in seen:
+        qs = [int(qubits[2 * i])] + ([int(qubits[2 * i + 1])] if qubits[2 * i + 1] >= 0 else [])
+        for q in qs:
+            assert last.get(q, -1) < i
+            last[q] = i
+    # light-cone scheduling: one exchange serves the whole brickwork
+    assert sum(s.relayout is not None for s in segs) <= 2
 
 
 @pytest.mark.parametrize("P,n,layers", [(2, 8, 5), (4, 9, 6), (8, 10, 4)])
