@@ -5,7 +5,7 @@ Default workload (N=1): config 2 -- 28-qubit random brickwork, depth 20
 One step = evolve(prepare("0"*28), circuit) on resident HBM state.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
-                    [--extra ucc12,expect30,ucc32]
+                    [--extra ucc12,expect30,ucc32,fused30]
 
 Prints ONE JSON line (rank 0).  value = amplitude-updates/s (sum over the 830
 gates of 2^n, per second, whole job); e2e = the same metric through the public
@@ -252,6 +252,41 @@ def extra_expect30(steps=3):
             "hbm_gbs_sweeps": st["n_passes"] * 16 * (1 << n) / dt / 1e9}
 
 
+def extra_fused30(steps=3):
+    """North-star fused gate application at 30 qubits: a config-4-shaped UCC
+    circuit (all singles + 2,000 doubles, 15 electrons) on 30 qubits, evolve
+    only, resident state.  Reports HBM GB/s over the launched passes
+    (32 B x 2^30 per pass) against MEASURED_PEAKS.json."""
+    import torch
+
+    from paper_2208_10978_b200 import engine
+    from paper_2208_10978_b200 import statevector as sv
+    from paper_2208_10978_b200 import workloads as W
+
+    cfg = W.config4(seed=0, n_qubits=30, n_electrons=15, n_doubles=2000, n_terms=10)
+    be = engine.StateVectorBackend()
+    s0 = be.prepare(cfg["reference"])
+    psi = be.evolve(s0, cfg["circuit"])  # plan + specialise
+    psi.synchronize()
+    del psi
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        psi = be.evolve(s0, cfg["circuit"])
+        psi.synchronize()
+        ts.append(time.perf_counter() - t0)
+        st = sv.last_plan_stats()
+        del psi
+    dt = min(ts)
+    passes = st["n_passes"]
+    peak, _ = load_peaks()
+    gbs = passes * 32.0 * (1 << 30) / dt / 1e9
+    return {"workload": "30q UCC-shaped circuit (config 4 construction at n=30, 15 e): "
+                        f"{st['n_rotations']} Pauli rotations, evolve only",
+            "metric": "amplitude-updates/s", "value": st["n_rotations"] * (1 << 30) / dt,
+            "s_per_evolve": dt, "passes": passes, "hbm_gbs": gbs, "hbm_frac": gbs / peak}
+
+
 def extra_ucc32(steps=1):
     from paper_2208_10978_b200 import engine
     from paper_2208_10978_b200 import statevector as sv
@@ -270,9 +305,19 @@ def extra_ucc32(steps=1):
         e = be.expectation(psi, cfg["hamiltonian"])
         del psi
     dt = (time.perf_counter() - t0) / steps
+    psi = be.evolve(s0, cfg["circuit"])
+    psi.synchronize()
+    t1 = time.perf_counter()
+    psi2 = be.evolve(s0, cfg["circuit"])
+    psi2.synchronize()
+    t_ev = time.perf_counter() - t1
+    del psi, psi2
+    peak, _ = load_peaks()
+    gbs = st_ev["n_passes"] * 32.0 * (1 << 32) / t_ev / 1e9
     return {"workload": "config4: 32q UCC (16,512 rotations) + 5,000-term H",
             "metric": "energy evals/s", "value": 1.0 / dt, "s_per_eval": dt, "energy": e,
-            "evolve_passes": st_ev["n_passes"]}
+            "evolve_passes": st_ev["n_passes"], "s_per_evolve": t_ev, "evolve_hbm_gbs": gbs,
+            "evolve_hbm_frac": gbs / peak}
 
 
 def run_engine(args, rank, world, local):
@@ -397,12 +442,16 @@ def run_engine(args, rank, world, local):
         "clocks": clocks.summary(),
     }
 
-    extras = [e for e in (args.extra or "").split(",") if e]
+    extras = [e for e in (args.extra or "").split(",") if e and e != "none"]
     if rank == 0 and extras:
         line["extra"] = {}
         for e in extras:
-            fn = {"ucc12": extra_ucc12, "expect30": extra_expect30, "ucc32": extra_ucc32}[e]
-            line["extra"][e] = fn()
+            fn = {"ucc12": extra_ucc12, "expect30": extra_expect30, "ucc32": extra_ucc32,
+                  "fused30": extra_fused30}[e]
+            try:
+                line["extra"][e] = fn()
+            except Exception as exc:  # an extra must never cost the headline line
+                line["extra"][e] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, kind, desc = cpu_sample_run(circ, REF_SAMPLE_GATES)
@@ -517,7 +566,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--extra", default="")
+    ap.add_argument("--extra", default="ucc12,fused30,expect30,ucc32",
+                    help="secondary workloads (configs 1, 3, 4 and the 30q fused-gate roofline); 'none' to skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, world, local = dist_env()
