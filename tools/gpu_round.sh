@@ -4,4 +4,4 @@ timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/pyt
 cat gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --steps 10 --warmup 3 --extra ucc12,expect30 > gpurun_out/bench.log 2>&1; echo bench rc=$?
 tail -5 gpurun_out/bench.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --extra none > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
