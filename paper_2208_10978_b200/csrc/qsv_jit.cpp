@@ -421,6 +421,36 @@ __device__ __forceinline__ void wht8(const double2 *sm, u32 pl, u32 sF, double (
         }
     }
 }
+// l0-side amplitudes of the thread's 8 pairs for highest flip bit H (shared
+// by every group of the sweep with that H)
+template <int H>
+__device__ __forceinline__ u32 load_x(const double2 *sm, u32 pl, double2 (&X)[8])
+{
+    const u32 b0 = swz(ins0(pl, H));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) X[j] = sm[b0 ^ swz(ins0(256u * j, H))];
+    return b0;
+}
+template <bool RE, bool IM, int H>
+__device__ __forceinline__ void wht8x(const double2 *sm, u32 b0, const double2 (&X)[8], u32 sF,
+                                      double (&Wr)[8], double (&Wi)[8])
+{
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double2 x = X[j], y = sm[b0 ^ swz(ins0(256u * j, H)) ^ sF];
+        if (RE) Wr[j] = fma(x.x, y.x, x.y * y.y);
+        if (IM) Wi[j] = fma(x.x, y.y, -x.y * y.x);
+    }
+#pragma unroll
+    for (int b = 1; b < 8; b <<= 1) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (r & b) continue;
+            if (RE) { const double u = Wr[r], v = Wr[r | b]; Wr[r] = u + v; Wr[r | b] = u - v; }
+            if (IM) { const double u = Wi[r], v = Wi[r | b]; Wi[r] = u + v; Wi[r | b] = u - v; }
+        }
+    }
+}
 __device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ u64 tbase(u64 tile, int lane, int ncomp, int comp_lane)
 {
@@ -668,10 +698,18 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
     if (nterms > 24) return false;
     std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";
     char buf[512];
-    for (const GroupRec &G : sp.groups) {
+    int prev_h = -1;
+    for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
+        const GroupRec &G = sp.groups[gi];
         const bool need_re = G.t_im > G.t0, need_im = G.t1 > G.t_im;
+        if (G.h != prev_h) {  // new run of groups with this highest flip bit
+            if (prev_h >= 0) fn += "  }\n";
+            snprintf(buf, sizeof(buf), "  { double2 X[8];\n    const u32 b0 = load_x<%d>(sm, pl, X);\n", G.h);
+            fn += buf;
+            prev_h = G.h;
+        }
         snprintf(buf, sizeof(buf),
-                 "  { double Wr[8], Wi[8];\n    wht8<%s, %s, %d>(sm, pl, %uu, Wr, Wi);\n",
+                 "  { double Wr[8], Wi[8];\n    wht8x<%s, %s, %d>(sm, b0, X, %uu, Wr, Wi);\n",
                  need_re ? "true" : "false", need_im ? "true" : "false", G.h, h_swz(G.f_loc));
         fn += buf;
         for (int t = G.t0; t < G.t1; ++t) {
@@ -685,6 +723,7 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
         }
         fn += "  }\n";
     }
+    if (prev_h >= 0) fn += "  }\n";
     fn += "}\n";
     snprintf(buf, sizeof(buf), "#define MAXT %d\n", nterms);
     src = buf;

@@ -1085,6 +1085,12 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     std::vector<int> order(flips.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        if (jit_layout) {
+            // specialised sweeps share the l0-side loads of groups with the
+            // same highest flip bit: keep such groups adjacent
+            const int ha = highest_bit(flips[a]), hb = highest_bit(flips[b]);
+            if (ha != hb) return ha > hb;
+        }
         const int pa = popc64(flips[a] & ~low), pb = popc64(flips[b] & ~low);
         if (pa != pb) return pa > pb;
         return members[a].size() > members[b].size();
@@ -1150,9 +1156,15 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
             sp.terms.push_back(tr);
             sp.map.push_back(t);
         }
-        // heavier groups first so the two warp halves stay balanced
-        std::stable_sort(bin.groups.begin(), bin.groups.end(),
-                         [&](int a, int b) { return members[a].size() > members[b].size(); });
+        // heavier groups first so the two warp halves stay balanced; with the
+        // specialised layout, groups with the same highest flip bit adjacent
+        std::stable_sort(bin.groups.begin(), bin.groups.end(), [&](int a, int b) {
+            if (jit_layout) {
+                const int ha = highest_bit(flips[a]), hb = highest_bit(flips[b]);
+                if (ha != hb) return ha > hb;
+            }
+            return members[a].size() > members[b].size();
+        });
         for (int gi : bin.groups) {
             GroupRec gr{};
             gr.f_loc = compress(flips[gi], sp.geom);
