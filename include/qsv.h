@@ -119,6 +119,16 @@ int qsv_norm(const qsv_state *s, double *out);
 int qsv_axpby(qsv_state *y, const qsv_state *x, double alpha_re, double alpha_im, double beta_re,
               double beta_im);
 
+/* sample (statevector.py:124-147) after the caller's basis rotation: draw
+ * `shots` outcomes from |psi|^2 exactly as numpy's
+ * Generator(Philox(seed)).choice(2^n, shots, p=|psi|^2/sum) does (cumsum cdf,
+ * 53-bit uniforms of the Philox4x64-10 stream with key philox_key[2] =
+ * Philox(seed).state['key'], searchsorted 'right'); out_mean = mean of
+ * (-1)^{popc(outcome & support_mask)}.  outcomes (nullable, shots int64)
+ * receives the drawn basis indices. */
+int qsv_sample_parity(const qsv_state *s, uint64_t support_mask, int64_t shots,
+                      const uint64_t *philox_key, double *out_mean, int64_t *outcomes);
+
 /* Planner only (no device work; usable without a GPU): the plan that
  * qsv_apply_gates / qsv_expectation would execute for these inputs. */
 int qsv_plan_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,

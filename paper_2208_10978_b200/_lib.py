@@ -51,7 +51,8 @@ EXPORTED = (
     "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_apply_1q", "qsv_apply_2q",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
-    "qsv_plan_expectation", "qsv_debug_plan_json", "qsv_jit_info", "qsv_last_plan_stats",
+    "qsv_plan_expectation", "qsv_debug_plan_json", "qsv_sample_parity", "qsv_jit_info",
+    "qsv_last_plan_stats",
 )
 
 _lib = None
@@ -92,6 +93,7 @@ def _declare(L):
         "qsv_plan_expectation": ([ctypes.c_int, i64, u64p, u64p, u64p, sp], ctypes.c_int),
         "qsv_debug_plan_json": ([ctypes.c_int, i64, i32p, i32p, dp, ctypes.c_char_p, i64,
                                  ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_sample_parity": ([vp, u64, i64, u64p, dp, ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_jit_info": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_last_plan_stats": ([sp], ctypes.c_int),
     }

@@ -969,6 +969,35 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     return QSV_OK;
 }
 
+int qsv_sample_parity(const qsv_state *s, uint64_t support_mask, int64_t shots,
+                      const uint64_t *philox_key, double *out_mean, int64_t *outcomes)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (!philox_key || !out_mean) return fail_code(QSV_ERR_INVALID, "null key or output");
+    if (shots < 1) return fail_code(QSV_ERR_INVALID, "shots must be >= 1");
+    if (s->n < 64 && (support_mask >> s->n)) return fail_code(QSV_ERR_INVALID, "support mask out of range");
+    QSV_CUDA(cudaSetDevice(s->device));
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(s->device, &c)) return rc;
+    const size_t scratch = sample_scratch_bytes(s->dim);
+    const size_t out_bytes = outcomes ? (((size_t)shots * 8 + 255) & ~(size_t)255) : 0;
+    if (int rc = ensure_work(*c, s->stream, scratch + out_bytes + 256)) return rc;
+    if (c->stage_pending) {  // the workspace head may still feed an earlier program upload
+        QSV_CUDA(cudaStreamSynchronize(s->stream));
+        c->stage_pending = false;
+    }
+    int64_t *d_out = outcomes ? (int64_t *)((char *)c->d_work + scratch) : nullptr;
+    unsigned long long odd = 0;
+    QSV_CUDA(launch_sample_parity(s->amps, s->dim, shots, philox_key[0], philox_key[1], support_mask,
+                                  c->d_work, scratch, d_out, &odd, s->stream));
+    if (outcomes)
+        QSV_CUDA(cudaMemcpy(outcomes, d_out, (size_t)shots * 8, cudaMemcpyDeviceToHost));
+    // np.mean(1 - 2 parity): an exact integer sum, one rounding
+    *out_mean = (double)(shots - 2 * (int64_t)odd) / (double)shots;
+    return QSV_OK;
+}
+
 int qsv_jit_info(int *available, int64_t *launches)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);

@@ -165,6 +165,10 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
 bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims &g,
                 const uint64_t *d_offhi, const int32_t *d_geo, const double *d_params, int nparams,
                 int grid, cudaStream_t st);
+size_t sample_scratch_bytes(uint64_t dim);
+cudaError_t launch_sample_parity(const double2 *psi, uint64_t dim, int64_t shots, uint64_t k0,
+                                 uint64_t k1, uint64_t support, void *scratch, size_t scratch_bytes,
+                                 int64_t *d_outcomes, unsigned long long *h_odd, cudaStream_t st);
 struct SweepPlan;
 bool jit_sweep_source(const SweepPlan &sp, std::string &src);
 bool jit_sweep_launch(int device, const std::string &src, const double2 *psi, const TileDims &g,

@@ -369,6 +369,33 @@ def vdot(a: StateVector, b: StateVector) -> complex:
     return complex(out[0], out[1])
 
 
+def sample(s: StateVector, p, shots: int, seed: int) -> float:
+    """Shot-based estimate of <P> (statevector.py:124-147): the support is
+    rotated into the Z basis (H for X, HY for Y) on a device copy, then the
+    kernel draws `shots` outcomes from |psi|^2 with the reference's exact
+    Philox4x64-10 stream (numpy seeds the key) and returns the mean parity."""
+    from .circuit import Circuit, Gate
+
+    if shots < 1:
+        raise ValueError("shots must be >= 1")
+    gates = []
+    support = 0
+    for q, axis in p.factors:
+        if q >= s.n_qubits:
+            raise ValueError(f"string index {q} out of range for {s.n_qubits} qubits")
+        support |= 1 << q
+        if axis == "X":
+            gates.append(Gate("H", (q,)))
+        elif axis == "Y":
+            gates.append(Gate("HY", (q,)))
+    rotated = evolve(s, Circuit(s.n_qubits, tuple(gates), 0)) if gates else s.copy()
+    key = np.ascontiguousarray(np.random.Philox(seed).state["state"]["key"], dtype=np.uint64)
+    mean = ctypes.c_double()
+    _lib.check(_lib.lib().qsv_sample_parity(rotated.handle, support, int(shots), _lib.u64ptr(key),
+                                            ctypes.byref(mean), None))
+    return float(mean.value)
+
+
 def reverse_gradient(c, theta, h, s0: StateVector) -> np.ndarray:
     """Gradient of <psi(theta)|H|psi(theta)> over all parameters in one
     backward sweep with a single application of H (statevector.py:153-163)."""

@@ -362,3 +362,33 @@ def test_reverse_gradient_ucc_vs_oracle_14q():
     grad = sv.reverse_gradient(circ, theta, h, sv.init_state(ref))
     grad_ref = O.reverse_gradient(circ, theta, h, O.init_state(ref), n)
     assert np.abs(grad - grad_ref).max() <= 1e-10
+
+
+def test_sample_golden_and_outcomes():
+    """Device shot sampling: same estimates as the reference (golden) and the
+    same drawn outcomes as the oracle (Philox stream reproduced on device)."""
+    import ctypes
+
+    from paper_2208_10978_b200 import _lib
+    from paper_2208_10978_b200.pauli import PauliString
+
+    g = np.load(f"{__import__('conftest').GOLDEN}/sample_golden.npz")
+    for k in range(3):
+        p = PauliString.from_label(str(g[f"c{k}_label"]))
+        s = sv.from_amplitudes(g[f"c{k}_amps"])
+        m = sv.sample(s, p, int(g[f"c{k}_shots"]), int(g[f"c{k}_seed"]))
+        assert m == float(g[f"c{k}_mean"])
+    # outcome-level parity on a Z string (no rotation) at 16 qubits
+    rng = np.random.default_rng(3)
+    st = random_state(16, rng)
+    p = PauliString.from_label("Z0 Z5 Z15")
+    mean_ref, out_ref = O.sample(st, p, 100000, 42, return_outcomes=True)
+    key = np.ascontiguousarray(np.random.Philox(42).state["state"]["key"], dtype=np.uint64)
+    outs = np.zeros(100000, dtype=np.int64)
+    mean = ctypes.c_double()
+    s = sv.from_amplitudes(st)
+    _lib.check(_lib.lib().qsv_sample_parity(s.handle, (1 << 0) | (1 << 5) | (1 << 15), 100000,
+                                            _lib.u64ptr(key), ctypes.byref(mean),
+                                            outs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+    assert np.array_equal(outs, out_ref)
+    assert mean.value == mean_ref

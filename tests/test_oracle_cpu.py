@@ -116,3 +116,15 @@ def test_oracle_reverse_gradient_golden(case, n):
     s0 = O.init_state(str(g[f"{case}_ref"]))
     grad = O.reverse_gradient(circ, g[f"{case}_theta"], h, s0, n)
     assert np.abs(grad - g[f"{case}_grad"]).max() <= 1e-12
+
+
+def test_oracle_sample_golden():
+    """oracle.sample (statevector.py:124-147) reproduces the reference's own
+    shot estimates (tests/golden/make_sample_golden.py) exactly."""
+    from paper_2208_10978_b200.pauli import PauliString
+
+    g = np.load(os.path.join(GOLDEN, "sample_golden.npz"))
+    for k in range(3):
+        p = PauliString.from_label(str(g[f"c{k}_label"]))
+        m = O.sample(g[f"c{k}_amps"], p, int(g[f"c{k}_shots"]), int(g[f"c{k}_seed"]))
+        assert m == float(g[f"c{k}_mean"])
