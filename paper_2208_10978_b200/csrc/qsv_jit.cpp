@@ -754,6 +754,16 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
         todo.push_back({s, &m});
     }
     if (todo.empty()) return 0;
+    if (const char *dump = getenv("QSV_JIT_DUMP")) {  // debug: write the generated sources
+        for (size_t i = 0; i < todo.size(); ++i) {
+            char path[512];
+            snprintf(path, sizeof(path), "%s/qsv_jit_%zu_%zu.cu", dump, mods.size(), i);
+            if (FILE *f = fopen(path, "w")) {
+                fputs(todo[i].first->c_str(), f);
+                fclose(f);
+            }
+        }
+    }
     const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;
     size_t next = 0;

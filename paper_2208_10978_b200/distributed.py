@@ -170,6 +170,9 @@ class ProcessGroupComm:
         self.rank = dist.get_rank(group)
         self.owned = [self.rank]
         self.piece_bytes = piece_bytes
+        # gloo moves host tensors only: device shards are staged through host
+        # memory (tests of the process-group plumbing on a single GPU)
+        self.nccl = dist.get_backend(group) == "nccl"
 
     def _device(self, like):
         return like.device
@@ -434,12 +437,16 @@ class DistStateVector:
             piece = max(1, min(chunk, self.comm.piece_bytes // row_bytes))
             staging = torch.empty((len(lst), piece) + tuple(t.shape[1:]), dtype=t.dtype,
                                   device=t.device)
+            host = t.is_cuda and not self.comm.nccl
+            if host:
+                staging = staging.cpu()
             for off in range(0, chunk, piece):
                 w = min(piece, chunk - off)
                 ops = []
                 for j, (c, p) in enumerate(lst):
                     src = t[c * chunk + off: c * chunk + off + w]
-                    ops.append(dist.P2POp(dist.isend, src.contiguous(), p, group))
+                    src = src.cpu() if host else src.contiguous()
+                    ops.append(dist.P2POp(dist.isend, src, p, group))
                     ops.append(dist.P2POp(dist.irecv, staging[j, :w], p, group))
                 for req in dist.batch_isend_irecv(ops):
                     req.wait()
@@ -585,10 +592,15 @@ class DistStateVector:
                 self.engine.synchronize(self.shards[r])
                 mine = self.engine.tensor(self.shards[r])
                 theirs = self.engine.tensor(buf)
-                ops = [dist.P2POp(dist.isend, mine, p, self.comm.group),
-                       dist.P2POp(dist.irecv, theirs, p, self.comm.group)]
+                host = mine.is_cuda and not self.comm.nccl
+                snd = mine.cpu() if host else mine
+                rcv = torch.empty_like(snd) if host else theirs
+                ops = [dist.P2POp(dist.isend, snd, p, self.comm.group),
+                       dist.P2POp(dist.irecv, rcv, p, self.comm.group)]
                 for req in dist.batch_isend_irecv(ops):
                     req.wait()
+                if host:
+                    theirs.copy_(rcv)
                 if theirs.is_cuda:
                     torch.cuda.current_stream(theirs.device).synchronize()
                 out[r] = buf
