@@ -744,17 +744,156 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
         cur = 0;
         D = 0;
     };
+    // Partitioned block order: cut the tile's bits into fixed groups of 4
+    // adjacent bits and emit, group after group, every op that is ready (its
+    // predecessors on shared bits emitted) and confined to the group; ops
+    // spanning groups (brickwork CNOTs across a cut) are emitted between
+    // clusters, where a permutation only changes the SMEM map.  A brickwork
+    // pass then needs ~one register block per group per two layers instead
+    // of one per layer.  Order-safe: ops sharing a bit keep their order.
+    std::vector<char> cluster_start;
+    const char *env_part = getenv("QSV_BLOCK_PARTITION");
+    if (!(env_part && env_part[0] == '0') && src.size() > 2 && m >= 8) {
+        const int N = (int)src.size();
+        std::vector<uint32_t> sp(N), rq(N);
+        for (int i = 0; i < N; ++i) {
+            sp[i] = supp(src[i]);
+            rq[i] = is_perm(src[i].type) ? sp[i] : req(src[i]);
+        }
+        std::vector<int> npred(N, 0);
+        std::vector<std::vector<int>> succ(N);
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < i; ++j)
+                if ((sp[i] & sp[j]) || (sp[i] == 0 && sp[j] == 0)) {
+                    succ[j].push_back(i);
+                    ++npred[i];
+                }
+        // candidate partitions: groups of 4 consecutive bits starting at
+        // offset 0..3 (the first group takes the bits below the offset)
+        auto build_order = [&](int shift, std::vector<OpRec> &order, std::vector<char> &starts) {
+            std::vector<int> np = npred;
+            std::vector<char> done(N, 0);
+            order.clear();
+            order.reserve(N);
+            starts.assign(N, 0);
+            int left = N;
+            auto emit = [&](int i, bool start) {
+                starts[order.size()] = start ? 1 : 0;
+                done[i] = 1;
+                --left;
+                order.push_back(src[i]);
+                for (int k : succ[i]) --np[k];
+            };
+            std::vector<uint32_t> groups;
+            uint32_t g0 = (1u << shift) - 1u;
+            for (int b = shift; b < m; b += kBlockBits) {
+                uint32_t G = (((1u << kBlockBits) - 1u) << b) & ((1u << m) - 1u);
+                if (g0) {
+                    G |= g0;  // may exceed 4 bits: split below
+                    g0 = 0;
+                }
+                if (__builtin_popcount(G) > kBlockBits) {
+                    groups.push_back(G & ((1u << shift) - 1u));
+                    G &= ~((1u << shift) - 1u);
+                }
+                if (G) groups.push_back(G);
+            }
+            while (left > 0) {
+                bool progress = false;
+                for (uint32_t G : groups) {
+                    bool first = true;
+                    for (bool more = true; more;) {
+                        more = false;
+                        for (int i = 0; i < N; ++i)
+                            if (!done[i] && np[i] == 0 && rq[i] != 0 && (rq[i] & ~G) == 0) {
+                                emit(i, first);
+                                first = false;
+                                more = progress = true;
+                            }
+                    }
+                }
+                for (int i = 0; i < N; ++i)
+                    if (!done[i] && np[i] == 0) {
+                        bool inside = false;
+                        for (uint32_t G : groups)
+                            if (rq[i] != 0 && (rq[i] & ~G) == 0) inside = true;
+                        if (inside) continue;
+                        emit(i, true);
+                        progress = true;
+                    }
+                if (!progress)
+                    for (int i = 0; i < N; ++i)
+                        if (!done[i] && np[i] == 0) {
+                            emit(i, true);
+                            break;
+                        }
+            }
+        };
+        std::vector<OpRec> order, cand;
+        std::vector<char> cand_starts;
+        // keep the partitioned order only if it yields fewer register blocks
+        // (dry run of the block former below: same flush rules, no output)
+        auto count_blocks = [&](const std::vector<OpRec> &ops, const std::vector<char> *starts) {
+            int blocks = 0;
+            bool pend = false;
+            uint32_t c2 = 0, d2 = 0;
+            for (size_t oi = 0; oi < ops.size(); ++oi) {
+                const OpRec &op = ops[oi];
+                if (starts && (*starts)[oi] && pend) { ++blocks; pend = false; c2 = d2 = 0; }
+                const uint32_t su = supp(op);
+                if (is_perm(op.type)) {
+                    if (!pend) continue;
+                    if (!(su & d2) && ((su & ~c2) == 0 ||
+                                       (starts && __builtin_popcount(c2 | su) <= kBlockBits))) {
+                        c2 |= su;
+                    } else {
+                        d2 |= su;
+                    }
+                    continue;
+                }
+                const uint32_t r2 = req(op);
+                if ((su & d2) && pend) { ++blocks; pend = false; c2 = d2 = 0; }
+                if (op.type == OP_ROTG && __builtin_popcount(op.f) > kBlockBits) {
+                    if (pend) ++blocks;
+                    ++blocks;
+                    pend = false;
+                    c2 = d2 = 0;
+                    continue;
+                }
+                if (pend && __builtin_popcount(c2 | r2) > kBlockBits) { ++blocks; pend = false; c2 = d2 = 0; }
+                pend = true;
+                c2 |= r2;
+            }
+            return blocks + (pend ? 1 : 0);
+        };
+        int best = count_blocks(src, nullptr);
+        for (int shift = 0; shift < kBlockBits; ++shift) {
+            build_order(shift, cand, cand_starts);
+            const int nb = count_blocks(cand, &cand_starts);
+            if (nb < best) {
+                best = nb;
+                order.swap(cand);
+                cluster_start.swap(cand_starts);
+            }
+        }
+        if (!order.empty()) src.swap(order);
+        else cluster_start.clear();
+    }
     // Permutations inside an open block whose bits fit the block become
     // register relabelings (free in specialised passes) instead of being
     // deferred to the SMEM map, which would force a new block as soon as a
     // later op touches their qubits (every brickwork CNOT would split blocks).
     const char *env_inreg = getenv("QSV_INREG_PERMS");
     const bool inreg_perms = !(env_inreg && env_inreg[0] == '0');
-    for (const OpRec &op : src) {
+    for (size_t oi = 0; oi < src.size(); ++oi) {
+        const OpRec &op = src[oi];
+        if (!cluster_start.empty() && cluster_start[oi] && !pending.empty()) flush();
         if (is_perm(op.type)) {
             if (pending.empty()) {
                 apply_perm(op);  // free: only the map changes
-            } else if (inreg_perms && !(supp(op) & D) && (supp(op) & ~cur) == 0) {
+            } else if (inreg_perms && !(supp(op) & D) &&
+                       ((supp(op) & ~cur) == 0 ||
+                        (!cluster_start.empty() && __builtin_popcount(cur | supp(op)) <= kBlockBits))) {
                 cur |= supp(op);
                 pending.push_back(op);
             } else {
