@@ -595,20 +595,8 @@ tile_block_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *_
 }
 
 
-// ---------------------------------------------------------------------------
-// Warp-specialised full-tile pass (m = 12): one persistent CTA per SM with a
-// 3-stage ring of 64 KiB SMEM tiles.  Warps 0-7 (kT threads) run the register
-// blocks; warps 8-11 (kIo threads) stream tiles in with LDGSTS and out with
-// streaming STG.  While the compute warps work on tile i, the I/O warps load
-// tile i+1 and write back tile i-1, so HBM traffic overlaps the FP64 work
-// instead of alternating with it.  Hand-off by mbarriers:
-//   full[s]     -- cp.async completion of every I/O thread (noinc arrive)
-//   computed[s] -- every compute thread finished its last block on stage s
-// The I/O warps order "store tile i-3 from stage s" before "load tile i into
-// stage s" with a named barrier among themselves.
-constexpr int kIo = 128;
+// ---- mbarrier / async-copy helpers of the ring pipeline ----
 constexpr int kStages = 3;
-constexpr int kWsThreads = kT + kIo;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -636,122 +624,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *b)
 {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void io_sync()
-{
-    asm volatile("bar.sync 2, %0;" ::"n"(kIo) : "memory");
-}
-
-template <bool STAGED>
-__global__ void __launch_bounds__(kWsThreads, 1)
-tile_ws_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__restrict__ g_offhi,
-               const int32_t *__restrict__ g_geo, const PassProgram prog)
-{
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int m = kMaxTileBits;
-    constexpr int tsize = 1 << m;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);  // [kStages]
-    uint64_t *computed = full + kStages;                      // [kStages]
-    uint32_t *st_k = reinterpret_cast<uint32_t *>(computed + kStages);  // [32]
-    double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);        // kStages x tsize
-    const int c = g.c;
-    uint64_t *offhi = reinterpret_cast<uint64_t *>(bufs + kStages * tsize);
-    const int nhi = 1 << (m - c);
-    const uint32_t tid = threadIdx.x;
-    for (int i = tid; i < nhi; i += kWsThreads) offhi[i] = __ldg(g_offhi + i);
-    const BlockRec *blocks = prog.blocks;
-    const OpRec *ops = prog.ops;
-    const RotRec *rots = prog.rots;
-    const double *params = prog.params;
-    if (STAGED) {
-        double *sp = reinterpret_cast<double *>(offhi + nhi + (nhi & 1));
-        RotRec *sr = reinterpret_cast<RotRec *>(sp + ((prog.nparams + 1) & ~1));
-        OpRec *so = reinterpret_cast<OpRec *>(sr + prog.nrots);
-        BlockRec *sb = reinterpret_cast<BlockRec *>(so + prog.nops);
-        for (int i = tid; i < prog.nparams; i += kWsThreads) sp[i] = __ldg(prog.params + i);
-        const int4 *gs = reinterpret_cast<const int4 *>(prog.rots);
-        for (int i = tid; i < prog.nrots * 2; i += kWsThreads) reinterpret_cast<int4 *>(sr)[i] = __ldg(gs + i);
-        gs = reinterpret_cast<const int4 *>(prog.ops);
-        for (int i = tid; i < prog.nops * 2; i += kWsThreads) reinterpret_cast<int4 *>(so)[i] = __ldg(gs + i);
-        gs = reinterpret_cast<const int4 *>(prog.blocks);
-        for (int i = tid; i < prog.nblocks * 3; i += kWsThreads) reinterpret_cast<int4 *>(sb)[i] = __ldg(gs + i);
-        params = sp;
-        rots = sr;
-        ops = so;
-        blocks = sb;
-    }
-    // store map of logical l = io_tid + kIo * k: bits 0..6 from io_tid, 7..11 from k
-    if (tid < 32) {
-        uint32_t v = 0;
-        for (int j = 0; j < 5; ++j)
-            if ((tid >> j) & 1u) v ^= (uint32_t)__ldg(g_geo + 32 + 7 + j);
-        st_k[tid] = v;
-    }
-    if (tid == 0) {
-        for (int st = 0; st < kStages; ++st) {
-            mbar_init(full + st, kIo);
-            mbar_init(computed + st, kT);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    const uint64_t ntiles = 1ull << g.ncomp;
-    if ((uint64_t)blockIdx.x >= ntiles) return;
-    const int ntile_cta = (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1;
-    const int lane = tid & 31;
-    const int comp_lane = __ldg(g_geo + lane);
-    const uint32_t cmask = (1u << c) - 1u;
-
-    if (tid >= (uint32_t)kT) {
-        // ---------------- I/O warps ----------------
-        const uint32_t io = tid - kT;
-        uint32_t st_base = (uint32_t)__ldg(g_geo + 44);
-        for (int i = 0; i < 7; ++i)
-            if ((io >> i) & 1u) st_base ^= (uint32_t)__ldg(g_geo + 32 + i);
-        auto load = [&](int it) {
-            const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
-            const uint64_t b = tbase(tile, lane, g.ncomp, comp_lane);
-            double2 *buf = bufs + (it % kStages) * tsize;
-            const double2 *src = psi + b;
-#pragma unroll 8
-            for (int k = 0; k < tsize / kIo; ++k) {
-                const uint32_t l = io + k * kIo;
-                cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
-            }
-            cp_async_mbar_arrive(full + (it % kStages));
-        };
-        load(0);
-        for (int it = 0; it < ntile_cta; ++it) {
-            if (it + 1 < ntile_cta) {
-                io_sync();  // every I/O thread is done reading stage (it+1)%3 (tile it-2)
-                load(it + 1);
-            }
-            const int st = it % kStages;
-            mbar_wait(computed + st, (uint32_t)((it / kStages) & 1));
-            const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
-            const uint64_t b = tbase(tile, lane, g.ncomp, comp_lane);
-            const double2 *sm = bufs + st * tsize;
-            double2 *dst = psi + b;
-#pragma unroll 8
-            for (int k = 0; k < tsize / kIo; ++k) {
-                const uint32_t l = io + k * kIo;
-                __stcs(dst + (l & cmask) + offhi[l >> c], sm[st_base ^ st_k[k]]);
-            }
-        }
-        cp_async_wait<0>();
-    } else {
-        // ---------------- compute warps ----------------
-        for (int it = 0; it < ntile_cta; ++it) {
-            const int st = it % kStages;
-            const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
-            const uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
-            mbar_wait(full + st, (uint32_t)((it / kStages) & 1));
-            run_blocks<false, 1>(bufs + st * tsize, blocks, prog.nblocks, ops, rots, params, base,
-                                 tid, m);
-            mbar_arrive(computed + st);
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -932,28 +804,6 @@ cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *
             tile_ring_kernel<true><<<grid_for(1), kRingThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
         else
             tile_ring_kernel<false><<<grid_for(1), kRingThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
-        return cudaGetLastError();
-    }
-    static const char *env_ws = getenv("QSV_TILE_WS");  // 1: enable the warp-specialised kernel
-    const bool ws_ok = g.m == kMaxTileBits && env_ws && env_ws[0] == '1';
-    if (ws_ok) {
-        static bool ws_configured = false;
-        if (!ws_configured) {
-            cudaError_t e = cudaFuncSetAttribute(tile_ws_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-            if (e != cudaSuccess) return e;
-            e = cudaFuncSetAttribute(tile_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     max_smem);
-            if (e != cudaSuccess) return e;
-            ws_configured = true;
-        }
-        const size_t ws_base = 256 + ((size_t)kStages * 16 << g.m) + 8 * (nhi + (nhi & 1));
-        const bool ws_staged = ws_base + prog_bytes <= (size_t)max_smem;
-        const size_t smem = ws_staged ? ws_base + prog_bytes : ws_base;
-        if (ws_staged)
-            tile_ws_kernel<true><<<grid_for(1), kWsThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
-        else
-            tile_ws_kernel<false><<<grid_for(1), kWsThreads, smem, st>>>(psi, g, d_offhi, d_geo, prog);
         return cudaGetLastError();
     }
     // two CTAs per SM need <= ~113 KB each: single tile buffer + staged program
