@@ -172,28 +172,36 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
 bool match_block(const int32_t *kinds, const int32_t *qubits, int64_t N, int64_t i, Rot &out,
                  int64_t &len)
 {
+    // Qubit order is not required to be ascending (the reference emits
+    // ascending order, circuit.py:271-281, but a relabelled circuit -- e.g. a
+    // shard's local segment in distributed.py -- is not): the block is
+    // exp(-i theta/2 P) whenever the basis qubits are distinct, the ladder is a
+    // chain over distinct qubits and everything is mirrored exactly.
     int64_t j = i;
     int bq[64], bk[64], nb = 0;
+    uint64_t bmask = 0;
     while (j < N && (kinds[j] == K_H || kinds[j] == K_HY)) {
         const int q = qubits[2 * j];
-        if (nb > 0 && q <= bq[nb - 1]) break;
-        if (nb >= 64) return false;
+        if (((bmask >> q) & 1ull) || nb >= 64) break;
+        bmask |= 1ull << q;
         bq[nb] = q;
         bk[nb] = kinds[j];
         ++nb;
         ++j;
     }
     int s[66], ns = 0;
+    uint64_t smask = 0;
     while (j < N && kinds[j] == K_CNOT) {
         const int a = qubits[2 * j], b = qubits[2 * j + 1];
         if (ns == 0) {
-            if (!(a < b)) break;
             s[0] = a;
             s[1] = b;
             ns = 2;
+            smask = (1ull << a) | (1ull << b);
         } else {
-            if (a != s[ns - 1] || !(b > a) || ns >= 64) break;
+            if (a != s[ns - 1] || ((smask >> b) & 1ull) || ns >= 64) break;
             s[ns++] = b;
+            smask |= 1ull << b;
         }
         ++j;
     }

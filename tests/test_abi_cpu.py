@@ -167,3 +167,43 @@ def test_emulated_ucc_groups_match_oracle(n, ne, ndoubles):
     out, prog = _emulate(circ, psi0)
     assert any(op[0] == 9 for op in prog["ops"])  # fused groups present
     assert np.abs(out - O.evolve(psi0, circ.gates)).max() <= 1e-12
+
+
+def test_pattern_matcher_relabelled_qubits():
+    """A pauli_evolution block whose qubits were relabelled (non-ascending
+    order, as in a shard's remapped segment) is still one direct rotation."""
+    rng = np.random.default_rng(1)
+    n = 16
+    perm = rng.permutation(n)
+    gates = []
+    for _ in range(30):
+        w = int(rng.integers(2, 7))
+        pos = rng.choice(n, size=w, replace=False)
+        axes = rng.choice(list("XYZ"), size=w)
+        s = PauliString(tuple(zip((int(p) for p in pos), axes)))
+        for g in evolution_gates(s, Constant(float(rng.uniform(-1, 1)))):
+            gates.append(Gate(g.kind, tuple(int(perm[q]) for q in g.qubits), g.params))
+    st = plan(Circuit(n, tuple(gates), 0))
+    assert st["n_rotations"] == 30
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_emulated_relabelled_rotations_match_oracle(seed):
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(40 + seed)
+    n = 13
+    perm = rng.permutation(n)
+    gates = []
+    for _ in range(40):
+        w = int(rng.integers(1, 6))
+        pos = rng.choice(n, size=w, replace=False)
+        axes = rng.choice(list("XYZ"), size=w)
+        s = PauliString(tuple(zip((int(p) for p in pos), axes)))
+        for g in evolution_gates(s, Constant(float(rng.uniform(-1, 1)))):
+            gates.append(Gate(g.kind, tuple(int(perm[q]) for q in g.qubits), g.params))
+    circ = Circuit(n, tuple(gates), 0)
+    a = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    st = a / np.linalg.norm(a)
+    out, prog = _emulate(circ, st)
+    assert np.abs(out - O.evolve(st, circ.gates)).max() <= 1e-12
