@@ -695,7 +695,7 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
 {
     if (sp.global || sp.geom.m != kMaxTileBits || sp.ndiag != 0 || sp.groups.empty()) return false;
     const int nterms = (int)sp.terms.size();
-    if (nterms > 24) return false;
+    if (nterms > 48) return false;
     std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";
     char buf[512];
     int prev_h = -1;

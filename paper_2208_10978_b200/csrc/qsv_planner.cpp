@@ -1228,7 +1228,9 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     // Bin flip groups into sweeps: a sweep's tile must hold every group's
     // flip bits.  First-fit decreasing on the high-bit need; capacity is
     // bounded by the shared-memory accumulators (kFlipCap strings).
-    const int kFlipCap = jit_layout ? 24 : 512, kDiagCap = 2048, kGroupCap = 256;
+    const char *env_sc = getenv("QSV_SWEEP_TERMS");  // strings per specialised sweep (default 24)
+    const int jit_cap = env_sc ? std::max(4, std::min(48, atoi(env_sc))) : 24;
+    const int kFlipCap = jit_layout ? jit_cap : 512, kDiagCap = 2048, kGroupCap = 256;
     std::vector<int> order(flips.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {

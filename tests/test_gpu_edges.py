@@ -1,0 +1,94 @@
+"""Edge cases of the CUDA path vs the CPU oracle: tiny and tile-boundary
+state sizes, empty circuits and Hamiltonians, identity strings, identity
+rotations (global phase), the specialised-pass threshold, invalid inputs.
+Tolerances: amplitudes 1e-10 max-abs, energies 1e-10 relative."""
+
+import numpy as np
+import pytest
+
+from conftest import random_state
+from oracle import oracle as O
+from paper_2208_10978_b200 import statevector as sv
+from paper_2208_10978_b200 import workloads as W
+from paper_2208_10978_b200.circuit import Circuit, Constant, Gate
+from paper_2208_10978_b200.pauli import PauliString, PauliSum, PauliTerm
+
+pytestmark = pytest.mark.gpu
+
+
+def _mixed(n, G, seed):
+    rng = np.random.default_rng(seed)
+    kinds = ["H", "HY", "X", "CNOT", "SWAP", "RZ", "RY", "U3", "CU3"]
+    npar = {"RZ": 1, "RY": 1, "U3": 3, "CU3": 3}
+    gates = []
+    for _ in range(G):
+        k = kinds[rng.integers(len(kinds))]
+        nq = 2 if k in ("CNOT", "SWAP", "CU3") else 1
+        if nq > n:
+            k, nq = "U3", 1
+        qs = tuple(int(q) for q in rng.choice(n, size=nq, replace=False))
+        gates.append(Gate(k, qs, tuple(Constant(float(v)) for v in rng.uniform(-3, 3, npar.get(k, 0)))))
+    return Circuit(n, tuple(gates), 0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 11, 12, 13])
+def test_sizes_around_the_tile(n):
+    rng = np.random.default_rng(n)
+    circ = _mixed(n, 60, n)
+    st = random_state(n, rng)
+    out = sv.evolve(sv.from_amplitudes(st), circ).amplitudes
+    assert np.abs(out - O.evolve(st, circ.gates)).max() <= 1e-10
+    h = W.dense_random_hamiltonian(n, 30, rng)
+    ref = O.evolve(st, circ.gates)
+    e = sv.expectation(sv.from_amplitudes(ref), h)
+    e_ref = O.expectation(ref, h, n)
+    assert abs(e - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
+
+
+@pytest.mark.parametrize("n", [21, 22])
+def test_specialisation_threshold(n):
+    # QSV_JIT_MIN_QUBITS defaults to 22: both sides of the switch
+    circ = W.brickwork(n, 3, seed=n)
+    out = sv.evolve(sv.init_state("0" * n), circ).amplitudes
+    assert np.abs(out - O.evolve(O.init_state("0" * n), circ.gates)).max() <= 1e-10
+
+
+def test_empty_circuit_and_hamiltonian():
+    n = 6
+    st = random_state(n, np.random.default_rng(0))
+    s = sv.from_amplitudes(st)
+    out = sv.evolve(s, Circuit(n, (), 0))
+    assert np.array_equal(out.amplitudes, st)
+    assert sv.expectation(s, PauliSum(())) == 0.0
+
+
+def test_identity_string_and_identity_rotation():
+    n = 7
+    rng = np.random.default_rng(1)
+    st = random_state(n, rng)
+    h = PauliSum((PauliTerm(2.5, PauliString(())), PauliTerm(-0.5, PauliString.from_label("Z3 X1"))))
+    e = sv.expectation(sv.from_amplitudes(st), h)
+    assert abs(e - O.expectation(st, h, n)) <= 1e-12
+    # exp(-i t/2 I) is the global phase exp(-i t/2) (statevector semantics of a rotation list)
+    x = np.array([0, 0b101], dtype=np.uint64)
+    y = np.array([0, 0], dtype=np.uint64)
+    z = np.array([0, 0b10], dtype=np.uint64)
+    theta = np.array([0.7, -0.3])
+    out = sv.apply_rotations(sv.from_amplitudes(st), x, y, z, theta).amplitudes
+    ref = st * np.exp(-0.35j)
+    scratch = np.empty_like(ref)
+    O.apply_pauli(ref, 0b101, 0, 0b10, scratch)
+    ref = np.cos(-0.15) * ref - 1j * np.sin(-0.15) * scratch
+    assert np.abs(out - ref).max() <= 1e-12
+
+
+def test_invalid_inputs_raise():
+    s = sv.init_state("0000")
+    with pytest.raises(ValueError):
+        sv.evolve(s, Circuit(5, (Gate("H", (4,)),), 0))
+    with pytest.raises(ValueError):
+        sv.expectation(s, PauliSum((PauliTerm(1.0, PauliString.from_label("X4")),)))
+    with pytest.raises(ValueError):
+        sv.sample(s, PauliString.from_label("Z0"), 0, 1)
+    with pytest.raises(ValueError):
+        sv.from_amplitudes(np.ones(3))
