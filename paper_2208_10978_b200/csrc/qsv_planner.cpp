@@ -6,6 +6,7 @@
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <unordered_map>
 
 namespace qsv {
@@ -164,6 +165,77 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
         S.pass_hi[placed] |= need;
         S.pass_cost[placed] += it.cost;
         item_pass[i] = placed;
+    }
+    return S;
+}
+
+// Lookahead pass construction: passes are built one at a time; a pass opens
+// with the earliest ready item (every conflicting earlier item scheduled) and
+// then repeatedly takes, from a window of upcoming ready items, the one that
+// grows the tile's high-bit set least -- commuting items (disjoint qubits /
+// even symplectic product) are pulled forward past non-fitting ones, so
+// passes fill with items that share tile bits instead of closing as soon as
+// the next item in circuit order does not fit.
+Schedule schedule_lookahead(const std::vector<Item> &items, const std::vector<Rot> &R, int m, int c,
+                            int cost_cap, int window)
+{
+    Schedule S;
+    const uint64_t low = c >= 64 ? ~0ull : ((1ull << c) - 1ull);
+    const int free_slots = m - c;
+    const int N = (int)items.size();
+    std::vector<int> npend(N, 0);
+    std::vector<std::vector<int>> succ(N);
+    for (int i = 0; i < N; ++i)
+        for (int j = 0; j < i; ++j)
+            if (conflict(items[j], items[i], R)) {
+                succ[j].push_back(i);
+                ++npend[i];
+            }
+    std::vector<char> done(N, 0);
+    int first = 0, left = N;
+    auto take = [&](int i, int p) {
+        done[i] = 1;
+        --left;
+        S.pass_items[p].push_back(i);
+        S.pass_hi[p] |= items[i].req & ~low;
+        S.pass_cost[p] += items[i].cost;
+        for (int k : succ[i]) --npend[k];
+    };
+    while (left > 0) {
+        while (first < N && done[first]) ++first;
+        int start = -1;
+        for (int i = first; i < N; ++i)
+            if (!done[i] && npend[i] == 0) {
+                start = i;
+                break;
+            }
+        const uint64_t need0 = items[start].req & ~low;
+        const bool fits = popc64(need0) <= free_slots;
+        S.pass_items.emplace_back();
+        S.pass_hi.push_back(0);
+        S.pass_global.push_back(!fits);
+        S.pass_cost.push_back(0);
+        const int p = (int)S.pass_items.size() - 1;
+        take(start, p);
+        if (!fits) continue;
+        for (;;) {
+            int best = -1, best_growth = 1 << 30;
+            const int lim = std::min(N, first + window);
+            for (int i = first; i < lim; ++i) {
+                if (done[i] || npend[i] != 0) continue;
+                const uint64_t need = items[i].req & ~low;
+                if (popc64(S.pass_hi[p] | need) > free_slots) continue;
+                if (items[i].cost != 0 && S.pass_cost[p] + items[i].cost > cost_cap) continue;
+                const int growth = popc64(need & ~S.pass_hi[p]);
+                if (growth < best_growth) {
+                    best_growth = growth;
+                    best = i;
+                    if (growth == 0) break;
+                }
+            }
+            if (best < 0) break;
+            take(best, p);
+        }
     }
     return S;
 }
@@ -1041,6 +1113,21 @@ uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, con
     return h;
 }
 
+// QSV_SCHED: "order" (first fit in circuit order, backfilling earlier passes),
+// "lookahead" (above); default: both, keep the one with fewer passes.
+Schedule pick_schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int n, int m, int c)
+{
+    const char *env = getenv("QSV_SCHED");
+    const char *env_cap = getenv("QSV_PASS_COST_CAP");
+    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 48;
+    if (env && std::string(env) == "order") return schedule(items, R, n, m, c);
+    if (items.size() > 20000) return schedule(items, R, n, m, c);  // O(N^2) conflict graph
+    Schedule L = schedule_lookahead(items, R, m, c, cost_cap, 512);
+    if (env && std::string(env) == "lookahead") return L;
+    Schedule O = schedule(items, R, n, m, c);
+    return L.pass_items.size() < O.pass_items.size() ? L : O;
+}
+
 void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, ProgramTemplate &t)
 {
     t = ProgramTemplate();
@@ -1086,7 +1173,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
         }
     }
     fuse_clusters(items, kinds, qubits, t);
-    Schedule S = schedule(items, R, n, m, c);
+    Schedule S = pick_schedule(items, R, n, m, c);
     emit_program(n, m, c, items, R, kinds, qubits, S, t);
     t.n_input = N;
     t.src_kinds.assign(kinds, kinds + N);
@@ -1101,7 +1188,7 @@ void plan_rotations(int n, const std::vector<Rot> &R, int64_t n_input, ProgramTe
     choose_tile(n, m, c);
     std::vector<Item> items;
     build_items_from_rots(R, items);
-    Schedule S = schedule(items, R, n, m, c);
+    Schedule S = pick_schedule(items, R, n, m, c);
     emit_program(n, m, c, items, R, nullptr, nullptr, S, t);
     t.n_input = n_input;
     t.n_rotations = (int64_t)R.size();
