@@ -431,7 +431,9 @@ def run_engine(args, rank, world, local):
                      "kernel": "qsv_pass (NVRTC-specialised tile pass)",
                      "ms_per_launch": t_pass * 1e3, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": 32 * dim,
-                     "traffic_source": "ncu dram__bytes_read+write of one pass (profiles/r01_jit_pass_ncu.txt)"},
+                     "traffic_source": "ncu dram__bytes_read+write of one pass (profiles/r01_jit_pass_ncu.txt)",
+                     "note": "each pass carries up to 64 dense 2x2 gates and is FP64-bound, "
+                             "not HBM-bound: see the fp64 key for the binding roofline"},
         # the pass is FP64-bound as much as HBM-bound: 560 dense 2x2 complex
         # gates x 2^28 amplitudes x 8 real FMAs = 1.2e12 DFMA per step
         "fp64": {"dfma_per_step": n_u1 * dim * 8, "achieved_tflops": 2 * n_u1 * dim * 8 / t_step / 1e12,

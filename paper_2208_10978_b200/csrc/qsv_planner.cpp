@@ -123,11 +123,12 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
     const uint64_t low = c >= 64 ? ~0ull : ((1ull << c) - 1ull);
     const int free_slots = m - c;
     std::vector<int> item_pass(items.size(), 0);
-    // FP64 budget of one pass (complex FMAs per amplitude).  A pass much
-    // heavier than the HBM time of a pass only grows the specialised kernel
-    // past the instruction cache; the excess is better spent in later passes.
+    // FP64 budget of one pass (complex FMAs per amplitude).  With the
+    // lookahead scheduler fewer, heavier passes win (config 2: cap 48 -> 27
+    // passes / 82 ms, 128 -> 16 passes / 75 ms, FP64-bound); the cap only
+    // keeps specialised kernels from growing without bound.
     const char *env_cap = getenv("QSV_PASS_COST_CAP");
-    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 48;
+    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 128;
     for (size_t i = 0; i < items.size(); ++i) {
         const Item &it = items[i];
         const uint64_t need = it.req & ~low;
@@ -1119,7 +1120,7 @@ Schedule pick_schedule(const std::vector<Item> &items, const std::vector<Rot> &R
 {
     const char *env = getenv("QSV_SCHED");
     const char *env_cap = getenv("QSV_PASS_COST_CAP");
-    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 48;
+    const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 128;
     if (env && std::string(env) == "order") return schedule(items, R, n, m, c);
     if (items.size() > 20000) return schedule(items, R, n, m, c);  // O(N^2) conflict graph
     Schedule L = schedule_lookahead(items, R, m, c, cost_cap, 512);
