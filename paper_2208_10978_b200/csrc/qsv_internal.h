@@ -44,7 +44,7 @@ enum OpType : int32_t {
 
 struct OpRec {  // 32 B
     int32_t type;
-    int32_t a, b, h;  // h: highest flip bit (ROTG) / matrix class (U1: 0 general, 1 m00 real, 2 real)
+    int32_t a, b, h;  // h: highest flip bit (ROTG) / matrix class (U1: 0 general, 1 m00 real, 2 real, 3 m00+m10 real)
     int32_t r0, r1, p;
     uint32_t f;
 };

@@ -485,6 +485,40 @@ void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t
     items.swap(out);
 }
 
+// Structural phase deferral (see PhaseDefer): a U3 item whose next item on
+// its qubit is a CNOT with that qubit as control, followed on that qubit by
+// another U3 item.  Returns per-gate flags for emit_program.
+void find_phase_defers(const std::vector<Item> &items, const int32_t *kinds, const int32_t *qubits,
+                       int n, ProgramTemplate &t)
+{
+    const char *env = getenv("QSV_PHASE_DEFER");
+    if (env && env[0] == '0') return;
+    // per qubit: the item indices touching it, in order
+    std::vector<std::vector<int>> on(n);
+    for (int i = 0; i < (int)items.size(); ++i)
+        for (int q = 0; q < n; ++q)
+            if ((items[i].supp >> q) & 1ull) on[q].push_back(i);
+    auto plain_u3 = [&](int it) {
+        return items[it].gate >= 0 && items[it].cluster < 0 && !items[it].rot &&
+               kinds[items[it].gate] == K_U3;
+    };
+    std::vector<char> is_src(items.size(), 0), is_dst(items.size(), 0);
+    for (int q = 0; q < n; ++q) {
+        const auto &v = on[q];
+        for (size_t k = 0; k + 2 < v.size(); ++k) {
+            const int a = v[k], x = v[k + 1], b = v[k + 2];
+            if (!plain_u3(a) || !plain_u3(b)) continue;
+            const Item &cx = items[x];
+            if (cx.gate < 0 || cx.cluster >= 0 || kinds[cx.gate] != K_CNOT || qubits[2 * cx.gate] != q)
+                continue;
+            if (is_src[a]) continue;
+            is_src[a] = 1;
+            is_dst[b] = 1;
+            t.defers.push_back(PhaseDefer{items[a].gate, items[b].gate});
+        }
+    }
+}
+
 // Fixed 2x2 / 4x4 matrices of the permutation gates (circuit.py:36-45).
 void perm_matrix(int kind, double *o)
 {
@@ -652,6 +686,9 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
                 // 1 = m00 real (U3: m00 = cos(theta/2); HY)
                 if (op.type == OP_U1)
                     op.h = (kind == K_H || kind == K_RY) ? 2 : (kind == K_U3 || kind == K_HY) ? 1 : 0;
+                if (op.type == OP_U1 && kind == K_U3)
+                    for (const PhaseDefer &d : t.defers)
+                        if (d.src == gi) op.h = 3;  // V: m00 and m10 real
                 const int np = param_count(kind);
                 if (np) {
                     op.p = (int)t.n_params;
@@ -1174,6 +1211,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
         }
     }
     fuse_clusters(items, kinds, qubits, t);
+    find_phase_defers(items, kinds, qubits, n, t);
     Schedule S = pick_schedule(items, R, n, m, c);
     emit_program(n, m, c, items, R, kinds, qubits, S, t);
     t.n_input = N;
@@ -1207,7 +1245,28 @@ void materialize_gates(ProgramTemplate &t, const double *values)
 void materialize_params(ProgramTemplate &t, const double *values, double *params)
 {
     materialize_gates(t, values);
-    for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, params + f.offset);
+    if (t.defers.empty()) {
+        for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, params + f.offset);
+    } else {
+        std::unordered_map<int, double> add_lambda;  // receiving gate -> phi of its source
+        std::unordered_map<int, char> deferring;
+        for (const PhaseDefer &d : t.defers) {
+            add_lambda[d.dst] += values[3 * (size_t)d.src + 1];
+            deferring[d.src] = 1;
+        }
+        for (const ParamFill &f : t.fills) {
+            const double *v = values + 3 * (size_t)f.src;
+            if (f.kind != K_U3) {
+                gate_matrix(f.kind, v, params + f.offset);
+                continue;
+            }
+            double vv[3] = {v[0], v[1], v[2]};
+            auto it = add_lambda.find(f.src);
+            if (it != add_lambda.end()) vv[2] += it->second;
+            if (deferring.count(f.src)) vv[1] = 0.0;  // V = U3(t, 0, l): the phi phase moves on
+            gate_matrix(K_U3, vv, params + f.offset);
+        }
+    }
     for (const ClusterFill &cf : t.cfills)
         if (cf.offset >= 0)
             cluster_matrix(cf, t.src_kinds.data(), t.src_qubits.data(), values, params + cf.offset);

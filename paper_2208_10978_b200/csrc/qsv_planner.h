@@ -48,6 +48,17 @@ struct ParamFill {
     int kind;    // gate kind
 };
 
+// Phase deferral of a U3 whose qubit next acts as a CNOT control and then
+// receives another U3: U3(t,p,l) = diag(1, e^{ip}) V(t,l) with
+// V = [[c, -e^{il} s], [s, e^{il} c]] (two real entries: 12 DFMA per pair
+// instead of 14), and diag(1, e^{ip}) commutes with the CNOT control, so it is
+// folded into the receiving U3 as l' = l + p.  Decided from structure; the
+// angles are applied when parameters are materialised.
+struct PhaseDefer {
+    int src;   // deferring U3 gate index (applied as V)
+    int dst;   // receiving U3 gate index (lambda += phi of src)
+};
+
 // A fused same-flip rotation group (OP_GMAT): the table of 2 x 2^(w-1)
 // complex 2x2 matrices is rebuilt from the angles on every call.
 struct GmatFill {
@@ -76,6 +87,7 @@ struct ProgramTemplate {
     std::vector<ParamFill> fills;  // matrices refreshed per call
     std::vector<GmatFill> gfills;  // fused group tables refreshed per call
     std::vector<ClusterFill> cfills;  // dense-fused gate clusters refreshed per call
+    std::vector<PhaseDefer> defers;   // U3 phase deferrals (see PhaseDefer)
     size_t n_params = 0;
     // global-fallback rotation records (full 64-bit masks), per pass: rots[r0..r1)
     int64_t n_input = 0, n_rotations = 0, n_items = 0, n_fallback = 0, n_blocks = 0;
