@@ -765,6 +765,33 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
                 if ((bits >> b) & 1u) pos[k++] = b;
                 else nb[kn++] = b;
             }
+            // Thread bits 0-2 index the 8 lanes of a quarter warp, whose 16 B
+            // LDS/STS must land in 8 distinct granules of a 128 B bank row:
+            // put first three non-block bits whose swizzled slot columns are
+            // independent in their granule bits (low 3 bits).  Any order of
+            // the thread bits is valid -- gather, scatter and the per-block
+            // sign / thread-bit tables all use this same nb[] order.
+            if (kn >= 3) {
+                int pick[3], np = 0;
+                uint32_t basis[3] = {0, 0, 0};  // reduced granule vectors
+                for (int i = 0; i < kn && np < 3; ++i) {
+                    uint32_t v = swz16(Ab[nb[i]]) & 7u;
+                    for (int j = 0; j < np; ++j)
+                        if ((v ^ basis[j]) < v) v ^= basis[j];
+                    if (v == 0) continue;
+                    // keep the basis in echelon form (distinct leading bits)
+                    basis[np] = v;
+                    for (int a = np; a > 0 && basis[a] > basis[a - 1]; --a) std::swap(basis[a], basis[a - 1]);
+                    pick[np++] = i;
+                }
+                if (np == 3) {
+                    int reordered[12], r = 0;
+                    for (int j = 0; j < 3; ++j) reordered[r++] = nb[pick[j]];
+                    for (int i = 0; i < kn; ++i)
+                        if (i != pick[0] && i != pick[1] && i != pick[2]) reordered[r++] = nb[i];
+                    for (int i = 0; i < kn; ++i) nb[i] = reordered[i];
+                }
+            }
             auto local = [&](int b) {
                 for (int j = 0; j < RB; ++j)
                     if (pos[j] == b) return j;
