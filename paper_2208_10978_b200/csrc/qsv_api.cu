@@ -112,12 +112,6 @@ struct Blob {
         if (n) std::memcpy(bytes.data() + off, p, n);
         return off;
     }
-    size_t reserve(size_t n)
-    {
-        size_t off = (bytes.size() + 255) & ~(size_t)255;
-        bytes.resize(off + n);
-        return off;
-    }
 };
 
 // Upload blob into the head of the device workspace; extra = trailing scratch.

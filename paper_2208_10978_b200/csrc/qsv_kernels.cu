@@ -27,8 +27,6 @@ namespace qsv {
 namespace {
 
 constexpr int kTileThreads = 256;
-constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kMaxPer = (1 << kMaxTileBits) / kTileThreads;  // amplitudes per thread (16)
 constexpr int kRotPairs = 2;                                 // pairs held in registers per rotation sweep
 constexpr int kTermChunk = 8;
 

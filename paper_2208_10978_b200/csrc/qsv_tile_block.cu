@@ -606,11 +606,6 @@ __device__ __forceinline__ void mbar_init(uint64_t *b, int count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *b)
-{
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
-                 : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
 {
     asm volatile(
@@ -651,7 +646,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
 tile_ring_kernel(double2 *__restrict__ psi, const TileDims g, const uint64_t *__restrict__ g_offhi,
                  const int32_t *__restrict__ g_geo, const PassProgram prog)
 {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int m = kMaxTileBits;
     constexpr int tsize = 1 << m;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);            // [2 * kStages]
