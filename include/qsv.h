@@ -136,6 +136,15 @@ int qsv_plan_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const in
 int qsv_plan_expectation(int n_qubits, int64_t n_terms, const uint64_t *x, const uint64_t *y,
                          const uint64_t *z, qsv_plan_stats *out);
 
+/* The planner's recognition of pauli_evolution blocks (circuit.py:271-281):
+ * count receives the number of blocks; the first min(count, cap) are written
+ * as spans[3k..3k+2] = {first gate, gate count, index of the RZ gate whose
+ * bound value is theta} and masks[3k..3k+2] = {x, y, z} of P (the block is
+ * exp(-i theta/2 P)).  Used by the sharded path to schedule rotations whose
+ * flips avoid the global qubits as local work.  No device work. */
+int qsv_match_rotations(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                        int64_t cap, int64_t *spans, uint64_t *masks, int64_t *count);
+
 /* Debug: the compiled tile program for a gate list as JSON (planner output
  * consumed by the CPU emulator in tests/).  needed receives the buffer size. */
 int qsv_debug_plan_json(int n_qubits, int64_t n_gates, const int32_t *kinds,

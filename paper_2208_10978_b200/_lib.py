@@ -51,7 +51,8 @@ EXPORTED = (
     "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_apply_1q", "qsv_apply_2q",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
-    "qsv_plan_expectation", "qsv_debug_plan_json", "qsv_sample_parity", "qsv_jit_info",
+    "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_sample_parity",
+    "qsv_jit_info",
     "qsv_last_plan_stats",
 )
 
@@ -94,6 +95,8 @@ def _declare(L):
         "qsv_debug_plan_json": ([ctypes.c_int, i64, i32p, i32p, dp, ctypes.c_char_p, i64,
                                  ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_sample_parity": ([vp, u64, i64, u64p, dp, ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_match_rotations": ([ctypes.c_int, i64, i32p, i32p, i64, ctypes.POINTER(i64), u64p,
+                                 ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_jit_info": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_last_plan_stats": ([sp], ctypes.c_int),
     }
@@ -153,6 +156,23 @@ def jit_info() -> tuple[bool, int]:
     av, n = ctypes.c_int(0), ctypes.c_int64(0)
     check(lib().qsv_jit_info(ctypes.byref(av), ctypes.byref(n)))
     return bool(av.value), int(n.value)
+
+
+def match_rotations(n_qubits: int, kinds, qubits):
+    """Recognised pauli_evolution blocks: (spans int64[R, 3] = start, length,
+    rz gate; masks uint64[R, 3] = x, y, z)."""
+    import numpy as np
+
+    cnt = ctypes.c_int64(0)
+    check(lib().qsv_match_rotations(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits), 0, None,
+                                    None, ctypes.byref(cnt)))
+    spans = np.zeros((cnt.value, 3), dtype=np.int64)
+    masks = np.zeros((cnt.value, 3), dtype=np.uint64)
+    if cnt.value:
+        check(lib().qsv_match_rotations(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits), cnt.value,
+                                        spans.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                        u64ptr(masks), ctypes.byref(cnt)))
+    return spans, masks
 
 
 def dptr(a):

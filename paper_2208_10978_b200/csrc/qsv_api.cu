@@ -857,6 +857,35 @@ int qsv_apply_2q(qsv_state *s, const double *m, int q0, int q1)
     return run_template(s, t, params);
 }
 
+int qsv_match_rotations(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                        int64_t cap, int64_t *spans, uint64_t *masks, int64_t *count)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!count) return fail_code(QSV_ERR_INVALID, "null output");
+    if (n < 1 || n > kMaxQubits) return fail_code(QSV_ERR_RESOURCE, "qubit count out of range");
+    if (n_gates < 0 || (n_gates > 0 && (!kinds || !qubits)))
+        return fail_code(QSV_ERR_INVALID, "bad gate arrays");
+    qsv_state fake;
+    fake.n = n;
+    if (int rc = validate_gates(&fake, n_gates, kinds, qubits)) return rc;
+    std::vector<RotSpan> out;
+    match_rotations(n_gates, kinds, qubits, out);
+    *count = (int64_t)out.size();
+    for (int64_t k = 0; k < (int64_t)out.size() && k < cap; ++k) {
+        if (spans) {
+            spans[3 * k] = out[k].start;
+            spans[3 * k + 1] = out[k].len;
+            spans[3 * k + 2] = out[k].rz;
+        }
+        if (masks) {
+            masks[3 * k] = out[k].x;
+            masks[3 * k + 1] = out[k].y;
+            masks[3 * k + 2] = out[k].z;
+        }
+    }
+    return QSV_OK;
+}
+
 int qsv_plan_gates(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
                    qsv_plan_stats *out)
 {

@@ -1163,6 +1163,22 @@ void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<in
     comp32[44] = pp ? pp->store_t : 0;
 }
 
+void match_rotations(int64_t N, const int32_t *kinds, const int32_t *qubits, std::vector<RotSpan> &out)
+{
+    out.clear();
+    int64_t i = 0;
+    while (i < N) {
+        Rot rot;
+        int64_t len = 0;
+        if (match_block(kinds, qubits, N, i, rot, len)) {
+            out.push_back(RotSpan{i, len, rot.x, rot.y, rot.z, (int64_t)rot.src});
+            i += len;
+        } else {
+            ++i;
+        }
+    }
+}
+
 uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits)
 {
     uint64_t h = 1469598103934665603ull ^ (uint64_t)n_qubits;

@@ -142,4 +142,14 @@ void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<in
 
 uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits);
 
+// pauli_evolution blocks recognised in a gate list (the planner's matcher):
+// gates [start, start + len) equal exp(-i theta/2 P(x, y, z)), theta = the
+// bound value of gate rz.
+struct RotSpan {
+    int64_t start, len;
+    uint64_t x, y, z;
+    int64_t rz;
+};
+void match_rotations(int64_t n_gates, const int32_t *kinds, const int32_t *qubits, std::vector<RotSpan> &out);
+
 }  // namespace qsv

@@ -41,6 +41,7 @@ compute goes through a ``LocalEngine``; ``CudaEngine`` is the product one.
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import math
 from dataclasses import dataclass
 from typing import Optional
@@ -48,6 +49,10 @@ from typing import Optional
 import numpy as np
 
 K_SWAP = 4  # gate-kind code of SWAP (include/qsv.h)
+
+# sharded plans keyed on (gate-list structure, qubit count, local qubits,
+# qubit map): energy evaluations only refresh angles
+_PLAN_CACHE: dict = {}
 
 
 # ---------------------------------------------------------------------------
@@ -107,6 +112,16 @@ class CudaEngine:
                                               ctypes.byref(re), ctypes.byref(im), _lib.dptr(per),
                                               None))
         return per
+
+    def apply_rotations(self, shard, x, y, z, theta) -> None:
+        """In place: prod_r exp(-i theta_r/2 P_r) (qsv_apply_pauli_rotations)."""
+        from . import _lib
+
+        if len(theta) == 0:
+            return
+        _lib.check(_lib.lib().qsv_apply_pauli_rotations(shard.handle, len(theta), _lib.u64ptr(x),
+                                                        _lib.u64ptr(y), _lib.u64ptr(z),
+                                                        _lib.dptr(theta), None))
 
     def apply_pauli(self, src, dst, x: int, y: int, z: int) -> None:
         """dst = P src (kernels.apply_pauli, _cykernels.pyx:76-102)."""
@@ -309,6 +324,130 @@ def plan_segments(kinds, qubits, n: int, n_local: int, perm):
     return segs, perm
 
 
+@dataclass
+class UnitSegment:
+    """Local work between relayouts: entries in order, each either
+    ("g", gate index or -1 for an inserted SWAP, q0, q1) with physical local
+    qubits, or ("r", x, y, z, zg, rz) -- a direct Pauli rotation with local
+    physical masks x/y/z, global Z bits zg (a per-rank sign of the angle) and
+    the gate index whose bound value is its angle."""
+    entries: list
+    relayout: Optional[Relayout]
+
+
+def _bits(mask: int):
+    while mask:
+        low = mask & -mask
+        yield low.bit_length() - 1
+        mask ^= low
+
+
+def plan_units(kinds, qubits, n: int, n_local: int, perm, spans, masks):
+    """Light-cone scheduling over units: recognised pauli_evolution blocks are
+    ONE unit each (exp(-i theta/2 P)), other gates are units of their own.  A
+    rotation is local when its flip (x|y) avoids the global qubits -- Z on a
+    global qubit is a per-rank sign of the angle -- so a UCC circuit's CNOT
+    ladders through global qubits no longer force exchanges.  A unit runs now
+    when it is local and commutes with every deferred unit (rotations:
+    symplectic product; otherwise disjoint support).  Returns (segments, perm)."""
+    g = n - n_local
+    perm = list(perm)
+    inv = [0] * n
+    for q, p in enumerate(perm):
+        inv[p] = q
+    units = []  # (kind, a, b, supp, flip, x, y, z)
+    G = len(kinds)
+    span_at = {int(st): k for k, st in enumerate(spans[:, 0])} if len(spans) else {}
+    i = 0
+    while i < G:
+        k = span_at.get(i)
+        if k is not None:
+            x, y, z = (int(v) for v in masks[k])
+            units.append(("r", int(spans[k, 2]), 0, x | y | z, x | y, x, y, z))
+            i += int(spans[k, 1])
+            continue
+        gq = _gate_qubits(qubits, i)
+        sm = 0
+        for q in gq:
+            sm |= 1 << q
+        units.append(("g", i, 0, sm, 0, 0, 0, 0))
+        i += 1
+
+    def needs(u):
+        return u[4] if u[0] == "r" else u[3]
+
+    def anti(a, b):
+        ax, az = a[5] | a[6], a[6] | a[7]
+        bx, bz = b[5] | b[6], b[6] | b[7]
+        return (bin(ax & bz).count("1") + bin(az & bx).count("1")) & 1
+
+    def conflict(a, b):
+        if not (a[3] & b[3]):
+            return False
+        if a[0] == "r" and b[0] == "r":
+            return bool(anti(a, b))
+        return True
+
+    def phys(mask):
+        out = 0
+        for q in _bits(mask):
+            out |= 1 << perm[q]
+        return out
+
+    lmask = (1 << n_local) - 1
+    segs = []
+    entries = []
+    remaining = list(range(len(units)))
+    while True:
+        deferred = []
+        dunion = 0
+        for ui in remaining:
+            u = units[ui]
+            local = (phys(needs(u)) >> n_local) == 0
+            ok = local
+            if ok and (u[3] & dunion):
+                for dj in deferred:
+                    if conflict(units[dj], u):
+                        ok = False
+                        break
+            if ok:
+                if u[0] == "g":
+                    gq = _gate_qubits(qubits, u[1])
+                    entries.append(("g", u[1], perm[gq[0]], perm[gq[1]] if len(gq) == 2 else -1))
+                else:
+                    px, py, pz = phys(u[5]), phys(u[6]), phys(u[7])
+                    entries.append(("r", px & lmask, py & lmask, pz & lmask, pz >> n_local, u[1]))
+            else:
+                deferred.append(ui)
+                dunion |= u[3]
+        remaining = deferred
+        if not remaining:
+            break
+        # bring in the global qubits the deferred units need, head first
+        bring, first_use = [], {}
+        for pos, ui in enumerate(remaining):
+            for q in _bits(needs(units[ui])):
+                first_use.setdefault(q, pos)
+                if perm[q] >= n_local and q not in bring and len(bring) < g:
+                    bring.append(q)
+        head = set(_bits(needs(units[remaining[0]])))
+        cand = sorted((inv[p] for p in range(n_local) if inv[p] not in head and inv[p] not in bring),
+                      key=lambda q: (-first_use.get(q, math.inf), q))
+        if len(cand) < len(bring):
+            raise ValueError("too few local qubits for a relayout")
+        victims = cand[:len(bring)]
+        swaps = []
+        _move_victims(perm, inv, victims, n_local, swaps)
+        for a, b in swaps:
+            entries.append(("g", -1, a, b))
+        S = tuple(perm[b] - n_local for b in bring)
+        segs.append(UnitSegment(entries, Relayout(S)))
+        _apply_relayout_to_map(perm, inv, bring, victims, n_local)
+        entries = []
+    segs.append(UnitSegment(entries, None))
+    return segs, perm
+
+
 def plan_localize(flips: list[int], n: int, n_local: int, perm):
     """Relayout that makes flips[0] (logical mask) local, evicting the local
     qubits least used by the other flips.  Returns (swaps, Relayout, new perm)."""
@@ -464,7 +603,25 @@ class DistStateVector:
     # -- gates ---------------------------------------------------------------
     def apply_flat(self, kinds, qubits, values) -> None:
         """Apply a flattened bound gate list (logical qubits) in place."""
-        segs, perm = plan_segments(kinds, qubits, self.n_qubits, self.n_local, self.perm)
+        key = (hashlib.blake2b(kinds.tobytes() + qubits.tobytes(), digest_size=16).digest(),
+               self.n_qubits, self.n_local, tuple(self.perm))
+        plan = _PLAN_CACHE.get(key)
+        if plan is None:
+            from . import _lib
+
+            spans, masks = _lib.match_rotations(self.n_qubits, kinds, qubits)
+            if len(spans):
+                plan = ("units",) + plan_units(kinds, qubits, self.n_qubits, self.n_local, self.perm,
+                                               spans, masks)
+            else:
+                plan = ("gates",) + plan_segments(kinds, qubits, self.n_qubits, self.n_local, self.perm)
+            if len(_PLAN_CACHE) >= 16:
+                _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+            _PLAN_CACHE[key] = plan
+        if plan[0] == "units":
+            self._apply_units(kinds, qubits, values, plan[1], plan[2])
+            return
+        segs, perm = plan[1], plan[2]
         for seg in segs:
             L = len(seg.src)
             if L:
@@ -478,6 +635,43 @@ class DistStateVector:
                         sv_[3 * j:3 * j + 3] = values[3 * i:3 * i + 3]
                 for r in self.comm.owned:
                     self.engine.apply_gates(self.shards[r], sk, seg.qubits, sv_)
+            if seg.relayout is not None:
+                self._relayout(seg.relayout)
+        self.perm = perm
+
+    def _apply_units(self, kinds, qubits, values, segs, perm) -> None:
+        for seg in segs:
+            k = 0
+            E = seg.entries
+            while k < len(E):
+                j = k
+                while j < len(E) and E[j][0] == E[k][0]:
+                    j += 1
+                run = E[k:j]
+                if E[k][0] == "g":
+                    L = len(run)
+                    sk = np.empty(L, dtype=np.int32)
+                    sq = np.empty(2 * L, dtype=np.int32)
+                    sv_ = np.zeros(3 * L, dtype=np.float64)
+                    for t, (_, gi, a, b) in enumerate(run):
+                        sq[2 * t], sq[2 * t + 1] = a, b
+                        if gi < 0:
+                            sk[t] = K_SWAP
+                        else:
+                            sk[t] = kinds[gi]
+                            sv_[3 * t:3 * t + 3] = values[3 * gi:3 * gi + 3]
+                    for r in self.comm.owned:
+                        self.engine.apply_gates(self.shards[r], sk, sq, sv_)
+                else:
+                    x = np.array([e[1] for e in run], dtype=np.uint64)
+                    y = np.array([e[2] for e in run], dtype=np.uint64)
+                    z = np.array([e[3] for e in run], dtype=np.uint64)
+                    zg = [e[4] for e in run]
+                    th = np.array([values[3 * e[5]] for e in run], dtype=np.float64)
+                    for r in self.comm.owned:
+                        sign = np.array([-1.0 if bin(m & r).count("1") & 1 else 1.0 for m in zg])
+                        self.engine.apply_rotations(self.shards[r], x, y, z, th * sign)
+                k = j
             if seg.relayout is not None:
                 self._relayout(seg.relayout)
         self.perm = perm

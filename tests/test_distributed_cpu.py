@@ -60,6 +60,12 @@ class OracleEngine:
     def apply_pauli(self, src, dst, x, y, z):
         O.apply_pauli(src.amps, int(x), int(y), int(z), dst.amps)
 
+    def apply_rotations(self, shard, x, y, z, theta):
+        scratch = np.empty_like(shard.amps)
+        for k in range(len(theta)):
+            O.apply_pauli(shard.amps, int(x[k]), int(y[k]), int(z[k]), scratch)
+            shard.amps[:] = np.cos(theta[k] / 2) * shard.amps - 1j * np.sin(theta[k] / 2) * scratch
+
     def vdot(self, a, b):
         return complex(np.vdot(a.amps, b.amps))
 

@@ -107,3 +107,18 @@ def test_process_group_sharded_on_device(D):
         assert np.abs(amps - ref).max() < 1e-10
         assert abs(e - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
         assert nrel >= 1
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_sharded_ucc_units_16q(D, P):
+    """UCC rotations as units: flips off the global qubits run as direct
+    rotations with a per-rank angle sign for global Z; others via relayouts."""
+    cfg = W.config1(seed=4, n_qubits=16, n_electrons=8, n_terms=100)
+    ref = O.evolve(O.init_state(cfg["reference"]), cfg["circuit"].gates)
+    be = D.DistributedBackend(D.LoopbackComm(P))
+    psi = be.evolve(be.prepare(cfg["reference"]), cfg["circuit"])
+    assert np.abs(psi.amplitudes() - ref).max() < 1e-10
+    assert psi.stats["relayouts"] >= 1
+    e = be.expectation(psi, cfg["hamiltonian"])
+    e_ref = O.expectation(ref, cfg["hamiltonian"], 16)
+    assert abs(e - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
