@@ -23,6 +23,8 @@
 // loads (and its planner entry points work) on machines without a GPU driver.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -575,8 +577,74 @@ struct Module {
 // device -> source -> module
 std::unordered_map<std::string, Module> g_mods[64];
 
+// Optional on-disk cubin cache (QSV_JIT_CACHE=dir, default ~/.cache/qsv_jit,
+// "0" disables): a pure compile-time saving, keyed by a 64-bit FNV-1a hash of
+// the generated source plus its length; a hit is only used when the cached
+// file also carries the exact source it was compiled from.
+std::string cache_path(const std::string &src)
+{
+    const char *env = getenv("QSV_JIT_CACHE");
+    std::string dir;
+    if (env) {
+        if (env[0] == '0' && env[1] == 0) return "";
+        dir = env;
+    } else if (const char *home = getenv("HOME")) {
+        dir = std::string(home) + "/.cache/qsv_jit";
+    } else {
+        return "";
+    }
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char ch : src) {
+        h ^= ch;
+        h *= 1099511628211ull;
+    }
+    char name[64];
+    snprintf(name, sizeof(name), "/%016llx_%zu.bin", (unsigned long long)h, src.size());
+    return dir + name;
+}
+
+bool cache_load(const std::string &path, const std::string &src, std::vector<char> &cubin)
+{
+    if (path.empty()) return false;
+    FILE *f = fopen(path.c_str(), "rb");
+    if (!f) return false;
+    uint64_t ls = 0, lc = 0;
+    bool ok = fread(&ls, 8, 1, f) == 1 && ls == src.size();
+    std::string stored;
+    if (ok) {
+        stored.resize(ls);
+        ok = fread(&stored[0], 1, ls, f) == ls && stored == src && fread(&lc, 8, 1, f) == 1 && lc > 0;
+    }
+    if (ok) {
+        cubin.resize(lc);
+        ok = fread(cubin.data(), 1, lc, f) == lc;
+    }
+    fclose(f);
+    return ok;
+}
+
+void cache_store(const std::string &path, const std::string &src, const std::vector<char> &cubin)
+{
+    if (path.empty()) return;
+    const std::string dir = path.substr(0, path.rfind('/'));
+    std::string cmd_dir;
+    for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
+        if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)getpid());
+    FILE *f = fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const uint64_t ls = src.size(), lc = cubin.size();
+    bool ok = fwrite(&ls, 8, 1, f) == 1 && fwrite(src.data(), 1, ls, f) == ls && fwrite(&lc, 8, 1, f) == 1 &&
+              fwrite(cubin.data(), 1, lc, f) == lc;
+    ok = (fclose(f) == 0) && ok;
+    if (ok) rename(tmp.c_str(), path.c_str());
+    else remove(tmp.c_str());
+}
+
 bool compile(const std::string &src, Module &m)
 {
+    const std::string cpath = cache_path(src);
+    if (cache_load(cpath, src, m.cubin)) return true;
     nvrtcProgram prog = nullptr;
     if (g_api.CreateProgram(&prog, src.c_str(), "qsv_pass.cu", 0, nullptr, nullptr) != 0) {
         m.log = "nvrtcCreateProgram failed";
@@ -601,6 +669,7 @@ bool compile(const std::string &src, Module &m)
         }
     }
     g_api.DestroyProgram(&prog);
+    if (ok) cache_store(cpath, src, m.cubin);
     return ok;
 }
 
