@@ -194,49 +194,80 @@ Schedule schedule_lookahead(const std::vector<Item> &items, const std::vector<Ro
             }
     std::vector<char> done(N, 0);
     int first = 0, left = N;
-    auto take = [&](int i, int p) {
-        done[i] = 1;
-        --left;
-        S.pass_items[p].push_back(i);
-        S.pass_hi[p] |= items[i].req & ~low;
-        S.pass_cost[p] += items[i].cost;
-        for (int k : succ[i]) --npend[k];
+    // Fill one pass greedily from `seed`; with `undo` the changes are rolled
+    // back and only the pass's (work, items) score is returned.
+    std::vector<int> taken;
+    auto fill = [&](int seed, bool undo, uint64_t &hi, int &cost) {
+        taken.clear();
+        hi = 0;
+        cost = 0;
+        auto take = [&](int i) {
+            done[i] = 1;
+            taken.push_back(i);
+            hi |= items[i].req & ~low;
+            cost += items[i].cost;
+            for (int k : succ[i]) --npend[k];
+        };
+        take(seed);
+        if (popc64(items[seed].req & ~low) <= free_slots) {
+            for (;;) {
+                int best = -1, best_growth = 1 << 30;
+                const int lim = std::min(N, first + window);
+                for (int i = first; i < lim; ++i) {
+                    if (done[i] || npend[i] != 0) continue;
+                    const uint64_t need = items[i].req & ~low;
+                    if (popc64(hi | need) > free_slots) continue;
+                    if (items[i].cost != 0 && cost + items[i].cost > cost_cap) continue;
+                    const int growth = popc64(need & ~hi);
+                    if (growth < best_growth) {
+                        best_growth = growth;
+                        best = i;
+                        if (growth == 0) break;
+                    }
+                }
+                if (best < 0) break;
+                take(best);
+            }
+        }
+        if (undo)
+            for (int i : taken) {
+                done[i] = 0;
+                for (int k : succ[i]) ++npend[k];
+            }
     };
+    const char *env_seeds = getenv("QSV_SCHED_SEEDS");
+    const int nseeds = env_seeds ? std::max(1, atoi(env_seeds)) : (N <= 4096 ? 8 : 1);
     while (left > 0) {
         while (first < N && done[first]) ++first;
-        int start = -1;
-        for (int i = first; i < N; ++i)
-            if (!done[i] && npend[i] == 0) {
-                start = i;
-                break;
-            }
-        const uint64_t need0 = items[start].req & ~low;
-        const bool fits = popc64(need0) <= free_slots;
-        S.pass_items.emplace_back();
-        S.pass_hi.push_back(0);
-        S.pass_global.push_back(!fits);
-        S.pass_cost.push_back(0);
-        const int p = (int)S.pass_items.size() - 1;
-        take(start, p);
-        if (!fits) continue;
-        for (;;) {
-            int best = -1, best_growth = 1 << 30;
-            const int lim = std::min(N, first + window);
-            for (int i = first; i < lim; ++i) {
-                if (done[i] || npend[i] != 0) continue;
-                const uint64_t need = items[i].req & ~low;
-                if (popc64(S.pass_hi[p] | need) > free_slots) continue;
-                if (items[i].cost != 0 && S.pass_cost[p] + items[i].cost > cost_cap) continue;
-                const int growth = popc64(need & ~S.pass_hi[p]);
-                if (growth < best_growth) {
-                    best_growth = growth;
-                    best = i;
-                    if (growth == 0) break;
+        // candidate seeds: the first ready items; keep the one whose pass
+        // carries the most work (then the most items)
+        int cands[64], nc = 0;
+        for (int i = first; i < N && nc < nseeds && nc < 64; ++i)
+            if (!done[i] && npend[i] == 0) cands[nc++] = i;
+        int start = cands[0];
+        if (nc > 1 && popc64(items[start].req & ~low) <= free_slots) {
+            long best_score = -1;
+            for (int k = 0; k < nc; ++k) {
+                if (popc64(items[cands[k]].req & ~low) > free_slots) continue;
+                uint64_t hi;
+                int cost;
+                fill(cands[k], true, hi, cost);
+                const long score = (long)cost * 4096 + (long)taken.size();
+                if (score > best_score) {
+                    best_score = score;
+                    start = cands[k];
                 }
             }
-            if (best < 0) break;
-            take(best, p);
         }
+        const bool fits = popc64(items[start].req & ~low) <= free_slots;
+        uint64_t hi;
+        int cost;
+        fill(start, false, hi, cost);
+        S.pass_items.push_back(taken);
+        S.pass_hi.push_back(hi);
+        S.pass_global.push_back(!fits);
+        S.pass_cost.push_back(cost);
+        left -= (int)taken.size();
     }
     return S;
 }
