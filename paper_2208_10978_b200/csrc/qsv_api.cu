@@ -959,7 +959,8 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
         for (int b = p.block_begin; b < p.block_end; ++b) {
             const BlockRec &br = t.blocks[b];
             if (b > p.block_begin) j += ",";
-            j += "{\"kind\":" + std::to_string(br.kind) + ",\"op0\":" + std::to_string(br.op0) +
+            j += "{\"kind\":" + std::to_string(br.kind) + ",\"flags\":" + std::to_string(br.pad0) +
+                 ",\"op0\":" + std::to_string(br.op0) +
                  ",\"op1\":" + std::to_string(br.op1) + ",\"tswz\":" + std::to_string(br.tswz) +
                  ",\"cols\":[";
             for (int i = 0; i < 12; ++i) j += (i ? "," : "") + std::to_string(br.cols[i]);

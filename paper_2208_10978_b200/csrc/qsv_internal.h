@@ -70,7 +70,7 @@ struct BlockRec {  // 48 B
     int32_t op0, op1;
     uint16_t cols[12];
     uint16_t tswz;
-    uint16_t pad0;
+    uint16_t pad0;  // bit 0: warp-local entry (the transition into this block needs only __syncwarp)
     int32_t pad[2];
 };
 

@@ -748,7 +748,10 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
             snprintf(buf, sizeof(buf), "    sm[sb ^ %uu] = a[%d];\n", E[r], r);
             body += buf;
         }
-        body += "  }\n  gsync(bar);\n";
+        // group barrier, or only __syncwarp when the next block keeps this
+        // warp's W-coset of slots (BlockRec.pad0 bit 0, qsv_planner.cpp)
+        if (bi + 1 < nblocks && (blocks[bi + 1].pad0 & 1)) body += "  }\n  __syncwarp();\n";
+        else body += "  }\n  gsync(bar);\n";
     }
     snprintf(buf, sizeof(buf), "#define QSV_NPARAMS %d\n", std::max(1, nparams));
     src = buf;

@@ -773,11 +773,43 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
             default: return 0u;  // diagonal ops fit any block
         }
     };
+    // Warp-local block transitions: three tile bits W are kept as the warp
+    // index bits (thread bits 5-7) of every block whose register bits avoid
+    // them.  Consecutive such blocks then read and write the same W-coset of
+    // slots per warp (a permutation between them must not move W bits), so
+    // the transition needs only __syncwarp instead of a group barrier --
+    // warps run ahead of each other through chains of blocks.  W = the three
+    // tile bits fewest ops need in registers.
+    uint32_t Wmask = 0;
+    bool has_rot = false;
+    for (const OpRec &op : src) has_rot |= op.type == OP_ROTG || op.type == OP_ROTD;
+    // (measured: a gain on gate passes, a loss on rotation-group passes,
+    // where the fixed warp bits cost bank-conflict-free coset orders)
+    if (m == kMaxTileBits && kBlockBits == 4 && !has_rot) {
+        int cnt[12] = {0};
+        for (const OpRec &op : src)
+            if (op.type == OP_U1 || op.type == OP_U2 || op.type == OP_ROTG)
+                for (int b = 0; b < m; ++b) cnt[b] += (req(op) >> b) & 1u;
+        for (int k = 0; k < 3; ++k) {
+            int best = -1;
+            for (int b = m - 1; b >= 0; --b)
+                if (!((Wmask >> b) & 1u) && (best < 0 || cnt[b] < cnt[best])) best = b;
+            Wmask |= 1u << best;
+        }
+        const char *env_wl = getenv("QSV_WARP_LOCAL");
+        if (env_wl && env_wl[0] == '0') Wmask = 0;
+    }
+    bool prev_conform = false, perm_breaks = false;
     auto apply_perm = [&](const OpRec &op) {
         // psi'(L) = psi(P L) with P an involution, data unmoved: map' = map o P
         if (op.type == OP_CX) A[op.a] ^= A[op.b];
         else if (op.type == OP_SWAP) std::swap(A[op.a], A[op.b]);
         else tr ^= A[op.a];
+        // does P move W bits (map a warp's W-coset onto another)?
+        const uint32_t moved = op.type == OP_CX ? (1u << op.b)
+                               : op.type == OP_SWAP ? ((1u << op.a) | (1u << op.b))
+                                                    : (1u << op.a);
+        if (moved & Wmask) perm_breaks = true;
     };
     std::vector<OpRec> pending, perms;
     uint32_t cur = 0, D = 0;
@@ -789,8 +821,10 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
     auto flush = [&]() {
         if (!pending.empty()) {
             constexpr int RB = kBlockBits, TB = kMaxTileBits - kBlockBits;
+            const bool conform = Wmask != 0 && (cur & Wmask) == 0;
             uint32_t bits = cur;
-            for (int b = m - 1; b >= 0 && __builtin_popcount(bits) < RB; --b) bits |= 1u << b;
+            for (int b = m - 1; b >= 0 && __builtin_popcount(bits) < RB; --b)
+                if (!conform || !((Wmask >> b) & 1u)) bits |= 1u << b;
             int pos[RB], nb[12], k = 0, kn = 0;
             for (int b = 0; b < m; ++b) {
                 if ((bits >> b) & 1u) pos[k++] = b;
@@ -802,10 +836,22 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
             // independent in their granule bits (low 3 bits).  Any order of
             // the thread bits is valid -- gather, scatter and the per-block
             // sign / thread-bit tables all use this same nb[] order.
-            if (kn >= 3) {
+            // conforming blocks: the W bits go last (thread bits 5-7)
+            int kl = kn;  // leading (lane + low thread) bits eligible for reordering
+            if (conform) {
+                int lead[12], tail[12], nl = 0, nt = 0;
+                for (int i = 0; i < kn; ++i) {
+                    if ((Wmask >> nb[i]) & 1u) tail[nt++] = nb[i];
+                    else lead[nl++] = nb[i];
+                }
+                for (int i = 0; i < nl; ++i) nb[i] = lead[i];
+                for (int i = 0; i < nt; ++i) nb[nl + i] = tail[i];
+                kl = nl;
+            }
+            if (kl >= 3) {
                 int pick[3], np = 0;
                 uint32_t basis[3] = {0, 0, 0};  // reduced granule vectors
-                for (int i = 0; i < kn && np < 3; ++i) {
+                for (int i = 0; i < kl && np < 3; ++i) {
                     uint32_t v = swz16(Ab[nb[i]]) & 7u;
                     for (int j = 0; j < np; ++j)
                         if ((v ^ basis[j]) < v) v ^= basis[j];
@@ -818,9 +864,9 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
                 if (np == 3) {
                     int reordered[12], r = 0;
                     for (int j = 0; j < 3; ++j) reordered[r++] = nb[pick[j]];
-                    for (int i = 0; i < kn; ++i)
+                    for (int i = 0; i < kl; ++i)
                         if (i != pick[0] && i != pick[1] && i != pick[2]) reordered[r++] = nb[i];
-                    for (int i = 0; i < kn; ++i) nb[i] = reordered[i];
+                    for (int i = 0; i < kl; ++i) nb[i] = reordered[i];
                 }
             }
             auto local = [&](int b) {
@@ -853,6 +899,10 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
             };
             BlockRec br{};
             br.kind = 0;
+            // entry flag: the transition into this block may be __syncwarp
+            br.pad0 = (prev_conform && conform && !perm_breaks) ? 1 : 0;
+            prev_conform = conform;
+            perm_breaks = false;
             for (int i = 0; i < kn && i < TB; ++i) br.cols[i] = swz16(Ab[nb[i]]);
             for (int j = 0; j < RB; ++j) br.cols[TB + j] = swz16(Ab[pos[j]]);
             br.tswz = swz16(tb);
@@ -1082,6 +1132,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
         if (s & D) flush();
         if (op.type == OP_ROTG && __builtin_popcount(op.f) > kBlockBits) {
             flush();
+            prev_conform = false;
             BlockRec br{};
             br.kind = 1;
             for (int b = 0; b < 12; ++b) br.cols[b] = swz16(A[b]);
