@@ -1,6 +1,6 @@
-"""Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
-synccheck): specialised + interpreted tile passes, fused rotation groups,
-expectation sweeps, sampling, gradient -- each checked against the oracle."""
+"""Small end-to-end check on the GPU: specialised + interpreted tile passes,
+fused rotation groups, expectation sweeps and sampling, each against the
+oracle (run with QSV_JIT_MIN_QUBITS=14 to force the specialised kernels)."""
 import os
 import sys
 
@@ -26,4 +26,4 @@ e = sv.expectation(psi, h)
 assert abs(e - O.expectation(ref, h, n)) < 1e-10 * max(1, abs(e))
 m = sv.sample(psi, PauliString.from_label("Z0 X3"), 2000, 5)
 assert m == O.sample(ref, PauliString.from_label("Z0 X3"), 2000, 5)
-print("sanitize workload ok", n)
+print("check_small ok", n)
