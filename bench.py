@@ -583,10 +583,16 @@ def main():
         run_reference(args, rank, world)
         return
     if world > 1:
+        import torch
         import torch.distributed as dist
+        # bind the rank's GPU before NCCL creates its communicator;
         # --dist-backend gloo: plumbing test of the sharded path on one GPU
         # (device shards staged through host memory); never a bench number
-        dist.init_process_group(args.dist_backend)
+        if args.dist_backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     if world > 1:
         run_engine_dist(args, rank, world, local)
     else:
