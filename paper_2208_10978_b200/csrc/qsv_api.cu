@@ -6,6 +6,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cfloat>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -140,12 +142,53 @@ int check_state(const qsv_state *s)
     return QSV_OK;
 }
 
+// QSV_HOST_PROFILE=1: per-phase host time of an API call on stderr.
+struct HostProfile {
+    const char *what;
+    bool on;
+    std::chrono::steady_clock::time_point t0, t;
+    std::string line;
+    explicit HostProfile(const char *w) : what(w)
+    {
+        const char *e = getenv("QSV_HOST_PROFILE");
+        on = e && e[0] == '1';
+        if (on) t0 = t = std::chrono::steady_clock::now();
+    }
+    void mark(const char *phase)
+    {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        char buf[96];
+        snprintf(buf, sizeof(buf), " %s %.1f us", phase,
+                 std::chrono::duration<double, std::micro>(now - t).count());
+        line += buf;
+        t = now;
+    }
+    ~HostProfile()
+    {
+        if (on)
+            fprintf(stderr, "qsv host %s:%s (total %.1f us)\n", what, line.c_str(),
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                        .count());
+    }
+};
+
+// Specialised sources of a cached program and their loaded modules (built on
+// the first specialised run, reused by every later one).
+struct JitCache {
+    int device = -1;
+    std::vector<std::string> src;
+    std::vector<const void *> mod;
+};
+
 // Cache of structural gate plans.
 struct CacheEntry {
     uint64_t hash;
     int n;
     std::vector<int32_t> kinds, qubits;
     ProgramTemplate tpl;
+    int uses = 0;  // runs of this structure (hot programs get specialised passes)
+    JitCache jc;
 };
 std::list<CacheEntry> g_cache;
 constexpr size_t kCacheMax = 8;
@@ -185,8 +228,10 @@ int op_param_count(const OpRec &op)
     }
 }
 
-int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params)
+int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params, int uses = 0,
+                 JitCache *jc = nullptr)
 {
+    HostProfile prof("run_template");
     DeviceCtx *c = nullptr;
     int rc = ctx_for(s->device, &c);
     if (rc) return rc;
@@ -197,8 +242,16 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     const size_t o_par = b.add(params.data(), params.size() * sizeof(double));
     struct PassOff { size_t off, comp, blk, ops, rots, par; int nblk, nops, nrots, npar; bool lite; };
     std::vector<PassOff> po(t.passes.size());
-    const bool jit = jit_enabled(s->n);
-    std::vector<std::string> jit_src(jit ? t.passes.size() : 0);
+    const bool jit = jit_enabled(s->n, uses);
+    JitCache local;
+    if (!jc) jc = &local;
+    const bool jit_cached = jit && jc->device == s->device && jc->src.size() == t.passes.size();
+    if (jit && !jit_cached) {
+        jc->device = -1;
+        jc->src.assign(t.passes.size(), std::string());
+        jc->mod.assign(t.passes.size(), nullptr);
+    }
+    std::vector<std::string> &jit_src = jc->src;
     {
         std::vector<uint64_t> offhi;
         std::vector<int32_t> comp;
@@ -252,7 +305,7 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
             o.nops = (int)lops.size();
             o.nrots = r_hi - r_lo;
             o.npar = p_hi - p_lo;
-            if (jit)
+            if (jit && !jit_cached)
                 jit_source(p.geom, lblk.data(), o.nblk, lops.data(), t.rots.data() + r_lo, o.npar,
                            jit_src[k]);
             o.blk = b.add(lblk.data(), lblk.size() * sizeof(BlockRec));
@@ -261,17 +314,22 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
             o.par = b.add(params.data() + p_lo, (size_t)o.npar * sizeof(double));
         }
     }
+    prof.mark("blob");
     char *d = nullptr;
     size_t scratch = 0;
     rc = upload_blob(*c, s->stream, b, 0, &d, &scratch);
     if (rc) return rc;
-    if (jit) {
+    prof.mark("upload");
+    if (jit && !jit_cached) {
         std::vector<const std::string *> srcs;
         for (const std::string &src : jit_src)
             if (!src.empty()) srcs.push_back(&src);
         std::string err;
         if (!srcs.empty() && jit_prepare(s->device, srcs, err) && getenv("QSV_JIT_VERBOSE"))
             fprintf(stderr, "qsv jit: %s\n", err.c_str());
+        for (size_t k = 0; k < jit_src.size(); ++k)
+            jc->mod[k] = jit_src[k].empty() ? nullptr : jit_module(s->device, jit_src[k]);
+        jc->device = s->device;
     }
     const OpRec *d_ops = (const OpRec *)(d + o_ops);
     const RotRec *d_rots = (const RotRec *)(d + o_rots);
@@ -288,12 +346,13 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                 QSV_CUDA(launch_rot_global(s->amps, s->n, p.flip, d_rots + op.r0, op.r1 - op.r0,
                                            s->stream));
             }
-        } else if (jit && !jit_src[k].empty() &&
-                   jit_launch(s->device, jit_src[k], s->amps, dims_of(p.geom),
-                              (const uint64_t *)(d + o.off), (const int32_t *)(d + o.comp),
-                              (const double *)(d + o.par), o.npar,
-                              (int)std::min<uint64_t>(1ull << p.geom.ncomp, (uint64_t)num_sms(s->device)),
-                              s->stream)) {
+        } else if (jit && jc->mod[k] &&
+                   jit_launch_module(jc->mod[k], s->amps, dims_of(p.geom),
+                                     (const uint64_t *)(d + o.off), (const int32_t *)(d + o.comp),
+                                     (const double *)(d + o.par), o.npar,
+                                     (int)std::min<uint64_t>(1ull << p.geom.ncomp,
+                                                             (uint64_t)num_sms(s->device)),
+                                     s->stream)) {
             ++g_jit_launches;
         } else if (p.geom.m >= kBlockBits + 1) {
             QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
@@ -307,6 +366,7 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                                       p.op_end - p.op_begin, d_rots, d_par, s->stream));
         }
     }
+    prof.mark("launch");
     return QSV_OK;
 }
 
@@ -503,9 +563,12 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
         return QSV_OK;
     }
     if (!kinds || !qubits || !values) return fail_code(QSV_ERR_INVALID, "null gate arrays");
-    if (int rc = validate_gates(s, n_gates, kinds, qubits)) return rc;
-    for (int64_t i = 0; i < 3 * n_gates; ++i)
-        if (!std::isfinite(values[i])) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
+    HostProfile prof("apply_gates");
+    {
+        bool finite = true;  // branch-free so the loop vectorises
+        for (int64_t i = 0; i < 3 * n_gates; ++i) finite &= std::fabs(values[i]) <= DBL_MAX;
+        if (!finite) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
+    }
     QSV_CUDA(cudaSetDevice(s->device));
     const uint64_t h = hash_structure(s->n, n_gates, kinds, qubits);
     ProgramTemplate *tpl = nullptr;
@@ -516,11 +579,14 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
             std::memcmp(it->qubits.data(), qubits, n_gates * 8) == 0) {
             g_cache.splice(g_cache.begin(), g_cache, it);
             tpl = &g_cache.front().tpl;
+            ++g_cache.front().uses;
             hit = true;
             break;
         }
     }
+    // a hit has the kinds / qubits of a structure validated when it was planned
     if (!tpl) {
+        if (int rc = validate_gates(s, n_gates, kinds, qubits)) return rc;
         CacheEntry e;
         e.hash = h;
         e.n = s->n;
@@ -531,10 +597,14 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
         if (g_cache.size() > kCacheMax) g_cache.pop_back();
         tpl = &g_cache.front().tpl;
     }
+    prof.mark("lookup");
     std::vector<double> params(tpl->n_params);
     materialize_params(*tpl, values, params.data());
+    prof.mark("materialize");
     fill_stats(*tpl, hit, stats);
-    return run_template(s, *tpl, params);
+    const int rc = run_template(s, *tpl, params, g_cache.front().uses + 1, &g_cache.front().jc);
+    prof.mark("run");
+    return rc;
 }
 
 static int validate_masks(int n, int64_t S, const uint64_t *x, const uint64_t *y,
@@ -670,7 +740,8 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
             o.comp = b.add(comp.data(), comp.size() * sizeof(int32_t));
         }
         o.rows = sp.global ? expect_global_grid(s->n)
-                           : expect_sweep_grid(dims_of(sp.geom), (int)sp.terms.size(), sp.ndiag);
+                           : expect_sweep_grid(dims_of(sp.geom), (int)sp.terms.size(), sp.ndiag,
+                                             (int)sp.groups.size());
         max_partial = std::max(max_partial, (size_t)std::max(o.rows, 16 * num_sms(s->device)) *
                                                 sp.terms.size());
         offs.push_back(o);

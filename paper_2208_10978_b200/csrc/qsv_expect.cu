@@ -23,6 +23,7 @@
 // Partial sums go to per-(CTA, string) slots reduced in a fixed order, so
 // results are deterministic.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <stdint.h>
 
 #include "qsv_internal.h"
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kT, 1)
 expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
                      const uint64_t *__restrict__ g_offhi, const int32_t *__restrict__ g_comp,
                      const GroupRec *__restrict__ groups, int ngroups,
-                     const TermRec *__restrict__ terms, int nterms, int ndiag,
+                     const TermRec *__restrict__ terms, int nterms, int ndiag, int gsplit,
                      double *__restrict__ partial)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -122,8 +123,13 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
     const int items_per_group = npairs / qsize;
     double *wscr = scr + warp * 16 * 32;
     __syncthreads();
+    // small states (fewer tiles than CTAs): gsplit CTAs share a tile, each
+    // taking every gsplit-th (group, quarter) item; the last one does the
+    // Z-only strings
     const uint64_t ntiles = 1ull << g.ncomp;
-    uint64_t tile = blockIdx.x;
+    const int split = blockIdx.x % gsplit;
+    const uint64_t tstride = gridDim.x / gsplit;
+    uint64_t tile = blockIdx.x / gsplit;
     if (tile >= ntiles) return;
     uint64_t base = tbase(tile, lane, g.ncomp, comp_lane);
     {
@@ -132,9 +138,9 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
         for (int l = threadIdx.x; l < tsize; l += kT) cp_async16(bufs + l, src + (l & cmask) + offhi[l >> c]);
         cp_async_commit();
     }
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    for (int it = 0; tile < ntiles; ++it, tile += tstride) {
         double2 *sm = bufs + (it & 1) * tsize;
-        const uint64_t next = tile + gridDim.x;
+        const uint64_t next = tile + tstride;
         if (next < ntiles) {  // prefetch the next tile into the other buffer
             const double2 *src = psi + tbase(next, lane, g.ncomp, comp_lane);
             double2 *dstb = bufs + ((it + 1) & 1) * tsize;
@@ -145,7 +151,7 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
         cp_async_wait<1>();
         __syncthreads();
         // ---- flip groups: items (group, quarter) round-robin over warps ----
-        for (int item = warp; item < ngroups * items_per_group; item += kW) {
+        for (int item = warp + kW * split; item < ngroups * items_per_group; item += kW * gsplit) {
             const int gi = item / items_per_group, slot = item % items_per_group;
             const uint32_t f = __ldg(&groups[gi].f_loc);
             const int h = __ldg(&groups[gi].h);
@@ -184,7 +190,7 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
             }
         }
         // ---- Z-only strings: WHT of |psi|^2 over the tile ----
-        if (ndiag > 0) {
+        if (ndiag > 0 && split == gsplit - 1) {
             double p[kPer];
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
@@ -242,7 +248,9 @@ size_t sweep2_smem(const TileDims &g, int nterms, int ndiag)
 
 }  // namespace
 
-int expect_sweep_grid(const TileDims &g, int nterms, int ndiag)
+// Grid of one sweep: tiles over CTAs (persistent, per_sm CTAs per SM); when
+// there are fewer tiles than CTA slots, *gsplit CTAs share each tile's items.
+int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, int *gsplit)
 {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -259,7 +267,15 @@ int expect_sweep_grid(const TileDims &g, int nterms, int ndiag)
     if (per_sm < 1) per_sm = 1;
     const uint64_t ntiles = 1ull << g.ncomp;
     const uint64_t cap = (uint64_t)num_sms(dev) * per_sm;
-    return (int)(ntiles < cap ? ntiles : cap);
+    int split = 1;
+    if (ntiles < cap) {
+        const int npairs = 1 << (g.m - 1);
+        const int items = ngroups * (npairs / (npairs < 512 ? npairs : 512));
+        const uint64_t want = (uint64_t)(items + kW - 1) / kW;  // one item per warp
+        split = (int)std::max<uint64_t>(1, std::min<uint64_t>(cap / ntiles, want));
+    }
+    if (gsplit) *gsplit = split;
+    return ntiles < cap ? (int)(ntiles * split) : (int)cap;
 }
 
 cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
@@ -267,10 +283,11 @@ cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uin
                                 const TermRec *d_terms, int nterms, int ndiag, double *d_partial,
                                 int *grid_out, cudaStream_t st)
 {
-    const int grid = expect_sweep_grid(g, nterms, ndiag);
+    int split = 1;
+    const int grid = expect_sweep_grid(g, nterms, ndiag, ngroups, &split);
     *grid_out = grid;
     expect_sweep2_kernel<<<grid, kT, sweep2_smem(g, nterms, ndiag), st>>>(
-        psi, g, d_offhi, d_comp, d_groups, ngroups, d_terms, nterms, ndiag, d_partial);
+        psi, g, d_offhi, d_comp, d_groups, ngroups, d_terms, nterms, ndiag, split, d_partial);
     return cudaGetLastError();
 }
 

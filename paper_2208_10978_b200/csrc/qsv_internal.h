@@ -155,9 +155,9 @@ cudaError_t launch_expect_global(const double2 *psi, int n, const GroupRec *d_gr
                                  const uint64_t *d_gflip, int ngroups, const TermRec *d_terms,
                                  int nterms, double *d_partial, int *grid_out, cudaStream_t st);
 int expect_global_grid(int n);
-int expect_sweep_grid(const TileDims &g, int nterms, int ndiag);
+int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, int *gsplit = nullptr);
 // run-time specialised tile passes (qsv_jit.cpp)
-bool jit_enabled(int n_qubits);
+bool jit_enabled(int n_qubits, int uses = 0);
 const char *jit_unavailable_reason();
 bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const OpRec *ops,
                 const RotRec *rots, int nparams, std::string &src);
@@ -165,6 +165,12 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
 bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims &g,
                 const uint64_t *d_offhi, const int32_t *d_geo, const double *d_params, int nparams,
                 int grid, cudaStream_t st);
+// Loaded module of a prepared source (nullptr if unavailable); stable for the
+// process lifetime, so a cached program launches without re-hashing sources.
+const void *jit_module(int device, const std::string &src);
+bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const uint64_t *d_offhi,
+                       const int32_t *d_geo, const double *d_params, int nparams, int grid,
+                       cudaStream_t st);
 size_t sample_scratch_bytes(uint64_t dim);
 cudaError_t launch_sample_parity(const double2 *psi, uint64_t dim, int64_t shots, uint64_t k0,
                                  uint64_t k1, uint64_t support, void *scratch, size_t scratch_bytes,

@@ -673,13 +673,20 @@ bool compile(const std::string &src, Module &m)
     return ok;
 }
 
-bool jit_wanted(int n)
+// Specialise every pass from QSV_JIT_MIN_QUBITS (default 22) qubits up; below
+// that only hot programs: a cached circuit structure run QSV_JIT_HOT_USES
+// (default 3; 0 = never) times -- e.g. the fixed ansatz of a VQE loop, whose
+// one-off NVRTC compile is then amortised over every later evaluation.
+bool jit_wanted(int n, int uses)
 {
     const char *e = getenv("QSV_JIT");
     if (e && e[0] == '0') return false;
     const char *mq = getenv("QSV_JIT_MIN_QUBITS");
     const int min_q = mq ? atoi(mq) : 22;
-    return n >= min_q;
+    if (n >= min_q) return true;
+    const char *hu = getenv("QSV_JIT_HOT_USES");
+    const int hot = hu ? atoi(hu) : 3;
+    return hot > 0 && uses >= hot && n >= kMaxTileBits;
 }
 
 }  // namespace
@@ -810,7 +817,7 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
     return true;
 }
 
-bool jit_enabled(int n) { return jit_wanted(n) && load_api(); }
+bool jit_enabled(int n, int uses) { return jit_wanted(n, uses) && load_api(); }
 
 const char *jit_unavailable_reason() { return g_api.why.c_str(); }
 
@@ -879,10 +886,24 @@ bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims
                 const uint64_t *d_offhi, const int32_t *d_geo, const double *d_params, int nparams,
                 int grid, cudaStream_t st)
 {
+    return jit_launch_module(jit_module(device, src), psi, g, d_offhi, d_geo, d_params, nparams,
+                             grid, st);
+}
+
+const void *jit_module(int device, const std::string &src)
+{
     auto &mods = g_mods[device];
     auto it = mods.find(src);
-    if (it == mods.end() || it->second.failed || !it->second.fn) return false;
-    Module &m = it->second;
+    if (it == mods.end() || it->second.failed || !it->second.fn) return nullptr;
+    return &it->second;
+}
+
+bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const uint64_t *d_offhi,
+                       const int32_t *d_geo, const double *d_params, int nparams, int grid,
+                       cudaStream_t st)
+{
+    if (!mod) return false;
+    const Module &m = *static_cast<const Module *>(mod);
     if (nparams > 0)
         if (g_api.MemcpyDtoDAsync(m.cparams, (CUdeviceptr)d_params, (size_t)nparams * 8, st) != 0)
             return false;

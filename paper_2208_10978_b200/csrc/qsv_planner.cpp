@@ -94,7 +94,25 @@ struct Item {
     uint64_t a_union = 0, b_union = 0;
     int cluster = -1;         // dense-fused gate cluster (index into ProgramTemplate::cfills)
     int cost = 2;             // FP64 work (complex FMAs per amplitude) -- bounds a pass
+    int par = 8;              // parameter doubles (specialised passes hold them in 64 KiB __constant__)
 };
+
+// Parameter doubles of a gate (op_param_count of the op it becomes) and of a
+// same-flip rotation group (one OP_GMAT table: 16 << (|f| - 1) doubles).
+int gate_par(int kind);
+int rot_par(uint64_t flip)
+{
+    const int w = popc64(flip);
+    return (w >= 1 && w <= 4) ? (16 << (w - 1)) : 0;
+}
+
+// Parameter budget of one pass: a specialised pass keeps its matrices in
+// 64 KiB of constant memory (jit_source rejects > 8192 doubles).
+int pass_param_cap()
+{
+    const char *e = getenv("QSV_PASS_PARAM_CAP");
+    return e ? std::max(1, atoi(e)) : 8192;
+}
 
 bool conflict(const Item &A, const Item &B, const std::vector<Rot> &R)
 {
@@ -115,6 +133,7 @@ struct Schedule {
     std::vector<uint64_t> pass_hi;
     std::vector<bool> pass_global;
     std::vector<int> pass_cost;
+    std::vector<int> pass_par;
 };
 
 Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int n, int m, int c)
@@ -129,6 +148,7 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
     // keeps specialised kernels from growing without bound.
     const char *env_cap = getenv("QSV_PASS_COST_CAP");
     const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 128;
+    const int par_cap = pass_param_cap();
     for (size_t i = 0; i < items.size(); ++i) {
         const Item &it = items[i];
         const uint64_t need = it.req & ~low;
@@ -147,7 +167,8 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
             for (int p = earliest; p <= last; ++p) {
                 if (S.pass_global[p]) continue;
                 if (popc64(S.pass_hi[p] | need) <= free_slots &&
-                    (S.pass_cost[p] + it.cost <= cost_cap || it.cost == 0)) {
+                    (S.pass_cost[p] + it.cost <= cost_cap || it.cost == 0) &&
+                    S.pass_par[p] + it.par <= par_cap) {
                     placed = p;
                     break;
                 }
@@ -160,11 +181,13 @@ Schedule schedule(const std::vector<Item> &items, const std::vector<Rot> &R, int
             S.pass_hi.push_back(0);
             S.pass_global.push_back(!fits);
             S.pass_cost.push_back(0);
+            S.pass_par.push_back(0);
             placed = (int)S.pass_items.size() - 1;
         }
         S.pass_items[placed].push_back((int)i);
         S.pass_hi[placed] |= need;
         S.pass_cost[placed] += it.cost;
+        S.pass_par[placed] += it.par;
         item_pass[i] = placed;
     }
     return S;
@@ -197,15 +220,18 @@ Schedule schedule_lookahead(const std::vector<Item> &items, const std::vector<Ro
     // Fill one pass greedily from `seed`; with `undo` the changes are rolled
     // back and only the pass's (work, items) score is returned.
     std::vector<int> taken;
+    const int par_cap = pass_param_cap();
     auto fill = [&](int seed, bool undo, uint64_t &hi, int &cost) {
         taken.clear();
         hi = 0;
         cost = 0;
+        int par = 0;
         auto take = [&](int i) {
             done[i] = 1;
             taken.push_back(i);
             hi |= items[i].req & ~low;
             cost += items[i].cost;
+            par += items[i].par;
             for (int k : succ[i]) --npend[k];
         };
         take(seed);
@@ -218,6 +244,7 @@ Schedule schedule_lookahead(const std::vector<Item> &items, const std::vector<Ro
                     const uint64_t need = items[i].req & ~low;
                     if (popc64(hi | need) > free_slots) continue;
                     if (items[i].cost != 0 && cost + items[i].cost > cost_cap) continue;
+                    if (par + items[i].par > par_cap) continue;
                     const int growth = popc64(need & ~hi);
                     if (growth < best_growth) {
                         best_growth = growth;
@@ -360,6 +387,7 @@ void build_items_from_rots(const std::vector<Rot> &R, std::vector<Item> &items)
         Item it;
         it.rot = true;
         it.cost = 0;
+        it.par = rot_par(a);
         it.rots.push_back((int)r);
         it.a_union = a;
         it.b_union = b;
@@ -388,6 +416,16 @@ int gate_cost(int kind)
         case K_RZ: return 1;
         case K_CU3: return 4;
         default: return 2;
+    }
+}
+
+int gate_par(int kind)
+{
+    switch (kind) {
+        case K_X: case K_CNOT: case K_SWAP: return 0;
+        case K_RZ: return 4;
+        case K_CU3: return 32;
+        default: return 8;
     }
 }
 
@@ -426,6 +464,7 @@ void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t
         it.supp = s;
         it.req = s;
         it.cost = gate_cost(kinds[gi]);
+        it.par = gate_par(kinds[gi]);
         return it;
     };
     auto close = [&](int ci) {
@@ -448,6 +487,7 @@ void fuse_clusters(std::vector<Item> &items, const int32_t *kinds, const int32_t
             it.supp = C.qs;
             it.req = C.qs;
             it.cost = fused_cost;
+            it.par = nq == 2 ? 32 : 8;
             t.cfills.push_back(std::move(cf));
             out.push_back(std::move(it));
         } else {
@@ -1261,6 +1301,9 @@ void match_rotations(int64_t N, const int32_t *kinds, const int32_t *qubits, std
     }
 }
 
+// Cache key of a gate structure.  Only a screen: a cache hit is confirmed by
+// comparing the full kind / qubit arrays, so the key samples at most 1024
+// gates (evenly spaced) and stays O(1) for long UCC circuits.
 uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits)
 {
     uint64_t h = 1469598103934665603ull ^ (uint64_t)n_qubits;
@@ -1269,7 +1312,8 @@ uint64_t hash_structure(int n_qubits, int64_t n_gates, const int32_t *kinds, con
         h *= 1099511628211ull;
     };
     mix((uint64_t)n_gates);
-    for (int64_t i = 0; i < n_gates; ++i) {
+    const int64_t step = n_gates > 1024 ? n_gates / 1024 : 1;
+    for (int64_t i = 0; i < n_gates; i += step) {
         mix(((uint64_t)(uint32_t)kinds[i] << 40) ^ ((uint64_t)(uint32_t)qubits[2 * i] << 20) ^
             (uint64_t)(uint32_t)qubits[2 * i + 1]);
     }
@@ -1314,7 +1358,8 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
             } else {
                 Item it;
                 it.rot = true;
-            it.cost = 0;  // rotation groups run in the interpreted kernel: no pass budget
+                it.cost = 0;  // a same-flip group is one GMAT: bounded by the parameter budget
+                it.par = rot_par(a);
                 it.rots.push_back(r);
                 it.a_union = a;
                 it.b_union = b;
@@ -1331,6 +1376,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
             it.supp = s;
             it.req = s;
             it.cost = gate_cost(kinds[i]);
+            it.par = gate_par(kinds[i]);
             items.push_back(std::move(it));
             ++i;
         }
@@ -1409,56 +1455,71 @@ void materialize_rotations(ProgramTemplate &t, const double *theta)
 
 void materialize_gmats(const ProgramTemplate &t, double *params)
 {
+    static const std::vector<uint8_t> par8 = [] {
+        std::vector<uint8_t> v(256);
+        for (int i = 0; i < 256; ++i) v[i] = (uint8_t)(__builtin_popcount((unsigned)i) & 1);
+        return v;
+    }();
+    std::vector<double> kre, kim;
+    std::vector<uint8_t> yodd;
     for (const GmatFill &g : t.gfills) {
         const int ncfg = 1 << (g.w - 1);
+        const int nr = g.r1 - g.r0;
+        // kappa = i^q sin per rotation; R = [[c, kappa sg1], [kappa sg0, c]]
+        kre.assign(nr, 0.0);
+        kim.assign(nr, 0.0);
+        yodd.resize(nr);
+        for (int r = 0; r < nr; ++r) {
+            const RotRec &R = t.rots[g.r0 + r];
+            yodd[r] = (uint8_t)((R.q >> 2) & 1);
+            switch (R.q & 3) {
+                case 0: kre[r] = R.s; break;
+                case 1: kim[r] = R.s; break;
+                case 2: kre[r] = -R.s; break;
+                default: kim[r] = -R.s; break;
+            }
+        }
         int fpos[8], k = 0;
         for (int j = 0; j < 8; ++j)
             if ((g.F >> j) & 1) fpos[k++] = j;
-        for (int cp = 0; cp < 2; ++cp) {
-            for (int cfg = 0; cfg < ncfg; ++cfg) {
-                // r1's bits on F: bit H set, the others from cfg (ascending, H skipped)
-                uint32_t r1 = 1u << g.H;
-                for (int i = 0, c = 0; i < g.w; ++i) {
-                    if (fpos[i] == g.H) continue;
-                    if ((cfg >> c) & 1) r1 |= 1u << fpos[i];
-                    ++c;
-                }
-                double M[8] = {1, 0, 0, 0, 0, 0, 1, 0};  // identity, row-major complex
-                for (int r = g.r0; r < g.r1; ++r) {
-                    const RotRec &R = t.rots[r];
-                    const int yodd = (R.q >> 2) & 1;
-                    const int q = R.q & 3;
-                    const int s1 = (cp + __builtin_popcount(r1 & g.yF[r - g.r0])) & 1;
-                    const int s0 = s1 ^ yodd;
-                    // kappa = i^q sin; R = [[c, kappa sg1], [kappa sg0, c]]
-                    double kre = 0, kim = 0;
-                    switch (q) {
-                        case 0: kre = R.s; break;
-                        case 1: kim = R.s; break;
-                        case 2: kre = -R.s; break;
-                        default: kim = -R.s; break;
-                    }
-                    const double b_re = s1 ? -kre : kre, b_im = s1 ? -kim : kim;
-                    const double c_re = s0 ? -kre : kre, c_im = s0 ? -kim : kim;
-                    const double Rm[8] = {R.c, 0, b_re, b_im, c_re, c_im, R.c, 0};
-                    double N[8];
-                    for (int i = 0; i < 2; ++i)
-                        for (int j = 0; j < 2; ++j) {
-                            double re = 0, im = 0;
-                            for (int l = 0; l < 2; ++l) {
-                                const double ar = Rm[2 * (2 * i + l)], ai = Rm[2 * (2 * i + l) + 1];
-                                const double br = M[2 * (2 * l + j)], bi = M[2 * (2 * l + j) + 1];
-                                re += ar * br - ai * bi;
-                                im += ar * bi + ai * br;
-                            }
-                            N[2 * (2 * i + j)] = re;
-                            N[2 * (2 * i + j) + 1] = im;
-                        }
-                    for (int i = 0; i < 8; ++i) M[i] = N[i];
-                }
-                double *dst = params + g.offset + 8 * (cp * ncfg + cfg);
-                for (int i = 0; i < 8; ++i) dst[i] = M[i];
+        for (int cfg = 0; cfg < ncfg; ++cfg) {
+            // r1's bits on F: bit H set, the others from cfg (ascending, H skipped)
+            uint32_t r1 = 1u << g.H;
+            for (int i = 0, c = 0; i < g.w; ++i) {
+                if (fpos[i] == g.H) continue;
+                if ((cfg >> c) & 1) r1 |= 1u << fpos[i];
+                ++c;
             }
+            double M[8] = {1, 0, 0, 0, 0, 0, 1, 0};  // identity, row-major complex
+            for (int r = 0; r < nr; ++r) {
+                const double cr = t.rots[g.r0 + r].c;
+                const int s1 = par8[(r1 & g.yF[r]) & 255u];
+                const int s0 = s1 ^ yodd[r];
+                const double b_re = s1 ? -kre[r] : kre[r], b_im = s1 ? -kim[r] : kim[r];
+                const double c_re = s0 ? -kre[r] : kre[r], c_im = s0 ? -kim[r] : kim[r];
+                // M <- R M with R = [[c, b], [cc, c]]: rows mix, two columns
+                for (int j = 0; j < 2; ++j) {
+                    const double a0r = M[2 * j], a0i = M[2 * j + 1];
+                    const double a1r = M[4 + 2 * j], a1i = M[4 + 2 * j + 1];
+                    M[2 * j] = cr * a0r + (b_re * a1r - b_im * a1i);
+                    M[2 * j + 1] = cr * a0i + (b_re * a1i + b_im * a1r);
+                    M[4 + 2 * j] = cr * a1r + (c_re * a0r - c_im * a0i);
+                    M[4 + 2 * j + 1] = cr * a1i + (c_re * a0i + c_im * a0r);
+                }
+            }
+            // common parity cp = 1 negates every off-diagonal factor:
+            // R' = Z R Z, so the product is Z M Z (exactly: only signs change)
+            double *d0 = params + g.offset + 8 * cfg;
+            double *d1 = params + g.offset + 8 * (ncfg + cfg);
+            for (int i = 0; i < 8; ++i) d0[i] = M[i];
+            d1[0] = M[0];
+            d1[1] = M[1];
+            d1[2] = -M[2];
+            d1[3] = -M[3];
+            d1[4] = -M[4];
+            d1[5] = -M[5];
+            d1[6] = M[6];
+            d1[7] = M[7];
         }
     }
 }

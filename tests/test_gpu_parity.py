@@ -91,7 +91,7 @@ def test_config1_full(config1_golden):
     cfg = W.config1(seed=0)
     psi = sv.evolve(sv.init_state(cfg["reference"]), cfg["circuit"])
     st = sv.last_plan_stats()
-    assert st["n_rotations"] == 1872 and st["n_passes"] == 1
+    assert st["n_rotations"] == 1872 and st["n_passes"] == 4  # parameter budget per pass
     assert np.abs(psi.amplitudes - config1_golden["amplitudes"]).max() <= AMP_TOL
     assert rel(sv.expectation(psi, cfg["hamiltonian"]), float(config1_golden["energy"])) <= REL_TOL
 
