@@ -607,6 +607,11 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
     return rc;
 }
 
+static bool sweep_is_wide(const SweepPlan &sp)
+{
+    return !sp.groups.empty() && (sp.groups.front().pad[0] & 1);
+}
+
 static int validate_masks(int n, int64_t S, const uint64_t *x, const uint64_t *y,
                           const uint64_t *z)
 {
@@ -741,7 +746,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
         }
         o.rows = sp.global ? expect_global_grid(s->n)
                            : expect_sweep_grid(dims_of(sp.geom), (int)sp.terms.size(), sp.ndiag,
-                                             (int)sp.groups.size());
+                                             (int)sp.groups.size(), sweep_is_wide(sp));
         max_partial = std::max(max_partial, (size_t)std::max(o.rows, 16 * num_sms(s->device)) *
                                                 sp.terms.size());
         offs.push_back(o);
@@ -777,7 +782,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
             QSV_CUDA(launch_expect_sweep(s->amps, dims_of(sp.geom), (const uint64_t *)(d + o.off),
                                          (const int32_t *)(d + o.comp), (const GroupRec *)(d + o.g),
                                          (int)sp.groups.size(), (const TermRec *)(d + o.t), nterms,
-                                         sp.ndiag, d_partial, &rows, s->stream));
+                                         sp.ndiag, sweep_is_wide(sp), d_partial, &rows, s->stream));
         }
         QSV_CUDA(launch_reduce_columns(d_partial, rows, nterms, (const int32_t *)(d + o.m),
                                        d_per_term, s->stream));

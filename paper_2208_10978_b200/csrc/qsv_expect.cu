@@ -97,12 +97,58 @@ __device__ __forceinline__ void eval_terms(const double *scr, int lane, uint32_t
     }
 }
 
+// Position of pair index p (11 bits) inside a 2048-double half of the
+// transform scratch: low 4 bits XOR-swizzled by bits 4-7, so every access
+// pattern of tile_wht is conflict-free (two wavefronts per warp).
+__device__ __forceinline__ int wpos(uint32_t p) { return (int)(p ^ ((p >> 4) & 15u)); }
+
+// Walsh-Hadamard transform of 4096 values held as v[k] = value at index
+// threadIdx.x + 256 k.  Index bits 8.. (8 + kbits) run in registers first:
+// kbits = 3 keeps bit 11 apart (two independent 2048-point transforms, e.g.
+// Re w | Im w), kbits = 4 transforms all 12 bits.  Bits 0-3 and 4-7 then run
+// in registers after two transposes through S (4096 doubles, swizzled
+// halves).  On return S holds the transform: index i at
+// S[(i >> 11) * 2048 + wpos(i & 2047)].
+__device__ __forceinline__ void tile_wht(double (&v)[16], int kbits, double *S)
+{
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int b = 1; b < 16; b <<= 1) {
+        if (b >= (1 << kbits)) break;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            if (r & b) continue;
+            const double u = v[r], w = v[r | b];
+            v[r] = u + w;
+            v[r | b] = u - w;
+        }
+    }
+    __syncthreads();  // S free (previous lookups done)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) S[(k >> 3) * 2048 + wpos((uint32_t)(t + 256 * (k & 7)))] = v[k];
+    __syncthreads();
+    double *H = S + (t >> 7) * 2048;
+    const uint32_t tp = t & 127;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = H[wpos((tp << 4) | r)];
+    wht16(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) H[wpos((tp << 4) | r)] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = H[wpos((tp & 15u) | (r << 4) | ((tp >> 4) << 8))];
+    wht16(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) H[wpos((tp & 15u) | (r << 4) | ((tp >> 4) << 8))] = v[r];
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kT, 1)
 expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
                      const uint64_t *__restrict__ g_offhi, const int32_t *__restrict__ g_comp,
                      const GroupRec *__restrict__ groups, int ngroups,
                      const TermRec *__restrict__ terms, int nterms, int ndiag, int gsplit,
-                     double *__restrict__ partial)
+                     int wide, double *__restrict__ partial)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = g.m, c = g.c;
@@ -110,12 +156,13 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
     const int npairs = tsize >> 1;
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);    // 2 x tsize (double-buffered)
     double *scr = reinterpret_cast<double *>(bufs + 2 * tsize);  // [kW][16][32]
-    double *acc = scr + kW * 16 * 32;                           // flip: [nflip][kSlots], then diag
+    double *acc = scr + kW * 16 * 32;  // flip: [nflip][kSlots] (wide sweeps: [nflip]), then diag
     const int nflip = nterms - ndiag;
-    double *accd = acc + nflip * kSlots;
+    const int slots = wide ? 1 : kSlots;
+    double *accd = acc + nflip * slots;
     uint64_t *offhi = reinterpret_cast<uint64_t *>(accd + ndiag);
     for (int i = threadIdx.x; i < (1 << (m - c)); i += kT) offhi[i] = __ldg(g_offhi + i);
-    for (int i = threadIdx.x; i < nflip * kSlots + ndiag; i += kT) acc[i] = 0.0;
+    for (int i = threadIdx.x; i < nflip * slots + ndiag; i += kT) acc[i] = 0.0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int comp_lane = __ldg(g_comp + lane);
     const uint32_t cmask = (1u << c) - 1u;
@@ -151,7 +198,8 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
         cp_async_wait<1>();
         __syncthreads();
         // ---- flip groups: items (group, quarter) round-robin over warps ----
-        for (int item = warp + kW * split; item < ngroups * items_per_group; item += kW * gsplit) {
+        for (int item = warp + kW * split; !wide && item < ngroups * items_per_group;
+             item += kW * gsplit) {
             const int gi = item / items_per_group, slot = item % items_per_group;
             const uint32_t f = __ldg(&groups[gi].f_loc);
             const int h = __ldg(&groups[gi].h);
@@ -189,8 +237,44 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
                 __syncwarp();
             }
         }
+        // ---- wide groups (12-bit tiles): transform of the pair products ----
+        for (int gi = split; wide && gi < ngroups; gi += gsplit) {
+            const uint32_t f = __ldg(&groups[gi].f_loc);
+            const int h = __ldg(&groups[gi].h);
+            const int t0 = __ldg(&groups[gi].t0), tim = __ldg(&groups[gi].t_im),
+                      t1 = __ldg(&groups[gi].t1);
+            double v[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t l0 = ins0(threadIdx.x + 256 * k, h), l1 = l0 ^ f;
+                const double2 x = sm[l0], y = sm[l1];
+                v[k] = fma(x.x, y.x, x.y * y.y);
+                v[8 + k] = fma(x.x, y.y, -x.y * y.x);
+            }
+            tile_wht(v, 3, scr);
+            for (int t = t0 + threadIdx.x; t < t1; t += kT) {
+                const uint32_t sp = __ldg(&terms[t].s_loc);
+                const double val = scr[(t >= tim ? 2048 : 0) + wpos(sp)];
+                const uint32_t sg = __popcll(base & __ldg(&terms[t].s_hi)) & 1u;
+                acc[t - ndiag] += __ldg(&terms[t].scale) * (sg ? -val : val);
+            }
+        }
         // ---- Z-only strings: WHT of |psi|^2 over the tile ----
-        if (ndiag > 0 && split == gsplit - 1) {
+        if (ndiag > 0 && split == gsplit - 1 && m == kMaxTileBits) {
+            double v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const double2 a = sm[threadIdx.x + 256 * k];
+                v[k] = fma(a.x, a.x, a.y * a.y);
+            }
+            tile_wht(v, 4, scr);
+            for (int t = threadIdx.x; t < ndiag; t += kT) {
+                const uint32_t sp = __ldg(&terms[t].s_loc);
+                const double val = scr[(sp >> 11) * 2048 + wpos(sp & 2047u)];
+                const uint32_t tp = __popcll(base & __ldg(&terms[t].s_hi)) & 1u;
+                accd[t] += tp ? -val : val;
+            }
+        } else if (ndiag > 0 && split == gsplit - 1) {
             double p[kPer];
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
@@ -234,23 +318,23 @@ expect_sweep2_kernel(const double2 *__restrict__ psi, const TileDims g,
             v = accd[t];
         } else {
             v = 0.0;
-            for (int s = 0; s < kSlots; ++s) v += acc[(t - ndiag) * kSlots + s];
+            for (int s = 0; s < slots; ++s) v += acc[(t - ndiag) * slots + s];
         }
         partial[(size_t)blockIdx.x * nterms + t] = v;
     }
 }
 
-size_t sweep2_smem(const TileDims &g, int nterms, int ndiag)
+size_t sweep2_smem(const TileDims &g, int nterms, int ndiag, bool wide)
 {
     return ((size_t)32 << g.m) + (size_t)8 * kW * 16 * 32 +
-           (size_t)8 * ((nterms - ndiag) * kSlots + ndiag) + ((size_t)8 << (g.m - g.c));
+           (size_t)8 * ((nterms - ndiag) * (wide ? 1 : kSlots) + ndiag) + ((size_t)8 << (g.m - g.c));
 }
 
 }  // namespace
 
 // Grid of one sweep: tiles over CTAs (persistent, per_sm CTAs per SM); when
 // there are fewer tiles than CTA slots, *gsplit CTAs share each tile's items.
-int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, int *gsplit)
+int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, bool wide, int *gsplit)
 {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -262,7 +346,7 @@ int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, int
     }
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expect_sweep2_kernel, kT,
-                                                      sweep2_smem(g, nterms, ndiag)) != cudaSuccess)
+                                                      sweep2_smem(g, nterms, ndiag, wide)) != cudaSuccess)
         per_sm = 1;
     if (per_sm < 1) per_sm = 1;
     const uint64_t ntiles = 1ull << g.ncomp;
@@ -271,7 +355,8 @@ int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, int
     if (ntiles < cap) {
         const int npairs = 1 << (g.m - 1);
         const int items = ngroups * (npairs / (npairs < 512 ? npairs : 512));
-        const uint64_t want = (uint64_t)(items + kW - 1) / kW;  // one item per warp
+        // one item per warp; wide sweeps: one group per CTA
+        const uint64_t want = wide ? (uint64_t)ngroups : (uint64_t)(items + kW - 1) / kW;
         split = (int)std::max<uint64_t>(1, std::min<uint64_t>(cap / ntiles, want));
     }
     if (gsplit) *gsplit = split;
@@ -280,14 +365,15 @@ int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, int
 
 cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                                 const int32_t *d_comp, const GroupRec *d_groups, int ngroups,
-                                const TermRec *d_terms, int nterms, int ndiag, double *d_partial,
-                                int *grid_out, cudaStream_t st)
+                                const TermRec *d_terms, int nterms, int ndiag, bool wide,
+                                double *d_partial, int *grid_out, cudaStream_t st)
 {
     int split = 1;
-    const int grid = expect_sweep_grid(g, nterms, ndiag, ngroups, &split);
+    const int grid = expect_sweep_grid(g, nterms, ndiag, ngroups, wide, &split);
     *grid_out = grid;
-    expect_sweep2_kernel<<<grid, kT, sweep2_smem(g, nterms, ndiag), st>>>(
-        psi, g, d_offhi, d_comp, d_groups, ngroups, d_terms, nterms, ndiag, split, d_partial);
+    expect_sweep2_kernel<<<grid, kT, sweep2_smem(g, nterms, ndiag, wide), st>>>(
+        psi, g, d_offhi, d_comp, d_groups, ngroups, d_terms, nterms, ndiag, split, wide ? 1 : 0,
+        d_partial);
     return cudaGetLastError();
 }
 

@@ -94,7 +94,7 @@ struct GroupRec {   // a flip group of an expectation sweep (32 B)
     uint32_t f_loc;
     int32_t h;
     int32_t t0, t_im, t1;  // terms [t0, t_im) use Re w, [t_im, t1) use Im w
-    int32_t pad[3];
+    int32_t pad[3];        // pad[0] bit 0: wide group (tile-wide transform path)
 };
 
 struct TermRec {    // 24 B
@@ -139,8 +139,8 @@ cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *
                                const double *d_params, int nparams, bool lite, cudaStream_t st);
 cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                                 const int32_t *d_comp, const GroupRec *d_groups, int ngroups,
-                                const TermRec *d_terms, int nterms, int ndiag, double *d_partial,
-                                int *grid_out, cudaStream_t st);
+                                const TermRec *d_terms, int nterms, int ndiag, bool wide,
+                                double *d_partial, int *grid_out, cudaStream_t st);
 cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
                                   double *out, cudaStream_t st);
 cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStream_t st);
@@ -155,7 +155,8 @@ cudaError_t launch_expect_global(const double2 *psi, int n, const GroupRec *d_gr
                                  const uint64_t *d_gflip, int ngroups, const TermRec *d_terms,
                                  int nterms, double *d_partial, int *grid_out, cudaStream_t st);
 int expect_global_grid(int n);
-int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, int *gsplit = nullptr);
+int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, bool wide,
+                      int *gsplit = nullptr);
 // run-time specialised tile passes (qsv_jit.cpp)
 bool jit_enabled(int n_qubits, int uses = 0);
 const char *jit_unavailable_reason();

@@ -779,6 +779,7 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
 bool jit_sweep_source(const SweepPlan &sp, std::string &src)
 {
     if (sp.global || sp.geom.m != kMaxTileBits || sp.ndiag != 0 || sp.groups.empty()) return false;
+    if (sp.groups.front().pad[0] & 1) return false;  // wide groups: interpreted transform path
     const int nterms = (int)sp.terms.size();
     if (nterms > 48) return false;
     std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";

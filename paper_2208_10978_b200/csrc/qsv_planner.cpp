@@ -1580,22 +1580,32 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     struct Bin {
         uint64_t hi = 0;
         int nterms = 0;
+        bool wide = false;
         std::vector<int> groups;
         std::vector<int32_t> diag;
     };
+    // Wide groups (more strings than a specialised sweep holds) take the
+    // tile-wide Walsh-Hadamard path of the interpreted sweep: one transform of
+    // the group's pair products per tile, then one lookup per string -- so
+    // they share sweeps (with the Z-only strings) instead of one sweep each.
+    const int kWideMin = jit_layout ? jit_cap : 24, kWideCap = 2048;
+    const bool wide_ok = m == kMaxTileBits;
     std::vector<Bin> bins;
     std::vector<int> global_groups;
     for (int gi : order) {
         const uint64_t need = flips[gi] & ~low;
         const int nt = (int)members[gi].size();
-        if (popc64(need) > free_slots || nt > 512) {
+        const bool wide = wide_ok && nt > kWideMin;
+        if (popc64(need) > free_slots || nt > (wide ? kWideCap : 512)) {
             global_groups.push_back(gi);
             continue;
         }
+        const int cap = wide ? kWideCap : kFlipCap;
         int placed = -1;
-        // a group above the (specialised-sweep) cap gets an interpreted sweep of its own
-        for (size_t b = 0; b < bins.size() && nt <= kFlipCap; ++b) {
-            if (bins[b].nterms + nt > kFlipCap || (int)bins[b].groups.size() >= kGroupCap) continue;
+        // a narrow group above the (specialised-sweep) cap gets a sweep of its own
+        for (size_t b = 0; b < bins.size() && nt <= cap; ++b) {
+            if (bins[b].wide != wide) continue;
+            if (bins[b].nterms + nt > cap || (int)bins[b].groups.size() >= kGroupCap) continue;
             if (popc64(bins[b].hi | need) <= free_slots) {
                 placed = (int)b;
                 break;
@@ -1603,18 +1613,29 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
         }
         if (placed < 0) {
             bins.emplace_back();
+            bins.back().wide = wide;
             placed = (int)bins.size() - 1;
         }
         bins[placed].hi |= need;
         bins[placed].nterms += nt;
         bins[placed].groups.push_back(gi);
     }
-    // Z-only strings ride along with the first sweeps (any tile works), or
-    // get sweeps of their own for the specialised flip-only kernel
-    const size_t first_diag_bin = jit_layout ? bins.size() : 0;
-    for (size_t d0 = 0, b = first_diag_bin; d0 < diag.size(); d0 += kDiagCap, ++b) {
-        if (b >= bins.size()) bins.emplace_back();
-        bins[b].diag.assign(diag.begin() + d0, diag.begin() + std::min(diag.size(), d0 + kDiagCap));
+    // Z-only strings ride along with the wide sweeps, else the first sweeps
+    // (any tile works), or -- for the specialised flip-only kernel -- sweeps
+    // of their own
+    std::vector<size_t> diag_bins;
+    for (size_t b = 0; b < bins.size(); ++b)
+        if (bins[b].wide) diag_bins.push_back(b);
+    if (!jit_layout)
+        for (size_t b = 0; b < bins.size(); ++b)
+            if (!bins[b].wide) diag_bins.push_back(b);
+    for (size_t d0 = 0, k = 0; d0 < diag.size(); d0 += kDiagCap, ++k) {
+        if (k >= diag_bins.size()) {
+            bins.emplace_back();
+            diag_bins.push_back(bins.size() - 1);
+        }
+        bins[diag_bins[k]].diag.assign(diag.begin() + d0,
+                                       diag.begin() + std::min(diag.size(), d0 + kDiagCap));
     }
 
     auto term_scale = [&](int64_t t) {
@@ -1651,6 +1672,7 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
             GroupRec gr{};
             gr.f_loc = compress(flips[gi], sp.geom);
             gr.h = highest_bit(gr.f_loc);
+            gr.pad[0] = bin.wide ? 1 : 0;  // tile-wide transform path
             const uint32_t lowmask_h = (1u << gr.h) - 1u;
             gr.t0 = (int)sp.terms.size();
             for (int pass = 0; pass < 2; ++pass) {  // Re-w strings, then Im-w strings

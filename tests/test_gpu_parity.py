@@ -392,3 +392,25 @@ def test_sample_golden_and_outcomes():
                                             outs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
     assert np.array_equal(outs, out_ref)
     assert mean.value == mean_ref
+
+
+@pytest.mark.parametrize("jit", [False, True])
+def test_config3_shaped_wide_groups_vs_oracle(jit, monkeypatch):
+    """Config-3 construction at 16 qubits: 900 Z-only strings and 16 flip
+    groups of 25-78 strings (X/Y on one qubit times Z patterns) -- the
+    tile-wide Walsh-Hadamard path -- next to narrow groups (specialised
+    sweeps when jit)."""
+    if jit:
+        monkeypatch.setenv("QSV_JIT_MIN_QUBITS", "14")
+    n = 16
+    h = W.config3_hamiltonian(seed=1, n_qubits=n, n_terms=3000)
+    rng = np.random.default_rng(5)
+    st = random_state(n, rng)
+    s = sv.from_amplitudes(st)
+    ref, per_ref = O.expectation(st, h, n, per_term=True)
+    re, im, per = sv.expectation_terms(s, h)
+    assert rel(re, ref) <= REL_TOL
+    assert np.abs(per - per_ref[:, 0]).max() <= 1e-12
+    # the same strings with coefficients changed: plan cache hit, same sweeps
+    h2 = PauliSum(tuple(PauliTerm(2.0 * t.coefficient, t.string) for t in h.terms))
+    assert rel(sv.expectation(s, h2), 2.0 * ref) <= REL_TOL
