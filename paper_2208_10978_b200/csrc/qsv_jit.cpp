@@ -439,7 +439,9 @@ __device__ __forceinline__ u32 load_x(const double2 *sm, u32 pl, double2 (&X)[8]
     for (int j = 0; j < 8; ++j) X[j] = sm[b0 ^ swz(ins0(256u * j, H))];
     return b0;
 }
-template <bool RE, bool IM, int H>
+// WRE / WIM: transform that component (else its strings sum the 8 products
+// directly with their sign pattern: cheaper for <= 3 strings per component)
+template <bool RE, bool IM, bool WRE, bool WIM, int H>
 __device__ __forceinline__ void wht8x(const double2 *sm, u32 b0, const double2 (&X)[8], u32 sF,
                                       double (&Wr)[8], double (&Wi)[8])
 {
@@ -454,8 +456,8 @@ __device__ __forceinline__ void wht8x(const double2 *sm, u32 b0, const double2 (
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             if (r & b) continue;
-            if (RE) { const double u = Wr[r], v = Wr[r | b]; Wr[r] = u + v; Wr[r | b] = u - v; }
-            if (IM) { const double u = Wi[r], v = Wi[r | b]; Wi[r] = u + v; Wi[r | b] = u - v; }
+            if (RE && WRE) { const double u = Wr[r], v = Wr[r | b]; Wr[r] = u + v; Wr[r | b] = u - v; }
+            if (IM && WIM) { const double u = Wi[r], v = Wi[r | b]; Wi[r] = u + v; Wi[r | b] = u - v; }
         }
     }
 }
@@ -794,17 +796,38 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
             fn += buf;
             prev_h = G.h;
         }
+        // a component with <= kDirect strings skips its 8-point transform
+        // (24 adds) and sums each string's 8 products directly (7 adds)
+        const int kDirect = 3;
+        const bool w_re = G.t_im - G.t0 > kDirect, w_im = G.t1 - G.t_im > kDirect;
         snprintf(buf, sizeof(buf),
-                 "  { double Wr[8], Wi[8];\n    wht8x<%s, %s, %d>(sm, b0, X, %uu, Wr, Wi);\n",
-                 need_re ? "true" : "false", need_im ? "true" : "false", G.h, h_swz(G.f_loc));
+                 "  { double Wr[8], Wi[8];\n    wht8x<%s, %s, %s, %s, %d>(sm, b0, X, %uu, Wr, Wi);\n",
+                 need_re ? "true" : "false", need_im ? "true" : "false", w_re ? "true" : "false",
+                 w_im ? "true" : "false", G.h, h_swz(G.f_loc));
         fn += buf;
         for (int t = G.t0; t < G.t1; ++t) {
             const TermRec &tr = sp.terms[t];
+            const char *W = tr.use_im ? "Wi" : "Wr";
+            const unsigned msk = (tr.s_loc >> 8) & 7u;
+            std::string val;
+            if (tr.use_im ? w_im : w_re) {
+                snprintf(buf, sizeof(buf), "%s[%u]", W, msk);
+                val = buf;
+            } else {  // W[m] of the transform = sum_j (-1)^{|j & m|} w_j
+                val = "(";
+                for (unsigned j = 0; j < 8; ++j) {
+                    snprintf(buf, sizeof(buf), "%s%s[%u]", j == 0 ? "" : (__builtin_popcount(j & msk) & 1) ? " - " : " + ", W, j);
+                    val += buf;
+                }
+                val += ")";
+            }
             // scale folded in: the term's sweep total is scale * sum_p sign(p) w_p
             snprintf(buf, sizeof(buf),
-                     "    acc[%d] = fma(((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g, %s[%u], acc[%d]);\n",
-                     t, tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale,
-                     tr.use_im ? "Wi" : "Wr", (tr.s_loc >> 8) & 7u, t);
+                     "    acc[%d] = fma(((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g, ",
+                     t, tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
+            fn += buf;
+            fn += val;
+            snprintf(buf, sizeof(buf), ", acc[%d]);\n", t);
             fn += buf;
         }
         fn += "  }\n";

@@ -375,14 +375,28 @@ __device__ __forceinline__ double warp_sum(double v)
     return v;
 }
 
-__global__ void reduce_columns_kernel(const double *__restrict__ partial, int rows, int cols,
-                                      const int32_t *__restrict__ map, double *__restrict__ out)
+// Column sums of partial[rows][cols] (per-CTA partial sums of a sweep).
+// Block = 32 columns (lanes, coalesced) x 32 row slices (warps); each warp
+// sums rows r = warp (mod 32), then lane-column partials are added in slice
+// order: a fixed summation order, so results are deterministic.
+__global__ void __launch_bounds__(1024) reduce_columns_kernel(const double *__restrict__ partial,
+                                                              int rows, int cols,
+                                                              const int32_t *__restrict__ map,
+                                                              double *__restrict__ out)
 {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= cols) return;
+    __shared__ double part[32][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
     double s = 0.0;
-    for (int r = 0; r < rows; ++r) s += partial[(size_t)r * cols + t];
-    out[map ? map[t] : t] = s;
+    if (t < cols)
+        for (int r = warp; r < rows; r += 32) s += partial[(size_t)r * cols + t];
+    part[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && t < cols) {
+        double v = 0.0;
+        for (int w = 0; w < 32; ++w) v += part[w][lane];
+        out[map ? map[t] : t] = v;
+    }
 }
 
 // ---- K4 / K5 / K6 -------------------------------------------------------
@@ -629,7 +643,7 @@ cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, con
                                   double *out, cudaStream_t st)
 {
     if (cols <= 0) return cudaSuccess;
-    reduce_columns_kernel<<<(cols + 127) / 128, 128, 0, st>>>(partial, rows, cols, d_map, out);
+    reduce_columns_kernel<<<(cols + 31) / 32, 1024, 0, st>>>(partial, rows, cols, d_map, out);
     return cudaGetLastError();
 }
 
