@@ -75,6 +75,13 @@ int qsv_set_basis(qsv_state *s, uint64_t index);
 /* Host <-> device in dump_state layout (statevector.py:214-216). */
 int qsv_upload(qsv_state *s, const double *host);
 int qsv_download(const qsv_state *s, double *host);
+/* Asynchronous qsv_download: the copy runs on a separate copy stream once the
+ * state's queued work is done, overlapping work queued afterwards on other
+ * states (pinned host buffers give a truly asynchronous copy).  The state may
+ * keep being used: the next call that modifies or frees it first waits for
+ * the copy.  qsv_download_wait blocks until the host buffer is complete. */
+int qsv_download_async(qsv_state *s, double *host);
+int qsv_download_wait(qsv_state *s);
 
 /* kernels.apply_1q (kernels/__init__.py:21; _cykernels.pyx:19-38): m = 2x2 row-major complex128. */
 int qsv_apply_1q(qsv_state *s, const double *m, int qubit);

@@ -48,7 +48,8 @@ class PlanStats(ctypes.Structure):
 EXPORTED = (
     "qsv_abi_version", "qsv_last_error", "qsv_device_count", "qsv_create", "qsv_destroy",
     "qsv_n_qubits", "qsv_set_stream", "qsv_get_stream", "qsv_device_ptr", "qsv_synchronize",
-    "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_apply_1q", "qsv_apply_2q",
+    "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_download_async",
+    "qsv_download_wait", "qsv_apply_1q", "qsv_apply_2q",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
     "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_sample_parity",
@@ -79,6 +80,8 @@ def _declare(L):
         "qsv_set_basis": ([vp, u64], ctypes.c_int),
         "qsv_upload": ([vp, vp], ctypes.c_int),
         "qsv_download": ([vp, vp], ctypes.c_int),
+        "qsv_download_async": ([vp, vp], ctypes.c_int),
+        "qsv_download_wait": ([vp], ctypes.c_int),
         "qsv_apply_1q": ([vp, dp, ctypes.c_int], ctypes.c_int),
         "qsv_apply_2q": ([vp, dp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "qsv_apply_pauli": ([vp, vp, u64, u64, u64], ctypes.c_int),

@@ -39,6 +39,7 @@ struct DeviceCtx {
     size_t h_bytes = 0;
     cudaEvent_t stage_ev = nullptr;
     bool stage_pending = false;
+    cudaStream_t copy_stream = nullptr;  // asynchronous downloads (lazily created)
 };
 DeviceCtx g_dev[64];
 
@@ -139,6 +140,21 @@ int upload_blob(DeviceCtx &c, cudaStream_t st, const Blob &b, size_t extra, char
 int check_state(const qsv_state *s)
 {
     if (!s || !s->amps) return fail_code(QSV_ERR_INVALID, "null or destroyed state handle");
+    return QSV_OK;
+}
+
+// Order work that modifies (or frees) s after its in-flight asynchronous
+// download: a device-side wait on the state's stream, or (host) a blocking
+// wait for the copy itself.
+int settle(qsv_state *s, bool host = false)
+{
+    if (!s || !s->dl_pending) return QSV_OK;
+    if (host) {
+        QSV_CUDA(cudaEventSynchronize(s->dl_done));
+    } else {
+        QSV_CUDA(cudaStreamWaitEvent(s->stream, s->dl_done, 0));
+    }
+    s->dl_pending = false;
     return QSV_OK;
 }
 
@@ -444,10 +460,12 @@ int qsv_destroy(qsv_state *s)
     if (!s) return QSV_OK;
     if (s->amps) {
         cudaSetDevice(s->device);
+        settle(s, true);
         cudaStreamSynchronize(s->stream);
         cudaFree(s->amps);
         s->amps = nullptr;
     }
+    if (s->dl_done) cudaEventDestroy(s->dl_done);
     delete s;
     return QSV_OK;
 }
@@ -464,6 +482,7 @@ int qsv_set_stream(qsv_state *s, void *stream)
     if (int rc = check_state(s)) return rc;
     DeviceCtx *c = nullptr;
     if (int rc = ctx_for(s->device, &c)) return rc;
+    if (int rc = settle(s, true)) return rc;
     s->stream = stream ? (cudaStream_t)stream : c->stream;
     return QSV_OK;
 }
@@ -478,6 +497,8 @@ int qsv_get_stream(const qsv_state *s, void **stream)
 int qsv_device_ptr(const qsv_state *s, void **ptr)
 {
     if (int rc = check_state(s)) return rc;
+    // the caller may write through the pointer: no copy may still be reading
+    if (int rc = settle(const_cast<qsv_state *>(s), true)) return rc;
     *ptr = (void *)s->amps;
     return QSV_OK;
 }
@@ -487,6 +508,7 @@ int qsv_synchronize(qsv_state *s)
     if (int rc = check_state(s)) return rc;
     QSV_CUDA(cudaSetDevice(s->device));
     QSV_CUDA(cudaStreamSynchronize(s->stream));
+    if (int rc = settle(s, true)) return rc;
     return QSV_OK;
 }
 
@@ -497,6 +519,7 @@ int qsv_copy(qsv_state *dst, const qsv_state *src)
     if (dst->n != src->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
     QSV_CUDA(cudaSetDevice(dst->device));
     if (dst == src) return QSV_OK;
+    if (int rc = settle(dst)) return rc;
     QSV_CUDA(cudaMemcpyAsync(dst->amps, src->amps, 16 * dst->dim, cudaMemcpyDeviceToDevice,
                              dst->stream));
     return QSV_OK;
@@ -507,6 +530,7 @@ int qsv_set_basis(qsv_state *s, uint64_t index)
     if (int rc = check_state(s)) return rc;
     if (index >= s->dim) return fail_code(QSV_ERR_INVALID, "basis index out of range");
     QSV_CUDA(cudaSetDevice(s->device));
+    if (int rc = settle(s)) return rc;
     QSV_CUDA(launch_set_basis(s->amps, s->dim, index, s->stream));
     return QSV_OK;
 }
@@ -516,6 +540,7 @@ int qsv_upload(qsv_state *s, const double *host)
     if (int rc = check_state(s)) return rc;
     if (!host) return fail_code(QSV_ERR_INVALID, "null host buffer");
     QSV_CUDA(cudaSetDevice(s->device));
+    if (int rc = settle(s)) return rc;
     QSV_CUDA(cudaMemcpyAsync(s->amps, host, 16 * s->dim, cudaMemcpyHostToDevice, s->stream));
     QSV_CUDA(cudaStreamSynchronize(s->stream));
     return QSV_OK;
@@ -529,6 +554,31 @@ int qsv_download(const qsv_state *s, double *host)
     QSV_CUDA(cudaMemcpyAsync(host, s->amps, 16 * s->dim, cudaMemcpyDeviceToHost, s->stream));
     QSV_CUDA(cudaStreamSynchronize(s->stream));
     return QSV_OK;
+}
+
+int qsv_download_async(qsv_state *s, double *host)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (!host) return fail_code(QSV_ERR_INVALID, "null host buffer");
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(s->device, &c)) return rc;
+    if (!c->copy_stream) QSV_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    if (!s->dl_done) QSV_CUDA(cudaEventCreateWithFlags(&s->dl_done, cudaEventDisableTiming));
+    // copy stream: after the state's queued work, then the copy, then dl_done
+    QSV_CUDA(cudaEventRecord(s->dl_done, s->stream));
+    QSV_CUDA(cudaStreamWaitEvent(c->copy_stream, s->dl_done, 0));
+    QSV_CUDA(cudaMemcpyAsync(host, s->amps, 16 * s->dim, cudaMemcpyDeviceToHost, c->copy_stream));
+    QSV_CUDA(cudaEventRecord(s->dl_done, c->copy_stream));
+    s->dl_pending = true;
+    return QSV_OK;
+}
+
+int qsv_download_wait(qsv_state *s)
+{
+    if (int rc = check_state(s)) return rc;
+    QSV_CUDA(cudaSetDevice(s->device));
+    return settle(s, true);
 }
 
 static int validate_gates(const qsv_state *s, int64_t n, const int32_t *kinds,
@@ -563,6 +613,7 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
         return QSV_OK;
     }
     if (!kinds || !qubits || !values) return fail_code(QSV_ERR_INVALID, "null gate arrays");
+    if (int rc = settle(s)) return rc;
     HostProfile prof("apply_gates");
     {
         bool finite = true;  // branch-free so the loop vectorises
@@ -634,6 +685,7 @@ int qsv_apply_pauli_rotations(qsv_state *s, int64_t n, const uint64_t *x, const 
     if (n < 0) return fail_code(QSV_ERR_INVALID, "negative rotation count");
     if (n == 0) return QSV_OK;
     if (!x || !y || !z || !theta) return fail_code(QSV_ERR_INVALID, "null rotation arrays");
+    if (int rc = settle(s)) return rc;
     if (int rc = validate_masks(s->n, n, x, y, z)) return rc;
     for (int64_t r = 0; r < n; ++r)
         if (!std::isfinite(theta[r])) return fail_code(QSV_ERR_INVALID, "non-finite rotation angle");
@@ -821,6 +873,7 @@ int qsv_apply_pauli(const qsv_state *src, qsv_state *dst, uint64_t x, uint64_t y
     if (src == dst) return fail_code(QSV_ERR_INVALID, "apply_pauli needs distinct src and dst");
     if (int rc = validate_masks(src->n, 1, &x, &y, &z)) return rc;
     QSV_CUDA(cudaSetDevice(src->device));
+    if (int rc = settle(dst, dst->stream != src->stream)) return rc;
     QSV_CUDA(launch_apply_pauli(src->amps, dst->amps, src->dim, x, y, z, 1.0, 0.0, 0, src->stream));
     return QSV_OK;
 }
@@ -837,6 +890,7 @@ int qsv_apply_operator(const qsv_state *src, qsv_state *dst, int64_t S, const ui
         return fail_code(QSV_ERR_INVALID, "bad term arrays");
     if (int rc = validate_masks(src->n, S, x, y, z)) return rc;
     QSV_CUDA(cudaSetDevice(src->device));
+    if (int rc = settle(dst, dst->stream != src->stream)) return rc;
     if (S == 0) {
         QSV_CUDA(cudaMemsetAsync(dst->amps, 0, 16 * dst->dim, src->stream));
         return QSV_OK;
@@ -893,6 +947,7 @@ int qsv_axpby(qsv_state *y, const qsv_state *x, double are, double aim, double b
     if (int rc = check_state(x)) return rc;
     if (x->n != y->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
     QSV_CUDA(cudaSetDevice(y->device));
+    if (int rc = settle(y)) return rc;
     QSV_CUDA(launch_axpby(y->amps, x->amps, y->dim, are, aim, bre, bim, y->stream));
     return QSV_OK;
 }
@@ -904,6 +959,7 @@ int qsv_apply_1q(qsv_state *s, const double *m, int qubit)
     if (qubit < 0 || qubit >= s->n) return fail_code(QSV_ERR_INVALID, "qubit out of range");
     std::lock_guard<std::recursive_mutex> lk(g_mu);
     QSV_CUDA(cudaSetDevice(s->device));
+    if (int rc = settle(s)) return rc;
     ProgramTemplate t;
     int32_t kind = K_U3, q[2] = {qubit, -1};
     plan_gates(s->n, 1, &kind, q, t);
@@ -924,6 +980,7 @@ int qsv_apply_2q(qsv_state *s, const double *m, int q0, int q1)
         return fail_code(QSV_ERR_INVALID, "bad qubit pair");
     std::lock_guard<std::recursive_mutex> lk(g_mu);
     QSV_CUDA(cudaSetDevice(s->device));
+    if (int rc = settle(s)) return rc;
     ProgramTemplate t;
     int32_t kind = K_CU3, q[2] = {q0, q1};
     plan_gates(s->n, 1, &kind, q, t);

@@ -121,6 +121,9 @@ struct qsv_state {
     size_t h_stage_bytes = 0;
     cudaEvent_t stage_done = nullptr;
     bool stage_pending = false;
+    // asynchronous download (qsv_download_async) in flight on the copy stream
+    cudaEvent_t dl_done = nullptr;
+    bool dl_pending = false;
 };
 
 namespace qsv {

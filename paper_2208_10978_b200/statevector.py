@@ -54,6 +54,7 @@ def _release(n: int, device: int, h: int) -> None:
     L = _lib._lib
     if L is None:
         return
+    L.qsv_download_wait(ctypes.c_void_p(h))  # no copy may outlive its host buffer
     bucket = _POOL.setdefault((n, device), [])
     if len(bucket) < _POOL_MAX and n < 30:
         bucket.append(h)
@@ -84,7 +85,7 @@ class _Handle:
 class StateVector:
     """Dense 2^n complex128 state in device memory (statevector.py:26-39)."""
 
-    __slots__ = ("n_qubits", "device", "_h", "_basis")
+    __slots__ = ("n_qubits", "device", "_h", "_basis", "_dl_buf")
 
     def __init__(self, n_qubits: int, amplitudes=None, device: int = 0):
         self.n_qubits = int(n_qubits)
@@ -146,6 +147,21 @@ class StateVector:
         if out.dtype != np.complex128 or out.size != (1 << self.n_qubits) or not out.flags.c_contiguous:
             raise ValueError("output must be a contiguous complex128 array of length 2^n")
         _lib.check(_lib.lib().qsv_download(self.handle, out.ctypes.data_as(ctypes.c_void_p)))
+
+    def download_async(self, out: np.ndarray) -> None:
+        """Start copying the amplitudes into `out` (pinned memory for a truly
+        asynchronous copy) on the device's copy stream; work queued afterwards
+        on other states overlaps it.  `wait_download()` completes it; the next
+        call that modifies this state waits for it on the device."""
+        if out.dtype != np.complex128 or out.size != (1 << self.n_qubits) or not out.flags.c_contiguous:
+            raise ValueError("output must be a contiguous complex128 array of length 2^n")
+        _lib.check(_lib.lib().qsv_download_async(self.handle, out.ctypes.data_as(ctypes.c_void_p)))
+        self._dl_buf = out  # keep the host buffer alive while the copy is in flight
+
+    def wait_download(self) -> None:
+        if self._h is not None:
+            _lib.check(_lib.lib().qsv_download_wait(self.handle))
+        self._dl_buf = None
 
     def norm(self) -> float:
         if self.basis_index is not None:

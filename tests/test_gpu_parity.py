@@ -414,3 +414,31 @@ def test_config3_shaped_wide_groups_vs_oracle(jit, monkeypatch):
     # the same strings with coefficients changed: plan cache hit, same sweeps
     h2 = PauliSum(tuple(PauliTerm(2.0 * t.coefficient, t.string) for t in h.terms))
     assert rel(sv.expectation(s, h2), 2.0 * ref) <= REL_TOL
+
+
+def test_download_async_snapshot_and_reuse():
+    """download_async copies the state as of the call: work queued on the same
+    state afterwards waits for the copy; other states run alongside."""
+    n = 20
+    rng = np.random.default_rng(21)
+    circ = W.brickwork(n, 4, seed=3)
+    st = random_state(n, rng)
+    a = sv.from_amplitudes(st)
+    ref_a = O.evolve(st, circ.gates)
+    a2 = sv.evolve(a, circ)
+    buf = np.empty(1 << n, dtype=np.complex128)
+    a2.download_async(buf)
+    sv.apply_circuit_inplace(a2, circ)      # modifies a2 right after: must wait for the copy
+    b = sv.evolve(sv.init_state("0" * n), circ)  # independent work alongside
+    a2.wait_download()
+    assert np.abs(buf - ref_a).max() <= AMP_TOL
+    assert np.abs(a2.amplitudes - O.evolve(ref_a, circ.gates)).max() <= AMP_TOL
+    assert np.abs(b.amplitudes - O.evolve(O.init_state("0" * n), circ.gates)).max() <= AMP_TOL
+    # dropping a state with a copy in flight: the pool waits before reuse
+    bufs = [np.empty(1 << n, dtype=np.complex128) for _ in range(3)]
+    for k in range(3):
+        s = sv.evolve(sv.from_amplitudes(st), circ)
+        s.download_async(bufs[k])
+        del s
+    for k in range(3):
+        assert np.abs(bufs[k] - ref_a).max() <= AMP_TOL
