@@ -103,15 +103,113 @@ class Circuit:
         return len(self.gates)
 
 
-def bind(c, theta: Sequence[float]) -> Circuit:
+class _BindPlan:
+    """Flattened parametric structure of a circuit: kinds / qubits as in
+    flatten_bound, constant parameter values, and the (slot, index, scale,
+    offset) of every Affine parameter -- so bind is O(#params) numpy work."""
+
+    __slots__ = ("kinds", "qubits", "const", "slot", "index", "scale", "offset", "__weakref__")
+
+    def __init__(self, c):
+        gates = c.gates
+        G = len(gates)
+        codes = _lib.KIND_CODES
+        self.kinds = np.empty(G, dtype=np.int32)
+        self.qubits = np.full(2 * G, -1, dtype=np.int32)
+        self.const = np.zeros(3 * G, dtype=np.float64)
+        slot, index, scale, offset = [], [], [], []
+        for i, g in enumerate(gates):
+            self.kinds[i] = codes[g.kind]
+            qs = g.qubits
+            self.qubits[2 * i] = qs[0]
+            if len(qs) == 2:
+                self.qubits[2 * i + 1] = qs[1]
+            for k, p in enumerate(g.params):
+                if not hasattr(p, "value"):  # Affine (ours or the reference's: duck-typed)
+                    slot.append(3 * i + k)
+                    index.append(p.index)
+                    scale.append(p.scale)
+                    offset.append(p.offset)
+                else:
+                    self.const[3 * i + k] = p.value
+        self.slot = np.asarray(slot, dtype=np.int64)
+        self.index = np.asarray(index, dtype=np.int64)
+        self.scale = np.asarray(scale, dtype=np.float64)
+        self.offset = np.asarray(offset, dtype=np.float64)
+
+
+_BIND_PLANS: dict = {}  # id(parametric circuit) -> (circuit, plan); small LRU
+
+
+def _bind_plan(c) -> _BindPlan:
+    hit = _BIND_PLANS.get(id(c))
+    if hit is not None and hit[0] is c:
+        return hit[1]
+    plan = _BindPlan(c)
+    if len(_BIND_PLANS) >= 8:
+        _BIND_PLANS.pop(next(iter(_BIND_PLANS)))
+    _BIND_PLANS[id(c)] = (c, plan)
+    return plan
+
+
+class BoundCircuit:
+    """Result of ``bind``: a bound circuit whose flattened arrays are computed
+    up front (vectorised Affine evaluation, bit-identical to evaluating each
+    parameter: scale * theta[index] + offset in float64) and whose Gate
+    objects are only built if someone reads ``gates``.  Duck-types Circuit
+    (n_qubits, gates, n_params = 0, is_bound, len)."""
+
+    __slots__ = ("n_qubits", "n_params", "_kinds", "_qubits", "_values", "_src", "_gates",
+                 "__weakref__")
+
+    def __init__(self, src, kinds, qubits, values):
+        self.n_qubits = src.n_qubits
+        self.n_params = 0
+        self._src = src
+        self._kinds, self._qubits, self._values = kinds, qubits, values
+        self._gates = None
+
+    @property
+    def gates(self) -> tuple:
+        if self._gates is None:
+            v = self._values
+            self._gates = tuple(
+                Gate(g.kind, g.qubits, tuple(Constant(float(v[3 * i + k])) for k in range(len(g.params))))
+                for i, g in enumerate(self._src.gates))
+        return self._gates
+
+    def flat(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        return self._kinds, self._qubits, self._values
+
+    def is_bound(self) -> bool:
+        return True
+
+    def __len__(self) -> int:
+        return len(self._kinds)
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, BoundCircuit):
+            other = Circuit(other.n_qubits, other.gates, 0)
+        return Circuit(self.n_qubits, self.gates, 0) == other
+
+    __hash__ = None
+
+
+def bind(c, theta: Sequence[float]) -> BoundCircuit:
+    """Evaluate every parameter at theta (circuit.py:145-156).  The parametric
+    structure is flattened once per circuit object; each call is then a
+    vectorised gather + multiply-add over the Affine slots (~us instead of
+    ~ms per 10k gates) and the engine consumes the arrays directly."""
     theta = np.asarray(theta, dtype=float)
     if theta.shape != (c.n_params,):
         raise ValueError(f"expected {c.n_params} parameter values, got {theta.shape}")
     if not np.all(np.isfinite(theta)):
         raise ValueError("parameter values must be finite")
-    gates = tuple(Gate(g.kind, g.qubits, tuple(Constant(float(p.evaluate(theta))) for p in g.params))
-                  for g in c.gates)
-    return Circuit(c.n_qubits, gates, 0)
+    plan = _bind_plan(c)
+    values = plan.const.copy()
+    if len(plan.slot):
+        values[plan.slot] = plan.scale * theta[plan.index] + plan.offset
+    return BoundCircuit(c, plan.kinds, plan.qubits, values)
 
 
 def gate_matrix(kind: str, values: Sequence[float] = ()) -> np.ndarray:
@@ -234,6 +332,8 @@ def rotation_circuit(n_qubits: int, rotations: Iterable[tuple[object, float]]) -
 
 def flatten_bound(c) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     """Bound circuit -> (kinds int32[G], qubits int32[2G], values float64[3G])."""
+    if isinstance(c, BoundCircuit):
+        return c.flat()
     gates = c.gates
     G = len(gates)
     codes = _lib.KIND_CODES

@@ -245,6 +245,9 @@ def _id_cache_put(cache: dict, obj, value, limit: int) -> None:
 
 
 def _flat(c):
+    flat = getattr(c, "flat", None)
+    if flat is not None and callable(flat):  # BoundCircuit: arrays computed by bind
+        return flat()
     hit = _id_cache_get(_FLAT_CACHE, c)
     if hit is not None:
         return hit
@@ -267,7 +270,7 @@ def evolve(s: StateVector, c) -> StateVector:
         raise ValueError("circuit and state qubit counts differ")
     # a circuit already in the flatten cache is known to be bound (walking
     # 37k gates for is_bound() costs ~6 ms per energy evaluation at config 1)
-    if _id_cache_get(_FLAT_CACHE, c) is None and not c.is_bound():
+    if not hasattr(c, "flat") and _id_cache_get(_FLAT_CACHE, c) is None and not c.is_bound():
         raise RuntimeError("circuit must be bound before evolution")
     out = StateVector._empty(s.n_qubits, s.device)
     if s.basis_index is not None:

@@ -18,7 +18,7 @@ import math
 
 import numpy as np
 
-from .circuit import Circuit, Constant, Gate, evolution_gates
+from .circuit import Affine, Circuit, Constant, Gate, evolution_gates
 from .pauli import PauliString, PauliSum, PauliTerm, multiply
 
 # ---------------------------------------------------------------------------
@@ -80,6 +80,15 @@ def rotations_circuit(n_qubits: int, strings, thetas) -> Circuit:
     for s, th in zip(strings, thetas):
         gates.extend(evolution_gates(s, Constant(-0.5 * float(th))))
     return Circuit(n_qubits, tuple(gates), 0)
+
+
+def parametric_rotations_circuit(n_qubits: int, strings) -> Circuit:
+    """The same blocks with theta_k as parameter k (Affine(k, -1/2)): what a
+    VQE loop binds every iteration (bind(c, thetas) == rotations_circuit)."""
+    gates: list[Gate] = []
+    for k, s in enumerate(strings):
+        gates.extend(evolution_gates(s, Affine(k, -0.5)))
+    return Circuit(n_qubits, tuple(gates), len(strings))
 
 
 def hf_bitstring(n_electrons: int, n_qubits: int) -> str:

@@ -99,3 +99,30 @@ def test_plan_partition_lpt():
     loads = [sum(plan.costs[i] for i in p) for p in plan.partitions]
     assert max(loads) <= sum(plan.costs) / 2 + max(plan.costs)
     assert plan.partitions == engine.plan_partition(h, 2).partitions  # deterministic
+
+
+def test_vectorised_bind_matches_per_gate_evaluation():
+    """bind's numpy gather + multiply-add gives the same bits as evaluating
+    each Affine (circuit.py:145-156), and the lazily built gates match."""
+    from paper_2208_10978_b200 import workloads as W
+    from paper_2208_10978_b200.circuit import BoundCircuit, evolution_gates, flatten_bound
+
+    cfg = W.config1(seed=3, n_qubits=8, n_electrons=4, n_terms=10)
+    strings = W.ucc_rotation_strings(8, 4)
+    gates = []
+    for k, s in enumerate(strings):
+        gates.extend(evolution_gates(s, Affine(k, -0.5, 0.125 * (k % 3))))
+    gates.append(Gate("U3", (1,), (Affine(0, 2.0, 0.5), Constant(0.3), Affine(1, -1.5))))
+    c = Circuit(8, tuple(gates), len(strings))
+    theta = np.random.default_rng(0).uniform(-1, 1, len(strings))
+    b = bind(c, theta)
+    assert isinstance(b, BoundCircuit) and b.is_bound() and len(b) == len(gates)
+    k, q, v = flatten_bound(b)
+    for i, g in enumerate(c.gates):
+        for j, p in enumerate(g.params):
+            assert v[3 * i + j] == p.evaluate(theta)  # bit-identical
+        assert b.gates[i].bound_values() == tuple(p.evaluate(theta) for p in g.params)
+    assert b == Circuit(8, b.gates, 0)
+    k2, q2, v2 = flatten_bound(Circuit(8, b.gates, 0))
+    assert np.array_equal(k, k2) and np.array_equal(q, q2) and np.array_equal(v, v2)
+    assert cfg["circuit"].n_qubits == 8
