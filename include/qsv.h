@@ -136,6 +136,15 @@ int qsv_axpby(qsv_state *y, const qsv_state *x, double alpha_re, double alpha_im
 int qsv_sample_parity(const qsv_state *s, uint64_t support_mask, int64_t shots,
                       const uint64_t *philox_key, double *out_mean, int64_t *outcomes);
 
+/* Reverse-mode gradient of a Pauli-rotation product (statevector.py:153-211
+ * restricted to circuits made of pauli_evolution blocks, circuit.py:254-281):
+ * on entry phi = U|psi0>, lam = H U|psi0> with U = prod_r exp(-i theta_r/2 P_r)
+ * (r = 0..R-1 in application order); on return grad[r] = dE/dtheta_r of
+ * E = <psi0|U^dag H U|psi0>, phi = |psi0> and lam = U^dag H U|psi0> (both
+ * un-rotated in place on the device; the host reads grad once). */
+int qsv_rotation_adjoint(qsv_state *phi, qsv_state *lam, int64_t R, const uint64_t *x,
+                         const uint64_t *y, const uint64_t *z, const double *theta, double *grad);
+
 /* Planner only (no device work; usable without a GPU): the plan that
  * qsv_apply_gates / qsv_expectation would execute for these inputs. */
 int qsv_plan_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,

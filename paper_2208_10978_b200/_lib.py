@@ -53,7 +53,7 @@ EXPORTED = (
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
     "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_sample_parity",
-    "qsv_jit_info",
+    "qsv_jit_info", "qsv_rotation_adjoint",
     "qsv_last_plan_stats",
 )
 
@@ -101,6 +101,7 @@ def _declare(L):
         "qsv_match_rotations": ([ctypes.c_int, i64, i32p, i32p, i64, ctypes.POINTER(i64), u64p,
                                  ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_jit_info": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_rotation_adjoint": ([vp, vp, i64, u64p, u64p, u64p, dp, dp], ctypes.c_int),
         "qsv_last_plan_stats": ([sp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():

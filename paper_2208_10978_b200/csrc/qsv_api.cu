@@ -941,6 +941,46 @@ int qsv_norm(const qsv_state *s, double *out)
     return QSV_OK;
 }
 
+int qsv_rotation_adjoint(qsv_state *phi, qsv_state *lam, int64_t R, const uint64_t *x,
+                         const uint64_t *y, const uint64_t *z, const double *theta, double *grad)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(phi)) return rc;
+    if (int rc = check_state(lam)) return rc;
+    if (phi == lam) return fail_code(QSV_ERR_INVALID, "rotation_adjoint needs distinct states");
+    if (phi->n != lam->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
+    if (R < 0) return fail_code(QSV_ERR_INVALID, "negative rotation count");
+    if (R == 0) return QSV_OK;
+    if (!x || !y || !z || !theta || !grad) return fail_code(QSV_ERR_INVALID, "null arrays");
+    if (int rc = validate_masks(phi->n, R, x, y, z)) return rc;
+    for (int64_t r = 0; r < R; ++r)
+        if (!std::isfinite(theta[r])) return fail_code(QSV_ERR_INVALID, "non-finite rotation angle");
+    QSV_CUDA(cudaSetDevice(phi->device));
+    if (int rc = settle(phi)) return rc;
+    if (int rc = settle(lam, lam->stream != phi->stream)) return rc;
+    if (lam->stream != phi->stream) QSV_CUDA(cudaStreamSynchronize(lam->stream));
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(phi->device, &c)) return rc;
+    Blob b;
+    const size_t ox = b.add(x, R * 8), oy = b.add(y, R * 8), oz = b.add(z, R * 8),
+                 ot = b.add(theta, R * 8);
+    const size_t scratch_doubles = adjoint_scratch_doubles(phi->n, R, phi->device);
+    char *d = nullptr;
+    size_t scratch = 0;
+    if (int rc = upload_blob(*c, phi->stream, b, (scratch_doubles + R) * 8 + 256, &d, &scratch))
+        return rc;
+    double *d_grad = (double *)(d + scratch);
+    double *d_scr = d_grad + R;
+    QSV_CUDA(launch_rotation_adjoint(phi->amps, lam->amps, phi->n, R, (const uint64_t *)(d + ox),
+                                     (const uint64_t *)(d + oy), (const uint64_t *)(d + oz), x, y, z,
+                                     (const double *)(d + ot), d_scr, d_grad, phi->stream));
+    if (int rc = ensure_stage(*c, (size_t)R * 8)) return rc;
+    QSV_CUDA(cudaMemcpyAsync(c->h_stage, d_grad, (size_t)R * 8, cudaMemcpyDeviceToHost, phi->stream));
+    QSV_CUDA(cudaStreamSynchronize(phi->stream));
+    std::memcpy(grad, c->h_stage, (size_t)R * 8);
+    return QSV_OK;
+}
+
 int qsv_axpby(qsv_state *y, const qsv_state *x, double are, double aim, double bre, double bim)
 {
     if (int rc = check_state(y)) return rc;

@@ -144,6 +144,13 @@ cudaError_t launch_expect_sweep(const double2 *psi, const TileDims &g, const uin
                                 const int32_t *d_comp, const GroupRec *d_groups, int ngroups,
                                 const TermRec *d_terms, int nterms, int ndiag, bool wide,
                                 double *d_partial, int *grid_out, cudaStream_t st);
+int elementwise_grid(uint64_t dim, int device);
+int adjoint_smem_max_qubits();
+size_t adjoint_scratch_doubles(int n, int64_t R, int device);
+cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R, const uint64_t *X,
+                                    const uint64_t *Y, const uint64_t *Z, const uint64_t *hX,
+                                    const uint64_t *hY, const uint64_t *hZ, const double *theta,
+                                    double *d_scratch, double *d_grad, cudaStream_t st);
 cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
                                   double *out, cudaStream_t st);
 cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStream_t st);

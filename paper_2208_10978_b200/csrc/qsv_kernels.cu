@@ -585,14 +585,14 @@ __global__ void __launch_bounds__(T) expect_global_kernel(const double2 *__restr
 
 int g_num_sms[64] = {0};
 
+}  // namespace
+
 int elementwise_grid(uint64_t dim, int device)
 {
     const uint64_t want = (dim + 255) / 256;
     const uint64_t cap = (uint64_t)num_sms(device) * 8;
     return (int)(want < cap ? (want ? want : 1) : cap);
 }
-
-}  // namespace
 
 int num_sms(int device)
 {

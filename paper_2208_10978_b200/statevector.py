@@ -20,6 +20,7 @@ Layout: basis-index bit k is qubit k (statevector.py:4-5).
 from __future__ import annotations
 
 import ctypes
+import os
 import weakref
 from typing import Optional
 
@@ -423,6 +424,51 @@ def reverse_gradient(c, theta, h, s0: StateVector) -> np.ndarray:
     return reverse_gradient_general(c, theta, lambda s: apply_operator(s, h), s0)
 
 
+def _rotation_program(c):
+    """If every gate of c sits in a recognised pauli_evolution block
+    (circuit.py:271-281) and the only parameters are the blocks' RZ angles,
+    return (x, y, z masks, rz gate index per block); else None."""
+    from .circuit import _bind_plan
+
+    plan = _bind_plan(c)
+    G = len(plan.kinds)
+    if G == 0:
+        return None
+    spans, masks = _lib.match_rotations(c.n_qubits, plan.kinds, plan.qubits)
+    if len(spans) == 0 or spans[0, 0] != 0 or int(spans[:, 1].sum()) != G:
+        return None
+    if np.any(spans[1:, 0] != spans[:-1, 0] + spans[:-1, 1]):
+        return None
+    rz = spans[:, 2]
+    if not np.all(np.isin(plan.slot, 3 * rz)):
+        return None
+    return (np.ascontiguousarray(masks[:, 0]), np.ascontiguousarray(masks[:, 1]),
+            np.ascontiguousarray(masks[:, 2]), rz)
+
+
+def _rotation_gradient(c, theta, apply_h, s0: StateVector, prog) -> np.ndarray:
+    """Device adjoint sweep over the rotations (qsv_rotation_adjoint): the
+    block angle is its RZ value, dE/dtheta_k = sum over blocks of
+    scale * Im <lam_r|P_r|phi_r>."""
+    from .circuit import _bind_plan, bind
+
+    x, y, z, rz = prog
+    bound = bind(c, theta)
+    values = bound.flat()[2]
+    angles = np.ascontiguousarray(values[3 * rz])
+    psi = evolve(s0, bound)
+    lam = apply_h(psi)
+    g = np.zeros(len(rz), dtype=np.float64)
+    _lib.check(_lib.lib().qsv_rotation_adjoint(psi.handle, lam.handle, len(rz), _lib.u64ptr(x),
+                                               _lib.u64ptr(y), _lib.u64ptr(z), _lib.dptr(angles),
+                                               _lib.dptr(g)))
+    plan = _bind_plan(c)
+    block_of_slot = np.searchsorted(3 * rz, plan.slot)
+    grad = np.zeros(c.n_params, dtype=np.float64)
+    np.add.at(grad, plan.index, plan.scale * g[block_of_slot])
+    return grad
+
+
 def reverse_gradient_general(c, theta, apply_h, s0: StateVector) -> np.ndarray:
     """Reverse-mode sweep (Algorithm 1, statevector.py:166-211) on device states.
 
@@ -442,6 +488,14 @@ def reverse_gradient_general(c, theta, apply_h, s0: StateVector) -> np.ndarray:
     for gate in c.gates:
         if gate.params and gate.kind not in ("RZ", "RY", "U3", "CU3"):
             raise ValueError(f"gate kind {gate.kind} is not differentiable")
+    if theta.shape != (c.n_params,):
+        raise ValueError(f"expected {c.n_params} parameter values, got {theta.shape}")
+    # circuits made of pauli_evolution blocks (UCC ansatze): one device-side
+    # adjoint sweep over the rotations, no per-parameter host round trips
+    if os.environ.get("QSV_ROTATION_ADJOINT", "1") != "0":
+        prog = _rotation_program(c)
+        if prog is not None:
+            return _rotation_gradient(c, theta, apply_h, s0, prog)
     n = c.n_qubits
     bound = bind(c, theta)
     psi = evolve(s0, bound)

@@ -442,3 +442,29 @@ def test_download_async_snapshot_and_reuse():
         del s
     for k in range(3):
         assert np.abs(bufs[k] - ref_a).max() <= AMP_TOL
+
+
+@pytest.mark.parametrize("n,ne,count", [(10, 4, 200), (14, 6, 150)])
+def test_rotation_adjoint_matches_general_path(monkeypatch, n, ne, count):
+    """qsv_rotation_adjoint (one device sweep; shared-memory kernel at
+    n <= 12, two launches per rotation above) vs the gate-level reverse
+    sweep and the CPU oracle; shared parameters (several blocks on one
+    theta, scale / offset) accumulate like the reference's per-gate loop."""
+    from paper_2208_10978_b200.circuit import Affine, Circuit, evolution_gates
+
+    rng = np.random.default_rng(n)
+    strings = W.ucc_rotation_strings(n, ne)[:count]
+    gates = []
+    for k, s in enumerate(strings):
+        gates.extend(evolution_gates(s, Affine(k % 60, -0.5 * (1 + (k % 3)), 0.01 * (k % 5))))
+    circ = Circuit(n, tuple(gates), 60)
+    assert sv._rotation_program(circ) is not None
+    theta = rng.uniform(-0.3, 0.3, 60)
+    h = W.sparse_random_hamiltonian(n, 60, rng, z_only=10)
+    ref = W.hf_bitstring(ne, n)
+    fast = sv.reverse_gradient(circ, theta, h, sv.init_state(ref))
+    monkeypatch.setenv("QSV_ROTATION_ADJOINT", "0")
+    slow = sv.reverse_gradient(circ, theta, h, sv.init_state(ref))
+    assert np.abs(fast - slow).max() <= 1e-10
+    grad_ref = O.reverse_gradient(circ, theta, h, O.init_state(ref), n)
+    assert np.abs(fast - grad_ref).max() <= 1e-10
