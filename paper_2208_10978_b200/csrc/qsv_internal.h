@@ -112,15 +112,7 @@ struct qsv_state {
     int device = 0;
     uint64_t dim = 0;
     double2 *amps = nullptr;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    // per-state workspace (lazily grown)
-    void *d_work = nullptr;
-    size_t d_work_bytes = 0;
-    void *h_stage = nullptr;  // pinned staging for host->device programs
-    size_t h_stage_bytes = 0;
-    cudaEvent_t stage_done = nullptr;
-    bool stage_pending = false;
+    cudaStream_t stream = nullptr;  // the device's library stream unless qsv_set_stream
     // asynchronous download (qsv_download_async) in flight on the copy stream
     cudaEvent_t dl_done = nullptr;
     bool dl_pending = false;
