@@ -92,3 +92,26 @@ def test_invalid_inputs_raise():
         sv.sample(s, PauliString.from_label("Z0"), 0, 1)
     with pytest.raises(ValueError):
         sv.from_amplitudes(np.ones(3))
+
+
+@pytest.mark.parametrize("n,ne", [(12, 6), (13, 6)])
+def test_hot_program_specialisation(n, ne):
+    """Below the specialisation threshold a structure is compiled once it has
+    run QSV_JIT_HOT_USES (3) times; every run -- interpreted, then
+    specialised, with new angles each time -- matches the oracle."""
+    from paper_2208_10978_b200 import _lib
+    from paper_2208_10978_b200.circuit import bind
+
+    strings = W.ucc_rotation_strings(n, ne)[:160]
+    param = W.parametric_rotations_circuit(n, strings)
+    ref = W.hf_bitstring(ne, n)
+    rng = np.random.default_rng(n)
+    _, before = _lib.jit_info()
+    for k in range(4):
+        theta = rng.uniform(-0.3, 0.3, len(strings))
+        bound = bind(param, theta)
+        psi = sv.evolve(sv.init_state(ref), bound)
+        exp = O.evolve(O.init_state(ref), W.rotations_circuit(n, strings, theta).gates)
+        assert np.abs(psi.amplitudes - exp).max() <= 1e-10
+    _, after = _lib.jit_info()
+    assert after > before  # the later runs used specialised passes
