@@ -895,6 +895,35 @@ int qsv_apply_operator(const qsv_state *src, qsv_state *dst, int64_t S, const ui
         QSV_CUDA(cudaMemsetAsync(dst->amps, 0, 16 * dst->dim, src->stream));
         return QSV_OK;
     }
+    if (src->n <= 16 && S >= 4) {
+        // small (L2-resident) state: one kernel over all strings instead of S
+        // launches, same per-string arithmetic and order
+        std::lock_guard<std::recursive_mutex> lk(g_mu);
+        DeviceCtx *c = nullptr;
+        if (int rc = ctx_for(src->device, &c)) return rc;
+        std::vector<uint64_t> fs(2 * S);
+        std::vector<double> cf(2 * S);
+        for (int64_t t = 0; t < S; ++t) {
+            fs[2 * t] = x[t] | y[t];
+            fs[2 * t + 1] = y[t] | z[t];
+            const int wy = __builtin_popcountll(y[t]) & 3;  // i^{|y|}, as launch_apply_pauli
+            double pre = 1.0, pim = 0.0;
+            if (wy == 1) { pre = 0.0; pim = 1.0; }
+            else if (wy == 2) { pre = -1.0; }
+            else if (wy == 3) { pre = 0.0; pim = -1.0; }
+            const double cre = coef_re[t], cim = coef_im ? coef_im[t] : 0.0;
+            cf[2 * t] = cre * pre - cim * pim;
+            cf[2 * t + 1] = cre * pim + cim * pre;
+        }
+        Blob b;
+        const size_t of = b.add(fs.data(), fs.size() * 8), oc = b.add(cf.data(), cf.size() * 8);
+        char *d = nullptr;
+        size_t scratch = 0;
+        if (int rc = upload_blob(*c, src->stream, b, 0, &d, &scratch)) return rc;
+        QSV_CUDA(launch_apply_operator_small(src->amps, dst->amps, src->dim, (const uint64_t *)(d + of),
+                                             (const double2 *)(d + oc), (int)S, src->stream));
+        return QSV_OK;
+    }
     for (int64_t t = 0; t < S; ++t) {
         QSV_CUDA(launch_apply_pauli(src->amps, dst->amps, src->dim, x[t], y[t], z[t], coef_re[t],
                                     coef_im ? coef_im[t] : 0.0, t > 0 ? 1 : 0, src->stream));

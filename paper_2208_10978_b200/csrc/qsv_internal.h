@@ -146,6 +146,9 @@ cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R
 cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
                                   double *out, cudaStream_t st);
 cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStream_t st);
+cudaError_t launch_apply_operator_small(const double2 *src, double2 *dst, uint64_t dim,
+                                        const uint64_t *d_fs, const double2 *d_coefs, int S,
+                                        cudaStream_t st);
 cudaError_t launch_apply_pauli(const double2 *src, double2 *dst, uint64_t dim, uint64_t x,
                                uint64_t y, uint64_t z, double cre, double cim, int accumulate,
                                cudaStream_t st);

@@ -426,6 +426,27 @@ __global__ void apply_pauli_kernel(const double2 *__restrict__ src, double2 *__r
     }
 }
 
+// H|psi> for small states (L2-resident): one kernel over all strings,
+// dst[j] = sum_t coef_t (-1)^{popc((j^f_t) & s_t)} src[j ^ f_t] accumulated in
+// string order with the per-string kernel's arithmetic (bit-identical to S
+// apply_pauli launches).  terms: [f, s] per string, coefs: i^{|y|}-folded.
+__global__ void __launch_bounds__(256) apply_operator_small_kernel(
+    const double2 *__restrict__ src, double2 *__restrict__ dst, uint64_t dim,
+    const uint64_t *__restrict__ fs, const double2 *__restrict__ coefs, int S)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < dim; j += stride) {
+        double2 d = make_double2(0.0, 0.0);
+        for (int t = 0; t < S; ++t) {
+            const uint64_t i = j ^ __ldg(fs + 2 * t);
+            double2 v = cmul(__ldg(coefs + t), __ldg(src + i));
+            if (__popcll(i & __ldg(fs + 2 * t + 1)) & 1) v = make_double2(-v.x, -v.y);
+            d = t == 0 ? v : make_double2(d.x + v.x, d.y + v.y);
+        }
+        dst[j] = d;
+    }
+}
+
 // mode 0: sum conj(a) b ; mode 1: sum |a|^2 (imag = 0)
 template <int T>
 __global__ void __launch_bounds__(T) dot_partial_kernel(const double2 *__restrict__ a,
@@ -652,6 +673,18 @@ cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStr
     int dev = 0;
     cudaGetDevice(&dev);
     set_basis_kernel<<<elementwise_grid(dim, dev), 256, 0, st>>>(psi, dim, index);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_operator_small(const double2 *src, double2 *dst, uint64_t dim,
+                                        const uint64_t *d_fs, const double2 *d_coefs, int S,
+                                        cudaStream_t st)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t want = (dim + 255) / 256;
+    const int grid = (int)(want ? want : 1);
+    apply_operator_small_kernel<<<grid, 256, 0, st>>>(src, dst, dim, d_fs, d_coefs, S);
     return cudaGetLastError();
 }
 
