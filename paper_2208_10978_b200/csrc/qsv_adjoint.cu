@@ -73,7 +73,7 @@ constexpr int kSmemT = 1024;
 __global__ void __launch_bounds__(kSmemT, 1)
 adjoint_smem_kernel(double2 *__restrict__ phi_g, double2 *__restrict__ lam_g, int n, int R,
                     const uint64_t *__restrict__ X, const uint64_t *__restrict__ Y,
-                    const uint64_t *__restrict__ Z, const double *__restrict__ theta,
+                    const uint64_t *__restrict__ Z, const double2 *__restrict__ cs,
                     double *__restrict__ grad)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -110,8 +110,8 @@ adjoint_smem_kernel(double2 *__restrict__ phi_g, double2 *__restrict__ lam_g, in
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (lane == 0) grad[r] = v;
         }
-        double sn, c;
-        sincos(0.5 * __ldg(theta + r), &sn, &c);
+        const double2 csr = __ldg(cs + r);  // cos, sin of theta_r / 2 (host libm)
+        const double c = csr.x, sn = csr.y;
         if (f != 0) {
             const int h = 31 - __clz(f);
             for (uint32_t p = tid; p < dim / 2; p += kSmemT) {
@@ -171,10 +171,10 @@ __global__ void __launch_bounds__(kT) adjoint_dot_kernel(const double2 *__restri
 __global__ void __launch_bounds__(kT) adjoint_unrotate_kernel(double2 *__restrict__ phi,
                                                               double2 *__restrict__ lam, uint64_t dim,
                                                               uint64_t f, uint64_t s, int ny,
-                                                              const double *__restrict__ theta, int r)
+                                                              const double2 *__restrict__ cs, int r)
 {
-    double sn, c;
-    sincos(0.5 * __ldg(theta + r), &sn, &c);
+    const double2 csr = __ldg(cs + r);
+    const double c = csr.x, sn = csr.y;
     const uint64_t stride = (uint64_t)gridDim.x * kT;
     if (f != 0) {
         const int h = 63 - __clzll(f);
@@ -207,11 +207,11 @@ size_t adjoint_scratch_doubles(int n, int64_t R, int device)
     return (size_t)elementwise_grid(1ull << n, device) * (size_t)R + (size_t)R;
 }
 
-// X/Y/Z/theta: device arrays of R rotations in forward order; d_scratch of
+// X/Y/Z/cs (cos, sin of theta/2): device arrays of R rotations in forward order; d_scratch of
 // adjoint_scratch_doubles(); the gradient lands in d_grad[R].
 cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R, const uint64_t *X,
                                     const uint64_t *Y, const uint64_t *Z, const uint64_t *hX,
-                                    const uint64_t *hY, const uint64_t *hZ, const double *theta,
+                                    const uint64_t *hY, const uint64_t *hZ, const double2 *cs,
                                     double *d_scratch, double *d_grad, cudaStream_t st)
 {
     if (R <= 0) return cudaSuccess;
@@ -226,7 +226,7 @@ cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R
                                  32 << 12);
             configured = true;
         }
-        adjoint_smem_kernel<<<1, kSmemT, smem, st>>>(phi, lam, n, (int)R, X, Y, Z, theta, d_grad);
+        adjoint_smem_kernel<<<1, kSmemT, smem, st>>>(phi, lam, n, (int)R, X, Y, Z, cs, d_grad);
         return cudaGetLastError();
     }
     const int G = elementwise_grid(dim, dev);
@@ -234,7 +234,7 @@ cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R
         const uint64_t f = hX[r] | hY[r], s = hY[r] | hZ[r];
         const int ny = __builtin_popcountll(hY[r]) & 3;
         adjoint_dot_kernel<<<G, kT, 0, st>>>(phi, lam, dim, f, s, ny, (int)r, (int)R, d_scratch);
-        adjoint_unrotate_kernel<<<G, kT, 0, st>>>(phi, lam, dim, f, s, ny, theta, (int)r);
+        adjoint_unrotate_kernel<<<G, kT, 0, st>>>(phi, lam, dim, f, s, ny, cs, (int)r);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -990,9 +990,14 @@ int qsv_rotation_adjoint(qsv_state *phi, qsv_state *lam, int64_t R, const uint64
     if (lam->stream != phi->stream) QSV_CUDA(cudaStreamSynchronize(lam->stream));
     DeviceCtx *c = nullptr;
     if (int rc = ctx_for(phi->device, &c)) return rc;
+    std::vector<double> cs(2 * R);  // cos, sin of theta/2 (as the rotation passes: host libm)
+    for (int64_t r = 0; r < R; ++r) {
+        cs[2 * r] = std::cos(0.5 * theta[r]);
+        cs[2 * r + 1] = std::sin(0.5 * theta[r]);
+    }
     Blob b;
     const size_t ox = b.add(x, R * 8), oy = b.add(y, R * 8), oz = b.add(z, R * 8),
-                 ot = b.add(theta, R * 8);
+                 ot = b.add(cs.data(), R * 16);
     const size_t scratch_doubles = adjoint_scratch_doubles(phi->n, R, phi->device);
     char *d = nullptr;
     size_t scratch = 0;
@@ -1002,7 +1007,7 @@ int qsv_rotation_adjoint(qsv_state *phi, qsv_state *lam, int64_t R, const uint64
     double *d_scr = d_grad + R;
     QSV_CUDA(launch_rotation_adjoint(phi->amps, lam->amps, phi->n, R, (const uint64_t *)(d + ox),
                                      (const uint64_t *)(d + oy), (const uint64_t *)(d + oz), x, y, z,
-                                     (const double *)(d + ot), d_scr, d_grad, phi->stream));
+                                     (const double2 *)(d + ot), d_scr, d_grad, phi->stream));
     if (int rc = ensure_stage(*c, (size_t)R * 8)) return rc;
     QSV_CUDA(cudaMemcpyAsync(c->h_stage, d_grad, (size_t)R * 8, cudaMemcpyDeviceToHost, phi->stream));
     QSV_CUDA(cudaStreamSynchronize(phi->stream));

@@ -141,7 +141,7 @@ int adjoint_smem_max_qubits();
 size_t adjoint_scratch_doubles(int n, int64_t R, int device);
 cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R, const uint64_t *X,
                                     const uint64_t *Y, const uint64_t *Z, const uint64_t *hX,
-                                    const uint64_t *hY, const uint64_t *hZ, const double *theta,
+                                    const uint64_t *hY, const uint64_t *hZ, const double2 *cs,
                                     double *d_scratch, double *d_grad, cudaStream_t st);
 cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
                                   double *out, cudaStream_t st);
