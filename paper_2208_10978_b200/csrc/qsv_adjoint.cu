@@ -12,14 +12,18 @@
 // P convention (kernels.apply_pauli, _cykernels.pyx:76-102):
 //     (P a)_j = i^{|y|} (-1)^{popc((j ^ f) & (y | z))} a_{j ^ f},   f = x | y.
 //
-// Small states (2^n <= 4096, both vectors in shared memory): ONE CTA runs
-// the whole backward sweep -- per rotation one block reduction and one
-// in-SMEM update, no launches, no host round trips.  Larger states: two
-// launches per rotation (partial inner products into a [block][rotation]
-// array, then the fused update of both vectors); one deterministic column
-// reduction at the end.  Either way the host reads the gradient once.
+// Consecutive rotations with the same flip f (the strings of one excitation)
+// act on the same amplitude pairs (j, j ^ f), so they are processed as a run:
+// each thread keeps its pairs in registers across the run (per-rotation
+// partial inner products, then the un-rotation) -- one read and one write of
+// both vectors per run.  Default: one launch per run over every SM
+// (partials into a [block][rotation] array, one deterministic column
+// reduction at the end); QSV_ADJOINT=smem: for 2^n <= 4096 a single CTA runs
+// the whole sweep in shared memory (no launches, but one SM of FP64: 2.2x
+// slower at 12 qubits).  Either way the host reads the gradient once.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "qsv_internal.h"
 
@@ -68,8 +72,36 @@ __device__ __forceinline__ double2 unrotate_diag(double2 a, uint64_t j, uint64_t
     return make_double2(fma(sn, p.x, c * a.x), fma(sn, p.y, c * a.y));
 }
 
-constexpr int kSmemT = 1024;
+constexpr int kSmemT = 512;
+constexpr int kPPT = 4;     // amplitude pairs per thread (2^12 / 2 / 512)
+constexpr int kGroup = 8;   // rotations of one same-flip run handled in registers
 
+// Block sum of v[0..g) (fixed order: lanes, then warps) into grad[r_top - k].
+__device__ __forceinline__ void block_sums(double (&v)[kGroup], int g, double (*red)[kSmemT / 32],
+                                           double *grad, int r_top)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {
+        if (k >= g) break;
+        double a = v[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) red[k][warp] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < g) {
+        double a = 0.0;
+        for (int w = 0; w < kSmemT / 32; ++w) a += red[threadIdx.x][w];
+        grad[r_top - (int)threadIdx.x] = a;
+    }
+}
+
+// Whole backward sweep in one CTA, both vectors in shared memory.  A run of
+// consecutive rotations with the same flip f acts on the same amplitude
+// pairs (j, j ^ f): each thread keeps its pairs in registers across the run
+// (partial inner products per rotation, then the un-rotation), so a run
+// costs one load / store of the pairs and one batched block reduction.
 __global__ void __launch_bounds__(kSmemT, 1)
 adjoint_smem_kernel(double2 *__restrict__ phi_g, double2 *__restrict__ lam_g, int n, int R,
                     const uint64_t *__restrict__ X, const uint64_t *__restrict__ Y,
@@ -80,58 +112,73 @@ adjoint_smem_kernel(double2 *__restrict__ phi_g, double2 *__restrict__ lam_g, in
     const uint32_t dim = 1u << n;
     double2 *phi = reinterpret_cast<double2 *>(smem_raw);
     double2 *lam = phi + dim;
-    __shared__ double red[kSmemT / 32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double red[kGroup][kSmemT / 32];
+    const int tid = threadIdx.x;
     for (uint32_t j = tid; j < dim; j += kSmemT) {
         phi[j] = phi_g[j];
         lam[j] = lam_g[j];
     }
     __syncthreads();
-    for (int r = R - 1; r >= 0; --r) {
-        const uint64_t x = __ldg(X + r), y = __ldg(Y + r), z = __ldg(Z + r);
-        const uint32_t f = (uint32_t)(x | y);
-        const uint64_t s = y | z;
-        const int ny = __popcll(y) & 3;
-        // Im <lam| P |phi>
-        double acc = 0.0;
-        for (uint32_t j = tid; j < dim; j += kSmemT) {
-            const uint32_t i = j ^ f;
-            double2 w = mul_ipow(phi[i], ny);
-            if (__popcll((uint64_t)i & s) & 1) w = make_double2(-w.x, -w.y);
-            acc += im_cdot(lam[j], w);
-        }
+    int r = R - 1;
+    while (r >= 0) {
+        const uint32_t f = (uint32_t)(__ldg(X + r) | __ldg(Y + r));
+        int r_lo = r;
+        while (r_lo > 0 && r - r_lo + 1 < kGroup &&
+               (uint32_t)(__ldg(X + r_lo - 1) | __ldg(Y + r_lo - 1)) == f)
+            --r_lo;
+        const int g = r - r_lo + 1;
+        double part[kGroup];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) red[warp] = acc;
-        __syncthreads();  // every read of phi / lam for this rotation is done
-        if (warp == 0) {
-            double v = lane < kSmemT / 32 ? red[lane] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) grad[r] = v;
-        }
-        const double2 csr = __ldg(cs + r);  // cos, sin of theta_r / 2 (host libm)
-        const double c = csr.x, sn = csr.y;
+        for (int k = 0; k < kGroup; ++k) part[k] = 0.0;
         if (f != 0) {
             const int h = 31 - __clz(f);
-            for (uint32_t p = tid; p < dim / 2; p += kSmemT) {
+#pragma unroll
+            for (int q = 0; q < kPPT; ++q) {
+                const uint32_t p = tid + q * kSmemT;
+                if (p >= dim / 2) break;
                 const uint32_t j0 = (uint32_t)ins0_64(p, h), j1 = j0 ^ f;
-                double2 a0 = phi[j0], a1 = phi[j1];
-                unrotate_pair(a0, a1, j0, j1, s, ny, c, sn);
+                double2 a0 = phi[j0], a1 = phi[j1], b0 = lam[j0], b1 = lam[j1];
+                for (int k = 0; k < g; ++k) {
+                    const int rr = r - k;
+                    const uint64_t y = __ldg(Y + rr), sm = y | __ldg(Z + rr);
+                    const int ny = __popcll(y) & 3;
+                    // Im <lam|P|phi> over the pair: (P a)_{j0} = i^ny sg(j1) a1, ...
+                    double2 w0 = mul_ipow(a1, ny), w1 = mul_ipow(a0, ny);
+                    if (__popcll(j1 & sm) & 1) w0 = make_double2(-w0.x, -w0.y);
+                    if (__popcll(j0 & sm) & 1) w1 = make_double2(-w1.x, -w1.y);
+                    part[k] += im_cdot(b0, w0) + im_cdot(b1, w1);
+                    const double2 csr = __ldg(cs + rr);
+                    unrotate_pair(a0, a1, j0, j1, sm, ny, csr.x, csr.y);
+                    unrotate_pair(b0, b1, j0, j1, sm, ny, csr.x, csr.y);
+                }
                 phi[j0] = a0;
                 phi[j1] = a1;
-                double2 b0 = lam[j0], b1 = lam[j1];
-                unrotate_pair(b0, b1, j0, j1, s, ny, c, sn);
                 lam[j0] = b0;
                 lam[j1] = b1;
             }
-        } else {
+        } else {  // diagonal strings: every amplitude on its own
             for (uint32_t j = tid; j < dim; j += kSmemT) {
-                phi[j] = unrotate_diag(phi[j], j, s, ny, c, sn);
-                lam[j] = unrotate_diag(lam[j], j, s, ny, c, sn);
+                double2 a = phi[j], b = lam[j];
+                for (int k = 0; k < g; ++k) {
+                    const int rr = r - k;
+                    const uint64_t y = __ldg(Y + rr), sm = y | __ldg(Z + rr);
+                    const int ny = __popcll(y) & 3;
+                    double2 w = mul_ipow(a, ny);
+                    if (__popcll((uint64_t)j & sm) & 1) w = make_double2(-w.x, -w.y);
+                    part[k] += im_cdot(b, w);
+                    const double2 csr = __ldg(cs + rr);
+                    a = unrotate_diag(a, j, sm, ny, csr.x, csr.y);
+                    b = unrotate_diag(b, j, sm, ny, csr.x, csr.y);
+                }
+                phi[j] = a;
+                lam[j] = b;
             }
         }
+        // grad[r - k] for k < g (the reduction's barrier also orders this
+        // run's SMEM writes before the next run's reads)
+        block_sums(part, g, red, grad, r);
         __syncthreads();
+        r = r_lo - 1;
     }
     for (uint32_t j = tid; j < dim; j += kSmemT) {
         phi_g[j] = phi[j];
@@ -139,62 +186,99 @@ adjoint_smem_kernel(double2 *__restrict__ phi_g, double2 *__restrict__ lam_g, in
     }
 }
 
-constexpr int kT = 256;
+constexpr int kT = 128;
 
-// partial[b * R + r] = block b's share of Im <lam| P_r |phi>
-__global__ void __launch_bounds__(kT) adjoint_dot_kernel(const double2 *__restrict__ phi,
-                                                         const double2 *__restrict__ lam,
-                                                         uint64_t dim, uint64_t f, uint64_t s, int ny,
-                                                         int r, int R, double *__restrict__ partial)
+// One same-flip run (rotations r_top, r_top-1, .., r_top-g+1) over the whole
+// vector: every thread takes pairs (j, j ^ f) grid-stride, accumulates each
+// rotation's inner product and un-rotates the pair in registers; the block's
+// per-rotation sums go to partial[block][rotation] (reduced at the end in a
+// fixed order).  Diagonal runs (f == 0) take single amplitudes.
+__global__ void __launch_bounds__(kT) adjoint_run_kernel(
+    double2 *__restrict__ phi, double2 *__restrict__ lam, uint64_t dim, uint64_t f, int r_top, int g,
+    const uint64_t *__restrict__ Y, const uint64_t *__restrict__ Z, const double2 *__restrict__ cs,
+    int R, double *__restrict__ partial)
 {
-    __shared__ double red[kT / 32];
-    double acc = 0.0;
-    const uint64_t stride = (uint64_t)gridDim.x * kT;
-    for (uint64_t j = (uint64_t)blockIdx.x * kT + threadIdx.x; j < dim; j += stride) {
-        const uint64_t i = j ^ f;
-        double2 w = mul_ipow(phi[i], ny);
-        if (__popcll(i & s) & 1) w = make_double2(-w.x, -w.y);
-        acc += im_cdot(lam[j], w);
-    }
+    __shared__ double red[kGroup][kT / 32];
+    double part[kGroup];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) red[warp] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double v = 0.0;
-        for (int w = 0; w < kT / 32; ++w) v += red[w];
-        partial[(size_t)blockIdx.x * R + r] = v;
+    for (int k = 0; k < kGroup; ++k) part[k] = 0.0;
+    uint64_t sm[kGroup];
+    int ny[kGroup];
+    double2 csr[kGroup];
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {
+        if (k >= g) break;
+        const uint64_t y = __ldg(Y + r_top - k);
+        sm[k] = y | __ldg(Z + r_top - k);
+        ny[k] = __popcll(y) & 3;
+        csr[k] = __ldg(cs + r_top - k);
     }
-}
-
-__global__ void __launch_bounds__(kT) adjoint_unrotate_kernel(double2 *__restrict__ phi,
-                                                              double2 *__restrict__ lam, uint64_t dim,
-                                                              uint64_t f, uint64_t s, int ny,
-                                                              const double2 *__restrict__ cs, int r)
-{
-    const double2 csr = __ldg(cs + r);
-    const double c = csr.x, sn = csr.y;
     const uint64_t stride = (uint64_t)gridDim.x * kT;
     if (f != 0) {
         const int h = 63 - __clzll(f);
         for (uint64_t p = (uint64_t)blockIdx.x * kT + threadIdx.x; p < dim / 2; p += stride) {
             const uint64_t j0 = ins0_64(p, h), j1 = j0 ^ f;
-            double2 a0 = phi[j0], a1 = phi[j1];
-            unrotate_pair(a0, a1, j0, j1, s, ny, c, sn);
+            double2 a0 = phi[j0], a1 = phi[j1], b0 = lam[j0], b1 = lam[j1];
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+                if (k >= g) break;
+                double2 w0 = mul_ipow(a1, ny[k]), w1 = mul_ipow(a0, ny[k]);
+                if (__popcll(j1 & sm[k]) & 1) w0 = make_double2(-w0.x, -w0.y);
+                if (__popcll(j0 & sm[k]) & 1) w1 = make_double2(-w1.x, -w1.y);
+                part[k] += im_cdot(b0, w0) + im_cdot(b1, w1);
+                unrotate_pair(a0, a1, j0, j1, sm[k], ny[k], csr[k].x, csr[k].y);
+                unrotate_pair(b0, b1, j0, j1, sm[k], ny[k], csr[k].x, csr[k].y);
+            }
             phi[j0] = a0;
             phi[j1] = a1;
-            double2 b0 = lam[j0], b1 = lam[j1];
-            unrotate_pair(b0, b1, j0, j1, s, ny, c, sn);
             lam[j0] = b0;
             lam[j1] = b1;
         }
     } else {
         for (uint64_t j = (uint64_t)blockIdx.x * kT + threadIdx.x; j < dim; j += stride) {
-            phi[j] = unrotate_diag(phi[j], j, s, ny, c, sn);
-            lam[j] = unrotate_diag(lam[j], j, s, ny, c, sn);
+            double2 a = phi[j], b = lam[j];
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+                if (k >= g) break;
+                double2 w = mul_ipow(a, ny[k]);
+                if (__popcll(j & sm[k]) & 1) w = make_double2(-w.x, -w.y);
+                part[k] += im_cdot(b, w);
+                a = unrotate_diag(a, j, sm[k], ny[k], csr[k].x, csr[k].y);
+                b = unrotate_diag(b, j, sm[k], ny[k], csr[k].x, csr[k].y);
+            }
+            phi[j] = a;
+            lam[j] = b;
         }
     }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {
+        if (k >= g) break;
+        double v = part[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[k][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < g) {
+        double v = 0.0;
+        for (int w = 0; w < kT / 32; ++w) v += red[threadIdx.x][w];
+        partial[(size_t)blockIdx.x * R + (r_top - (int)threadIdx.x)] = v;
+    }
+}
+
+int run_grid(uint64_t dim, int device)
+{
+    const uint64_t want = (dim / 2 + kT - 1) / kT;
+    const uint64_t cap = (uint64_t)num_sms(device) * 16;
+    return (int)(want < cap ? (want ? want : 1) : cap);
+}
+
+bool use_smem_kernel(int n)
+{
+    // QSV_ADJOINT=smem|runs; default: runs (every SM works on each run)
+    const char *e = getenv("QSV_ADJOINT");
+    return e && e[0] == 's' && n <= 12;
 }
 
 }  // namespace
@@ -203,12 +287,13 @@ int adjoint_smem_max_qubits() { return 12; }
 
 size_t adjoint_scratch_doubles(int n, int64_t R, int device)
 {
-    if (n <= adjoint_smem_max_qubits()) return (size_t)R;
-    return (size_t)elementwise_grid(1ull << n, device) * (size_t)R + (size_t)R;
+    if (use_smem_kernel(n)) return (size_t)R;
+    return (size_t)run_grid(1ull << n, device) * (size_t)R + (size_t)R;
 }
 
-// X/Y/Z/cs (cos, sin of theta/2): device arrays of R rotations in forward order; d_scratch of
-// adjoint_scratch_doubles(); the gradient lands in d_grad[R].
+// X/Y/Z/cs (cos, sin of theta/2): device arrays of R rotations in forward
+// order (hX/hY/hZ: the same masks on the host, to form the same-flip runs);
+// d_scratch of adjoint_scratch_doubles(); the gradient lands in d_grad[R].
 cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R, const uint64_t *X,
                                     const uint64_t *Y, const uint64_t *Z, const uint64_t *hX,
                                     const uint64_t *hY, const uint64_t *hZ, const double2 *cs,
@@ -218,23 +303,25 @@ cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t dim = 1ull << n;
-    if (n <= adjoint_smem_max_qubits()) {
+    if (use_smem_kernel(n)) {
         const size_t smem = 32 * (size_t)dim;
         static bool configured = false;
         if (!configured) {
             cudaFuncSetAttribute(adjoint_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 32 << 12);
+                                 32 << 12);  // 2 x 4096 amplitudes
             configured = true;
         }
         adjoint_smem_kernel<<<1, kSmemT, smem, st>>>(phi, lam, n, (int)R, X, Y, Z, cs, d_grad);
         return cudaGetLastError();
     }
-    const int G = elementwise_grid(dim, dev);
-    for (int64_t r = R - 1; r >= 0; --r) {
-        const uint64_t f = hX[r] | hY[r], s = hY[r] | hZ[r];
-        const int ny = __builtin_popcountll(hY[r]) & 3;
-        adjoint_dot_kernel<<<G, kT, 0, st>>>(phi, lam, dim, f, s, ny, (int)r, (int)R, d_scratch);
-        adjoint_unrotate_kernel<<<G, kT, 0, st>>>(phi, lam, dim, f, s, ny, cs, (int)r);
+    const int G = run_grid(dim, dev);
+    for (int64_t r = R - 1; r >= 0;) {
+        const uint64_t f = hX[r] | hY[r];
+        int64_t lo = r;
+        while (lo > 0 && r - lo + 1 < kGroup && (hX[lo - 1] | hY[lo - 1]) == f) --lo;
+        adjoint_run_kernel<<<G, kT, 0, st>>>(phi, lam, dim, f, (int)r, (int)(r - lo + 1), Y, Z, cs,
+                                             (int)R, d_scratch);
+        r = lo - 1;
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

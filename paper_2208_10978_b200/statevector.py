@@ -419,9 +419,12 @@ def sample(s: StateVector, p, shots: int, seed: int) -> float:
 def reverse_gradient(c, theta, h, s0: StateVector) -> np.ndarray:
     """Gradient of <psi(theta)|H|psi(theta)> over all parameters in one
     backward sweep with a single application of H (statevector.py:153-163)."""
-    if not h.is_hermitian():
+    if not _is_hermitian(h):
         raise ValueError("reverse-mode gradient requires a Hermitian operator")
     return reverse_gradient_general(c, theta, lambda s: apply_operator(s, h), s0)
+
+
+_ROT_PROG_CACHE: dict = {}
 
 
 def _rotation_program(c):
@@ -485,17 +488,20 @@ def reverse_gradient_general(c, theta, apply_h, s0: StateVector) -> np.ndarray:
     from . import kernels
 
     theta = np.asarray(theta, dtype=float)
+    if theta.shape != (c.n_params,):
+        raise ValueError(f"expected {c.n_params} parameter values, got {theta.shape}")
+    # circuits made of pauli_evolution blocks (UCC ansatze; only RZ angles
+    # are parameters): one device-side adjoint sweep over the rotations
+    if os.environ.get("QSV_ROTATION_ADJOINT", "1") != "0":
+        prog = _id_cache_get(_ROT_PROG_CACHE, c)
+        if prog is None:
+            prog = (_rotation_program(c),)
+            _id_cache_put(_ROT_PROG_CACHE, c, prog, _FLAT_MAX)
+        if prog[0] is not None:
+            return _rotation_gradient(c, theta, apply_h, s0, prog[0])
     for gate in c.gates:
         if gate.params and gate.kind not in ("RZ", "RY", "U3", "CU3"):
             raise ValueError(f"gate kind {gate.kind} is not differentiable")
-    if theta.shape != (c.n_params,):
-        raise ValueError(f"expected {c.n_params} parameter values, got {theta.shape}")
-    # circuits made of pauli_evolution blocks (UCC ansatze): one device-side
-    # adjoint sweep over the rotations, no per-parameter host round trips
-    if os.environ.get("QSV_ROTATION_ADJOINT", "1") != "0":
-        prog = _rotation_program(c)
-        if prog is not None:
-            return _rotation_gradient(c, theta, apply_h, s0, prog)
     n = c.n_qubits
     bound = bind(c, theta)
     psi = evolve(s0, bound)

@@ -444,8 +444,9 @@ def test_download_async_snapshot_and_reuse():
         assert np.abs(bufs[k] - ref_a).max() <= AMP_TOL
 
 
+@pytest.mark.parametrize("kernel", ["runs", "smem"])
 @pytest.mark.parametrize("n,ne,count", [(10, 4, 200), (14, 6, 150)])
-def test_rotation_adjoint_matches_general_path(monkeypatch, n, ne, count):
+def test_rotation_adjoint_matches_general_path(monkeypatch, n, ne, count, kernel):
     """qsv_rotation_adjoint (one device sweep; shared-memory kernel at
     n <= 12, two launches per rotation above) vs the gate-level reverse
     sweep and the CPU oracle; shared parameters (several blocks on one
@@ -462,6 +463,7 @@ def test_rotation_adjoint_matches_general_path(monkeypatch, n, ne, count):
     theta = rng.uniform(-0.3, 0.3, 60)
     h = W.sparse_random_hamiltonian(n, 60, rng, z_only=10)
     ref = W.hf_bitstring(ne, n)
+    monkeypatch.setenv("QSV_ADJOINT", kernel)  # smem: single-CTA kernel (n <= 12 only)
     fast = sv.reverse_gradient(circ, theta, h, sv.init_state(ref))
     monkeypatch.setenv("QSV_ROTATION_ADJOINT", "0")
     slow = sv.reverse_gradient(circ, theta, h, sv.init_state(ref))
