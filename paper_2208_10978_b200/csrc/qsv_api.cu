@@ -6,7 +6,6 @@
 #include <stdlib.h>
 
 #include <algorithm>
-#include <cfloat>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -195,6 +194,12 @@ struct JitCache {
     int device = -1;
     std::vector<std::string> src;
     std::vector<const void *> mod;
+    // fast path once every pass has a module: per-pass geometry tables and
+    // parameter window, so a run uploads only tables + parameters
+    bool all_jit = false;
+    std::vector<std::vector<uint64_t>> offhi;
+    std::vector<std::vector<int32_t>> comp;
+    std::vector<int> p_lo, npar;
 };
 
 // Cache of structural gate plans.
@@ -244,19 +249,57 @@ int op_param_count(const OpRec &op)
     }
 }
 
+// A cached program whose every pass is specialised: upload each pass's
+// geometry tables and parameter window, copy-and-launch.
+int run_template_jit(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params,
+                     JitCache &jc, DeviceCtx &c)
+{
+    HostProfile prof("run_template_jit");
+    Blob b;
+    const size_t np = t.passes.size();
+    std::vector<size_t> o_off(np), o_comp(np), o_par(np);
+    for (size_t k = 0; k < np; ++k) {
+        if (!jc.mod[k]) continue;
+        o_off[k] = b.add(jc.offhi[k].data(), jc.offhi[k].size() * sizeof(uint64_t));
+        o_comp[k] = b.add(jc.comp[k].data(), jc.comp[k].size() * sizeof(int32_t));
+        o_par[k] = b.add(params.data() + jc.p_lo[k], (size_t)jc.npar[k] * sizeof(double));
+    }
+    prof.mark("blob");
+    char *d = nullptr;
+    size_t scratch = 0;
+    if (int rc = upload_blob(c, s->stream, b, 0, &d, &scratch)) return rc;
+    prof.mark("upload");
+    for (size_t k = 0; k < np; ++k) {
+        const PassPlan &p = t.passes[k];
+        if (!jc.mod[k]) continue;
+        if (!jit_launch_module(jc.mod[k], s->amps, dims_of(p.geom), (const uint64_t *)(d + o_off[k]),
+                               (const int32_t *)(d + o_comp[k]), (const double *)(d + o_par[k]),
+                               jc.npar[k],
+                               (int)std::min<uint64_t>(1ull << p.geom.ncomp, (uint64_t)num_sms(s->device)),
+                               s->stream))
+            return fail_code(QSV_ERR_CUDA, "specialised pass launch failed");
+        ++g_jit_launches;
+    }
+    prof.mark("launch");
+    return QSV_OK;
+}
+
 int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params, int uses = 0,
                  JitCache *jc = nullptr)
 {
-    HostProfile prof("run_template");
     DeviceCtx *c = nullptr;
     int rc = ctx_for(s->device, &c);
     if (rc) return rc;
+    if (jc && jc->all_jit && jc->device == s->device && jc->src.size() == t.passes.size() &&
+        jit_enabled(s->n, uses))
+        return run_template_jit(s, t, params, *jc, *c);
+    HostProfile prof("run_template");
     Blob b;
     // global (shared) arrays for the legacy / fallback kernels
     const size_t o_ops = b.add(t.ops.data(), t.ops.size() * sizeof(OpRec));
     const size_t o_rots = b.add(t.rots.data(), t.rots.size() * sizeof(RotRec));
     const size_t o_par = b.add(params.data(), params.size() * sizeof(double));
-    struct PassOff { size_t off, comp, blk, ops, rots, par; int nblk, nops, nrots, npar; bool lite; };
+    struct PassOff { size_t off, comp, blk, ops, rots, par; int nblk, nops, nrots, npar, par_lo; bool lite; };
     std::vector<PassOff> po(t.passes.size());
     const bool jit = jit_enabled(s->n, uses);
     JitCache local;
@@ -321,6 +364,7 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
             o.nops = (int)lops.size();
             o.nrots = r_hi - r_lo;
             o.npar = p_hi - p_lo;
+            o.par_lo = p_lo;
             if (jit && !jit_cached)
                 jit_source(p.geom, lblk.data(), o.nblk, lops.data(), t.rots.data() + r_lo, o.npar,
                            jit_src[k]);
@@ -346,6 +390,28 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
         for (size_t k = 0; k < jit_src.size(); ++k)
             jc->mod[k] = jit_src[k].empty() ? nullptr : jit_module(s->device, jit_src[k]);
         jc->device = s->device;
+        // every pass that does work specialised (no global / small-tile /
+        // fallback passes): later runs take run_template_jit
+        bool all = true;
+        for (size_t k = 0; k < t.passes.size(); ++k) {
+            const PassPlan &p = t.passes[k];
+            const bool idle = p.op_end <= p.op_begin && !p.map_permuted;
+            if (!idle && (p.global || !jc->mod[k])) all = false;
+            if (idle && jc->mod[k]) all = false;  // keep the general path's semantics
+        }
+        if (all) {
+            jc->offhi.assign(t.passes.size(), {});
+            jc->comp.assign(t.passes.size(), {});
+            jc->p_lo.assign(t.passes.size(), 0);
+            jc->npar.assign(t.passes.size(), 0);
+            for (size_t k = 0; k < t.passes.size(); ++k) {
+                if (!jc->mod[k]) continue;
+                geom_tables(t.passes[k].geom, jc->offhi[k], jc->comp[k], &t.passes[k]);
+                jc->p_lo[k] = (int)(po[k].par_lo);
+                jc->npar[k] = po[k].npar;
+            }
+        }
+        jc->all_jit = all;
     }
     const OpRec *d_ops = (const OpRec *)(d + o_ops);
     const RotRec *d_rots = (const RotRec *)(d + o_rots);
@@ -616,9 +682,14 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
     if (int rc = settle(s)) return rc;
     HostProfile prof("apply_gates");
     {
-        bool finite = true;  // branch-free so the loop vectorises
-        for (int64_t i = 0; i < 3 * n_gates; ++i) finite &= std::fabs(values[i]) <= DBL_MAX;
-        if (!finite) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
+        // exponent all ones <=> inf / nan; an integer OR-reduction vectorises
+        uint64_t bad = 0;
+        for (int64_t i = 0; i < 3 * n_gates; ++i) {
+            uint64_t b;
+            std::memcpy(&b, values + i, 8);
+            bad |= (uint64_t)(((b >> 52) & 0x7ffu) == 0x7ffu);
+        }
+        if (bad) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
     }
     QSV_CUDA(cudaSetDevice(s->device));
     const uint64_t h = hash_structure(s->n, n_gates, kinds, qubits);
