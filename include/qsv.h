@@ -145,6 +145,17 @@ int qsv_sample_parity(const qsv_state *s, uint64_t support_mask, int64_t shots,
 int qsv_rotation_adjoint(qsv_state *phi, qsv_state *lam, int64_t R, const uint64_t *x,
                          const uint64_t *y, const uint64_t *z, const double *theta, double *grad);
 
+/* Prepared programs: qsv_prepare_gates validates and plans a gate structure
+ * (kinds / qubits as for qsv_apply_gates) once and returns an id;
+ * qsv_apply_prepared(s, id, values) then runs it with new parameter values
+ * (3 per gate) without the per-call structure lookup -- the bind-and-evolve
+ * loop of vqe_minimize (engine.py:455-457).  Ids stay valid until released. */
+int qsv_prepare_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                      int64_t *program_id);
+int qsv_apply_prepared(qsv_state *s, int64_t program_id, const double *values,
+                       qsv_plan_stats *stats);
+int qsv_release_program(int64_t program_id);
+
 /* Planner only (no device work; usable without a GPU): the plan that
  * qsv_apply_gates / qsv_expectation would execute for these inputs. */
 int qsv_plan_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,

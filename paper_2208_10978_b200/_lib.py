@@ -53,7 +53,8 @@ EXPORTED = (
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
     "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_sample_parity",
-    "qsv_jit_info", "qsv_rotation_adjoint",
+    "qsv_jit_info", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
+    "qsv_release_program",
     "qsv_last_plan_stats",
 )
 
@@ -102,6 +103,9 @@ def _declare(L):
                                  ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_jit_info": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_rotation_adjoint": ([vp, vp, i64, u64p, u64p, u64p, dp, dp], ctypes.c_int),
+        "qsv_prepare_gates": ([ctypes.c_int, i64, i32p, i32p, ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_apply_prepared": ([vp, i64, dp, sp], ctypes.c_int),
+        "qsv_release_program": ([i64], ctypes.c_int),
         "qsv_last_plan_stats": ([sp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():

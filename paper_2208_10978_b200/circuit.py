@@ -108,9 +108,12 @@ class _BindPlan:
     flatten_bound, constant parameter values, and the (slot, index, scale,
     offset) of every Affine parameter -- so bind is O(#params) numpy work."""
 
-    __slots__ = ("kinds", "qubits", "const", "slot", "index", "scale", "offset", "__weakref__")
+    __slots__ = ("n_qubits", "kinds", "qubits", "const", "slot", "index", "scale", "offset", "_pid",
+                 "__weakref__")
 
     def __init__(self, c):
+        self.n_qubits = c.n_qubits
+        self._pid = None
         gates = c.gates
         G = len(gates)
         codes = _lib.KIND_CODES
@@ -137,6 +140,27 @@ class _BindPlan:
         self.scale = np.asarray(scale, dtype=np.float64)
         self.offset = np.asarray(offset, dtype=np.float64)
 
+    def program_id(self) -> int:
+        """Id of this structure prepared in the library (qsv_prepare_gates):
+        validated and planned once, released with the plan."""
+        if self._pid is None:
+            import ctypes
+            import weakref
+
+            pid = ctypes.c_int64()
+            _lib.check(_lib.lib().qsv_prepare_gates(self.n_qubits, len(self.kinds),
+                                                    _lib.i32ptr(self.kinds), _lib.i32ptr(self.qubits),
+                                                    ctypes.byref(pid)))
+            self._pid = pid.value
+            weakref.finalize(self, _release_program, pid.value)
+        return self._pid
+
+
+def _release_program(pid: int) -> None:
+    L = _lib._lib
+    if L is not None:
+        L.qsv_release_program(pid)
+
 
 _BIND_PLANS: dict = {}  # id(parametric circuit) -> (circuit, plan); small LRU
 
@@ -159,13 +183,14 @@ class BoundCircuit:
     objects are only built if someone reads ``gates``.  Duck-types Circuit
     (n_qubits, gates, n_params = 0, is_bound, len)."""
 
-    __slots__ = ("n_qubits", "n_params", "_kinds", "_qubits", "_values", "_src", "_gates",
+    __slots__ = ("n_qubits", "n_params", "_kinds", "_qubits", "_values", "_src", "_gates", "_plan",
                  "__weakref__")
 
-    def __init__(self, src, kinds, qubits, values):
+    def __init__(self, src, kinds, qubits, values, plan=None):
         self.n_qubits = src.n_qubits
         self.n_params = 0
         self._src = src
+        self._plan = plan
         self._kinds, self._qubits, self._values = kinds, qubits, values
         self._gates = None
 
@@ -209,7 +234,7 @@ def bind(c, theta: Sequence[float]) -> BoundCircuit:
     values = plan.const.copy()
     if len(plan.slot):
         values[plan.slot] = plan.scale * theta[plan.index] + plan.offset
-    return BoundCircuit(c, plan.kinds, plan.qubits, values)
+    return BoundCircuit(c, plan.kinds, plan.qubits, values, plan)
 
 
 def gate_matrix(kind: str, values: Sequence[float] = ()) -> np.ndarray:

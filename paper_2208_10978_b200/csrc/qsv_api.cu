@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <list>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -727,6 +728,76 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
     const int rc = run_template(s, *tpl, params, g_cache.front().uses + 1, &g_cache.front().jc);
     prof.mark("run");
     return rc;
+}
+
+// Prepared programs (qsv_prepare_gates): a validated, planned structure
+// addressed by id, so a caller that re-runs one circuit structure with new
+// angles (a VQE loop) skips the per-call structure lookup.
+static std::map<int64_t, CacheEntry> g_prepared;
+static int64_t g_next_program = 1;
+
+int qsv_prepare_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                      int64_t *program_id)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!program_id) return fail_code(QSV_ERR_INVALID, "null output");
+    *program_id = 0;
+    if (n_qubits < 1 || n_qubits > kMaxQubits)
+        return fail_code(QSV_ERR_RESOURCE, "qubit count out of range");
+    if (n_gates < 0 || (n_gates > 0 && (!kinds || !qubits)))
+        return fail_code(QSV_ERR_INVALID, "bad gate arrays");
+    qsv_state fake;
+    fake.n = n_qubits;
+    if (int rc = validate_gates(&fake, n_gates, kinds, qubits)) return rc;
+    CacheEntry e;
+    e.hash = 0;
+    e.n = n_qubits;
+    e.kinds.assign(kinds, kinds + n_gates);
+    e.qubits.assign(qubits, qubits + 2 * n_gates);
+    if (n_gates > 0) plan_gates(n_qubits, n_gates, kinds, qubits, e.tpl);
+    const int64_t id = g_next_program++;
+    g_prepared.emplace(id, std::move(e));
+    *program_id = id;
+    return QSV_OK;
+}
+
+int qsv_apply_prepared(qsv_state *s, int64_t program_id, const double *values, qsv_plan_stats *stats)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    auto it = g_prepared.find(program_id);
+    if (it == g_prepared.end()) return fail_code(QSV_ERR_INVALID, "unknown program id");
+    CacheEntry &e = it->second;
+    if (e.n != s->n) return fail_code(QSV_ERR_INVALID, "program and state qubit counts differ");
+    const int64_t n_gates = (int64_t)e.kinds.size();
+    if (n_gates == 0) {
+        ProgramTemplate empty;
+        fill_stats(empty, false, stats);
+        return QSV_OK;
+    }
+    if (!values) return fail_code(QSV_ERR_INVALID, "null gate values");
+    if (int rc = settle(s)) return rc;
+    uint64_t bad = 0;
+    for (int64_t i = 0; i < 3 * n_gates; ++i) {
+        uint64_t b;
+        std::memcpy(&b, values + i, 8);
+        bad |= (uint64_t)(((b >> 52) & 0x7ffu) == 0x7ffu);
+    }
+    if (bad) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
+    QSV_CUDA(cudaSetDevice(s->device));
+    const bool hit = e.uses > 0;
+    ++e.uses;
+    std::vector<double> params(e.tpl.n_params);
+    materialize_params(e.tpl, values, params.data());
+    fill_stats(e.tpl, hit, stats);
+    return run_template(s, e.tpl, params, e.uses, &e.jc);
+}
+
+int qsv_release_program(int64_t program_id)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    g_prepared.erase(program_id);
+    return QSV_OK;
 }
 
 static bool sweep_is_wide(const SweepPlan &sp)

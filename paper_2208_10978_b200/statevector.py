@@ -259,6 +259,13 @@ def _flat(c):
 
 def apply_circuit_inplace(s: StateVector, c) -> None:
     """Apply a bound circuit to s in place (the loop of statevector.py:72-73)."""
+    plan = getattr(c, "_plan", None)
+    if plan is not None and plan.n_qubits == s.n_qubits:
+        # bind() result: the structure is prepared in the library once
+        values = c.flat()[2]
+        _lib.check(_lib.lib().qsv_apply_prepared(s.handle, plan.program_id(), _lib.dptr(values),
+                                                 ctypes.byref(_last_stats)))
+        return
     kinds, qubits, values = _flat(c)
     _lib.check(_lib.lib().qsv_apply_gates(s.handle, len(kinds), _lib.i32ptr(kinds),
                                           _lib.i32ptr(qubits), _lib.dptr(values),

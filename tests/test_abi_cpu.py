@@ -209,3 +209,25 @@ def test_emulated_relabelled_rotations_match_oracle(seed):
     st = a / np.linalg.norm(a)
     out, prog = _emulate(circ, st)
     assert np.abs(out - O.evolve(st, circ.gates)).max() <= 1e-12
+
+
+def test_prepared_programs_host_side():
+    """qsv_prepare_gates validates and plans on the host (no GPU needed);
+    bind() results carry the plan whose program id the engine runs."""
+    import ctypes
+
+    from paper_2208_10978_b200 import _lib
+    from paper_2208_10978_b200.circuit import bind
+
+    strings = W.ucc_rotation_strings(8, 4)[:20]
+    param = W.parametric_rotations_circuit(8, strings)
+    b = bind(param, np.linspace(-0.1, 0.1, len(strings)))
+    pid = b._plan.program_id()
+    assert pid > 0 and b._plan.program_id() == pid  # prepared once
+    bad = ctypes.c_int64()
+    k = np.array([3], dtype=np.int32)            # CNOT with equal qubits
+    q = np.array([1, 1], dtype=np.int32)
+    rc = _lib.lib().qsv_prepare_gates(8, 1, _lib.i32ptr(k), _lib.i32ptr(q), ctypes.byref(bad))
+    assert rc != 0 and bad.value == 0
+    assert _lib.lib().qsv_release_program(pid) == 0
+    b._plan._pid = None  # released above; a later use prepares again
