@@ -112,7 +112,7 @@ struct Blob {
     {
         size_t off = (bytes.size() + 255) & ~(size_t)255;
         bytes.resize(off + n);
-        if (n) std::memcpy(bytes.data() + off, p, n);
+        if (n && p) std::memcpy(bytes.data() + off, p, n);
         return off;
     }
 };
@@ -201,7 +201,22 @@ struct JitCache {
     std::vector<std::vector<uint64_t>> offhi;
     std::vector<std::vector<int32_t>> comp;
     std::vector<int> p_lo, npar;
+    // OP_GMAT tables filled on the device in the fast path: per table its
+    // pass and offset inside that pass's parameter window, and the groups'
+    // concatenated yF bytes
+    std::vector<int> gmat_pass, gmat_rel, gmat_yf;
+    std::vector<uint8_t> yF;
+    // per pass: window ranges [a, b) (doubles) NOT covered by GMAT tables --
+    // the only parameters the host must upload when the tables are filled
+    // on the device (an all-GMAT window lives in device scratch only)
+    std::vector<std::vector<std::pair<int, int>>> host_ranges;
 };
+
+bool fast_path(const qsv_state *s, const ProgramTemplate &t, const JitCache *jc, int uses)
+{
+    return jc && jc->all_jit && jc->device == s->device && jc->src.size() == t.passes.size() &&
+           jit_enabled(s->n, uses);
+}
 
 // Cache of structural gate plans.
 struct CacheEntry {
@@ -253,22 +268,64 @@ int op_param_count(const OpRec &op)
 // A cached program whose every pass is specialised: upload each pass's
 // geometry tables and parameter window, copy-and-launch.
 int run_template_jit(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params,
-                     JitCache &jc, DeviceCtx &c)
+                     JitCache &jc, DeviceCtx &c, bool gmats_on_device)
 {
     HostProfile prof("run_template_jit");
     Blob b;
     const size_t np = t.passes.size();
     std::vector<size_t> o_off(np), o_comp(np), o_par(np);
+    std::vector<char> in_scratch(np, 0);
+    size_t scratch_bytes = 0;
     for (size_t k = 0; k < np; ++k) {
         if (!jc.mod[k]) continue;
         o_off[k] = b.add(jc.offhi[k].data(), jc.offhi[k].size() * sizeof(uint64_t));
         o_comp[k] = b.add(jc.comp[k].data(), jc.comp[k].size() * sizeof(int32_t));
-        o_par[k] = b.add(params.data() + jc.p_lo[k], (size_t)jc.npar[k] * sizeof(double));
+        if (gmats_on_device && jc.host_ranges[k].empty()) {  // tables only: device scratch
+            in_scratch[k] = 1;
+            o_par[k] = scratch_bytes;  // relative to the scratch base, fixed below
+            scratch_bytes += ((size_t)jc.npar[k] * 8 + 255) & ~(size_t)255;
+        } else if (gmats_on_device) {  // upload only the non-table parameters
+            o_par[k] = b.add(nullptr, (size_t)jc.npar[k] * sizeof(double));
+            for (const auto &rg : jc.host_ranges[k])
+                std::memcpy(b.bytes.data() + o_par[k] + (size_t)rg.first * 8,
+                            params.data() + jc.p_lo[k] + rg.first, (size_t)(rg.second - rg.first) * 8);
+        } else {
+            o_par[k] = b.add(params.data() + jc.p_lo[k], (size_t)jc.npar[k] * sizeof(double));
+        }
+    }
+    const int ng = gmats_on_device ? (int)t.gfills.size() : 0;
+    size_t o_jobs = 0, o_cs = 0, o_q = 0, o_yf = 0;
+    if (ng) {
+        std::vector<double> cs(2 * t.rots.size());
+        std::vector<int32_t> q(t.rots.size());
+        for (size_t r = 0; r < t.rots.size(); ++r) {
+            cs[2 * r] = t.rots[r].c;
+            cs[2 * r + 1] = t.rots[r].s;
+            q[r] = t.rots[r].q;
+        }
+        o_cs = b.add(cs.data(), cs.size() * sizeof(double));
+        o_q = b.add(q.data(), q.size() * sizeof(int32_t));
+        o_yf = b.add(jc.yF.data(), jc.yF.size());
+        o_jobs = b.add(nullptr, (size_t)ng * sizeof(GmatJob));  // filled once offsets are final
+    }
+    // upload_blob puts the scratch right after the blob (256-B aligned)
+    const size_t scratch_base = (b.bytes.size() + 255) & ~(size_t)255;
+    for (size_t k = 0; k < np; ++k)
+        if (in_scratch[k]) o_par[k] += scratch_base;
+    for (int i = 0; i < ng; ++i) {
+        const GmatFill &g = t.gfills[i];
+        const GmatJob job{(uint64_t)(o_par[jc.gmat_pass[i]] + (size_t)jc.gmat_rel[i] * 8), g.r0, g.r1,
+                          g.F, g.H, g.w, jc.gmat_yf[i]};
+        std::memcpy(b.bytes.data() + o_jobs + (size_t)i * sizeof(GmatJob), &job, sizeof(GmatJob));
     }
     prof.mark("blob");
     char *d = nullptr;
     size_t scratch = 0;
-    if (int rc = upload_blob(c, s->stream, b, 0, &d, &scratch)) return rc;
+    if (int rc = upload_blob(c, s->stream, b, scratch_bytes, &d, &scratch)) return rc;
+    if (scratch != scratch_base) return fail_code(QSV_ERR_CUDA, "unexpected workspace layout");
+    if (ng)
+        QSV_CUDA(launch_gmat_fill(d, (const GmatJob *)(d + o_jobs), ng, (const double2 *)(d + o_cs),
+                                  (const int32_t *)(d + o_q), (const uint8_t *)(d + o_yf), s->stream));
     prof.mark("upload");
     for (size_t k = 0; k < np; ++k) {
         const PassPlan &p = t.passes[k];
@@ -285,15 +342,15 @@ int run_template_jit(qsv_state *s, ProgramTemplate &t, const std::vector<double>
     return QSV_OK;
 }
 
+// gmats_on_device: params lack the OP_GMAT tables (materialize_params with
+// with_gmats = false); only valid when fast_path() holds.
 int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params, int uses = 0,
-                 JitCache *jc = nullptr)
+                 JitCache *jc = nullptr, bool gmats_on_device = false)
 {
     DeviceCtx *c = nullptr;
     int rc = ctx_for(s->device, &c);
     if (rc) return rc;
-    if (jc && jc->all_jit && jc->device == s->device && jc->src.size() == t.passes.size() &&
-        jit_enabled(s->n, uses))
-        return run_template_jit(s, t, params, *jc, *c);
+    if (fast_path(s, t, jc, uses)) return run_template_jit(s, t, params, *jc, *c, gmats_on_device);
     HostProfile prof("run_template");
     Blob b;
     // global (shared) arrays for the legacy / fallback kernels
@@ -410,6 +467,42 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                 geom_tables(t.passes[k].geom, jc->offhi[k], jc->comp[k], &t.passes[k]);
                 jc->p_lo[k] = (int)(po[k].par_lo);
                 jc->npar[k] = po[k].npar;
+            }
+            // the pass window holding each OP_GMAT table
+            jc->gmat_pass.assign(t.gfills.size(), -1);
+            jc->gmat_rel.assign(t.gfills.size(), 0);
+            jc->gmat_yf.assign(t.gfills.size(), 0);
+            jc->yF.clear();
+            for (size_t i = 0; i < t.gfills.size(); ++i) {
+                const GmatFill &g = t.gfills[i];
+                const int len = 16 << (g.w - 1);
+                for (size_t k = 0; k < t.passes.size(); ++k)
+                    if (jc->mod[k] && g.offset >= jc->p_lo[k] &&
+                        g.offset + len <= jc->p_lo[k] + jc->npar[k]) {
+                        jc->gmat_pass[i] = (int)k;
+                        jc->gmat_rel[i] = g.offset - jc->p_lo[k];
+                        break;
+                    }
+                if (jc->gmat_pass[i] < 0) all = false;
+                jc->gmat_yf[i] = (int)jc->yF.size();
+                jc->yF.insert(jc->yF.end(), g.yF.begin(), g.yF.end());
+            }
+            // window ranges not covered by tables
+            jc->host_ranges.assign(t.passes.size(), {});
+            for (size_t k = 0; k < t.passes.size() && all; ++k) {
+                if (!jc->mod[k]) continue;
+                std::vector<char> cov(jc->npar[k], 0);
+                for (size_t i = 0; i < t.gfills.size(); ++i)
+                    if (jc->gmat_pass[i] == (int)k)
+                        std::fill(cov.begin() + jc->gmat_rel[i],
+                                  cov.begin() + jc->gmat_rel[i] + (16 << (t.gfills[i].w - 1)), 1);
+                for (int a = 0; a < jc->npar[k];) {
+                    if (cov[a]) { ++a; continue; }
+                    int e = a;
+                    while (e < jc->npar[k] && !cov[e]) ++e;
+                    jc->host_ranges[k].push_back({a, e});
+                    a = e;
+                }
             }
         }
         jc->all_jit = all;
@@ -721,11 +814,13 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
         tpl = &g_cache.front().tpl;
     }
     prof.mark("lookup");
+    CacheEntry &ce = g_cache.front();
+    const bool dev_gmats = fast_path(s, *tpl, &ce.jc, ce.uses + 1) && !tpl->gfills.empty();
     std::vector<double> params(tpl->n_params);
-    materialize_params(*tpl, values, params.data());
+    materialize_params(*tpl, values, params.data(), !dev_gmats);
     prof.mark("materialize");
     fill_stats(*tpl, hit, stats);
-    const int rc = run_template(s, *tpl, params, g_cache.front().uses + 1, &g_cache.front().jc);
+    const int rc = run_template(s, *tpl, params, ce.uses + 1, &ce.jc, dev_gmats);
     prof.mark("run");
     return rc;
 }
@@ -787,10 +882,11 @@ int qsv_apply_prepared(qsv_state *s, int64_t program_id, const double *values, q
     QSV_CUDA(cudaSetDevice(s->device));
     const bool hit = e.uses > 0;
     ++e.uses;
+    const bool dev_gmats = fast_path(s, e.tpl, &e.jc, e.uses) && !e.tpl.gfills.empty();
     std::vector<double> params(e.tpl.n_params);
-    materialize_params(e.tpl, values, params.data());
+    materialize_params(e.tpl, values, params.data(), !dev_gmats);
     fill_stats(e.tpl, hit, stats);
-    return run_template(s, e.tpl, params, e.uses, &e.jc);
+    return run_template(s, e.tpl, params, e.uses, &e.jc, dev_gmats);
 }
 
 int qsv_release_program(int64_t program_id)

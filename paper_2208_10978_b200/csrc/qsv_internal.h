@@ -146,6 +146,14 @@ cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R
 cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, const int32_t *d_map,
                                   double *out, cudaStream_t st);
 cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStream_t st);
+struct GmatJob {     // one OP_GMAT table filled on the device
+    uint64_t dst;     // byte offset of the table from the blob base
+    int32_t r0, r1;   // rotations of the group (cs / q / yF index)
+    int32_t F, H, w;  // block-local flip, its highest bit, popcount
+    int32_t yf;       // offset of the group's yF bytes
+};
+cudaError_t launch_gmat_fill(char *base, const GmatJob *d_jobs, int njobs, const double2 *d_cs,
+                             const int32_t *d_q, const uint8_t *d_yF, cudaStream_t st);
 cudaError_t launch_apply_operator_small(const double2 *src, double2 *dst, uint64_t dim,
                                         const uint64_t *d_fs, const double2 *d_coefs, int S,
                                         cudaStream_t st);

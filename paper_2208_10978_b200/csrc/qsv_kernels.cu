@@ -447,6 +447,67 @@ __global__ void __launch_bounds__(256) apply_operator_small_kernel(
     }
 }
 
+// OP_GMAT tables on the device (the restatement of materialize_gmats,
+// qsv_planner.cpp): one thread per (group, flip-pattern configuration)
+// multiplies the group's rotations R = [[c, kappa sg1], [kappa sg0, c]],
+// kappa = i^q sin, and writes the table for common parity 0 and its
+// Z-conjugate for parity 1 at base + dst.
+__global__ void gmat_fill_kernel(char *__restrict__ base, const GmatJob *__restrict__ jobs, int njobs,
+                                 const double2 *__restrict__ cs, const int32_t *__restrict__ q,
+                                 const uint8_t *__restrict__ yF)
+{
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = id >> 3, cfg = id & 7;
+    if (j >= njobs) return;
+    const GmatJob g = jobs[j];
+    const int ncfg = 1 << (g.w - 1);
+    if (cfg >= ncfg) return;
+    uint32_t r1 = 1u << g.H;
+    for (int c = 0, b = 0; b < 8; ++b) {  // flip bits ascending, H skipped
+        if (!((g.F >> b) & 1) || b == g.H) continue;
+        if ((cfg >> c) & 1) r1 |= 1u << b;
+        ++c;
+    }
+    double M[8] = {1, 0, 0, 0, 0, 0, 1, 0};
+    for (int r = g.r0; r < g.r1; ++r) {
+        const double2 csr = cs[r];
+        const int qq = q[r];
+        double kre = 0.0, kim = 0.0;
+        switch (qq & 3) {
+            case 0: kre = csr.y; break;
+            case 1: kim = csr.y; break;
+            case 2: kre = -csr.y; break;
+            default: kim = -csr.y; break;
+        }
+        const int s1 = __popc(r1 & yF[g.yf + (r - g.r0)]) & 1;
+        const int s0 = s1 ^ ((qq >> 2) & 1);
+        const double b_re = s1 ? -kre : kre, b_im = s1 ? -kim : kim;
+        const double c_re = s0 ? -kre : kre, c_im = s0 ? -kim : kim;
+        const double cr = csr.x;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double a0r = M[2 * k], a0i = M[2 * k + 1];
+            const double a1r = M[4 + 2 * k], a1i = M[4 + 2 * k + 1];
+            M[2 * k] = cr * a0r + (b_re * a1r - b_im * a1i);
+            M[2 * k + 1] = cr * a0i + (b_re * a1i + b_im * a1r);
+            M[4 + 2 * k] = cr * a1r + (c_re * a0r - c_im * a0i);
+            M[4 + 2 * k + 1] = cr * a1i + (c_re * a0i + c_im * a0r);
+        }
+    }
+    double *d0 = reinterpret_cast<double *>(base + g.dst) + 8 * cfg;
+    double *d1 = reinterpret_cast<double *>(base + g.dst) + 8 * (ncfg + cfg);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d0[i] = M[i];
+    d1[0] = M[0];
+    d1[1] = M[1];
+    d1[2] = -M[2];
+    d1[3] = -M[3];
+    d1[4] = -M[4];
+    d1[5] = -M[5];
+    d1[6] = M[6];
+    d1[7] = M[7];
+}
+
 // mode 0: sum conj(a) b ; mode 1: sum |a|^2 (imag = 0)
 template <int T>
 __global__ void __launch_bounds__(T) dot_partial_kernel(const double2 *__restrict__ a,
@@ -673,6 +734,15 @@ cudaError_t launch_set_basis(double2 *psi, uint64_t dim, uint64_t index, cudaStr
     int dev = 0;
     cudaGetDevice(&dev);
     set_basis_kernel<<<elementwise_grid(dim, dev), 256, 0, st>>>(psi, dim, index);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gmat_fill(char *base, const GmatJob *d_jobs, int njobs, const double2 *d_cs,
+                             const int32_t *d_q, const uint8_t *d_yF, cudaStream_t st)
+{
+    if (njobs <= 0) return cudaSuccess;
+    const int threads = 8 * njobs;
+    gmat_fill_kernel<<<(threads + 127) / 128, 128, 0, st>>>(base, d_jobs, njobs, d_cs, d_q, d_yF);
     return cudaGetLastError();
 }
 

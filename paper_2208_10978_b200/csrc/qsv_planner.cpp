@@ -1413,7 +1413,7 @@ void materialize_gates(ProgramTemplate &t, const double *values)
     }
 }
 
-void materialize_params(ProgramTemplate &t, const double *values, double *params)
+void materialize_params(ProgramTemplate &t, const double *values, double *params, bool with_gmats)
 {
     materialize_gates(t, values);
     if (t.defers.empty()) {
@@ -1441,7 +1441,7 @@ void materialize_params(ProgramTemplate &t, const double *values, double *params
     for (const ClusterFill &cf : t.cfills)
         if (cf.offset >= 0)
             cluster_matrix(cf, t.src_kinds.data(), t.src_qubits.data(), values, params + cf.offset);
-    materialize_gmats(t, params);
+    if (with_gmats) materialize_gmats(t, params);
 }
 
 void materialize_rotations(ProgramTemplate &t, const double *theta)

@@ -113,7 +113,9 @@ void materialize_gmats(const ProgramTemplate &t, double *params);
 // Every angle-dependent parameter of a gate-list template (gate matrices,
 // fused cluster matrices, fused group tables) into params[t.n_params];
 // refreshes t.rots first.
-void materialize_params(ProgramTemplate &t, const double *values, double *params);
+// with_gmats = false: leave the OP_GMAT tables to the device (gmat fill kernel)
+void materialize_params(ProgramTemplate &t, const double *values, double *params,
+                        bool with_gmats = true);
 // Gate matrix restatement of circuit.py:198-223 (row-major complex128).
 int gate_matrix(int kind, const double *v, double *out);
 
