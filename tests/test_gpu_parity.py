@@ -470,3 +470,21 @@ def test_rotation_adjoint_matches_general_path(monkeypatch, n, ne, count, kernel
     assert np.abs(fast - slow).max() <= 1e-10
     grad_ref = O.reverse_gradient(circ, theta, h, O.init_state(ref), n)
     assert np.abs(fast - grad_ref).max() <= 1e-10
+
+
+def test_jit_fast_path_repeated_angles(jit_from_14):
+    """A specialised program re-run with new angles takes the fast path
+    (cached geometry tables, OP_GMAT tables filled on the device): every run
+    matches the oracle."""
+    from paper_2208_10978_b200.circuit import bind
+
+    n, ne = 16, 8
+    strings = W.ucc_rotation_strings(n, ne)[:300]
+    param = W.parametric_rotations_circuit(n, strings)
+    ref = W.hf_bitstring(ne, n)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        theta = rng.uniform(-0.4, 0.4, len(strings))
+        psi = sv.evolve(sv.init_state(ref), bind(param, theta))
+        exp = O.evolve(O.init_state(ref), W.rotations_circuit(n, strings, theta).gates)
+        assert np.abs(psi.amplitudes - exp).max() <= AMP_TOL
