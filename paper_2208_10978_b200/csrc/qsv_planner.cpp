@@ -1528,6 +1528,33 @@ void materialize_gmats(const ProgramTemplate &t, double *params)
 // Expectation sweeps
 // ---------------------------------------------------------------------------
 
+// Reorder terms [a, b) so that consecutive terms read different shared-memory
+// banks in the tile-wide transform lookups (index wpos(s) = s ^ ((s >> 4) & 15)
+// within a 2048-double half: bank pair = its low 4 bits): round-robin over the
+// 16 bank buckets, so a half-warp's 16 lookups are conflict-free when the
+// buckets are balanced.  Term order inside a sweep is free (map[] restores it).
+void bank_interleave(std::vector<TermRec> &terms, std::vector<int32_t> &map, size_t a, size_t b)
+{
+    if (b - a < 2) return;
+    std::vector<std::vector<size_t>> bucket(16);
+    for (size_t i = a; i < b; ++i) {
+        const uint32_t sp = terms[i].s_loc & 2047u;
+        bucket[(sp ^ (sp >> 4)) & 15u].push_back(i);
+    }
+    std::vector<TermRec> t2;
+    std::vector<int32_t> m2;
+    t2.reserve(b - a);
+    m2.reserve(b - a);
+    for (size_t round = 0; t2.size() < b - a; ++round)
+        for (int k = 0; k < 16; ++k)
+            if (round < bucket[k].size()) {
+                t2.push_back(terms[bucket[k][round]]);
+                m2.push_back(map[bucket[k][round]]);
+            }
+    std::copy(t2.begin(), t2.end(), terms.begin() + a);
+    std::copy(m2.begin(), m2.end(), map.begin() + a);
+}
+
 void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, const uint64_t *z,
                       std::vector<SweepPlan> &out, bool jit_layout)
 {
@@ -1659,6 +1686,7 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
             sp.terms.push_back(tr);
             sp.map.push_back(t);
         }
+        if (m == kMaxTileBits) bank_interleave(sp.terms, sp.map, 0, sp.terms.size());
         // heavier groups first so the two warp halves stay balanced; with the
         // specialised layout, groups with the same highest flip bit adjacent
         std::stable_sort(bin.groups.begin(), bin.groups.end(), [&](int a, int b) {
@@ -1692,6 +1720,10 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
                 }
             }
             gr.t1 = (int)sp.terms.size();
+            if (bin.wide) {  // tile-wide path: one lookup per string per tile
+                bank_interleave(sp.terms, sp.map, gr.t0, gr.t_im);
+                bank_interleave(sp.terms, sp.map, gr.t_im, gr.t1);
+            }
             sp.groups.push_back(gr);
         }
         out.push_back(std::move(sp));
