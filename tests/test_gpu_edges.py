@@ -115,3 +115,31 @@ def test_hot_program_specialisation(n, ne):
         assert np.abs(psi.amplitudes - exp).max() <= 1e-10
     _, after = _lib.jit_info()
     assert after > before  # the later runs used specialised passes
+
+
+def test_prepared_program_and_async_download_errors():
+    """Prepared programs: unknown ids, qubit-count mismatch and non-finite
+    values fail loudly; a bound circuit on a state of another size is
+    rejected; download_wait without a pending copy is a no-op."""
+    import ctypes
+
+    from paper_2208_10978_b200 import _lib
+    from paper_2208_10978_b200.circuit import bind
+
+    strings = W.ucc_rotation_strings(6, 2)[:8]
+    param = W.parametric_rotations_circuit(6, strings)
+    b = bind(param, np.full(len(strings), 0.1))
+    pid = b._plan.program_id()
+    s6, s7 = sv.init_state("000000"), sv.init_state("0000000")
+    vals = b.flat()[2].copy()
+    L = _lib.lib()
+    assert L.qsv_apply_prepared(s6.handle, 987654321, _lib.dptr(vals), None) != 0
+    assert L.qsv_apply_prepared(s7.handle, pid, _lib.dptr(vals), None) != 0
+    vals[3] = np.nan
+    assert L.qsv_apply_prepared(s6.handle, pid, _lib.dptr(vals), None) != 0
+    with pytest.raises(ValueError):
+        sv.evolve(s7, b)
+    out = sv.evolve(s6, b)
+    out.wait_download()  # nothing pending
+    ref = O.evolve(O.init_state("000000"), W.rotations_circuit(6, strings, np.full(len(strings), 0.1)).gates)
+    assert np.abs(out.amplitudes - ref).max() <= 1e-10
