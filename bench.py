@@ -387,6 +387,7 @@ def run_engine(args, rank, world, local):
         dist.barrier()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
+    _, jit_before = _lib.jit_info()
     with ClockSampler(dev) as clocks:
         torch.cuda.synchronize(dev)
         start.record(stream)
@@ -395,20 +396,11 @@ def run_engine(args, rank, world, local):
             del psi
         end.record(stream)
         torch.cuda.synchronize(dev)
+    _, jit_after = _lib.jit_info()
     t_step = start.elapsed_time(end) / 1e3 / args.steps
-
-    # set_basis share of a step (one elementwise write of 16 B x 2^n)
-    tmp = sv.StateVector._empty(N_QUBITS, dev)
-    b0 = torch.cuda.Event(enable_timing=True)
-    b1 = torch.cuda.Event(enable_timing=True)
-    b0.record(stream)
-    for _ in range(args.steps):
-        _lib.check(_lib.lib().qsv_set_basis(tmp.handle, 0))
-    b1.record(stream)
-    torch.cuda.synchronize(dev)
-    t_basis = b0.elapsed_time(b1) / 1e3 / args.steps
-    del tmp
-    t_pass = (t_step - t_basis) / passes
+    # |0..0> is synthesised by the first pass (qsv_evolve_basis): the step is
+    # exactly its passes
+    t_pass = t_step / passes
 
     t_max = t_step
     if world > 1:
@@ -450,7 +442,10 @@ def run_engine(args, rank, world, local):
         assert np.array_equal(host_out[0], host_out[1])
 
     peak, peak_kind = load_peaks()
-    achieved = 32.0 * dim / t_pass / 1e9
+    # 32 B x 2^n per pass (16 read + 16 write), except the first pass, which
+    # synthesises |0..0> and only writes: mean over the step's launches
+    alg_bytes = (32.0 * passes - 16.0) / passes * dim
+    achieved = alg_bytes / t_pass / 1e9
     line = {
         "metric": "amplitude-updates/s", "value": value, "unit": "amplitude-updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
@@ -468,7 +463,7 @@ def run_engine(args, rank, world, local):
                      "frac": achieved / peak, "traffic": TRAFFIC_PER_LAUNCH,
                      "kernel": "qsv_pass (NVRTC-specialised tile pass)",
                      "ms_per_launch": t_pass * 1e3, "peak_source": peak_kind,
-                     "algorithmic_bytes_per_launch": 32 * dim,
+                     "algorithmic_bytes_per_launch": alg_bytes,
                      "traffic_source": "ncu dram__bytes_read+write of one pass (profiles/r01_jit_pass_ncu.txt)",
                      "note": "each pass carries up to 64 dense 2x2 gates and is FP64-bound, "
                              "not HBM-bound: see the fp64 key for the binding roofline"},
@@ -478,7 +473,9 @@ def run_engine(args, rank, world, local):
                  "peak_tflops": FP64_PEAK_TFLOPS,
                  "frac": 2 * n_u1 * dim * 8 / t_step / 1e12 / FP64_PEAK_TFLOPS,
                  "peak_source": "148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200 FP64 vector)"},
-        "gpu_launches": args.steps * (passes + 1),
+        # specialised pass launches counted by the library over the timed
+        # region (the evolve from |0..0> needs no separate set_basis kernel)
+        "gpu_launches": int(jit_after - jit_before),
         "clocks": clocks.summary(),
     }
 

@@ -155,6 +155,13 @@ int qsv_prepare_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const
 int qsv_apply_prepared(qsv_state *s, int64_t program_id, const double *values,
                        qsv_plan_stats *stats);
 int qsv_release_program(int64_t program_id);
+/* evolve from a basis state (statevector.py:65-74 with init_state, :42-54):
+ * s = gates |index>.  Fused: the first specialised pass synthesises |index>
+ * instead of reading the state (saves one full write + read of the vector). */
+int qsv_evolve_basis(qsv_state *s, uint64_t index, int64_t n_gates, const int32_t *kinds,
+                     const int32_t *qubits, const double *values, qsv_plan_stats *stats);
+int qsv_evolve_basis_prepared(qsv_state *s, uint64_t index, int64_t program_id,
+                              const double *values, qsv_plan_stats *stats);
 
 /* Planner only (no device work; usable without a GPU): the plan that
  * qsv_apply_gates / qsv_expectation would execute for these inputs. */

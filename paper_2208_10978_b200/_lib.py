@@ -54,7 +54,7 @@ EXPORTED = (
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
     "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_sample_parity",
     "qsv_jit_info", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
-    "qsv_release_program",
+    "qsv_release_program", "qsv_evolve_basis", "qsv_evolve_basis_prepared",
     "qsv_last_plan_stats",
 )
 
@@ -106,6 +106,8 @@ def _declare(L):
         "qsv_prepare_gates": ([ctypes.c_int, i64, i32p, i32p, ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_apply_prepared": ([vp, i64, dp, sp], ctypes.c_int),
         "qsv_release_program": ([i64], ctypes.c_int),
+        "qsv_evolve_basis": ([vp, u64, i64, i32p, i32p, dp, sp], ctypes.c_int),
+        "qsv_evolve_basis_prepared": ([vp, u64, i64, dp, sp], ctypes.c_int),
         "qsv_last_plan_stats": ([sp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():

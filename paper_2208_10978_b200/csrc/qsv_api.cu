@@ -268,7 +268,7 @@ int op_param_count(const OpRec &op)
 // A cached program whose every pass is specialised: upload each pass's
 // geometry tables and parameter window, copy-and-launch.
 int run_template_jit(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params,
-                     JitCache &jc, DeviceCtx &c, bool gmats_on_device)
+                     JitCache &jc, DeviceCtx &c, bool gmats_on_device, uint64_t basis)
 {
     HostProfile prof("run_template_jit");
     Blob b;
@@ -327,6 +327,7 @@ int run_template_jit(qsv_state *s, ProgramTemplate &t, const std::vector<double>
         QSV_CUDA(launch_gmat_fill(d, (const GmatJob *)(d + o_jobs), ng, (const double2 *)(d + o_cs),
                                   (const int32_t *)(d + o_q), (const uint8_t *)(d + o_yf), s->stream));
     prof.mark("upload");
+    bool first = true;
     for (size_t k = 0; k < np; ++k) {
         const PassPlan &p = t.passes[k];
         if (!jc.mod[k]) continue;
@@ -334,23 +335,28 @@ int run_template_jit(qsv_state *s, ProgramTemplate &t, const std::vector<double>
                                (const int32_t *)(d + o_comp[k]), (const double *)(d + o_par[k]),
                                jc.npar[k],
                                (int)std::min<uint64_t>(1ull << p.geom.ncomp, (uint64_t)num_sms(s->device)),
-                               s->stream))
+                               s->stream, first ? basis : ~0ull))
             return fail_code(QSV_ERR_CUDA, "specialised pass launch failed");
+        first = false;
         ++g_jit_launches;
     }
+    if (first && basis != ~0ull) QSV_CUDA(launch_set_basis(s->amps, s->dim, basis, s->stream));
     prof.mark("launch");
     return QSV_OK;
 }
 
 // gmats_on_device: params lack the OP_GMAT tables (materialize_params with
 // with_gmats = false); only valid when fast_path() holds.
+// basis != ~0: the state is first set to |basis> -- fused into the first
+// pass when that pass is specialised, else a set_basis launch.
 int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params, int uses = 0,
-                 JitCache *jc = nullptr, bool gmats_on_device = false)
+                 JitCache *jc = nullptr, bool gmats_on_device = false, uint64_t basis = ~0ull)
 {
     DeviceCtx *c = nullptr;
     int rc = ctx_for(s->device, &c);
     if (rc) return rc;
-    if (fast_path(s, t, jc, uses)) return run_template_jit(s, t, params, *jc, *c, gmats_on_device);
+    if (fast_path(s, t, jc, uses))
+        return run_template_jit(s, t, params, *jc, *c, gmats_on_device, basis);
     HostProfile prof("run_template");
     Blob b;
     // global (shared) arrays for the legacy / fallback kernels
@@ -510,6 +516,21 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
     const OpRec *d_ops = (const OpRec *)(d + o_ops);
     const RotRec *d_rots = (const RotRec *)(d + o_rots);
     const double *d_par = (const double *)(d + o_par);
+    // the basis state can be synthesised by the first pass that runs only if
+    // that pass is specialised
+    size_t k_first = t.passes.size();
+    for (size_t k = 0; k < t.passes.size(); ++k) {
+        const PassPlan &p = t.passes[k];
+        if (p.op_end > p.op_begin || p.map_permuted) {
+            k_first = k;
+            break;
+        }
+    }
+    if (basis != ~0ull &&
+        !(k_first < t.passes.size() && jit && jc->mod[k_first] && !t.passes[k_first].global)) {
+        QSV_CUDA(launch_set_basis(s->amps, s->dim, basis, s->stream));
+        basis = ~0ull;
+    }
     for (size_t k = 0; k < t.passes.size(); ++k) {
         const PassPlan &p = t.passes[k];
         const PassOff &o = po[k];
@@ -522,24 +543,33 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
                 QSV_CUDA(launch_rot_global(s->amps, s->n, p.flip, d_rots + op.r0, op.r1 - op.r0,
                                            s->stream));
             }
-        } else if (jit && jc->mod[k] &&
-                   jit_launch_module(jc->mod[k], s->amps, dims_of(p.geom),
-                                     (const uint64_t *)(d + o.off), (const int32_t *)(d + o.comp),
-                                     (const double *)(d + o.par), o.npar,
-                                     (int)std::min<uint64_t>(1ull << p.geom.ncomp,
-                                                             (uint64_t)num_sms(s->device)),
-                                     s->stream)) {
-            ++g_jit_launches;
-        } else if (p.geom.m >= kBlockBits + 1) {
-            QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
-                                        (const int32_t *)(d + o.comp), (const BlockRec *)(d + o.blk),
-                                        o.nblk, (const OpRec *)(d + o.ops), o.nops,
-                                        (const RotRec *)(d + o.rots), o.nrots,
-                                        (const double *)(d + o.par), o.npar, o.lite, s->stream));
         } else {
-            QSV_CUDA(launch_tile_pass(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
-                                      (const int32_t *)(d + o.comp), d_ops + p.op_begin,
-                                      p.op_end - p.op_begin, d_rots, d_par, s->stream));
+            bool done = false;
+            if (jit && jc->mod[k]) {
+                done = jit_launch_module(jc->mod[k], s->amps, dims_of(p.geom),
+                                         (const uint64_t *)(d + o.off), (const int32_t *)(d + o.comp),
+                                         (const double *)(d + o.par), o.npar,
+                                         (int)std::min<uint64_t>(1ull << p.geom.ncomp,
+                                                                 (uint64_t)num_sms(s->device)),
+                                         s->stream, k == k_first ? basis : ~0ull);
+                if (done) ++g_jit_launches;
+            }
+            if (k == k_first && basis != ~0ull) {  // not synthesised by a specialised pass
+                if (!done) QSV_CUDA(launch_set_basis(s->amps, s->dim, basis, s->stream));
+                basis = ~0ull;
+            }
+            if (done) {
+            } else if (p.geom.m >= kBlockBits + 1) {
+                QSV_CUDA(launch_tile_blocks(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
+                                            (const int32_t *)(d + o.comp), (const BlockRec *)(d + o.blk),
+                                            o.nblk, (const OpRec *)(d + o.ops), o.nops,
+                                            (const RotRec *)(d + o.rots), o.nrots,
+                                            (const double *)(d + o.par), o.npar, o.lite, s->stream));
+            } else {
+                QSV_CUDA(launch_tile_pass(s->amps, dims_of(p.geom), (const uint64_t *)(d + o.off),
+                                          (const int32_t *)(d + o.comp), d_ops + p.op_begin,
+                                          p.op_end - p.op_begin, d_rots, d_par, s->stream));
+            }
         }
     }
     prof.mark("launch");
@@ -761,8 +791,27 @@ static int validate_gates(const qsv_state *s, int64_t n, const int32_t *kinds,
     return QSV_OK;
 }
 
+static int apply_gates_impl(qsv_state *s, int64_t n_gates, const int32_t *kinds,
+                            const int32_t *qubits, const double *values, qsv_plan_stats *stats,
+                            uint64_t basis);
+
 int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
                     const double *values, qsv_plan_stats *stats)
+{
+    return apply_gates_impl(s, n_gates, kinds, qubits, values, stats, ~0ull);
+}
+
+int qsv_evolve_basis(qsv_state *s, uint64_t index, int64_t n_gates, const int32_t *kinds,
+                     const int32_t *qubits, const double *values, qsv_plan_stats *stats)
+{
+    if (int rc = check_state(s)) return rc;
+    if (index >= s->dim) return fail_code(QSV_ERR_INVALID, "basis index out of range");
+    return apply_gates_impl(s, n_gates, kinds, qubits, values, stats, index);
+}
+
+static int apply_gates_impl(qsv_state *s, int64_t n_gates, const int32_t *kinds,
+                            const int32_t *qubits, const double *values, qsv_plan_stats *stats,
+                            uint64_t basis)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
@@ -770,6 +819,7 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
     if (n_gates == 0) {
         ProgramTemplate empty;
         fill_stats(empty, false, stats);
+        if (basis != ~0ull) return qsv_set_basis(s, basis);
         return QSV_OK;
     }
     if (!kinds || !qubits || !values) return fail_code(QSV_ERR_INVALID, "null gate arrays");
@@ -820,7 +870,7 @@ int qsv_apply_gates(qsv_state *s, int64_t n_gates, const int32_t *kinds, const i
     materialize_params(*tpl, values, params.data(), !dev_gmats);
     prof.mark("materialize");
     fill_stats(*tpl, hit, stats);
-    const int rc = run_template(s, *tpl, params, ce.uses + 1, &ce.jc, dev_gmats);
+    const int rc = run_template(s, *tpl, params, ce.uses + 1, &ce.jc, dev_gmats, basis);
     prof.mark("run");
     return rc;
 }
@@ -856,7 +906,24 @@ int qsv_prepare_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const
     return QSV_OK;
 }
 
+static int apply_prepared_impl(qsv_state *s, int64_t program_id, const double *values,
+                               qsv_plan_stats *stats, uint64_t basis);
+
 int qsv_apply_prepared(qsv_state *s, int64_t program_id, const double *values, qsv_plan_stats *stats)
+{
+    return apply_prepared_impl(s, program_id, values, stats, ~0ull);
+}
+
+int qsv_evolve_basis_prepared(qsv_state *s, uint64_t index, int64_t program_id, const double *values,
+                              qsv_plan_stats *stats)
+{
+    if (int rc = check_state(s)) return rc;
+    if (index >= s->dim) return fail_code(QSV_ERR_INVALID, "basis index out of range");
+    return apply_prepared_impl(s, program_id, values, stats, index);
+}
+
+static int apply_prepared_impl(qsv_state *s, int64_t program_id, const double *values,
+                               qsv_plan_stats *stats, uint64_t basis)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
@@ -868,6 +935,7 @@ int qsv_apply_prepared(qsv_state *s, int64_t program_id, const double *values, q
     if (n_gates == 0) {
         ProgramTemplate empty;
         fill_stats(empty, false, stats);
+        if (basis != ~0ull) return qsv_set_basis(s, basis);
         return QSV_OK;
     }
     if (!values) return fail_code(QSV_ERR_INVALID, "null gate values");
@@ -886,7 +954,7 @@ int qsv_apply_prepared(qsv_state *s, int64_t program_id, const double *values, q
     std::vector<double> params(e.tpl.n_params);
     materialize_params(e.tpl, values, params.data(), !dev_gmats);
     fill_stats(e.tpl, hit, stats);
-    return run_template(s, e.tpl, params, e.uses, &e.jc, dev_gmats);
+    return run_template(s, e.tpl, params, e.uses, &e.jc, dev_gmats, basis);
 }
 
 int qsv_release_program(int64_t program_id)

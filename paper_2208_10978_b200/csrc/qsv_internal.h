@@ -182,9 +182,11 @@ bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims
 // Loaded module of a prepared source (nullptr if unavailable); stable for the
 // process lifetime, so a cached program launches without re-hashing sources.
 const void *jit_module(int device, const std::string &src);
+// basis != ~0: the pass reads |basis> instead of psi (first pass of an evolve
+// from a basis state: no HBM read, no separate set_basis write)
 bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                        const int32_t *d_geo, const double *d_params, int nparams, int grid,
-                       cudaStream_t st);
+                       cudaStream_t st, uint64_t basis = ~0ull);
 size_t sample_scratch_bytes(uint64_t dim);
 cudaError_t launch_sample_parity(const double2 *psi, uint64_t dim, int64_t shots, uint64_t k0,
                                  uint64_t k1, uint64_t support, void *scratch, size_t scratch_bytes,

@@ -303,13 +303,17 @@ __device__ __forceinline__ void cp_async_mbar_arrive(u64 *b)
 {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(saddr(b)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(u64 *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
 __device__ __forceinline__ int ring_bar(int it) { return it % KSTAGES + KSTAGES * ((it / KSTAGES) & 1); }
 
 __device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar, u64 base);
 
 extern "C" __global__ void __launch_bounds__(2 * KT, 1)
 qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_offhi,
-         const int *__restrict__ g_geo)
+         const int *__restrict__ g_geo, u64 basis)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     u64 *full = reinterpret_cast<u64 *>(smem_raw);
@@ -346,6 +350,16 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
         const u64 tile = blockIdx.x + (u64)it * gridDim.x;
         const u64 b = tbase(tile, lane, ncomp, comp_lane);
         double2 *buf = bufs + (it % KSTAGES) * TSIZE;
+        if (basis != ~0ull) {  // the pass starts from |basis>: synthesise, no HBM read
+#pragma unroll 4
+            for (int k = 0; k < TSIZE / KT; ++k) {
+                const u32 l = tid + k * KT;
+                const u64 gi = b + (l & cmask) + offhi[l >> c];
+                buf[swz(l)] = make_double2(gi == basis ? 1.0 : 0.0, 0.0);
+            }
+            mbar_arrive(full + ring_bar(it));
+            return;
+        }
         const double2 *src = psi + b;
 #pragma unroll 4
         for (int k = 0; k < TSIZE / KT; ++k) {
@@ -911,7 +925,7 @@ bool jit_launch(int device, const std::string &src, double2 *psi, const TileDims
                 int grid, cudaStream_t st)
 {
     return jit_launch_module(jit_module(device, src), psi, g, d_offhi, d_geo, d_params, nparams,
-                             grid, st);
+                             grid, st, ~0ull);
 }
 
 const void *jit_module(int device, const std::string &src)
@@ -924,7 +938,7 @@ const void *jit_module(int device, const std::string &src)
 
 bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                        const int32_t *d_geo, const double *d_params, int nparams, int grid,
-                       cudaStream_t st)
+                       cudaStream_t st, uint64_t basis)
 {
     if (!mod) return false;
     const Module &m = *static_cast<const Module *>(mod);
@@ -932,7 +946,7 @@ bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const u
         if (g_api.MemcpyDtoDAsync(m.cparams, (CUdeviceptr)d_params, (size_t)nparams * 8, st) != 0)
             return false;
     int ncomp = g.ncomp, c = g.c;
-    void *args[] = {&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo};
+    void *args[] = {&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo, &basis};
     const unsigned smem = 256 + 3 * (16u << kMaxTileBits) + 8u * (1u << (kMaxTileBits - g.c));
     return g_api.LaunchKernel(m.fn, (unsigned)grid, 1, 1, 512, 1, 1, smem, st, args, nullptr) == 0;
 }

@@ -257,19 +257,29 @@ def _flat(c):
     return flat
 
 
-def apply_circuit_inplace(s: StateVector, c) -> None:
-    """Apply a bound circuit to s in place (the loop of statevector.py:72-73)."""
+def apply_circuit_inplace(s: StateVector, c, basis: Optional[int] = None) -> None:
+    """Apply a bound circuit to s in place (the loop of statevector.py:72-73).
+    With basis: s is first set to |basis> (fused into the first pass)."""
+    L = _lib.lib()
     plan = getattr(c, "_plan", None)
     if plan is not None and plan.n_qubits == s.n_qubits:
         # bind() result: the structure is prepared in the library once
         values = c.flat()[2]
-        _lib.check(_lib.lib().qsv_apply_prepared(s.handle, plan.program_id(), _lib.dptr(values),
-                                                 ctypes.byref(_last_stats)))
+        if basis is None:
+            _lib.check(L.qsv_apply_prepared(s.handle, plan.program_id(), _lib.dptr(values),
+                                            ctypes.byref(_last_stats)))
+        else:
+            _lib.check(L.qsv_evolve_basis_prepared(s.handle, basis, plan.program_id(),
+                                                   _lib.dptr(values), ctypes.byref(_last_stats)))
         return
     kinds, qubits, values = _flat(c)
-    _lib.check(_lib.lib().qsv_apply_gates(s.handle, len(kinds), _lib.i32ptr(kinds),
-                                          _lib.i32ptr(qubits), _lib.dptr(values),
-                                          ctypes.byref(_last_stats)))
+    if basis is None:
+        _lib.check(L.qsv_apply_gates(s.handle, len(kinds), _lib.i32ptr(kinds), _lib.i32ptr(qubits),
+                                     _lib.dptr(values), ctypes.byref(_last_stats)))
+    else:
+        _lib.check(L.qsv_evolve_basis(s.handle, basis, len(kinds), _lib.i32ptr(kinds),
+                                      _lib.i32ptr(qubits), _lib.dptr(values),
+                                      ctypes.byref(_last_stats)))
 
 
 def evolve(s: StateVector, c) -> StateVector:
@@ -281,11 +291,11 @@ def evolve(s: StateVector, c) -> StateVector:
     if not hasattr(c, "flat") and _id_cache_get(_FLAT_CACHE, c) is None and not c.is_bound():
         raise RuntimeError("circuit must be bound before evolution")
     out = StateVector._empty(s.n_qubits, s.device)
-    if s.basis_index is not None:
-        _lib.check(_lib.lib().qsv_set_basis(out.handle, s.basis_index))
+    if s.basis_index is not None:  # |index> is synthesised by the first pass
+        apply_circuit_inplace(out, c, s.basis_index)
     else:
         _lib.check(_lib.lib().qsv_copy(out.handle, s.handle))
-    apply_circuit_inplace(out, c)
+        apply_circuit_inplace(out, c)
     return out
 
 
