@@ -580,6 +580,30 @@ def run_engine_dist(args, rank, world, local):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
 
+    # UCC energy evals/s at P GPUs (BASELINE metric; config 4 sharded):
+    # every rank takes part; one warm-up evaluation (plans, specialisation)
+    extras = [e for e in (args.extra or "").split(",") if e and e != "none"]
+    ucc = None
+    if "ucc32" in extras:
+        nq = int(os.environ.get("QSV_BENCH_UCC_QUBITS", "32"))
+        cfg = W.config4(seed=0, n_qubits=nq, n_electrons=nq // 2)
+        s0 = be.prepare(cfg["reference"])
+        e = be.expectation(be.evolve(s0, cfg["circuit"]), cfg["hamiltonian"])
+        dist.barrier()
+        torch.cuda.synchronize(local)
+        t0 = time.perf_counter()
+        psi = be.evolve(s0, cfg["circuit"])
+        e = be.expectation(psi, cfg["hamiltonian"])  # returns a float: synchronised
+        rel, sent_u = psi.stats["relayouts"], psi.stats["relayout_bytes_sent"]
+        del psi
+        tu = torch.tensor([time.perf_counter() - t0], device=dev_t)
+        dist.all_reduce(tu, op=dist.ReduceOp.MAX)
+        ucc = {"workload": f"config4 construction at {nq}q (UCC rotations + 5,000-term H), "
+                           f"state sharded x{world}",
+               "metric": "energy evals/s", "value": 1.0 / float(tu.item()),
+               "s_per_eval": float(tu.item()), "energy": e, "relayouts": rel,
+               "relayout_bytes_sent_per_gpu": sent_u}
+
     peak, peak_kind = load_peaks()
     passes = None
     if rank == 0:
@@ -610,6 +634,8 @@ def run_engine_dist(args, rank, world, local):
             "gpu_launches": None,
             "clocks": clocks.summary(),
         }
+        if ucc is not None:
+            line["extra"] = {"ucc32_sharded": ucc}
         print(json.dumps(line), flush=True)
 
 
