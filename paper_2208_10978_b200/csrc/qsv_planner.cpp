@@ -1329,7 +1329,9 @@ Schedule pick_schedule(const std::vector<Item> &items, const std::vector<Rot> &R
     const int cost_cap = env_cap ? std::max(1, atoi(env_cap)) : 128;
     if (env && std::string(env) == "order") return schedule(items, R, n, m, c);
     if (items.size() > 20000) return schedule(items, R, n, m, c);  // O(N^2) conflict graph
-    Schedule L = schedule_lookahead(items, R, m, c, cost_cap, 512);
+    const char *env_win = getenv("QSV_SCHED_WINDOW");
+    const int window = env_win ? std::max(8, atoi(env_win)) : 512;
+    Schedule L = schedule_lookahead(items, R, m, c, cost_cap, window);
     if (env && std::string(env) == "lookahead") return L;
     Schedule O = schedule(items, R, n, m, c);
     return L.pass_items.size() < O.pass_items.size() ? L : O;
