@@ -488,3 +488,26 @@ def test_jit_fast_path_repeated_angles(jit_from_14):
         psi = sv.evolve(sv.init_state(ref), bind(param, theta))
         exp = O.evolve(O.init_state(ref), W.rotations_circuit(n, strings, theta).gates)
         assert np.abs(psi.amplitudes - exp).max() <= AMP_TOL
+
+
+def test_ucc_mirror_24q_two_contiguous_bits():
+    """24-qubit UCC-shaped circuit followed by its inverse returns to the HF
+    state (1e-10): rotation-dominated programs at n >= 22 are planned with 2
+    contiguous low qubits when that needs fewer HBM passes (pick_contig)."""
+    from paper_2208_10978_b200 import _lib
+
+    n, ne = 24, 12
+    rng = np.random.default_rng(24)
+    strings = W.ucc_rotation_strings(n, ne)[:400]
+    theta = rng.uniform(-0.5, 0.5, len(strings))
+    fwd = W.rotations_circuit(n, strings, theta)
+    back = W.rotations_circuit(n, strings[::-1], -theta[::-1])
+    circ = Circuit(n, fwd.gates + back.gates, 0)
+    kinds, qubits, values = sv._flat(fwd)
+    plan = _lib.debug_plan(n, kinds, qubits, values)
+    assert min(p["c"] for p in plan["passes"] if not p["global"]) == 2  # (tiles may extend it)
+    ref = W.hf_bitstring(ne, n)
+    out = sv.evolve(sv.init_state(ref), circ).amplitudes
+    expect = np.zeros(1 << n, dtype=np.complex128)
+    expect[O.init_state(ref).argmax()] = 1.0
+    assert np.abs(out - expect).max() <= AMP_TOL
