@@ -801,18 +801,93 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
     std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";
     char buf[512];
     int prev_h = -1;
-    for (size_t gi = 0; gi < sp.groups.size(); ++gi) {
+    // a component with <= kDirect strings skips its 8-point transform
+    // (24 adds) and sums each string's 8 products directly (7 adds)
+    const int kDirect = 3;
+    auto direct = [&](const GroupRec &G) {
+        return G.t_im - G.t0 <= kDirect && G.t1 - G.t_im <= kDirect;
+    };
+    // tile positions of pair bits 8..10 for highest flip bit H (ins0 skips H)
+    auto rpos = [](int H, int k) { return (8 + k) + ((8 + k) >= H ? 1 : 0); };
+    const char *env_share = getenv("QSV_SWEEP_SHARE");
+    const bool share = !(env_share && env_share[0] == '0');
+    auto sign_expr = [&](const TermRec &tr) {
+        snprintf(buf, sizeof(buf), "((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g",
+                 tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
+        return std::string(buf);
+    };
+    size_t gi = 0;
+    while (gi < sp.groups.size()) {
         const GroupRec &G = sp.groups[gi];
-        const bool need_re = G.t_im > G.t0, need_im = G.t1 > G.t_im;
         if (G.h != prev_h) {  // new run of groups with this highest flip bit
             if (prev_h >= 0) fn += "  }\n";
             snprintf(buf, sizeof(buf), "  { double2 X[8];\n    const u32 b0 = load_x<%d>(sm, pl, X);\n", G.h);
             fn += buf;
             prev_h = G.h;
         }
-        // a component with <= kDirect strings skips its 8-point transform
-        // (24 adds) and sums each string's 8 products directly (7 adds)
-        const int kDirect = 3;
+        if (share && direct(G)) {
+            // groups whose flips differ from G's only in the pair-bit positions
+            // 8..10 read a permutation of G's l1-side amplitudes: ONE load of
+            // y_j serves them all (member k uses pair j ^ d_k)
+            uint32_t R = 0;
+            for (int k = 0; k < 3; ++k) R |= 1u << rpos(G.h, k);
+            std::vector<std::pair<size_t, unsigned>> cls{{gi, 0u}};
+            size_t k = gi + 1;
+            while (k < sp.groups.size() && sp.groups[k].h == G.h && direct(sp.groups[k]) &&
+                   ((sp.groups[k].f_loc ^ G.f_loc) & ~R) == 0) {
+                const uint32_t D = sp.groups[k].f_loc ^ G.f_loc;
+                unsigned d = 0;
+                for (int q = 0; q < 3; ++q) d |= ((D >> rpos(G.h, q)) & 1u) << q;
+                cls.push_back({k, d});
+                ++k;
+            }
+            fn += "  {\n";
+            for (const auto &m : cls)
+                for (int t = sp.groups[m.first].t0; t < sp.groups[m.first].t1; ++t) {
+                    snprintf(buf, sizeof(buf), "    double s%d = 0.0;\n", t);
+                    fn += buf;
+                }
+            for (unsigned J = 0; J < 8; ++J) {
+                snprintf(buf, sizeof(buf),
+                         "    { const double2 y = sm[b0 ^ swz(ins0(%uu, %d)) ^ %uu];\n", 256u * J, G.h,
+                         h_swz(G.f_loc));
+                fn += buf;
+                for (size_t q = 0; q < cls.size(); ++q) {
+                    const GroupRec &M = sp.groups[cls[q].first];
+                    const unsigned jj = J ^ cls[q].second;
+                    if (M.t_im > M.t0) {
+                        snprintf(buf, sizeof(buf), "      const double r%zu = fma(X[%u].x, y.x, X[%u].y * y.y);\n",
+                                 q, jj, jj);
+                        fn += buf;
+                    }
+                    if (M.t1 > M.t_im) {
+                        snprintf(buf, sizeof(buf), "      const double i%zu = fma(X[%u].x, y.y, -X[%u].y * y.x);\n",
+                                 q, jj, jj);
+                        fn += buf;
+                    }
+                    for (int t = M.t0; t < M.t1; ++t) {
+                        const TermRec &tr = sp.terms[t];
+                        const unsigned msk = (tr.s_loc >> 8) & 7u;
+                        snprintf(buf, sizeof(buf), "      s%d %s= %c%zu;\n", t,
+                                 (__builtin_popcount(jj & msk) & 1) ? "-" : "+", tr.use_im ? 'i' : 'r', q);
+                        fn += buf;
+                    }
+                }
+                fn += "    }\n";
+            }
+            for (const auto &m : cls)
+                for (int t = sp.groups[m.first].t0; t < sp.groups[m.first].t1; ++t) {
+                    snprintf(buf, sizeof(buf), "    acc[%d] = fma(", t);
+                    fn += buf;
+                    fn += sign_expr(sp.terms[t]);
+                    snprintf(buf, sizeof(buf), ", s%d, acc[%d]);\n", t, t);
+                    fn += buf;
+                }
+            fn += "  }\n";
+            gi = k;
+            continue;
+        }
+        const bool need_re = G.t_im > G.t0, need_im = G.t1 > G.t_im;
         const bool w_re = G.t_im - G.t0 > kDirect, w_im = G.t1 - G.t_im > kDirect;
         snprintf(buf, sizeof(buf),
                  "  { double Wr[8], Wi[8];\n    wht8x<%s, %s, %s, %s, %d>(sm, b0, X, %uu, Wr, Wi);\n",
@@ -836,15 +911,15 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
                 val += ")";
             }
             // scale folded in: the term's sweep total is scale * sum_p sign(p) w_p
-            snprintf(buf, sizeof(buf),
-                     "    acc[%d] = fma(((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g, ",
-                     t, tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
+            snprintf(buf, sizeof(buf), "    acc[%d] = fma(", t);
             fn += buf;
-            fn += val;
+            fn += sign_expr(tr);
+            fn += ", " + val;
             snprintf(buf, sizeof(buf), ", acc[%d]);\n", t);
             fn += buf;
         }
         fn += "  }\n";
+        ++gi;
     }
     if (prev_h >= 0) fn += "  }\n";
     fn += "}\n";

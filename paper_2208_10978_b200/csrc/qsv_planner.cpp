@@ -1713,10 +1713,22 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
         if (m == kMaxTileBits) bank_interleave(sp.terms, sp.map, 0, sp.terms.size());
         // heavier groups first so the two warp halves stay balanced; with the
         // specialised layout, groups with the same highest flip bit adjacent
+        // specialised sweeps: within a run, flips that differ only in the
+        // tile positions of pair bits 8..10 adjacent (they share one load of
+        // the l1-side amplitudes, jit_sweep_source)
+        auto share_key = [&](int g) {
+            const uint32_t fl = compress(flips[g], sp.geom);
+            const int H = highest_bit(fl);
+            uint32_t R = 0;
+            for (int k = 0; k < 3; ++k) R |= 1u << ((8 + k) + ((8 + k) >= H ? 1 : 0));
+            return fl & ~R;
+        };
         std::stable_sort(bin.groups.begin(), bin.groups.end(), [&](int a, int b) {
             if (jit_layout) {
                 const int ha = highest_bit(flips[a]), hb = highest_bit(flips[b]);
                 if (ha != hb) return ha > hb;
+                const uint32_t ka = share_key(a), kb = share_key(b);
+                if (ka != kb) return ka < kb;
             }
             return members[a].size() > members[b].size();
         });
