@@ -271,7 +271,7 @@ Schedule schedule_lookahead(const std::vector<Item> &items, const std::vector<Ro
         int cands[64], nc = 0;
         for (int i = first; i < N && nc < nseeds && nc < 64; ++i)
             if (!done[i] && npend[i] == 0) cands[nc++] = i;
-        int start = cands[0];
+        int start = nc ? cands[0] : first;  // a DAG always has a ready item
         if (nc > 1 && popc64(items[start].req & ~low) <= free_slots) {
             long best_score = -1;
             for (int k = 0; k < nc; ++k) {
