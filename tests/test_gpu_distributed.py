@@ -122,3 +122,19 @@ def test_sharded_ucc_units_16q(D, P):
     e = be.expectation(psi, cfg["hamiltonian"])
     e_ref = O.expectation(ref, cfg["hamiltonian"], 16)
     assert abs(e - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
+
+
+def test_sharded_bound_circuit_from_bind(D):
+    """bind() results (BoundCircuit: arrays, lazily built gates) go through the
+    sharded path like reference Circuit objects."""
+    from paper_2208_10978_b200.circuit import bind
+
+    n, ne, P = 14, 6, 4
+    strings = W.ucc_rotation_strings(n, ne)[:120]
+    param = W.parametric_rotations_circuit(n, strings)
+    theta = np.random.default_rng(3).uniform(-0.4, 0.4, len(strings))
+    ref = W.hf_bitstring(ne, n)
+    be = D.DistributedBackend(D.LoopbackComm(P))
+    psi = be.evolve(be.prepare(ref), bind(param, theta))
+    exp = O.evolve(O.init_state(ref), W.rotations_circuit(n, strings, theta).gates)
+    assert np.abs(psi.amplitudes() - exp).max() < 1e-10
