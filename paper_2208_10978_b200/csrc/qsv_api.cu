@@ -897,9 +897,23 @@ int qsv_prepare_gates(int n_qubits, int64_t n_gates, const int32_t *kinds, const
     CacheEntry e;
     e.hash = 0;
     e.n = n_qubits;
-    e.kinds.assign(kinds, kinds + n_gates);
-    e.qubits.assign(qubits, qubits + 2 * n_gates);
-    if (n_gates > 0) plan_gates(n_qubits, n_gates, kinds, qubits, e.tpl);
+    // an identical structure already planned by qsv_apply_gates: copy its plan
+    // (and its specialised modules) instead of planning again
+    const uint64_t h = n_gates > 0 ? hash_structure(n_qubits, n_gates, kinds, qubits) : 0;
+    bool copied = false;
+    for (const CacheEntry &c : g_cache)
+        if (n_gates > 0 && c.hash == h && c.n == n_qubits && (int64_t)c.kinds.size() == n_gates &&
+            std::memcmp(c.kinds.data(), kinds, n_gates * 4) == 0 &&
+            std::memcmp(c.qubits.data(), qubits, n_gates * 8) == 0) {
+            e = c;
+            copied = true;
+            break;
+        }
+    if (!copied) {
+        e.kinds.assign(kinds, kinds + n_gates);
+        e.qubits.assign(qubits, qubits + 2 * n_gates);
+        if (n_gates > 0) plan_gates(n_qubits, n_gates, kinds, qubits, e.tpl);
+    }
     const int64_t id = g_next_program++;
     g_prepared.emplace(id, std::move(e));
     *program_id = id;

@@ -257,29 +257,68 @@ def _flat(c):
     return flat
 
 
+class _Program:
+    """A gate structure prepared in the library (qsv_prepare_gates) for one
+    circuit object: re-running that object skips the per-call lookup."""
+
+    __slots__ = ("n_qubits", "pid", "__weakref__")
+
+    def __init__(self, n_qubits: int, kinds, qubits):
+        pid = ctypes.c_int64()
+        _lib.check(_lib.lib().qsv_prepare_gates(n_qubits, len(kinds), _lib.i32ptr(kinds),
+                                                _lib.i32ptr(qubits), ctypes.byref(pid)))
+        self.n_qubits = n_qubits
+        self.pid = pid.value
+        weakref.finalize(self, _release_program, pid.value)
+
+    def program_id(self) -> int:
+        return self.pid
+
+
+def _release_program(pid: int) -> None:
+    L = _lib._lib
+    if L is not None:
+        L.qsv_release_program(pid)
+
+
+_PROG_CACHE: dict = {}
+
+
 def apply_circuit_inplace(s: StateVector, c, basis: Optional[int] = None) -> None:
     """Apply a bound circuit to s in place (the loop of statevector.py:72-73).
-    With basis: s is first set to |basis> (fused into the first pass)."""
+    With basis: s is first set to |basis> (fused into the first pass).  The
+    circuit's structure runs as a prepared program (bind() results carry
+    theirs; other circuit objects get one on first use); the values are read
+    from the circuit every call."""
     L = _lib.lib()
     plan = getattr(c, "_plan", None)
     if plan is not None and plan.n_qubits == s.n_qubits:
-        # bind() result: the structure is prepared in the library once
         values = c.flat()[2]
-        if basis is None:
-            _lib.check(L.qsv_apply_prepared(s.handle, plan.program_id(), _lib.dptr(values),
-                                            ctypes.byref(_last_stats)))
-        else:
-            _lib.check(L.qsv_evolve_basis_prepared(s.handle, basis, plan.program_id(),
-                                                   _lib.dptr(values), ctypes.byref(_last_stats)))
-        return
-    kinds, qubits, values = _flat(c)
-    if basis is None:
-        _lib.check(L.qsv_apply_gates(s.handle, len(kinds), _lib.i32ptr(kinds), _lib.i32ptr(qubits),
-                                     _lib.dptr(values), ctypes.byref(_last_stats)))
     else:
-        _lib.check(L.qsv_evolve_basis(s.handle, basis, len(kinds), _lib.i32ptr(kinds),
-                                      _lib.i32ptr(qubits), _lib.dptr(values),
-                                      ctypes.byref(_last_stats)))
+        kinds, qubits, values = _flat(c)
+        plan = _id_cache_get(_PROG_CACHE, c)
+        if not isinstance(plan, _Program) or plan.n_qubits != s.n_qubits:
+            if plan is None:
+                # first run of this object: the library's structure cache
+                # (shared by equal structures in different objects)
+                _id_cache_put(_PROG_CACHE, c, "seen", _FLAT_MAX)
+                if basis is None:
+                    _lib.check(L.qsv_apply_gates(s.handle, len(kinds), _lib.i32ptr(kinds),
+                                                 _lib.i32ptr(qubits), _lib.dptr(values),
+                                                 ctypes.byref(_last_stats)))
+                else:
+                    _lib.check(L.qsv_evolve_basis(s.handle, basis, len(kinds), _lib.i32ptr(kinds),
+                                                  _lib.i32ptr(qubits), _lib.dptr(values),
+                                                  ctypes.byref(_last_stats)))
+                return
+            plan = _Program(s.n_qubits, kinds, qubits)  # re-run: prepare (reuses the cached plan)
+            _id_cache_put(_PROG_CACHE, c, plan, _FLAT_MAX)
+    if basis is None:
+        _lib.check(L.qsv_apply_prepared(s.handle, plan.program_id(), _lib.dptr(values),
+                                        ctypes.byref(_last_stats)))
+    else:
+        _lib.check(L.qsv_evolve_basis_prepared(s.handle, basis, plan.program_id(),
+                                               _lib.dptr(values), ctypes.byref(_last_stats)))
 
 
 def evolve(s: StateVector, c) -> StateVector:
