@@ -213,7 +213,9 @@ def extra_ucc12(steps=20):
     cfg = W.config1(seed=0)
     be = engine.StateVectorBackend()
     s0 = be.prepare(cfg["reference"])
-    for _ in range(3):
+    # warm-up to steady state: plan, prepared program, specialised passes
+    # (compiled once a structure has run QSV_JIT_HOT_USES times)
+    for _ in range(6):
         be.expectation(be.evolve(s0, cfg["circuit"]), cfg["hamiltonian"])
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -226,7 +228,7 @@ def extra_ucc12(steps=20):
 
     param = W.parametric_rotations_circuit(cfg["n_qubits"], cfg["strings"])
     thetas = cfg["thetas"]
-    for _ in range(3):  # warm-up: the prepared program gets its specialised passes
+    for _ in range(6):  # warm-up: the prepared program gets its specialised passes
         e_b = be.expectation(be.evolve(s0, bind(param, thetas)), cfg["hamiltonian"])
     assert abs(e_b - e) <= 1e-12 * max(1.0, abs(e))
     t0 = time.perf_counter()
