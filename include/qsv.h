@@ -11,8 +11,11 @@
  *    index order -- the little-endian <c16 layout of dump_state
  *    (statevector.py:214-216).  Pin host buffers for full PCIe speed.
  *  - Device memory is owned by the handle; host pointers are borrowed for
- *    the duration of the call only.  All calls are ordered on the handle's
- *    CUDA stream; calls that return host values synchronise that stream.
+ *    the duration of the call only.  All work of all states on one device
+ *    is ordered on that device's library stream (qsv_get_stream): states
+ *    share the device's scratch, pinned staging buffer and specialised
+ *    kernels' __constant__ banks, so one stream per device is what keeps them
+ *    race-free.  Calls that return host values synchronise that stream.
  *  - Every call returns QSV_OK (0) or an error code; qsv_last_error() gives a
  *    thread-local message.  The Python layer maps codes to the reference's
  *    exception types (errors.py:9-22; ValueError / ArithmeticError).
@@ -57,13 +60,21 @@ typedef struct qsv_plan_stats {
 int qsv_abi_version(void);
 const char *qsv_last_error(void);
 int qsv_device_count(int *out);
+/* Free / total device memory (cudaMemGetInfo): lets callers reject a state
+ * that cannot fit before allocating it (statevector.py:47-50 rejects
+ * oversized states up front with ResourceLimitError). */
+int qsv_mem_info(int device, uint64_t *free_bytes, uint64_t *total_bytes);
 
 /* Handle lifetime.  qsv_create allocates 16 * 2^n bytes on `device` and
  * leaves the amplitudes uninitialised.  (StateVector, statevector.py:26-39) */
 int qsv_create(qsv_state **out, int n_qubits, int device);
 int qsv_destroy(qsv_state *s);
 int qsv_n_qubits(const qsv_state *s, int *out);
-int qsv_set_stream(qsv_state *s, void *cuda_stream); /* NULL -> library-owned stream */
+/* qsv_set_stream: order this state's later work after everything already
+ * queued on cuda_stream (an event fence; NULL = no-op).  Library work still
+ * runs on the device's library stream, returned by qsv_get_stream -- wait on
+ * it (e.g. torch.cuda.ExternalStream) before consuming qsv_device_ptr data. */
+int qsv_set_stream(qsv_state *s, void *cuda_stream);
 int qsv_get_stream(const qsv_state *s, void **cuda_stream);
 int qsv_device_ptr(const qsv_state *s, void **ptr);   /* zero-copy view (DLPack/torch) */
 int qsv_synchronize(qsv_state *s);

@@ -16,14 +16,22 @@
  * qubit k (statevector.py:1-6).  Gate matrices are row-major complex128
  * (statevector.py:58, np.ascontiguousarray).
  *
- * Single-threaded on purpose: the reference kernels are `with nogil` loops
- * with no prange (_cykernels.pyx:29, 58, 96).
+ * Single-threaded by default, like the reference kernels (`with nogil` loops
+ * with no prange, _cykernels.pyx:29, 58, 96).  oracle_set_threads(T) lets the
+ * parity TESTS split the gate / Pauli loops over T OpenMP threads: every pair
+ * (or output element) is still computed by exactly the arithmetic below, so
+ * results are bit-identical to the single-threaded run; only vdot's summation
+ * order is kept serial.
  */
 #include <complex.h>
 #include <stdint.h>
 #include <stddef.h>
 
 typedef double _Complex cplx;
+
+static int g_threads = 1;
+
+void oracle_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
 
 /* _cykernels.pyx:19-38 -- in-place 2x2 on pairs (i, i + 2^q). */
 void oracle_apply_1q(double *state_, int64_t dim, const double *matrix_, int qubit)
@@ -33,6 +41,17 @@ void oracle_apply_1q(double *state_, int64_t dim, const double *matrix_, int qub
     int64_t stride = (int64_t)1 << qubit;
     int64_t n_blocks = dim >> (qubit + 1);
     cplx m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+    if (g_threads > 1 && dim >= (1 << 16)) {
+        /* same pairs, enumerated by pair index k -> i0 = k with a 0 inserted at bit q */
+#pragma omp parallel for num_threads(g_threads) schedule(static)
+        for (int64_t k = 0; k < (dim >> 1); ++k) {
+            int64_t i0 = ((k >> qubit) << (qubit + 1)) | (k & (stride - 1)), i1 = i0 + stride;
+            cplx a = state[i0], b = state[i1];
+            state[i0] = m00 * a + m01 * b;
+            state[i1] = m10 * a + m11 * b;
+        }
+        return;
+    }
     for (int64_t blk = 0; blk < n_blocks; ++blk) {
         int64_t base = blk * (stride << 1);
         for (int64_t low = 0; low < stride; ++low) {
@@ -58,6 +77,7 @@ void oracle_apply_2q(double *state_, int64_t dim, const double *matrix_, int q0,
     cplx m[4][4];
     for (int r = 0; r < 4; ++r)
         for (int c = 0; c < 4; ++c) m[r][c] = mm[4 * r + c];
+#pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1 && dim >= (1 << 16))
     for (int64_t k = 0; k < (dim >> 2); ++k) {
         int64_t i = ((k >> lo) << (lo + 1)) | (k & mask_lo);
         i = ((i >> hi) << (hi + 1)) | (i & mask_hi);
@@ -80,6 +100,7 @@ void oracle_apply_pauli(const double *state_, int64_t dim, uint64_t x_mask, uint
     uint64_t sign_mask = y_mask | z_mask;
     int wy = __builtin_popcountll(y_mask) & 3;
     cplx phase = wy == 0 ? 1.0 : (wy == 1 ? I : (wy == 2 ? -1.0 : -I));
+#pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1 && dim >= (1 << 16))
     for (int64_t j = 0; j < dim; ++j) {
         uint64_t i = (uint64_t)j ^ flip;
         if (__builtin_popcountll(i & sign_mask) & 1)
@@ -132,6 +153,7 @@ void oracle_apply_operator(const double *state, int64_t dim, int64_t n_terms, co
     for (int64_t t = 0; t < n_terms; ++t) {
         cplx c = coef_re[t] + I * coef_im[t];
         oracle_apply_pauli(state, dim, x[t], y[t], z[t], scratch_);
+#pragma omp parallel for num_threads(g_threads) schedule(static) if (g_threads > 1 && dim >= (1 << 16))
         for (int64_t j = 0; j < dim; ++j) out[j] += c * scratch[j];
     }
 }

@@ -46,7 +46,7 @@ class PlanStats(ctypes.Structure):
 
 # Every symbol include/qsv.h declares (checked by tests/test_abi_cpu.py).
 EXPORTED = (
-    "qsv_abi_version", "qsv_last_error", "qsv_device_count", "qsv_create", "qsv_destroy",
+    "qsv_abi_version", "qsv_last_error", "qsv_device_count", "qsv_mem_info", "qsv_create", "qsv_destroy",
     "qsv_n_qubits", "qsv_set_stream", "qsv_get_stream", "qsv_device_ptr", "qsv_synchronize",
     "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_download_async",
     "qsv_download_wait", "qsv_apply_1q", "qsv_apply_2q",
@@ -70,6 +70,7 @@ def _declare(L):
         "qsv_abi_version": ([], ctypes.c_int),
         "qsv_last_error": ([], ctypes.c_char_p),
         "qsv_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "qsv_mem_info": ([ctypes.c_int, u64p, u64p], ctypes.c_int),
         "qsv_create": ([ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "qsv_destroy": ([vp], ctypes.c_int),
         "qsv_n_qubits": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),

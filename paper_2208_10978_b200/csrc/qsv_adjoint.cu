@@ -305,12 +305,12 @@ cudaError_t launch_rotation_adjoint(double2 *phi, double2 *lam, int n, int64_t R
     const uint64_t dim = 1ull << n;
     if (use_smem_kernel(n)) {
         const size_t smem = 32 * (size_t)dim;
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(adjoint_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 32 << 12);  // 2 x 4096 amplitudes
-            configured = true;
-        }
+        static PerDeviceOnce once;
+        cudaError_t e = once.run([] {
+            return cudaFuncSetAttribute(adjoint_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        32 << 12);  // 2 x 4096 amplitudes
+        });
+        if (e != cudaSuccess) return e;
         adjoint_smem_kernel<<<1, kSmemT, smem, st>>>(phi, lam, n, (int)R, X, Y, Z, cs, d_grad);
         return cudaGetLastError();
     }

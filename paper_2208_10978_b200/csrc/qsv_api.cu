@@ -70,13 +70,29 @@ int ctx_for(int device, DeviceCtx **out)
     return QSV_OK;
 }
 
+constexpr size_t kBigWork = (size_t)1 << 30;
+
+// Free a workspace that a large one-off request grew past 1 GiB, so a sample
+// of a big state does not pin tens of GiB for the rest of the process.
+int release_big_work(DeviceCtx &c, cudaStream_t st)
+{
+    if (c.d_bytes < kBigWork) return QSV_OK;
+    QSV_CUDA(cudaStreamSynchronize(st));
+    QSV_CUDA(cudaFree(c.d_work));
+    c.d_work = nullptr;
+    c.d_bytes = 0;
+    return QSV_OK;
+}
+
 int ensure_work(DeviceCtx &c, cudaStream_t st, size_t bytes)
 {
     if (c.d_bytes >= bytes) return QSV_OK;
     QSV_CUDA(cudaStreamSynchronize(st));
     if (c.d_work) QSV_CUDA(cudaFree(c.d_work));
     c.d_work = nullptr;
-    size_t want = std::max<size_t>(bytes + bytes / 2, (size_t)1 << 20);
+    // small requests grow with headroom; large ones (sampling a >= 27-qubit
+    // state) are allocated exactly and released after use (release_big_work)
+    size_t want = bytes >= kBigWork ? bytes : std::max<size_t>(bytes + bytes / 2, (size_t)1 << 20);
     if (cudaMalloc(&c.d_work, want) != cudaSuccess) {
         cudaGetLastError();
         c.d_bytes = 0;
@@ -218,10 +234,30 @@ bool fast_path(const qsv_state *s, const ProgramTemplate &t, const JitCache *jc,
            jit_enabled(s->n, uses);
 }
 
+// Planner / sweep knobs that change a plan: part of every cache key, so a
+// process that changes one (tests pin tile geometries this way) never reuses a
+// plan made under another setting.
+std::string planner_knobs()
+{
+    static const char *names[] = {"QSV_MIN_CONTIG", "QSV_FUSE_QUBITS", "QSV_PASS_PARAM_CAP",
+                                  "QSV_PASS_COST_CAP", "QSV_SCHED_SEEDS", "QSV_SCHED",
+                                  "QSV_SCHED_WINDOW", "QSV_PHASE_DEFER", "QSV_WARP_LOCAL",
+                                  "QSV_BLOCK_PARTITION", "QSV_INREG_PERMS", "QSV_SWEEP_TERMS",
+                                  "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS"};
+    std::string k;
+    for (const char *nm : names) {
+        const char *v = getenv(nm);
+        k += v ? v : "-";
+        k += '|';
+    }
+    return k;
+}
+
 // Cache of structural gate plans.
 struct CacheEntry {
     uint64_t hash;
     int n;
+    std::string knobs;
     std::vector<int32_t> kinds, qubits;
     ProgramTemplate tpl;
     int uses = 0;  // runs of this structure (hot programs get specialised passes)
@@ -233,6 +269,7 @@ constexpr size_t kCacheMax = 8;
 struct ExpCacheEntry {
     uint64_t hash;
     int n;
+    std::string knobs;
     bool jit = false;
     std::vector<std::string> jit_src;  // per sweep ("" = interpreted)
     std::vector<uint64_t> x, y, z;
@@ -618,6 +655,19 @@ int qsv_device_count(int *out)
     return QSV_OK;
 }
 
+int qsv_mem_info(int device, uint64_t *free_bytes, uint64_t *total_bytes)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!free_bytes || !total_bytes) return fail_code(QSV_ERR_INVALID, "null output");
+    if (device < 0 || device >= 64) return fail_code(QSV_ERR_INVALID, "device index out of range");
+    QSV_CUDA(cudaSetDevice(device));
+    size_t f = 0, t = 0;
+    QSV_CUDA(cudaMemGetInfo(&f, &t));
+    *free_bytes = f;
+    *total_bytes = t;
+    return QSV_OK;
+}
+
 int qsv_create(qsv_state **out, int n_qubits, int device)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);
@@ -667,13 +717,21 @@ int qsv_n_qubits(const qsv_state *s, int *out)
     return QSV_OK;
 }
 
+// Every state keeps the device's library stream (shared scratch, pinned
+// staging and __constant__ banks are ordered by it); a caller's stream is
+// joined by an event fence instead of replacing it.
 int qsv_set_stream(qsv_state *s, void *stream)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
     DeviceCtx *c = nullptr;
     if (int rc = ctx_for(s->device, &c)) return rc;
-    if (int rc = settle(s, true)) return rc;
-    s->stream = stream ? (cudaStream_t)stream : c->stream;
+    if (!stream || (cudaStream_t)stream == c->stream) return QSV_OK;
+    cudaEvent_t ev;
+    QSV_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    QSV_CUDA(cudaEventRecord(ev, (cudaStream_t)stream));
+    QSV_CUDA(cudaStreamWaitEvent(c->stream, ev, 0));
+    QSV_CUDA(cudaEventDestroy(ev));  // released once the wait has been satisfied
     return QSV_OK;
 }
 
@@ -686,6 +744,7 @@ int qsv_get_stream(const qsv_state *s, void **stream)
 
 int qsv_device_ptr(const qsv_state *s, void **ptr)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
     // the caller may write through the pointer: no copy may still be reading
     if (int rc = settle(const_cast<qsv_state *>(s), true)) return rc;
@@ -695,6 +754,7 @@ int qsv_device_ptr(const qsv_state *s, void **ptr)
 
 int qsv_synchronize(qsv_state *s)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
     QSV_CUDA(cudaSetDevice(s->device));
     QSV_CUDA(cudaStreamSynchronize(s->stream));
@@ -704,6 +764,7 @@ int qsv_synchronize(qsv_state *s)
 
 int qsv_copy(qsv_state *dst, const qsv_state *src)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(dst)) return rc;
     if (int rc = check_state(src)) return rc;
     if (dst->n != src->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
@@ -717,6 +778,7 @@ int qsv_copy(qsv_state *dst, const qsv_state *src)
 
 int qsv_set_basis(qsv_state *s, uint64_t index)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
     if (index >= s->dim) return fail_code(QSV_ERR_INVALID, "basis index out of range");
     QSV_CUDA(cudaSetDevice(s->device));
@@ -727,6 +789,7 @@ int qsv_set_basis(qsv_state *s, uint64_t index)
 
 int qsv_upload(qsv_state *s, const double *host)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
     if (!host) return fail_code(QSV_ERR_INVALID, "null host buffer");
     QSV_CUDA(cudaSetDevice(s->device));
@@ -738,6 +801,7 @@ int qsv_upload(qsv_state *s, const double *host)
 
 int qsv_download(const qsv_state *s, double *host)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
     if (!host) return fail_code(QSV_ERR_INVALID, "null host buffer");
     QSV_CUDA(cudaSetDevice(s->device));
@@ -766,6 +830,7 @@ int qsv_download_async(qsv_state *s, double *host)
 
 int qsv_download_wait(qsv_state *s)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(s)) return rc;
     QSV_CUDA(cudaSetDevice(s->device));
     return settle(s, true);
@@ -837,10 +902,12 @@ static int apply_gates_impl(qsv_state *s, int64_t n_gates, const int32_t *kinds,
     }
     QSV_CUDA(cudaSetDevice(s->device));
     const uint64_t h = hash_structure(s->n, n_gates, kinds, qubits);
+    const std::string knobs = planner_knobs();
     ProgramTemplate *tpl = nullptr;
     bool hit = false;
     for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
         if (it->hash == h && it->n == s->n && (int64_t)it->kinds.size() == n_gates &&
+            it->knobs == knobs &&
             std::memcmp(it->kinds.data(), kinds, n_gates * 4) == 0 &&
             std::memcmp(it->qubits.data(), qubits, n_gates * 8) == 0) {
             g_cache.splice(g_cache.begin(), g_cache, it);
@@ -856,6 +923,7 @@ static int apply_gates_impl(qsv_state *s, int64_t n_gates, const int32_t *kinds,
         CacheEntry e;
         e.hash = h;
         e.n = s->n;
+        e.knobs = knobs;
         e.kinds.assign(kinds, kinds + n_gates);
         e.qubits.assign(qubits, qubits + 2 * n_gates);
         plan_gates(s->n, n_gates, kinds, qubits, e.tpl);
@@ -1058,11 +1126,13 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
 
     const uint64_t h = hash_masks(s->n, S, x, y, z);
     const bool jit = jit_enabled(s->n);
+    const std::string knobs = planner_knobs();
     std::vector<SweepPlan> *plan = nullptr;
     std::vector<std::string> *jsrc = nullptr;
     bool hit = false;
     for (auto it = g_exp_cache.begin(); it != g_exp_cache.end(); ++it) {
         if (it->hash == h && it->n == s->n && it->jit == jit && (int64_t)it->x.size() == S &&
+            it->knobs == knobs &&
             std::memcmp(it->x.data(), x, S * 8) == 0 && std::memcmp(it->y.data(), y, S * 8) == 0 &&
             std::memcmp(it->z.data(), z, S * 8) == 0) {
             g_exp_cache.splice(g_exp_cache.begin(), g_exp_cache, it);
@@ -1076,6 +1146,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
         ExpCacheEntry e;
         e.hash = h;
         e.n = s->n;
+        e.knobs = knobs;
         e.x.assign(x, x + S);
         e.y.assign(y, y + S);
         e.z.assign(z, z + S);
@@ -1187,6 +1258,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
 
 int qsv_apply_pauli(const qsv_state *src, qsv_state *dst, uint64_t x, uint64_t y, uint64_t z)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(src)) return rc;
     if (int rc = check_state(dst)) return rc;
     if (src->n != dst->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
@@ -1202,6 +1274,7 @@ int qsv_apply_operator(const qsv_state *src, qsv_state *dst, int64_t S, const ui
                        const uint64_t *y, const uint64_t *z, const double *coef_re,
                        const double *coef_im)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(src)) return rc;
     if (int rc = check_state(dst)) return rc;
     if (src->n != dst->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
@@ -1218,7 +1291,6 @@ int qsv_apply_operator(const qsv_state *src, qsv_state *dst, int64_t S, const ui
     if (src->n <= 16 && S >= 4) {
         // small (L2-resident) state: one kernel over all strings instead of S
         // launches, same per-string arithmetic and order
-        std::lock_guard<std::recursive_mutex> lk(g_mu);
         DeviceCtx *c = nullptr;
         if (int rc = ctx_for(src->device, &c)) return rc;
         std::vector<uint64_t> fs(2 * S);
@@ -1337,6 +1409,7 @@ int qsv_rotation_adjoint(qsv_state *phi, qsv_state *lam, int64_t R, const uint64
 
 int qsv_axpby(qsv_state *y, const qsv_state *x, double are, double aim, double bre, double bim)
 {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (int rc = check_state(y)) return rc;
     if (int rc = check_state(x)) return rc;
     if (x->n != y->n) return fail_code(QSV_ERR_INVALID, "state qubit counts differ");
@@ -1546,7 +1619,7 @@ int qsv_sample_parity(const qsv_state *s, uint64_t support_mask, int64_t shots,
         QSV_CUDA(cudaMemcpy(outcomes, d_out, (size_t)shots * 8, cudaMemcpyDeviceToHost));
     // np.mean(1 - 2 parity): an exact integer sum, one rounding
     *out_mean = (double)(shots - 2 * (int64_t)odd) / (double)shots;
-    return QSV_OK;
+    return release_big_work(*c, s->stream);
 }
 
 int qsv_jit_info(int *available, int64_t *launches)

@@ -338,12 +338,12 @@ int expect_sweep_grid(const TileDims &g, int nterms, int ndiag, int ngroups, boo
 {
     int dev = 0;
     cudaGetDevice(&dev);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(expect_sweep2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
-        configured = true;
-    }
+    static PerDeviceOnce once;
+    cudaError_t ea = once.run([] {
+        return cudaFuncSetAttribute(expect_sweep2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024);
+    });
+    if (ea != cudaSuccess) return ea;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expect_sweep2_kernel, kT,
                                                       sweep2_smem(g, nterms, ndiag, wide)) != cudaSuccess)

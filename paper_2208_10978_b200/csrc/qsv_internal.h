@@ -9,10 +9,32 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
 namespace qsv {
+
+// One-time setup per device (kernel attributes such as the dynamic shared
+// memory cap are per device context): run(f) calls f once for the current
+// device, thread-safely, and again on a device that has not seen it yet.
+class PerDeviceOnce {
+    std::mutex mu_;
+    bool done_[64] = {};
+
+public:
+    template <class F>
+    cudaError_t run(F f)
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu_);
+        if (dev >= 0 && dev < 64 && done_[dev]) return cudaSuccess;
+        const cudaError_t e = f();
+        if (e == cudaSuccess && dev >= 0 && dev < 64) done_[dev] = true;
+        return e;
+    }
+};
 
 // Largest tile (in qubits) a CTA keeps resident in shared memory: 2^12
 // amplitudes x 16 B = 64 KiB, so three CTAs fit one SM's 228 KiB.

@@ -697,14 +697,13 @@ cudaError_t launch_tile_pass(double2 *psi, const TileDims &g, const uint64_t *d_
                              const int32_t *d_comp, const OpRec *d_ops, int nops,
                              const RotRec *d_rots, const double *d_params, cudaStream_t st)
 {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tile_pass_kernel<kTileThreads>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(((size_t)16 << kMaxTileBits) + 8192));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static PerDeviceOnce once;
+    cudaError_t ea = once.run([] {
+        return cudaFuncSetAttribute(tile_pass_kernel<kTileThreads>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(((size_t)16 << kMaxTileBits) + 8192));
+    });
+    if (ea != cudaSuccess) return ea;
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t smem = tile_smem_bytes(g);

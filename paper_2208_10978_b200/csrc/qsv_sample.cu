@@ -112,14 +112,16 @@ int grid_for(uint64_t n, int device)
 static inline size_t up256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 // Scratch layout (caller-provided device workspace of sample_scratch_bytes),
-// every part 256 B aligned: [p: 8*dim][cdf: 8*dim][denom, last, odd count][cub temp]
+// every part 256 B aligned: [p, scanned in place into the cdf: 8*dim]
+// [denom, last, odd count][cub temp] -- one 8-byte array per amplitude, so a
+// 32-qubit state needs 32 GiB of scratch, not 64.
 size_t sample_scratch_bytes(uint64_t dim)
 {
     size_t t1 = 0, t2 = 0;
     cub::DeviceReduce::Sum(nullptr, t1, (const double *)nullptr, (double *)nullptr, (int64_t)dim);
-    cub::DeviceScan::InclusiveSum(nullptr, t2, (const double *)nullptr, (double *)nullptr, (int64_t)dim);
+    cub::DeviceScan::InclusiveSum(nullptr, t2, (double *)nullptr, (double *)nullptr, (int64_t)dim);
     const size_t temp = t1 > t2 ? t1 : t2;
-    return 2 * up256(8 * dim) + 256 + up256(temp);
+    return up256(8 * dim) + 256 + up256(temp);
 }
 
 cudaError_t launch_sample_parity(const double2 *psi, uint64_t dim, int64_t shots, uint64_t k0,
@@ -130,12 +132,12 @@ cudaError_t launch_sample_parity(const double2 *psi, uint64_t dim, int64_t shots
     cudaGetDevice(&dev);
     char *base = (char *)scratch;
     double *p = (double *)base;
-    double *cdf = (double *)(base + up256(8 * dim));
-    double *denom = (double *)(base + 2 * up256(8 * dim));
+    double *cdf = p;  // inclusive scan in place (same additions in the same order)
+    double *denom = (double *)(base + up256(8 * dim));
     double *last = denom + 1;
     unsigned long long *odd = (unsigned long long *)(denom + 2);
-    void *temp = base + 2 * up256(8 * dim) + 256;
-    size_t temp_bytes = scratch_bytes - 2 * up256(8 * dim) - 256;
+    void *temp = base + up256(8 * dim) + 256;
+    size_t temp_bytes = scratch_bytes - up256(8 * dim) - 256;
     cudaError_t e;
     probs_kernel<<<grid_for(dim, dev), 256, 0, st>>>(psi, p, dim);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

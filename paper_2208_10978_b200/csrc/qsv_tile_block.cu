@@ -751,20 +751,19 @@ cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *
                                const OpRec *d_ops, int nops, const RotRec *d_rots, int nrots,
                                const double *d_params, int nparams, bool lite, cudaStream_t st)
 {
-    static bool configured = false;
+    static PerDeviceOnce once;
     const int max_smem = 227 * 1024;
-    if (!configured) {
+    cudaError_t ea = once.run([] {
         cudaError_t e = cudaFuncSetAttribute(tile_block_kernel<true, false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(tile_block_kernel<false, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(tile_block_kernel<true, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+        return cudaFuncSetAttribute(tile_block_kernel<true, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+    });
+    if (ea != cudaSuccess) return ea;
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t nhi = (size_t)1 << (g.m - g.c);
@@ -782,16 +781,15 @@ cudaError_t launch_tile_blocks(double2 *psi, const TileDims &g, const uint64_t *
     };
     static const char *env_ring = getenv("QSV_TILE_RING");  // 0: disable the ring kernel
     if (lite && g.m == kMaxTileBits && !(env_ring && env_ring[0] == '0')) {
-        static bool ring_configured = false;
-        if (!ring_configured) {
+        static PerDeviceOnce ring_once;
+        cudaError_t er = ring_once.run([] {
             cudaError_t e = cudaFuncSetAttribute(tile_ring_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             if (e != cudaSuccess) return e;
-            e = cudaFuncSetAttribute(tile_ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     max_smem);
-            if (e != cudaSuccess) return e;
-            ring_configured = true;
-        }
+            return cudaFuncSetAttribute(tile_ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024);
+        });
+        if (er != cudaSuccess) return er;
         const size_t rb = 256 + ((size_t)kStages * 16 << g.m) + 8 * (nhi + (nhi & 1));
         const bool rs = rb + prog_bytes <= (size_t)max_smem;
         const size_t smem = rs ? rb + prog_bytes : rb;

@@ -31,8 +31,11 @@ from .circuit import flatten_bound
 from .errors import ResourceLimitError
 from .pauli import term_arrays
 
-# One B200 holds 2^33 complex128 amplitudes (128 GiB) next to its workspace;
-# larger states need the multi-GPU path (distributed.py).
+# One B200 holds 2^33 complex128 amplitudes (128 GiB) next to its workspace:
+# enough for init_state -> evolve (|index> is synthesised in the output, no
+# copy) -> expectation at 33 qubits.  Calls that hold a second state (see
+# _alloc) need <= 32 qubits and raise ResourceLimitError, with the sizes, when
+# the second state does not fit.  Larger states: distributed.py.
 QUBIT_CAP = 33
 
 _POOL: dict[tuple[int, int], list[int]] = {}
@@ -45,8 +48,29 @@ def _alloc(n: int, device: int) -> int:
     if bucket:
         return bucket.pop()
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib().qsv_create(ctypes.byref(h), n, device))
+    try:
+        _lib.check(_lib.lib().qsv_create(ctypes.byref(h), n, device))
+    except ResourceLimitError:
+        release_pool()  # pooled buffers of other sizes may be what is in the way
+        try:
+            _lib.check(_lib.lib().qsv_create(ctypes.byref(h), n, device))
+        except ResourceLimitError as e:
+            free, total = mem_info(device)
+            raise ResourceLimitError(
+                f"a {n}-qubit state needs {(16 << n) / 2**30:.1f} GiB but device {device} has "
+                f"{free / 2**30:.1f} of {total / 2**30:.1f} GiB free; evolve of a non-basis "
+                f"state, copy(), apply_rotations, apply_operator, apply_pauli_string, sample and "
+                f"reverse_gradient each hold a second state (one B200 fits one 33-qubit state, "
+                f"or two 32-qubit states); larger problems shard over GPUs (distributed.py)"
+            ) from e
     return h.value
+
+
+def mem_info(device: int = 0) -> tuple[int, int]:
+    """(free, total) device memory in bytes."""
+    f, t = ctypes.c_uint64(), ctypes.c_uint64()
+    _lib.check(_lib.lib().qsv_mem_info(device, ctypes.byref(f), ctypes.byref(t)))
+    return f.value, t.value
 
 
 def _release(n: int, device: int, h: int) -> None:
@@ -236,13 +260,22 @@ def _id_cache_get(cache: dict, obj):
 
 
 def _id_cache_put(cache: dict, obj, value, limit: int) -> None:
+    key = id(obj)
+
+    def _drop(r, cache=cache, key=key):
+        # the object died: drop its entry (and with it a prepared program's
+        # library-side plan) now instead of at FIFO eviction
+        hit = cache.get(key)
+        if hit is not None and hit[0] is r:
+            del cache[key]
+
     try:
-        ref = weakref.ref(obj)
+        ref = weakref.ref(obj, _drop)
     except TypeError:
         return
     if len(cache) >= limit:
         cache.pop(next(iter(cache)))
-    cache[id(obj)] = (ref, value)
+    cache[key] = (ref, value)
 
 
 def _flat(c):

@@ -13,6 +13,11 @@ GOLDEN = os.path.join(REPO, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built libqsv.so")
+    # the C oracle's gate loops may use every host core in the parity tests
+    # (bit-identical to one thread: same per-pair arithmetic)
+    from oracle import oracle as O
+
+    O.set_threads(min(32, os.cpu_count() or 1))
 
 
 @pytest.fixture(scope="session")
