@@ -41,10 +41,54 @@ sys.path.insert(0, REPO)
 N_QUBITS = 28
 LAYERS = 20
 SEED = 0
-REF_SAMPLE_GATES = 6  # reference arm: first gates of the circuit per step (~1.2-2.5 s each)
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2
 # dram__bytes_read.sum + dram__bytes_write.sum of one config-2 pass (ncu --set full, r01)
 TRAFFIC_PER_LAUNCH = 4.295412e9 + 4.238421e9
+
+
+def load_fp64_peak() -> tuple[float, str]:
+    """Measured DFMA/s of this B200 (tools/peaks_probe.cu -> profiles/r02_peaks_probe.json);
+    fallback: 148 SMs x 64 DFMA/clk x 1.965 GHz."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r02_peaks_probe.json")) as fh:
+            return float(json.load(fh)["dfma_per_s"]), "measured (tools/peaks_probe.cu)"
+    except Exception:
+        return 148 * 64 * 1.965e9, "nominal 148 x 64 DFMA/clk x 1.965 GHz"
+
+
+def load_fp64_counts() -> dict | None:
+    """FP64-pipe instructions (thread level) the specialised passes of one
+    config-2 step execute, from ncu (smsp__sass_thread_inst_executed_op_
+    {dfma,dmul,dadd}_pred_on.sum over the step's launches): a property of the
+    compiled plan, so it is measured once per build and timed live here."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r02_fp64_counts.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+def fp64_roofline(t_step: float, passes: int, nominal_dfma: int, hbm: dict) -> dict:
+    """The config-2 step is FP64-bound: achieved FP64 TFLOP/s (DFMA = 2 flop,
+    DMUL / DADD = 1) of the instructions actually executed, against the
+    measured DFMA peak; the HBM view rides along."""
+    peak_dfma, src = load_fp64_peak()
+    counts = load_fp64_counts()
+    out = {"bound": "fp64", "unit": "TFLOP/s", "peak": 2 * peak_dfma / 1e12, "peak_source": src,
+           "kernel": "qsv_pass (NVRTC-specialised tile pass)", "traffic": hbm["traffic"],
+           "nominal_dfma_per_step": nominal_dfma,
+           "nominal_note": "8 DFMA per amplitude per dense 2x2 complex gate (SURVEY 8(d)); the "
+                           "kernels issue fewer (real m00, phase deferral)",
+           "hbm": hbm}
+    if counts and counts.get("passes") == passes:
+        flops = 2 * counts["dfma"] + counts["dmul"] + counts["dadd"]
+        inst = counts["dfma"] + counts["dmul"] + counts["dadd"]
+        out.update({"achieved": flops / t_step / 1e12, "frac": flops / t_step / 1e12 / out["peak"],
+                    "fp64_pipe_frac": inst / t_step / peak_dfma,
+                    "fp64_inst_per_step": counts, "counts_source": counts.get("source")})
+    else:
+        out.update({"achieved": None, "frac": None,
+                    "counts_source": "missing or stale profiles/r02_fp64_counts.json"})
+    return out
 
 
 def load_peaks() -> tuple[float, str]:
@@ -137,61 +181,211 @@ def _reference_modules():
     return "port", None, None
 
 
-def cpu_sample_run(circuit, n_gates: int):
-    """Time the reference evolve of the first n_gates gates on a 2^n state.
-    Returns (seconds, kind, description)."""
+def host_info(workers: int | None = None) -> dict:
+    """Cores, CPU model, RAM (and W) recorded beside every CPU number
+    (BASELINE.md 3)."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    ram = None
+    try:
+        import psutil
+
+        ram = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        pass
+    d = {"os_cpu_count": os.cpu_count(), "cpu_model": model, "ram_gib": ram}
+    if workers is not None:
+        d["workers"] = workers
+    return d
+
+
+def _avail_ram() -> int:
+    try:
+        import psutil
+
+        return int(psutil.virtual_memory().available)
+    except Exception:
+        return 16 << 30
+
+
+def ref_sample_gates(circuit, step: int, worker: int):
+    """Gates of one reference-arm step: 2 U3 + 1 CNOT (the circuit's 560:270
+    mix), taken at positions that rotate with the step and the worker so the
+    sample walks the whole circuit."""
+    u3 = [g for g in circuit.gates if g.kind == "U3"]
+    cx = [g for g in circuit.gates if g.kind == "CNOT"]
+    k = 37 * worker + 3 * step
+    return [u3[(2 * k) % len(u3)], u3[(2 * k + 1) % len(u3)], cx[k % len(cx)]]
+
+
+def _ref_gate_worker(wid, n, steps, barrier, out_q):
+    """One reference worker: its own 2^n state; each step applies the sample
+    gates with the reference's own per-gate routine (statevector._apply_gate,
+    statevector.py:57-62 -- the body of evolve's loop, Cython kernels)."""
     import numpy as np
 
-    kind, RC, RSV = _reference_modules()
-    n = circuit.n_qubits
-    gates = circuit.gates[:n_gates]
-    if kind == "reference":
-        rgates = tuple(RC.Gate(g.kind, g.qubits, tuple(RC.Constant(p.value) for p in g.params))
-                       for g in gates)
-        rc = RC.Circuit(n, rgates, 0)
-        amps = np.zeros(1 << n, dtype=np.complex128)
-        amps[0] = 1.0
-        s0 = RSV.StateVector(n, amps)
-        t0 = time.perf_counter()
-        RSV.evolve(s0, rc)  # includes the reference's own state copy (statevector.py:71)
-        dt = time.perf_counter() - t0
-        desc = (f"first {n_gates} of {len(circuit.gates)} gates of the {n}q brickwork via "
-                "vqekit.statevector.evolve (oracle/_ref, Cython kernels, 1 thread)")
-        return dt, kind, desc
-    from oracle import oracle as O
+    from paper_2208_10978_b200 import workloads as W
 
+    _, RC, RSV = _reference_modules()
+    circ = W.brickwork(n, LAYERS, SEED)
     amps = np.zeros(1 << n, dtype=np.complex128)
     amps[0] = 1.0
+    times = []
+    for k in range(steps):
+        gates = ref_sample_gates(circ, k, wid)
+        barrier.wait()
+        t0 = time.perf_counter()
+        for g in gates:
+            RSV._apply_gate(amps, g.kind, tuple(g.qubits), tuple(p.value for p in g.params))
+        t1 = time.perf_counter()
+        barrier.wait()
+        times.append((t0, t1))
+    out_q.put((wid, times))
+
+
+def reference_gate_throughput(n: int, steps: int, warmup: int, workers: int | None = None) -> dict:
+    """The reference's own CPU gate loop on the config-2 circuit family, with
+    all the host cores it can use: the reference evolve is single-threaded
+    (no prange in _cykernels.pyx), so W independent worker processes each
+    run the sample on their own 2^n state, concurrently (barrier per step).
+    Step time = latest finish - earliest start over the workers."""
+    import multiprocessing as mp
+
+    kind, _, _ = _reference_modules()
+    if kind != "reference":
+        raise RuntimeError("oracle/_ref (the reference build) is missing")
+    if workers is None:
+        by_ram = max(1, (_avail_ram() - (8 << 30)) // (16 << n))  # 1 state + headroom each
+        workers = int(max(1, min(os.cpu_count() or 1, by_ram)))
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(workers)
+    q = ctx.Queue()
+    total = warmup + steps
+    procs = [ctx.Process(target=_ref_gate_worker, args=(w, n, total, barrier, q)) for w in range(workers)]
+    for p in procs:
+        p.start()
+    res = dict(q.get() for _ in procs)
+    for p in procs:
+        p.join()
+    per_step = []
+    for k in range(warmup, total):
+        t0 = min(res[w][k][0] for w in res)
+        t1 = max(res[w][k][1] for w in res)
+        per_step.append(t1 - t0)
+    t = sum(per_step) / len(per_step)
+    value = workers * 3 * (1 << n) / t
+    return {"value": value, "unit": "amplitude-updates/s", "cores": workers, "kind": "reference",
+            "seconds_per_step": t,
+            "sample": (f"{workers} worker processes x (2 U3 + 1 CNOT of the {n}q depth-{LAYERS} "
+                       f"brickwork, rotating through all 830 gates) per step via "
+                       f"vqekit.statevector._apply_gate (oracle/_ref, Cython kernels; evolve's "
+                       f"single 16*2^n-byte state copy per circuit excluded)"),
+            "host": host_info(workers)}
+
+
+def reference_ucc12(evals: int = 3) -> dict:
+    """Config 1 in full on the reference: evolve + expectation through its own
+    StateVectorBackend (engine.py:59-75; 1 core -- evolve is single-threaded
+    and the backend's expectation is the serial statevector.expectation)."""
+    _, RC, RSV = _reference_modules()
+    import vqekit.engine as RE
+    import vqekit.pauli as RP
+
+    from paper_2208_10978_b200 import workloads as W
+
+    cfg = W.config1(seed=0)
+    n = cfg["n_qubits"]
+    rgates = tuple(RC.Gate(g.kind, g.qubits, tuple(RC.Constant(p.value) for p in g.params))
+                   for g in cfg["circuit"].gates)
+    circ = RC.Circuit(n, rgates, 0)
+    terms = []
+    for t in cfg["hamiltonian"].terms:
+        terms.append(RP.PauliTerm(complex(t.coefficient),
+                                  RP.PauliString(tuple(t.string.factors))))
+    h = RP.PauliSum(tuple(terms))
+    be = RE.StateVectorBackend()
+    s0 = be.prepare(cfg["reference"])
+    e = be.expectation(be.evolve(s0, circ), h)  # warm
     t0 = time.perf_counter()
-    O.evolve(amps, gates)
-    dt = time.perf_counter() - t0
-    return dt, "port", f"first {n_gates} gates via oracle/oracle.c (C restatement, 1 thread)"
+    for _ in range(evals):
+        e = be.expectation(be.evolve(s0, circ), h)
+    dt = (time.perf_counter() - t0) / evals
+    return {"value": 1.0 / dt, "unit": "energy evals/s", "cores": 1, "kind": "reference",
+            "energy": e, "s_per_eval": dt,
+            "sample": f"config 1 in full ({len(rgates)} gates + 500 strings), {evals} evaluations "
+                      "through vqekit.engine.StateVectorBackend (1 thread)",
+            "host": host_info(1)}
+
+
+def reference_expect30(workers: int | None = None) -> dict:
+    """Config 3 (30 q, 10,000 strings) on the reference, extrapolated from a
+    stratified sample: one string per worker (first half Z-only, the rest
+    with flips, from the config-3 Hamiltonian) measured through the
+    reference's own expectation_parallel (fork pool, OPENBLAS_NUM_THREADS=1,
+    engine.py:177-199) on the config-3 state; time per string per worker x
+    10,000 / W = the extrapolated full expectation."""
+    import numpy as np
+
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    _, RC, RSV = _reference_modules()
+    import vqekit.engine as RE
+    import vqekit.pauli as RP
+
+    from paper_2208_10978_b200 import workloads as W
+
+    n = 30
+    if workers is None:
+        by_ram = (_avail_ram() - (24 << 30)) // (16 << n)  # state + one scratch per worker
+        workers = int(max(1, min(os.cpu_count() or 1, by_ram)))
+    h = W.config3_hamiltonian(seed=0)
+    zs = [t for t in h.terms if all(a == "Z" for _, a in t.string.factors)]
+    fl = [t for t in h.terms if not all(a == "Z" for _, a in t.string.factors)]
+    pick = zs[: workers // 2] + fl[: workers - workers // 2]
+    terms = tuple(RP.PauliTerm(complex(t.coefficient), RP.PauliString(tuple(t.string.factors)))
+                  for t in pick)
+    hs = RP.PauliSum(terms)
+    amps = W.config3_state(seed=0)
+    st = RSV.StateVector(n, amps)
+    plan = RE.plan_partition(hs, workers)
+    old = RE._PARALLEL_MIN_TERMS
+    RE._PARALLEL_MIN_TERMS = 1  # a W-string sample must still take the fork-pool path
+    try:
+        t0 = time.perf_counter()
+        RE.expectation_parallel(st, hs, plan)
+        dt = time.perf_counter() - t0
+    finally:
+        RE._PARALLEL_MIN_TERMS = old
+    per_string = dt  # each worker measured one string in dt (wall, incl. fork)
+    full = per_string * len(h.terms) / workers
+    return {"value": 1.0 / full, "unit": "expectations/s", "cores": workers, "kind": "reference",
+            "s_per_eval_extrapolated": full, "sample_seconds": dt, "extrapolated": True,
+            "sample": f"{len(pick)} strings ({workers // 2} Z-only + {workers - workers // 2} "
+                      "with flips) of the config-3 H, one per worker, via "
+                      "vqekit.engine.expectation_parallel (fork pool, OPENBLAS_NUM_THREADS=1) "
+                      "on the config-3 state; x 10,000 / W",
+            "host": host_info(workers)}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from paper_2208_10978_b200 import workloads as W
-
-    circ = W.brickwork(N_QUBITS, LAYERS, SEED)
-    for _ in range(args.warmup):
-        cpu_sample_run(circ, REF_SAMPLE_GATES)
-    times = []
-    kind = desc = None
-    for _ in range(args.steps):
-        dt, kind, desc = cpu_sample_run(circ, REF_SAMPLE_GATES)
-        times.append(dt)
-    per = sum(times) / len(times)
-    value = REF_SAMPLE_GATES * (1 << N_QUBITS) / per
+    r = reference_gate_throughput(N_QUBITS, args.steps, args.warmup)
+    value = r["value"]
     line = {
         "impl": "reference", "metric": "amplitude-updates/s", "value": value,
         "unit": "amplitude-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c128", "data": "synthetic",
+        "ms_per_step": r["seconds_per_step"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": "config2: 28q random brickwork depth 20 (830 gates), seed 0",
-                   "sample": f"first {REF_SAMPLE_GATES} gates per step"},
-        "cpu_baseline": {"value": value, "unit": "amplitude-updates/s", "cores": 1, "kind": kind,
-                         "sample": desc},
+                   "sample": "2 U3 + 1 CNOT per worker per step"},
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "host")},
         "e2e": {"value": value, "unit": "amplitude-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -344,6 +538,7 @@ def extra_ucc32(steps=1):
     gbs = (st_ev["n_passes"] * 32.0 - 16.0) * (1 << 32) / t_ev / 1e9  # first pass: write only
     return {"workload": "config4: 32q UCC (16,512 rotations) + 5,000-term H",
             "metric": "energy evals/s", "value": 1.0 / dt, "s_per_eval": dt, "energy": e,
+            "decomposed_gates": len(cfg["circuit"].gates),
             "evolve_passes": st_ev["n_passes"], "s_per_evolve": t_ev, "evolve_hbm_gbs": gbs,
             "evolve_hbm_frac": gbs / peak}
 
@@ -461,20 +656,14 @@ def run_engine(args, rank, world, local):
                 "d2h_bytes_per_step": 16 * dim, "ms_per_step": t_e2e * 1e3, "steps": e2e_steps,
                 "note": "StateVector.download_async: step k's 4 GiB D2H overlaps step k+1's "
                         "evolve; timed until the last download completes"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": TRAFFIC_PER_LAUNCH,
-                     "kernel": "qsv_pass (NVRTC-specialised tile pass)",
-                     "ms_per_launch": t_pass * 1e3, "peak_source": peak_kind,
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "traffic_source": "ncu dram__bytes_read+write of one pass (profiles/r01_jit_pass_ncu.txt)",
-                     "note": "each pass carries up to 64 dense 2x2 gates and is FP64-bound, "
-                             "not HBM-bound: see the fp64 key for the binding roofline"},
-        # the pass is FP64-bound as much as HBM-bound: 560 dense 2x2 complex
-        # gates x 2^28 amplitudes x 8 real FMAs = 1.2e12 DFMA per step
-        "fp64": {"dfma_per_step": n_u1 * dim * 8, "achieved_tflops": 2 * n_u1 * dim * 8 / t_step / 1e12,
-                 "peak_tflops": FP64_PEAK_TFLOPS,
-                 "frac": 2 * n_u1 * dim * 8 / t_step / 1e12 / FP64_PEAK_TFLOPS,
-                 "peak_source": "148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200 FP64 vector)"},
+        "roofline": fp64_roofline(t_step, passes, n_u1 * dim * 8,
+                                  {"achieved": achieved, "peak": peak, "unit": "GB/s",
+                                   "frac": achieved / peak, "peak_source": peak_kind,
+                                   "algorithmic_bytes_per_launch": alg_bytes,
+                                   "ms_per_launch": t_pass * 1e3,
+                                   "traffic": TRAFFIC_PER_LAUNCH,
+                                   "traffic_source": "ncu dram__bytes_read+write of one pass "
+                                                     "(profiles/r01_jit_pass_ncu.txt)"}),
         # specialised pass launches counted by the library over the timed
         # region (the evolve from |0..0> needs no separate set_basis kernel)
         "gpu_launches": int(jit_after - jit_before),
@@ -493,9 +682,40 @@ def run_engine(args, rank, world, local):
                 line["extra"][e] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dt, kind, desc = cpu_sample_run(circ, REF_SAMPLE_GATES)
-        line["cpu_baseline"] = {"value": REF_SAMPLE_GATES * dim / dt, "unit": "amplitude-updates/s",
-                                "cores": 1, "kind": kind, "sample": desc, "seconds": dt}
+        # the reference's own gate loop on all host cores, 2 steps (~20 s)
+        try:
+            r = reference_gate_throughput(N_QUBITS, steps=2, warmup=0)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                      "host", "seconds_per_step")}
+        except Exception as exc:
+            line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        ex = line.get("extra", {})
+        cpu_legs = {"ucc12": reference_ucc12, "expect30": reference_expect30}
+        for name, fn in cpu_legs.items():
+            if name in ex and "error" not in ex[name]:
+                try:
+                    ex[name]["cpu_reference"] = fn()
+                    ex[name]["vs_cpu_reference"] = ex[name]["value"] / ex[name]["cpu_reference"]["value"]
+                except Exception as exc:
+                    ex[name]["cpu_reference"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        if "ucc32" in ex and "error" not in ex["ucc32"] and "value" in line.get("cpu_baseline", {}):
+            # config 4 cannot run on the CPU (64 GiB state + copy, ~5e5 gates):
+            # per-core gate rate at 28 q x the decomposed gate count at 32 q,
+            # plus 5,000 strings at the per-string cost of the config-3 sample x 4
+            cb = line["cpu_baseline"]
+            per_core = cb["value"] / cb["cores"]
+            gates32 = ex["ucc32"].get("decomposed_gates", 0)
+            t_ev = gates32 * float(1 << 32) / per_core
+            e30 = ex.get("expect30", {}).get("cpu_reference", {})
+            t_h = (e30["s_per_eval_extrapolated"] * e30["cores"] / 10_000 * 4 * 5_000
+                   if "s_per_eval_extrapolated" in e30 else 0.0)
+            ex["ucc32"]["cpu_reference"] = {
+                "kind": "reference", "extrapolated": True, "cores": 1,
+                "s_per_eval_extrapolated": t_ev + t_h, "value": 1.0 / (t_ev + t_h),
+                "unit": "energy evals/s",
+                "sample": "evolve: decomposed gates x 2^32 / the reference's per-core gate rate "
+                          "(cpu_baseline); H: 5,000 x the config-3 per-string time x 4 (1 core)"}
+            ex["ucc32"]["vs_cpu_reference"] = ex["ucc32"]["value"] * (t_ev + t_h)
     if rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -355,30 +355,74 @@ def rotation_circuit(n_qubits: int, rotations: Iterable[tuple[object, float]]) -
 # ---------------------------------------------------------------------------
 
 
+class _FlatStructure:
+    """Flattened structure of a gate list (kinds, qubits, parameter slots),
+    kept so a fresh circuit object with the same structure -- what the
+    reference's bind() returns every evaluation (engine.py:457) -- only needs
+    its parameter values pulled."""
+
+    __slots__ = ("kind_list", "qubit_list", "kinds", "qubits", "slots", "n_values")
+
+    def __init__(self, kind_list, qubit_list, param_counts):
+        G = len(kind_list)
+        codes = _lib.KIND_CODES
+        self.kind_list, self.qubit_list = kind_list, qubit_list
+        self.kinds = np.fromiter((codes[k] for k in kind_list), dtype=np.int32, count=G)
+        q = np.full(2 * G, -1, dtype=np.int32)
+        q0 = np.fromiter((qs[0] for qs in qubit_list), dtype=np.int32, count=G)
+        q1 = np.fromiter((qs[1] if len(qs) == 2 else -1 for qs in qubit_list), dtype=np.int32, count=G)
+        q[0::2], q[1::2] = q0, q1
+        self.qubits = q
+        pc = np.asarray(param_counts, dtype=np.int64)
+        gate_of = np.repeat(np.arange(G, dtype=np.int64), pc)
+        first = np.repeat(np.cumsum(pc) - pc, pc)
+        self.slots = 3 * gate_of + (np.arange(len(gate_of), dtype=np.int64) - first)
+        self.n_values = 3 * G
+
+
+_FLAT_STRUCTS: list = []  # most recent first
+
+
+def _unbound() -> RuntimeError:
+    return RuntimeError("circuit must be bound before evolution")
+
+
 def flatten_bound(c) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
-    """Bound circuit -> (kinds int32[G], qubits int32[2G], values float64[3G])."""
+    """Bound circuit -> (kinds int32[G], qubits int32[2G], values float64[3G]).
+    Raises RuntimeError (statevector.py:69-70) if a parameter is unbound.
+
+    The gate walk is three list comprehensions (kinds, qubits, parameter
+    values): a structure seen before is recognised by list equality and its
+    arrays reused; only the values are scattered into place."""
     if isinstance(c, BoundCircuit):
         return c.flat()
     gates = c.gates
-    G = len(gates)
-    codes = _lib.KIND_CODES
-    kinds = np.empty(G, dtype=np.int32)
-    qubits = np.full(2 * G, -1, dtype=np.int32)
-    values = np.zeros(3 * G, dtype=np.float64)
-    for i, g in enumerate(gates):
-        kinds[i] = codes[g.kind]
-        qs = g.qubits
-        qubits[2 * i] = qs[0]
-        if len(qs) == 2:
-            qubits[2 * i + 1] = qs[1]
-        ps = g.params
-        if ps:
-            for k, p in enumerate(ps):
-                v = getattr(p, "value", None)
-                if v is None:
-                    raise RuntimeError(f"gate {g.kind} has unbound parameters")
-                values[3 * i + k] = v
-    return kinds, qubits, values
+    kind_list = [g.kind for g in gates]
+    qubit_list = [g.qubits for g in gates]
+    try:
+        pv = [p.value for g in gates for p in g.params]
+    except AttributeError:
+        raise _unbound() from None
+    st = None
+    for k, cand in enumerate(_FLAT_STRUCTS):
+        if cand.kind_list == kind_list and cand.qubit_list == qubit_list:
+            st = cand
+            if k:
+                _FLAT_STRUCTS.insert(0, _FLAT_STRUCTS.pop(k))
+            break
+    if st is None:
+        st = _FlatStructure(kind_list, qubit_list, [len(g.params) for g in gates])
+        _FLAT_STRUCTS.insert(0, st)
+        del _FLAT_STRUCTS[4:]
+    values = np.zeros(st.n_values, dtype=np.float64)
+    if pv:
+        if len(pv) != len(st.slots):
+            st = _FlatStructure(kind_list, qubit_list, [len(g.params) for g in gates])
+        try:
+            values[st.slots] = pv
+        except (TypeError, ValueError):
+            raise _unbound() from None
+    return st.kinds, st.qubits, values
 
 
 def _expr_json(e) -> dict:

@@ -358,10 +358,9 @@ def evolve(s: StateVector, c) -> StateVector:
     """Apply a bound circuit; returns a new state (statevector.py:65-74)."""
     if c.n_qubits != s.n_qubits:
         raise ValueError("circuit and state qubit counts differ")
-    # a circuit already in the flatten cache is known to be bound (walking
-    # 37k gates for is_bound() costs ~6 ms per energy evaluation at config 1)
-    if not hasattr(c, "flat") and _id_cache_get(_FLAT_CACHE, c) is None and not c.is_bound():
-        raise RuntimeError("circuit must be bound before evolution")
+    # boundness (statevector.py:69-70) is checked by the flattening itself
+    # (RuntimeError on an unbound parameter), before any device work
+    _flat(c)
     out = StateVector._empty(s.n_qubits, s.device)
     if s.basis_index is not None:  # |index> is synthesised by the first pass
         apply_circuit_inplace(out, c, s.basis_index)
@@ -573,7 +572,7 @@ def reverse_gradient_general(c, theta, apply_h, s0: StateVector) -> np.ndarray:
     commuting, i.e. 2 Re <psi_l|dU|psi_before> = Im <U^dag psi_l| P |psi_before>:
     one apply_pauli + one vdot instead of a copy, a derivative pass and a vdot.
     """
-    from .circuit import Affine, Circuit, bind, dagger_gate, gate_derivative
+    from .circuit import Circuit, bind, dagger_gate, gate_derivative
     from . import kernels
 
     theta = np.asarray(theta, dtype=float)
@@ -607,7 +606,8 @@ def reverse_gradient_general(c, theta, apply_h, s0: StateVector) -> np.ndarray:
             pend.clear()
 
     for gate, bg in zip(reversed(c.gates), reversed(bound.gates)):
-        slots = [(k, e) for k, e in enumerate(gate.params) if isinstance(e, Affine)]
+        # Affine slots (ours or the reference's: duck-typed, no .value)
+        slots = [(k, e) for k, e in enumerate(gate.params) if not hasattr(e, "value")]
         d = dagger_gate(bg)
         if not slots:
             pend_r.append(d)

@@ -126,3 +126,139 @@ def test_vectorised_bind_matches_per_gate_evaluation():
     k2, q2, v2 = flatten_bound(Circuit(8, b.gates, 0))
     assert np.array_equal(k, k2) and np.array_equal(q, q2) and np.array_equal(v, v2)
     assert cfg["circuit"].n_qubits == 8
+
+
+def _ref_engine():
+    import os
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "vqekit")):
+        pytest.skip("oracle/_ref (reference build) not built")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import vqekit.engine as RE
+    import vqekit.pauli as RP
+
+    return RE, RP
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3, 4, 8, 16])
+def test_plan_partition_equals_reference(workers):
+    """LPT split identical to the reference's plan_partition (engine.py:131-147)
+    on a config-3-style Hamiltonian with many equal weights (tie rules)."""
+    RE, RP = _ref_engine()
+    from paper_2208_10978_b200 import workloads as W
+
+    h = W.sparse_random_hamiltonian(12, 300, np.random.default_rng(workers), z_only=90)
+    rh = RP.PauliSum(tuple(RP.PauliTerm(complex(t.coefficient), RP.PauliString(tuple(t.string.factors)))
+                           for t in h.terms))
+    ours = engine.plan_partition(h, workers)
+    ref = RE.plan_partition(rh, workers)
+    assert ours.partitions == ref.partitions
+    assert ours.costs == ref.costs
+
+
+class _HostState:
+    def __init__(self, amps):
+        self.amps = amps
+        self.n_qubits = int(amps.size).bit_length() - 1
+
+
+class _OraclePerTerm:
+    """Per-term <P_t> from the C oracle (test stand-in for the CUDA engine)."""
+
+    def expectation_terms(self, state, x, y, z):
+        from oracle import oracle as O
+
+        out = np.zeros(len(x))
+        scratch = np.empty_like(state.amps)
+        for k in range(len(x)):
+            O.apply_pauli(state.amps, int(x[k]), int(y[k]), int(z[k]), scratch)
+            out[k] = O.vdot(state.amps, scratch).real
+        return out
+
+
+def test_expectation_parallel_worker_invariant_and_equals_reference():
+    """SPEC acceptance #8: W in {1,2,4,8} identical to 1e-12; equal to the
+    reference's own expectation_parallel on the same state and plan."""
+    RE, RP = _ref_engine()
+    import vqekit.statevector as RSV
+
+    from conftest import random_state
+    from paper_2208_10978_b200 import workloads as W
+
+    n = 10
+    rng = np.random.default_rng(8)
+    h = W.sparse_random_hamiltonian(n, 400, rng, z_only=120)
+    st = random_state(n, rng)
+    rh = RP.PauliSum(tuple(RP.PauliTerm(complex(t.coefficient), RP.PauliString(tuple(t.string.factors)))
+                           for t in h.terms))
+    vals = []
+    for w in (1, 2, 4, 8):
+        e = engine.expectation_parallel(_HostState(st), h, engine.plan_partition(h, w),
+                                        engine=_OraclePerTerm())
+        e_ref = RE.expectation_parallel(RSV.StateVector(n, st), rh, RE.plan_partition(rh, w))
+        assert abs(e - e_ref) <= 1e-12 * max(1.0, abs(e_ref))
+        vals.append(e)
+    assert max(vals) - min(vals) <= 1e-12 * max(1.0, abs(vals[0]))
+
+
+def _a16_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    from conftest import random_state
+    from paper_2208_10978_b200 import distributed as D
+    from paper_2208_10978_b200 import workloads as W
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 9
+        rng = np.random.default_rng(4)
+        h = W.sparse_random_hamiltonian(n, 200, rng, z_only=60)
+        st = random_state(n, rng)  # every rank holds the same replica
+        comm = D.ProcessGroupComm()
+        out = {w: engine.expectation_parallel(_HostState(st), h, engine.plan_partition(h, w),
+                                              comm=comm, engine=_OraclePerTerm())
+               for w in (1, 2, 4, 8)}
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_expectation_parallel_two_ranks_gloo():
+    """Replicated state on 2 ranks: worker w evaluated on rank w % 2, partials
+    gathered and summed in worker order -- same value on every rank, for
+    every W, as the single-process sum."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from conftest import random_state
+    from paper_2208_10978_b200 import workloads as W
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_a16_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 9
+    rng = np.random.default_rng(4)
+    h = W.sparse_random_hamiltonian(n, 200, rng, z_only=60)
+    st = random_state(n, rng)
+    for w in (1, 2, 4, 8):
+        single = engine.expectation_parallel(_HostState(st), h, engine.plan_partition(h, w),
+                                             engine=_OraclePerTerm())
+        assert res[0][w] == res[1][w] == single
