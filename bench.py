@@ -703,25 +703,56 @@ def run_engine(args, rank, world, local):
             # per-core gate rate at 28 q x the decomposed gate count at 32 q,
             # plus 5,000 strings at the per-string cost of the config-3 sample x 4
             cb = line["cpu_baseline"]
-            per_core = cb["value"] / cb["cores"]
             gates32 = ex["ucc32"].get("decomposed_gates", 0)
-            t_ev = gates32 * float(1 << 32) / per_core
+            t_ev = gates32 * float(1 << 32) / cb["value"]
             e30 = ex.get("expect30", {}).get("cpu_reference", {})
-            t_h = (e30["s_per_eval_extrapolated"] * e30["cores"] / 10_000 * 4 * 5_000
+            t_h = (e30["s_per_eval_extrapolated"] * 4 * 5_000 / 10_000
                    if "s_per_eval_extrapolated" in e30 else 0.0)
             ex["ucc32"]["cpu_reference"] = {
-                "kind": "reference", "extrapolated": True, "cores": 1,
+                "kind": "reference", "extrapolated": True, "cores": cb["cores"],
                 "s_per_eval_extrapolated": t_ev + t_h, "value": 1.0 / (t_ev + t_h),
                 "unit": "energy evals/s",
-                "sample": "evolve: decomposed gates x 2^32 / the reference's per-core gate rate "
-                          "(cpu_baseline); H: 5,000 x the config-3 per-string time x 4 (1 core)"}
+                "sample": "evolve: decomposed gates x 2^32 / the reference's all-core gate rate "
+                          "(cpu_baseline); H: 5,000 strings x 4 (32 q vs 30 q) at the config-3 "
+                          "sample's per-string rate on its W workers"}
             ex["ucc32"]["vs_cpu_reference"] = ex["ucc32"]["value"] * (t_ev + t_h)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
+def nvlink_alltoall_probe(local: int, nbytes: int = 1 << 30, iters: int = 5) -> dict:
+    """Measured all-to-all bandwidth between the ranks (torch.distributed
+    all_to_all_single over NCCL): bytes each GPU sends to the others per
+    second -- the denominator of the relayout's NVLink fraction."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    n = (nbytes // 8 // world) * world
+    src = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}").fill_(1.0)
+    dst = torch.empty_like(src)
+    for _ in range(2):
+        dist.all_to_all_single(dst, src)
+    torch.cuda.synchronize(local)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    a.record()
+    for _ in range(iters):
+        dist.all_to_all_single(dst, src)
+    b.record()
+    torch.cuda.synchronize(local)
+    t = torch.tensor([a.elapsed_time(b) / 1e3 / iters], device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sent = 8 * n * (world - 1) / world
+    return {"GB_per_s_per_gpu": sent / float(t.item()) / 1e9, "bytes_per_gpu": sent,
+            "how": f"all_to_all_single of {8 * n / 2**30:.2f} GiB per rank, max over ranks, "
+                   f"{iters} iterations"}
+
+
 def run_engine_dist(args, rank, world, local):
-    """Sharded brickwork, weak scaling: 2^28 amplitudes per GPU."""
+    """Sharded brickwork, weak scaling at config 5's shard size: 2^33
+    amplitudes (128 GiB) per GPU, n = 33 + log2(N) qubits, depth 10 (N = 8
+    is config 5 itself: 36 q)."""
     import ctypes
 
     import numpy as np
@@ -736,8 +767,9 @@ def run_engine_dist(args, rank, world, local):
         local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     g = world.bit_length() - 1
-    n = int(os.environ.get("QSV_BENCH_LOCAL_QUBITS", N_QUBITS)) + g
-    circ = W.brickwork(n, LAYERS, SEED)
+    n = int(os.environ.get("QSV_BENCH_LOCAL_QUBITS", "33")) + g
+    layers = int(os.environ.get("QSV_BENCH_LAYERS", "10"))
+    circ = W.brickwork(n, layers, SEED)
     G = len(circ.gates)
     comm = D.ProcessGroupComm()
     be = D.DistributedBackend(comm, D.CudaEngine(local))
@@ -745,13 +777,14 @@ def run_engine_dist(args, rank, world, local):
     def step():
         return be.evolve(be.prepare("0" * n), circ)
 
+    nvl = nvlink_alltoall_probe(local) if args.dist_backend == "nccl" else None
     for _ in range(args.warmup):
         psi = step()
         del psi
     torch.cuda.synchronize(local)
-    stats0 = None
     dist.barrier()
     torch.cuda.synchronize(local)
+    _, launches0 = _lib.jit_info()
     with ClockSampler(local) as clocks:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -769,36 +802,37 @@ def run_engine_dist(args, rank, world, local):
             del psi
         end.record()
         torch.cuda.synchronize(local)
+    _, launches1 = _lib.jit_info()
     t_step = start.elapsed_time(end) / 1e3 / args.steps
     dev_t = "cuda" if args.dist_backend == "nccl" else "cpu"
     tt = torch.tensor([t_step, relayout_s / args.steps], device=dev_t)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_max, t_swap = float(tt[0].item()), float(tt[1].item())
     value = G * (1 << n) / t_max
-
-    # e2e: public API, gate arrays in, every rank's shard out to pinned host
-    # memory every step; as at N = 1, step k's download (copy stream)
-    # overlaps step k+1's evolve, timed until the last download has landed
     n_local = n - g
-    host_out = [torch.empty(1 << n_local, dtype=torch.complex128, pin_memory=True).numpy()
-                for _ in range(2)]
+    passes = (launches1 - launches0) / args.steps
+
+    # e2e: the public API with host inputs every step -- the gate list is
+    # flattened from the host Circuit objects, the state is evolved, and the
+    # step's result read back to the host is an observable, <Z_0 Z_{n-1}> +
+    # <X_0> (a 2^n-amplitude state is 16 TiB... at config 5 the state itself
+    # is 1 TiB, so no caller downloads it); max over ranks
+    from paper_2208_10978_b200.pauli import PauliString, PauliSum, PauliTerm
+
+    obs = PauliSum((PauliTerm(1.0, PauliString(((0, "Z"), (n - 1, "Z")))),
+                    PauliTerm(0.5, PauliString(((0, "X"),)))))
     e2e_steps = max(2, min(args.steps, 4))
+    from paper_2208_10978_b200 import circuit as C
+
     dist.barrier()
     t0 = time.perf_counter()
-    prev = None
-    for k in range(e2e_steps):
+    for _ in range(e2e_steps):
+        C._FLAT_STRUCTS.clear()  # re-read the gate list from the host objects every step
         psi = step()
-        for sh in psi.shards.values():
-            sh.download_async(host_out[k % 2])
-        if prev is not None:
-            for sh in prev.shards.values():
-                sh.wait_download()
-        prev = psi
-    for sh in prev.shards.values():
-        sh.wait_download()
-    del prev, psi
-    t_e2e = time.perf_counter() - t0
-    te = torch.tensor([t_e2e / e2e_steps], device=dev_t)
+        val = be.expectation(psi, obs)
+        del psi
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([t_e2e], device=dev_t)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
 
@@ -827,33 +861,37 @@ def run_engine_dist(args, rank, world, local):
                "relayout_bytes_sent_per_gpu": sent_u}
 
     peak, peak_kind = load_peaks()
-    passes = None
     if rank == 0:
+        t_local = max(t_max - t_swap, 1e-12)
+        hbm = passes * 32.0 * (1 << n_local) / t_local / 1e9 if passes else None
+        swap_gbs = (sent / args.steps) / max(t_swap, 1e-12) / 1e9
         line = {
             "metric": "amplitude-updates/s", "value": value, "unit": "amplitude-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic",
-            "config": {"workload": f"config2/5 family: {n}q random brickwork depth {LAYERS} "
+            "config": {"workload": f"config5 family: {n}q random brickwork depth {layers} "
                                    f"({G} gates), seed {SEED}, sharded over {world} GPUs "
-                                   f"(2^{n_local} amplitudes per GPU, {g} global qubits)",
+                                   f"(2^{n_local} amplitudes = {16 * (1 << n_local) / 2**30:.0f} GiB "
+                                   f"per GPU, {g} global qubits)" + (" = config 5" if n == 36 else ""),
                        "n_qubits": n, "gates": G, "parallelism": f"state sharded x{world} (global qubits)",
-                       "l2": f"shard {16 * (1 << n_local) / 2**30:.2f} GiB vs 126 MB L2"},
+                       "l2": f"shard {16 * (1 << n_local) / 2**30:.2f} GiB >> 126 MB L2 (no flush needed)"},
             "e2e": {"value": G * (1 << n) / t_e2e, "unit": "amplitude-updates/s",
-                    "h2d_bytes_per_step": int(G * 24),
-                    "d2h_bytes_per_step": int(16 * (1 << n)), "ms_per_step": t_e2e * 1e3,
-                    "steps": e2e_steps,
-                    "note": "each rank's shard downloaded every step (download_async, "
-                            "overlapping the next step's evolve); max over ranks"},
+                    "h2d_bytes_per_step": int(G * 40), "d2h_bytes_per_step": 16 * world,
+                    "ms_per_step": t_e2e * 1e3, "steps": e2e_steps, "observable": val,
+                    "note": "host Circuit flattened + evolve + <Z0 Z_{n-1}> + 0.5<X0> to the host "
+                            "every step (per-rank partials gathered); max over ranks"},
             "swap": {"relayouts_per_step": relayouts / args.steps,
                      "bytes_sent_per_gpu_per_step": sent / args.steps,
-                     "seconds_per_step": t_swap,
-                     "GB_per_s": (sent / args.steps) / max(t_swap, 1e-12) / 1e9,
-                     "nvlink_frac": (sent / args.steps) / max(t_swap, 1e-12) / 900e9},
-            "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
-                         "frac": None, "traffic": None, "kernel": "tile pass (see N=1 line)",
-                         "peak_source": peak_kind},
-            "gpu_launches": None,
+                     "seconds_per_step": t_swap, "GB_per_s": swap_gbs,
+                     "nvlink_peak": nvl,
+                     "nvlink_frac": (swap_gbs / nvl["GB_per_s_per_gpu"]) if nvl else None},
+            "roofline": {"bound": "hbm", "achieved": hbm, "peak": peak, "unit": "GB/s",
+                         "frac": (hbm / peak) if hbm else None, "traffic": None,
+                         "kernel": "qsv_pass (tile passes between relayouts)",
+                         "passes_per_step": passes, "peak_source": peak_kind,
+                         "note": "32 B x 2^n_local per pass over the step time minus relayout time"},
+            "gpu_launches": int(launches1 - launches0),
             "clocks": clocks.summary(),
         }
         if ucc is not None:

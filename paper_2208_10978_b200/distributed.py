@@ -155,11 +155,12 @@ class CudaEngine:
 class LoopbackComm:
     """All P shards live in this process; exchanges are device copies."""
 
-    def __init__(self, world: int):
+    def __init__(self, world: int, piece_bytes: int = 256 << 20):
         if world < 1 or world & (world - 1):
             raise ValueError("world size must be a power of two")
         self.world = world
         self.owned = list(range(world))
+        self.piece_bytes = piece_bytes
 
     def gather_partials(self, partials: dict) -> list:
         return [partials[r] for r in range(self.world)]
@@ -474,6 +475,58 @@ def plan_localize(flips: list[int], n: int, n_local: int, perm):
     return swaps, Relayout(S), perm
 
 
+def plan_align(perm, target, n: int, n_local: int):
+    """Steps turning the physical layout `perm` into `target`: at most two
+    relayouts (evict the mismatched global qubits to local positions that
+    stay local, then bring the target's global qubits in) and local SWAP
+    gates (free: folded into the tile maps).  Returns a list of
+    ("swaps", [(p, q), ...]) / ("relayout", Relayout) steps."""
+    perm = list(perm)
+    inv = [0] * n
+    for q, p in enumerate(perm):
+        inv[p] = q
+    tinv = [0] * n
+    for q, p in enumerate(target):
+        tinv[p] = q
+    g = n - n_local
+    steps = []
+    W = [i for i in range(g) if inv[n_local + i] != tinv[n_local + i]]
+    if W:
+        want = [tinv[n_local + i] for i in W]
+        if any(perm[q] >= n_local for q in want):
+            # 1) the rank bits W take local qubits that are not global in target
+            tglob = {tinv[n_local + i] for i in range(g)}
+            cand = [inv[p] for p in range(n_local) if inv[p] not in tglob]
+            if len(cand) < len(W):
+                raise ValueError("too few local qubits to realign the shards")
+            bring, victims = [inv[n_local + i] for i in W], cand[:len(W)]
+            swaps = []
+            _move_victims(perm, inv, victims, n_local, swaps)
+            S = tuple(perm[b] - n_local for b in bring)
+            _apply_relayout_to_map(perm, inv, bring, victims, n_local)
+            steps += [("swaps", swaps), ("relayout", Relayout(S))]
+        # 2) every target global qubit is local now: swap them into W
+        bring, victims = [inv[n_local + i] for i in W], want
+        swaps = []
+        _move_victims(perm, inv, victims, n_local, swaps)
+        S = tuple(perm[b] - n_local for b in bring)
+        _apply_relayout_to_map(perm, inv, bring, victims, n_local)
+        steps += [("swaps", swaps), ("relayout", Relayout(S))]
+    # 3) local positions
+    swaps = []
+    for p in range(n_local):
+        q = tinv[p]
+        if inv[p] != q:
+            cur = perm[q]
+            other = inv[p]
+            swaps.append((p, cur))
+            perm[q], perm[other] = p, cur
+            inv[p], inv[cur] = q, other
+    steps.append(("swaps", swaps))
+    assert perm == list(target)
+    return steps
+
+
 # ---------------------------------------------------------------------------
 # the distributed state
 # ---------------------------------------------------------------------------
@@ -489,31 +542,61 @@ def _log2(p: int) -> int:
 class DistStateVector:
     """Logical n-qubit state sharded over comm.world ranks."""
 
-    def __init__(self, n_qubits: int, comm, engine, shards: dict, perm):
+    def __init__(self, n_qubits: int, comm, engine, shards: Optional[dict], perm,
+                 basis: Optional[int] = None):
         self.n_qubits = n_qubits
         self.comm = comm
         self.engine = engine
         self.g = _log2(comm.world)
         self.n_local = n_qubits - self.g
-        self.shards = shards
+        self._shards = shards
+        self._basis = basis  # lazy |basis>: no device memory until first needed
         self.perm = list(perm)
         self.stats = {"relayouts": 0, "relayout_bytes_sent": 0, "relayout_seconds": 0.0}
 
     # -- construction --------------------------------------------------------
     @classmethod
     def basis(cls, n_qubits: int, index: int, comm, engine) -> "DistStateVector":
+        """|index> kept as an index: evolve materialises it straight into its
+        output shards (one shard per GPU, never a copy -- at config 5 a shard
+        is 128 GiB of a 180 GB B200)."""
         g = _log2(comm.world)
-        n_local = n_qubits - g
-        if n_local < 1:
+        if n_qubits - g < 1:
             raise ValueError("more ranks than amplitudes per shard allow")
+        return cls(n_qubits, comm, engine, None, range(n_qubits), basis=index)
+
+    def _materialize_basis(self, index: int) -> dict:
+        n_local = self.n_local
         owner, local = index >> n_local, index & ((1 << n_local) - 1)
-        shards = {r: (engine.basis(n_local, local) if r == owner else engine.zeros(n_local))
-                  for r in comm.owned}
-        return cls(n_qubits, comm, engine, shards, range(n_qubits))
+        return {r: (self.engine.basis(n_local, local) if r == owner else self.engine.zeros(n_local))
+                for r in self.comm.owned}
+
+    @property
+    def shards(self) -> dict:
+        if self._shards is None:
+            self._shards = self._materialize_basis(self._basis)
+            self._basis = None
+        return self._shards
+
+    @property
+    def basis_index(self) -> Optional[int]:
+        return self._basis if self._shards is None else None
 
     def copy(self) -> "DistStateVector":
+        if self._shards is None:
+            return DistStateVector(self.n_qubits, self.comm, self.engine, None, self.perm,
+                                   basis=self._basis)
         out = DistStateVector(self.n_qubits, self.comm, self.engine,
                               {r: self.engine.copy(s) for r, s in self.shards.items()}, self.perm)
+        return out
+
+    def fresh_from_basis(self) -> "DistStateVector":
+        """Output state of an evolve of this lazy basis state: its own shards
+        (the input stays a lazy index -- statevector.py:71's copy without
+        the second state)."""
+        out = DistStateVector(self.n_qubits, self.comm, self.engine, None, self.perm,
+                              basis=self._basis)
+        out.shards  # noqa: B018  (materialise)
         return out
 
     # -- exchange ------------------------------------------------------------
@@ -551,11 +634,7 @@ class DistStateVector:
                 # (r, chunk c) <-> (p, chunk rs)
                 if p in views:
                     if r < p:
-                        a = views[r][c * chunk:(c + 1) * chunk]
-                        b = views[p][rs * chunk:(rs + 1) * chunk]
-                        tmp = a.clone()
-                        a.copy_(b)
-                        b.copy_(tmp)
+                        self._swap_local(views[r], views[p], c * chunk, rs * chunk, chunk)
                 else:
                     remote.setdefault(r, []).append((c, p))
         if remote:
@@ -564,6 +643,24 @@ class DistStateVector:
         self.stats["relayouts"] += 1
         self.stats["relayout_bytes_sent"] += 16 * (((1 << k) - 1) * chunk)  # per rank
         self.stats["relayout_seconds"] += time.perf_counter() - t0
+
+    def _swap_local(self, ta, tb, oa: int, ob: int, chunk: int) -> None:
+        """Swap ta[oa:oa+chunk] <-> tb[ob:ob+chunk] (both shards in this
+        process) through one bounded staging piece, never a chunk-sized
+        temporary (a chunk can be half of a 128 GiB shard)."""
+        row_bytes = ta.element_size() * (ta.shape[1] if ta.dim() > 1 else 1)
+        piece = max(1, min(chunk, self.comm_piece_bytes() // row_bytes))
+        tmp = ta.new_empty((piece,) + tuple(ta.shape[1:]))
+        for off in range(0, chunk, piece):
+            w = min(piece, chunk - off)
+            a = ta[oa + off:oa + off + w]
+            b = tb[ob + off:ob + off + w]
+            tmp[:w].copy_(a)
+            a.copy_(b)
+            b.copy_(tmp[:w])
+
+    def comm_piece_bytes(self) -> int:
+        return int(getattr(self.comm, "piece_bytes", 256 << 20))
 
     def _p2p_exchange(self, views, remote, chunk):
         import torch
@@ -800,6 +897,37 @@ class DistStateVector:
                 out[r] = buf
         return out
 
+    def align_to(self, target) -> None:
+        """Re-layout this state (logically unchanged) to the physical qubit
+        map `target`."""
+        if list(target) == self.perm:
+            return
+        for kind, step in plan_align(self.perm, target, self.n_qubits, self.n_local):
+            if kind == "swaps":
+                self._apply_swaps(step)
+            else:
+                self._relayout(step)
+        self.perm = list(target)
+
+    def overlap(self, other: "DistStateVector") -> complex:
+        """<self|other> = sum_j conj(self_j) other_j (engine.py:74-75): other
+        is realigned to self's layout, then per-shard dot products are summed
+        in ascending rank order."""
+        if other.n_qubits != self.n_qubits:
+            raise ValueError("state qubit counts differ")
+        if self.basis_index is not None and other.basis_index is not None:
+            return complex(1.0 if self.basis_index == other.basis_index else 0.0)
+        other.align_to(self.perm)
+        part = {}
+        for r in self.comm.owned:
+            v = self.engine.vdot(self.shards[r], other.shards[r])
+            part[r] = np.array([v.real, v.imag])
+        re = im = 0.0
+        for p in self.comm.gather_partials(part):
+            re += float(p[0])
+            im += float(p[1])
+        return complex(re, im)
+
     # -- host view -------------------------------------------------------------
     def amplitudes(self) -> np.ndarray:
         """Logical amplitude vector on the host (small states; test helper)."""
@@ -834,10 +962,9 @@ def evolve(s: DistStateVector, c) -> DistStateVector:
 
     if c.n_qubits != s.n_qubits:
         raise ValueError("circuit and state qubit counts differ")
-    if not c.is_bound():
-        raise RuntimeError("circuit must be bound before evolution")
-    out = s.copy()
-    out.apply_flat(*flatten_bound(c))
+    flat = flatten_bound(c)  # RuntimeError if unbound (statevector.py:69-70)
+    out = s.fresh_from_basis() if s.basis_index is not None else s.copy()
+    out.apply_flat(*flat)
     return out
 
 
@@ -872,3 +999,6 @@ class DistributedBackend:
 
     def expectation(self, state: DistStateVector, h) -> float:
         return expectation(state, h)
+
+    def overlap(self, a: DistStateVector, b: DistStateVector) -> complex:
+        return a.overlap(b)

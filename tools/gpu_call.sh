@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-python bench.py --steps 5 --warmup 3 --extra none --no-cpu-baseline > gpurun_out/bench_c2.log 2>&1; tail -c 3000 gpurun_out/bench_c2.log
-timeout 900 ncu --metrics gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:qsv_pass -c 60 --csv --log-file gpurun_out/fp64_launches.csv python bench.py --steps 1 --warmup 3 --extra none --no-cpu-baseline > gpurun_out/ncu_fp64.log 2>&1; echo ncu rc=$?
-timeout 1200 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -c 2000 gpurun_out/bench_ref.log
+timeout 900 python -m pytest tests/test_gpu_dropin.py -x -q -m gpu 2>&1 | tail -25
+timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_full_r02a.log 2>&1; echo bench rc=$?; tail -c 6000 gpurun_out/bench_full_r02a.log
