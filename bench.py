@@ -509,6 +509,33 @@ def extra_fused30(steps=3):
             "s_per_evolve": dt, "passes": passes, "hbm_gbs": gbs, "hbm_frac": gbs / peak}
 
 
+def extra_brick33(steps=2):
+    """Single-GPU base of the weak-scaling family the N > 1 lines run: the
+    config-5 brickwork construction (depth 10) on 33 qubits = 2^33 amplitudes
+    (128 GiB), one B200, from |0...0> (R_1 of E_N = R_N / (N R_1))."""
+    from paper_2208_10978_b200 import statevector as sv
+    from paper_2208_10978_b200 import workloads as W
+
+    n = 33
+    circ = W.brickwork(n, 10, SEED)
+    sv.release_pool()
+    psi = sv.evolve(sv.init_state("0" * n), circ)  # plan + specialise
+    psi.synchronize()
+    del psi
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        psi = sv.evolve(sv.init_state("0" * n), circ)
+        psi.synchronize()
+        ts.append(time.perf_counter() - t0)
+        passes = sv.last_plan_stats()["n_passes"]
+        del psi
+    dt = min(ts)
+    return {"workload": f"config5 construction on 33q (depth 10, {len(circ.gates)} gates), 1 GPU, "
+                        "128 GiB state", "metric": "amplitude-updates/s",
+            "value": len(circ.gates) * float(1 << n) / dt, "s_per_evolve": dt, "passes": passes}
+
+
 def extra_ucc32(steps=1):
     from paper_2208_10978_b200 import engine
     from paper_2208_10978_b200 import statevector as sv
@@ -675,7 +702,7 @@ def run_engine(args, rank, world, local):
         line["extra"] = {}
         for e in extras:
             fn = {"ucc12": extra_ucc12, "expect30": extra_expect30, "ucc32": extra_ucc32,
-                  "fused30": extra_fused30}[e]
+                  "fused30": extra_fused30, "brick33": extra_brick33}[e]
             try:
                 line["extra"][e] = fn()
             except Exception as exc:  # an extra must never cost the headline line
@@ -905,7 +932,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--extra", default="ucc12,fused30,expect30,ucc32",
+    ap.add_argument("--extra", default="ucc12,fused30,expect30,ucc32,brick33",
                     help="secondary workloads (configs 1, 3, 4 and the 30q fused-gate roofline); 'none' to skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])

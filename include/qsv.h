@@ -190,6 +190,13 @@ int qsv_plan_expectation(int n_qubits, int64_t n_terms, const uint64_t *x, const
 int qsv_match_rotations(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
                         int64_t cap, int64_t *spans, uint64_t *masks, int64_t *count);
 
+/* Debug / test export: the specialised (NVRTC) source of sweep `k` of the
+ * expectation plan for these strings ("" when that sweep is interpreted);
+ * the planner runs on the host, no device needed. */
+int qsv_debug_sweep_source(int n_qubits, int64_t S, const uint64_t *x, const uint64_t *y,
+                           const uint64_t *z, int64_t k, char *out, int64_t cap, int64_t *needed,
+                           int64_t *n_sweeps);
+
 /* Debug: the compiled tile program for a gate list as JSON (planner output
  * consumed by the CPU emulator in tests/).  needed receives the buffer size. */
 int qsv_debug_plan_json(int n_qubits, int64_t n_gates, const int32_t *kinds,

@@ -52,7 +52,7 @@ EXPORTED = (
     "qsv_download_wait", "qsv_apply_1q", "qsv_apply_2q",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
-    "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_sample_parity",
+    "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_debug_sweep_source", "qsv_sample_parity",
     "qsv_jit_info", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
     "qsv_release_program", "qsv_evolve_basis", "qsv_evolve_basis_prepared",
     "qsv_last_plan_stats",
@@ -99,6 +99,8 @@ def _declare(L):
         "qsv_plan_expectation": ([ctypes.c_int, i64, u64p, u64p, u64p, sp], ctypes.c_int),
         "qsv_debug_plan_json": ([ctypes.c_int, i64, i32p, i32p, dp, ctypes.c_char_p, i64,
                                  ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_debug_sweep_source": ([ctypes.c_int, i64, u64p, u64p, u64p, i64, ctypes.c_char_p, i64,
+                                    ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_sample_parity": ([vp, u64, i64, u64p, dp, ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_match_rotations": ([ctypes.c_int, i64, i32p, i32p, i64, ctypes.POINTER(i64), u64p,
                                  ctypes.POINTER(i64)], ctypes.c_int),
@@ -160,6 +162,17 @@ def debug_plan(n_qubits: int, kinds, qubits, values) -> dict:
     check(lib().qsv_debug_plan_json(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits),
                                     dptr(values), buf, need.value, ctypes.byref(need)))
     return json.loads(buf.value.decode())
+
+
+def debug_sweep_source(n_qubits: int, x, y, z, k: int) -> tuple[str, int]:
+    """(specialised source of sweep k of the expectation plan, number of sweeps)."""
+    need, ns = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(lib().qsv_debug_sweep_source(n_qubits, len(x), u64ptr(x), u64ptr(y), u64ptr(z), k, None, 0,
+                                       ctypes.byref(need), ctypes.byref(ns)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(lib().qsv_debug_sweep_source(n_qubits, len(x), u64ptr(x), u64ptr(y), u64ptr(z), k, buf,
+                                       need.value, ctypes.byref(need), ctypes.byref(ns)))
+    return buf.value.decode(), ns.value
 
 
 def jit_info() -> tuple[bool, int]:

@@ -1523,6 +1523,24 @@ int qsv_plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y,
     return QSV_OK;
 }
 
+int qsv_debug_sweep_source(int n, int64_t S, const uint64_t *x, const uint64_t *y,
+                           const uint64_t *z, int64_t k, char *out, int64_t cap, int64_t *needed,
+                           int64_t *n_sweeps)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (n < 1 || n > kMaxQubits) return fail_code(QSV_ERR_RESOURCE, "qubit count out of range");
+    if (S < 0 || (S > 0 && (!x || !y || !z))) return fail_code(QSV_ERR_INVALID, "bad term arrays");
+    if (int rc = validate_masks(n, S, x, y, z)) return rc;
+    std::vector<SweepPlan> plan;
+    plan_expectation(n, S, x, y, z, plan, true);
+    if (n_sweeps) *n_sweeps = (int64_t)plan.size();
+    std::string src;
+    if (k >= 0 && k < (int64_t)plan.size()) jit_sweep_source(plan[k], src);
+    if (needed) *needed = (int64_t)src.size() + 1;
+    if (out && cap > (int64_t)src.size()) std::memcpy(out, src.c_str(), src.size() + 1);
+    return QSV_OK;
+}
+
 // Debug export of the compiled tile program (JSON) for the CPU emulator in
 // tests/ -- lets the planner and its encoding be verified without a GPU.
 int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,

@@ -792,9 +792,229 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
 // longest-processing-time on cost = pairs x (2 + 2 + terms); each warp keeps
 // one per-lane accumulator per string across all of its tiles, so the warp
 // reduction happens once per kernel instead of once per (tile, string).
+// Register-coset sweep.  The specialised sweep above is bound by shared-memory
+// bandwidth (LSU shared wavefronts at 73-84 % of peak, profiles/r02_sweep_ncu.txt):
+// every flip group re-reads 32 KiB of partner amplitudes per tile.  Here the
+// groups of a sweep are packed into PHASES whose flips span a subspace V of
+// the tile bits with dim V <= 4; in a phase each of the 256 threads of a tile
+// group loads ONE coset w + V (16 amplitudes, 64 KiB per tile in total) into
+// registers and forms the pair products of EVERY group of the phase from
+// registers (a flip F in V pairs coset elements c and c ^ F).  V's basis is
+// kept in reduced echelon form with pivots = highest bits, so F's highest bit
+// is a pivot and the pair representative (that bit clear) is a static coset
+// coordinate; the coset bases w range over the complement W = {pivot bits
+// 0}, whose basis is ordered so that swz(w) mod 8 differs across each
+// quarter-warp (conflict-free 16-B loads).  Per string the sign of pair c is
+// (-1)^{|w & s|} (thread) x (-1)^{|vec(c) & s|} (static, a character of the
+// 3 non-pivot-H coordinates -> an 8-point Walsh-Hadamard index).
+bool jit_sweep_source_coset(const SweepPlan &sp, std::string &src)
+{
+    const int nterms = (int)sp.terms.size();
+    if (nterms > 48) return false;
+    struct Phase {
+        uint32_t b[4] = {0, 0, 0, 0};
+        int piv[4] = {-1, -1, -1, -1};
+        int dim = 0;
+        std::vector<size_t> groups;
+        uint32_t reduce(uint32_t v) const
+        {
+            for (int i = 0; i < dim; ++i)
+                if ((v >> piv[i]) & 1u) v ^= b[i];
+            return v;
+        }
+        void insert(uint32_t v)
+        {
+            v = reduce(v);
+            if (!v) return;
+            const int p = 31 - __builtin_clz(v);
+            for (int i = 0; i < dim; ++i)
+                if ((b[i] >> p) & 1u) b[i] ^= v;
+            b[dim] = v;
+            piv[dim] = p;
+            ++dim;
+        }
+        uint32_t vec(unsigned c) const
+        {
+            uint32_t v = 0;
+            for (int i = 0; i < 4; ++i)
+                if ((c >> i) & 1u) v ^= b[i];
+            return v;
+        }
+        unsigned coord(uint32_t v) const
+        {
+            unsigned c = 0;
+            for (int i = 0; i < 4; ++i)
+                if ((v >> piv[i]) & 1u) c |= 1u << i;
+            return c;
+        }
+    };
+    // greedy phases: heaviest groups first; a group joins the current phase
+    // if its flip is already spanned or the span can still grow
+    std::vector<size_t> order(sp.groups.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        return sp.groups[a].t1 - sp.groups[a].t0 > sp.groups[b].t1 - sp.groups[b].t0;
+    });
+    std::vector<Phase> phases;
+    std::vector<bool> used(sp.groups.size(), false);
+    for (size_t oi = 0; oi < order.size(); ++oi) {
+        if (used[order[oi]]) continue;
+        Phase ph;
+        ph.insert(sp.groups[order[oi]].f_loc);
+        ph.groups.push_back(order[oi]);
+        used[order[oi]] = true;
+        for (;;) {
+            // every group the span already holds is free: take them all
+            for (size_t oj = oi + 1; oj < order.size(); ++oj) {
+                const size_t g = order[oj];
+                if (!used[g] && ph.reduce(sp.groups[g].f_loc) == 0) {
+                    ph.groups.push_back(g);
+                    used[g] = true;
+                }
+            }
+            if (ph.dim >= 4) break;
+            // grow the span by the next heaviest group
+            size_t pick = order.size();
+            for (size_t oj = oi + 1; oj < order.size(); ++oj)
+                if (!used[order[oj]]) {
+                    pick = oj;
+                    break;
+                }
+            if (pick == order.size()) break;
+            ph.insert(sp.groups[order[pick]].f_loc);
+            ph.groups.push_back(order[pick]);
+            used[order[pick]] = true;
+        }
+        for (int q = 0; ph.dim < 4 && q < kMaxTileBits; ++q) ph.insert(1u << q);  // pad to 4 dims
+        // pivots ascending in basis order (cosmetic; coordinates follow)
+        phases.push_back(ph);
+    }
+    char buf[512];
+    std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";
+    const int kDirect = 3;
+    for (const Phase &ph : phases) {
+        // complement basis: non-pivot unit vectors; the first three chosen so
+        // that swz(.) mod 8 is independent (quarter-warp conflict freedom)
+        std::vector<uint32_t> unit;
+        for (int q = 0; q < kMaxTileBits; ++q) {
+            bool pv = false;
+            for (int i = 0; i < 4; ++i) pv |= ph.piv[i] == q;
+            if (!pv) unit.push_back(1u << q);
+        }
+        std::vector<uint32_t> U;
+        {
+            bool found = false;
+            for (size_t a = 0; a < unit.size() && !found; ++a)
+                for (size_t b2 = 0; b2 < unit.size() && !found; ++b2)
+                    for (size_t c2 = 0; c2 < unit.size() && !found; ++c2) {
+                        if (a == b2 || a == c2 || b2 == c2) continue;
+                        const uint32_t x0 = h_swz(unit[a]) & 7u, x1 = h_swz(unit[b2]) & 7u,
+                                       x2 = h_swz(unit[c2]) & 7u;
+                        if (x0 && x1 && x2 && x0 != x1 && (x0 ^ x1) != x2 && x2 != x0 && x2 != x1) {
+                            U = {unit[a], unit[b2], unit[c2]};
+                            for (size_t d = 0; d < unit.size(); ++d)
+                                if (d != a && d != b2 && d != c2) U.push_back(unit[d]);
+                            found = true;
+                        }
+                    }
+            if (!found) U = unit;
+        }
+        fn += "  {\n    u32 w = 0u, sw = 0u;\n";
+        for (int i = 0; i < 8; ++i) {
+            snprintf(buf, sizeof(buf), "    if ((pl >> %d) & 1u) { w ^= %uu; sw ^= %uu; }\n", i, U[i],
+                     h_swz(U[i]));
+            fn += buf;
+        }
+        fn += "    double2 A[16];\n";
+        for (unsigned cc = 0; cc < 16; ++cc) {
+            snprintf(buf, sizeof(buf), "    A[%u] = sm[sw ^ %uu];\n", cc, h_swz(ph.vec(cc)));
+            fn += buf;
+        }
+        for (size_t g : ph.groups) {
+            const GroupRec &G = sp.groups[g];
+            const unsigned cF = ph.coord(G.f_loc);
+            int mH = -1;
+            for (int i = 0; i < 4; ++i)
+                if (ph.piv[i] == G.h) mH = i;
+            if (mH < 0 || !((cF >> mH) & 1u)) return false;  // cannot happen (echelon form)
+            int other[3], no = 0;
+            for (int i = 0; i < 4; ++i)
+                if (i != mH) other[no++] = i;
+            const bool need_re = G.t_im > G.t0, need_im = G.t1 > G.t_im;
+            const bool w_re = G.t_im - G.t0 > kDirect, w_im = G.t1 - G.t_im > kDirect;
+            fn += "    { double Wr[8], Wi[8];\n";
+            for (unsigned k = 0; k < 8; ++k) {
+                unsigned cc = 0;
+                for (int j = 0; j < 3; ++j)
+                    if ((k >> j) & 1u) cc |= 1u << other[j];
+                const unsigned cy = cc ^ cF;
+                if (need_re) {
+                    snprintf(buf, sizeof(buf), "      Wr[%u] = fma(A[%u].x, A[%u].x, A[%u].y * A[%u].y);\n", k, cc, cy,
+                             cc, cy);
+                    fn += buf;
+                }
+                if (need_im) {
+                    snprintf(buf, sizeof(buf), "      Wi[%u] = fma(A[%u].x, A[%u].y, -A[%u].y * A[%u].x);\n", k, cc,
+                             cy, cc, cy);
+                    fn += buf;
+                }
+            }
+            auto emit_wht = [&](const char *W) {
+                for (int bb = 1; bb < 8; bb <<= 1)
+                    for (int r = 0; r < 8; ++r) {
+                        if (r & bb) continue;
+                        snprintf(buf, sizeof(buf), "      { const double u = %s[%d], v = %s[%d]; %s[%d] = u + v; %s[%d] = u - v; }\n",
+                                 W, r, W, r | bb, W, r, W, r | bb);
+                        fn += buf;
+                    }
+            };
+            if (need_re && w_re) emit_wht("Wr");
+            if (need_im && w_im) emit_wht("Wi");
+            for (int t = G.t0; t < G.t1; ++t) {
+                const TermRec &tr = sp.terms[t];
+                const uint32_t sl = h_ins0(tr.s_loc, G.h);  // tile-local sign mask, bit H clear
+                unsigned ms = 0;
+                for (int j = 0; j < 3; ++j)
+                    if (__builtin_popcount(ph.b[other[j]] & sl) & 1) ms |= 1u << j;
+                const char *W = tr.use_im ? "Wi" : "Wr";
+                std::string val;
+                if (tr.use_im ? w_im : w_re) {
+                    snprintf(buf, sizeof(buf), "%s[%u]", W, ms);
+                    val = buf;
+                } else {
+                    val = "(";
+                    for (unsigned j = 0; j < 8; ++j) {
+                        snprintf(buf, sizeof(buf), "%s%s[%u]",
+                                 j == 0 ? "" : (__builtin_popcount(j & ms) & 1) ? " - " : " + ", W, j);
+                        val += buf;
+                    }
+                    val += ")";
+                }
+                snprintf(buf, sizeof(buf),
+                         "      acc[%d] = fma(((__popc(w & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g, %s, acc[%d]);\n",
+                         t, sl, (unsigned long long)tr.s_hi, -tr.scale, tr.scale, val.c_str(), t);
+                fn += buf;
+            }
+            fn += "    }\n";
+        }
+        fn += "  }\n";
+    }
+    fn += "}\n";
+    snprintf(buf, sizeof(buf), "#define MAXT %d\n", nterms);
+    src = buf;
+    src += kSweepSkeleton;
+    src += fn;
+    return true;
+}
+
 bool jit_sweep_source(const SweepPlan &sp, std::string &src)
 {
     if (sp.global || sp.geom.m != kMaxTileBits || sp.ndiag != 0 || sp.groups.empty()) return false;
+    if (sp.groups.front().pad[0] & 1) return false;  // wide groups: interpreted transform path
+    {
+        const char *env_cs = getenv("QSV_SWEEP_COSET");  // 0: pair-bit sweep (A/B)
+        if (!(env_cs && env_cs[0] == '0') && jit_sweep_source_coset(sp, src)) return true;
+    }
     if (sp.groups.front().pad[0] & 1) return false;  // wide groups: interpreted transform path
     const int nterms = (int)sp.terms.size();
     if (nterms > 48) return false;
