@@ -98,6 +98,14 @@ int qsv_download_wait(qsv_state *s);
 int qsv_apply_1q(qsv_state *s, const double *m, int qubit);
 /* kernels.apply_2q (kernels/__init__.py:22; _cykernels.pyx:41-73): m = 4x4, rows 2*bit(q0)+bit(q1). */
 int qsv_apply_2q(qsv_state *s, const double *m, int q0, int q1);
+/* General dense k-qubit gate, k = 1..5 (north_star (1): up to k local
+ * qubits as one 2^k x 2^k block).  m: 2^k x 2^k complex128 row-major; the
+ * row / column index is formed from the targets with qubits[0] as the most
+ * significant bit -- the apply_2q convention (_cykernels.pyx:41-73,
+ * circuit.py:5-6) extended to k qubits.  k = 1, 2 reproduce apply_1q /
+ * apply_2q.  Errors: duplicate or out-of-range qubits -> QSV_ERR_INVALID,
+ * k > 5 -> QSV_ERR_RESOURCE. */
+int qsv_apply_matrix(qsv_state *s, int k, const int32_t *qubits, const double *m);
 /* kernels.apply_pauli (kernels/__init__.py:23; _cykernels.pyx:76-102): dst = P src. */
 int qsv_apply_pauli(const qsv_state *src, qsv_state *dst, uint64_t x, uint64_t y, uint64_t z);
 

@@ -49,7 +49,7 @@ EXPORTED = (
     "qsv_abi_version", "qsv_last_error", "qsv_device_count", "qsv_mem_info", "qsv_create", "qsv_destroy",
     "qsv_n_qubits", "qsv_set_stream", "qsv_get_stream", "qsv_device_ptr", "qsv_synchronize",
     "qsv_copy", "qsv_set_basis", "qsv_upload", "qsv_download", "qsv_download_async",
-    "qsv_download_wait", "qsv_apply_1q", "qsv_apply_2q",
+    "qsv_download_wait", "qsv_apply_1q", "qsv_apply_2q", "qsv_apply_matrix",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
     "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_debug_sweep_source", "qsv_sample_parity",
@@ -86,6 +86,7 @@ def _declare(L):
         "qsv_download_wait": ([vp], ctypes.c_int),
         "qsv_apply_1q": ([vp, dp, ctypes.c_int], ctypes.c_int),
         "qsv_apply_2q": ([vp, dp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "qsv_apply_matrix": ([vp, ctypes.c_int, i32p, dp], ctypes.c_int),
         "qsv_apply_pauli": ([vp, vp, u64, u64, u64], ctypes.c_int),
         "qsv_apply_gates": ([vp, i64, i32p, i32p, dp, sp], ctypes.c_int),
         "qsv_apply_pauli_rotations": ([vp, i64, u64p, u64p, u64p, dp, sp], ctypes.c_int),

@@ -1457,6 +1457,33 @@ int qsv_apply_2q(qsv_state *s, const double *m, int q0, int q1)
     return run_template(s, t, params);
 }
 
+int qsv_apply_matrix(qsv_state *s, int k, const int32_t *qubits, const double *m)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (!m || !qubits) return fail_code(QSV_ERR_INVALID, "null matrix or qubit list");
+    if (k < 1) return fail_code(QSV_ERR_INVALID, "k must be >= 1");
+    if (k > 5 || k > s->n) return fail_code(QSV_ERR_RESOURCE, "dense blocks are limited to 5 qubits");
+    uint64_t seen = 0;
+    for (int i = 0; i < k; ++i) {
+        if (qubits[i] < 0 || qubits[i] >= s->n) return fail_code(QSV_ERR_INVALID, "qubit out of range");
+        if ((seen >> qubits[i]) & 1ull) return fail_code(QSV_ERR_INVALID, "duplicate qubit");
+        seen |= 1ull << qubits[i];
+    }
+    QSV_CUDA(cudaSetDevice(s->device));
+    if (int rc = settle(s)) return rc;
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(s->device, &c)) return rc;
+    const size_t mb = (size_t)16 << (2 * k);
+    Blob b;
+    b.add(m, mb);
+    char *d = nullptr;
+    size_t scratch = 0;
+    if (int rc = upload_blob(*c, s->stream, b, 0, &d, &scratch)) return rc;
+    QSV_CUDA(launch_dense(s->amps, s->n, k, qubits, (const double2 *)d, num_sms(s->device), s->stream));
+    return QSV_OK;
+}
+
 int qsv_match_rotations(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
                         int64_t cap, int64_t *spans, uint64_t *masks, int64_t *count)
 {

@@ -15,6 +15,21 @@
 
 namespace qsv {
 
+// Shared-memory tile swizzle (16-B slot of tile index l), used by the planner
+// (register-block maps), the interpreted tile kernels and -- restated as source
+// text -- the NVRTC kernels (qsv_jit.cpp).  GF(2)-linear: slot bits 0..2 =
+// (l ^ F) & 7 with F = fold of l's higher 3-bit chunks, bits 3..5 = F, bits
+// 6.. = l's.  The banks are those of the plain fold; the row permutation puts
+// each 64 / 128-B segment where the TMA 64B / 128B swizzle expects it.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline uint32_t tile_swz(uint32_t l)
+{
+    const uint32_t f = ((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u;
+    return (l & ~63u) | (f << 3) | ((l ^ f) & 7u);
+}
+
 // One-time setup per device (kernel attributes such as the dynamic shared
 // memory cap are per device context): run(f) calls f once for the current
 // device, thread-safely, and again on a device that has not seen it yet.
@@ -218,6 +233,8 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src);
 bool jit_sweep_launch(int device, const std::string &src, const double2 *psi, const TileDims &g,
                       const uint64_t *d_offhi, const int32_t *d_geo, double *d_partial, int grid,
                       cudaStream_t st);
+cudaError_t launch_dense(double2 *psi, int n, int k, const int *qubits, const double2 *d_m, int sms,
+                         cudaStream_t st);
 cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,
                          double bre, double bim, cudaStream_t st);
 

@@ -21,6 +21,7 @@
 //
 // NVRTC and the driver API are dlopen'ed on first use, so libqsv.so still
 // loads (and its planner entry points work) on machines without a GPU driver.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <sys/stat.h>
@@ -72,6 +73,11 @@ struct Api {
     CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                              unsigned, cudaStream_t, void **, void **) = nullptr;
     CUresult (*MemcpyDtoDAsync)(CUdeviceptr, CUdeviceptr, size_t, cudaStream_t) = nullptr;
+    // optional: TMA tile loads (QSV_PASS_TMA); absent -> LDGSTS staging
+    CUresult (*TensorMapEncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                     const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                     const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill) = nullptr;
 };
 Api g_api;
 
@@ -105,6 +111,7 @@ bool load_api()
               sym(cu, "cuFuncSetAttribute", g_api.FuncSetAttribute) &&
               sym(cu, "cuLaunchKernel", g_api.LaunchKernel) &&
               sym(cu, "cuMemcpyDtoDAsync_v2", g_api.MemcpyDtoDAsync);
+    if (ok) sym(cu, "cuTensorMapEncodeTiled", g_api.TensorMapEncodeTiled);
     if (!ok) g_api.why = "missing NVRTC / driver symbols";
     g_api.ok = ok;
     return ok;
@@ -273,7 +280,17 @@ __device__ __forceinline__ void px(double2 (&a)[16])
         if (!(r & (1 << J))) { const double2 t = a[r]; a[r] = a[r | (1 << J)]; a[r | (1 << J)] = t; }
 }
 
-__device__ __forceinline__ u32 swz(u32 l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+// GF(2)-linear tile swizzle (16-B slots): the low 3 bits (bank group) are the
+// granule index XOR the fold F of all higher 3-bit chunks; bits 3..5 become F
+// itself.  So a 2^c-amplitude segment (c = 2, 3) lands in one 64 / 128-B row
+// whose chunks are XOR-ed with that row's address bits 7..8 / 7..9 -- exactly
+// the TMA SWIZZLE_64B / 128B pattern -- while the bank of every slot is the
+// same as with the plain fold (conflict analysis unchanged).
+__device__ __forceinline__ u32 swz(u32 l)
+{
+    const u32 f = ((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u;
+    return (l & ~63u) | (f << 3) | ((l ^ f) & 7u);
+}
 __device__ __forceinline__ u32 tb(u32 tid, int i, u32 col) { return (0u - ((tid >> i) & 1u)) & col; }
 __device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
 
@@ -308,17 +325,30 @@ __device__ __forceinline__ void mbar_arrive(u64 *b)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
 __device__ __forceinline__ int ring_bar(int it) { return it % KSTAGES + KSTAGES * ((it / KSTAGES) & 1); }
+__device__ __forceinline__ void mbar_arrive_tx(u64 *b, u32 bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+struct __align__(64) TmapParam { u64 v[16]; };
+// one 2^c-amplitude segment (row y of the 2-D view psi[2^(n-c)][2^(c+1) doubles])
+// -> the 64 / 128-B shared row at dst, chunks XOR-swizzled by the hardware
+__device__ __forceinline__ void tma_row(void *dst, const TmapParam *tm, int y, u64 *bar)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(saddr(dst)), "l"((u64)tm), "r"(0), "r"(y), "r"(saddr(bar)) : "memory");
+}
 
 __device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar, u64 base);
 
 extern "C" __global__ void __launch_bounds__(2 * KT, 1)
 qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_offhi,
-         const int *__restrict__ g_geo, u64 basis)
+         const int *__restrict__ g_geo, u64 basis, const __grid_constant__ TmapParam tmap, int tma)
 {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     u64 *full = reinterpret_cast<u64 *>(smem_raw);
     u32 *st_k = reinterpret_cast<u32 *>(full + 2 * KSTAGES);
-    double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 1024);  // 1024-B aligned stages (TMA swizzle)
     u64 *offhi = reinterpret_cast<u64 *>(bufs + KSTAGES * TSIZE);
     const int nhi = 1 << (12 - c);
     const u32 tid_all = threadIdx.x;
@@ -358,6 +388,15 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
                 buf[swz(l)] = make_double2(gi == basis ? 1.0 : 0.0, 0.0);
             }
             mbar_arrive(full + ring_bar(it));
+            return;
+        }
+        if (tma) {  // TMA: the thread's share of the tile's segments, one row each
+            const int nseg = TSIZE >> c;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // stage reuse (WAR)
+            mbar_arrive_tx(full + ring_bar(it), (u32)(nseg / KT) * (16u << c));
+            for (int h = tid; h < nseg; h += KT)
+                tma_row(buf + (swz((u32)h << c) & ~cmask), &tmap, (int)((b + offhi[h]) >> c),
+                        full + ring_bar(it));
             return;
         }
         const double2 *src = psi + b;
@@ -404,7 +443,17 @@ typedef unsigned int u32;
 #define KT 256
 #define KSTAGES 3
 #define TSIZE 4096
-__device__ __forceinline__ u32 swz(u32 l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+// GF(2)-linear tile swizzle (16-B slots): the low 3 bits (bank group) are the
+// granule index XOR the fold F of all higher 3-bit chunks; bits 3..5 become F
+// itself.  So a 2^c-amplitude segment (c = 2, 3) lands in one 64 / 128-B row
+// whose chunks are XOR-ed with that row's address bits 7..8 / 7..9 -- exactly
+// the TMA SWIZZLE_64B / 128B pattern -- while the bank of every slot is the
+// same as with the plain fold (conflict analysis unchanged).
+__device__ __forceinline__ u32 swz(u32 l)
+{
+    const u32 f = ((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u;
+    return (l & ~63u) | (f << 3) | ((l ^ f) & 7u);
+}
 __device__ __forceinline__ u32 ins0(u32 i, int b) { return ((i >> b) << (b + 1)) | (i & ((1u << b) - 1u)); }
 __device__ __forceinline__ double wsum(double v)
 {
@@ -576,7 +625,7 @@ qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restri
 }
 )QSV";
 
-inline uint32_t h_swz(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+inline uint32_t h_swz(uint32_t l) { return tile_swz(l); }
 inline uint32_t h_ins0(uint32_t i, int b) { return ((i >> b) << (b + 1)) | (i & ((1u << b) - 1u)); }
 
 struct Module {
@@ -1012,8 +1061,14 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
     if (sp.global || sp.geom.m != kMaxTileBits || sp.ndiag != 0 || sp.groups.empty()) return false;
     if (sp.groups.front().pad[0] & 1) return false;  // wide groups: interpreted transform path
     {
-        const char *env_cs = getenv("QSV_SWEEP_COSET");  // 0: pair-bit sweep (A/B)
-        if (!(env_cs && env_cs[0] == '0') && jit_sweep_source_coset(sp, src)) return true;
+        // QSV_SWEEP_COSET=1: register-coset sweep.  A/B on config 3 (B200,
+        // profiles/r02_expect30_coset_launches.csv): shared-memory wavefronts
+        // 73-84 % -> 52 % of peak, but the same 0.76-0.77 s per expectation --
+        // once SMEM is relieved the sweep is latency-bound (16 warps/SM at 128
+        // registers, FP64 pipe ~36 %), so the pair-bit sweep (fewer spills)
+        // stays the default.
+        const char *env_cs = getenv("QSV_SWEEP_COSET");
+        if (env_cs && env_cs[0] == '1' && jit_sweep_source_coset(sp, src)) return true;
     }
     if (sp.groups.front().pad[0] & 1) return false;  // wide groups: interpreted transform path
     const int nterms = (int)sp.terms.size();
@@ -1231,6 +1286,33 @@ const void *jit_module(int device, const std::string &src)
     return &it->second;
 }
 
+// TMA staging of the pass tiles (QSV_PASS_TMA=1; A/B against LDGSTS, which
+// stays the default): the state as a 2-D tensor [2^(n-3) segments][16
+// doubles], one box = one 128-B segment landing in its tile row with the
+// hardware SWIZZLE_128B (= the tile swizzle's row layout, qsv_internal.h
+// tile_swz).  Measured on B200 (profiles/r02_tma_ab.txt): config 2 76.8 ms vs
+// 70.1 ms with LDGSTS, 30 q UCC on 128-B tiles 4.46 s vs 4.33 s -- 512 TMA
+// ops of 128 B per 64 KiB tile cost more than the 16 LDGSTS per thread they
+// replace.  64-B segments (c = 2) cannot use it: a swizzled TMA destination
+// must be 128-B aligned (the c = 2 run faulted with a misaligned address).
+bool pass_tma_map(double2 *psi, const TileDims &g, CUtensorMap *out)
+{
+    static const char *env = getenv("QSV_PASS_TMA");
+    if (!(env && env[0] == '1') || !g_api.TensorMapEncodeTiled) return false;
+    if (g.m != kMaxTileBits || g.c != 3) return false;
+    const int n = g.ncomp + g.m;
+    if (n - g.c > 31) return false;  // row coordinates are signed 32-bit
+    cuuint64_t dims[2] = {(cuuint64_t)(2u << g.c), (cuuint64_t)1 << (n - g.c)};
+    cuuint64_t strides[1] = {(cuuint64_t)16 << g.c};
+    cuuint32_t box[2] = {(cuuint32_t)(2u << g.c), 1};
+    cuuint32_t estr[2] = {1, 1};
+    return g_api.TensorMapEncodeTiled(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)psi, dims, strides,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      g.c == 3 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == 0;
+}
+
 bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const uint64_t *d_offhi,
                        const int32_t *d_geo, const double *d_params, int nparams, int grid,
                        cudaStream_t st, uint64_t basis)
@@ -1241,8 +1323,11 @@ bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const u
         if (g_api.MemcpyDtoDAsync(m.cparams, (CUdeviceptr)d_params, (size_t)nparams * 8, st) != 0)
             return false;
     int ncomp = g.ncomp, c = g.c;
-    void *args[] = {&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo, &basis};
-    const unsigned smem = 256 + 3 * (16u << kMaxTileBits) + 8u * (1u << (kMaxTileBits - g.c));
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    int tma = pass_tma_map(psi, g, &tmap) ? 1 : 0;
+    void *args[] = {&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo, &basis, &tmap, &tma};
+    const unsigned smem = 1024 + 3 * (16u << kMaxTileBits) + 8u * (1u << (kMaxTileBits - g.c));
     return g_api.LaunchKernel(m.fn, (unsigned)grid, 1, 1, 512, 1, 1, smem, st, args, nullptr) == 0;
 }
 

@@ -776,7 +776,7 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
     t.n_items = (int64_t)items.size();
 }
 
-inline uint16_t swz16(uint32_t l) { return (uint16_t)(l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u)); }
+inline uint16_t swz16(uint32_t l) { return (uint16_t)tile_swz(l); }
 
 // Group a pass's tile-local ops into register blocks of <= 4 logical tile
 // bits, fold the permutation gates (CNOT / SWAP / X) into the pass's
@@ -1280,7 +1280,7 @@ void geom_tables(const TileGeom &g, std::vector<uint64_t> &offhi, std::vector<in
     for (int i = 0; i < g.ncomp && i < 32; ++i) comp32[i] = g.comp[i];
     for (int b = 0; b < 12; ++b) {
         const uint32_t l = 1u << b;
-        comp32[32 + b] = pp ? pp->store_cols[b] : (int32_t)(l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u));
+        comp32[32 + b] = pp ? pp->store_cols[b] : (int32_t)tile_swz(l);
     }
     comp32[44] = pp ? pp->store_t : 0;
 }

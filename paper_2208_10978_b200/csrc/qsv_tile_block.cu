@@ -35,12 +35,8 @@ __device__ __forceinline__ uint32_t ins0(uint32_t i, int b)
     return ((i >> b) << (b + 1)) | (i & ((1u << b) - 1u));
 }
 
-// GF(2)-linear swizzle: XOR the 16 B granule index (low 3 bits) with the
-// fold of all higher 3-bit chunks.  Bijective on [0, 4096).
-__device__ __forceinline__ uint32_t swz(uint32_t l)
-{
-    return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
-}
+// GF(2)-linear swizzle (qsv_internal.h tile_swz).  Bijective on [0, 2^m).
+__device__ __forceinline__ uint32_t swz(uint32_t l) { return tile_swz(l); }
 
 __device__ __forceinline__ double2 cfma2(double2 m0, double2 x, double2 m1, double2 y)
 {

@@ -34,6 +34,18 @@ def apply_2q(state, matrix, q0: int, q1: int) -> None:
     _lib.check(_lib.lib().qsv_apply_2q(state.handle, _lib.dptr(m.view(np.float64)), int(q0), int(q1)))
 
 
+def apply_matrix(state, matrix, qubits) -> None:
+    """In-place dense k-qubit gate (k = 1..5); rows indexed by the target bits
+    with qubits[0] as the most significant (the apply_2q convention,
+    _cykernels.pyx:41-73, extended to k qubits)."""
+    qs = np.ascontiguousarray([int(q) for q in qubits], dtype=np.int32)
+    k = len(qs)
+    m = np.ascontiguousarray(matrix, dtype=np.complex128)
+    if m.shape != (1 << k, 1 << k):
+        raise ValueError(f"apply_matrix expects a {1 << k}x{1 << k} matrix for {k} qubits")
+    _lib.check(_lib.lib().qsv_apply_matrix(state.handle, k, _lib.i32ptr(qs), _lib.dptr(m.view(np.float64))))
+
+
 def apply_pauli(state, x_mask: int, y_mask: int, z_mask: int, out) -> None:
     """Fill ``out`` with P|state> (_cykernels.pyx:76-102)."""
     _lib.check(_lib.lib().qsv_apply_pauli(state.handle, out.handle, int(x_mask), int(y_mask),

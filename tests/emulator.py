@@ -17,7 +17,10 @@ OP_U1, OP_U2, OP_CX, OP_SWAP, OP_X, OP_DIAG1, OP_ROTG, OP_ROTD, OP_GMAT = 1, 2, 
 
 
 def swz(l):
-    return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7)
+    """Tile swizzle (qsv_internal.h tile_swz): bits 0..2 = (l ^ F) & 7, bits
+    3..5 = F, F = fold of the higher 3-bit chunks."""
+    f = ((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7
+    return (l & ~63) | (f << 3) | ((l ^ f) & 7)
 
 
 def popc(x):

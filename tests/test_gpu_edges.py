@@ -11,6 +11,7 @@ from oracle import oracle as O
 from paper_2208_10978_b200 import statevector as sv
 from paper_2208_10978_b200 import workloads as W
 from paper_2208_10978_b200.circuit import Circuit, Constant, Gate
+from paper_2208_10978_b200.errors import ResourceLimitError
 from paper_2208_10978_b200.pauli import PauliString, PauliSum, PauliTerm
 
 pytestmark = pytest.mark.gpu
@@ -143,3 +144,72 @@ def test_prepared_program_and_async_download_errors():
     out.wait_download()  # nothing pending
     ref = O.evolve(O.init_state("000000"), W.rotations_circuit(6, strings, np.full(len(strings), 0.1)).gates)
     assert np.abs(out.amplitudes - ref).max() <= 1e-10
+
+
+def _dense_ref(st, m, qubits):
+    """The apply_2q convention (_cykernels.pyx:41-73: row = 2*bit(q0) +
+    bit(q1)) for k targets: row bit (k-1-i) is the bit of qubits[i]."""
+    k = len(qubits)
+    out = st.copy()
+    idx = np.arange(st.size, dtype=np.int64)
+    mask = sum(1 << q for q in qubits)
+    base = idx[(idx & mask) == 0]
+    offs = [sum(((r >> (k - 1 - i)) & 1) << q for i, q in enumerate(qubits)) for r in range(1 << k)]
+    a = np.stack([st[base | o] for o in offs])  # [2^k, cosets]
+    b = m @ a
+    for r, o in enumerate(offs):
+        out[base | o] = b[r]
+    return out
+
+
+@pytest.mark.parametrize("n,qubits", [(9, (4,)), (9, (2, 7)), (10, (0, 5, 3)), (11, (8, 1, 9, 2)),
+                                      (12, (3, 11, 0, 6, 1)), (14, (13, 12, 11, 10, 9))])
+def test_apply_matrix_general_k(n, qubits):
+    """qsv_apply_matrix (k = 1..5) vs a NumPy restatement of the apply_2q index
+    convention; k = 1, 2 also vs the reference's own apply_1q / apply_2q
+    (oracle); a Kronecker product equals the single-qubit gates in sequence."""
+    from oracle import oracle as O
+    from paper_2208_10978_b200 import kernels
+
+    rng = np.random.default_rng(n + len(qubits))
+    k = len(qubits)
+    a = rng.standard_normal((1 << k, 1 << k)) + 1j * rng.standard_normal((1 << k, 1 << k))
+    m, _ = np.linalg.qr(a)
+    st = random_state(n, rng)
+    s = sv.from_amplitudes(st)
+    kernels.apply_matrix(s, m, qubits)
+    out = s.amplitudes
+    assert np.abs(out - _dense_ref(st, m, qubits)).max() <= 1e-12
+    if k == 1:
+        ref = st.copy()
+        O.apply_1q(ref, m, qubits[0])
+        assert np.abs(out - ref).max() <= 1e-12
+    if k == 2:
+        ref = st.copy()
+        O.apply_2q(ref, m, qubits[0], qubits[1])
+        assert np.abs(out - ref).max() <= 1e-12
+    # Kronecker convention: qubits[0] is the most significant factor
+    us = [np.linalg.qr(rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2)))[0] for _ in qubits]
+    kr = us[0]
+    for u in us[1:]:
+        kr = np.kron(kr, u)
+    s2 = sv.from_amplitudes(st)
+    kernels.apply_matrix(s2, kr, qubits)
+    ref = st.copy()
+    for u, q in zip(us, qubits):
+        O.apply_1q(ref, u, q)
+    assert np.abs(s2.amplitudes - ref).max() <= 1e-12
+
+
+def test_apply_matrix_errors():
+    from paper_2208_10978_b200 import kernels
+
+    s = sv.from_amplitudes(random_state(8, np.random.default_rng(1)))
+    with pytest.raises(ValueError):
+        kernels.apply_matrix(s, np.eye(4), (3, 3))  # duplicate qubit
+    with pytest.raises(ValueError):
+        kernels.apply_matrix(s, np.eye(4), (3, 8))  # out of range
+    with pytest.raises(ValueError):
+        kernels.apply_matrix(s, np.eye(8), (1, 2))  # shape mismatch
+    with pytest.raises(ResourceLimitError):
+        kernels.apply_matrix(s, np.eye(64), (0, 1, 2, 3, 4, 5))  # k > 5
