@@ -262,3 +262,25 @@ def test_expectation_parallel_two_ranks_gloo():
         single = engine.expectation_parallel(_HostState(st), h, engine.plan_partition(h, w),
                                              engine=_OraclePerTerm())
         assert res[0][w] == res[1][w] == single
+
+
+@pytest.mark.parametrize("create,annihilate", [((7,), (2,)), ((9,), (0,)), ((6, 11), (3, 1)),
+                                               ((8, 10), (5, 4)), ((31, 16), (15, 0))])
+def test_jw_excitation_strings_equal_reference_jordan_wigner(create, annihilate):
+    """workloads.excitation_strings (the generator behind configs 1 and 4) vs
+    the reference's own fermion.jordan_wigner of T - T^dagger (fermion.py:345):
+    same strings, same coefficients (1e-15), and -- after the canonical sort
+    -- the same order."""
+    _ref_engine()  # puts oracle/_ref on sys.path (skips if absent)
+    import vqekit.fermion as RF
+
+    ops = [(m, True) for m in create] + [(m, False) for m in annihilate]
+    t = RF.FermionSum.from_terms([(1.0, ops)])
+    ref = RF.jordan_wigner(t - t.dagger())
+    ref_terms = sorted(((tt.string.factors, complex(tt.coefficient)) for tt in ref.terms),
+                       key=lambda kv: kv[0])
+    ours = W.excitation_strings(create, annihilate)
+    assert [s.factors for _, s in ours] == [f for f, _ in ref_terms]
+    for (c, _), (_, rc) in zip(ours, ref_terms):
+        assert abs(c - rc) <= 1e-15
+    assert len(ours) == (2 if len(create) == 1 else 8)
