@@ -243,7 +243,7 @@ std::string planner_knobs()
                                   "QSV_PASS_COST_CAP", "QSV_SCHED_SEEDS", "QSV_SCHED",
                                   "QSV_SCHED_WINDOW", "QSV_PHASE_DEFER", "QSV_WARP_LOCAL",
                                   "QSV_BLOCK_PARTITION", "QSV_INREG_PERMS", "QSV_SWEEP_TERMS",
-                                  "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS"};
+                                  "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS", "QSV_TILE_BITS"};
     std::string k;
     for (const char *nm : names) {
         const char *v = getenv(nm);

@@ -43,6 +43,8 @@ inline int local_of(const TileGeom &g, int q)
 void choose_tile(int n, int &m, int &c)
 {
     m = n < kMaxTileBits ? n : kMaxTileBits;
+    if (const char *env_m = getenv("QSV_TILE_BITS"))  // experiment: smaller tiles (more CTAs)
+        m = std::max(6, std::min(m, atoi(env_m)));
     if (m == n) {
         c = n;
     } else {

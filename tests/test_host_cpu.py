@@ -284,3 +284,43 @@ def test_jw_excitation_strings_equal_reference_jordan_wigner(create, annihilate)
     for (c, _), (_, rc) in zip(ours, ref_terms):
         assert abs(c - rc) <= 1e-15
     assert len(ours) == (2 if len(create) == 1 else 8)
+
+
+def test_integration_install_dispatches_host_states_to_the_reference():
+    """integration.install wraps exactly four reference attributes; host
+    (reference) states still go to the reference's own functions, and
+    uninstall restores the originals (no GPU needed)."""
+    RE, RP = _ref_engine()
+    import json
+    import os
+
+    import vqekit
+    import vqekit.circuit as RC
+    import vqekit.statevector as RSV
+
+    from conftest import GOLDEN
+    from paper_2208_10978_b200 import integration
+
+    with open(os.path.join(GOLDEN, "h2_sto3g.json")) as fh:
+        fx = json.load(fh)["h2_sto3g_d0735.fcidump"]
+    h = RP.read_pauli_sum(io.StringIO(fx["hamiltonian"]))
+    ansatz = RC.circuit_from_json(fx["ansatz"])
+    s0 = RSV.init_state(fx["reference"])
+    theta = np.array([0.1, -0.2])
+    before = (RSV.reverse_gradient, RSV.reverse_gradient_general, RSV.apply_operator,
+              RE.expectation_parallel)
+    g0 = RSV.reverse_gradient(ansatz, theta, h, s0)
+    integration.install(vqekit)
+    try:
+        assert integration.installed()
+        assert RSV.reverse_gradient is not before[0] and RE.expectation_parallel is not before[3]
+        assert np.array_equal(RSV.reverse_gradient(ansatz, theta, h, s0), g0)
+        st = RSV.evolve(s0, RC.bind(ansatz, theta))
+        plan = RE.plan_partition(h, 2)
+        assert RE.expectation_parallel(st, h, plan) == before[3](st, h, plan)
+        assert np.array_equal(RSV.apply_operator(st, h).amplitudes, before[2](st, h).amplitudes)
+    finally:
+        integration.uninstall()
+    assert (RSV.reverse_gradient, RSV.reverse_gradient_general, RSV.apply_operator,
+            RE.expectation_parallel) == before
+    assert not integration.installed()
