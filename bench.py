@@ -77,9 +77,11 @@ def fp64_roofline(t_step: float, passes: int, nominal_dfma: int, hbm: dict) -> d
            "kernel": "qsv_pass (NVRTC-specialised tile pass)", "traffic": hbm["traffic"],
            "nominal_dfma_per_step": nominal_dfma,
            "nominal_note": "8 DFMA per amplitude per dense 2x2 complex gate (SURVEY 8(d)); the "
-                           "kernels issue fewer (real m00, phase deferral)",
+                           "kernels issue fewer (normalised U3 forms: 6 per amplitude, 4 for "
+                           "phase-deferred shears)",
            "hbm": hbm}
-    if counts and counts.get("passes") == passes:
+    norm_now = os.environ.get("QSV_U3_NORM", "1") != "0"
+    if counts and counts.get("passes") == passes and bool(counts.get("u3_norm")) == norm_now:
         flops = 2 * counts["dfma"] + counts["dmul"] + counts["dadd"]
         inst = counts["dfma"] + counts["dmul"] + counts["dadd"]
         out.update({"achieved": flops / t_step / 1e12, "frac": flops / t_step / 1e12 / out["peak"],

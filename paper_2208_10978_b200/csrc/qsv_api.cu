@@ -243,15 +243,22 @@ std::string planner_knobs()
                                   "QSV_PASS_COST_CAP", "QSV_SCHED_SEEDS", "QSV_SCHED",
                                   "QSV_SCHED_WINDOW", "QSV_PHASE_DEFER", "QSV_WARP_LOCAL",
                                   "QSV_BLOCK_PARTITION", "QSV_INREG_PERMS", "QSV_SWEEP_TERMS",
-                                  "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS", "QSV_TILE_BITS"};
+                                  "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS", "QSV_TILE_BITS",
+                                  "QSV_U3_NORM"};
     std::string k;
     for (const char *nm : names) {
         const char *v = getenv(nm);
         k += v ? v : "-";
         k += '|';
     }
+    if (plain_u3()) k += "plain";
     return k;
 }
+
+struct PlainU3Scope {
+    PlainU3Scope() { set_plain_u3(true); }
+    ~PlainU3Scope() { set_plain_u3(false); }
+};
 
 // Cache of structural gate plans.
 struct CacheEntry {
@@ -932,6 +939,11 @@ static int apply_gates_impl(qsv_state *s, int64_t n_gates, const int32_t *kinds,
         tpl = &g_cache.front().tpl;
     }
     prof.mark("lookup");
+    if (!plain_u3() && needs_plain_u3(*tpl, values)) {
+        // an angle the normalised U3 forms cannot take: a plan without them
+        PlainU3Scope plain;
+        return apply_gates_impl(s, n_gates, kinds, qubits, values, stats, basis);
+    }
     CacheEntry &ce = g_cache.front();
     const bool dev_gmats = fast_path(s, *tpl, &ce.jc, ce.uses + 1) && !tpl->gfills.empty();
     std::vector<double> params(tpl->n_params);
@@ -1030,6 +1042,10 @@ static int apply_prepared_impl(qsv_state *s, int64_t program_id, const double *v
     }
     if (bad) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
     QSV_CUDA(cudaSetDevice(s->device));
+    if (!plain_u3() && needs_plain_u3(e.tpl, values)) {
+        PlainU3Scope plain;  // structure-cache path with a plan without normalised U3 forms
+        return apply_gates_impl(s, n_gates, e.kinds.data(), e.qubits.data(), values, stats, basis);
+    }
     const bool hit = e.uses > 0;
     ++e.uses;
     const bool dev_gmats = fast_path(s, e.tpl, &e.jc, e.uses) && !e.tpl.gfills.empty();

@@ -132,7 +132,7 @@ __device__ __forceinline__ double2 cmul(double ar, double ai, double2 x)
 }
 
 // dense 2x2 on register bit J; K = 0 general, 1 m00 real, 2 all real,
-// 3 m00 and m10 real
+// 3 m00 and m10 real, 4 m00 = 1, 6 m00 = m11 = 1
 template <int J, int K, int P>
 __device__ __forceinline__ void u1(double2 (&a)[16])
 {
@@ -146,6 +146,16 @@ __device__ __forceinline__ void u1(double2 (&a)[16])
             o0.y = fma(C[P], x.y, C[P + 2] * y.y);
             o1.x = fma(C[P + 4], x.x, C[P + 6] * y.x);
             o1.y = fma(C[P + 4], x.y, C[P + 6] * y.y);
+        } else if (K == 4) {  // m00 = 1 (U3 divided by cos(theta/2), qsv_planner.cpp U3Norm)
+            o0.x = fma(C[P + 2], y.x, fma(-C[P + 3], y.y, x.x));
+            o0.y = fma(C[P + 2], y.y, fma(C[P + 3], y.x, x.y));
+            o1.x = fma(C[P + 4], x.x, fma(-C[P + 5], x.y, fma(C[P + 6], y.x, -C[P + 7] * y.y)));
+            o1.y = fma(C[P + 4], x.y, fma(C[P + 5], x.x, fma(C[P + 6], y.y, C[P + 7] * y.x)));
+        } else if (K == 6) {  // m00 = m11 = 1: the shear of a phase-deferred U3 (U3Norm)
+            o0.x = fma(C[P + 2], y.x, fma(-C[P + 3], y.y, x.x));
+            o0.y = fma(C[P + 2], y.y, fma(C[P + 3], y.x, x.y));
+            o1.x = fma(C[P + 4], x.x, fma(-C[P + 5], x.y, y.x));
+            o1.y = fma(C[P + 4], x.y, fma(C[P + 5], x.x, y.y));
         } else if (K == 3) {  // m00 and m10 real (phase-deferred U3)
             o0.x = fma(C[P], x.x, fma(C[P + 2], y.x, -C[P + 3] * y.y));
             o0.y = fma(C[P], x.y, fma(C[P + 2], y.y, C[P + 3] * y.x));
@@ -792,7 +802,7 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
         for (int k = B.op0; k < B.op1; ++k) {
             const OpRec &op = ops[k];
             if (op.type == OP_U1) {
-                const int cls = (op.h >= 0 && op.h <= 3) ? op.h : 0;
+                const int cls = ((op.h >= 0 && op.h <= 4) || op.h == 6) ? op.h : 0;
                 snprintf(buf, sizeof(buf), "    u1<%d, %d, %d>(a);\n", op.a, cls, op.p);
             } else if (op.type == OP_U2) {
                 snprintf(buf, sizeof(buf), "    u2<%d, %d, %d>(a);\n", op.a, op.b, op.p);

@@ -664,6 +664,60 @@ void cluster_matrix(const ClusterFill &cf, const int32_t *kinds, const int32_t *
 
 void block_pass(ProgramTemplate &t, PassPlan &pp);
 
+// U3Norm.  A U3 (FP64-bound brickwork) costs 14 FP64 instructions per pair
+// (12 phase-deferred).  Dividing the gate by a real scalar changes only a
+// global factor, and the factors of one pass are multiplied back into ONE of
+// its gates (the sink), so the pass's output is exact:
+//   mode 4: U3 / c, c = cos(theta/2): m00 = 1 -> row 0 is 2 DFMA per
+//           component: 12 per pair;
+//   mode 6 (phase-deferring U3, see PhaseDefer):
+//           U3(t, 0, l) = c diag(1, e^{il}) [[1, -e^{il} tan], [e^{-il} tan, 1]]
+//           -- the diag(1, e^{il}) is deferred with the phi phase (it commutes
+//           with the CNOT control and lands in the next U3's lambda), the
+//           shear costs 8 per pair.
+// Brickwork (config 2): 12.7 -> ~10 FP64 instructions per pair per U3.  An
+// angle with |cos(theta/2)| < 1e-3 sends the call to a plan without the
+// normalised forms (set_plain_u3), so tan never blows up.
+void assign_u3_norm(ProgramTemplate &t, const PassPlan &pp, int pass, const int32_t *kinds)
+{
+    if ((int)t.pass_sink.size() <= pass) t.pass_sink.resize(pass + 1, -1);
+    if (t.fill_mode.size() < t.fills.size()) {
+        t.fill_mode.resize(t.fills.size(), 0);
+        t.fill_pass.resize(t.fills.size(), -1);
+    }
+    const char *env = getenv("QSV_U3_NORM");
+    if (plain_u3() || (env && env[0] == '0')) return;
+    // the pass's plain U3 ops and their fills
+    std::vector<std::pair<int, int>> u3;  // (op index, fill index)
+    for (int k = pp.op_begin; k < pp.op_end; ++k) {
+        const OpRec &op = t.ops[k];
+        if (op.type != OP_U1 || op.p < 0) continue;
+        for (size_t f = 0; f < t.fills.size(); ++f)
+            if (t.fills[f].offset == op.p && t.fills[f].kind == K_U3) {
+                u3.push_back({k, (int)f});
+                break;
+            }
+    }
+    if (u3.size() < 2) return;
+    // sink: a non-deferring U3 if there is one (it loses 2 of 14, a deferring one 4 of 12)
+    size_t sink = 0;
+    for (size_t i = 0; i < u3.size(); ++i)
+        if (t.ops[u3[i].first].h != 3) {
+            sink = i;
+            break;
+        }
+    t.pass_sink[pass] = u3[sink].second;
+    for (size_t i = 0; i < u3.size(); ++i) {
+        t.fill_pass[u3[i].second] = pass;
+        if (i == sink) continue;
+        OpRec &op = t.ops[u3[i].first];
+        const int mode = op.h == 3 ? 6 : 4;
+        op.h = mode;
+        t.fill_mode[u3[i].second] = (int8_t)mode;
+    }
+    (void)kinds;
+}
+
 void emit_program(int n, int m, int c, const std::vector<Item> &items, const std::vector<Rot> &R,
                   const int32_t *kinds, const int32_t *qubits, const Schedule &S,
                   ProgramTemplate &t)
@@ -772,6 +826,7 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
             t.ops.push_back(op);
         }
         pp.op_end = (int)t.ops.size();
+        assign_u3_norm(t, pp, (int)t.passes.size(), kinds);
         if (g.m >= kBlockBits + 1) block_pass(t, pp);
         t.passes.push_back(pp);
     }
@@ -1209,6 +1264,19 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
 
 }  // namespace
 
+thread_local bool t_plain_u3 = false;
+void set_plain_u3(bool on) { t_plain_u3 = on; }
+bool plain_u3() { return t_plain_u3; }
+
+bool needs_plain_u3(const ProgramTemplate &t, const double *values)
+{
+    for (size_t f = 0; f < t.fill_mode.size(); ++f)
+        if (t.fill_mode[f] && std::fabs(std::cos(0.5 * values[3 * (size_t)t.fills[f].src])) < 1e-3)
+            return true;
+    return false;
+}
+
+
 int gate_matrix(int kind, const double *v, double *o)
 {
     // circuit.py:36-45 (fixed), :164-171 (_u3_matrix), :198-223 (gate_matrix)
@@ -1442,16 +1510,34 @@ void materialize_gates(ProgramTemplate &t, const double *values)
 void materialize_params(ProgramTemplate &t, const double *values, double *params, bool with_gmats)
 {
     materialize_gates(t, values);
-    if (t.defers.empty()) {
+    const bool norm = !t.fill_mode.empty() && !t.pass_sink.empty();
+    if (t.defers.empty() && !norm) {
         for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, params + f.offset);
     } else {
-        std::unordered_map<int, double> add_lambda;  // receiving gate -> phi of its source
+        // deferred phases: a deferring U3 hands phi (and, in shear mode, its
+        // effective lambda) to its receiving U3; processed in gate order so
+        // chains of deferrals accumulate
+        std::unordered_map<int, int8_t> mode_of;  // gate -> fill mode
+        if (norm)
+            for (size_t f = 0; f < t.fills.size(); ++f)
+                if (f < t.fill_mode.size() && t.fill_mode[f]) mode_of[t.fills[f].src] = t.fill_mode[f];
+        std::vector<PhaseDefer> ds = t.defers;
+        std::sort(ds.begin(), ds.end(), [](const PhaseDefer &a, const PhaseDefer &b) { return a.src < b.src; });
+        std::unordered_map<int, double> add_lambda;  // receiving gate -> deferred phase
         std::unordered_map<int, char> deferring;
-        for (const PhaseDefer &d : t.defers) {
-            add_lambda[d.dst] += values[3 * (size_t)d.src + 1];
+        for (const PhaseDefer &d : ds) {
             deferring[d.src] = 1;
+            double give = values[3 * (size_t)d.src + 1];  // phi
+            auto m = mode_of.find(d.src);
+            if (m != mode_of.end() && m->second == 6) {
+                auto a = add_lambda.find(d.src);
+                give += values[3 * (size_t)d.src + 2] + (a != add_lambda.end() ? a->second : 0.0);
+            }
+            add_lambda[d.dst] += give;
         }
-        for (const ParamFill &f : t.fills) {
+        std::vector<double> mu(t.pass_sink.size(), 1.0);
+        for (size_t fi = 0; fi < t.fills.size(); ++fi) {
+            const ParamFill &f = t.fills[fi];
             const double *v = values + 3 * (size_t)f.src;
             if (f.kind != K_U3) {
                 gate_matrix(f.kind, v, params + f.offset);
@@ -1461,8 +1547,33 @@ void materialize_params(ProgramTemplate &t, const double *values, double *params
             auto it = add_lambda.find(f.src);
             if (it != add_lambda.end()) vv[2] += it->second;
             if (deferring.count(f.src)) vv[1] = 0.0;  // V = U3(t, 0, l): the phi phase moves on
-            gate_matrix(K_U3, vv, params + f.offset);
+            const int mode = norm && fi < t.fill_mode.size() ? t.fill_mode[fi] : 0;
+            double *o = params + f.offset;
+            if (mode == 6) {  // c diag(1, e^{il}) [[1, -e^{il} tn], [e^{-il} tn, 1]]
+                const double c = std::cos(0.5 * vv[0]), tn = std::tan(0.5 * vv[0]);
+                const double cl = std::cos(vv[2]), sl = std::sin(vv[2]);
+                o[0] = 1.0; o[1] = 0.0;
+                o[2] = -cl * tn; o[3] = -sl * tn;
+                o[4] = cl * tn; o[5] = -sl * tn;
+                o[6] = 1.0; o[7] = 0.0;
+                mu[t.fill_pass[fi]] *= c;
+                continue;
+            }
+            gate_matrix(K_U3, vv, o);
+            if (mode == 4) {  // U3 / c: m00 = 1 exactly
+                const double c = o[0], inv = 1.0 / c;
+                for (int k = 2; k < 8; ++k) o[k] *= inv;
+                o[0] = 1.0;
+                o[1] = 0.0;
+                mu[t.fill_pass[fi]] *= c;
+            }
         }
+        if (norm)
+            for (size_t p = 0; p < t.pass_sink.size(); ++p)
+                if (t.pass_sink[p] >= 0 && mu[p] != 1.0) {
+                    double *o = params + t.fills[t.pass_sink[p]].offset;
+                    for (int k = 0; k < 8; ++k) o[k] *= mu[p];
+                }
     }
     for (const ClusterFill &cf : t.cfills)
         if (cf.offset >= 0)

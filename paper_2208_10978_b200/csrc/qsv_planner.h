@@ -88,6 +88,13 @@ struct ProgramTemplate {
     std::vector<GmatFill> gfills;  // fused group tables refreshed per call
     std::vector<ClusterFill> cfills;  // dense-fused gate clusters refreshed per call
     std::vector<PhaseDefer> defers;   // U3 phase deferrals (see PhaseDefer)
+    // Normalised U3 forms (see U3Norm in qsv_planner.cpp), per ParamFill:
+    // 0 plain, 4 row 0 divided by m00 (m00 = 1), 6 shear (m00 = m11 = 1,
+    // both phases deferred); the pass's product of the divisors multiplies
+    // its sink fill.
+    std::vector<int8_t> fill_mode;
+    std::vector<int> fill_pass;
+    std::vector<int> pass_sink;       // per pass: ParamFill index of the sink, -1: none
     size_t n_params = 0;
     // global-fallback rotation records (full 64-bit masks), per pass: rots[r0..r1)
     int64_t n_input = 0, n_rotations = 0, n_items = 0, n_fallback = 0, n_blocks = 0;
@@ -114,6 +121,13 @@ void materialize_gmats(const ProgramTemplate &t, double *params);
 // fused cluster matrices, fused group tables) into params[t.n_params];
 // refreshes t.rots first.
 // with_gmats = false: leave the OP_GMAT tables to the device (gmat fill kernel)
+// Plain (un-normalised) U3 forms for the next plans of this thread: set when
+// a call's angles make a normalised form ill-conditioned (|cos(theta/2)| tiny).
+void set_plain_u3(bool on);
+bool plain_u3();
+// True if the template uses a normalised U3 form these angles cannot take.
+bool needs_plain_u3(const ProgramTemplate &t, const double *values);
+
 void materialize_params(ProgramTemplate &t, const double *values, double *params,
                         bool with_gmats = true);
 // Gate matrix restatement of circuit.py:198-223 (row-major complex128).

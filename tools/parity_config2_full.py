@@ -1,12 +1,14 @@
 """Full-size parity of the headline workload: config 2 (28-qubit brickwork,
-830 gates) on the B200 vs the C oracle (oracle/liboracle.so, one core,
-~20 min), same seeded gates.  Prints max |d psi|, ||d psi||_2 and the norms."""
+830 gates) on the B200 vs the C oracle (oracle/liboracle.so; ORACLE_THREADS
+OpenMP threads, bit-identical to one core, which takes ~10-20 min), same seeded
+gates.  Prints max |d psi|, ||d psi||_2 and the norms."""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np
 from oracle import oracle as O
 from paper_2208_10978_b200 import statevector as sv, workloads as W
 
+O.set_threads(int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1)))
 n = 28
 circ = W.brickwork(n, 20, seed=0)
 t0 = time.perf_counter()
