@@ -626,12 +626,25 @@ qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restri
         asm volatile("cp.async.wait_all;" ::: "memory");
     }
     // one row per (CTA, warp): reduce_columns sums rows in a fixed order
+#ifdef SWEEP_COLS_ON
+    // per-warp string sets: the row has one column per string of the sweep
+    double *row = partial + (size_t)(blockIdx.x * 16 + grp * 8 + warp) * NTERMS;
+    for (int i = lane; i < NTERMS; i += 32) row[i] = 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < MAXT; ++i) {
+        const double v = wsum(acc[i]);
+        const int col = SWEEP_COLS[warp * MAXT + i];
+        if (lane == 0 && col >= 0) row[col] = v;
+    }
+#else
     double *row = partial + (size_t)(blockIdx.x * 16 + grp * 8 + warp) * MAXT;
 #pragma unroll
     for (int i = 0; i < MAXT; ++i) {
         const double v = wsum(acc[i]);
         if (lane == 0) row[i] = v;
     }
+#endif
 }
 )QSV";
 
@@ -851,6 +864,256 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
 // longest-processing-time on cost = pairs x (2 + 2 + terms); each warp keeps
 // one per-lane accumulator per string across all of its tiles, so the warp
 // reduction happens once per kernel instead of once per (tile, string).
+// Pair-bit sweep code for the flip groups gl (in that order): per H run one
+// load of the l0-side amplitudes, per group (or share class) the l1-side
+// loads, products, 8-point transform / direct sums; string t accumulates
+// into acc[slot[t]].  Uses `pl` (0..255, the thread's pair base) and `base`.
+static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, const std::vector<int> &slot,
+                         std::string &fn)
+{
+    char buf[512];
+    int prev_h = -1;
+    // a component with <= kDirect strings skips its 8-point transform
+    // (24 adds) and sums each string's 8 products directly (7 adds)
+    const int kDirect = 3;
+    auto direct = [&](const GroupRec &G) {
+        return G.t_im - G.t0 <= kDirect && G.t1 - G.t_im <= kDirect;
+    };
+    // tile positions of pair bits 8..10 for highest flip bit H (ins0 skips H)
+    auto rpos = [](int H, int k) { return (8 + k) + ((8 + k) >= H ? 1 : 0); };
+    const char *env_share = getenv("QSV_SWEEP_SHARE");
+    const bool share = !(env_share && env_share[0] == '0');
+    auto sign_expr = [&](const TermRec &tr) {
+        snprintf(buf, sizeof(buf), "((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g",
+                 tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
+        return std::string(buf);
+    };
+    size_t gi = 0;
+    while (gi < gl.size()) {
+        const GroupRec &G = sp.groups[gl[gi]];
+        if (G.h != prev_h) {  // new run of groups with this highest flip bit
+            if (prev_h >= 0) fn += "  }\n";
+            snprintf(buf, sizeof(buf), "  { double2 X[8];\n    const u32 b0 = load_x<%d>(sm, pl, X);\n", G.h);
+            fn += buf;
+            prev_h = G.h;
+        }
+        if (share && direct(G)) {
+            // groups whose flips differ from G's only in the pair-bit positions
+            // 8..10 read a permutation of G's l1-side amplitudes: ONE load of
+            // y_j serves them all (member k uses pair j ^ d_k)
+            uint32_t R = 0;
+            for (int k = 0; k < 3; ++k) R |= 1u << rpos(G.h, k);
+            std::vector<std::pair<size_t, unsigned>> cls{{gl[gi], 0u}};
+            size_t k = gi + 1;
+            while (k < gl.size() && sp.groups[gl[k]].h == G.h && direct(sp.groups[gl[k]]) &&
+                   ((sp.groups[gl[k]].f_loc ^ G.f_loc) & ~R) == 0) {
+                const uint32_t D = sp.groups[gl[k]].f_loc ^ G.f_loc;
+                unsigned d = 0;
+                for (int q = 0; q < 3; ++q) d |= ((D >> rpos(G.h, q)) & 1u) << q;
+                cls.push_back({gl[k], d});
+                ++k;
+            }
+            fn += "  {\n";
+            for (const auto &m : cls)
+                for (int t = sp.groups[m.first].t0; t < sp.groups[m.first].t1; ++t) {
+                    snprintf(buf, sizeof(buf), "    double s%d = 0.0;\n", t);
+                    fn += buf;
+                }
+            for (unsigned J = 0; J < 8; ++J) {
+                snprintf(buf, sizeof(buf),
+                         "    { const double2 y = sm[b0 ^ swz(ins0(%uu, %d)) ^ %uu];\n", 256u * J, G.h,
+                         h_swz(G.f_loc));
+                fn += buf;
+                for (size_t q = 0; q < cls.size(); ++q) {
+                    const GroupRec &M = sp.groups[cls[q].first];
+                    const unsigned jj = J ^ cls[q].second;
+                    if (M.t_im > M.t0) {
+                        snprintf(buf, sizeof(buf), "      const double r%zu = fma(X[%u].x, y.x, X[%u].y * y.y);\n",
+                                 q, jj, jj);
+                        fn += buf;
+                    }
+                    if (M.t1 > M.t_im) {
+                        snprintf(buf, sizeof(buf), "      const double i%zu = fma(X[%u].x, y.y, -X[%u].y * y.x);\n",
+                                 q, jj, jj);
+                        fn += buf;
+                    }
+                    for (int t = M.t0; t < M.t1; ++t) {
+                        const TermRec &tr = sp.terms[t];
+                        const unsigned msk = (tr.s_loc >> 8) & 7u;
+                        snprintf(buf, sizeof(buf), "      s%d %s= %c%zu;\n", t,
+                                 (__builtin_popcount(jj & msk) & 1) ? "-" : "+", tr.use_im ? 'i' : 'r', q);
+                        fn += buf;
+                    }
+                }
+                fn += "    }\n";
+            }
+            for (const auto &m : cls)
+                for (int t = sp.groups[m.first].t0; t < sp.groups[m.first].t1; ++t) {
+                    snprintf(buf, sizeof(buf), "    acc[%d] = fma(", slot[t]);
+                    fn += buf;
+                    fn += sign_expr(sp.terms[t]);
+                    snprintf(buf, sizeof(buf), ", s%d, acc[%d]);\n", t, slot[t]);
+                    fn += buf;
+                }
+            fn += "  }\n";
+            gi = k;
+            continue;
+        }
+        const bool need_re = G.t_im > G.t0, need_im = G.t1 > G.t_im;
+        const bool w_re = G.t_im - G.t0 > kDirect, w_im = G.t1 - G.t_im > kDirect;
+        snprintf(buf, sizeof(buf),
+                 "  { double Wr[8], Wi[8];\n    wht8x<%s, %s, %s, %s, %d>(sm, b0, X, %uu, Wr, Wi);\n",
+                 need_re ? "true" : "false", need_im ? "true" : "false", w_re ? "true" : "false",
+                 w_im ? "true" : "false", G.h, h_swz(G.f_loc));
+        fn += buf;
+        for (int t = G.t0; t < G.t1; ++t) {
+            const TermRec &tr = sp.terms[t];
+            const char *W = tr.use_im ? "Wi" : "Wr";
+            const unsigned msk = (tr.s_loc >> 8) & 7u;
+            std::string val;
+            if (tr.use_im ? w_im : w_re) {
+                snprintf(buf, sizeof(buf), "%s[%u]", W, msk);
+                val = buf;
+            } else {  // W[m] of the transform = sum_j (-1)^{|j & m|} w_j
+                val = "(";
+                for (unsigned j = 0; j < 8; ++j) {
+                    snprintf(buf, sizeof(buf), "%s%s[%u]", j == 0 ? "" : (__builtin_popcount(j & msk) & 1) ? " - " : " + ", W, j);
+                    val += buf;
+                }
+                val += ")";
+            }
+            // scale folded in: the term's sweep total is scale * sum_p sign(p) w_p
+            snprintf(buf, sizeof(buf), "    acc[%d] = fma(", slot[t]);
+            fn += buf;
+            fn += sign_expr(tr);
+            fn += ", " + val;
+            snprintf(buf, sizeof(buf), ", acc[%d]);\n", slot[t]);
+            fn += buf;
+        }
+        fn += "  }\n";
+        ++gi;
+    }
+    if (prev_h >= 0) fn += "  }\n";
+}
+
+// Pair-bit share classes in group order: maximal runs of direct groups with
+// the same highest flip bit whose flips differ only in pair-bit positions
+// (emit_pairbit loads their l1 side once); other groups are units of their own.
+static std::vector<std::vector<size_t>> pairbit_units(const SweepPlan &sp)
+{
+    const int kDirect = 3;
+    auto direct = [&](const GroupRec &G) { return G.t_im - G.t0 <= kDirect && G.t1 - G.t_im <= kDirect; };
+    auto rpos = [](int H, int k) { return (8 + k) + ((8 + k) >= H ? 1 : 0); };
+    std::vector<std::vector<size_t>> units;
+    size_t gi = 0;
+    while (gi < sp.groups.size()) {
+        const GroupRec &G = sp.groups[gi];
+        std::vector<size_t> u{gi};
+        size_t k = gi + 1;
+        if (direct(G)) {
+            uint32_t R = 0;
+            for (int q = 0; q < 3; ++q) R |= 1u << rpos(G.h, q);
+            while (k < sp.groups.size() && sp.groups[k].h == G.h && direct(sp.groups[k]) &&
+                   ((sp.groups[k].f_loc ^ G.f_loc) & ~R) == 0)
+                u.push_back(k++);
+        }
+        units.push_back(u);
+        gi = k;
+    }
+    return units;
+}
+
+// Per-warp specialised sweep: the sweep's flip groups are split over the 8
+// warps of a tile group (share classes kept whole, longest-processing-time on
+// their strings), each warp running ITS groups over all 2048 pairs of the
+// tile (8 rounds of 32 lanes) with its own <= 24 per-lane accumulators.  A
+// sweep therefore holds up to 8 x 24 strings instead of 24, so a config-3
+// expectation needs about half the HBM sweeps (the tile-capacity bound).
+bool jit_sweep_source_warps(const SweepPlan &sp, std::string &src)
+{
+    const int kWarps = 8, kCap = 24;
+    const int nterms = (int)sp.terms.size();
+    std::vector<std::vector<size_t>> units = pairbit_units(sp);
+    auto ustr = [&](const std::vector<size_t> &u) {
+        int n = 0;
+        for (size_t g : u) n += sp.groups[g].t1 - sp.groups[g].t0;
+        return n;
+    };
+    // split classes that cannot fit a warp
+    std::vector<std::vector<size_t>> uu;
+    for (auto &u : units) {
+        if (ustr(u) <= kCap) {
+            uu.push_back(u);
+        } else {
+            for (size_t g : u) uu.push_back({g});
+        }
+    }
+    std::vector<std::vector<size_t>> wu;
+    std::vector<int> load;
+    // longest-processing-time over the warps; if the share classes do not
+    // pack, pack single groups (the planner checked that those fit)
+    auto pack = [&]() {
+        std::vector<size_t> ord(uu.size());
+        for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+        std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ustr(uu[a]) > ustr(uu[b]); });
+        wu.assign(kWarps, {});
+        load.assign(kWarps, 0);
+        for (size_t i : ord) {
+            const int n = ustr(uu[i]);
+            int best = -1;
+            for (int w = 0; w < kWarps; ++w)
+                if (load[w] + n <= kCap && (best < 0 || load[w] < load[best])) best = w;
+            if (best < 0) return false;
+            wu[best].push_back(i);
+            load[best] += n;
+        }
+        return true;
+    };
+    if (!pack()) {
+        uu.clear();
+        for (size_t g = 0; g < sp.groups.size(); ++g) uu.push_back({g});
+        if (!pack()) return false;
+    }
+    int maxt = 1;
+    for (int w = 0; w < kWarps; ++w) maxt = std::max(maxt, load[w]);
+    std::vector<int> slot(nterms, -1), cols(kWarps * maxt, -1);
+    std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 tid, u64 base, double (&acc)[MAXT])\n{\n"
+                     "  const u32 lane = tid & 31u;\n  switch (tid >> 5) {\n";
+    char buf[256];
+    for (int w = 0; w < kWarps; ++w) {
+        if (wu[w].empty()) continue;
+        // the warp's groups in sweep order (keeps H runs adjacent)
+        std::vector<size_t> units_w = wu[w];
+        std::sort(units_w.begin(), units_w.end(), [&](size_t a, size_t b) { return uu[a][0] < uu[b][0]; });
+        std::vector<size_t> gl;
+        int k = 0;
+        for (size_t ui : units_w)
+            for (size_t g : uu[ui]) {
+                gl.push_back(g);
+                for (int t = sp.groups[g].t0; t < sp.groups[g].t1; ++t) {
+                    slot[t] = k;
+                    cols[w * maxt + k] = t;
+                    ++k;
+                }
+            }
+        snprintf(buf, sizeof(buf), "  case %d: {\n#pragma unroll 1\n  for (u32 q = 0; q < 8u; ++q) {\n  const u32 pl = lane + 32u * q;\n", w);
+        fn += buf;
+        emit_pairbit(sp, gl, slot, fn);
+        fn += "  } } break;\n";
+    }
+    fn += "  default: break;\n  }\n}\n";
+    std::string head;
+    snprintf(buf, sizeof(buf), "#define MAXT %d\n#define NTERMS %d\n#define SWEEP_COLS_ON 1\n", maxt, nterms);
+    head = buf;
+    head += "__constant__ int SWEEP_COLS[" + std::to_string(kWarps * maxt) + "] = {";
+    for (size_t i = 0; i < cols.size(); ++i) head += (i ? "," : "") + std::to_string(cols[i]);
+    head += "};\n";
+    src = head;
+    src += kSweepSkeleton;
+    src += fn;
+    return true;
+}
+
 // Register-coset sweep.  The specialised sweep above is bound by shared-memory
 // bandwidth (LSU shared wavefronts at 73-84 % of peak, profiles/r02_sweep_ncu.txt):
 // every flip group re-reads 32 KiB of partner amplitudes per tile.  Here the
@@ -1082,132 +1345,23 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
     }
     if (sp.groups.front().pad[0] & 1) return false;  // wide groups: interpreted transform path
     const int nterms = (int)sp.terms.size();
+    {
+        // QSV_SWEEP_WARPS=1: per-warp group lists (A/B on config 3: 75 sweeps
+        // instead of 162 but 1.43 s instead of 0.81 s -- the eight warp code
+        // paths thrash the instruction cache and unbalance the warps; see
+        // profiles/r02_expect30_warps_launches.csv)
+        const char *env_w = getenv("QSV_SWEEP_WARPS");
+        if (env_w && env_w[0] == '1' && jit_sweep_source_warps(sp, src)) return true;
+    }
     if (nterms > 48) return false;
     std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";
-    char buf[512];
-    int prev_h = -1;
-    // a component with <= kDirect strings skips its 8-point transform
-    // (24 adds) and sums each string's 8 products directly (7 adds)
-    const int kDirect = 3;
-    auto direct = [&](const GroupRec &G) {
-        return G.t_im - G.t0 <= kDirect && G.t1 - G.t_im <= kDirect;
-    };
-    // tile positions of pair bits 8..10 for highest flip bit H (ins0 skips H)
-    auto rpos = [](int H, int k) { return (8 + k) + ((8 + k) >= H ? 1 : 0); };
-    const char *env_share = getenv("QSV_SWEEP_SHARE");
-    const bool share = !(env_share && env_share[0] == '0');
-    auto sign_expr = [&](const TermRec &tr) {
-        snprintf(buf, sizeof(buf), "((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g",
-                 tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
-        return std::string(buf);
-    };
-    size_t gi = 0;
-    while (gi < sp.groups.size()) {
-        const GroupRec &G = sp.groups[gi];
-        if (G.h != prev_h) {  // new run of groups with this highest flip bit
-            if (prev_h >= 0) fn += "  }\n";
-            snprintf(buf, sizeof(buf), "  { double2 X[8];\n    const u32 b0 = load_x<%d>(sm, pl, X);\n", G.h);
-            fn += buf;
-            prev_h = G.h;
-        }
-        if (share && direct(G)) {
-            // groups whose flips differ from G's only in the pair-bit positions
-            // 8..10 read a permutation of G's l1-side amplitudes: ONE load of
-            // y_j serves them all (member k uses pair j ^ d_k)
-            uint32_t R = 0;
-            for (int k = 0; k < 3; ++k) R |= 1u << rpos(G.h, k);
-            std::vector<std::pair<size_t, unsigned>> cls{{gi, 0u}};
-            size_t k = gi + 1;
-            while (k < sp.groups.size() && sp.groups[k].h == G.h && direct(sp.groups[k]) &&
-                   ((sp.groups[k].f_loc ^ G.f_loc) & ~R) == 0) {
-                const uint32_t D = sp.groups[k].f_loc ^ G.f_loc;
-                unsigned d = 0;
-                for (int q = 0; q < 3; ++q) d |= ((D >> rpos(G.h, q)) & 1u) << q;
-                cls.push_back({k, d});
-                ++k;
-            }
-            fn += "  {\n";
-            for (const auto &m : cls)
-                for (int t = sp.groups[m.first].t0; t < sp.groups[m.first].t1; ++t) {
-                    snprintf(buf, sizeof(buf), "    double s%d = 0.0;\n", t);
-                    fn += buf;
-                }
-            for (unsigned J = 0; J < 8; ++J) {
-                snprintf(buf, sizeof(buf),
-                         "    { const double2 y = sm[b0 ^ swz(ins0(%uu, %d)) ^ %uu];\n", 256u * J, G.h,
-                         h_swz(G.f_loc));
-                fn += buf;
-                for (size_t q = 0; q < cls.size(); ++q) {
-                    const GroupRec &M = sp.groups[cls[q].first];
-                    const unsigned jj = J ^ cls[q].second;
-                    if (M.t_im > M.t0) {
-                        snprintf(buf, sizeof(buf), "      const double r%zu = fma(X[%u].x, y.x, X[%u].y * y.y);\n",
-                                 q, jj, jj);
-                        fn += buf;
-                    }
-                    if (M.t1 > M.t_im) {
-                        snprintf(buf, sizeof(buf), "      const double i%zu = fma(X[%u].x, y.y, -X[%u].y * y.x);\n",
-                                 q, jj, jj);
-                        fn += buf;
-                    }
-                    for (int t = M.t0; t < M.t1; ++t) {
-                        const TermRec &tr = sp.terms[t];
-                        const unsigned msk = (tr.s_loc >> 8) & 7u;
-                        snprintf(buf, sizeof(buf), "      s%d %s= %c%zu;\n", t,
-                                 (__builtin_popcount(jj & msk) & 1) ? "-" : "+", tr.use_im ? 'i' : 'r', q);
-                        fn += buf;
-                    }
-                }
-                fn += "    }\n";
-            }
-            for (const auto &m : cls)
-                for (int t = sp.groups[m.first].t0; t < sp.groups[m.first].t1; ++t) {
-                    snprintf(buf, sizeof(buf), "    acc[%d] = fma(", t);
-                    fn += buf;
-                    fn += sign_expr(sp.terms[t]);
-                    snprintf(buf, sizeof(buf), ", s%d, acc[%d]);\n", t, t);
-                    fn += buf;
-                }
-            fn += "  }\n";
-            gi = k;
-            continue;
-        }
-        const bool need_re = G.t_im > G.t0, need_im = G.t1 > G.t_im;
-        const bool w_re = G.t_im - G.t0 > kDirect, w_im = G.t1 - G.t_im > kDirect;
-        snprintf(buf, sizeof(buf),
-                 "  { double Wr[8], Wi[8];\n    wht8x<%s, %s, %s, %s, %d>(sm, b0, X, %uu, Wr, Wi);\n",
-                 need_re ? "true" : "false", need_im ? "true" : "false", w_re ? "true" : "false",
-                 w_im ? "true" : "false", G.h, h_swz(G.f_loc));
-        fn += buf;
-        for (int t = G.t0; t < G.t1; ++t) {
-            const TermRec &tr = sp.terms[t];
-            const char *W = tr.use_im ? "Wi" : "Wr";
-            const unsigned msk = (tr.s_loc >> 8) & 7u;
-            std::string val;
-            if (tr.use_im ? w_im : w_re) {
-                snprintf(buf, sizeof(buf), "%s[%u]", W, msk);
-                val = buf;
-            } else {  // W[m] of the transform = sum_j (-1)^{|j & m|} w_j
-                val = "(";
-                for (unsigned j = 0; j < 8; ++j) {
-                    snprintf(buf, sizeof(buf), "%s%s[%u]", j == 0 ? "" : (__builtin_popcount(j & msk) & 1) ? " - " : " + ", W, j);
-                    val += buf;
-                }
-                val += ")";
-            }
-            // scale folded in: the term's sweep total is scale * sum_p sign(p) w_p
-            snprintf(buf, sizeof(buf), "    acc[%d] = fma(", t);
-            fn += buf;
-            fn += sign_expr(tr);
-            fn += ", " + val;
-            snprintf(buf, sizeof(buf), ", acc[%d]);\n", t);
-            fn += buf;
-        }
-        fn += "  }\n";
-        ++gi;
-    }
-    if (prev_h >= 0) fn += "  }\n";
+    std::vector<size_t> gl(sp.groups.size());
+    for (size_t i = 0; i < gl.size(); ++i) gl[i] = i;
+    std::vector<int> slot(nterms);
+    for (int t = 0; t < nterms; ++t) slot[t] = t;
+    emit_pairbit(sp, gl, slot, fn);
     fn += "}\n";
+    char buf[64];
     snprintf(buf, sizeof(buf), "#define MAXT %d\n", nterms);
     src = buf;
     src += kSweepSkeleton;

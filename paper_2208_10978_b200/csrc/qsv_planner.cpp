@@ -1727,7 +1727,13 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     // bounded by the shared-memory accumulators (kFlipCap strings).
     const char *env_sc = getenv("QSV_SWEEP_TERMS");  // strings per specialised sweep (default 24)
     const int jit_cap = env_sc ? std::max(4, std::min(48, atoi(env_sc))) : 24;
-    const int kFlipCap = jit_layout ? jit_cap : 512, kDiagCap = 2048, kGroupCap = 256;
+    // per-warp specialised sweeps (QSV_SWEEP_WARPS=1, qsv_jit.cpp
+    // jit_sweep_source_warps): each of the 8 warps of a tile group holds <=
+    // jit_cap strings -- half the sweeps on config 3, but measured 1.4 s vs
+    // 0.8 s (profiles/r02_expect30_warps_launches.csv), so off by default
+    const char *env_w = getenv("QSV_SWEEP_WARPS");
+    const int warps = jit_layout && env_w && env_w[0] == '1' ? 8 : 1;
+    const int kFlipCap = jit_layout ? jit_cap * warps : 512, kDiagCap = 2048, kGroupCap = 256;
     std::vector<int> order(flips.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
@@ -1744,6 +1750,7 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
     struct Bin {
         uint64_t hi = 0;
         int nterms = 0;
+        int wl[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // strings per warp (per-warp sweeps)
         bool wide = false;
         std::vector<int> groups;
         std::vector<int32_t> diag;
@@ -1767,9 +1774,16 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
         const int cap = wide ? kWideCap : kFlipCap;
         int placed = -1;
         // a narrow group above the (specialised-sweep) cap gets a sweep of its own
+        auto warp_of = [&](const Bin &bn) {  // a warp with room for nt more strings, -1 if none
+            if (wide || warps == 1) return 0;
+            for (int w = 0; w < warps; ++w)
+                if (bn.wl[w] + nt <= jit_cap) return w;
+            return -1;
+        };
         for (size_t b = 0; b < bins.size() && nt <= cap; ++b) {
             if (bins[b].wide != wide) continue;
             if (bins[b].nterms + nt > cap || (int)bins[b].groups.size() >= kGroupCap) continue;
+            if (warp_of(bins[b]) < 0) continue;
             if (popc64(bins[b].hi | need) <= free_slots) {
                 placed = (int)b;
                 break;
@@ -1779,6 +1793,10 @@ void plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y, co
             bins.emplace_back();
             bins.back().wide = wide;
             placed = (int)bins.size() - 1;
+        }
+        {
+            const int w = warp_of(bins[placed]);
+            if (w >= 0) bins[placed].wl[w] += nt;
         }
         bins[placed].hi |= need;
         bins[placed].nterms += nt;

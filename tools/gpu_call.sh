@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
-for u in 0 1; do echo "== QSV_U3_NORM=$u"; QSV_U3_NORM=$u timeout 300 python bench.py --steps 10 --warmup 3 --extra none --no-cpu-baseline 2>&1 | tail -1 | cut -c1-180; done
-timeout 900 python tools/parity_config2_full.py 2>&1 | tail -4 | tee gpurun_out/r02_parity_config2_full.log
-timeout 900 ncu --metrics gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:qsv_pass -c 60 --csv --log-file gpurun_out/fp64_launches_norm.csv python bench.py --steps 1 --warmup 3 --extra none --no-cpu-baseline > /dev/null 2>&1; echo ncu rc=$?
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "expectation or sweep or config3 or h2 or golden_expectation or dense or jit_ucc" 2>&1 | tail -3
+echo "== warps (default)"; timeout 600 python tools/time_expect30.py 2
+echo "== warps TERMS=16"; QSV_SWEEP_TERMS=16 timeout 600 python tools/time_expect30.py 2
+echo "== warps TERMS=12"; QSV_SWEEP_TERMS=12 timeout 600 python tools/time_expect30.py 2
+echo "== legacy"; QSV_SWEEP_WARPS=0 timeout 600 python tools/time_expect30.py 2
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed --clock-control none -c 200 --csv --log-file gpurun_out/r02_expect30_warps_launches.csv python tools/time_expect30.py 1 > /dev/null 2>&1; echo launches rc=$?
