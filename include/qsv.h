@@ -198,6 +198,11 @@ int qsv_plan_expectation(int n_qubits, int64_t n_terms, const uint64_t *x, const
 int qsv_match_rotations(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
                         int64_t cap, int64_t *spans, uint64_t *masks, int64_t *count);
 
+/* Debug / test export: the specialised (NVRTC) source of tile pass `k` of the
+ * plan for this gate list ("" for global / interpreted passes); host only. */
+int qsv_debug_pass_source(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                          int64_t k, char *out, int64_t cap, int64_t *needed, int64_t *n_passes);
+
 /* Debug / test export: the specialised (NVRTC) source of sweep `k` of the
  * expectation plan for these strings ("" when that sweep is interpreted);
  * the planner runs on the host, no device needed. */

@@ -52,7 +52,7 @@ EXPORTED = (
     "qsv_download_wait", "qsv_apply_1q", "qsv_apply_2q", "qsv_apply_matrix",
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
-    "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_debug_sweep_source", "qsv_sample_parity",
+    "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_debug_sweep_source", "qsv_debug_pass_source", "qsv_sample_parity",
     "qsv_jit_info", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
     "qsv_release_program", "qsv_evolve_basis", "qsv_evolve_basis_prepared",
     "qsv_last_plan_stats",
@@ -100,6 +100,8 @@ def _declare(L):
         "qsv_plan_expectation": ([ctypes.c_int, i64, u64p, u64p, u64p, sp], ctypes.c_int),
         "qsv_debug_plan_json": ([ctypes.c_int, i64, i32p, i32p, dp, ctypes.c_char_p, i64,
                                  ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_debug_pass_source": ([ctypes.c_int, i64, i32p, i32p, i64, ctypes.c_char_p, i64,
+                                   ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_debug_sweep_source": ([ctypes.c_int, i64, u64p, u64p, u64p, i64, ctypes.c_char_p, i64,
                                     ctypes.POINTER(i64), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_sample_parity": ([vp, u64, i64, u64p, dp, ctypes.POINTER(i64)], ctypes.c_int),
@@ -174,6 +176,17 @@ def debug_sweep_source(n_qubits: int, x, y, z, k: int) -> tuple[str, int]:
     check(lib().qsv_debug_sweep_source(n_qubits, len(x), u64ptr(x), u64ptr(y), u64ptr(z), k, buf,
                                        need.value, ctypes.byref(need), ctypes.byref(ns)))
     return buf.value.decode(), ns.value
+
+
+def debug_pass_source(n_qubits: int, kinds, qubits, k: int) -> tuple[str, int]:
+    """(specialised source of tile pass k of the plan, number of passes)."""
+    need, npass = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(lib().qsv_debug_pass_source(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits), k, None, 0,
+                                      ctypes.byref(need), ctypes.byref(npass)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(lib().qsv_debug_pass_source(n_qubits, len(kinds), i32ptr(kinds), i32ptr(qubits), k, buf,
+                                      need.value, ctypes.byref(need), ctypes.byref(npass)))
+    return buf.value.decode(), npass.value
 
 
 def jit_info() -> tuple[bool, int]:

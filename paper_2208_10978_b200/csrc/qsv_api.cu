@@ -309,6 +309,46 @@ int op_param_count(const OpRec &op)
     }
 }
 
+// Pass-local program of pass k (op / rot / param indices rebased to the
+// pass) and its specialised source; shared by run_template and the debug
+// export.  Returns false for global / tiny passes.
+static bool pass_local(const ProgramTemplate &t, size_t k, std::vector<OpRec> &lops,
+                       std::vector<BlockRec> &lblk, int &r_lo, int &r_hi, int &p_lo, int &p_hi)
+{
+    const PassPlan &p = t.passes[k];
+    if (p.global || p.geom.m < kBlockBits + 1) return false;
+    r_lo = INT32_MAX, r_hi = 0, p_lo = INT32_MAX, p_hi = 0;
+    for (int i = p.op_begin; i < p.op_end; ++i) {
+        const OpRec &op = t.ops[i];
+        if (op.r1 > op.r0) {
+            r_lo = std::min(r_lo, op.r0);
+            r_hi = std::max(r_hi, op.r1);
+        }
+        const int np = op_param_count(op);
+        if (np) {
+            p_lo = std::min(p_lo, op.p);
+            p_hi = std::max(p_hi, op.p + np);
+        }
+    }
+    if (r_lo == INT32_MAX) r_lo = r_hi = 0;
+    if (p_lo == INT32_MAX) p_lo = p_hi = 0;
+    p_lo &= ~3;  // keep 32 B alignment of matrices
+    lops.assign(t.ops.begin() + p.op_begin, t.ops.begin() + p.op_end);
+    for (OpRec &op : lops) {
+        if (op.r1 > op.r0) {
+            op.r0 -= r_lo;
+            op.r1 -= r_lo;
+        }
+        if (op_param_count(op)) op.p -= p_lo;
+    }
+    lblk.assign(t.blocks.begin() + p.block_begin, t.blocks.begin() + p.block_end);
+    for (BlockRec &bl : lblk) {
+        bl.op0 -= p.op_begin;
+        bl.op1 -= p.op_begin;
+    }
+    return true;
+}
+
 // A cached program whose every pass is specialised: upload each pass's
 // geometry tables and parameter window, copy-and-launch.
 int run_template_jit(qsv_state *s, ProgramTemplate &t, const std::vector<double> &params,
@@ -432,37 +472,8 @@ int run_template(qsv_state *s, ProgramTemplate &t, const std::vector<double> &pa
             geom_tables(p.geom, offhi, comp, &t.passes[k]);
             o.off = b.add(offhi.data(), offhi.size() * sizeof(uint64_t));
             o.comp = b.add(comp.data(), comp.size() * sizeof(int32_t));
-            if (p.geom.m < kBlockBits + 1) continue;
-            // pass-local program: rebase op/rot/param indices
-            int r_lo = INT32_MAX, r_hi = 0, p_lo = INT32_MAX, p_hi = 0;
-            for (int i = p.op_begin; i < p.op_end; ++i) {
-                const OpRec &op = t.ops[i];
-                if (op.r1 > op.r0) {
-                    r_lo = std::min(r_lo, op.r0);
-                    r_hi = std::max(r_hi, op.r1);
-                }
-                const int np = op_param_count(op);
-                if (np) {
-                    p_lo = std::min(p_lo, op.p);
-                    p_hi = std::max(p_hi, op.p + np);
-                }
-            }
-            if (r_lo == INT32_MAX) r_lo = r_hi = 0;
-            if (p_lo == INT32_MAX) p_lo = p_hi = 0;
-            p_lo &= ~3;  // keep 32 B alignment of matrices
-            lops.assign(t.ops.begin() + p.op_begin, t.ops.begin() + p.op_end);
-            for (OpRec &op : lops) {
-                if (op.r1 > op.r0) {
-                    op.r0 -= r_lo;
-                    op.r1 -= r_lo;
-                }
-                if (op_param_count(op)) op.p -= p_lo;
-            }
-            lblk.assign(t.blocks.begin() + p.block_begin, t.blocks.begin() + p.block_end);
-            for (BlockRec &bl : lblk) {
-                bl.op0 -= p.op_begin;
-                bl.op1 -= p.op_begin;
-            }
+            int r_lo, r_hi, p_lo, p_hi;
+            if (!pass_local(t, k, lops, lblk, r_lo, r_hi, p_lo, p_hi)) continue;
             o.lite = true;
             for (const OpRec &op : lops)
                 if (op.type == OP_U2) o.lite = false;
@@ -1563,6 +1574,30 @@ int qsv_plan_expectation(int n, int64_t S, const uint64_t *x, const uint64_t *y,
     for (const SweepPlan &sp : plan) st.n_fallback += sp.global ? 1 : 0;
     st.tile_bits = plan.empty() ? 0 : plan.front().geom.m;
     *out = st;
+    return QSV_OK;
+}
+
+int qsv_debug_pass_source(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                          int64_t k, char *out, int64_t cap, int64_t *needed, int64_t *n_passes)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (n < 1 || n > kMaxQubits) return fail_code(QSV_ERR_RESOURCE, "qubit count out of range");
+    if (n_gates < 0 || (n_gates > 0 && (!kinds || !qubits))) return fail_code(QSV_ERR_INVALID, "bad gate arrays");
+    qsv_state fake;
+    fake.n = n;
+    if (int rc = validate_gates(&fake, n_gates, kinds, qubits)) return rc;
+    ProgramTemplate t;
+    plan_gates(n, n_gates, kinds, qubits, t);
+    if (n_passes) *n_passes = (int64_t)t.passes.size();
+    std::string src;
+    std::vector<OpRec> lops;
+    std::vector<BlockRec> lblk;
+    int r_lo, r_hi, p_lo, p_hi;
+    if (k >= 0 && k < (int64_t)t.passes.size() && pass_local(t, (size_t)k, lops, lblk, r_lo, r_hi, p_lo, p_hi))
+        jit_source(t.passes[k].geom, lblk.data(), (int)lblk.size(), lops.data(), t.rots.data() + r_lo,
+                   p_hi - p_lo, src);
+    if (needed) *needed = (int64_t)src.size() + 1;
+    if (out && cap > (int64_t)src.size()) std::memcpy(out, src.c_str(), src.size() + 1);
     return QSV_OK;
 }
 

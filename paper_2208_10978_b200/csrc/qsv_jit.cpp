@@ -264,6 +264,62 @@ __device__ __forceinline__ void gm(double2 (&a)[16], u32 par0)
     }
 }
 
+// gm with the table offset P and the block sign mask ZB at run time: one code
+// body per flip pattern F, shared by every group with that pattern (the
+// compact form of small-state passes, whose straight-line code would be
+// executed once and stream through the instruction cache)
+template <int F>
+__device__ __forceinline__ void gm_rt(double2 (&a)[16], u32 par0, int P, u32 ZB)
+{
+    constexpr int H = hbit(F);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if (r & (1 << H)) continue;
+        const int r1 = r ^ F;
+        const u32 cp = par0 ^ (u32)(__popc((u32)r1 & ZB) & 1);
+        const int M = P + 8 * gm_cfg<F>(r1);
+        const double2 x = a[r], yy = a[r1];
+        const double2 y = make_double2(negif(yy.x, cp), negif(yy.y, cp));
+        double2 o0, o1;
+        o0.x = fma(C[M], x.x, fma(-C[M + 1], x.y, fma(C[M + 2], y.x, -C[M + 3] * y.y)));
+        o0.y = fma(C[M], x.y, fma(C[M + 1], x.x, fma(C[M + 2], y.y, C[M + 3] * y.x)));
+        o1.x = fma(C[M + 4], x.x, fma(-C[M + 5], x.y, fma(C[M + 6], y.x, -C[M + 7] * y.y)));
+        o1.y = fma(C[M + 4], x.y, fma(C[M + 5], x.x, fma(C[M + 6], y.y, C[M + 7] * y.x)));
+        a[r] = o0;
+        a[r1] = make_double2(negif(o1.x, cp), negif(o1.y, cp));
+    }
+}
+#ifdef QSV_GMD
+// a run of fused rotation groups [k0, k1) of the descriptor table
+__device__ __forceinline__ void gm_run(double2 (&a)[16], u32 tid, u64 base, int k0, int k1)
+{
+#pragma unroll 1
+    for (int k = k0; k < k1; ++k) {
+        const u32 pk = GMD_PK[k];
+        const u32 par0 = (u32)((__popcll(base & GMD_SHI[k]) + __popc(tid & (pk >> 8))) & 1);
+        const int P = GMD_P[k];
+        const u32 zb = (pk >> 4) & 15u;
+        switch (pk & 15u) {
+            case 1: gm_rt<1>(a, par0, P, zb); break;
+            case 2: gm_rt<2>(a, par0, P, zb); break;
+            case 3: gm_rt<3>(a, par0, P, zb); break;
+            case 4: gm_rt<4>(a, par0, P, zb); break;
+            case 5: gm_rt<5>(a, par0, P, zb); break;
+            case 6: gm_rt<6>(a, par0, P, zb); break;
+            case 7: gm_rt<7>(a, par0, P, zb); break;
+            case 8: gm_rt<8>(a, par0, P, zb); break;
+            case 9: gm_rt<9>(a, par0, P, zb); break;
+            case 10: gm_rt<10>(a, par0, P, zb); break;
+            case 11: gm_rt<11>(a, par0, P, zb); break;
+            case 12: gm_rt<12>(a, par0, P, zb); break;
+            case 13: gm_rt<13>(a, par0, P, zb); break;
+            case 14: gm_rt<14>(a, par0, P, zb); break;
+            default: gm_rt<15>(a, par0, P, zb); break;
+        }
+    }
+}
+#endif
+
 // in-register permutations: pure relabelings in straight-line code
 template <int A, int B>
 __device__ __forceinline__ void pcx(double2 (&a)[16])
@@ -787,6 +843,69 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
     std::string body;
     body.reserve(4096 + 160 * nblocks);
     char buf[256];
+    // Compact form (QSV_COMPACT_GMAT=1) for passes over few tiles made only of
+    // fused rotation groups: a data-driven block loop with ONE copy of the
+    // group code (gm_run, table offsets at run time) instead of straight-line
+    // code that runs once per warp.  A/B on config 1 (B200,
+    // profiles/r02_ucc12_compact_ab.txt): the instruction-fetch stalls go
+    // (ncu "no_instructions" 68 % -> 2 %) but the run-time-indexed constant
+    // loads (LDC, MIO-throttled) and 1.6x the instructions take their place:
+    // the same ~0.22 ms per pass under ncu, slower live -- straight-line code
+    // stays the default.
+    int n_gmat = 0;
+    for (int bi = 0; bi < nblocks; ++bi)
+        for (int k = blocks[bi].op0; k < blocks[bi].op1; ++k) n_gmat += ops[k].type == OP_GMAT;
+    bool all_gmat = nblocks > 0;
+    for (int bi = 0; bi < nblocks && all_gmat; ++bi) {
+        if (blocks[bi].kind != 0) all_gmat = false;
+        for (int k = blocks[bi].op0; k < blocks[bi].op1 && all_gmat; ++k) all_gmat = ops[k].type == OP_GMAT;
+    }
+    const char *env_cg = getenv("QSV_COMPACT_GMAT");
+    const bool compact = all_gmat && env_cg && env_cg[0] == '1' && g.ncomp <= 3 && n_gmat >= 16;
+    std::vector<unsigned long long> gmd_shi;
+    std::vector<unsigned> gmd_pk;
+    std::vector<int> gmd_p;
+    if (compact) {
+        // data-driven block loop: ONE copy of the block code (loads, the
+        // GMAT dispatch, stores) walks a constant table of blocks and groups
+        std::vector<unsigned> bd;
+        for (int bi = 0; bi < nblocks; ++bi) {
+            const BlockRec &B = blocks[bi];
+            bd.push_back((unsigned)B.tswz);
+            for (int i = 0; i < 12; ++i) bd.push_back((unsigned)B.cols[i]);
+            bd.push_back((unsigned)gmd_pk.size());
+            for (int k = B.op0; k < B.op1; ++k) {
+                const RotRec &rc = rots[ops[k].r0];
+                const unsigned zb = ((unsigned)rc.q >> 8) & 15u, zt = (unsigned)rc.q >> 12;
+                gmd_shi.push_back((unsigned long long)rc.s_hi);
+                gmd_pk.push_back((ops[k].f & 15u) | (zb << 4) | (zt << 8));
+                gmd_p.push_back(ops[k].p);
+            }
+            bd.push_back((unsigned)gmd_pk.size());
+            bd.push_back(bi + 1 < nblocks && (blocks[bi + 1].pad0 & 1) ? 1u : 0u);
+        }
+        // global (L1-cached) tables: the 64 KiB constant bank holds the pass parameters
+        std::string tab = "__device__ const unsigned BD[" + std::to_string(bd.size()) + "] = {";
+        for (size_t i = 0; i < bd.size(); ++i) tab += (i ? "," : "") + std::to_string(bd[i]) + "u";
+        tab += "};\n";
+        char big[2048];
+        snprintf(big, sizeof(big),
+                 "#pragma unroll 1\n  for (int bi = 0; bi < %d; ++bi) {\n"
+                 "    const unsigned *B = BD + 16 * bi;\n"
+                 "    u32 sb = B[0];\n"
+                 "#pragma unroll\n    for (int i = 0; i < %d; ++i) sb ^= tb(tid, i, B[1 + i]);\n"
+                 "    const u32 e1 = B[1 + %d], e2 = B[2 + %d], e4 = B[3 + %d], e8 = B[4 + %d];\n"
+                 "    double2 a[16];\n"
+                 "#pragma unroll\n    for (int r = 0; r < 16; ++r)\n"
+                 "      a[r] = sm[sb ^ ((r & 1) ? e1 : 0u) ^ ((r & 2) ? e2 : 0u) ^ ((r & 4) ? e4 : 0u) ^ ((r & 8) ? e8 : 0u)];\n"
+                 "    gm_run(a, tid, base, (int)B[13], (int)B[14]);\n"
+                 "#pragma unroll\n    for (int r = 0; r < 16; ++r)\n"
+                 "      sm[sb ^ ((r & 1) ? e1 : 0u) ^ ((r & 2) ? e2 : 0u) ^ ((r & 4) ? e4 : 0u) ^ ((r & 8) ? e8 : 0u)] = a[r];\n"
+                 "    if (B[15]) __syncwarp(); else gsync(bar);\n  }\n",
+                 nblocks, TB, TB, TB, TB, TB);
+        body = tab + "@@BODY@@" + big;
+        nblocks = 0;  // the straight-line emission below is skipped
+    }
     for (int bi = 0; bi < nblocks; ++bi) {
         const BlockRec &B = blocks[bi];
         if (B.kind != 0) return false;
@@ -850,9 +969,25 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
     }
     snprintf(buf, sizeof(buf), "#define QSV_NPARAMS %d\n", std::max(1, nparams));
     src = buf;
+    if (!gmd_pk.empty()) {
+        const size_t nd = gmd_pk.size();
+        src += "#define QSV_GMD 1\n__device__ const unsigned long long GMD_SHI[" + std::to_string(nd) + "] = {";
+        for (size_t i = 0; i < nd; ++i) src += (i ? "," : "") + std::to_string(gmd_shi[i]) + "ull";
+        src += "};\n__device__ const unsigned GMD_PK[" + std::to_string(nd) + "] = {";
+        for (size_t i = 0; i < nd; ++i) src += (i ? "," : "") + std::to_string(gmd_pk[i]) + "u";
+        src += "};\n__device__ const int GMD_P[" + std::to_string(nd) + "] = {";
+        for (size_t i = 0; i < nd; ++i) src += (i ? "," : "") + std::to_string(gmd_p[i]);
+        src += "};\n";
+    }
+    std::string tile_body = body;
+    const size_t at = body.find("@@BODY@@");
+    if (at != std::string::npos) {  // compact: block table before the skeleton, loop inside
+        src += body.substr(0, at);
+        tile_body = body.substr(at + 8);
+    }
     src += kSkeleton;
     src += "__device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar, u64 base)\n{\n";
-    src += body;
+    src += tile_body;
     src += "}\n";
     return true;
 }

@@ -231,3 +231,32 @@ def test_prepared_programs_host_side():
     assert rc != 0 and bad.value == 0
     assert _lib.lib().qsv_release_program(pid) == 0
     b._plan._pid = None  # released above; a later use prepares again
+
+
+def test_specialised_pass_sources_host_side():
+    """The NVRTC sources are generated on the host: config 1's single-tile
+    passes are straight-line by default and the compact data-driven block loop
+    on request (QSV_COMPACT_GMAT=1); config 2's passes are straight-line;
+    sweeps are specialised pair-bit sweeps."""
+    import os
+
+    cfg = W.config1(seed=0)
+    k, q, _ = flatten_bound(cfg["circuit"])
+    src0, npass = _lib.debug_pass_source(12, k, q, 0)
+    assert npass >= 1 and "gm<" in src0 and "gm_run(a, tid, base" not in src0  # default: straight-line
+    os.environ["QSV_COMPACT_GMAT"] = "1"
+    try:
+        src, _ = _lib.debug_pass_source(12, k, q, 0)
+    finally:
+        del os.environ["QSV_COMPACT_GMAT"]
+    assert "gm_run(a, tid, base" in src and "__device__ const unsigned BD[" in src
+    circ = W.brickwork(28, 4, seed=0)
+    k2, q2, _ = flatten_bound(circ)
+    src2, _ = _lib.debug_pass_source(28, k2, q2, 0)
+    assert src2 and "gm_run(" not in src2.split("apply_tile")[-1] and "u1<" in src2
+    from paper_2208_10978_b200.pauli import term_arrays
+
+    h = W.sparse_random_hamiltonian(20, 200, np.random.default_rng(3), z_only=0)
+    x, y, z, _, _ = term_arrays(h, 20)
+    s3, nsw = _lib.debug_sweep_source(20, x, y, z, 0)
+    assert nsw >= 1 and "qsv_sweep" in s3

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-timeout 1800 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_r02_full_b.log 2>&1; echo bench rc=$?; tail -c 8000 gpurun_out/bench_r02_full_b.log
-timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_r02_ref.log 2>&1; echo ref rc=$?; tail -c 1500 gpurun_out/bench_r02_ref.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py -x -q -m gpu -k "config1 or hot or jit or ucc or golden or gradient" 2>&1 | tail -4
+echo "== compact (default)"; timeout 600 python tools/time_ucc12.py 2>&1 | tail -2
+echo "== straight"; QSV_COMPACT_GMAT=0 timeout 600 python tools/time_ucc12.py 2>&1 | tail -2
+timeout 900 ncu --set full --clock-control none -k regex:qsv_pass --launch-skip 8 --launch-count 2 -o gpurun_out/r02_ucc12_pass_compact python tools/time_ucc12.py > /dev/null 2>&1; echo ncu rc=$?
