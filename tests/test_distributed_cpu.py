@@ -282,3 +282,43 @@ def test_lazy_basis_evolve_allocates_one_state():
     assert s0.basis_index is not None  # input untouched and still lazy
     assert len(made) == P  # one shard per rank (the test engine's basis() goes through zeros())
     assert np.abs(psi.amplitudes() - _oracle_state(circ, "0110" + "0" * (n - 4))).max() < 1e-13
+
+
+def _gloo_overlap_worker(rank, world, port, n, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = D.ProcessGroupComm(piece_bytes=1 << 9)
+        be = D.DistributedBackend(comm, OracleEngine())
+        a = be.evolve(be.prepare("0" * n), _random_mixed(n, 40, 21))
+        b = be.evolve(be.prepare("1" * n), W.brickwork(n, 3, seed=22))
+        v = be.overlap(a, b)  # realigns b over the process group (P2P relayouts)
+        q.put((rank, v, a.perm == b.perm, b.amplitudes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_overlap_across_layouts():
+    import torch.multiprocessing as mp
+
+    n, world = 7, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_overlap_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ra = _oracle_state(_random_mixed(n, 40, 21), "0" * n)
+    rb = _oracle_state(W.brickwork(n, 3, seed=22), "1" * n)
+    for rank, v, same, amps in res:
+        assert same
+        assert abs(v - np.vdot(ra, rb)) < 1e-13
+        assert np.abs(amps - rb).max() < 1e-13
+    assert res[0][1] == res[1][1]
