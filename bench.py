@@ -469,11 +469,32 @@ def extra_expect30(steps=3):
     dt = (time.perf_counter() - t0) / steps
     st = sv.last_plan_stats()
     prods = len(h) * (1 << n)
+    peak, peak_kind = load_peaks()
+    peak_dfma, fp_src = load_fp64_peak()
+    gbs = st["n_passes"] * 16 * (1 << n) / dt / 1e9
+    roof = {"bound": "issue", "hbm": {"achieved": gbs, "peak": peak, "unit": "GB/s",
+                                      "frac": gbs / peak, "peak_source": peak_kind,
+                                      "algorithmic_bytes": st["n_passes"] * 16 * (1 << n)},
+            "note": "each sweep reads the state once (16 B x 2^30); the work is the "
+                    "per-(string, pair) products, signs and transforms"}
+    try:
+        with open(os.path.join(REPO, "profiles", "r02_expect30_counts.json")) as fh:
+            cnt = json.load(fh)
+        if cnt.get("sweeps") == st["n_passes"]:
+            sm_clk = 1.965e9
+            issue_peak = 148 * 4 * sm_clk  # warp instructions / s (one per SMSP per clock)
+            fp = cnt["dfma"] + cnt["dmul"] + cnt["dadd"]
+            roof.update({"achieved": cnt["warp_inst"] / dt, "peak": issue_peak,
+                         "unit": "warp-instructions/s", "frac": cnt["warp_inst"] / dt / issue_peak,
+                         "fp64_pipe_frac": fp / dt / peak_dfma, "counts": cnt,
+                         "peak_note": "148 SMs x 4 schedulers x 1 warp-instruction/clk x 1.965 GHz"})
+    except Exception:
+        pass
     return {"workload": "config3: 30q expectation, 10,000 strings (30% Z-only), random state "
                         "(torch-generated on device)",
             "metric": "expectations/s", "value": 1.0 / dt, "ms_per_eval": dt * 1e3,
             "sweeps": st["n_passes"], "term_amplitude_products_per_s": prods / dt,
-            "hbm_gbs_sweeps": st["n_passes"] * 16 * (1 << n) / dt / 1e9}
+            "hbm_gbs_sweeps": gbs, "roofline": roof}
 
 
 def extra_fused30(steps=3):

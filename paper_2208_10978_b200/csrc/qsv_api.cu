@@ -244,7 +244,8 @@ std::string planner_knobs()
                                   "QSV_SCHED_WINDOW", "QSV_PHASE_DEFER", "QSV_WARP_LOCAL",
                                   "QSV_BLOCK_PARTITION", "QSV_INREG_PERMS", "QSV_SWEEP_TERMS",
                                   "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS", "QSV_TILE_BITS",
-                                  "QSV_U3_NORM"};
+                                  "QSV_U3_NORM", "QSV_SWEEP_FUSE1", "QSV_SWEEP_COSET",
+                                  "QSV_SWEEP_WARPS", "QSV_COMPACT_GMAT", "QSV_PASS_TMA"};
     std::string k;
     for (const char *nm : names) {
         const char *v = getenv(nm);

@@ -1018,6 +1018,8 @@ static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, con
     auto rpos = [](int H, int k) { return (8 + k) + ((8 + k) >= H ? 1 : 0); };
     const char *env_share = getenv("QSV_SWEEP_SHARE");
     const bool share = !(env_share && env_share[0] == '0');
+    const char *env_fs = getenv("QSV_SWEEP_FUSE1");  // 0: product + add even for single strings
+    const bool fuse_single = !(env_fs && env_fs[0] == '0');
     auto sign_expr = [&](const TermRec &tr) {
         snprintf(buf, sizeof(buf), "((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g",
                  tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
@@ -1062,12 +1064,17 @@ static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, con
                 for (size_t q = 0; q < cls.size(); ++q) {
                     const GroupRec &M = sp.groups[cls[q].first];
                     const unsigned jj = J ^ cls[q].second;
-                    if (M.t_im > M.t0) {
+                    // a component with ONE string accumulates its product
+                    // straight into the string's sum (2 DFMA, negation free)
+                    // instead of product (DMUL + DFMA) + add
+                    const bool fuse_re = fuse_single && M.t_im - M.t0 == 1;
+                    const bool fuse_im = fuse_single && M.t1 - M.t_im == 1;
+                    if (M.t_im > M.t0 && !fuse_re) {
                         snprintf(buf, sizeof(buf), "      const double r%zu = fma(X[%u].x, y.x, X[%u].y * y.y);\n",
                                  q, jj, jj);
                         fn += buf;
                     }
-                    if (M.t1 > M.t_im) {
+                    if (M.t1 > M.t_im && !fuse_im) {
                         snprintf(buf, sizeof(buf), "      const double i%zu = fma(X[%u].x, y.y, -X[%u].y * y.x);\n",
                                  q, jj, jj);
                         fn += buf;
@@ -1075,8 +1082,18 @@ static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, con
                     for (int t = M.t0; t < M.t1; ++t) {
                         const TermRec &tr = sp.terms[t];
                         const unsigned msk = (tr.s_loc >> 8) & 7u;
-                        snprintf(buf, sizeof(buf), "      s%d %s= %c%zu;\n", t,
-                                 (__builtin_popcount(jj & msk) & 1) ? "-" : "+", tr.use_im ? 'i' : 'r', q);
+                        const bool neg = __builtin_popcount(jj & msk) & 1;
+                        if (tr.use_im ? fuse_im : fuse_re) {
+                            if (tr.use_im)  // Im(conj x y) = x.re y.im - x.im y.re
+                                snprintf(buf, sizeof(buf), "      s%d = fma(%sX[%u].x, y.y, fma(%sX[%u].y, y.x, s%d));\n",
+                                         t, neg ? "-" : "", jj, neg ? "" : "-", jj, t);
+                            else  // Re(conj x y) = x.re y.re + x.im y.im
+                                snprintf(buf, sizeof(buf), "      s%d = fma(%sX[%u].x, y.x, fma(%sX[%u].y, y.y, s%d));\n",
+                                         t, neg ? "-" : "", jj, neg ? "-" : "", jj, t);
+                        } else {
+                            snprintf(buf, sizeof(buf), "      s%d %s= %c%zu;\n", t, neg ? "-" : "+",
+                                     tr.use_im ? 'i' : 'r', q);
+                        }
                         fn += buf;
                     }
                 }
