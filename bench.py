@@ -81,7 +81,9 @@ def fp64_roofline(t_step: float, passes: int, nominal_dfma: int, hbm: dict) -> d
                            "phase-deferred shears)",
            "hbm": hbm}
     norm_now = os.environ.get("QSV_U3_NORM", "1") != "0"
-    if counts and counts.get("passes") == passes and bool(counts.get("u3_norm")) == norm_now:
+    cz_now = os.environ.get("QSV_CZ_DEFER", "1") != "0"
+    if (counts and counts.get("passes") == passes and bool(counts.get("u3_norm")) == norm_now
+            and bool(counts.get("cz_defer")) == cz_now):
         flops = 2 * counts["dfma"] + counts["dmul"] + counts["dadd"]
         inst = counts["dfma"] + counts["dmul"] + counts["dadd"]
         out.update({"achieved": flops / t_step / 1e12, "frac": flops / t_step / 1e12 / out["peak"],

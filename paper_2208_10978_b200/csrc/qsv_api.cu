@@ -245,7 +245,8 @@ std::string planner_knobs()
                                   "QSV_BLOCK_PARTITION", "QSV_INREG_PERMS", "QSV_SWEEP_TERMS",
                                   "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS", "QSV_TILE_BITS",
                                   "QSV_U3_NORM", "QSV_SWEEP_FUSE1", "QSV_SWEEP_COSET",
-                                  "QSV_SWEEP_WARPS", "QSV_COMPACT_GMAT", "QSV_PASS_TMA"};
+                                  "QSV_SWEEP_WARPS", "QSV_COMPACT_GMAT", "QSV_PASS_TMA",
+                                  "QSV_CZ_DEFER"};
     std::string k;
     for (const char *nm : names) {
         const char *v = getenv(nm);
@@ -303,6 +304,7 @@ int op_param_count(const OpRec &op)
 {
     switch (op.type) {
         case OP_U1: return 8;
+        case OP_U1C: return 16;
         case OP_U2: return 32;
         case OP_DIAG1: return 4;
         case OP_GMAT: return 16 << (__builtin_popcount(op.f) - 1);

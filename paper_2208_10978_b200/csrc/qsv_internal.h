@@ -77,6 +77,8 @@ enum OpType : int32_t {
     OP_ROTD = 8,   // diagonal (Z-only) rotations, rots[r0..r1)
     OP_GMAT = 9,   // fused same-flip group: per pair one 2x2 from params[p..], selected by
                    // (common sign parity, flip-bit pattern); rots[r0] holds the common masks
+    OP_U1C = 10,   // dense 2x2 on a selected by bit b: params[p..p+8) if bit b = 0, [p+8..p+16)
+                   // if 1 (a U3 that absorbed a deferred controlled phase, qsv_planner.cpp CzDefer)
 };
 
 struct OpRec {  // 32 B

@@ -177,6 +177,34 @@ __device__ __forceinline__ void u1(double2 (&a)[16])
     }
 }
 
+// u1 selected by register bit JB: matrix P if bit JB = 0, P + 8 if 1 (OP_U1C);
+// K = 1 (m00 real) or 4 (m00 = 1), as u1
+template <int J, int JB, int K, int P>
+__device__ __forceinline__ void u1c(double2 (&a)[16])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        if (r & (1 << J)) continue;
+        const int Q = P + 8 * ((r >> JB) & 1);
+        const double2 x = a[r], y = a[r | (1 << J)];
+        double2 o0, o1;
+        if (K == 4) {
+            o0.x = fma(C[Q + 2], y.x, fma(-C[Q + 3], y.y, x.x));
+            o0.y = fma(C[Q + 2], y.y, fma(C[Q + 3], y.x, x.y));
+        } else if (K == 1) {
+            o0.x = fma(C[Q], x.x, fma(C[Q + 2], y.x, -C[Q + 3] * y.y));
+            o0.y = fma(C[Q], x.y, fma(C[Q + 2], y.y, C[Q + 3] * y.x));
+        } else {
+            o0.x = fma(C[Q], x.x, fma(-C[Q + 1], x.y, fma(C[Q + 2], y.x, -C[Q + 3] * y.y)));
+            o0.y = fma(C[Q], x.y, fma(C[Q + 1], x.x, fma(C[Q + 2], y.y, C[Q + 3] * y.x)));
+        }
+        o1.x = fma(C[Q + 4], x.x, fma(-C[Q + 5], x.y, fma(C[Q + 6], y.x, -C[Q + 7] * y.y)));
+        o1.y = fma(C[Q + 4], x.y, fma(C[Q + 5], x.x, fma(C[Q + 6], y.y, C[Q + 7] * y.x)));
+        a[r] = o0;
+        a[r | (1 << J)] = o1;
+    }
+}
+
 // dense 4x4 on register bits (JA = MSB of the row index, JB)
 template <int JA, int JB, int P>
 __device__ __forceinline__ void u2(double2 (&a)[16])
@@ -911,7 +939,7 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
         if (B.kind != 0) return false;
         for (int k = B.op0; k < B.op1; ++k) {
             const int t = ops[k].type;
-            if (t != OP_U1 && t != OP_U2 && t != OP_DIAG1 && t != OP_GMAT && t != OP_CX &&
+            if (t != OP_U1 && t != OP_U1C && t != OP_U2 && t != OP_DIAG1 && t != OP_GMAT && t != OP_CX &&
                 t != OP_SWAP && t != OP_X)
                 return false;
         }
@@ -936,6 +964,9 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
             if (op.type == OP_U1) {
                 const int cls = ((op.h >= 0 && op.h <= 4) || op.h == 6) ? op.h : 0;
                 snprintf(buf, sizeof(buf), "    u1<%d, %d, %d>(a);\n", op.a, cls, op.p);
+            } else if (op.type == OP_U1C) {
+                const int cls = (op.h == 1 || op.h == 4) ? op.h : 0;
+                snprintf(buf, sizeof(buf), "    u1c<%d, %d, %d, %d>(a);\n", op.a, op.b, cls, op.p);
             } else if (op.type == OP_U2) {
                 snprintf(buf, sizeof(buf), "    u2<%d, %d, %d>(a);\n", op.a, op.b, op.p);
             } else if (op.type == OP_CX) {

@@ -592,6 +592,55 @@ void find_phase_defers(const std::vector<Item> &items, const int32_t *kinds, con
     }
 }
 
+// The control qubit of a CzDefer's OP_U1C: the qubit of its source U3.
+inline int czdefer_target_qubit(const CzDefer &d, const int32_t *qubits) { return qubits[2 * d.src]; }
+
+// Controlled-phase deferrals (see CzDefer): for a CNOT(c, t) item between a
+// plain U3 G on t (not a PhaseDefer source) and plain U3s T (next on t) and K
+// (next on c, not a deferral source, K before T in item order), G's phase
+// goes to T, to K, and to K's control-selected copy; K then also requires t
+// (its control) in registers and must run before T, which the added support
+// bit enforces in every scheduler (items sharing a qubit are ordered).
+void find_cz_defers(std::vector<Item> &items, const int32_t *kinds, const int32_t *qubits, int n,
+                    int m, ProgramTemplate &t)
+{
+    const char *env = getenv("QSV_CZ_DEFER");
+    if ((env && env[0] == '0') || m < kBlockBits + 1) return;
+    std::vector<std::vector<int>> on(n);
+    for (int i = 0; i < (int)items.size(); ++i)
+        for (int q = 0; q < n; ++q)
+            if ((items[i].supp >> q) & 1ull) on[q].push_back(i);
+    auto plain_u3 = [&](int it) {
+        return it >= 0 && items[it].gate >= 0 && items[it].cluster < 0 && !items[it].rot &&
+               kinds[items[it].gate] == K_U3;
+    };
+    std::unordered_map<int, char> pd_src;  // gate -> PhaseDefer source
+    for (const PhaseDefer &d : t.defers) pd_src[d.src] = 1;
+    std::vector<char> cz_src(items.size(), 0), cz_ctl(items.size(), 0);
+    auto pos_in = [](const std::vector<int> &v, int x) {
+        for (size_t k = 0; k < v.size(); ++k)
+            if (v[k] == x) return (int)k;
+        return -1;
+    };
+    for (int x = 0; x < (int)items.size(); ++x) {
+        const Item &cx = items[x];
+        if (cx.gate < 0 || cx.cluster >= 0 || cx.rot || kinds[cx.gate] != K_CNOT) continue;
+        const int c = qubits[2 * cx.gate], tq = qubits[2 * cx.gate + 1];
+        const int pt = pos_in(on[tq], x), pc = pos_in(on[c], x);
+        if (pt < 1 || pt + 1 >= (int)on[tq].size() || pc < 0 || pc + 1 >= (int)on[c].size()) continue;
+        const int G = on[tq][pt - 1], T = on[tq][pt + 1], K = on[c][pc + 1];
+        if (!plain_u3(G) || !plain_u3(T) || !plain_u3(K) || K >= T) continue;
+        if (pd_src.count(items[G].gate) || pd_src.count(items[K].gate)) continue;
+        if (cz_src[G] || cz_ctl[G] || cz_src[K] || cz_ctl[K]) continue;
+        cz_src[G] = 1;
+        cz_ctl[K] = 1;
+        items[K].supp |= 1ull << tq;
+        items[K].req |= 1ull << tq;
+        items[K].par = 16;
+        t.czdefers.push_back(CzDefer{items[G].gate, items[T].gate, items[K].gate});
+    }
+}
+
 // Fixed 2x2 / 4x4 matrices of the permutation gates (circuit.py:36-45).
 void perm_matrix(int kind, double *o)
 {
@@ -691,7 +740,7 @@ void assign_u3_norm(ProgramTemplate &t, const PassPlan &pp, int pass, const int3
     std::vector<std::pair<int, int>> u3;  // (op index, fill index)
     for (int k = pp.op_begin; k < pp.op_end; ++k) {
         const OpRec &op = t.ops[k];
-        if (op.type != OP_U1 || op.p < 0) continue;
+        if ((op.type != OP_U1 && op.type != OP_U1C) || op.p < 0) continue;
         for (size_t f = 0; f < t.fills.size(); ++f)
             if (t.fills[f].offset == op.p && t.fills[f].kind == K_U3) {
                 u3.push_back({k, (int)f});
@@ -699,13 +748,14 @@ void assign_u3_norm(ProgramTemplate &t, const PassPlan &pp, int pass, const int3
             }
     }
     if (u3.size() < 2) return;
-    // sink: a non-deferring U3 if there is one (it loses 2 of 14, a deferring one 4 of 12)
-    size_t sink = 0;
-    for (size_t i = 0; i < u3.size(); ++i)
-        if (t.ops[u3[i].first].h != 3) {
-            sink = i;
-            break;
-        }
+    // sink: a plain non-deferring U3 if there is one (it loses 2 of 14, a
+    // deferring one 4 of 12); a controlled one only as the last resort
+    size_t sink = u3.size();
+    for (size_t i = 0; i < u3.size() && sink == u3.size(); ++i)
+        if (t.ops[u3[i].first].h != 3 && t.ops[u3[i].first].type == OP_U1) sink = i;
+    for (size_t i = 0; i < u3.size() && sink == u3.size(); ++i)
+        if (t.ops[u3[i].first].type == OP_U1) sink = i;
+    if (sink == u3.size()) sink = 0;
     t.pass_sink[pass] = u3[sink].second;
     for (size_t i = 0; i < u3.size(); ++i) {
         t.fill_pass[u3[i].second] = pass;
@@ -808,18 +858,34 @@ void emit_program(int n, int m, int c, const std::vector<Item> &items, const std
                     case K_CU3: op.type = OP_U2; break;
                     default: op.type = OP_U1; break;
                 }
+                int ctrl = 0;
+                if (kind == K_U3)
+                    for (const CzDefer &d : t.czdefers)
+                        if (d.ctl == gi) {
+                            // controlled by the CNOT target of the deferral
+                            int tq = -1;
+                            for (const CzDefer &e : t.czdefers)
+                                if (e.ctl == gi) tq = czdefer_target_qubit(e, qubits);
+                            op.type = OP_U1C;
+                            op.b = local_of(g, tq);
+                            ctrl = 1;
+                            break;
+                        }
                 // matrix class of a U1 (lets specialised passes drop zero
                 // imaginary parts): 2 = all entries real (H, RY),
                 // 1 = m00 real (U3: m00 = cos(theta/2); HY)
-                if (op.type == OP_U1)
+                if (op.type == OP_U1 || op.type == OP_U1C)
                     op.h = (kind == K_H || kind == K_RY) ? 2 : (kind == K_U3 || kind == K_HY) ? 1 : 0;
-                if (op.type == OP_U1 && kind == K_U3)
+                if (op.type == OP_U1 && kind == K_U3) {
                     for (const PhaseDefer &d : t.defers)
                         if (d.src == gi) op.h = 3;  // V: m00 and m10 real
-                const int np = param_count(kind);
+                    for (const CzDefer &d : t.czdefers)
+                        if (d.src == gi) op.h = 3;  // V too: its phase is deferred
+                }
+                const int np = ctrl ? 16 : param_count(kind);
                 if (np) {
                     op.p = (int)t.n_params;
-                    t.fills.push_back(ParamFill{(int)t.n_params, gi, kind});
+                    t.fills.push_back(ParamFill{(int)t.n_params, gi, kind, ctrl});
                     t.n_params += np;
                 }
             }
@@ -856,7 +922,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
     auto supp = [&](const OpRec &op) -> uint32_t {
         switch (op.type) {
             case OP_U1: case OP_X: case OP_DIAG1: return 1u << op.a;
-            case OP_U2: case OP_CX: case OP_SWAP: return (1u << op.a) | (1u << op.b);
+            case OP_U2: case OP_U1C: case OP_CX: case OP_SWAP: return (1u << op.a) | (1u << op.b);
             case OP_ROTG: return op.f | rot_signs(op);
             case OP_ROTD: return rot_signs(op);
             default: return 0u;
@@ -865,7 +931,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
     auto req = [](const OpRec &op) -> uint32_t {
         switch (op.type) {
             case OP_U1: return 1u << op.a;
-            case OP_U2: return (1u << op.a) | (1u << op.b);
+            case OP_U2: case OP_U1C: return (1u << op.a) | (1u << op.b);
             case OP_ROTG: return op.f;
             default: return 0u;  // diagonal ops fit any block
         }
@@ -885,7 +951,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
     if (m == kMaxTileBits && kBlockBits == 4 && !has_rot) {
         int cnt[12] = {0};
         for (const OpRec &op : src)
-            if (op.type == OP_U1 || op.type == OP_U2 || op.type == OP_ROTG)
+            if (op.type == OP_U1 || op.type == OP_U2 || op.type == OP_U1C || op.type == OP_ROTG)
                 for (int b = 0; b < m; ++b) cnt[b] += (req(op) >> b) & 1u;
         for (int k = 0; k < 3; ++k) {
             int best = -1;
@@ -1007,7 +1073,7 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
             for (OpRec op : pending) {
                 switch (op.type) {
                     case OP_U1: op.a = local(op.a); break;
-                    case OP_U2: op.a = local(op.a); op.b = local(op.b); break;
+                    case OP_U2: case OP_U1C: op.a = local(op.a); op.b = local(op.b); break;
                     case OP_DIAG1: {
                         const int j = local(op.a);
                         op.b = j >= 0 ? 0 : thread_index(op.a);
@@ -1475,6 +1541,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
     }
     fuse_clusters(items, kinds, qubits, t);
     find_phase_defers(items, kinds, qubits, n, t);
+    find_cz_defers(items, kinds, qubits, n, m, t);
     Schedule S = pick_schedule(items, R, n, m, c);
     pick_contig(items, R, n, m, c, S);
     emit_program(n, m, c, items, R, kinds, qubits, S, t);
@@ -1511,7 +1578,7 @@ void materialize_params(ProgramTemplate &t, const double *values, double *params
 {
     materialize_gates(t, values);
     const bool norm = !t.fill_mode.empty() && !t.pass_sink.empty();
-    if (t.defers.empty() && !norm) {
+    if (t.defers.empty() && t.czdefers.empty() && !norm) {
         for (const ParamFill &f : t.fills) gate_matrix(f.kind, values + 3 * (size_t)f.src, params + f.offset);
     } else {
         // deferred phases: a deferring U3 hands phi (and, in shear mode, its
@@ -1521,11 +1588,17 @@ void materialize_params(ProgramTemplate &t, const double *values, double *params
         if (norm)
             for (size_t f = 0; f < t.fills.size(); ++f)
                 if (f < t.fill_mode.size() && t.fill_mode[f]) mode_of[t.fills[f].src] = t.fill_mode[f];
-        std::vector<PhaseDefer> ds = t.defers;
-        std::sort(ds.begin(), ds.end(), [](const PhaseDefer &a, const PhaseDefer &b) { return a.src < b.src; });
+        // both deferral kinds, in source gate order (a source's effective
+        // lambda includes what earlier sources handed it)
+        struct Dv { int src, dst, ctl; };
+        std::vector<Dv> ds;
+        for (const PhaseDefer &d : t.defers) ds.push_back({d.src, d.dst, -1});
+        for (const CzDefer &d : t.czdefers) ds.push_back({d.src, d.tgt, d.ctl});
+        std::sort(ds.begin(), ds.end(), [](const Dv &a, const Dv &b) { return a.src < b.src; });
         std::unordered_map<int, double> add_lambda;  // receiving gate -> deferred phase
+        std::unordered_map<int, double> ctl_lambda;  // OP_U1C gate -> extra lambda when its control is 1
         std::unordered_map<int, char> deferring;
-        for (const PhaseDefer &d : ds) {
+        for (const Dv &d : ds) {
             deferring[d.src] = 1;
             double give = values[3 * (size_t)d.src + 1];  // phi
             auto m = mode_of.find(d.src);
@@ -1534,6 +1607,10 @@ void materialize_params(ProgramTemplate &t, const double *values, double *params
                 give += values[3 * (size_t)d.src + 2] + (a != add_lambda.end() ? a->second : 0.0);
             }
             add_lambda[d.dst] += give;
+            if (d.ctl >= 0) {  // e^{ib (x_t ^ x_c)} = e^{ib x_t} e^{ib x_c} e^{-2ib x_t x_c}
+                add_lambda[d.ctl] += give;
+                ctl_lambda[d.ctl] -= 2.0 * give;
+            }
         }
         std::vector<double> mu(t.pass_sink.size(), 1.0);
         for (size_t fi = 0; fi < t.fills.size(); ++fi) {
@@ -1560,19 +1637,29 @@ void materialize_params(ProgramTemplate &t, const double *values, double *params
                 continue;
             }
             gate_matrix(K_U3, vv, o);
-            if (mode == 4) {  // U3 / c: m00 = 1 exactly
+            if (f.ctrl) {  // OP_U1C: the matrix for control bit 1 follows
+                double v1[3] = {vv[0], vv[1], vv[2]};
+                auto cl = ctl_lambda.find(f.src);
+                if (cl != ctl_lambda.end()) v1[2] += cl->second;
+                gate_matrix(K_U3, v1, o + 8);
+            }
+            if (mode == 4) {  // U3 / c: m00 = 1 exactly (both matrices of an OP_U1C)
                 const double c = o[0], inv = 1.0 / c;
-                for (int k = 2; k < 8; ++k) o[k] *= inv;
-                o[0] = 1.0;
-                o[1] = 0.0;
+                for (int h = 0; h <= f.ctrl; ++h) {
+                    double *q = o + 8 * h;
+                    for (int k = 2; k < 8; ++k) q[k] *= inv;
+                    q[0] = 1.0;
+                    q[1] = 0.0;
+                }
                 mu[t.fill_pass[fi]] *= c;
             }
         }
         if (norm)
             for (size_t p = 0; p < t.pass_sink.size(); ++p)
                 if (t.pass_sink[p] >= 0 && mu[p] != 1.0) {
-                    double *o = params + t.fills[t.pass_sink[p]].offset;
-                    for (int k = 0; k < 8; ++k) o[k] *= mu[p];
+                    const ParamFill &sf = t.fills[t.pass_sink[p]];
+                    double *o = params + sf.offset;
+                    for (int k = 0; k < 8 * (1 + sf.ctrl); ++k) o[k] *= mu[p];
                 }
     }
     for (const ClusterFill &cf : t.cfills)

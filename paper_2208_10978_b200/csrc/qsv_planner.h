@@ -43,9 +43,23 @@ struct PassPlan {
 };
 
 struct ParamFill {
-    int offset;  // into params
-    int src;     // gate index
-    int kind;    // gate kind
+    int offset;    // into params
+    int src;       // gate index
+    int kind;      // gate kind
+    int ctrl = 0;  // 1: OP_U1C -- two matrices (control bit 0 / 1), 16 doubles
+};
+
+// Controlled-phase deferral of a U3 whose qubit t next acts as a CNOT TARGET
+// (the case PhaseDefer cannot take): its phase diag(1, e^{ib}) on t passes the
+// CNOT(c, t) as e^{ib (x_t ^ x_c)} = e^{ib x_t} e^{ib x_c} e^{-2ib x_c x_t}:
+// the first factor joins the next U3 on t (lambda += b), the second the next
+// U3 on c (lambda += b), the third makes that U3 on c controlled by x_t
+// (lambda += b - 2b when x_t = 1: OP_U1C), applied before the U3 on t.  The
+// source then needs no phase at all (U3Norm shear, 8 FP64 per pair).
+struct CzDefer {
+    int src;   // deferring U3 (on t)
+    int tgt;   // next U3 on t (lambda += b)
+    int ctl;   // next U3 on c, becomes OP_U1C controlled by t
 };
 
 // Phase deferral of a U3 whose qubit next acts as a CNOT control and then
@@ -88,6 +102,7 @@ struct ProgramTemplate {
     std::vector<GmatFill> gfills;  // fused group tables refreshed per call
     std::vector<ClusterFill> cfills;  // dense-fused gate clusters refreshed per call
     std::vector<PhaseDefer> defers;   // U3 phase deferrals (see PhaseDefer)
+    std::vector<CzDefer> czdefers;    // controlled-phase deferrals (see CzDefer)
     // Normalised U3 forms (see U3Norm in qsv_planner.cpp), per ParamFill:
     // 0 plain, 4 row 0 divided by m00 (m00 = 1), 6 shear (m00 = m11 = 1,
     // both phases deferred); the pass's product of the divisors multiplies

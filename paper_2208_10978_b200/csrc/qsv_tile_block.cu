@@ -282,6 +282,21 @@ __device__ __forceinline__ void dispatch_pair(int ja, int jb, double2 (&a)[kR], 
 }
 
 template <int A, int B> struct W_u2 { __device__ static void run(double2 (&a)[kR], const double *P) { r_u2<A, B>(a, P); } };
+// OP_U1C: 2x2 on bit A, matrix P (bit B = 0) or P + 8 (bit B = 1)
+template <int A, int B> struct W_u1c {
+    __device__ static void run(double2 (&a)[kR], const double *P)
+    {
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            if (r & (1 << A)) continue;
+            const double *Q = P + 8 * ((r >> B) & 1);
+            const double2 m00 = ld2(Q), m01 = ld2(Q + 2), m10 = ld2(Q + 4), m11 = ld2(Q + 6);
+            const double2 x = a[r], y = a[r | (1 << A)];
+            a[r] = cfma2(m00, x, m01, y);
+            a[r | (1 << A)] = cfma2(m10, x, m11, y);
+        }
+    }
+};
 
 // in-register permutations (block-local bits): CNOT control A target B, SWAP, X
 template <int A, int B> struct W_cx {
@@ -420,6 +435,7 @@ __device__ __forceinline__ void run_blocks(double2 *sm, const BlockRec *blocks, 
                     const int type = w0.x, oa = w0.y, ob = w0.z;
                     switch (type) {
                         case OP_U1: dispatch_u1(oa, a, params + w1.z); break;
+                        case OP_U1C: dispatch_pair<W_u1c>(oa, ob, a, params + w1.z); break;
                         case OP_U2:
                             if (!LITE) dispatch_pair<W_u2>(oa, ob, a, params + w1.z);
                             break;

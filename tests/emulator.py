@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-OP_U1, OP_U2, OP_CX, OP_SWAP, OP_X, OP_DIAG1, OP_ROTG, OP_ROTD, OP_GMAT = 1, 2, 3, 4, 5, 6, 7, 8, 9
+OP_U1, OP_U2, OP_CX, OP_SWAP, OP_X, OP_DIAG1, OP_ROTG, OP_ROTD, OP_GMAT, OP_U1C = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 
 
 def swz(l):
@@ -53,6 +53,16 @@ def run_block(a, ops, rots, params, tid, base, blk_ops, RB):
             for r in range(R):
                 if r & J:
                     continue
+                x, y = a[:, r].copy(), a[:, r | J].copy()
+                a[:, r] = m00 * x + m01 * y
+                a[:, r | J] = m10 * x + m11 * y
+        elif typ == OP_U1C:  # 2x2 on bit oa, matrix selected by bit ob
+            J = 1 << oa
+            for r in range(R):
+                if r & J:
+                    continue
+                q = p + 8 * ((r >> ob) & 1)
+                m00, m01, m10, m11 = (_c(params, q, k) for k in range(4))
                 x, y = a[:, r].copy(), a[:, r | J].copy()
                 a[:, r] = m00 * x + m01 * y
                 a[:, r | J] = m10 * x + m11 * y
