@@ -1634,6 +1634,10 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     if (int rc = validate_gates(&fake, n_gates, kinds, qubits)) return rc;
     ProgramTemplate t;
     plan_gates(n, n_gates, kinds, qubits, t);
+    if (!plain_u3() && values && needs_plain_u3(t, values)) {  // as apply_gates_impl
+        PlainU3Scope plain;
+        return qsv_debug_plan_json(n, n_gates, kinds, qubits, values, out, cap, needed);
+    }
     std::vector<double> params(t.n_params);
     materialize_params(t, values, params.data());
     std::string j = "{\"n\":" + std::to_string(n) + ",\"block_bits\":" +

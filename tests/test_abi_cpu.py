@@ -260,3 +260,27 @@ def test_specialised_pass_sources_host_side():
     x, y, z, _, _ = term_arrays(h, 20)
     s3, nsw = _lib.debug_sweep_source(20, x, y, z, 0)
     assert nsw >= 1 and "qsv_sweep" in s3
+
+
+def test_emulated_singular_u3_angles_take_the_plain_plan():
+    """U3 angles whose cos(theta/2) vanishes (theta = pi: an X-like gate) or is
+    tiny cannot take the normalised U3 forms (row 0 divided by cos(theta/2));
+    the call is planned without them (set_plain_u3) and stays exact."""
+    import emulator
+    from oracle import oracle as O
+    from paper_2208_10978_b200.circuit import Circuit, Constant, Gate
+
+    n = 12
+    base = W.brickwork(n, 6, seed=8)
+    gates = list(base.gates)
+    for i, g in enumerate(gates):  # a few U3s at theta = pi and pi - 1e-6
+        if g.kind == "U3" and i % 7 == 3:
+            th = np.pi if i % 2 else np.pi - 1e-6
+            gates[i] = Gate("U3", g.qubits, (Constant(th),) + tuple(g.params[1:]))
+    circ = Circuit(n, tuple(gates), 0)
+    k, q, v = flatten_bound(circ)
+    prog = _lib.debug_plan(n, k, q, v)
+    psi0 = O.init_state("0" * n)
+    out = emulator.run_program(prog, psi0)
+    assert np.all(np.isfinite(out))
+    assert np.abs(out - O.evolve(psi0, circ.gates)).max() <= 1e-12

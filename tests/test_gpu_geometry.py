@@ -111,3 +111,22 @@ def test_config2_family_26q_depth20_vs_oracle(monkeypatch):
     d = np.abs(out - ref)
     assert d.max() <= AMP_TOL
     assert float(np.sqrt((d * d).sum())) <= 1e-10
+
+
+def test_singular_u3_angles_fall_back_to_plain_forms(jit14):
+    """U3s at theta = pi (cos(theta/2) = 0) cannot take the normalised forms:
+    the call runs a plan without them (specialised passes) and matches the
+    oracle; the same structure at regular angles keeps the normalised plan."""
+    from paper_2208_10978_b200.circuit import Circuit, Constant, Gate
+
+    n = 18
+    base = W.brickwork(n, 8, seed=71)
+    gates = list(base.gates)
+    for i, g in enumerate(gates):
+        if g.kind == "U3" and i % 9 == 4:
+            gates[i] = Gate("U3", g.qubits, (Constant(np.pi),) + tuple(g.params[1:]))
+    for circ in (Circuit(n, tuple(gates), 0), base):
+        out = sv.evolve(sv.init_state("0" * n), circ).amplitudes
+        ref = O.evolve(O.init_state("0" * n), circ.gates)
+        assert np.all(np.isfinite(out))
+        assert np.abs(out - ref).max() <= AMP_TOL
