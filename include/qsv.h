@@ -198,6 +198,33 @@ int qsv_plan_expectation(int n_qubits, int64_t n_terms, const uint64_t *x, const
 int qsv_match_rotations(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
                         int64_t cap, int64_t *spans, uint64_t *masks, int64_t *count);
 
+/* ---- multi-device state (one process, P = 2^g shards) --------------------
+ * The single-process counterpart of the sharded path (distributed.py; the
+ * reference's own parallelism is one process with forked workers,
+ * engine.py:169-199): rank r keeps the 2^(n-g) amplitudes whose physical
+ * index bits [n-g, n) equal r on device_ids[r] (ids may repeat: several
+ * shards on one device).  Gate lists are cut into local segments by the
+ * light-cone scheduler with qubit-swap relayouts (pairwise chunk exchange,
+ * cudaMemcpyPeerAsync over NVLink / NVSwitch) between them; a logical ->
+ * physical qubit map is kept, never swapped back.  qsv_dist_set_basis is lazy
+ * (init_state, statevector.py:42-54); qsv_dist_expectation reduces the ranks'
+ * partials in ascending order (engine.py:199); qsv_dist_download returns the
+ * logical amplitudes in dump_state order (statevector.py:214-216). */
+typedef struct qsv_dist qsv_dist;
+int qsv_dist_create(qsv_dist **out, int n_qubits, int n_ranks, const int *device_ids);
+int qsv_dist_destroy(qsv_dist *d);
+int qsv_dist_set_basis(qsv_dist *d, uint64_t index);
+int qsv_dist_apply_gates(qsv_dist *d, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
+                         const double *values);
+int qsv_dist_expectation(qsv_dist *d, int64_t n_terms, const uint64_t *x, const uint64_t *y,
+                         const uint64_t *z, const double *coef_re, const double *coef_im,
+                         double *out_re, double *out_im);
+int qsv_dist_download(qsv_dist *d, double *host);
+/* ranks, local qubits, relayouts so far, bytes each rank sent, qubit map
+ * (perm[q] = physical position of logical qubit q; any pointer may be NULL) */
+int qsv_dist_info(const qsv_dist *d, int *n_ranks, int *local_qubits, int64_t *relayouts,
+                  int64_t *bytes_sent_per_rank, int32_t *perm);
+
 /* Debug / test export: the specialised (NVRTC) source of tile pass `k` of the
  * plan for this gate list ("" for global / interpreted passes); host only. */
 int qsv_debug_pass_source(int n_qubits, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,

@@ -55,7 +55,8 @@ EXPORTED = (
     "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_debug_sweep_source", "qsv_debug_pass_source", "qsv_sample_parity",
     "qsv_jit_info", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
     "qsv_release_program", "qsv_evolve_basis", "qsv_evolve_basis_prepared",
-    "qsv_last_plan_stats",
+    "qsv_last_plan_stats", "qsv_dist_create", "qsv_dist_destroy", "qsv_dist_set_basis",
+    "qsv_dist_apply_gates", "qsv_dist_expectation", "qsv_dist_download", "qsv_dist_info",
 )
 
 _lib = None
@@ -71,6 +72,15 @@ def _declare(L):
         "qsv_last_error": ([], ctypes.c_char_p),
         "qsv_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
         "qsv_mem_info": ([ctypes.c_int, u64p, u64p], ctypes.c_int),
+        "qsv_dist_create": ([ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+                            ctypes.c_int),
+        "qsv_dist_destroy": ([vp], ctypes.c_int),
+        "qsv_dist_set_basis": ([vp, u64], ctypes.c_int),
+        "qsv_dist_apply_gates": ([vp, i64, i32p, i32p, dp], ctypes.c_int),
+        "qsv_dist_expectation": ([vp, i64, u64p, u64p, u64p, dp, dp, dp, dp], ctypes.c_int),
+        "qsv_dist_download": ([vp, vp], ctypes.c_int),
+        "qsv_dist_info": ([vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                           ctypes.POINTER(i64), ctypes.POINTER(i64), i32p], ctypes.c_int),
         "qsv_create": ([ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "qsv_destroy": ([vp], ctypes.c_int),
         "qsv_n_qubits": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
