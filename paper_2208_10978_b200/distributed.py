@@ -663,6 +663,13 @@ class DistStateVector:
         return int(getattr(self.comm, "piece_bytes", 256 << 20))
 
     def _p2p_exchange(self, views, remote, chunk):
+        """Pairwise chunk swap with the remote partners, one bounded piece at
+        a time: send piece k of the outgoing chunk and receive the partner's
+        piece k into a staging slot in the same group, then copy it into place
+        (an in-place swap needs the slot: a receive into the piece being sent
+        in the same round would race, and a receive posted a round later
+        deadlocks the paired sends).  With NCCL, ``wait()`` only orders the
+        CUDA stream -- the host does not block per piece."""
         import torch
 
         dist = self.comm.dist
