@@ -246,7 +246,7 @@ std::string planner_knobs()
                                   "QSV_SWEEP_SHARE", "QSV_JIT", "QSV_JIT_MIN_QUBITS", "QSV_TILE_BITS",
                                   "QSV_U3_NORM", "QSV_SWEEP_FUSE1", "QSV_SWEEP_COSET",
                                   "QSV_SWEEP_WARPS", "QSV_COMPACT_GMAT", "QSV_PASS_TMA",
-                                  "QSV_CZ_DEFER"};
+                                  "QSV_CZ_DEFER", "QSV_SWEEP_ONETILE"};
     std::string k;
     for (const char *nm : names) {
         const char *v = getenv(nm);

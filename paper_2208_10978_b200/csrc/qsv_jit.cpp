@@ -534,7 +534,14 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
 const char *kSweepSkeleton = R"QSV(
 typedef unsigned long long u64;
 typedef unsigned int u32;
-#define KT 256
+// SW_GROUPS tile groups of KT threads per CTA (2 x 256: each group sweeps
+// its own tiles; 1 x 512: the whole CTA sweeps one tile, two more loading);
+// a thread's pairs are p = pl + KT j, j < SW_NJ = 2048 / KT
+#ifndef SW_GROUPS
+#define SW_GROUPS 2
+#endif
+#define KT (512 / SW_GROUPS)
+#define SW_NJ (2048 / KT)
 #define KSTAGES 3
 #define TSIZE 4096
 // GF(2)-linear tile swizzle (16-B slots): the low 3 bits (bank group) are the
@@ -570,16 +577,16 @@ __device__ __forceinline__ void wht8(const double2 *sm, u32 pl, u32 sF, double (
 {
     const u32 b0 = swz(ins0(pl, H));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const u32 a0 = b0 ^ swz(ins0(256u * j, H));
+    for (int j = 0; j < SW_NJ; ++j) {
+        const u32 a0 = b0 ^ swz(ins0((u32)KT * j, H));
         const double2 x = sm[a0], y = sm[a0 ^ sF];
         if (RE) Wr[j] = fma(x.x, y.x, x.y * y.y);
         if (IM) Wi[j] = fma(x.x, y.y, -x.y * y.x);
     }
 #pragma unroll
-    for (int b = 1; b < 8; b <<= 1) {
+    for (int b = 1; b < SW_NJ; b <<= 1) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < SW_NJ; ++r) {
             if (r & b) continue;
             if (RE) { const double u = Wr[r], v = Wr[r | b]; Wr[r] = u + v; Wr[r | b] = u - v; }
             if (IM) { const double u = Wi[r], v = Wi[r | b]; Wi[r] = u + v; Wi[r | b] = u - v; }
@@ -593,7 +600,7 @@ __device__ __forceinline__ u32 load_x(const double2 *sm, u32 pl, double2 (&X)[8]
 {
     const u32 b0 = swz(ins0(pl, H));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) X[j] = sm[b0 ^ swz(ins0(256u * j, H))];
+    for (int j = 0; j < SW_NJ; ++j) X[j] = sm[b0 ^ swz(ins0((u32)KT * j, H))];
     return b0;
 }
 // WRE / WIM: transform that component (else its strings sum the 8 products
@@ -603,22 +610,22 @@ __device__ __forceinline__ void wht8x(const double2 *sm, u32 b0, const double2 (
                                       double (&Wr)[8], double (&Wi)[8])
 {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const double2 x = X[j], y = sm[b0 ^ swz(ins0(256u * j, H)) ^ sF];
+    for (int j = 0; j < SW_NJ; ++j) {
+        const double2 x = X[j], y = sm[b0 ^ swz(ins0((u32)KT * j, H)) ^ sF];
         if (RE) Wr[j] = fma(x.x, y.x, x.y * y.y);
         if (IM) Wi[j] = fma(x.x, y.y, -x.y * y.x);
     }
 #pragma unroll
-    for (int b = 1; b < 8; b <<= 1) {
+    for (int b = 1; b < SW_NJ; b <<= 1) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < SW_NJ; ++r) {
             if (r & b) continue;
             if (RE && WRE) { const double u = Wr[r], v = Wr[r | b]; Wr[r] = u + v; Wr[r | b] = u - v; }
             if (IM && WIM) { const double u = Wi[r], v = Wi[r | b]; Wi[r] = u + v; Wi[r | b] = u - v; }
         }
     }
 }
-__device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void gsync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(KT) : "memory"); }
 __device__ __forceinline__ u64 tbase(u64 tile, int lane, int ncomp, int comp_lane)
 {
     u64 bit = (lane < ncomp && ((tile >> lane) & 1ull)) ? (1ull << comp_lane) : 0ull;
@@ -650,7 +657,7 @@ __device__ __forceinline__ int ring_bar(int it) { return it % KSTAGES + KSTAGES 
 // generated: every flip group of the sweep on one tile (acc[] persists across tiles)
 __device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT]);
 
-extern "C" __global__ void __launch_bounds__(2 * KT, 1)
+extern "C" __global__ void __launch_bounds__(512, 1)
 qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_offhi,
           const int *__restrict__ g_geo, double *__restrict__ partial)
 {
@@ -660,7 +667,7 @@ qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restri
     u64 *offhi = reinterpret_cast<u64 *>(bufs + KSTAGES * TSIZE);
     const int nhi = 1 << (12 - c);
     const u32 tid_all = threadIdx.x;
-    for (int i = tid_all; i < nhi; i += 2 * KT) offhi[i] = __ldg(g_offhi + i);
+    for (int i = tid_all; i < nhi; i += 512) offhi[i] = __ldg(g_offhi + i);
     if (tid_all == 0) {
         for (int s = 0; s < 2 * KSTAGES; ++s) mbar_init(full + s, KT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -691,13 +698,15 @@ qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restri
             }
             cp_async_mbar_arrive(full + ring_bar(it));
         };
-        if (grp == 0) {
+        if (SW_GROUPS == 1) {
+            for (int it = 0; it < KSTAGES && it < T; ++it) load(it);
+        } else if (grp == 0) {
             load(0);
             if (T > 2) load(2);
         } else if (T > 1) {
             load(1);
         }
-        for (int it = grp; it < T; it += 2) {
+        for (int it = grp; it < T; it += SW_GROUPS) {
             const u64 tile = blockIdx.x + (u64)it * gridDim.x;
             const u64 base = tbase(tile, lane, ncomp, comp_lane);
             mbar_wait(full + ring_bar(it), (u32)((it / (2 * KSTAGES)) & 1));
@@ -722,7 +731,7 @@ qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restri
         if (lane == 0 && col >= 0) row[col] = v;
     }
 #else
-    double *row = partial + (size_t)(blockIdx.x * 16 + grp * 8 + warp) * MAXT;
+    double *row = partial + (size_t)(blockIdx.x * 16 + grp * (KT / 32) + warp) * MAXT;
 #pragma unroll
     for (int i = 0; i < MAXT; ++i) {
         const double v = wsum(acc[i]);
@@ -1035,25 +1044,29 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
 // loads, products, 8-point transform / direct sums; string t accumulates
 // into acc[slot[t]].  Uses `pl` (0..255, the thread's pair base) and `base`.
 static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, const std::vector<int> &slot,
-                         std::string &fn)
+                         std::string &fn, int nj = 8)
 {
+    // nj = pairs per thread (8: groups of 256 threads, 4: one group of 512);
+    // pair index p = pl + nt j with pl < nt = 2048 / nj
+    const unsigned nt = 2048u / (unsigned)nj;
+    const int lnt = nj == 8 ? 8 : 9, lnj = nj == 8 ? 3 : 2;
     char buf[512];
     int prev_h = -1;
     // a component with <= kDirect strings skips its 8-point transform
     // (24 adds) and sums each string's 8 products directly (7 adds)
-    const int kDirect = 3;
+    const int kDirect = nj == 8 ? 3 : 2;
     auto direct = [&](const GroupRec &G) {
         return G.t_im - G.t0 <= kDirect && G.t1 - G.t_im <= kDirect;
     };
     // tile positions of pair bits 8..10 for highest flip bit H (ins0 skips H)
-    auto rpos = [](int H, int k) { return (8 + k) + ((8 + k) >= H ? 1 : 0); };
+    auto rpos = [&](int H, int k) { return (lnt + k) + ((lnt + k) >= H ? 1 : 0); };
     const char *env_share = getenv("QSV_SWEEP_SHARE");
     const bool share = !(env_share && env_share[0] == '0');
     const char *env_fs = getenv("QSV_SWEEP_FUSE1");  // 0: product + add even for single strings
     const bool fuse_single = !(env_fs && env_fs[0] == '0');
     auto sign_expr = [&](const TermRec &tr) {
         snprintf(buf, sizeof(buf), "((__popc(pl & %uu) + __popcll(base & %lluull)) & 1) ? %.17g : %.17g",
-                 tr.s_loc & 255u, (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
+                 tr.s_loc & (nt - 1u), (unsigned long long)tr.s_hi, -tr.scale, tr.scale);
         return std::string(buf);
     };
     size_t gi = 0;
@@ -1070,14 +1083,14 @@ static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, con
             // 8..10 read a permutation of G's l1-side amplitudes: ONE load of
             // y_j serves them all (member k uses pair j ^ d_k)
             uint32_t R = 0;
-            for (int k = 0; k < 3; ++k) R |= 1u << rpos(G.h, k);
+            for (int k = 0; k < lnj; ++k) R |= 1u << rpos(G.h, k);
             std::vector<std::pair<size_t, unsigned>> cls{{gl[gi], 0u}};
             size_t k = gi + 1;
             while (k < gl.size() && sp.groups[gl[k]].h == G.h && direct(sp.groups[gl[k]]) &&
                    ((sp.groups[gl[k]].f_loc ^ G.f_loc) & ~R) == 0) {
                 const uint32_t D = sp.groups[gl[k]].f_loc ^ G.f_loc;
                 unsigned d = 0;
-                for (int q = 0; q < 3; ++q) d |= ((D >> rpos(G.h, q)) & 1u) << q;
+                for (int q = 0; q < lnj; ++q) d |= ((D >> rpos(G.h, q)) & 1u) << q;
                 cls.push_back({gl[k], d});
                 ++k;
             }
@@ -1087,9 +1100,9 @@ static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, con
                     snprintf(buf, sizeof(buf), "    double s%d = 0.0;\n", t);
                     fn += buf;
                 }
-            for (unsigned J = 0; J < 8; ++J) {
+            for (unsigned J = 0; J < (unsigned)nj; ++J) {
                 snprintf(buf, sizeof(buf),
-                         "    { const double2 y = sm[b0 ^ swz(ins0(%uu, %d)) ^ %uu];\n", 256u * J, G.h,
+                         "    { const double2 y = sm[b0 ^ swz(ins0(%uu, %d)) ^ %uu];\n", nt * J, G.h,
                          h_swz(G.f_loc));
                 fn += buf;
                 for (size_t q = 0; q < cls.size(); ++q) {
@@ -1112,7 +1125,7 @@ static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, con
                     }
                     for (int t = M.t0; t < M.t1; ++t) {
                         const TermRec &tr = sp.terms[t];
-                        const unsigned msk = (tr.s_loc >> 8) & 7u;
+                        const unsigned msk = (tr.s_loc >> lnt) & (unsigned)(nj - 1);
                         const bool neg = __builtin_popcount(jj & msk) & 1;
                         if (tr.use_im ? fuse_im : fuse_re) {
                             if (tr.use_im)  // Im(conj x y) = x.re y.im - x.im y.re
@@ -1152,14 +1165,14 @@ static void emit_pairbit(const SweepPlan &sp, const std::vector<size_t> &gl, con
         for (int t = G.t0; t < G.t1; ++t) {
             const TermRec &tr = sp.terms[t];
             const char *W = tr.use_im ? "Wi" : "Wr";
-            const unsigned msk = (tr.s_loc >> 8) & 7u;
+            const unsigned msk = (tr.s_loc >> lnt) & (unsigned)(nj - 1);
             std::string val;
             if (tr.use_im ? w_im : w_re) {
                 snprintf(buf, sizeof(buf), "%s[%u]", W, msk);
                 val = buf;
             } else {  // W[m] of the transform = sum_j (-1)^{|j & m|} w_j
                 val = "(";
-                for (unsigned j = 0; j < 8; ++j) {
+                for (unsigned j = 0; j < (unsigned)nj; ++j) {
                     snprintf(buf, sizeof(buf), "%s%s[%u]", j == 0 ? "" : (__builtin_popcount(j & msk) & 1) ? " - " : " + ", W, j);
                     val += buf;
                 }
@@ -1537,15 +1550,20 @@ bool jit_sweep_source(const SweepPlan &sp, std::string &src)
         if (env_w && env_w[0] == '1' && jit_sweep_source_warps(sp, src)) return true;
     }
     if (nterms > 48) return false;
+    // QSV_SWEEP_ONETILE=1: one 512-thread group per CTA sweeps one tile while
+    // the next two load (4 pairs per thread), instead of two 256-thread
+    // groups on alternate tiles with one tile in flight
+    const char *env_ot = getenv("QSV_SWEEP_ONETILE");
+    const bool onetile = env_ot && env_ot[0] == '1';
     std::string fn = "__device__ __forceinline__ void sweep_tile(const double2 *sm, u32 pl, u64 base, double (&acc)[MAXT])\n{\n";
     std::vector<size_t> gl(sp.groups.size());
     for (size_t i = 0; i < gl.size(); ++i) gl[i] = i;
     std::vector<int> slot(nterms);
     for (int t = 0; t < nterms; ++t) slot[t] = t;
-    emit_pairbit(sp, gl, slot, fn);
+    emit_pairbit(sp, gl, slot, fn, onetile ? 4 : 8);
     fn += "}\n";
-    char buf[64];
-    snprintf(buf, sizeof(buf), "#define MAXT %d\n", nterms);
+    char buf[96];
+    snprintf(buf, sizeof(buf), "#define MAXT %d\n#define SW_GROUPS %d\n", nterms, onetile ? 1 : 2);
     src = buf;
     src += kSweepSkeleton;
     src += fn;
