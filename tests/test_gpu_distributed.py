@@ -195,6 +195,15 @@ def test_native_multidevice_brickwork_vs_oracle(P, n, layers):
     assert np.abs(st.amplitudes - ref).max() < 1e-10
     info = st.info()
     assert info["ranks"] == P and info["relayouts"] >= 1
+    # the C++ scheduler is the Python one (distributed.plan_segments): same
+    # relayouts and the same final qubit map
+    from paper_2208_10978_b200 import distributed as Dm
+    from paper_2208_10978_b200.circuit import flatten_bound
+
+    k, q, _ = flatten_bound(circ)
+    segs, perm = Dm.plan_segments(k, q, n, n - (P.bit_length() - 1), list(range(n)))
+    assert info["relayouts"] == sum(1 for sg in segs if sg.relayout is not None)
+    assert info["perm"] == list(perm)
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
