@@ -292,12 +292,16 @@ __device__ __forceinline__ void gm(double2 (&a)[16], u32 par0)
     }
 }
 
+#ifdef QSV_GMD
 // gm with the table offset P and the block sign mask ZB at run time: one code
 // body per flip pattern F, shared by every group with that pattern (the
 // compact form of small-state passes, whose straight-line code would be
-// executed once and stream through the instruction cache)
+// executed once and stream through the instruction cache).  The matrices are
+// read from the pass's parameter copy in shared memory (QS: stage 2 of the
+// ring, which a pass over <= 2 tiles per CTA never fills) as 16-B broadcast
+// loads -- four per pair instead of eight run-time-indexed constant loads.
 template <int F>
-__device__ __forceinline__ void gm_rt(double2 (&a)[16], u32 par0, int P, u32 ZB)
+__device__ __forceinline__ void gm_rt(double2 (&a)[16], u32 par0, int P, u32 ZB, const double2 *QS)
 {
     constexpr int H = hbit(F);
 #pragma unroll
@@ -305,22 +309,26 @@ __device__ __forceinline__ void gm_rt(double2 (&a)[16], u32 par0, int P, u32 ZB)
         if (r & (1 << H)) continue;
         const int r1 = r ^ F;
         const u32 cp = par0 ^ (u32)(__popc((u32)r1 & ZB) & 1);
-        const int M = P + 8 * gm_cfg<F>(r1);
+        const double2 *M = QS + ((P + 8 * gm_cfg<F>(r1)) >> 1);
+        const double2 m01 = M[0], m23 = M[1], m45 = M[2], m67 = M[3];
         const double2 x = a[r], yy = a[r1];
         const double2 y = make_double2(negif(yy.x, cp), negif(yy.y, cp));
         double2 o0, o1;
-        o0.x = fma(C[M], x.x, fma(-C[M + 1], x.y, fma(C[M + 2], y.x, -C[M + 3] * y.y)));
-        o0.y = fma(C[M], x.y, fma(C[M + 1], x.x, fma(C[M + 2], y.y, C[M + 3] * y.x)));
-        o1.x = fma(C[M + 4], x.x, fma(-C[M + 5], x.y, fma(C[M + 6], y.x, -C[M + 7] * y.y)));
-        o1.y = fma(C[M + 4], x.y, fma(C[M + 5], x.x, fma(C[M + 6], y.y, C[M + 7] * y.x)));
+        o0.x = fma(m01.x, x.x, fma(-m01.y, x.y, fma(m23.x, y.x, -m23.y * y.y)));
+        o0.y = fma(m01.x, x.y, fma(m01.y, x.x, fma(m23.x, y.y, m23.y * y.x)));
+        o1.x = fma(m45.x, x.x, fma(-m45.y, x.y, fma(m67.x, y.x, -m67.y * y.y)));
+        o1.y = fma(m45.x, x.y, fma(m45.y, x.x, fma(m67.x, y.y, m67.y * y.x)));
         a[r] = o0;
         a[r1] = make_double2(negif(o1.x, cp), negif(o1.y, cp));
     }
 }
+#endif
 #ifdef QSV_GMD
 // a run of fused rotation groups [k0, k1) of the descriptor table
 __device__ __forceinline__ void gm_run(double2 (&a)[16], u32 tid, u64 base, int k0, int k1)
 {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const double2 *QS = reinterpret_cast<const double2 *>(smem_raw + 1024) + 2 * TSIZE;
 #pragma unroll 1
     for (int k = k0; k < k1; ++k) {
         const u32 pk = GMD_PK[k];
@@ -328,21 +336,21 @@ __device__ __forceinline__ void gm_run(double2 (&a)[16], u32 tid, u64 base, int 
         const int P = GMD_P[k];
         const u32 zb = (pk >> 4) & 15u;
         switch (pk & 15u) {
-            case 1: gm_rt<1>(a, par0, P, zb); break;
-            case 2: gm_rt<2>(a, par0, P, zb); break;
-            case 3: gm_rt<3>(a, par0, P, zb); break;
-            case 4: gm_rt<4>(a, par0, P, zb); break;
-            case 5: gm_rt<5>(a, par0, P, zb); break;
-            case 6: gm_rt<6>(a, par0, P, zb); break;
-            case 7: gm_rt<7>(a, par0, P, zb); break;
-            case 8: gm_rt<8>(a, par0, P, zb); break;
-            case 9: gm_rt<9>(a, par0, P, zb); break;
-            case 10: gm_rt<10>(a, par0, P, zb); break;
-            case 11: gm_rt<11>(a, par0, P, zb); break;
-            case 12: gm_rt<12>(a, par0, P, zb); break;
-            case 13: gm_rt<13>(a, par0, P, zb); break;
-            case 14: gm_rt<14>(a, par0, P, zb); break;
-            default: gm_rt<15>(a, par0, P, zb); break;
+            case 1: gm_rt<1>(a, par0, P, zb, QS); break;
+            case 2: gm_rt<2>(a, par0, P, zb, QS); break;
+            case 3: gm_rt<3>(a, par0, P, zb, QS); break;
+            case 4: gm_rt<4>(a, par0, P, zb, QS); break;
+            case 5: gm_rt<5>(a, par0, P, zb, QS); break;
+            case 6: gm_rt<6>(a, par0, P, zb, QS); break;
+            case 7: gm_rt<7>(a, par0, P, zb, QS); break;
+            case 8: gm_rt<8>(a, par0, P, zb, QS); break;
+            case 9: gm_rt<9>(a, par0, P, zb, QS); break;
+            case 10: gm_rt<10>(a, par0, P, zb, QS); break;
+            case 11: gm_rt<11>(a, par0, P, zb, QS); break;
+            case 12: gm_rt<12>(a, par0, P, zb, QS); break;
+            case 13: gm_rt<13>(a, par0, P, zb, QS); break;
+            case 14: gm_rt<14>(a, par0, P, zb, QS); break;
+            default: gm_rt<15>(a, par0, P, zb, QS); break;
         }
     }
 }
@@ -435,7 +443,12 @@ __device__ __forceinline__ void tma_row(void *dst, const TmapParam *tm, int y, u
 
 __device__ __forceinline__ void apply_tile(double2 *sm, u32 tid, int bar, u64 base);
 
-extern "C" __global__ void __launch_bounds__(2 * KT, 1)
+#ifdef QSV_GMD
+#define QSV_PASS_THREADS KT  // compact passes: one tile group (<= 255 registers)
+#else
+#define QSV_PASS_THREADS (2 * KT)
+#endif
+extern "C" __global__ void __launch_bounds__(QSV_PASS_THREADS, 1)
 qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_offhi,
          const int *__restrict__ g_geo, u64 basis, const __grid_constant__ TmapParam tmap, int tma)
 {
@@ -446,7 +459,7 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
     u64 *offhi = reinterpret_cast<u64 *>(bufs + KSTAGES * TSIZE);
     const int nhi = 1 << (12 - c);
     const u32 tid_all = threadIdx.x;
-    for (int i = tid_all; i < nhi; i += 2 * KT) offhi[i] = __ldg(g_offhi + i);
+    for (int i = tid_all; i < nhi; i += QSV_PASS_THREADS) offhi[i] = __ldg(g_offhi + i);
     if (tid_all < 16) {
         u32 v = 0;
         for (int j = 0; j < 4; ++j)
@@ -457,10 +470,19 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
         for (int s = 0; s < 2 * KSTAGES; ++s) mbar_init(full + s, KT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+#ifdef QSV_GMD
+    {  // the pass parameters into ring stage 2 (gm_rt's broadcast loads)
+        double *qs = reinterpret_cast<double *>(bufs + 2 * TSIZE);
+        for (int i = tid_all; i < QSV_NPARAMS; i += QSV_PASS_THREADS) qs[i] = C[i];
+    }
+#endif
     __syncthreads();
     const u64 ntiles = 1ull << ncomp;
     if ((u64)blockIdx.x >= ntiles) return;
     const int T = (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1;
+#ifdef QSV_GMD
+    if (T > 1) __trap();  // one tile per CTA (compact passes cover <= 8 tiles)
+#endif
     const int grp = (int)(tid_all / KT);
     const u32 tid = tid_all % KT;
     const int bar = 1 + grp;
@@ -750,6 +772,7 @@ struct Module {
     CUfunction fn = nullptr;
     CUdeviceptr cparams = 0;
     size_t cbytes = 0;
+    unsigned threads = 512;  // 256 for compact passes (one tile group)
     bool failed = false;
     std::vector<char> cubin;
     std::string log;
@@ -895,7 +918,8 @@ bool jit_source(const TileGeom &g, const BlockRec *blocks, int nblocks, const Op
     bool all_gmat = nblocks > 0;
     for (int bi = 0; bi < nblocks && all_gmat; ++bi) {
         if (blocks[bi].kind != 0) all_gmat = false;
-        for (int k = blocks[bi].op0; k < blocks[bi].op1 && all_gmat; ++k) all_gmat = ops[k].type == OP_GMAT;
+        for (int k = blocks[bi].op0; k < blocks[bi].op1 && all_gmat; ++k)
+            all_gmat = ops[k].type == OP_GMAT && (ops[k].p & 1) == 0;  // 16-B aligned matrices
     }
     const char *env_cg = getenv("QSV_COMPACT_GMAT");
     const bool compact = all_gmat && env_cg && env_cg[0] == '1' && g.ncomp <= 3 && n_gmat >= 16;
@@ -1626,8 +1650,11 @@ int jit_prepare(int device, const std::vector<const std::string *> &srcs, std::s
             err = "cuModuleLoadData / GetFunction failed";
             continue;
         }
-        const int smem = 256 + 3 * (16 << kMaxTileBits) + 8 * (1 << (kMaxTileBits - 1));  // any c >= 1
+        // the largest launch of either kind: a pass (1 KiB header for the
+        // 1024-B aligned TMA stages) over c = 1 tiles (2^11 offsets)
+        const int smem = 1024 + 3 * (16 << kMaxTileBits) + 8 * (1 << (kMaxTileBits - 1));
         g_api.FuncSetAttribute(m.fn, 8 /* CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES */, smem);
+        if (!m.sweep && todo[i].first->find("#define QSV_GMD") != std::string::npos) m.threads = 256;
         m.cubin.clear();
         m.cubin.shrink_to_fit();
     }
@@ -1693,7 +1720,7 @@ bool jit_launch_module(const void *mod, double2 *psi, const TileDims &g, const u
     int tma = pass_tma_map(psi, g, &tmap) ? 1 : 0;
     void *args[] = {&psi, &ncomp, &c, (void *)&d_offhi, (void *)&d_geo, &basis, &tmap, &tma};
     const unsigned smem = 1024 + 3 * (16u << kMaxTileBits) + 8u * (1u << (kMaxTileBits - g.c));
-    return g_api.LaunchKernel(m.fn, (unsigned)grid, 1, 1, 512, 1, 1, smem, st, args, nullptr) == 0;
+    return g_api.LaunchKernel(m.fn, (unsigned)grid, 1, 1, m.threads, 1, 1, smem, st, args, nullptr) == 0;
 }
 
 
