@@ -984,10 +984,55 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
     auto flush = [&]() {
         if (!pending.empty()) {
             constexpr int RB = kBlockBits, TB = kMaxTileBits - kBlockBits;
-            const bool conform = Wmask != 0 && (cur & Wmask) == 0;
-            uint32_t bits = cur;
-            for (int b = m - 1; b >= 0 && __builtin_popcount(bits) < RB; --b)
-                if (!conform || !((Wmask >> b) & 1u)) bits |= 1u << b;
+            bool conform = Wmask != 0 && (cur & Wmask) == 0;
+            // The filler register bits (beyond the ones the ops need) are free:
+            // if the default ones leave the lane-eligible thread columns (not
+            // in registers, not W bits of a conforming block) without three
+            // independent granule vectors, every LDS/STS of the block is a
+            // 2-way bank conflict -- pick fillers that keep the rank at 3, or
+            // else give up the warp-local W placement for this block (a group
+            // barrier instead of __syncwarp around it).
+            auto lane_rank = [&](uint32_t regs, bool conf) {
+                uint32_t basis[3] = {0, 0, 0};
+                int np = 0;
+                for (int b = 0; b < m && np < 3; ++b) {
+                    if (((regs >> b) & 1u) || (conf && ((Wmask >> b) & 1u))) continue;
+                    uint32_t v = swz16(Ab[b]) & 7u;
+                    for (int j = 0; j < np; ++j)
+                        if ((v ^ basis[j]) < v) v ^= basis[j];
+                    if (v == 0) continue;
+                    basis[np] = v;
+                    for (int a = np; a > 0 && basis[a] > basis[a - 1]; --a) std::swap(basis[a], basis[a - 1]);
+                    ++np;
+                }
+                return np;
+            };
+            auto fill = [&](bool conf) {
+                uint32_t regs = cur;
+                for (int b = m - 1; b >= 0 && __builtin_popcount(regs) < RB; --b)
+                    if (!conf || !((Wmask >> b) & 1u)) regs |= 1u << b;
+                if (lane_rank(regs, conf) == 3) return regs;
+                int cand[12], nc = 0;  // filler candidates, preferred (high) bits first
+                for (int b = m - 1; b >= 0; --b)
+                    if (!((cur >> b) & 1u) && (!conf || !((Wmask >> b) & 1u))) cand[nc++] = b;
+                const int need = RB - __builtin_popcount(cur);
+                for (uint32_t sel = 0; sel < (1u << nc); ++sel) {
+                    if (__builtin_popcount(sel) != need) continue;
+                    uint32_t alt = cur;
+                    for (int i = 0; i < nc; ++i)
+                        if ((sel >> i) & 1u) alt |= 1u << cand[i];
+                    if (lane_rank(alt, conf) == 3) return alt;
+                }
+                return regs;
+            };
+            uint32_t bits = fill(conform);
+            if (conform && lane_rank(bits, true) < 3) {
+                const uint32_t alt = fill(false);
+                if (lane_rank(alt, false) == 3) {
+                    bits = alt;
+                    conform = false;
+                }
+            }
             int pos[RB], nb[12], k = 0, kn = 0;
             for (int b = 0; b < m; ++b) {
                 if ((bits >> b) & 1u) pos[k++] = b;

@@ -284,3 +284,28 @@ def test_emulated_singular_u3_angles_take_the_plain_plan():
     out = emulator.run_program(prog, psi0)
     assert np.all(np.isfinite(out))
     assert np.abs(out - O.evolve(psi0, circ.gates)).max() <= 1e-12
+
+
+def test_gate_pass_blocks_bank_conflict_free():
+    """Every register block of config 2's plan puts three thread columns with
+    independent 16-B granule vectors on lane bits 0-2, so its 128-bit LDS/STS
+    are conflict-free (a block whose W-bit placement would leave rank 2 gives
+    it up; ncu showed 2-way conflicts on two such blocks before)."""
+    circ = W.brickwork(28, 20, seed=0)
+    k, q, v = flatten_bound(circ)
+    plan = _lib.debug_plan(28, k, q, v)
+
+    def rank(vs):
+        basis = []
+        for x in vs:
+            x &= 7
+            for b in basis:
+                x = min(x, x ^ b)
+            if x:
+                basis.append(x)
+                basis.sort(reverse=True)
+        return len(basis)
+
+    blocks = [b for p in plan["passes"] for b in p.get("blocks", []) if b["kind"] == 0]
+    assert len(blocks) > 100
+    assert all(rank(b["cols"][:3]) == 3 for b in blocks)
