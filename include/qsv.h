@@ -250,6 +250,13 @@ int qsv_debug_plan_json(int n_qubits, int64_t n_gates, const int32_t *kinds,
  * passes are specialised. */
 int qsv_jit_info(int *available, int64_t *launches);
 
+/* Small-state rotation programs: a program made only of Pauli rotations on
+ * <= 12 qubits (config 1) runs as one CTA with the state in shared memory
+ * instead of tile passes (replaces the same statevector.py:65-74 gate loop).
+ * launches = number of such launches so far in this process.  Env:
+ * QSV_SMALL=0 runs these programs as tile passes. */
+int qsv_small_info(int64_t *launches);
+
 /* Statistics of the last plan on the calling thread (see qsv_plan_stats). */
 int qsv_last_plan_stats(qsv_plan_stats *out);
 

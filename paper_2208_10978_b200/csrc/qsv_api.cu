@@ -895,6 +895,38 @@ int qsv_evolve_basis(qsv_state *s, uint64_t index, int64_t n_gates, const int32_
     return apply_gates_impl(s, n_gates, kinds, qubits, values, stats, index);
 }
 
+// Small-state rotation programs (qsv_small.cu): on by default, QSV_SMALL=0
+// runs them as tile passes (A/B and parity cross-checks).
+static bool small_enabled()
+{
+    const char *e = getenv("QSV_SMALL");
+    return !(e && e[0] == '0');
+}
+
+static int64_t g_small_launches = 0;
+
+static int run_small(qsv_state *s, const ProgramTemplate &t, const double *values, uint64_t basis)
+{
+    DeviceCtx *c = nullptr;
+    if (int rc = ctx_for(s->device, &c)) return rc;
+    const SmallProgram &sp = t.small;
+    Blob b;
+    const size_t o_g = b.add(sp.groups.data(), sp.groups.size() * sizeof(SmallGroup));
+    const size_t o_m = b.add(sp.meta.data(), sp.meta.size() * sizeof(int32_t));
+    const size_t o_c = b.add(sp.chunks.data(), sp.chunks.size() * sizeof(int32_t));
+    const size_t o_t = b.add(nullptr, sp.src.size() * sizeof(double));
+    double *th = reinterpret_cast<double *>(b.bytes.data() + o_t);
+    for (size_t r = 0; r < sp.src.size(); ++r) th[r] = values[3 * (size_t)sp.src[r]];
+    char *d = nullptr;
+    size_t scratch = 0;
+    if (int rc = upload_blob(*c, s->stream, b, 0, &d, &scratch)) return rc;
+    QSV_CUDA(launch_small(s->amps, s->n, basis, (const SmallGroup *)(d + o_g), (const int32_t *)(d + o_m),
+                          (const double *)(d + o_t), (const int32_t *)(d + o_c), (int)(sp.chunks.size() / 2),
+                          s->stream));
+    ++g_small_launches;
+    return QSV_OK;
+}
+
 static int apply_gates_impl(qsv_state *s, int64_t n_gates, const int32_t *kinds,
                             const int32_t *qubits, const double *values, qsv_plan_stats *stats,
                             uint64_t basis)
@@ -953,6 +985,10 @@ static int apply_gates_impl(qsv_state *s, int64_t n_gates, const int32_t *kinds,
         tpl = &g_cache.front().tpl;
     }
     prof.mark("lookup");
+    if (tpl->small.valid && small_enabled()) {
+        fill_stats(*tpl, hit, stats);
+        return run_small(s, *tpl, values, basis);
+    }
     if (!plain_u3() && needs_plain_u3(*tpl, values)) {
         // an angle the normalised U3 forms cannot take: a plan without them
         PlainU3Scope plain;
@@ -1056,6 +1092,10 @@ static int apply_prepared_impl(qsv_state *s, int64_t program_id, const double *v
     }
     if (bad) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
     QSV_CUDA(cudaSetDevice(s->device));
+    if (e.tpl.small.valid && small_enabled()) {
+        fill_stats(e.tpl, e.uses++ > 0, stats);
+        return run_small(s, e.tpl, values, basis);
+    }
     if (!plain_u3() && needs_plain_u3(e.tpl, values)) {
         PlainU3Scope plain;  // structure-cache path with a plan without normalised U3 forms
         return apply_gates_impl(s, n_gates, e.kinds.data(), e.qubits.data(), values, stats, basis);
@@ -1723,6 +1763,14 @@ int qsv_sample_parity(const qsv_state *s, uint64_t support_mask, int64_t shots,
     // np.mean(1 - 2 parity): an exact integer sum, one rounding
     *out_mean = (double)(shots - 2 * (int64_t)odd) / (double)shots;
     return release_big_work(*c, s->stream);
+}
+
+int qsv_small_info(int64_t *launches)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!launches) return fail_code(QSV_ERR_INVALID, "null output");
+    *launches = g_small_launches;
+    return QSV_OK;
 }
 
 int qsv_jit_info(int *available, int64_t *launches)

@@ -1470,6 +1470,7 @@ void match_rotations(int64_t N, const int32_t *kinds, const int32_t *qubits, std
 {
     out.clear();
     int64_t i = 0;
+    bool all_rot = true;
     while (i < N) {
         Rot rot;
         int64_t len = 0;
@@ -1546,6 +1547,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
     std::vector<Rot> R;
     std::vector<Item> items;
     int64_t i = 0;
+    bool all_rot = true;
     while (i < N) {
         Rot rot;
         int64_t len = 0;
@@ -1572,6 +1574,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
             }
             i += len;
         } else {
+            all_rot = false;
             Item it;
             it.gate = (int)i;
             uint64_t s = 1ull << qubits[2 * i];
@@ -1594,6 +1597,7 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
     t.src_kinds.assign(kinds, kinds + N);
     t.src_qubits.assign(qubits, qubits + 2 * N);
     t.n_rotations = (int64_t)R.size();
+    if (all_rot && n <= kSmallMaxQubits) build_small_program(n, R, t.small);
 }
 
 void plan_rotations(int n, const std::vector<Rot> &R, int64_t n_input, ProgramTemplate &t)

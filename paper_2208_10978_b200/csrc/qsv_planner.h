@@ -91,8 +91,42 @@ struct ClusterFill {
     std::vector<int> gates;   // source gate indices, in application order
 };
 
+// Small-state rotation program (qsv_small.cu): a state of <= kSmallMaxQubits
+// qubits made only of Pauli rotations runs as ONE CTA that keeps the whole
+// state in shared memory and walks the same-flip rotation groups with 1024
+// threads (a pair per thread per group), instead of tile passes whose
+// straight-line code would stream through one SM's instruction cache.
+constexpr int kSmallMaxQubits = 12;
+constexpr int kSmallMinQubits = 8;
+constexpr int kSmallShare = 3;  // null-space vectors kept per group (the kernel uses 2 or 3)
+struct SmallGroup {    // 64 B
+    uint32_t xm;       // flip mask (X and Y positions) shared by the group
+    // phase masks over the PAIR index p (lo = p with a 0 inserted at bit h):
+    // the basis of the rotations' phase-mask differences b0..b2 (0: unused)
+    // and the first rotation's phase mask z0, each with bit h removed --
+    // parity(lo & m) = parity(p & pm), so a pair's config is linear in p
+    uint32_t pm[4];
+    // kSmallShare independent pair-index vectors u with parity(u & pm[j]) = 0
+    // for all j, mapped to amplitude space (lu = u with a 0 inserted at h):
+    // the pairs p0 ^ span(u) share p0's config, so one thread applies them
+    // with one matrix load; piv = their pivot bits (ascending), where p0 has 0s
+    uint32_t lu[3];
+    int32_t piv[3];
+    int32_t h;         // pivot of xm: its highest bit (bit h of lo = 0)
+    int32_t r0, r1;    // rotations [r0, r1) in application order
+    int32_t dimb;      // number of basis differences (configs = 2^dimb, x 2 for the sign)
+};
+struct SmallProgram {
+    bool valid = false;
+    std::vector<SmallGroup> groups;
+    std::vector<int32_t> meta;    // per rotation: ny mod 4 | (ny odd) << 2 | coordinates << 3
+    std::vector<int32_t> src;     // per rotation: its angle is values[3 * src]
+    std::vector<int32_t> chunks;  // [g0, g1) group ranges sized for the shared-memory tables
+};
+
 struct ProgramTemplate {
     int n = 0, m = 0, c = 0;
+    SmallProgram small;  // valid: the whole program is rotations on <= 12 qubits
     std::vector<PassPlan> passes;
     std::vector<OpRec> ops;
     std::vector<BlockRec> blocks;
@@ -121,6 +155,9 @@ struct Rot {
     uint64_t x, y, z;
     int src;
 };
+
+// Build the small program of a rotation list (false: not eligible).
+bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp);
 
 // Build a template from a gate list (kinds/qubits as in qsv_apply_gates).
 void plan_gates(int n, int64_t n_gates, const int32_t *kinds, const int32_t *qubits,
