@@ -96,10 +96,13 @@ def test_invalid_inputs_raise():
 
 
 @pytest.mark.parametrize("n,ne", [(12, 6), (13, 6)])
-def test_hot_program_specialisation(n, ne):
+def test_hot_program_specialisation(n, ne, monkeypatch):
     """Below the specialisation threshold a structure is compiled once it has
     run QSV_JIT_HOT_USES (3) times; every run -- interpreted, then
-    specialised, with new angles each time -- matches the oracle."""
+    specialised, with new angles each time -- matches the oracle.  (Tile
+    passes forced: at 12 q a rotation-only program otherwise runs as a
+    small-state program, tests/test_gpu_small.py.)"""
+    monkeypatch.setenv("QSV_SMALL", "0")
     from paper_2208_10978_b200 import _lib
     from paper_2208_10978_b200.circuit import bind
 
