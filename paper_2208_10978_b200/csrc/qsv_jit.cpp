@@ -455,11 +455,16 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     u64 *full = reinterpret_cast<u64 *>(smem_raw);
     u32 *st_k = reinterpret_cast<u32 *>(full + 2 * KSTAGES);
+    u64 *offk = reinterpret_cast<u64 *>(smem_raw + 256);  // per-k global offsets (see below)
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 1024);  // 1024-B aligned stages (TMA swizzle)
     u64 *offhi = reinterpret_cast<u64 *>(bufs + KSTAGES * TSIZE);
     const int nhi = 1 << (12 - c);
     const u32 tid_all = threadIdx.x;
     for (int i = tid_all; i < nhi; i += QSV_PASS_THREADS) offhi[i] = __ldg(g_offhi + i);
+    if (tid_all < TSIZE / KT) {
+        const u32 l = tid_all * KT;
+        offk[tid_all] = (l & ((1u << c) - 1u)) + __ldg(g_offhi + (l >> c));
+    }
     if (tid_all < 16) {
         u32 v = 0;
         for (int j = 0; j < 4; ++j)
@@ -492,16 +497,21 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
     u32 st_base = (u32)__ldg(g_geo + 44);
     for (int i = 0; i < 8; ++i)
         if ((tid >> i) & 1u) st_base ^= (u32)__ldg(g_geo + 32 + i);
+    // loop-invariant parts of the tile addresses: slot l = tid + KT k is
+    // tid ^ KT k (tid < KT), and swz and the global offset (l & cmask) +
+    // offhi[l >> c] are both linear over disjoint index bits, so per k only a
+    // constant slot mask and one broadcast table entry offk[k] remain
+    const u32 swz_t = swz(tid);
+    const u64 goff_t = (u64)(tid & cmask) + offhi[tid >> c];
     auto load = [&](int it) {
         const u64 tile = blockIdx.x + (u64)it * gridDim.x;
         const u64 b = tbase(tile, lane, ncomp, comp_lane);
         double2 *buf = bufs + (it % KSTAGES) * TSIZE;
         if (basis != ~0ull) {  // the pass starts from |basis>: synthesise, no HBM read
-#pragma unroll 4
+#pragma unroll
             for (int k = 0; k < TSIZE / KT; ++k) {
-                const u32 l = tid + k * KT;
-                const u64 gi = b + (l & cmask) + offhi[l >> c];
-                buf[swz(l)] = make_double2(gi == basis ? 1.0 : 0.0, 0.0);
+                const u64 gi = b + goff_t + offk[k];
+                buf[swz_t ^ swz((u32)(k * KT))] = make_double2(gi == basis ? 1.0 : 0.0, 0.0);
             }
             mbar_arrive(full + ring_bar(it));
             return;
@@ -515,12 +525,10 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
                         full + ring_bar(it));
             return;
         }
-        const double2 *src = psi + b;
-#pragma unroll 4
-        for (int k = 0; k < TSIZE / KT; ++k) {
-            const u32 l = tid + k * KT;
-            cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
-        }
+        const double2 *src = psi + b + goff_t;
+#pragma unroll
+        for (int k = 0; k < TSIZE / KT; ++k)
+            cp_async16(buf + (swz_t ^ swz((u32)(k * KT))), src + offk[k]);
         cp_async_mbar_arrive(full + ring_bar(it));
     };
     if (grp == 0) {
@@ -536,12 +544,9 @@ qsv_pass(double2 *__restrict__ psi, int ncomp, int c, const u64 *__restrict__ g_
         mbar_wait(full + ring_bar(it), (u32)((it / (2 * KSTAGES)) & 1));
         double2 *sm = bufs + st * TSIZE;
         apply_tile(sm, tid, bar, base);
-        double2 *dst = psi + base;
-#pragma unroll 4
-        for (int k = 0; k < TSIZE / KT; ++k) {
-            const u32 l = tid + k * KT;
-            __stcs(dst + (l & cmask) + offhi[l >> c], sm[st_base ^ st_k[k]]);
-        }
+        double2 *dst = psi + base + goff_t;
+#pragma unroll
+        for (int k = 0; k < TSIZE / KT; ++k) __stcs(dst + offk[k], sm[st_base ^ st_k[k]]);
         if (it + KSTAGES < T) {
             gsync(bar);
             load(it + KSTAGES);
@@ -685,11 +690,16 @@ qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restri
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     u64 *full = reinterpret_cast<u64 *>(smem_raw);
+    u64 *offk = reinterpret_cast<u64 *>(smem_raw + 128);  // per-k global offsets (see qsv_pass)
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw + 256);
     u64 *offhi = reinterpret_cast<u64 *>(bufs + KSTAGES * TSIZE);
     const int nhi = 1 << (12 - c);
     const u32 tid_all = threadIdx.x;
     for (int i = tid_all; i < nhi; i += 512) offhi[i] = __ldg(g_offhi + i);
+    if (tid_all < TSIZE / KT) {
+        const u32 l = tid_all * KT;
+        offk[tid_all] = (l & ((1u << c) - 1u)) + __ldg(g_offhi + (l >> c));
+    }
     if (tid_all == 0) {
         for (int s = 0; s < 2 * KSTAGES; ++s) mbar_init(full + s, KT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -708,16 +718,17 @@ qsv_sweep(const double2 *__restrict__ psi, int ncomp, int c, const u64 *__restri
         const int T = (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1;
         const int comp_lane = __ldg(g_geo + lane);
         const u32 cmask = (1u << c) - 1u;
+        // loop-invariant address parts (see qsv_pass): l = tid ^ KT k
+        const u32 swz_t = swz(tid);
+        const u64 goff_t = (u64)(tid & cmask) + offhi[tid >> c];
         auto load = [&](int it) {
             const u64 tile = blockIdx.x + (u64)it * gridDim.x;
             const u64 b = tbase(tile, lane, ncomp, comp_lane);
             double2 *buf = bufs + (it % KSTAGES) * TSIZE;
-            const double2 *src = psi + b;
-#pragma unroll 4
-            for (int k = 0; k < TSIZE / KT; ++k) {
-                const u32 l = tid + k * KT;
-                cp_async16(buf + swz(l), src + (l & cmask) + offhi[l >> c]);
-            }
+            const double2 *src = psi + b + goff_t;
+#pragma unroll
+            for (int k = 0; k < TSIZE / KT; ++k)
+                cp_async16(buf + (swz_t ^ swz((u32)(k * KT))), src + offk[k]);
             cp_async_mbar_arrive(full + ring_bar(it));
         };
         if (SW_GROUPS == 1) {

@@ -1470,7 +1470,6 @@ void match_rotations(int64_t N, const int32_t *kinds, const int32_t *qubits, std
 {
     out.clear();
     int64_t i = 0;
-    bool all_rot = true;
     while (i < N) {
         Rot rot;
         int64_t len = 0;
