@@ -1680,8 +1680,17 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     }
     std::vector<double> params(t.n_params);
     materialize_params(t, values, params.data());
-    std::string j = "{\"n\":" + std::to_string(n) + ",\"block_bits\":" +
-                    std::to_string(kBlockBits) + ",\"passes\":[";
+    std::string j = "{\"n\":" + std::to_string(n) + ",\"block_bits\":" + std::to_string(kBlockBits);
+    // the small-state rotation program (qsv_small.cu), when the plan has one
+    j += ",\"small\":{\"valid\":" + std::to_string(t.small.valid ? 1 : 0) + ",\"groups\":[";
+    for (size_t g = 0; g < t.small.groups.size(); ++g) {
+        const SmallGroup &G = t.small.groups[g];
+        j += (g ? ",[" : "[") + std::to_string(G.xm) + "," + std::to_string(G.r0) + "," + std::to_string(G.r1) +
+             "," + std::to_string(G.dimb) + "]";
+    }
+    j += "],\"chunks\":[";
+    for (size_t i = 0; i < t.small.chunks.size(); ++i) j += (i ? "," : "") + std::to_string(t.small.chunks[i]);
+    j += "]},\"passes\":[";
     char buf[256];
     for (size_t k = 0; k < t.passes.size(); ++k) {
         const PassPlan &p = t.passes[k];

@@ -309,3 +309,43 @@ def test_gate_pass_blocks_bank_conflict_free():
     blocks = [b for p in plan["passes"] for b in p.get("blocks", []) if b["kind"] == 0]
     assert len(blocks) > 100
     assert all(rank(b["cols"][:3]) == 3 for b in blocks)
+
+
+def test_small_program_grouping_host_side():
+    """Small-state rotation programs (csrc/qsv_small.cu) are built on the
+    host: config 1 is 261 same-flip groups (36 singles of 2 strings, 225
+    doubles of 8) in 4 shared-memory chunks; mixed gates, diagonal strings,
+    fewer than 8 or more than 12 qubits leave no small program (tile passes)."""
+    import collections
+
+    from paper_2208_10978_b200.circuit import Circuit, Constant, Gate
+    from paper_2208_10978_b200.pauli import PauliString
+
+    cfg = W.config1(seed=0)
+    k, q, v = flatten_bound(cfg["circuit"])
+    sm = _lib.debug_plan(12, k, q, v)["small"]
+    assert sm["valid"] == 1 and len(sm["groups"]) == 261
+    assert collections.Counter(g[2] - g[1] for g in sm["groups"]) == {8: 225, 2: 36}
+    assert sm["chunks"] == [0, 80, 80, 160, 160, 240, 240, 261]
+    assert all(g[3] <= 3 for g in sm["groups"])  # <= 8 sign-pattern configs per group
+    rng = np.random.default_rng(2)
+    strings = W.ucc_rotation_strings(10, 5)[:60]
+    base = W.rotations_circuit(10, strings, rng.uniform(-1, 1, len(strings)))
+
+    def small_valid(circ, n):
+        kk, qq, vv = flatten_bound(circ)
+        return _lib.debug_plan(n, kk, qq, vv)["small"]["valid"]
+
+    assert small_valid(base, 10) == 1
+    mixed = Circuit(10, base.gates + (Gate("U3", (0,), (Constant(0.3), Constant(0.2), Constant(0.1))),), 0)
+    assert small_valid(mixed, 10) == 0
+    diag = W.rotations_circuit(10, [PauliString(((1, "Z"), (4, "Z")))] + strings,
+                               rng.uniform(-1, 1, len(strings) + 1))
+    assert small_valid(diag, 10) == 0
+    for n in (6, 13):
+        s_n = W.ucc_rotation_strings(n, n // 2)[:40]
+        assert small_valid(W.rotations_circuit(n, s_n, rng.uniform(-1, 1, len(s_n))), n) == 0
+    # one group of more than 2048 rotations does not fit a chunk's angle table
+    one = PauliString(((0, "X"), (1, "Y"), (2, "Z")))
+    assert small_valid(W.rotations_circuit(9, [one] * 2049, rng.uniform(-1, 1, 2049)), 9) == 0
+    assert small_valid(W.rotations_circuit(9, [one] * 2048, rng.uniform(-1, 1, 2048)), 9) == 1

@@ -148,3 +148,17 @@ def test_ineligible_programs_use_passes():
     out = sv.evolve(sv.init_state("0" * n), circ).amplitudes
     assert _lib.small_launches() == before
     assert np.abs(out - O.evolve(O.init_state("0" * n), circ.gates)).max() <= AMP_TOL
+
+
+def test_full_chunk_single_group(monkeypatch):
+    """One same-flip group of exactly 2048 rotations: a whole chunk's angle
+    table (the largest a small program takes)."""
+    n = 9
+    rng = np.random.default_rng(13)
+    one = PauliString(((0, "X"), (1, "Y"), (2, "Z"), (7, "Y")))
+    circ = W.rotations_circuit(n, [one] * 2048, rng.uniform(-0.01, 0.01, 2048))
+    out, out_passes, ran = run_both(circ, sv.init_state("101000000"), monkeypatch)
+    assert ran == 1
+    ref = O.evolve(O.init_state("101000000"), circ.gates)
+    assert np.abs(out - ref).max() <= AMP_TOL
+    assert np.abs(out_passes - ref).max() <= AMP_TOL
