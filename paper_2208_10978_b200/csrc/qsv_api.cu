@@ -920,9 +920,8 @@ static int run_small(qsv_state *s, const ProgramTemplate &t, const double *value
     char *d = nullptr;
     size_t scratch = 0;
     if (int rc = upload_blob(*c, s->stream, b, 0, &d, &scratch)) return rc;
-    QSV_CUDA(launch_small(s->amps, s->n, basis, (const SmallGroup *)(d + o_g), (const int32_t *)(d + o_m),
-                          (const double *)(d + o_t), (const int32_t *)(d + o_c), (int)(sp.chunks.size() / 2),
-                          s->stream));
+    QSV_CUDA(launch_small(s->amps, s->n, basis, sp, (const SmallGroup *)(d + o_g), (const int32_t *)(d + o_m),
+                          (const double *)(d + o_t), (const int32_t *)(d + o_c), s->stream));
     ++g_small_launches;
     return QSV_OK;
 }
@@ -1682,11 +1681,21 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     materialize_params(t, values, params.data());
     std::string j = "{\"n\":" + std::to_string(n) + ",\"block_bits\":" + std::to_string(kBlockBits);
     // the small-state rotation program (qsv_small.cu), when the plan has one
-    j += ",\"small\":{\"valid\":" + std::to_string(t.small.valid ? 1 : 0) + ",\"groups\":[";
+    j += ",\"small\":{\"valid\":" + std::to_string(t.small.valid ? 1 : 0) + ",\"ncls\":" +
+         std::to_string(t.small.ncls) + ",\"share\":" + std::to_string(t.small.share) + ",\"w\":[" +
+         std::to_string(t.small.w[0]) + "," + std::to_string(t.small.w[1]) + "," + std::to_string(t.small.w[2]) +
+         "],\"groups\":[";
+    // [xm, r0, r1, dimb, h, pm0..3, lu0, lu1, crow0..2, cpiv0..2, comb0..2, zpos0..4]
     for (size_t g = 0; g < t.small.groups.size(); ++g) {
         const SmallGroup &G = t.small.groups[g];
-        j += (g ? ",[" : "[") + std::to_string(G.xm) + "," + std::to_string(G.r0) + "," + std::to_string(G.r1) +
-             "," + std::to_string(G.dimb) + "]";
+        std::vector<int64_t> f = {G.xm, G.r0, G.r1, G.dimb, G.h, G.pm[0], G.pm[1], G.pm[2], G.pm[3], G.lu[0], G.lu[1]};
+        for (int i = 0; i < 3; ++i) f.push_back(G.crow[i]);
+        for (int i = 0; i < 3; ++i) f.push_back(G.cpiv[i]);
+        for (int i = 0; i < 3; ++i) f.push_back(G.comb[i]);
+        for (int i = 0; i < 5; ++i) f.push_back(G.zpos[i]);
+        j += g ? ",[" : "[";
+        for (size_t i = 0; i < f.size(); ++i) j += (i ? "," : "") + std::to_string(f[i]);
+        j += "]";
     }
     j += "],\"chunks\":[";
     for (size_t i = 0; i < t.small.chunks.size(); ++i) j += (i ? "," : "") + std::to_string(t.small.chunks[i]);

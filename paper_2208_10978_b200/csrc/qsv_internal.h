@@ -237,10 +237,11 @@ bool jit_sweep_launch(int device, const std::string &src, const double2 *psi, co
                       cudaStream_t st);
 cudaError_t launch_dense(double2 *psi, int n, int k, const int *qubits, const double2 *d_m, int sms,
                          cudaStream_t st);
-struct SmallGroup;  // qsv_planner.h
+struct SmallGroup;    // qsv_planner.h
+struct SmallProgram;  // qsv_planner.h
 // Small-state rotation program: one CTA, state in shared memory (qsv_small.cu).
-cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallGroup *groups, const int32_t *meta,
-                         const double *theta, const int32_t *chunks, int nchunks, cudaStream_t st);
+cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram &sp, const SmallGroup *groups,
+                         const int32_t *meta, const double *theta, const int32_t *chunks, cudaStream_t st);
 cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,
                          double bre, double bim, cudaStream_t st);
 

@@ -93,31 +93,39 @@ struct ClusterFill {
 
 // Small-state rotation program (qsv_small.cu): a state of <= kSmallMaxQubits
 // qubits made only of Pauli rotations runs as ONE CTA that keeps the whole
-// state in shared memory and walks the same-flip rotation groups with 1024
-// threads (a pair per thread per group), instead of tile passes whose
+// state in shared memory and walks the same-flip rotation groups (several
+// pairs per thread per group), instead of tile passes whose
 // straight-line code would stream through one SM's instruction cache.
 constexpr int kSmallMaxQubits = 12;
 constexpr int kSmallMinQubits = 8;
-constexpr int kSmallShare = 3;  // null-space vectors kept per group (the kernel uses 2 or 3)
-struct SmallGroup {    // 64 B
+struct SmallGroup {    // 100 B
     uint32_t xm;       // flip mask (X and Y positions) shared by the group
     // phase masks over the PAIR index p (lo = p with a 0 inserted at bit h):
     // the basis of the rotations' phase-mask differences b0..b2 (0: unused)
     // and the first rotation's phase mask z0, each with bit h removed --
     // parity(lo & m) = parity(p & pm), so a pair's config is linear in p
     uint32_t pm[4];
-    // kSmallShare independent pair-index vectors u with parity(u & pm[j]) = 0
-    // for all j, mapped to amplitude space (lu = u with a 0 inserted at h):
-    // the pairs p0 ^ span(u) share p0's config, so one thread applies them
-    // with one matrix load; piv = their pivot bits (ascending), where p0 has 0s
-    uint32_t lu[3];
-    int32_t piv[3];
+    // SmallProgram::share pair-index vectors u with parity(u & pm[j]) = 0 and
+    // parity(u & crow[k]) = 0, mapped to amplitude space (lu = u with a 0
+    // inserted at h): the pairs p0 ^ span(u) share p0's config and class, so
+    // one thread applies them with one matrix load
+    uint32_t lu[2];
+    // invariant classes (SmallProgram::ncls functionals w_k): the class rows
+    // over p (reduced: row k alone carries its pivot cpiv[k]), and which of
+    // the program's functionals each row combines (for its class value)
+    uint32_t crow[3];
+    int32_t cpiv[3];
+    uint32_t comb[3];
+    int32_t zpos[5];   // where p0 gets its zeros: the u pivots and class pivots, ascending
     int32_t h;         // pivot of xm: its highest bit (bit h of lo = 0)
     int32_t r0, r1;    // rotations [r0, r1) in application order
     int32_t dimb;      // number of basis differences (configs = 2^dimb, x 2 for the sign)
 };
 struct SmallProgram {
     bool valid = false;
+    int share = 2;     // log2 pairs per thread sharing a matrix load (1 or 2)
+    int ncls = 0;      // invariant GF(2) functionals used: 2^ncls independent classes
+    uint32_t w[3] = {0, 0, 0};  // the functionals (amplitude space): parity(i & w_k) is conserved
     std::vector<SmallGroup> groups;
     std::vector<int32_t> meta;    // per rotation: ny mod 4 | (ny odd) << 2 | coordinates << 3
     std::vector<int32_t> src;     // per rotation: its angle is values[3 * src]

@@ -26,13 +26,23 @@
 // chunk of groups are built by the CTA itself at the start of the chunk from
 // the raw angles (sincos on device).
 //
-// Bound: shared-memory bandwidth.  Per group every amplitude is read and
-// written once (2^n x 32 B) plus one 64-B matrix per thread: at n = 12,
-// 160 KiB per group at 128 B/clk ~ 1,300 cycles, ~170 us for config 1's 261
-// groups on one SM.
+// Invariant classes: a GF(2) functional w with parity(w & xm) = 0 for every
+// flip of the program is conserved by every rotation, so the amplitudes split
+// into classes that never mix.  A particle-number-conserving ansatz (UCC
+// singles and doubles: even-weight flips) conserves the parity of the index;
+// an evolve from a basis state (every energy evaluation) therefore only ever
+// touches that state's class -- half of the pairs -- and the other half stays
+// exactly zero.  The kernel enumerates the pairs of the reachable classes only.
+//
+// Bound: shared-memory bandwidth and latency on one SM.  Per group each
+// reachable amplitude is read and written once plus one 64-B matrix per
+// thread: config 1 (one class of 2,048 amplitudes, 256 threads x 4 pairs)
+// 160 us for 261 groups (262 us without the class restriction, 280 us as tile
+// passes).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "qsv_internal.h"
@@ -44,6 +54,8 @@ namespace qsv {
 constexpr int kSmallChunkRots = 2048;  // angles: 32 KiB of (cos, sin)
 constexpr int kSmallChunkGroups = 80;  // matrices: 80 x 16 configs x 80 B = 100 KiB
 constexpr int kRow = 5;                // double2 per matrix row (4 used; 80 B spreads rows over banks)
+size_t small_smem_bytes(int n);
+static_assert(sizeof(SmallGroup) % 4 == 0, "group records are copied as words");
 
 static inline uint32_t parity32(uint32_t v) { return (uint32_t)__builtin_popcount(v) & 1u; }
 
@@ -90,14 +102,56 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
         const uint32_t lowm = (1u << g.h) - 1u;
         const uint32_t ms[4] = {b[0], b[1], b[2], z0};
         for (int j = 0; j < 4; ++j) g.pm[j] = (ms[j] & lowm) | ((ms[j] >> 1) & ~lowm);
-        // three null-space vectors, reduced so each owns its pivot (its
-        // highest bit, as high as possible: the thread-to-pair map keeps the
-        // low bits consecutive across a warp)
-        uint32_t u[3] = {0, 0, 0};
+        sp.groups.push_back(g);
+        k = e;
+    }
+    // Invariant classes: every functional w with parity(w & xm) = 0 for all
+    // flips is conserved by every rotation (a pair lo, lo ^ xm has one value
+    // of it), so the 2^n amplitudes split into independent classes.  A
+    // particle-number-conserving ansatz (even-weight flips: UCC singles and
+    // doubles) conserves the total parity; an evolve from a basis state then
+    // only ever touches that state's class -- half the pairs.
+    std::vector<uint32_t> flips;
+    for (const SmallGroup &g : sp.groups)
+        if (std::find(flips.begin(), flips.end(), g.xm) == flips.end()) flips.push_back(g.xm);
+    uint32_t W[3] = {0, 0, 0};
+    int nw = 0;
+    for (uint32_t w = (1u << n) - 1u; w > 0 && nw < 3; --w) {
+        bool inv = true;
+        for (uint32_t x : flips)
+            if (parity32(w & x)) { inv = false; break; }
+        if (!inv) continue;
+        uint32_t r = w;
+        for (int i = 0; i < nw; ++i)
+            if ((r >> (31 - __builtin_clz(W[i]))) & 1u) r ^= W[i];
+        if (!r) continue;
+        const int pv = 31 - __builtin_clz(r);
+        for (int i = 0; i < nw; ++i)
+            if ((W[i] >> pv) & 1u) W[i] ^= r;
+        W[nw++] = r;
+    }
+    // 4 pairs per thread share a matrix load; classes used: keep >= 32
+    // threads busy per class at this n
+    int ncls = nw;
+    const int share = 2;
+    while (ncls > 0 && (n - 1) - ncls - share < 5) --ncls;
+    if ((n - 1) - ncls - share < 5) return false;
+    sp.ncls = ncls;
+    sp.share = share;
+    for (int i = 0; i < ncls; ++i) sp.w[i] = W[i];
+    for (SmallGroup &g : sp.groups) {
+        const uint32_t lowm = (1u << g.h) - 1u;
+        uint32_t wp[3] = {0, 0, 0};
+        for (int i = 0; i < ncls; ++i) wp[i] = (W[i] & lowm) | ((W[i] >> 1) & ~lowm);
+        // share null-space vectors of the four parity masks and the class
+        // rows, reduced so each owns its pivot (its highest bit, as high as
+        // possible: the thread-to-pair map keeps the low bits consecutive)
+        uint32_t u[2] = {0, 0};
         int nu = 0;
-        for (uint32_t v = pmask; v > 0 && nu < kSmallShare; --v) {
+        for (uint32_t v = pmask; v > 0 && nu < share; --v) {
             bool in_null = true;
             for (int j = 0; j < 4; ++j) in_null &= parity32(v & g.pm[j]) == 0;
+            for (int j = 0; j < ncls; ++j) in_null &= parity32(v & wp[j]) == 0;
             if (!in_null) continue;
             uint32_t r = v;
             for (int i = 0; i < nu; ++i)
@@ -108,20 +162,30 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
                 if ((u[i] >> pv) & 1u) u[i] ^= r;  // earlier vectors must not carry the new pivot
             u[nu++] = r;
         }
-        if (nu < kSmallShare) return false;
-        // pivots ascending for the zero insertion (a kernel sharing 2^s pairs
-        // uses the s highest: lu[3 - s .. 2])
-        int order[3] = {0, 1, 2};
-        for (int i = 0; i < nu; ++i)
-            for (int j = i + 1; j < nu; ++j)
-                if (__builtin_clz(u[order[j]]) > __builtin_clz(u[order[i]])) std::swap(order[i], order[j]);
+        if (nu < share) return false;
+        uint32_t upiv = 0;
         for (int i = 0; i < nu; ++i) {
-            const uint32_t ui = u[order[i]];
-            g.piv[i] = 31 - __builtin_clz(ui);
-            g.lu[i] = (ui & lowm) | ((ui & ~lowm) << 1);
+            upiv |= 1u << (31 - __builtin_clz(u[i]));
+            g.lu[i] = (u[i] & lowm) | ((u[i] & ~lowm) << 1);
         }
-        sp.groups.push_back(g);
-        k = e;
+        // class rows in reduced echelon form over pivots that are not u pivots
+        for (int i = 0; i < ncls; ++i) {
+            uint32_t r = wp[i], cb = 1u << i;
+            for (int j = 0; j < i; ++j)
+                if ((r >> g.cpiv[j]) & 1u) { r ^= g.crow[j]; cb ^= g.comb[j]; }
+            const uint32_t avail = r & ~upiv;
+            if (!avail) return false;
+            const int pv = 31 - __builtin_clz(avail);
+            for (int j = 0; j < i; ++j)
+                if ((g.crow[j] >> pv) & 1u) { g.crow[j] ^= r; g.comb[j] ^= cb; }
+            g.crow[i] = r;
+            g.comb[i] = cb;
+            g.cpiv[i] = pv;
+        }
+        int nz = 0;
+        for (int i = 0; i < nu; ++i) g.zpos[nz++] = 31 - __builtin_clz(u[i]);
+        for (int i = 0; i < ncls; ++i) g.zpos[nz++] = g.cpiv[i];
+        std::sort(g.zpos, g.zpos + nz);
     }
     // chunks of groups whose angles and matrices fit the shared tables
     int g0 = 0;
@@ -169,34 +233,47 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c)
 }
 
 // S = log2 pairs per thread sharing one matrix load; 2^(11 - S) threads
-template <int S>
-__global__ void __launch_bounds__((1 << (kSmallMaxQubits - 1)) >> S, 1)
+constexpr int kMaxThreads = 512;
+
+// One CTA of (pairs in a class) / 2^S threads; per group every thread
+// applies the group's matrix for its config to the 2^S pairs p0 ^ span(lu)
+// of each class this evolve can reach.  p0 comes from the thread index with
+// zeros inserted at the u and class pivots, the class pivots then set so that
+// p0 lies in the class.  The chunk's group records sit in shared memory.
+template <int S, int NC>
+__global__ void __launch_bounds__(kMaxThreads, 1)
 small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGroup *__restrict__ groups,
                  const int32_t *__restrict__ meta, const double *__restrict__ theta,
-                 const int32_t *__restrict__ chunks, int nchunks)
+                 const int32_t *__restrict__ chunks, int nchunks, uint32_t cls0, uint32_t cls1)
 {
     constexpr int kShare = 1 << S;
-    constexpr int kThreads = (1 << (kSmallMaxQubits - 1)) >> S;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t dim = 1u << n;
+    const uint32_t nthr = blockDim.x;
     double2 *st = reinterpret_cast<double2 *>(smem_raw);  // state
     double2 *cs = st + dim;                               // (cos, sin) of the chunk's angles
     double2 *mt = cs + kSmallChunkRots;                   // [group][16 configs][kRow]
+    SmallGroup *gs = reinterpret_cast<SmallGroup *>(mt + 16 * kRow * kSmallChunkGroups);  // the chunk's groups
     const uint32_t tid = threadIdx.x;
-    for (uint32_t i = tid; i < dim; i += kThreads)
+    for (uint32_t i = tid; i < dim; i += nthr)
         st[sslot(i)] = basis != ~0ull ? make_double2(i == basis ? 1.0 : 0.0, 0.0) : psi[i];
-    const bool active = tid < ((dim >> 1) >> S);
     for (int ch = 0; ch < nchunks; ++ch) {
         const int g0 = chunks[2 * ch], g1 = chunks[2 * ch + 1];
         const int rb = groups[g0].r0, re = groups[g1 - 1].r1;
-        for (int r = rb + (int)tid; r < re; r += kThreads) {
+        for (int r = rb + (int)tid; r < re; r += nthr) {
             double s, c;
             sincos(0.5 * theta[r], &s, &c);
             cs[r - rb] = make_double2(c, s);
         }
-        __syncthreads();  // angles ready; the previous chunk's last group is done with mt
-        for (int t = (int)tid; t < (g1 - g0) * 8; t += kThreads) {
-            const SmallGroup &G = groups[g0 + t / 8];
+        {
+            const int words = (g1 - g0) * (int)(sizeof(SmallGroup) / 4);
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(groups + g0);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(gs);
+            for (int i = (int)tid; i < words; i += nthr) dst[i] = src[i];
+        }
+        __syncthreads();  // angles and groups ready; the previous chunk is done with mt
+        for (int t = (int)tid; t < (g1 - g0) * 8; t += nthr) {
+            const SmallGroup &G = gs[t / 8];
             const uint32_t cfg = (uint32_t)(t & 7);
             if (cfg >= (1u << G.dimb)) continue;
             double2 m00 = make_double2(1.0, 0.0), m01 = make_double2(0.0, 0.0);
@@ -222,20 +299,24 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
             row[2] = make_double2(-m10.x, -m10.y); row[3] = m11;
         }
         __syncthreads();
-        for (int gi = g0; gi < g1; ++gi) {
-            if (active) {
-                const SmallGroup &G = groups[gi];
-                uint32_t p0 = tid;
+        for (int gi = 0; gi < g1 - g0; ++gi) {
+            const SmallGroup &G = gs[gi];
+            uint32_t q0 = tid;
 #pragma unroll
-                for (int i = 3 - S; i < 3; ++i) {  // zeros at the (ascending) pivots
-                    const uint32_t lm = (1u << G.piv[i]) - 1u;
-                    p0 = ((p0 & ~lm) << 1) | (p0 & lm);
-                }
+            for (int i = 0; i < S + NC; ++i) {  // zeros at the (ascending) u and class pivots
+                const uint32_t lm = (1u << G.zpos[i]) - 1u;
+                q0 = ((q0 & ~lm) << 1) | (q0 & lm);
+            }
+            const uint32_t lowm = (1u << G.h) - 1u, xm = G.xm;
+            for (uint32_t cl = cls0; cl < cls1; ++cl) {  // the classes this evolve can reach
+                uint32_t p0 = q0;
+#pragma unroll
+                for (int k = 0; k < NC; ++k)
+                    if (par(p0 & G.crow[k]) != par(G.comb[k] & cl)) p0 |= 1u << G.cpiv[k];
                 const uint32_t cfg = par(p0 & G.pm[0]) | (par(p0 & G.pm[1]) << 1) | (par(p0 & G.pm[2]) << 2) |
                                      (par(p0 & G.pm[3]) << 3);
-                const double2 *M = mt + ((gi - g0) * 16 + (int)cfg) * kRow;
+                const double2 *M = mt + (gi * 16 + (int)cfg) * kRow;
                 const double2 m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
-                const uint32_t lowm = (1u << G.h) - 1u;
                 const uint32_t lo0 = ((p0 & ~lowm) << 1) | (p0 & lowm);
                 uint32_t lo[kShare];
 #pragma unroll
@@ -243,58 +324,70 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
                     uint32_t v = lo0;
 #pragma unroll
                     for (int i = 0; i < S; ++i)
-                        if ((a >> i) & 1) v ^= G.lu[3 - S + i];
+                        if ((a >> i) & 1) v ^= G.lu[i];
                     lo[a] = v;
                 }
                 double2 x[kShare], y[kShare];
 #pragma unroll
                 for (int a = 0; a < kShare; ++a) {
                     x[a] = st[sslot(lo[a])];
-                    y[a] = st[sslot(lo[a] ^ G.xm)];
+                    y[a] = st[sslot(lo[a] ^ xm)];
                 }
 #pragma unroll
                 for (int a = 0; a < kShare; ++a) {
                     st[sslot(lo[a])] = cfma(m01, y[a], cmul(m00, x[a]));
-                    st[sslot(lo[a] ^ G.xm)] = cfma(m11, y[a], cmul(m10, x[a]));
+                    st[sslot(lo[a] ^ xm)] = cfma(m11, y[a], cmul(m10, x[a]));
                 }
             }
             __syncthreads();
         }
     }
-    for (uint32_t i = tid; i < dim; i += kThreads) psi[i] = st[sslot(i)];
+    for (uint32_t i = tid; i < dim; i += nthr) psi[i] = st[sslot(i)];
+}
+
+template <int NC>
+cudaError_t launch_nc(double2 *psi, int n, uint64_t basis, const SmallGroup *groups, const int32_t *meta,
+                      const double *theta, const int32_t *chunks, int nchunks, uint32_t c0, uint32_t c1,
+                      cudaStream_t st, size_t smem)
+{
+    static PerDeviceOnce once;
+    if (cudaError_t e = once.run([&] {
+            return cudaFuncSetAttribute(small_rot_kernel<2, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)small_smem_bytes(kSmallMaxQubits));
+        }))
+        return e;
+    const int threads = std::max(32, std::min(kMaxThreads, ((1 << n) >> 1) >> (2 + NC)));
+    small_rot_kernel<2, NC><<<1, threads, smem, st>>>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1);
+    return cudaGetLastError();
 }
 
 }  // namespace
 
 size_t small_smem_bytes(int n)
 {
-    return ((size_t)16 << n) + 16 * (size_t)kSmallChunkRots + 16 * (size_t)kRow * 16 * kSmallChunkGroups;
+    return ((size_t)16 << n) + 16 * (size_t)kSmallChunkRots + 16 * (size_t)kRow * 16 * kSmallChunkGroups +
+           sizeof(SmallGroup) * kSmallChunkGroups;
 }
 
-cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallGroup *groups,
-                         const int32_t *meta, const double *theta, const int32_t *chunks, int nchunks,
-                         cudaStream_t st)
+cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram &sp,
+                         const SmallGroup *groups, const int32_t *meta, const double *theta,
+                         const int32_t *chunks, cudaStream_t st)
 {
-    static PerDeviceOnce once;
-    const int smem = (int)small_smem_bytes(kSmallMaxQubits);
-    if (cudaError_t e = once.run([&] {
-            cudaError_t a = cudaFuncSetAttribute(small_rot_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (a != cudaSuccess) return a;
-            return cudaFuncSetAttribute(small_rot_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        }))
-        return e;
-    static const int share = [] {  // 4 pairs per thread (512 threads) or 8 (256): A/B knob
-        const char *e = getenv("QSV_SMALL_SHARE");
-        return e && e[0] == '3' ? 3 : 2;
-    }();
-    constexpr int P = 1 << (kSmallMaxQubits - 1);
-    if (share == 3)
-        small_rot_kernel<3><<<1, P >> 3, small_smem_bytes(n), st>>>(psi, n, basis, groups, meta, theta, chunks,
-                                                                    nchunks);
-    else
-        small_rot_kernel<2><<<1, P >> 2, small_smem_bytes(n), st>>>(psi, n, basis, groups, meta, theta, chunks,
-                                                                    nchunks);
-    return cudaGetLastError();
+    // from a basis state only its own class is ever non-zero
+    uint32_t c0 = 0, c1 = 1u << sp.ncls;
+    if (basis != ~0ull) {
+        c0 = 0;
+        for (int k = 0; k < sp.ncls; ++k) c0 |= (uint32_t)__builtin_parityll(basis & sp.w[k]) << k;
+        c1 = c0 + 1;
+    }
+    const int nchunks = (int)(sp.chunks.size() / 2);
+    const size_t smem = small_smem_bytes(n);
+    switch (sp.ncls) {
+        case 0: return launch_nc<0>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
+        case 1: return launch_nc<1>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
+        case 2: return launch_nc<2>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
+        default: return launch_nc<3>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
+    }
 }
 
 }  // namespace qsv

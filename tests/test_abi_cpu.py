@@ -349,3 +349,97 @@ def test_small_program_grouping_host_side():
     one = PauliString(((0, "X"), (1, "Y"), (2, "Z")))
     assert small_valid(W.rotations_circuit(9, [one] * 2049, rng.uniform(-1, 1, 2049)), 9) == 0
     assert small_valid(W.rotations_circuit(9, [one] * 2048, rng.uniform(-1, 1, 2048)), 9) == 1
+
+
+def _popc(v):
+    return bin(int(v)).count("1") & 1
+
+
+def _emulate_small(n, circ, basis):
+    """CPU mirror of small_rot_kernel's pair enumeration: the host tables
+    (debug_plan's "small") decide which pairs each thread covers; the
+    matrices are rebuilt here from the rotation list.  Returns the evolved
+    state and checks that every group covers each pair of the basis state's
+    class exactly once, with one config per thread."""
+    k, q, v = flatten_bound(circ)
+    plan = _lib.debug_plan(n, k, q, v)
+    sm = plan["small"]
+    assert sm["valid"] == 1
+    spans, masks = _lib.match_rotations(n, k, q)
+    R = [(int(m[0]), int(m[1]), int(m[2]), float(v[3 * int(s[2])])) for s, m in zip(spans, masks)]
+    ncls, S, W = sm["ncls"], sm["share"], sm["w"]
+    cls = sum(_popc(basis & W[j]) << j for j in range(ncls))
+    psi = np.zeros(1 << n, dtype=complex)
+    psi[basis] = 1.0
+    for g in sm["groups"]:
+        xm, r0, r1, dimb, h = g[0:5]
+        pm, lu = g[5:9], g[9:11]
+        crow, cpiv, comb, zpos = g[11:14], g[14:17], g[17:20], g[20:25]
+        rots = R[r0:r1]
+        z0 = rots[0][1] | rots[0][2]
+        # matrices per amplitude-space sign pattern of the group's strings
+        mats = {}
+        pairs_seen = set()
+        lowm = (1 << h) - 1
+        nthreads = (1 << (n - 1)) >> (S + ncls)
+        for t in range(nthreads):
+            q0 = t
+            for i in range(S + ncls):
+                lm = (1 << zpos[i]) - 1
+                q0 = ((q0 & ~lm) << 1) | (q0 & lm)
+            p0 = q0
+            for j in range(ncls):
+                if _popc(p0 & crow[j]) != _popc(comb[j] & cls):
+                    p0 |= 1 << cpiv[j]
+            cfg0 = tuple(_popc(p0 & m) for m in pm)
+            lo0 = ((p0 & ~lowm) << 1) | (p0 & lowm)
+            for a in range(1 << S):
+                lo = lo0
+                for i in range(S):
+                    if (a >> i) & 1:
+                        lo ^= lu[i]
+                p = (lo & lowm) | ((lo >> 1) & ~lowm)
+                assert tuple(_popc(p & m) for m in pm) == cfg0  # shared config
+                assert (lo >> h) & 1 == 0 and lo not in pairs_seen
+                pairs_seen.add(lo)
+                hi = lo ^ xm
+                M = np.eye(2, dtype=complex)
+                for (x, y, z, th) in rots:
+                    ny = bin(y).count("1")
+                    s_lo = -1 if _popc(lo & (y | z)) else 1
+                    c, s = np.cos(th / 2), np.sin(th / 2)
+                    off = -1j * s * (1j) ** ny * s_lo
+                    M = np.array([[c, off * (-1) ** ny], [off, c]]) @ M
+                psi[lo], psi[hi] = M[0, 0] * psi[lo] + M[0, 1] * psi[hi], M[1, 0] * psi[lo] + M[1, 1] * psi[hi]
+        want = {lo for lo in range(1 << n) if not (lo >> h) & 1
+                and sum(_popc(lo & W[j]) << j for j in range(ncls)) == cls}
+        assert pairs_seen == want
+    return psi, sm
+
+
+def test_small_program_enumeration_emulated():
+    """Invariant classes: a number-conserving UCC ansatz has only even-weight
+    flips, so the total parity of the index is conserved and an evolve from a
+    basis state touches half of the pairs.  The CPU mirror of the kernel's
+    enumeration covers exactly that class and matches the oracle."""
+    from oracle import oracle as O
+
+    rng0 = np.random.default_rng(5)
+    ucc = W.ucc_rotation_strings(10, 5)
+    strings = ucc[:40] + ucc[-80:]  # singles + the last ten doubles
+    circ = W.rotations_circuit(10, strings, rng0.uniform(-0.5, 0.5, len(strings)))
+    ref_bits = W.hf_bitstring(5, 10)
+    b = int(ref_bits[::-1], 2)
+    psi, sm = _emulate_small(10, circ, b)
+    assert sm["ncls"] == 1 and sm["w"][0] == 1023 and sm["share"] == 2
+    ref = O.evolve(O.init_state(ref_bits), circ.gates)
+    assert np.abs(psi - ref).max() <= 1e-12
+    # a program with odd-weight flips has no conserved parity
+    from paper_2208_10978_b200.pauli import PauliString
+
+    rng = np.random.default_rng(4)
+    strings = [PauliString(((0, "X"),)), PauliString(((1, "Y"), (3, "X"), (5, "Z")))] + W.ucc_rotation_strings(8, 4)[:20]
+    c2 = W.rotations_circuit(8, strings, rng.uniform(-1, 1, len(strings)))
+    psi2, sm2 = _emulate_small(8, c2, 0b1011)
+    assert sm2["ncls"] == 0
+    assert np.abs(psi2 - O.evolve(O.init_state("11010000"), c2.gates)).max() <= 1e-12
