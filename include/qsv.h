@@ -257,6 +257,16 @@ int qsv_jit_info(int *available, int64_t *launches);
  * QSV_SMALL=0 runs these programs as tile passes. */
 int qsv_small_info(int64_t *launches);
 
+/* Parity-reduced states: an evolve from a basis state by a rotation program
+ * whose flips all have even weight (particle-number-conserving ansatze)
+ * never leaves the basis state's index-parity class, so the half of the
+ * state in that class is evolved as an (n-1)-qubit state (statevector.py's
+ * ParityReduced).  dst (n qubits) = the full state: dst[j] = half[j without
+ * bit n-1] when parity(j & (wlow | 2^(n-1))) = cls, else 0.  Replaces the
+ * full-size gate loop of statevector.py:65-74 for such programs; the reduced
+ * result is exactly the reference's. */
+int qsv_embed_parity(qsv_state *dst, const qsv_state *half, uint64_t wlow, int cls);
+
 /* Statistics of the last plan on the calling thread (see qsv_plan_stats). */
 int qsv_last_plan_stats(qsv_plan_stats *out);
 

@@ -53,7 +53,7 @@ EXPORTED = (
     "qsv_apply_pauli", "qsv_apply_gates", "qsv_apply_pauli_rotations", "qsv_expectation",
     "qsv_apply_operator", "qsv_vdot", "qsv_norm", "qsv_axpby", "qsv_plan_gates",
     "qsv_plan_expectation", "qsv_match_rotations", "qsv_debug_plan_json", "qsv_debug_sweep_source", "qsv_debug_pass_source", "qsv_sample_parity",
-    "qsv_jit_info", "qsv_small_info", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
+    "qsv_jit_info", "qsv_small_info", "qsv_embed_parity", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
     "qsv_release_program", "qsv_evolve_basis", "qsv_evolve_basis_prepared",
     "qsv_last_plan_stats", "qsv_dist_create", "qsv_dist_destroy", "qsv_dist_set_basis",
     "qsv_dist_apply_gates", "qsv_dist_expectation", "qsv_dist_download", "qsv_dist_info",
@@ -119,6 +119,7 @@ def _declare(L):
                                  ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_jit_info": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_small_info": ([ctypes.POINTER(i64)], ctypes.c_int),
+        "qsv_embed_parity": ([vp, vp, u64, ctypes.c_int], ctypes.c_int),
         "qsv_rotation_adjoint": ([vp, vp, i64, u64p, u64p, u64p, dp, dp], ctypes.c_int),
         "qsv_prepare_gates": ([ctypes.c_int, i64, i32p, i32p, ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_apply_prepared": ([vp, i64, dp, sp], ctypes.c_int),

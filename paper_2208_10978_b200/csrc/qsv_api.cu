@@ -797,6 +797,22 @@ int qsv_copy(qsv_state *dst, const qsv_state *src)
     return QSV_OK;
 }
 
+int qsv_embed_parity(qsv_state *dst, const qsv_state *half, uint64_t wlow, int cls)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(dst)) return rc;
+    if (int rc = check_state(half)) return rc;
+    if (dst->n != half->n + 1) return fail_code(QSV_ERR_INVALID, "half state must have one qubit less");
+    if (wlow >> half->n) return fail_code(QSV_ERR_INVALID, "functional has bits beyond the half state");
+    if (cls != 0 && cls != 1) return fail_code(QSV_ERR_INVALID, "class must be 0 or 1");
+    if (dst == half) return fail_code(QSV_ERR_INVALID, "in-place embedding");
+    QSV_CUDA(cudaSetDevice(dst->device));
+    if (int rc = settle(dst)) return rc;
+    QSV_CUDA(launch_embed_parity(dst->amps, half->amps, dst->n, wlow, (uint32_t)cls, num_sms(dst->device),
+                                 dst->stream));
+    return QSV_OK;
+}
+
 int qsv_set_basis(qsv_state *s, uint64_t index)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);

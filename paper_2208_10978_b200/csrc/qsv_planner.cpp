@@ -97,6 +97,7 @@ struct Item {
     int cluster = -1;         // dense-fused gate cluster (index into ProgramTemplate::cfills)
     int cost = 2;             // FP64 work (complex FMAs per amplitude) -- bounds a pass
     int par = 8;              // parameter doubles (specialised passes hold them in 64 KiB __constant__)
+    uint64_t last_z = 0;      // rot items: Z mask of the last rotation (a change starts another OP_GMAT)
 };
 
 // Parameter doubles of a gate (op_param_count of the op it becomes) and of a
@@ -384,12 +385,15 @@ void build_items_from_rots(const std::vector<Rot> &R, std::vector<Item> &items)
             g.rots.push_back((int)r);
             g.b_union |= b;
             g.supp |= a | b;
+            if (R[r].z != g.last_z) g.par += rot_par(a);  // a run of another sign mask: its own table
+            g.last_z = R[r].z;
             continue;
         }
         Item it;
         it.rot = true;
         it.cost = 0;
         it.par = rot_par(a);
+        it.last_z = R[r].z;
         it.rots.push_back((int)r);
         it.a_union = a;
         it.b_union = b;
@@ -1134,38 +1138,43 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
                     for (int r = op.r0; r < op.r1; ++r)
                         t.rots[r].q = (t.rots[r].q & 0xff) | (int32_t)(comp_b(t.rots[r].s_loc) << 8) |
                                       (int32_t)(comp_t(t.rots[r].s_loc) << 12);
-                if (op.type == OP_ROTG && op.r1 - op.r0 >= 2) {
-                    // fuse when every string shares the sign bits off the flip
-                    // (JW Z-chain): one 2x2 per pair instead of r1-r0 rotations
+                if (op.type == OP_ROTG) {
+                    // fuse each run of strings that share the sign bits off the
+                    // flip (the JW Z-chain of one excitation): one 2x2 per pair
+                    // per run instead of one per rotation -- and a form the
+                    // specialised passes have (a lone rotation is a run of one)
                     const uint32_t fl = expand_b(op.f);
-                    const uint32_t zc = t.rots[op.r0].s_loc & ~fl;
-                    const uint64_t zh = t.rots[op.r0].s_hi;
-                    bool ok = true;
-                    for (int r = op.r0 + 1; r < op.r1 && ok; ++r)
-                        ok = (t.rots[r].s_loc & ~fl) == zc && t.rots[r].s_hi == zh;
-                    if (ok) {
+                    int r = op.r0;
+                    while (r < op.r1) {
+                        const uint32_t zc = t.rots[r].s_loc & ~fl;
+                        const uint64_t zh = t.rots[r].s_hi;
+                        int e = r + 1;
+                        while (e < op.r1 && (t.rots[e].s_loc & ~fl) == zc && t.rots[e].s_hi == zh) ++e;
                         GmatFill gf;
-                        gf.r0 = op.r0;
-                        gf.r1 = op.r1;
+                        gf.r0 = r;
+                        gf.r1 = e;
                         gf.F = (int)op.f;
                         gf.H = 31 - __builtin_clz(op.f);
                         gf.w = __builtin_popcount(op.f);
-                        for (int r = op.r0; r < op.r1; ++r)
-                            gf.yF.push_back((uint8_t)comp_b(t.rots[r].s_loc & fl));
+                        for (int k = r; k < e; ++k) gf.yF.push_back((uint8_t)comp_b(t.rots[k].s_loc & fl));
                         gf.offset = (int)t.n_params;
                         t.n_params += (size_t)8 * (2u << (gf.w - 1));
                         t.gfills.push_back(gf);
                         // common masks live in a dedicated record
-                        RotRec cr = t.rots[op.r0];
+                        RotRec cr = t.rots[r];
                         cr.q = (int32_t)(comp_b(zc) << 8) | (int32_t)(comp_t(zc) << 12);
                         cr.s_loc = zc;
                         t.rots.push_back(cr);
-                        t.rot_src.push_back(t.rot_src[op.r0]);
-                        op.type = OP_GMAT;
-                        op.p = gf.offset;
-                        op.r0 = (int)t.rots.size() - 1;
-                        op.r1 = op.r0 + 1;
+                        t.rot_src.push_back(t.rot_src[r]);
+                        OpRec g = op;
+                        g.type = OP_GMAT;
+                        g.p = gf.offset;
+                        g.r0 = (int)t.rots.size() - 1;
+                        g.r1 = g.r0 + 1;
+                        out.push_back(g);
+                        r = e;
                     }
+                    continue;
                 }
                 out.push_back(op);
             }
@@ -1362,7 +1371,10 @@ void block_pass(ProgramTemplate &t, PassPlan &pp)
         t.blocks[b].op0 += pp.op_begin;
         t.blocks[b].op1 += pp.op_begin;
     }
-    std::copy(out.begin(), out.end(), t.ops.begin() + pp.op_begin);
+    // the pass's ops are the tail of t.ops; a split rotation group can make
+    // the block-encoded list longer than the source
+    t.ops.erase(t.ops.begin() + pp.op_begin, t.ops.begin() + pp.op_end);
+    t.ops.insert(t.ops.begin() + pp.op_begin, out.begin(), out.end());
     pp.op_end = pp.op_begin + (int)out.size();
     pp.map_permuted = tr != 0;
     for (int b = 0; b < 12; ++b) {
@@ -1559,11 +1571,14 @@ void plan_gates(int n, int64_t N, const int32_t *kinds, const int32_t *qubits, P
                 g.rots.push_back(r);
                 g.b_union |= b;
                 g.supp |= a | b;
+                if (rot.z != g.last_z) g.par += rot_par(a);  // a run of another sign mask: its own table
+                g.last_z = rot.z;
             } else {
                 Item it;
                 it.rot = true;
-                it.cost = 0;  // a same-flip group is one GMAT: bounded by the parameter budget
+                it.cost = 0;  // a same-flip group is one GMAT per sign-mask run: bounded by the parameter budget
                 it.par = rot_par(a);
+                it.last_z = rot.z;
                 it.rots.push_back(r);
                 it.a_union = a;
                 it.b_union = b;

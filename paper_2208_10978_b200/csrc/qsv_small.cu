@@ -363,6 +363,35 @@ cudaError_t launch_nc(double2 *psi, int n, uint64_t basis, const SmallGroup *gro
 
 }  // namespace
 
+namespace {
+
+// Parity-reduced states (statevector.ParityReduced): the full n-qubit state
+// from the (n-1)-qubit half that holds one invariant class.  dst[j] =
+// src[j without its top bit] when parity(j & w) = cls, else 0 (w = all
+// ones on the low bits + the top bit).  One coalesced write per amplitude.
+__global__ void __launch_bounds__(256) embed_parity_kernel(double2 *__restrict__ dst,
+                                                           const double2 *__restrict__ src, uint64_t dim,
+                                                           uint64_t wlow, int top, uint32_t cls)
+{
+    const uint64_t topbit = 1ull << top;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < dim;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t pj = (uint32_t)(__popcll(j & (wlow | topbit)) & 1);
+        dst[j] = pj == cls ? src[j & ~topbit] : make_double2(0.0, 0.0);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_embed_parity(double2 *dst, const double2 *src, int n_dst, uint64_t wlow, uint32_t cls,
+                                int sms, cudaStream_t st)
+{
+    const uint64_t dim = 1ull << n_dst;
+    const uint64_t blocks = std::min<uint64_t>((dim + 255) / 256, (uint64_t)sms * 8);
+    embed_parity_kernel<<<(unsigned)blocks, 256, 0, st>>>(dst, src, dim, wlow, n_dst - 1, cls);
+    return cudaGetLastError();
+}
+
 size_t small_smem_bytes(int n)
 {
     return ((size_t)16 << n) + 16 * (size_t)kSmallChunkRots + 16 * (size_t)kRow * 16 * kSmallChunkGroups +

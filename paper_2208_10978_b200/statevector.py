@@ -27,6 +27,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
+from . import symmetry as _symmetry
 from .circuit import flatten_bound
 from .errors import ResourceLimitError
 from .pauli import term_arrays
@@ -354,13 +355,76 @@ def apply_circuit_inplace(s: StateVector, c, basis: Optional[int] = None) -> Non
                                                _lib.dptr(values), ctypes.byref(_last_stats)))
 
 
+class ParityReduced(StateVector):
+    """The result of an evolve from a basis state by an even-flip rotation
+    program (symmetry.py): only the basis state's index-parity class is
+    non-zero, held as an (n-1)-qubit half.  expectation() runs on the half;
+    anything else materialises the full state on first use of `handle`
+    (qsv_embed_parity), after which it behaves as a plain StateVector."""
+
+    __slots__ = ("_half", "_cls")
+
+    @classmethod
+    def _wrap(cls, n: int, half: StateVector, parity: int) -> "ParityReduced":
+        s = cls.__new__(cls)
+        s.n_qubits = n
+        s.device = half.device
+        s._h = None
+        s._basis = None
+        s._half = half
+        s._cls = int(parity)
+        return s
+
+    @property
+    def reduced(self) -> bool:
+        return self._h is None
+
+    def _ensure(self) -> None:
+        if self._h is None:
+            h = _Handle(self.n_qubits, self.device, _alloc(self.n_qubits, self.device))
+            wlow = (1 << (self.n_qubits - 1)) - 1
+            _lib.check(_lib.lib().qsv_embed_parity(ctypes.c_void_p(h.value), self._half.handle, wlow, self._cls))
+            self._h = h
+            self._half = None
+
+    @property
+    def basis_index(self) -> Optional[int]:
+        return None
+
+    def norm(self) -> float:
+        return self._half.norm() if self._h is None else StateVector.norm(self)
+
+    def synchronize(self) -> None:
+        (self._half if self._h is None else super()).synchronize()
+
+
+_last_reduction = {"n_eff": None}
+
+
+def last_reduction() -> dict:
+    """{'n_eff': qubits actually evolved} of the last evolve (None: full size)."""
+    return dict(_last_reduction)
+
+
 def evolve(s: StateVector, c) -> StateVector:
     """Apply a bound circuit; returns a new state (statevector.py:65-74)."""
     if c.n_qubits != s.n_qubits:
         raise ValueError("circuit and state qubit counts differ")
     # boundness (statevector.py:69-70) is checked by the flattening itself
     # (RuntimeError on an unbound parameter), before any device work
-    _flat(c)
+    kinds, qubits, values = _flat(c)
+    _last_reduction["n_eff"] = None
+    if s.basis_index is not None and s.n_qubits > 12 and _symmetry.enabled():
+        red = _symmetry.reduction_for(s.n_qubits, kinds, qubits)
+        if red is not None:  # the basis state's parity class, as an (n-1)-qubit state
+            b = s.basis_index
+            parity = bin(b).count("1") & 1
+            half = StateVector._empty(s.n_qubits - 1, s.device)
+            _lib.check(_lib.lib().qsv_evolve_basis_prepared(
+                half.handle, b & ((1 << (s.n_qubits - 1)) - 1), red.program().program_id(),
+                _lib.dptr(red.half_values(values, parity)), ctypes.byref(_last_stats)))
+            _last_reduction["n_eff"] = s.n_qubits - 1
+            return ParityReduced._wrap(s.n_qubits, half, parity)
     out = StateVector._empty(s.n_qubits, s.device)
     if s.basis_index is not None:  # |index> is synthesised by the first pass
         apply_circuit_inplace(out, c, s.basis_index)
@@ -407,6 +471,18 @@ def expectation_terms(s: StateVector, h) -> tuple[float, float, np.ndarray]:
     x, y, z, cr, ci = _hamiltonian(h, s.n_qubits)
     re, im = ctypes.c_double(), ctypes.c_double()
     per = np.zeros(len(cr), dtype=np.float64)
+    if isinstance(s, ParityReduced) and s.reduced:
+        # even-flip terms on the half (sigma folded into the coefficients);
+        # odd-flip terms map the class onto the empty one: exactly 0
+        x2, y2, z2, cr2, ci2, keep, sign = _symmetry.half_terms(s.n_qubits, x, y, z, cr, ci, s._cls)
+        per2 = np.zeros(len(cr2), dtype=np.float64)
+        if len(cr2):
+            _lib.check(_lib.lib().qsv_expectation(s._half.handle, len(cr2), _lib.u64ptr(x2), _lib.u64ptr(y2),
+                                                  _lib.u64ptr(z2), _lib.dptr(cr2), _lib.dptr(ci2),
+                                                  ctypes.byref(re), ctypes.byref(im), _lib.dptr(per2),
+                                                  None))
+        per[keep] = per2 * sign
+        return re.value, im.value, per
     if len(cr):
         _lib.check(_lib.lib().qsv_expectation(s.handle, len(cr), _lib.u64ptr(x), _lib.u64ptr(y),
                                               _lib.u64ptr(z), _lib.dptr(cr), _lib.dptr(ci),

@@ -101,8 +101,10 @@ def test_hot_program_specialisation(n, ne, monkeypatch):
     run QSV_JIT_HOT_USES (3) times; every run -- interpreted, then
     specialised, with new angles each time -- matches the oracle.  (Tile
     passes forced: at 12 q a rotation-only program otherwise runs as a
-    small-state program, tests/test_gpu_small.py.)"""
+    small-state program, tests/test_gpu_small.py, and from 13 q as a
+    parity-reduced half, tests/test_gpu_symmetry.py.)"""
     monkeypatch.setenv("QSV_SMALL", "0")
+    monkeypatch.setenv("QSV_PARITY", "0")  # full-size passes (the half: test_gpu_symmetry.py)
     from paper_2208_10978_b200 import _lib
     from paper_2208_10978_b200.circuit import bind
 

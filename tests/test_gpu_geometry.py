@@ -50,6 +50,7 @@ def test_ucc_forced_contig_vs_oracle(jit14, monkeypatch, contig):
     specialised passes, vs the oracle; then the energy of a config-3-style
     Hamiltonian on the result."""
     monkeypatch.setenv("QSV_MIN_CONTIG", contig)
+    monkeypatch.setenv("QSV_PARITY", "0")  # full-size tiles (the half: test_gpu_symmetry.py)
     n = 18
     cfg = W.config4(seed=40 + int(contig), n_qubits=n, n_electrons=8, n_doubles=40, n_terms=300)
     assert len(cfg["strings"]) >= 300
@@ -88,6 +89,7 @@ def test_ucc_default_knobs_22q_picks_two_contiguous_vs_oracle(monkeypatch):
     the oracle."""
     for k in ("QSV_MIN_CONTIG", "QSV_JIT_MIN_QUBITS", "QSV_JIT"):
         monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv("QSV_PARITY", "0")  # the full 22 q program (the half: test_gpu_symmetry.py)
     n = 22
     cfg = W.config4(seed=22, n_qubits=n, n_electrons=10, n_doubles=30, n_terms=200)
     assert len(cfg["strings"]) >= 300

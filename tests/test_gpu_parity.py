@@ -293,8 +293,10 @@ def test_jit_random_mixed_vs_oracle(jit_from_14, n, g):
 
 
 @pytest.mark.parametrize("n,ne", [(14, 6), (16, 8)])
-def test_jit_ucc_groups_vs_oracle(jit_from_14, n, ne):
+def test_jit_ucc_groups_vs_oracle(jit_from_14, n, ne, monkeypatch):
     # UCC-shaped circuits: fused same-flip groups (OP_GMAT) in specialised passes
+    # at full size (the parity reduction, tests/test_gpu_symmetry.py, off)
+    monkeypatch.setenv("QSV_PARITY", "0")
     cfg = W.config1(seed=n, n_qubits=n, n_electrons=ne, n_terms=200)
     _, before = jit_from_14.jit_info()
     psi = sv.evolve(sv.init_state(cfg["reference"]), cfg["circuit"])
