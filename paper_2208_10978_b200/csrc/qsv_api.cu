@@ -921,23 +921,53 @@ static bool small_enabled()
 
 static int64_t g_small_launches = 0;
 
+// The structure-only arrays of a small program live on the device once per
+// (template, device); an evolve uploads only its angles.
+static int small_dev_copy(const SmallProgram &sp, int device, const SmallProgram::DevCopy **out)
+{
+    for (const auto &d : sp.dev)
+        if (d->device == device) {
+            *out = d.get();
+            return QSV_OK;
+        }
+    Blob b;
+    auto d = std::make_shared<SmallProgram::DevCopy>();
+    d->device = device;
+    d->o_groups = b.add(sp.groups.data(), sp.groups.size() * sizeof(SmallGroup));
+    d->o_meta = b.add(sp.meta.data(), sp.meta.size() * sizeof(int32_t));
+    d->o_chunks = b.add(sp.chunks.data(), sp.chunks.size() * sizeof(int32_t));
+    d->o_xo = b.add(sp.xo.data(), sp.xo.size() * sizeof(uint32_t));
+    d->o_tab = b.add(sp.tab.data(), sp.tab.size() * sizeof(uint32_t));
+    if (cudaMalloc(&d->base, b.bytes.size()) != cudaSuccess) {
+        cudaGetLastError();
+        d->base = nullptr;
+        return fail_code(QSV_ERR_NOMEM, "small-program tables: device allocation failed");
+    }
+    QSV_CUDA(cudaMemcpy(d->base, b.bytes.data(), b.bytes.size(), cudaMemcpyHostToDevice));
+    sp.dev.push_back(d);
+    *out = d.get();
+    return QSV_OK;
+}
+
 static int run_small(qsv_state *s, const ProgramTemplate &t, const double *values, uint64_t basis)
 {
     DeviceCtx *c = nullptr;
     if (int rc = ctx_for(s->device, &c)) return rc;
     const SmallProgram &sp = t.small;
+    const SmallProgram::DevCopy *dc = nullptr;
+    if (int rc = small_dev_copy(sp, s->device, &dc)) return rc;
     Blob b;
-    const size_t o_g = b.add(sp.groups.data(), sp.groups.size() * sizeof(SmallGroup));
-    const size_t o_m = b.add(sp.meta.data(), sp.meta.size() * sizeof(int32_t));
-    const size_t o_c = b.add(sp.chunks.data(), sp.chunks.size() * sizeof(int32_t));
     const size_t o_t = b.add(nullptr, sp.src.size() * sizeof(double));
     double *th = reinterpret_cast<double *>(b.bytes.data() + o_t);
     for (size_t r = 0; r < sp.src.size(); ++r) th[r] = values[3 * (size_t)sp.src[r]];
     char *d = nullptr;
     size_t scratch = 0;
     if (int rc = upload_blob(*c, s->stream, b, 0, &d, &scratch)) return rc;
-    QSV_CUDA(launch_small(s->amps, s->n, basis, sp, (const SmallGroup *)(d + o_g), (const int32_t *)(d + o_m),
-                          (const double *)(d + o_t), (const int32_t *)(d + o_c), s->stream));
+    const char *k = dc->base;
+    QSV_CUDA(launch_small(s->amps, s->n, basis, sp, (const SmallGroup *)(k + dc->o_groups),
+                          (const int32_t *)(k + dc->o_meta), (const double *)(d + o_t),
+                          (const int32_t *)(k + dc->o_chunks), (const uint32_t *)(k + dc->o_xo),
+                          (const uint32_t *)(k + dc->o_tab), s->stream));
     ++g_small_launches;
     return QSV_OK;
 }
@@ -1701,18 +1731,21 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
          std::to_string(t.small.ncls) + ",\"share\":" + std::to_string(t.small.share) + ",\"w\":[" +
          std::to_string(t.small.w[0]) + "," + std::to_string(t.small.w[1]) + "," + std::to_string(t.small.w[2]) +
          "],\"groups\":[";
-    // [xm, r0, r1, dimb, h, pm0..3, lu0, lu1, crow0..2, cpiv0..2, comb0..2, zpos0..4]
+    // [xm, r0, r1, dimb, h, pm0..3, lu0, lu1]
     for (size_t g = 0; g < t.small.groups.size(); ++g) {
         const SmallGroup &G = t.small.groups[g];
         std::vector<int64_t> f = {G.xm, G.r0, G.r1, G.dimb, G.h, G.pm[0], G.pm[1], G.pm[2], G.pm[3], G.lu[0], G.lu[1]};
-        for (int i = 0; i < 3; ++i) f.push_back(G.crow[i]);
-        for (int i = 0; i < 3; ++i) f.push_back(G.cpiv[i]);
-        for (int i = 0; i < 3; ++i) f.push_back(G.comb[i]);
-        for (int i = 0; i < 5; ++i) f.push_back(G.zpos[i]);
         j += g ? ",[" : "[";
         for (size_t i = 0; i < f.size(); ++i) j += (i ? "," : "") + std::to_string(f[i]);
         j += "]";
     }
+    // the per-thread table and slot constants (small programs only: tests)
+    j += "],\"nthr\":" + std::to_string(t.small.nthr) + ",\"xo\":[";
+    const bool emit_tab = t.small.tab.size() <= ((size_t)1 << 18);
+    for (size_t i = 0; emit_tab && i < t.small.xo.size(); ++i) j += (i ? "," : "") + std::to_string(t.small.xo[i]);
+    j += "],\"tab\":[";
+    for (size_t i = 0; emit_tab && i < t.small.tab.size(); ++i)
+        j += (i ? "," : "") + std::to_string(t.small.tab[i]);
     j += "],\"chunks\":[";
     for (size_t i = 0; i < t.small.chunks.size(); ++i) j += (i ? "," : "") + std::to_string(t.small.chunks[i]);
     j += "]},\"passes\":[";

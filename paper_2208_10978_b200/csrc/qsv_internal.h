@@ -241,7 +241,8 @@ struct SmallGroup;    // qsv_planner.h
 struct SmallProgram;  // qsv_planner.h
 // Small-state rotation program: one CTA, state in shared memory (qsv_small.cu).
 cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram &sp, const SmallGroup *groups,
-                         const int32_t *meta, const double *theta, const int32_t *chunks, cudaStream_t st);
+                         const int32_t *meta, const double *theta, const int32_t *chunks, const uint32_t *xo,
+                         const uint32_t *tab, cudaStream_t st);
 // dst (n_dst qubits) = the parity class cls embedded from its (n_dst-1)-qubit half
 cudaError_t launch_embed_parity(double2 *dst, const double2 *src, int n_dst, uint64_t wlow, uint32_t cls,
                                 int sms, cudaStream_t st);

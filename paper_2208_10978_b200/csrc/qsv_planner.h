@@ -20,6 +20,7 @@
 
 #include <stdint.h>
 
+#include <memory>
 #include <vector>
 
 #include "qsv_internal.h"
@@ -98,25 +99,17 @@ struct ClusterFill {
 // straight-line code would stream through one SM's instruction cache.
 constexpr int kSmallMaxQubits = 12;
 constexpr int kSmallMinQubits = 8;
-struct SmallGroup {    // 100 B
+struct SmallGroup {    // 48 B
     uint32_t xm;       // flip mask (X and Y positions) shared by the group
     // phase masks over the PAIR index p (lo = p with a 0 inserted at bit h):
     // the basis of the rotations' phase-mask differences b0..b2 (0: unused)
     // and the first rotation's phase mask z0, each with bit h removed --
     // parity(lo & m) = parity(p & pm), so a pair's config is linear in p
     uint32_t pm[4];
-    // SmallProgram::share pair-index vectors u with parity(u & pm[j]) = 0 and
-    // parity(u & crow[k]) = 0, mapped to amplitude space (lu = u with a 0
-    // inserted at h): the pairs p0 ^ span(u) share p0's config and class, so
-    // one thread applies them with one matrix load
+    // share vectors (amplitude space, bit h = 0, parity(lu & pm[j]) = 0): the
+    // pairs lo0 ^ span(lu) share lo0's config, so one thread applies them with
+    // one matrix load; chosen inside the group's warp-run subspace
     uint32_t lu[2];
-    // invariant classes (SmallProgram::ncls functionals w_k): the class rows
-    // over p (reduced: row k alone carries its pivot cpiv[k]), and which of
-    // the program's functionals each row combines (for its class value)
-    uint32_t crow[3];
-    int32_t cpiv[3];
-    uint32_t comb[3];
-    int32_t zpos[5];   // where p0 gets its zeros: the u pivots and class pivots, ascending
     int32_t h;         // pivot of xm: its highest bit (bit h of lo = 0)
     int32_t r0, r1;    // rotations [r0, r1) in application order
     int32_t dimb;      // number of basis differences (configs = 2^dimb, x 2 for the sign)
@@ -130,6 +123,24 @@ struct SmallProgram {
     std::vector<int32_t> meta;    // per rotation: ny mod 4 | (ny odd) << 2 | coordinates << 3
     std::vector<int32_t> src;     // per rotation: its angle is values[3 * src]
     std::vector<int32_t> chunks;  // [g0, g1) group ranges sized for the shared-memory tables
+    // Per-thread addressing, resolved on the host once per structure so the
+    // kernel's per-group body is loads, FP64 and stores only:
+    //   tab[((g << ncls) | class) * nthr + t] = byte slot of the thread's first
+    //     pair's low amplitude | config << 16
+    //   xo[4 g .. 4 g + 3] = byte-slot XORs of the other three pairs' lows
+    //     (lu0, lu1, lu0 ^ lu1) and of the flip (low -> high amplitude)
+    int nthr = 0;
+    std::vector<uint32_t> tab;
+    std::vector<uint32_t> xo;
+    // device copy of the structure-only arrays (groups, meta, chunks, xo,
+    // tab), uploaded on first use per device; angles go up per evolve
+    struct DevCopy {
+        int device = -1;
+        char *base = nullptr;
+        size_t o_groups = 0, o_meta = 0, o_chunks = 0, o_xo = 0, o_tab = 0;
+        ~DevCopy();
+    };
+    mutable std::vector<std::shared_ptr<DevCopy>> dev;
 };
 
 struct ProgramTemplate {

@@ -19,12 +19,19 @@
 // with g = (-1)^(z0.lo) common to the group and sigma = (-1)^(d.lo) for the
 // string's phase-mask difference d = zm ^ z0 (in the span of <= 3 basis
 // vectors b_j: sigma is fixed by the 3 parities b_j.lo).  g enters every
-// off-diagonal entry, so the fused product is D M D with D = diag(1, g): 16
-// matrices per group (8 configs x g).  A pair's config is linear in its pair
-// index p, so the pairs p0 ^ span(u) for u in the null space of the four
-// parity masks all share p0's config (SmallGroup.lu).  The matrices of a
-// chunk of groups are built by the CTA itself at the start of the chunk from
-// the raw angles (sincos on device).
+// off-diagonal entry, so the fused product is D M D with D = diag(1, g): the
+// 8 configs' matrices M are built, and g = -1 negates the off-diagonals at use
+// (sign-bit XORs).  A pair's config is linear in its pair index p, so the pairs
+// lo0 ^ span(lu0, lu1) for lu in the null space of the four parity masks all
+// share lo0's config (SmallGroup.lu).  The matrices of a chunk of groups are
+// built by the CTA itself at the start of the chunk from the raw angles
+// (sincos on device).
+//
+// Warp runs: inside a run of consecutive groups every warp stays in one coset
+// of an 8-dimensional subspace holding the run's flips and share vectors, so
+// the groups of a run are separated by __syncwarp and only the run's end needs
+// a CTA barrier (config 1: 21 barriers instead of 261).  The thread -> pair map
+// is a host table (SmallProgram::tab) streamed a few groups ahead by cp.async.
 //
 // Invariant classes: a GF(2) functional w with parity(w & xm) = 0 for every
 // flip of the program is conserved by every rotation, so the amplitudes split
@@ -36,9 +43,8 @@
 //
 // Bound: shared-memory bandwidth and latency on one SM.  Per group each
 // reachable amplitude is read and written once plus one 64-B matrix per
-// thread: config 1 (one class of 2,048 amplitudes, 256 threads x 4 pairs)
-// 160 us for 261 groups (262 us without the class restriction, 280 us as tile
-// passes).
+// thread (4 pairs): config 1 (one class of 2,048 amplitudes, 256 threads)
+// walks 261 groups; history in profiles/r02_ucc12_small.txt.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -52,12 +58,53 @@ namespace qsv {
 
 // Shared-memory budget per chunk (the state takes 2^n x 16 B <= 64 KiB).
 constexpr int kSmallChunkRots = 2048;  // angles: 32 KiB of (cos, sin)
-constexpr int kSmallChunkGroups = 80;  // matrices: 80 x 16 configs x 80 B = 100 KiB
+constexpr int kSmallChunkGroups = 144;  // matrices: 144 x 8 configs x 80 B = 90 KiB (the group sign g
+                                        // is applied at use: D M D only negates the off-diagonals)
+constexpr int kRing = 8;               // table ring slots (per-thread entries of upcoming groups)
+constexpr int kAhead = 6;              // table entries in flight ahead of use
 constexpr int kRow = 5;                // double2 per matrix row (4 used; 80 B spreads rows over banks)
+constexpr uint32_t kSmallRunEnd = 1u << 31;         // xo[4 g + 3]: a CTA barrier follows group g
+constexpr size_t kSmallMaxTable = (size_t)16 << 20;  // per-thread table entries (64 MiB)
 size_t small_smem_bytes(int n);
 static_assert(sizeof(SmallGroup) % 4 == 0, "group records are copied as words");
 
 static inline uint32_t parity32(uint32_t v) { return (uint32_t)__builtin_popcount(v) & 1u; }
+
+// Shared-memory slot of amplitude l: the low 3 bits (16-B granule within a
+// 128-B row) are flipped by bit 3, so any three of the bits 0-3 -- the bits a
+// quarter warp's 8 pairs vary once the pivot bit is skipped -- reach 8
+// distinct granules.  Linear over GF(2): slot(a ^ b) = slot(a) ^ slot(b).
+__host__ __device__ __forceinline__ uint32_t small_slot(uint32_t l) { return l ^ (((l >> 3) & 1u) * 7u); }
+
+// A GF(2) subspace of small index vectors: basis kept by descending pivot
+// (highest bit), so reduce() clears the pivots in order.
+struct Gf2Span {
+    uint32_t b[32] = {0};
+    int d = 0;
+    static int piv(uint32_t v) { return 31 - __builtin_clz(v); }
+    uint32_t reduce(uint32_t v) const
+    {
+        for (int i = 0; i < d; ++i)
+            if ((v >> piv(b[i])) & 1u) v ^= b[i];
+        return v;
+    }
+    bool contains(uint32_t v) const { return reduce(v) == 0; }
+    bool add(uint32_t v)
+    {
+        const uint32_t r = reduce(v);
+        if (!r) return false;
+        int i = d++;
+        while (i > 0 && piv(b[i - 1]) < piv(r)) { b[i] = b[i - 1]; --i; }
+        b[i] = r;
+        return true;
+    }
+    std::vector<uint32_t> elements() const
+    {
+        std::vector<uint32_t> out(1u << d, 0);
+        for (uint32_t m = 1; m < (1u << d); ++m) out[m] = out[m & (m - 1)] ^ b[__builtin_ctz(m)];
+        return out;
+    }
+};
 
 bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
 {
@@ -65,7 +112,6 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
     if (n < kSmallMinQubits || n > kSmallMaxQubits || R.empty()) return false;
     for (const Rot &r : R)
         if ((r.x | r.y) == 0) return false;  // diagonal strings: not handled here
-    const uint32_t pmask = (1u << (n - 1)) - 1u;  // pair-index space
     size_t k = 0;
     while (k < R.size()) {
         SmallGroup g{};
@@ -139,54 +185,6 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
     sp.ncls = ncls;
     sp.share = share;
     for (int i = 0; i < ncls; ++i) sp.w[i] = W[i];
-    for (SmallGroup &g : sp.groups) {
-        const uint32_t lowm = (1u << g.h) - 1u;
-        uint32_t wp[3] = {0, 0, 0};
-        for (int i = 0; i < ncls; ++i) wp[i] = (W[i] & lowm) | ((W[i] >> 1) & ~lowm);
-        // share null-space vectors of the four parity masks and the class
-        // rows, reduced so each owns its pivot (its highest bit, as high as
-        // possible: the thread-to-pair map keeps the low bits consecutive)
-        uint32_t u[2] = {0, 0};
-        int nu = 0;
-        for (uint32_t v = pmask; v > 0 && nu < share; --v) {
-            bool in_null = true;
-            for (int j = 0; j < 4; ++j) in_null &= parity32(v & g.pm[j]) == 0;
-            for (int j = 0; j < ncls; ++j) in_null &= parity32(v & wp[j]) == 0;
-            if (!in_null) continue;
-            uint32_t r = v;
-            for (int i = 0; i < nu; ++i)
-                if ((r >> (31 - __builtin_clz(u[i]))) & 1u) r ^= u[i];
-            if (!r) continue;
-            const int pv = 31 - __builtin_clz(r);  // not an earlier pivot: r is reduced by them
-            for (int i = 0; i < nu; ++i)
-                if ((u[i] >> pv) & 1u) u[i] ^= r;  // earlier vectors must not carry the new pivot
-            u[nu++] = r;
-        }
-        if (nu < share) return false;
-        uint32_t upiv = 0;
-        for (int i = 0; i < nu; ++i) {
-            upiv |= 1u << (31 - __builtin_clz(u[i]));
-            g.lu[i] = (u[i] & lowm) | ((u[i] & ~lowm) << 1);
-        }
-        // class rows in reduced echelon form over pivots that are not u pivots
-        for (int i = 0; i < ncls; ++i) {
-            uint32_t r = wp[i], cb = 1u << i;
-            for (int j = 0; j < i; ++j)
-                if ((r >> g.cpiv[j]) & 1u) { r ^= g.crow[j]; cb ^= g.comb[j]; }
-            const uint32_t avail = r & ~upiv;
-            if (!avail) return false;
-            const int pv = 31 - __builtin_clz(avail);
-            for (int j = 0; j < i; ++j)
-                if ((g.crow[j] >> pv) & 1u) { g.crow[j] ^= r; g.comb[j] ^= cb; }
-            g.crow[i] = r;
-            g.comb[i] = cb;
-            g.cpiv[i] = pv;
-        }
-        int nz = 0;
-        for (int i = 0; i < nu; ++i) g.zpos[nz++] = 31 - __builtin_clz(u[i]);
-        for (int i = 0; i < ncls; ++i) g.zpos[nz++] = g.cpiv[i];
-        std::sort(g.zpos, g.zpos + nz);
-    }
     // chunks of groups whose angles and matrices fit the shared tables
     int g0 = 0;
     const int ng = (int)sp.groups.size();
@@ -200,18 +198,200 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
         sp.chunks.push_back(g1);
         g0 = g1;
     }
+    // Warp runs.  Per class the CTA holds 2^(n - ncls) amplitudes; every
+    // group of a run is applied with each warp confined to one coset of an
+    // 8-dimensional subspace V of the class (256 amplitudes: 32 lanes x 4
+    // pairs) that contains the run's flips and each group's two share
+    // vectors, so inside a run a warp only ever touches its own amplitudes
+    // and the groups are separated by __syncwarp; one CTA barrier ends the
+    // run (and every chunk).  Runs are grown greedily while V stays at <= 8
+    // dimensions.
+    const int dimE = n - ncls;
+    std::vector<uint32_t> E;  // the class direction space (functionals vanish)
+    for (uint32_t v = 0; v < (1u << n); ++v) {
+        bool in = true;
+        for (int k = 0; k < ncls; ++k) in &= parity32(v & W[k]) == 0;
+        if (in) E.push_back(v);
+    }
+    auto low3 = [](uint32_t v) { return small_slot(v) & 7u; };
+    // per group: amplitude-space parity masks (bit h free: share vectors have bit h = 0)
+    auto in_null = [&](const SmallGroup &G, uint32_t v) {
+        if ((v >> G.h) & 1u) return false;
+        const uint32_t lowm = (1u << G.h) - 1u;
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t am = (G.pm[j] & lowm) | ((G.pm[j] & ~lowm) << 1);
+            if (parity32(v & am)) return false;
+        }
+        return true;
+    };
+    auto share_dim = [&](const Gf2Span &V, const SmallGroup &G) {
+        Gf2Span S;
+        for (uint32_t e : V.elements())
+            if (in_null(G, e)) S.add(e);
+        return S;
+    };
+    sp.nthr = 1 << ((n - 1) - share - ncls);
+    const int nwarps = sp.nthr / 32;
+    const size_t entries = sp.groups.size() * ((size_t)sp.nthr << ncls);
+    if (entries > kSmallMaxTable) return false;
+    sp.tab.assign(entries, 0);
+    sp.xo.assign(4 * sp.groups.size(), 0);
+    std::vector<int> warp_of(1u << n, -1);
+    std::vector<uint32_t> cls_of(1u << n, 0);
+    for (uint32_t i = 0; i < (1u << n); ++i)
+        for (int k = 0; k < ncls; ++k) cls_of[i] |= parity32(i & W[k]) << k;
+    for (size_t ci = 0; ci < sp.chunks.size(); ci += 2) {
+        const int c0 = sp.chunks[ci], c1 = sp.chunks[ci + 1];
+        int g = c0;
+        while (g < c1) {
+            Gf2Span V;
+            int gg = g;
+            for (; gg < c1; ++gg) {
+                Gf2Span V1 = V;
+                V1.add(sp.groups[gg].xm);
+                bool ok = V1.d <= 8;
+                for (int m = g; m <= gg && ok; ++m) {
+                    const SmallGroup &G = sp.groups[m];
+                    while (ok && share_dim(V1, G).d < share) {
+                        // a vector of the group's null space (in E) not yet in V1,
+                        // preferring one that adds a new low slot pattern
+                        uint32_t best = 0;
+                        int best_score = -1;
+                        Gf2Span L;
+                        for (uint32_t e : V1.elements()) L.add(low3(e));
+                        for (uint32_t e : E) {
+                            if (!e || !in_null(G, e) || V1.contains(e)) continue;
+                            const int score = L.contains(low3(e)) ? 0 : 1;
+                            if (score > best_score) { best = e; best_score = score; }
+                            if (best_score == 1) break;
+                        }
+                        if (best_score < 0 || V1.d >= 8) { ok = false; break; }
+                        V1.add(best);
+                    }
+                }
+                if (!ok) break;
+                V = V1;
+            }
+            if (gg == g) return false;  // one group alone: no two share vectors in its class
+            // pad V to 8 dimensions inside E, widening its low slot patterns first
+            while (V.d < 8) {
+                Gf2Span L;
+                for (uint32_t e : V.elements()) L.add(low3(e));
+                uint32_t best = 0;
+                int best_score = -1;
+                for (uint32_t e : E) {
+                    if (!e || V.contains(e)) continue;
+                    const int score = L.contains(low3(e)) ? 0 : 1;
+                    if (score > best_score) { best = e; best_score = score; }
+                    if (best_score == 1) break;
+                }
+                if (best_score < 0) return false;
+                V.add(best);
+            }
+            // warp = coset of V inside the class: enumerate the cosets from
+            // each class's smallest index and a complement basis of V in E
+            Gf2Span Cs = V;
+            std::vector<uint32_t> comp;
+            for (uint32_t e : E)
+                if (Cs.add(e)) comp.push_back(e);
+            if ((int)comp.size() != dimE - 8 || (1 << comp.size()) != nwarps) return false;
+            const std::vector<uint32_t> Vel = V.elements();
+            for (uint32_t cl = 0; cl < (1u << ncls); ++cl) {
+                uint32_t b = 0;
+                while (cls_of[b] != cl) ++b;
+                for (int a = 0; a < nwarps; ++a) {
+                    uint32_t r = b;
+                    for (size_t k = 0; k < comp.size(); ++k)
+                        if ((a >> k) & 1) r ^= comp[k];
+                    for (uint32_t v : Vel) warp_of[r ^ v] = a;
+                }
+            }
+            for (int m = g; m < gg; ++m) {
+                SmallGroup &G = sp.groups[m];
+                // share vectors: two independent ones of V in the null space,
+                // preferring no low slot bits (the lanes' low slots then spread)
+                const Gf2Span S = share_dim(V, G);
+                std::vector<uint32_t> Sel = S.elements();
+                std::stable_sort(Sel.begin(), Sel.end(),
+                                 [&](uint32_t a, uint32_t b2) { return (low3(a) != 0) < (low3(b2) != 0); });
+                uint32_t u0 = 0, u1 = 0;
+                for (uint32_t e : Sel)
+                    if (e) { u0 = e; break; }
+                for (uint32_t e : Sel)
+                    if (e && e != u0) { u1 = e; break; }
+                if (!u0 || !u1) return false;
+                G.lu[0] = u0;
+                G.lu[1] = u1;
+                const uint32_t lowm = (1u << G.h) - 1u;
+                sp.xo[4 * m + 0] = small_slot(u0) << 4;
+                sp.xo[4 * m + 1] = small_slot(u1) << 4;
+                sp.xo[4 * m + 2] = small_slot(u0 ^ u1) << 4;
+                sp.xo[4 * m + 3] = (small_slot(G.xm) << 4) | (m == gg - 1 ? kSmallRunEnd : 0u);
+                const uint32_t span4[4] = {0, u0, u1, u0 ^ u1};
+                for (uint32_t cl = 0; cl < (1u << ncls); ++cl) {
+                    std::vector<std::vector<uint32_t>> quads(nwarps);
+                    for (uint32_t i = 0; i < (1u << n); ++i) {
+                        if (cls_of[i] != cl || ((i >> G.h) & 1u)) continue;
+                        if (i != std::min(std::min(i, i ^ u0), std::min(i ^ u1, i ^ u0 ^ u1))) continue;
+                        quads[warp_of[i]].push_back(i);
+                    }
+                    uint32_t *row = sp.tab.data() + (((size_t)m << ncls) | cl) * (size_t)sp.nthr;
+                    for (int w = 0; w < nwarps; ++w) {
+                        std::vector<uint32_t> &Q = quads[w];
+                        if (Q.size() != 32) return false;
+                        // lanes in quarters of 8 with distinct low slot
+                        // bits (conflict-free 128-bit accesses), greedily
+                        std::vector<bool> taken(32, false);
+                        for (int qt = 0; qt < 4; ++qt) {
+                            uint32_t used = 0;
+                            for (int j = 0; j < 8; ++j) {
+                                int pick = -1, pick_rep = 0, pick_opts = 99;
+                                for (int qi = 0; qi < 32; ++qi) {
+                                    if (taken[qi]) continue;
+                                    int opts = 0, rep = -1;
+                                    for (int a = 0; a < 4; ++a)
+                                        if (!((used >> low3(Q[qi] ^ span4[a])) & 1u)) {
+                                            ++opts;
+                                            if (rep < 0) rep = a;
+                                        }
+                                    if (opts && opts < pick_opts) { pick = qi; pick_rep = rep; pick_opts = opts; }
+                                }
+                                if (pick < 0) {  // no free pattern left: accept a conflict
+                                    for (int qi = 0; qi < 32 && pick < 0; ++qi)
+                                        if (!taken[qi]) pick = qi;
+                                    pick_rep = 0;
+                                }
+                                taken[pick] = true;
+                                const uint32_t lo0 = Q[pick] ^ span4[pick_rep];
+                                used |= 1u << low3(lo0);
+                                const uint32_t p0 = (lo0 & lowm) | ((lo0 >> 1) & ~lowm);
+                                const uint32_t cfg = parity32(p0 & G.pm[0]) | (parity32(p0 & G.pm[1]) << 1) |
+                                                     (parity32(p0 & G.pm[2]) << 2) | (parity32(p0 & G.pm[3]) << 3);
+                                row[w * 32 + qt * 8 + j] = (small_slot(lo0) << 4) | (cfg << 16);
+                            }
+                        }
+                    }
+                }
+            }
+            g = gg;
+        }
+    }
     sp.valid = true;
     return true;
 }
 
+SmallProgram::DevCopy::~DevCopy()
+{
+    if (!base) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return;  // runtime already torn down
+    cudaSetDevice(device);
+    cudaFree(base);
+    cudaSetDevice(cur);
+    cudaGetLastError();
+}
+
 namespace {
-
-// Slot of amplitude l: the low 3 bits (16-B granule within a 128-B row) are
-// flipped by bit 3, so any three of the bits 0-3 -- the bits a quarter warp's
-// 8 pairs vary once the pivot bit is skipped -- reach 8 distinct granules.
-__device__ __forceinline__ uint32_t sslot(uint32_t l) { return l ^ (((l >> 3) & 1u) * 7u); }
-
-__device__ __forceinline__ uint32_t par(uint32_t v) { return (uint32_t)__popc(v) & 1u; }
 
 // i^k * v for a real v
 __device__ __forceinline__ double2 ipow(int k, double v)
@@ -223,6 +403,12 @@ __device__ __forceinline__ double2 ipow(int k, double v)
         default: return make_double2(0.0, -v);
     }
 }
+// -v when sg = 1 << 31 (sign bits of both parts), else v: integer XORs, no FP64 issue
+__device__ __forceinline__ double2 flip_sign(double2 v, uint32_t sg)
+{
+    return make_double2(__hiloint2double(__double2hiint(v.x) ^ (int)sg, __double2loint(v.x)),
+                        __hiloint2double(__double2hiint(v.y) ^ (int)sg, __double2loint(v.y)));
+}
 __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -232,31 +418,59 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c)
     return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
 
-// S = log2 pairs per thread sharing one matrix load; 2^(11 - S) threads
 constexpr int kMaxThreads = 512;
 
-// One CTA of (pairs in a class) / 2^S threads; per group every thread
-// applies the group's matrix for its config to the 2^S pairs p0 ^ span(lu)
-// of each class this evolve can reach.  p0 comes from the thread index with
-// zeros inserted at the u and class pivots, the class pivots then set so that
-// p0 lies in the class.  The chunk's group records sit in shared memory.
-template <int S, int NC>
+// One CTA of (pairs in a class) / 4 threads; per group every thread applies
+// the group's matrix for its config to the 4 pairs p0 ^ span(lu0, lu1) of
+// each class this evolve can reach.  The thread -> pair map is the host's
+// table (SmallProgram::tab: first low slot | config << 16), read one item
+// ahead of use; the other slots are that slot XOR the group's constants
+// (small_slot is linear), so the per-group body is 4 matrix loads, 8
+// amplitude loads, 64 FP64, 8 stores and one barrier.  The chunk's group
+// records (for the matrix build) and slot constants sit in shared memory.
+template <int NC>
 __global__ void __launch_bounds__(kMaxThreads, 1)
 small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGroup *__restrict__ groups,
                  const int32_t *__restrict__ meta, const double *__restrict__ theta,
-                 const int32_t *__restrict__ chunks, int nchunks, uint32_t cls0, uint32_t cls1)
+                 const int32_t *__restrict__ chunks, int nchunks, const uint4 *__restrict__ xo,
+                 const uint32_t *__restrict__ tab, uint32_t cls0, uint32_t cls1)
 {
-    constexpr int kShare = 1 << S;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t dim = 1u << n;
     const uint32_t nthr = blockDim.x;
     double2 *st = reinterpret_cast<double2 *>(smem_raw);  // state
     double2 *cs = st + dim;                               // (cos, sin) of the chunk's angles
-    double2 *mt = cs + kSmallChunkRots;                   // [group][16 configs][kRow]
-    SmallGroup *gs = reinterpret_cast<SmallGroup *>(mt + 16 * kRow * kSmallChunkGroups);  // the chunk's groups
+    double2 *mt = cs + kSmallChunkRots;                   // [group][8 configs][kRow]
+    uint4 *xs = reinterpret_cast<uint4 *>(mt + 8 * kRow * kSmallChunkGroups);  // the chunk's slot XORs
+    uint32_t *ring = reinterpret_cast<uint32_t *>(xs + kSmallChunkGroups);        // [kRing][nthr] table entries
+    int32_t *ms = reinterpret_cast<int32_t *>(ring + kRing * kMaxThreads);       // the chunk's rotation meta
+    SmallGroup *gs = reinterpret_cast<SmallGroup *>(ms + kSmallChunkRots);        // the chunk's groups
+    unsigned char *sb = smem_raw;
     const uint32_t tid = threadIdx.x;
+    // the (group, class) items in order; each thread streams its own table
+    // entries kAhead items ahead of use through a shared-memory ring
+    // (cp.async, one commit group per item; a thread reads only its own slots)
+    const uint32_t ncl = cls1 - cls0;
+    const uint32_t n_items = (uint32_t)chunks[2 * nchunks - 1] * ncl;
+    const uint32_t ring_base = (uint32_t)__cvta_generic_to_shared(ring + tid);
+    uint32_t f_item = 0, f_g = 0, f_cl = cls0;  // next item to fetch and its (group, class)
+    auto fetch = [&]() {
+        if (f_item < n_items) {
+            const uint32_t *src = tab + (((size_t)f_g << NC) | f_cl) * nthr + tid;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(ring_base + (f_item % kRing) * nthr * 4u),
+                         "l"(src));
+            if (++f_cl == cls1) {
+                f_cl = cls0;
+                ++f_g;
+            }
+        }
+        ++f_item;
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    for (int k = 0; k < kAhead; ++k) fetch();
     for (uint32_t i = tid; i < dim; i += nthr)
-        st[sslot(i)] = basis != ~0ull ? make_double2(i == basis ? 1.0 : 0.0, 0.0) : psi[i];
+        st[small_slot(i)] = basis != ~0ull ? make_double2(i == basis ? 1.0 : 0.0, 0.0) : psi[i];
+    uint32_t item = 0;
     for (int ch = 0; ch < nchunks; ++ch) {
         const int g0 = chunks[2 * ch], g1 = chunks[2 * ch + 1];
         const int rb = groups[g0].r0, re = groups[g1 - 1].r1;
@@ -270,6 +484,8 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
             const uint32_t *src = reinterpret_cast<const uint32_t *>(groups + g0);
             uint32_t *dst = reinterpret_cast<uint32_t *>(gs);
             for (int i = (int)tid; i < words; i += nthr) dst[i] = src[i];
+            for (int i = (int)tid; i < g1 - g0; i += nthr) xs[i] = xo[g0 + i];
+            for (int r = rb + (int)tid; r < re; r += nthr) ms[r - rb] = meta[r];
         }
         __syncthreads();  // angles and groups ready; the previous chunk is done with mt
         for (int t = (int)tid; t < (g1 - g0) * 8; t += nthr) {
@@ -279,7 +495,7 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
             double2 m00 = make_double2(1.0, 0.0), m01 = make_double2(0.0, 0.0);
             double2 m10 = make_double2(0.0, 0.0), m11 = make_double2(1.0, 0.0);
             for (int r = G.r0; r < G.r1; ++r) {
-                const int mk = meta[r];
+                const int mk = ms[r - rb];
                 const double2 csr = cs[r - rb];
                 const double sig = (__popc((uint32_t)(mk >> 3) & cfg) & 1) ? -1.0 : 1.0;
                 // off-diagonals: b = -i s i^ny sigma (lo <- hi gets (-1)^ny more)
@@ -292,72 +508,59 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
                 const double2 n11 = cfma(b, m01, make_double2(c * m11.x, c * m11.y));
                 m00 = n00; m01 = n01; m10 = n10; m11 = n11;
             }
-            double2 *row = mt + ((t / 8) * 16 + (int)cfg) * kRow;
+            double2 *row = mt + t * kRow;  // [group][config]
             row[0] = m00; row[1] = m01; row[2] = m10; row[3] = m11;
-            row += 8 * kRow;  // g = 1: D M D, D = diag(1, -1)
-            row[0] = m00; row[1] = make_double2(-m01.x, -m01.y);
-            row[2] = make_double2(-m10.x, -m10.y); row[3] = m11;
         }
         __syncthreads();
         for (int gi = 0; gi < g1 - g0; ++gi) {
-            const SmallGroup &G = gs[gi];
-            uint32_t q0 = tid;
+            const uint4 X = xs[gi];
+            const uint32_t xh = X.w & 0xffffu;
+            for (uint32_t c = 0; c < ncl; ++c) {  // the classes this evolve can reach
+                fetch();
+                asm volatile("cp.async.wait_group %0;\n" ::"n"(kAhead));
+                const uint32_t e = ring[(item % kRing) * nthr + tid];
+                ++item;
+                const double2 *M = mt + (gi * 8 + (int)((e >> 16) & 7u)) * kRow;
+                const uint32_t sg = (e >> 19) << 31;  // g = -1: D M D, D = diag(1, -1)
+                const double2 m00 = M[0], m11 = M[3];
+                const double2 m01 = flip_sign(M[1], sg), m10 = flip_sign(M[2], sg);
+                const uint32_t o0 = e & 0xffffu;
+                const uint32_t lo[4] = {o0, o0 ^ X.x, o0 ^ X.y, o0 ^ X.z};
+                double2 x[4], y[4];
 #pragma unroll
-            for (int i = 0; i < S + NC; ++i) {  // zeros at the (ascending) u and class pivots
-                const uint32_t lm = (1u << G.zpos[i]) - 1u;
-                q0 = ((q0 & ~lm) << 1) | (q0 & lm);
-            }
-            const uint32_t lowm = (1u << G.h) - 1u, xm = G.xm;
-            for (uint32_t cl = cls0; cl < cls1; ++cl) {  // the classes this evolve can reach
-                uint32_t p0 = q0;
-#pragma unroll
-                for (int k = 0; k < NC; ++k)
-                    if (par(p0 & G.crow[k]) != par(G.comb[k] & cl)) p0 |= 1u << G.cpiv[k];
-                const uint32_t cfg = par(p0 & G.pm[0]) | (par(p0 & G.pm[1]) << 1) | (par(p0 & G.pm[2]) << 2) |
-                                     (par(p0 & G.pm[3]) << 3);
-                const double2 *M = mt + (gi * 16 + (int)cfg) * kRow;
-                const double2 m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
-                const uint32_t lo0 = ((p0 & ~lowm) << 1) | (p0 & lowm);
-                uint32_t lo[kShare];
-#pragma unroll
-                for (int a = 0; a < kShare; ++a) {
-                    uint32_t v = lo0;
-#pragma unroll
-                    for (int i = 0; i < S; ++i)
-                        if ((a >> i) & 1) v ^= G.lu[i];
-                    lo[a] = v;
-                }
-                double2 x[kShare], y[kShare];
-#pragma unroll
-                for (int a = 0; a < kShare; ++a) {
-                    x[a] = st[sslot(lo[a])];
-                    y[a] = st[sslot(lo[a] ^ xm)];
+                for (int a = 0; a < 4; ++a) {
+                    x[a] = *reinterpret_cast<const double2 *>(sb + lo[a]);
+                    y[a] = *reinterpret_cast<const double2 *>(sb + (lo[a] ^ xh));
                 }
 #pragma unroll
-                for (int a = 0; a < kShare; ++a) {
-                    st[sslot(lo[a])] = cfma(m01, y[a], cmul(m00, x[a]));
-                    st[sslot(lo[a] ^ xm)] = cfma(m11, y[a], cmul(m10, x[a]));
+                for (int a = 0; a < 4; ++a) {
+                    *reinterpret_cast<double2 *>(sb + lo[a]) = cfma(m01, y[a], cmul(m00, x[a]));
+                    *reinterpret_cast<double2 *>(sb + (lo[a] ^ xh)) = cfma(m11, y[a], cmul(m10, x[a]));
                 }
             }
-            __syncthreads();
+            // inside a warp run each warp owns its amplitudes: a warp barrier
+            if (X.w & kSmallRunEnd)
+                __syncthreads();
+            else
+                __syncwarp();
         }
     }
-    for (uint32_t i = tid; i < dim; i += nthr) psi[i] = st[sslot(i)];
+    for (uint32_t i = tid; i < dim; i += nthr) psi[i] = st[small_slot(i)];
 }
 
 template <int NC>
-cudaError_t launch_nc(double2 *psi, int n, uint64_t basis, const SmallGroup *groups, const int32_t *meta,
-                      const double *theta, const int32_t *chunks, int nchunks, uint32_t c0, uint32_t c1,
-                      cudaStream_t st, size_t smem)
+cudaError_t launch_nc(double2 *psi, int n, uint64_t basis, const SmallProgram &sp, const SmallGroup *groups,
+                      const int32_t *meta, const double *theta, const int32_t *chunks, const uint4 *xo,
+                      const uint32_t *tab, int nchunks, uint32_t c0, uint32_t c1, cudaStream_t st, size_t smem)
 {
     static PerDeviceOnce once;
     if (cudaError_t e = once.run([&] {
-            return cudaFuncSetAttribute(small_rot_kernel<2, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            return cudaFuncSetAttribute(small_rot_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)small_smem_bytes(kSmallMaxQubits));
         }))
         return e;
-    const int threads = std::max(32, std::min(kMaxThreads, ((1 << n) >> 1) >> (2 + NC)));
-    small_rot_kernel<2, NC><<<1, threads, smem, st>>>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1);
+    small_rot_kernel<NC><<<1, sp.nthr, smem, st>>>(psi, n, basis, groups, meta, theta, chunks, nchunks, xo, tab,
+                                                   c0, c1);
     return cudaGetLastError();
 }
 
@@ -394,13 +597,14 @@ cudaError_t launch_embed_parity(double2 *dst, const double2 *src, int n_dst, uin
 
 size_t small_smem_bytes(int n)
 {
-    return ((size_t)16 << n) + 16 * (size_t)kSmallChunkRots + 16 * (size_t)kRow * 16 * kSmallChunkGroups +
+    return ((size_t)16 << n) + 16 * (size_t)kSmallChunkRots + 16 * (size_t)kRow * 8 * kSmallChunkGroups +
+           16 * (size_t)kSmallChunkGroups + 4 * (size_t)kRing * kMaxThreads + 4 * (size_t)kSmallChunkRots +
            sizeof(SmallGroup) * kSmallChunkGroups;
 }
 
 cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram &sp,
                          const SmallGroup *groups, const int32_t *meta, const double *theta,
-                         const int32_t *chunks, cudaStream_t st)
+                         const int32_t *chunks, const uint32_t *xo, const uint32_t *tab, cudaStream_t st)
 {
     // from a basis state only its own class is ever non-zero
     uint32_t c0 = 0, c1 = 1u << sp.ncls;
@@ -411,12 +615,16 @@ cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram
     }
     const int nchunks = (int)(sp.chunks.size() / 2);
     const size_t smem = small_smem_bytes(n);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(xo);
+#define QSV_SMALL_LAUNCH(NC) \
+    launch_nc<NC>(psi, n, basis, sp, groups, meta, theta, chunks, x4, tab, nchunks, c0, c1, st, smem)
     switch (sp.ncls) {
-        case 0: return launch_nc<0>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
-        case 1: return launch_nc<1>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
-        case 2: return launch_nc<2>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
-        default: return launch_nc<3>(psi, n, basis, groups, meta, theta, chunks, nchunks, c0, c1, st, smem);
+        case 0: return QSV_SMALL_LAUNCH(0);
+        case 1: return QSV_SMALL_LAUNCH(1);
+        case 2: return QSV_SMALL_LAUNCH(2);
+        default: return QSV_SMALL_LAUNCH(3);
     }
+#undef QSV_SMALL_LAUNCH
 }
 
 }  // namespace qsv

@@ -326,7 +326,7 @@ def test_small_program_grouping_host_side():
     sm = _lib.debug_plan(12, k, q, v)["small"]
     assert sm["valid"] == 1 and len(sm["groups"]) == 261
     assert collections.Counter(g[2] - g[1] for g in sm["groups"]) == {8: 225, 2: 36}
-    assert sm["chunks"] == [0, 80, 80, 160, 160, 240, 240, 261]
+    assert sm["chunks"] == [0, 144, 144, 261]
     assert all(g[3] <= 3 for g in sm["groups"])  # <= 8 sign-pattern configs per group
     rng = np.random.default_rng(2)
     strings = W.ucc_rotation_strings(10, 5)[:60]
@@ -355,54 +355,60 @@ def _popc(v):
     return bin(int(v)).count("1") & 1
 
 
+def _slot(v):
+    """small_slot (csrc/qsv_small.cu): an involution on 16-B shared-memory slots."""
+    return v ^ (7 if (v >> 3) & 1 else 0)
+
+
 def _emulate_small(n, circ, basis):
-    """CPU mirror of small_rot_kernel's pair enumeration: the host tables
-    (debug_plan's "small") decide which pairs each thread covers; the
-    matrices are rebuilt here from the rotation list.  Returns the evolved
-    state and checks that every group covers each pair of the basis state's
-    class exactly once, with one config per thread."""
+    """CPU mirror of small_rot_kernel: the host table (debug_plan's "small":
+    per group and class, each thread's first pair slot | config << 16, the
+    share / flip slot XORs and the run-end flag) decides which pairs each
+    thread covers; the matrices are rebuilt here from the rotation list.
+    Returns the evolved state and checks that every group covers each pair of
+    the basis state's class exactly once with one config per thread, that the
+    lanes of each quarter warp hit distinct 16-B granules, and that inside a
+    warp run no two warps touch the same amplitude (so __syncwarp suffices)."""
     k, q, v = flatten_bound(circ)
     plan = _lib.debug_plan(n, k, q, v)
     sm = plan["small"]
     assert sm["valid"] == 1
     spans, masks = _lib.match_rotations(n, k, q)
     R = [(int(m[0]), int(m[1]), int(m[2]), float(v[3 * int(s[2])])) for s, m in zip(spans, masks)]
-    ncls, S, W = sm["ncls"], sm["share"], sm["w"]
+    ncls, W, nthr = sm["ncls"], sm["w"], sm["nthr"]
+    tab, xo = sm["tab"], sm["xo"]
+    assert len(tab) == len(sm["groups"]) * (nthr << ncls)
     cls = sum(_popc(basis & W[j]) << j for j in range(ncls))
     psi = np.zeros(1 << n, dtype=complex)
     psi[basis] = 1.0
-    for g in sm["groups"]:
+    owner = {}  # amplitude -> warp, within the current run
+    conflicts = []  # per quarter warp: lanes sharing a 16-B granule
+    for gi, g in enumerate(sm["groups"]):
         xm, r0, r1, dimb, h = g[0:5]
         pm, lu = g[5:9], g[9:11]
-        crow, cpiv, comb, zpos = g[11:14], g[14:17], g[17:20], g[20:25]
+        assert xo[4 * gi] >> 4 == _slot(lu[0]) and xo[4 * gi + 1] >> 4 == _slot(lu[1])
+        assert (xo[4 * gi + 3] & 0xFFFF) >> 4 == _slot(xm)
         rots = R[r0:r1]
-        z0 = rots[0][1] | rots[0][2]
-        # matrices per amplitude-space sign pattern of the group's strings
-        mats = {}
         pairs_seen = set()
         lowm = (1 << h) - 1
-        nthreads = (1 << (n - 1)) >> (S + ncls)
-        for t in range(nthreads):
-            q0 = t
-            for i in range(S + ncls):
-                lm = (1 << zpos[i]) - 1
-                q0 = ((q0 & ~lm) << 1) | (q0 & lm)
-            p0 = q0
-            for j in range(ncls):
-                if _popc(p0 & crow[j]) != _popc(comb[j] & cls):
-                    p0 |= 1 << cpiv[j]
-            cfg0 = tuple(_popc(p0 & m) for m in pm)
-            lo0 = ((p0 & ~lowm) << 1) | (p0 & lowm)
-            for a in range(1 << S):
-                lo = lo0
-                for i in range(S):
-                    if (a >> i) & 1:
-                        lo ^= lu[i]
+        for t in range(nthr):
+            e = tab[((gi << ncls) | cls) * nthr + t]
+            lo0 = _slot((e & 0xFFFF) >> 4)
+            cfg0 = (e >> 16) & 15
+            if t % 8 == 0:
+                granules = set()
+            granules.add(_slot(lo0) & 7)
+            if t % 8 == 7:
+                conflicts.append(8 - len(granules))
+            for a in range(4):
+                lo = lo0 ^ (lu[0] if a & 1 else 0) ^ (lu[1] if a & 2 else 0)
                 p = (lo & lowm) | ((lo >> 1) & ~lowm)
-                assert tuple(_popc(p & m) for m in pm) == cfg0  # shared config
+                assert sum(_popc(p & m) << j for j, m in enumerate(pm)) == cfg0  # shared config
                 assert (lo >> h) & 1 == 0 and lo not in pairs_seen
                 pairs_seen.add(lo)
                 hi = lo ^ xm
+                for amp in (lo, hi):
+                    assert owner.setdefault(amp, t // 32) == t // 32, "two warps in one run"
                 M = np.eye(2, dtype=complex)
                 for (x, y, z, th) in rots:
                     ny = bin(y).count("1")
@@ -414,6 +420,9 @@ def _emulate_small(n, circ, basis):
         want = {lo for lo in range(1 << n) if not (lo >> h) & 1
                 and sum(_popc(lo & W[j]) << j for j in range(ncls)) == cls}
         assert pairs_seen == want
+        if xo[4 * gi + 3] >> 31:  # a CTA barrier ends the run
+            owner = {}
+    sm["conflicts"] = conflicts
     return psi, sm
 
 
