@@ -959,7 +959,14 @@ static int run_small(qsv_state *s, const ProgramTemplate &t, const double *value
     Blob b;
     const size_t o_t = b.add(nullptr, sp.src.size() * sizeof(double));
     double *th = reinterpret_cast<double *>(b.bytes.data() + o_t);
-    for (size_t r = 0; r < sp.src.size(); ++r) th[r] = values[3 * (size_t)sp.src[r]];
+    uint64_t bad = 0;
+    for (size_t r = 0; r < sp.src.size(); ++r) {
+        th[r] = values[3 * (size_t)sp.src[r]];
+        uint64_t bits;
+        std::memcpy(&bits, th + r, 8);
+        bad |= (uint64_t)(((bits >> 52) & 0x7ffu) == 0x7ffu);
+    }
+    if (bad) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
     char *d = nullptr;
     size_t scratch = 0;
     if (int rc = upload_blob(*c, s->stream, b, 0, &d, &scratch)) return rc;
@@ -1129,6 +1136,12 @@ static int apply_prepared_impl(qsv_state *s, int64_t program_id, const double *v
     }
     if (!values) return fail_code(QSV_ERR_INVALID, "null gate values");
     if (int rc = settle(s)) return rc;
+    QSV_CUDA(cudaSetDevice(s->device));
+    if (e.tpl.small.valid && small_enabled()) {
+        // only the rotation angles are read (and checked) on this path
+        fill_stats(e.tpl, e.uses++ > 0, stats);
+        return run_small(s, e.tpl, values, basis);
+    }
     uint64_t bad = 0;
     for (int64_t i = 0; i < 3 * n_gates; ++i) {
         uint64_t b;
@@ -1136,11 +1149,6 @@ static int apply_prepared_impl(qsv_state *s, int64_t program_id, const double *v
         bad |= (uint64_t)(((b >> 52) & 0x7ffu) == 0x7ffu);
     }
     if (bad) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
-    QSV_CUDA(cudaSetDevice(s->device));
-    if (e.tpl.small.valid && small_enabled()) {
-        fill_stats(e.tpl, e.uses++ > 0, stats);
-        return run_small(s, e.tpl, values, basis);
-    }
     if (!plain_u3() && needs_plain_u3(e.tpl, values)) {
         PlainU3Scope plain;  // structure-cache path with a plan without normalised U3 forms
         return apply_gates_impl(s, n_gates, e.kinds.data(), e.qubits.data(), values, stats, basis);
@@ -1222,6 +1230,64 @@ int qsv_apply_pauli_rotations(qsv_state *s, int64_t n, const uint64_t *x, const 
     return QSV_OK;
 }
 
+// States of <= 12 qubits: one warp per string (qsv_small.cu), no sweep plan;
+// QSV_SMALL_EXPECT=0 takes the general sweeps (A/B and cross-checks).
+static bool small_expect_enabled()
+{
+    const char *e = getenv("QSV_SMALL_EXPECT");
+    return !(e && e[0] == '0');
+}
+
+static void finish_expectation(const std::vector<double> &vals, int64_t S, const double *coef_re,
+                               const double *coef_im, double *out_re, double *out_im, double *per_term)
+{
+    // term-order accumulation, as statevector.py:104-107
+    double re = 0.0, im = 0.0;
+    for (int64_t t = 0; t < S; ++t) {
+        re += coef_re[t] * vals[t];
+        if (coef_im) im += coef_im[t] * vals[t];
+    }
+    *out_re = re;
+    *out_im = im;
+    if (per_term) std::memcpy(per_term, vals.data(), (size_t)S * 8);
+}
+
+static int expectation_small(const qsv_state *s, DeviceCtx &c, int64_t S, const uint64_t *x, const uint64_t *y,
+                             const uint64_t *z, const double *coef_re, const double *coef_im, double *out_re,
+                             double *out_im, double *per_term, qsv_plan_stats *stats)
+{
+    Blob b;
+    const size_t o_r = b.add(nullptr, (size_t)S * 16);
+    uint32_t *rec = reinterpret_cast<uint32_t *>(b.bytes.data() + o_r);
+    for (int64_t t = 0; t < S; ++t) {
+        rec[4 * t + 0] = (uint32_t)(x[t] | y[t]);
+        rec[4 * t + 1] = (uint32_t)(y[t] | z[t]);
+        rec[4 * t + 2] = (uint32_t)(__builtin_popcountll(y[t]) & 3);
+        rec[4 * t + 3] = 0;
+    }
+    char *d = nullptr;
+    size_t scratch = 0;
+    if (int rc = upload_blob(c, s->stream, b, (size_t)S * 8 + 256, &d, &scratch)) return rc;
+    double *d_vals = (double *)(d + scratch);
+    QSV_CUDA(launch_expect_small(s->amps, s->n, (const uint32_t *)(d + o_r), (int)S, d_vals,
+                                 num_sms(s->device), s->stream));
+    if (int rc = ensure_stage(c, (size_t)S * 8)) return rc;
+    QSV_CUDA(cudaMemcpyAsync(c.h_stage, d_vals, (size_t)S * 8, cudaMemcpyDeviceToHost, s->stream));
+    QSV_CUDA(cudaStreamSynchronize(s->stream));
+    std::vector<double> vals(S);
+    std::memcpy(vals.data(), c.h_stage, (size_t)S * 8);
+    finish_expectation(vals, S, coef_re, coef_im, out_re, out_im, per_term);
+    qsv_plan_stats st{};
+    st.n_input_ops = S;
+    st.n_items = 1;
+    st.n_passes = 1;
+    st.tile_bits = s->n;
+    st.cache_hit = 1;
+    g_last_stats = st;
+    if (stats) *stats = st;
+    return QSV_OK;
+}
+
 int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint64_t *y,
                     const uint64_t *z, const double *coef_re, const double *coef_im,
                     double *out_re, double *out_im, double *per_term, qsv_plan_stats *stats)
@@ -1238,6 +1304,8 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
     QSV_CUDA(cudaSetDevice(s->device));
     DeviceCtx *c = nullptr;
     if (int rc = ctx_for(s->device, &c)) return rc;
+    if (s->n <= kSmallMaxQubits && small_expect_enabled())
+        return expectation_small(s, *c, S, x, y, z, coef_re, coef_im, out_re, out_im, per_term, stats);
 
     const uint64_t h = hash_masks(s->n, S, x, y, z);
     const bool jit = jit_enabled(s->n);
@@ -1350,15 +1418,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
     QSV_CUDA(cudaMemcpyAsync(c->h_stage, d_per_term, (size_t)S * 8, cudaMemcpyDeviceToHost, s->stream));
     QSV_CUDA(cudaStreamSynchronize(s->stream));
     std::memcpy(vals.data(), c->h_stage, (size_t)S * 8);
-    // term-order accumulation, as statevector.py:104-107
-    double re = 0.0, im = 0.0;
-    for (int64_t t = 0; t < S; ++t) {
-        re += coef_re[t] * vals[t];
-        if (coef_im) im += coef_im[t] * vals[t];
-    }
-    *out_re = re;
-    *out_im = im;
-    if (per_term) std::memcpy(per_term, vals.data(), (size_t)S * 8);
+    finish_expectation(vals, S, coef_re, coef_im, out_re, out_im, per_term);
     qsv_plan_stats st{};
     st.n_input_ops = S;
     st.n_items = (int64_t)plan->size();

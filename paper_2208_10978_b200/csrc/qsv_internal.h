@@ -244,6 +244,9 @@ cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram
                          const int32_t *meta, const double *theta, const int32_t *chunks, const uint32_t *xo,
                          const uint32_t *tab, cudaStream_t st);
 // dst (n_dst qubits) = the parity class cls embedded from its (n_dst-1)-qubit half
+// <P_t> of a state of <= 12 qubits, one warp per string (rec: 4 x u32 per string)
+cudaError_t launch_expect_small(const double2 *psi, int n, const uint32_t *rec, int S, double *out, int sms,
+                                cudaStream_t st);
 cudaError_t launch_embed_parity(double2 *dst, const double2 *src, int n_dst, uint64_t wlow, uint32_t cls,
                                 int sms, cudaStream_t st);
 cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,

@@ -162,3 +162,46 @@ def test_full_chunk_single_group(monkeypatch):
     ref = O.evolve(O.init_state("101000000"), circ.gates)
     assert np.abs(out - ref).max() <= AMP_TOL
     assert np.abs(out_passes - ref).max() <= AMP_TOL
+
+
+def test_non_finite_angle_rejected_on_small_path():
+    """The small-program path reads only the rotation angles of the gate list,
+    and a non-finite angle fails loudly (QSV_ERR_INVALID) instead of running."""
+    from paper_2208_10978_b200.circuit import bind
+
+    strings = W.ucc_rotation_strings(10, 5)[:40]
+    param = W.parametric_rotations_circuit(10, strings)
+    b = bind(param, np.full(len(strings), 0.1))
+    pid = b._plan.program_id()
+    k, q, vals = b.flat()
+    spans, _ = _lib.match_rotations(10, k, q)
+    s10 = sv.init_state("1111100000")
+    L = _lib.lib()
+    vals = vals.copy()
+    before = _lib.small_launches()
+    assert L.qsv_evolve_basis_prepared(s10.handle, 31, pid, _lib.dptr(vals), None) == 0
+    assert _lib.small_launches() == before + 1
+    vals[3 * int(spans[5][2])] = np.inf  # the angle of rotation 5
+    assert L.qsv_evolve_basis_prepared(s10.handle, 31, pid, _lib.dptr(vals), None) != 0
+    assert b"non-finite" in L.qsv_last_error()
+
+
+@pytest.mark.parametrize("n", [1, 6, 10, 12])
+def test_small_state_expectation_vs_oracle_and_sweeps(n, monkeypatch):
+    """States of <= 12 qubits take the one-launch expectation (a warp per
+    string, qsv_small.cu: expect_small_kernel): per-term <P_t> (every axis
+    mix, so all four i^ny phases) equal the CPU oracle's and the general
+    sweep path's (QSV_SMALL_EXPECT=0) on a random state.  Tolerance:
+    relative 1e-10 on the energy, 1e-12 absolute per term."""
+    rng = np.random.default_rng(n)
+    amps = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    amps /= np.linalg.norm(amps)
+    h = W.dense_random_hamiltonian(n, 300, rng)
+    s = sv.StateVector(n, amps)
+    re, im, per = sv.expectation_terms(s, h)
+    e_ref, per_ref = O.expectation(amps, h, n, per_term=True)
+    assert abs(re - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
+    assert np.abs(per - per_ref[:, 0]).max() <= 1e-12
+    monkeypatch.setenv("QSV_SMALL_EXPECT", "0")
+    re2, _, per2 = sv.expectation_terms(s, h)
+    assert np.abs(per - per2).max() <= 1e-12 and abs(re - re2) <= 1e-10 * max(1.0, abs(re))
