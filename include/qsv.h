@@ -224,6 +224,10 @@ int qsv_dist_download(qsv_dist *d, double *host);
  * (perm[q] = physical position of logical qubit q; any pointer may be NULL) */
 int qsv_dist_info(const qsv_dist *d, int *n_ranks, int *local_qubits, int64_t *relayouts,
                   int64_t *bytes_sent_per_rank, int32_t *perm);
+/* whether relayouts swap chunks in place over peer memory (every device pair
+ * can address the other, or shards share a device), and how many swap kernels
+ * have run; QSV_DIST_P2P=0 forces cudaMemcpyPeerAsync through staging */
+int qsv_dist_p2p_info(const qsv_dist *d, int *p2p, int64_t *swap_launches);
 
 /* Debug / test export: the specialised (NVRTC) source of tile pass `k` of the
  * plan for this gate list ("" for global / interpreted passes); host only. */

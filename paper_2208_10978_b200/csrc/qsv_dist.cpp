@@ -10,9 +10,13 @@
 // local-first light-cone scheduler (plan_segments) with qubit-swap relayouts
 // between them; expectation values are reduced over ranks in ascending order
 // (engine.py:199).  Shards are ordinary qsv_state handles, so every local pass
-// is the single-GPU engine; a relayout swaps contiguous chunks pairwise with
-// cudaMemcpyPeerAsync (NVLink / NVSwitch between devices, a device copy when
-// two ranks share a device) through a bounded staging piece.
+// is the single-GPU engine.  A relayout swaps contiguous chunks pairwise IN
+// PLACE over peer memory: a swap kernel reads and writes both chunks directly
+// (NVLink / NVSwitch P2P loads and stores; plain device memory when two ranks
+// share a device), each device of a pair swapping one half, ordered against
+// the shards' other work by events -- no staging copy, no host round trip.
+// Without peer access (or QSV_DIST_P2P=0) the swap falls back to
+// cudaMemcpyPeerAsync through a bounded staging piece.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,6 +40,9 @@ struct qsv_dist {
     std::vector<int> perm;            // logical qubit -> physical position
     std::vector<void *> staging;      // per rank: one piece on the rank's device
     size_t piece_bytes = 64u << 20;
+    bool p2p = false;                 // every pair of devices can address each other
+    std::vector<cudaEvent_t> ev_ready, ev_done;  // per rank: relayout ordering
+    int64_t swap_launches = 0;
     bool lazy = false;                // |basis> not yet materialised
     uint64_t basis = 0;
     int64_t relayouts = 0, bytes_sent = 0;  // per rank
@@ -196,7 +203,6 @@ int relayout(qsv_dist *d, const Relayout &rl)
 {
     const int k = (int)rl.S.size();
     if (k == 0) return QSV_OK;
-    if (int rc = sync_all(d)) return rc;
     const uint64_t chunk = 1ull << (d->n_local - k);
     auto s_value = [&](int r) {
         int v = 0;
@@ -208,6 +214,57 @@ int relayout(qsv_dist *d, const Relayout &rl)
         for (int i = 0; i < k; ++i) p = (p & ~(1 << rl.S[i])) | (((c >> i) & 1) << rl.S[i]);
         return p;
     };
+    const char *knob = getenv("QSV_DIST_P2P");
+    if (d->p2p && !(knob && knob[0] == '0')) {
+        // every shard's earlier work precedes any swap touching it: rank r's
+        // stream waits for the partners' ready events, swaps its half of
+        // each pair, and later work on r waits for the partners' done events
+        for (int r = 0; r < d->P; ++r) {
+            cudaSetDevice(d->devices[r]);
+            if (cudaEventRecord(d->ev_ready[r], d->shards[r]->stream) != cudaSuccess)
+                return fail_code(QSV_ERR_CUDA, "relayout event record failed");
+        }
+        for (int r = 0; r < d->P; ++r) {
+            qsv_state *A = d->shards[r];
+            cudaSetDevice(A->device);
+            const int rs = s_value(r);
+            for (int c = 0; c < (1 << k); ++c) {
+                if (c == rs) continue;
+                const int p = partner(r, c);
+                if (cudaStreamWaitEvent(A->stream, d->ev_ready[p], 0) != cudaSuccess)
+                    return fail_code(QSV_ERR_CUDA, "relayout event wait failed");
+            }
+            for (int c = 0; c < (1 << k); ++c) {
+                if (c == rs) continue;
+                const int p = partner(r, c);
+                // the pair {r, p}: r's chunk c <-> p's chunk rs; the lower
+                // rank swaps the first half, the higher one the second
+                const uint64_t half = chunk / 2;
+                const uint64_t off = p > r ? 0 : half, len = p > r ? half : chunk - half;
+                double2 *a = A->amps + (uint64_t)c * chunk + off;
+                double2 *b = d->shards[p]->amps + (uint64_t)rs * chunk + off;
+                if (launch_swap_chunks(a, b, len, num_sms(A->device), A->stream) != cudaSuccess)
+                    return fail_code(QSV_ERR_CUDA, "relayout swap kernel failed");
+                ++d->swap_launches;
+            }
+            if (cudaEventRecord(d->ev_done[r], A->stream) != cudaSuccess)
+                return fail_code(QSV_ERR_CUDA, "relayout event record failed");
+        }
+        for (int r = 0; r < d->P; ++r) {
+            qsv_state *A = d->shards[r];
+            cudaSetDevice(A->device);
+            const int rs = s_value(r);
+            for (int c = 0; c < (1 << k); ++c) {
+                if (c == rs) continue;
+                if (cudaStreamWaitEvent(A->stream, d->ev_done[partner(r, c)], 0) != cudaSuccess)
+                    return fail_code(QSV_ERR_CUDA, "relayout event wait failed");
+            }
+        }
+        ++d->relayouts;
+        d->bytes_sent += (int64_t)(16 * chunk) * ((1 << k) - 1);
+        return QSV_OK;
+    }
+    if (int rc = sync_all(d)) return rc;
     for (int r = 0; r < d->P; ++r) {
         const int rs = s_value(r);
         for (int c = 0; c < (1 << k); ++c) {
@@ -324,9 +381,20 @@ int qsv_dist_create(qsv_dist **out, int n_qubits, int n_ranks, const int *device
             return fail_code(QSV_ERR_NOMEM, "relayout staging allocation failed");
         }
         d->staging.push_back(stg);
+        cudaEvent_t e1 = nullptr, e2 = nullptr;
+        if (cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            qsv_dist_destroy(d);
+            return fail_code(QSV_ERR_CUDA, "relayout event creation failed");
+        }
+        d->ev_ready.push_back(e1);
+        d->ev_done.push_back(e2);
     }
-    // peer access between distinct devices (NVLink / NVSwitch); without it
+    // peer access between distinct devices (NVLink / NVSwitch): the swap
+    // kernels address the partner's shard directly; without it
     // cudaMemcpyPeerAsync still works, staged by the driver
+    d->p2p = true;
     for (int a : d->devices)
         for (int b : d->devices)
             if (a != b && !peer_done.count({a, b})) {
@@ -335,7 +403,11 @@ int qsv_dist_create(qsv_dist **out, int n_qubits, int n_ranks, const int *device
                 cudaDeviceCanAccessPeer(&can, a, b);
                 if (can) {
                     cudaSetDevice(a);
-                    if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) d->p2p = false;
+                    cudaGetLastError();
+                } else {
+                    d->p2p = false;
                 }
             }
     *out = d;
@@ -350,6 +422,11 @@ int qsv_dist_destroy(qsv_dist *d)
     for (size_t r = 0; r < d->staging.size(); ++r) {
         cudaSetDevice(d->devices[r]);
         cudaFree(d->staging[r]);
+    }
+    for (size_t r = 0; r < d->ev_ready.size(); ++r) {
+        cudaSetDevice(d->devices[r]);
+        cudaEventDestroy(d->ev_ready[r]);
+        cudaEventDestroy(d->ev_done[r]);
     }
     delete d;
     return QSV_OK;
@@ -509,6 +586,15 @@ int qsv_dist_download(qsv_dist *d, double *host)
         host[2 * i] = phys[2 * p];
         host[2 * i + 1] = phys[2 * p + 1];
     }
+    return QSV_OK;
+}
+
+int qsv_dist_p2p_info(const qsv_dist *d, int *p2p, int64_t *swap_launches)
+{
+    std::lock_guard<std::recursive_mutex> lk(d_mu);
+    if (!d) return fail_code(QSV_ERR_INVALID, "null handle");
+    if (p2p) *p2p = d->p2p ? 1 : 0;
+    if (swap_launches) *swap_launches = d->swap_launches;
     return QSV_OK;
 }
 

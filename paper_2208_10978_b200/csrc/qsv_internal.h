@@ -249,6 +249,8 @@ cudaError_t launch_expect_small(const double2 *psi, int n, const uint32_t *rec, 
                                 cudaStream_t st);
 cudaError_t launch_embed_parity(double2 *dst, const double2 *src, int n_dst, uint64_t wlow, uint32_t cls,
                                 int sms, cudaStream_t st);
+// a[i] <-> b[i] (i < n) over peer memory: the relayout exchange of qsv_dist.cpp
+cudaError_t launch_swap_chunks(double2 *a, double2 *b, uint64_t n, int sms, cudaStream_t st);
 cudaError_t launch_axpby(double2 *y, const double2 *x, uint64_t dim, double are, double aim,
                          double bre, double bim, cudaStream_t st);
 

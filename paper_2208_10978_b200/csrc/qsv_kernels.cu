@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "qsv_internal.h"
 
 namespace qsv {
@@ -725,6 +727,48 @@ cudaError_t launch_reduce_columns(const double *partial, int rows, int cols, con
 {
     if (cols <= 0) return cudaSuccess;
     reduce_columns_kernel<<<(cols + 31) / 32, 1024, 0, st>>>(partial, rows, cols, d_map, out);
+    return cudaGetLastError();
+}
+
+// Relayout chunk swap over peer memory (qsv_dist.cpp): a[i] <-> b[i] for
+// i < n, where b may live on another GPU (NVLink / NVSwitch P2P loads and
+// stores; the same device when two shards share one).  Each element is read
+// once and written once on each side -- no staging copy -- and the two
+// devices of a pair each run the swap on one half, so both directions of the
+// link and both GPUs' load/store units are busy.  Four 16-B elements per
+// thread are in flight before any store (peer latency ~1-2 us).
+__global__ void __launch_bounds__(256) swap_chunks_kernel(double2 *__restrict__ a, double2 *__restrict__ b,
+                                                          uint64_t n)
+{
+    constexpr int U = 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < n; i += U * stride) {
+        double2 va[U], vb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            va[u] = __ldcs(a + i + u * stride);
+            vb[u] = __ldcs(b + i + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            __stcs(a + i + u * stride, vb[u]);
+            __stcs(b + i + u * stride, va[u]);
+        }
+    }
+    for (; i < n; i += stride) {
+        const double2 va = __ldcs(a + i), vb = __ldcs(b + i);
+        __stcs(a + i, vb);
+        __stcs(b + i, va);
+    }
+}
+
+cudaError_t launch_swap_chunks(double2 *a, double2 *b, uint64_t n, int sms, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    const uint64_t want = (n + 255) / 256;
+    const int grid = (int)std::min<uint64_t>(want, (uint64_t)sms * 8);
+    swap_chunks_kernel<<<grid, 256, 0, st>>>(a, b, n);
     return cudaGetLastError();
 }
 

@@ -70,8 +70,11 @@ class MultiDeviceState:
         perm = np.zeros(self.n_qubits, dtype=np.int32)
         _lib.check(_lib.lib().qsv_dist_info(self._h, ctypes.byref(P), ctypes.byref(nl), ctypes.byref(rel),
                                             ctypes.byref(sent), _lib.i32ptr(perm)))
+        p2p, swaps = ctypes.c_int(), ctypes.c_int64()
+        _lib.check(_lib.lib().qsv_dist_p2p_info(self._h, ctypes.byref(p2p), ctypes.byref(swaps)))
         return {"ranks": P.value, "local_qubits": nl.value, "relayouts": rel.value,
-                "bytes_sent_per_rank": sent.value, "perm": perm.tolist()}
+                "bytes_sent_per_rank": sent.value, "perm": perm.tolist(),
+                "p2p": bool(p2p.value), "swap_launches": swaps.value}
 
 
 class MultiDeviceBackend:

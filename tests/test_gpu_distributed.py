@@ -182,11 +182,15 @@ def test_config5_structure_29q_one_state_of_memory(D):
 
 
 @pytest.mark.parametrize("P,n,layers", [(2, 14, 6), (4, 16, 5), (8, 18, 4)])
-def test_native_multidevice_brickwork_vs_oracle(P, n, layers):
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_native_multidevice_brickwork_vs_oracle(P, n, layers, p2p, monkeypatch):
     """qsv_dist (C++ planner + relayouts, P shards on device 0) vs the oracle;
-    the 20-layer light cone needs few relayouts."""
+    the 20-layer light cone needs few relayouts.  Relayouts run as in-place
+    swap kernels over peer memory (event-ordered, each rank of a pair swapping
+    one half) or, with QSV_DIST_P2P=0, as staged cudaMemcpyPeerAsync."""
     from paper_2208_10978_b200.multidevice import MultiDeviceState
 
+    monkeypatch.setenv("QSV_DIST_P2P", p2p)
     circ = W.brickwork(n, layers, seed=40 + P)
     st = MultiDeviceState(n, [0] * P)
     st.set_basis(0)
@@ -195,6 +199,8 @@ def test_native_multidevice_brickwork_vs_oracle(P, n, layers):
     assert np.abs(st.amplitudes - ref).max() < 1e-10
     info = st.info()
     assert info["ranks"] == P and info["relayouts"] >= 1
+    assert info["p2p"]  # shards sharing a device address each other
+    assert (info["swap_launches"] > 0) == (p2p == "1")
     # the C++ scheduler is the Python one (distributed.plan_segments): same
     # relayouts and the same final qubit map
     from paper_2208_10978_b200 import distributed as Dm
