@@ -70,6 +70,20 @@ int qsv_mem_info(int device, uint64_t *free_bytes, uint64_t *total_bytes);
 int qsv_create(qsv_state **out, int n_qubits, int device);
 int qsv_destroy(qsv_state *s);
 int qsv_n_qubits(const qsv_state *s, int *out);
+/* Cross-process relayout exchange (replaces the NCCL chunk send/recv of the
+ * reference-free sharded path, distributed.py; the reference itself has no
+ * sharding -- SPEC.md:398).  qsv_ipc_get_handle exports the state's device
+ * buffer (QSV_IPC_HANDLE_BYTES bytes); a partner process maps it with
+ * qsv_ipc_open and swaps chunks in place with qsv_swap_peer (amplitude
+ * offsets, n amplitudes; the peer range is the caller's to keep in bounds and
+ * ordered against the peer's own work).  qsv_swap_info: swap kernels run. */
+#define QSV_IPC_HANDLE_BYTES 64
+int qsv_ipc_get_handle(const qsv_state *s, void *handle);
+int qsv_ipc_open(int device, const void *handle, void **peer_base);
+int qsv_ipc_close(int device, void *peer_base);
+int qsv_swap_peer(qsv_state *s, uint64_t local_offset, void *peer_base, uint64_t peer_offset, uint64_t n);
+int qsv_swap_info(int64_t *launches);
+
 /* qsv_set_stream: order this state's later work after everything already
  * queued on cuda_stream (an event fence; NULL = no-op).  Library work still
  * runs on the device's library stream, returned by qsv_get_stream -- wait on

@@ -56,7 +56,8 @@ EXPORTED = (
     "qsv_jit_info", "qsv_small_info", "qsv_embed_parity", "qsv_rotation_adjoint", "qsv_prepare_gates", "qsv_apply_prepared",
     "qsv_release_program", "qsv_evolve_basis", "qsv_evolve_basis_prepared",
     "qsv_last_plan_stats", "qsv_dist_create", "qsv_dist_destroy", "qsv_dist_set_basis",
-    "qsv_dist_apply_gates", "qsv_dist_expectation", "qsv_dist_download", "qsv_dist_info", "qsv_dist_p2p_info",
+    "qsv_dist_apply_gates", "qsv_dist_expectation", "qsv_dist_download", "qsv_dist_info", "qsv_dist_p2p_info", "qsv_ipc_get_handle",
+    "qsv_ipc_open", "qsv_ipc_close", "qsv_swap_peer", "qsv_swap_info",
 )
 
 _lib = None
@@ -79,6 +80,11 @@ def _declare(L):
         "qsv_dist_apply_gates": ([vp, i64, i32p, i32p, dp], ctypes.c_int),
         "qsv_dist_expectation": ([vp, i64, u64p, u64p, u64p, dp, dp, dp, dp], ctypes.c_int),
         "qsv_dist_download": ([vp, vp], ctypes.c_int),
+        "qsv_ipc_get_handle": ([vp, ctypes.c_void_p], ctypes.c_int),
+        "qsv_ipc_open": ([ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+        "qsv_ipc_close": ([ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+        "qsv_swap_peer": ([vp, u64, ctypes.c_void_p, u64, u64], ctypes.c_int),
+        "qsv_swap_info": ([ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_dist_p2p_info": ([vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64)], ctypes.c_int),
         "qsv_dist_info": ([vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                            ctypes.POINTER(i64), ctypes.POINTER(i64), i32p], ctypes.c_int),

@@ -741,6 +741,71 @@ int qsv_n_qubits(const qsv_state *s, int *out)
 // Every state keeps the device's library stream (shared scratch, pinned
 // staging and __constant__ banks are ordered by it); a caller's stream is
 // joined by an event fence instead of replacing it.
+static int64_t g_swap_launches = 0;  // qsv_swap_peer kernels
+
+// ---- cross-process relayouts (distributed.py over torch.distributed) --------
+// A rank exports its shard with a CUDA IPC handle; its partners map it and
+// swap chunks with it in place through the same swap kernel as qsv_dist
+// (NVLink / NVSwitch P2P between GPUs of one node; plain device memory when
+// two processes share a GPU).  The caller orders the swap against the
+// partner's work (distributed.py: stream sync + barrier on both sides).
+
+int qsv_ipc_get_handle(const qsv_state *s, void *handle)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (!handle) return fail_code(QSV_ERR_INVALID, "null handle buffer");
+    QSV_CUDA(cudaSetDevice(s->device));
+    cudaIpcMemHandle_t h;
+    QSV_CUDA(cudaIpcGetMemHandle(&h, s->amps));
+    static_assert(sizeof(h) == QSV_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof(h));
+    return QSV_OK;
+}
+
+int qsv_ipc_open(int device, const void *handle, void **peer_base)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!handle || !peer_base) return fail_code(QSV_ERR_INVALID, "null argument");
+    *peer_base = nullptr;
+    QSV_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    QSV_CUDA(cudaIpcOpenMemHandle(peer_base, h, cudaIpcMemLazyEnablePeerAccess));
+    return QSV_OK;
+}
+
+int qsv_ipc_close(int device, void *peer_base)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!peer_base) return QSV_OK;
+    QSV_CUDA(cudaSetDevice(device));
+    QSV_CUDA(cudaIpcCloseMemHandle(peer_base));
+    return QSV_OK;
+}
+
+int qsv_swap_peer(qsv_state *s, uint64_t local_offset, void *peer_base, uint64_t peer_offset, uint64_t n)
+{
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (int rc = check_state(s)) return rc;
+    if (!peer_base) return fail_code(QSV_ERR_INVALID, "null peer pointer");
+    if (local_offset > s->dim || n > s->dim - local_offset)
+        return fail_code(QSV_ERR_INVALID, "swap range outside the state");
+    QSV_CUDA(cudaSetDevice(s->device));
+    if (int rc = settle(s)) return rc;
+    QSV_CUDA(launch_swap_chunks(s->amps + local_offset, (double2 *)peer_base + peer_offset, n,
+                                num_sms(s->device), s->stream));
+    ++g_swap_launches;
+    return QSV_OK;
+}
+
+int qsv_swap_info(int64_t *launches)
+{
+    if (!launches) return fail_code(QSV_ERR_INVALID, "null output");
+    *launches = g_swap_launches;
+    return QSV_OK;
+}
+
 int qsv_set_stream(qsv_state *s, void *stream)
 {
     std::lock_guard<std::recursive_mutex> lk(g_mu);

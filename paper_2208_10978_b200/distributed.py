@@ -43,6 +43,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -145,6 +146,33 @@ class CudaEngine:
 
     def download(self, shard) -> np.ndarray:
         return shard.amplitudes
+
+
+# ---------------------------------------------------------------------------
+# peer shards mapped through CUDA IPC (cross-process relayouts)
+# ---------------------------------------------------------------------------
+
+_IPC_MAPS: "dict[tuple[int, bytes], int]" = {}
+_IPC_MAX = 16
+
+
+def _ipc_map(device: int, handle: bytes) -> int:
+    """Device pointer of a partner's shard (qsv_ipc_open), cached by handle;
+    the oldest mappings are closed beyond _IPC_MAX."""
+    from . import _lib
+
+    key = (device, handle)
+    base = _IPC_MAPS.get(key)
+    if base is None:
+        ptr = ctypes.c_void_p()
+        _lib.check(_lib.lib().qsv_ipc_open(device, handle, ctypes.byref(ptr)))
+        base = ptr.value
+        if len(_IPC_MAPS) >= _IPC_MAX:
+            (d0, _), old = next(iter(_IPC_MAPS.items()))
+            _IPC_MAPS.pop(next(iter(_IPC_MAPS)))
+            _lib.lib().qsv_ipc_close(d0, ctypes.c_void_p(old))
+        _IPC_MAPS[key] = base
+    return base
 
 
 # ---------------------------------------------------------------------------
@@ -637,7 +665,9 @@ class DistStateVector:
                         self._swap_local(views[r], views[p], c * chunk, rs * chunk, chunk)
                 else:
                     remote.setdefault(r, []).append((c, p))
-        if remote:
+        if remote and self._ipc_enabled():
+            self._ipc_exchange(remote, chunk, s_value)
+        elif remote:
             self._p2p_exchange(views, remote, chunk)
         self._sync_after(views)
         self.stats["relayouts"] += 1
@@ -661,6 +691,43 @@ class DistStateVector:
 
     def comm_piece_bytes(self) -> int:
         return int(getattr(self.comm, "piece_bytes", 256 << 20))
+
+    def _ipc_enabled(self) -> bool:
+        """Device shards in several processes of one node: swap chunks in
+        place over peer memory (CUDA IPC + swap kernel) instead of NCCL
+        send/recv through staging.  QSV_DIST_IPC=0 keeps the NCCL path."""
+        return (isinstance(self.engine, CudaEngine) and isinstance(self.comm, ProcessGroupComm)
+                and os.environ.get("QSV_DIST_IPC", "1") != "0")
+
+    def _ipc_exchange(self, remote, chunk, s_value) -> None:
+        """Pairwise in-place chunk swap over peer memory: every rank exports
+        its shard (qsv_ipc_get_handle), maps its partners' (qsv_ipc_open,
+        cached) and swaps its half of each pair with the swap kernel
+        (qsv_swap_peer: the lower rank the first half, the higher the second),
+        so each byte is read and written once per side with no staging copy
+        and both directions of every link busy.  Ordering: every rank drains
+        its stream and meets the others at a barrier before any swap, and
+        again after its own swaps -- no kernel ever waits on another rank."""
+        from . import _lib
+
+        r = self.comm.rank
+        shard = self.shards[r]
+        L = _lib.lib()
+        h = (ctypes.c_char * 64)()
+        _lib.check(L.qsv_ipc_get_handle(shard.handle, h))
+        handles = self.comm.gather_arrays({r: bytes(h)})
+        shard.synchronize()
+        self.comm.barrier()  # every shard's earlier work is done
+        rs = s_value(r)
+        half = chunk // 2
+        for c, p in remote[r]:
+            base = _ipc_map(self.engine.device, handles[p])
+            off, ln = (0, half) if p > r else (half, chunk - half)
+            _lib.check(L.qsv_swap_peer(shard.handle, c * chunk + off, ctypes.c_void_p(base),
+                                       rs * chunk + off, ln))
+            self.stats["ipc_swaps"] = self.stats.get("ipc_swaps", 0) + 1
+        shard.synchronize()
+        self.comm.barrier()  # every half of every pair is swapped
 
     def _p2p_exchange(self, views, remote, chunk):
         """Pairwise chunk swap with the remote partners, one bounded piece at

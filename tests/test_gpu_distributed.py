@@ -71,18 +71,22 @@ def _pg_worker(rank, world, port, q):
         rng = np.random.default_rng(13)
         h = W.sparse_random_hamiltonian(n, 150, rng, z_only=40)
         e = be.expectation(psi, h)
-        q.put((rank, psi.amplitudes(), e, psi.stats["relayouts"]))
+        q.put((rank, psi.amplitudes(), e, psi.stats["relayouts"], psi.stats.get("ipc_swaps", 0)))
     finally:
         dist.destroy_process_group()
 
 
-def test_process_group_sharded_on_device(D):
-    """ProcessGroupComm + CudaEngine across 2 processes (gloo, shards staged
-    through host memory, both on this GPU): the multi-process plumbing of the
-    sharded path against the oracle."""
+@pytest.mark.parametrize("ipc", ["1", "0"])
+def test_process_group_sharded_on_device(D, ipc, monkeypatch):
+    """ProcessGroupComm + CudaEngine across 2 processes (gloo plumbing, both
+    on this GPU): the multi-process sharded path against the oracle, with the
+    relayout chunks swapped in place over CUDA IPC peer memory (default) or,
+    with QSV_DIST_IPC=0, sent through host staging."""
     import socket
 
     import torch.multiprocessing as mp
+
+    monkeypatch.setenv("QSV_DIST_IPC", ipc)
 
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -103,10 +107,11 @@ def test_process_group_sharded_on_device(D):
     rng = np.random.default_rng(13)
     h = W.sparse_random_hamiltonian(n, 150, rng, z_only=40)
     e_ref = O.expectation(ref, h, n)
-    for rank, amps, e, nrel in res:
+    for rank, amps, e, nrel, nswap in res:
         assert np.abs(amps - ref).max() < 1e-10
         assert abs(e - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
         assert nrel >= 1
+        assert (nswap > 0) == (ipc == "1")
 
 
 @pytest.mark.parametrize("P", [2, 8])
