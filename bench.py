@@ -11,17 +11,20 @@ Prints ONE JSON line (rank 0).  value = amplitude-updates/s (sum over the 830
 gates of 2^n, per second, whole job); e2e = the same metric through the public
 backend API with host buffers (gate arrays in, full amplitude vector out to
 pinned host memory) inside the timed region.  roofline = the dominant kernel
-(tile_block_kernel): algorithmic 32 B x 2^n per launch over its average launch
-duration (CUDA events on the library's stream), vs MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline = the reference (oracle/_ref: vqekit + Cython kernels, 1 thread --
-the reference evolve is single-threaded) on a bounded sample of the same
-circuit.
+(qsv_pass, the NVRTC-specialised tile pass): FP64-bound, achieved FP64 TFLOP/s
+of the instructions it executes (ncu counts) over the step time, vs the
+MEASURED DFMA peak (tools/peaks_probe.cu), with the HBM view beside it.
+cpu_baseline = the reference (oracle/_ref: vqekit + Cython kernels) on all
+host cores, a gate sample with the circuit's U3:CNOT mix.  --extra adds
+configs 1 / 3 / 4, the 30 q fused-gate roofline and the 33 q weak-scaling base.
 
-For N > 1 (torchrun, one rank per GPU, NCCL) the line measures the SHARDED
-engine (distributed.py): the same brickwork family on n = 28 + log2(N)
-qubits, so every GPU holds 2^28 amplitudes (weak scaling, SURVEY.md 8(e));
-gates on the top log2(N) (global) qubits trigger batched qubit-swap
-relayouts over NCCL.  value = total amplitude-updates/s of the whole job.
+For N > 1 (torchrun, one rank per GPU) the line measures the SHARDED engine
+(distributed.py) on the config-5 family: n = 33 + log2(N) qubits, 2^33
+amplitudes (128 GiB) per GPU (weak scaling; config 5 itself at N = 8).
+Relayouts swap chunks in place over peer memory (CUDA IPC mapping of the
+partner's shard + swap kernel, each rank one half of a pair); NCCL carries the
+plumbing (barriers, handle and partial gathers).  value = total
+amplitude-updates/s of the whole job.
 """
 
 from __future__ import annotations
@@ -795,6 +798,16 @@ def run_engine(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def _swap_launches() -> int:
+    import ctypes
+
+    from paper_2208_10978_b200 import _lib
+
+    v = ctypes.c_int64()
+    _lib.check(_lib.lib().qsv_swap_info(ctypes.byref(v)))
+    return v.value
+
+
 def nvlink_alltoall_probe(local: int, nbytes: int = 1 << 30, iters: int = 5) -> dict:
     """Measured all-to-all bandwidth between the ranks (torch.distributed
     all_to_all_single over NCCL): bytes each GPU sends to the others per
@@ -860,6 +873,7 @@ def run_engine_dist(args, rank, world, local):
     dist.barrier()
     torch.cuda.synchronize(local)
     _, launches0 = _lib.jit_info()
+    swaps0 = _swap_launches()
     with ClockSampler(local) as clocks:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -878,6 +892,7 @@ def run_engine_dist(args, rank, world, local):
         end.record()
         torch.cuda.synchronize(local)
     _, launches1 = _lib.jit_info()
+    swaps1 = _swap_launches()
     t_step = start.elapsed_time(end) / 1e3 / args.steps
     dev_t = "cuda" if args.dist_backend == "nccl" else "cpu"
     tt = torch.tensor([t_step, relayout_s / args.steps], device=dev_t)
@@ -966,7 +981,8 @@ def run_engine_dist(args, rank, world, local):
                          "kernel": "qsv_pass (tile passes between relayouts)",
                          "passes_per_step": passes, "peak_source": peak_kind,
                          "note": "32 B x 2^n_local per pass over the step time minus relayout time"},
-            "gpu_launches": int(launches1 - launches0),
+            "gpu_launches": int(launches1 - launches0) + int(swaps1 - swaps0),
+            "gpu_launches_note": "specialised tile passes + relayout swap kernels over peer memory (qsv_swap_peer)",
             "clocks": clocks.summary(),
         }
         if ucc is not None:
