@@ -1000,7 +1000,7 @@ static int small_dev_copy(const SmallProgram &sp, int device, const SmallProgram
     d->device = device;
     d->o_groups = b.add(sp.groups.data(), sp.groups.size() * sizeof(SmallGroup));
     d->o_meta = b.add(sp.meta.data(), sp.meta.size() * sizeof(int32_t));
-    d->o_chunks = b.add(sp.chunks.data(), sp.chunks.size() * sizeof(int32_t));
+    d->o_runs = b.add(sp.runs.data(), sp.runs.size() * sizeof(int32_t));
     d->o_xo = b.add(sp.xo.data(), sp.xo.size() * sizeof(uint32_t));
     d->o_tab = b.add(sp.tab.data(), sp.tab.size() * sizeof(uint32_t));
     if (cudaMalloc(&d->base, b.bytes.size()) != cudaSuccess) {
@@ -1038,7 +1038,7 @@ static int run_small(qsv_state *s, const ProgramTemplate &t, const double *value
     const char *k = dc->base;
     QSV_CUDA(launch_small(s->amps, s->n, basis, sp, (const SmallGroup *)(k + dc->o_groups),
                           (const int32_t *)(k + dc->o_meta), (const double *)(d + o_t),
-                          (const int32_t *)(k + dc->o_chunks), (const uint32_t *)(k + dc->o_xo),
+                          (const int32_t *)(k + dc->o_runs), (const uint32_t *)(k + dc->o_xo),
                           (const uint32_t *)(k + dc->o_tab), s->stream));
     ++g_small_launches;
     return QSV_OK;
@@ -1871,8 +1871,8 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
     j += "],\"tab\":[";
     for (size_t i = 0; emit_tab && i < t.small.tab.size(); ++i)
         j += (i ? "," : "") + std::to_string(t.small.tab[i]);
-    j += "],\"chunks\":[";
-    for (size_t i = 0; i < t.small.chunks.size(); ++i) j += (i ? "," : "") + std::to_string(t.small.chunks[i]);
+    j += "],\"runs\":[";
+    for (size_t i = 0; i < t.small.runs.size(); ++i) j += (i ? "," : "") + std::to_string(t.small.runs[i]);
     j += "]},\"passes\":[";
     char buf[256];
     for (size_t k = 0; k < t.passes.size(); ++k) {

@@ -241,7 +241,7 @@ struct SmallGroup;    // qsv_planner.h
 struct SmallProgram;  // qsv_planner.h
 // Small-state rotation program: one CTA, state in shared memory (qsv_small.cu).
 cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram &sp, const SmallGroup *groups,
-                         const int32_t *meta, const double *theta, const int32_t *chunks, const uint32_t *xo,
+                         const int32_t *meta, const double *theta, const int32_t *runs, const uint32_t *xo,
                          const uint32_t *tab, cudaStream_t st);
 // dst (n_dst qubits) = the parity class cls embedded from its (n_dst-1)-qubit half
 // <P_t> of a state of <= 12 qubits, one warp per string (rec: 4 x u32 per string)

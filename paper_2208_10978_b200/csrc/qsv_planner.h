@@ -122,7 +122,7 @@ struct SmallProgram {
     std::vector<SmallGroup> groups;
     std::vector<int32_t> meta;    // per rotation: ny mod 4 | (ny odd) << 2 | coordinates << 3
     std::vector<int32_t> src;     // per rotation: its angle is values[3 * src]
-    std::vector<int32_t> chunks;  // [g0, g1) group ranges sized for the shared-memory tables
+    std::vector<int32_t> runs;    // [g0, g1) warp runs (each ends with a CTA barrier)
     // Per-thread addressing, resolved on the host once per structure so the
     // kernel's per-group body is loads, FP64 and stores only:
     //   tab[((g << ncls) | class) * nthr + t] = byte slot of the thread's first
@@ -132,12 +132,12 @@ struct SmallProgram {
     int nthr = 0;
     std::vector<uint32_t> tab;
     std::vector<uint32_t> xo;
-    // device copy of the structure-only arrays (groups, meta, chunks, xo,
+    // device copy of the structure-only arrays (groups, meta, runs, xo,
     // tab), uploaded on first use per device; angles go up per evolve
     struct DevCopy {
         int device = -1;
         char *base = nullptr;
-        size_t o_groups = 0, o_meta = 0, o_chunks = 0, o_xo = 0, o_tab = 0;
+        size_t o_groups = 0, o_meta = 0, o_runs = 0, o_xo = 0, o_tab = 0;
         ~DevCopy();
     };
     mutable std::vector<std::shared_ptr<DevCopy>> dev;

@@ -23,9 +23,8 @@
 // 8 configs' matrices M are built, and g = -1 negates the off-diagonals at use
 // (sign-bit XORs).  A pair's config is linear in its pair index p, so the pairs
 // lo0 ^ span(lu0, lu1) for lu in the null space of the four parity masks all
-// share lo0's config (SmallGroup.lu).  The matrices of a chunk of groups are
-// built by the CTA itself at the start of the chunk from the raw angles
-// (sincos on device).
+// share lo0's config (SmallGroup.lu).  The matrices are built on the device
+// from the raw angles (sincos) by builder warps, one run ahead of use.
 //
 // Warp runs: inside a run of consecutive groups every warp stays in one coset
 // of an 8-dimensional subspace holding the run's flips and share vectors, so
@@ -56,10 +55,10 @@
 
 namespace qsv {
 
-// Shared-memory budget per chunk (the state takes 2^n x 16 B <= 64 KiB).
-constexpr int kSmallChunkRots = 2048;  // angles: 32 KiB of (cos, sin)
-constexpr int kSmallChunkGroups = 144;  // matrices: 144 x 8 configs x 80 B = 90 KiB (the group sign g
-                                        // is applied at use: D M D only negates the off-diagonals)
+// Shared-memory budget (the state takes 2^n x 16 B <= 64 KiB).
+constexpr int kSmallRunRots = 2048;   // angles of one run: 32 KiB of (cos, sin) + 8 KiB of meta
+constexpr int kSmallRunGroups = 48;   // matrices of one run: 48 x 8 configs x 80 B = 30 KiB, double-buffered
+                                      // (the group sign g is applied at use: D M D only negates the off-diagonals)
 constexpr int kRing = 8;               // table ring slots (per-thread entries of upcoming groups)
 constexpr int kAhead = 6;              // table entries in flight ahead of use
 constexpr int kRow = 5;                // double2 per matrix row (4 used; 80 B spreads rows over banks)
@@ -236,27 +235,16 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
     sp.ncls = ncls;
     sp.share = share;
     for (int i = 0; i < ncls; ++i) sp.w[i] = W[i];
-    // chunks of groups whose angles and matrices fit the shared tables
-    int g0 = 0;
     const int ng = (int)sp.groups.size();
-    while (g0 < ng) {
-        int g1 = g0;
-        while (g1 < ng && g1 - g0 < kSmallChunkGroups &&
-               sp.groups[g1].r1 - sp.groups[g0].r0 <= kSmallChunkRots)
-            ++g1;
-        if (g1 == g0) return false;  // one group alone exceeds the table (> 2048 rotations)
-        sp.chunks.push_back(g0);
-        sp.chunks.push_back(g1);
-        g0 = g1;
-    }
     // Warp runs.  Per class the CTA holds 2^(n - ncls) amplitudes; every
     // group of a run is applied with each warp confined to one coset of an
     // 8-dimensional subspace V of the class (256 amplitudes: 32 lanes x 4
     // pairs) that contains the run's flips and each group's two share
     // vectors, so inside a run a warp only ever touches its own amplitudes
     // and the groups are separated by __syncwarp; one CTA barrier ends the
-    // run (and every chunk).  Runs are grown greedily while V stays at <= 8
-    // dimensions.
+    // run.  Runs are grown greedily while V stays at <= 8 dimensions and the
+    // run's matrices and angles fit their shared-memory buffers (the builder
+    // warp prepares run r + 1 while the others apply run r).
     const int dimE = n - ncls;
     std::vector<uint32_t> E;  // the class direction space (functionals vanish)
     for (uint32_t v = 0; v < (1u << n); ++v) {
@@ -291,13 +279,15 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
     std::vector<uint32_t> cls_of(1u << n, 0);
     for (uint32_t i = 0; i < (1u << n); ++i)
         for (int k = 0; k < ncls; ++k) cls_of[i] |= parity32(i & W[k]) << k;
-    for (size_t ci = 0; ci < sp.chunks.size(); ci += 2) {
-        const int c0 = sp.chunks[ci], c1 = sp.chunks[ci + 1];
-        int g = c0;
+    {
+        const int c1 = ng;
+        int g = 0;
         while (g < c1) {
+            if (sp.groups[g].r1 - sp.groups[g].r0 > kSmallRunRots) return false;  // one group's angles exceed the buffer
             Gf2Span V;
             int gg = g;
             for (; gg < c1; ++gg) {
+                if (gg - g >= kSmallRunGroups || sp.groups[gg].r1 - sp.groups[g].r0 > kSmallRunRots) break;
                 Gf2Span V1 = V;
                 V1.add(sp.groups[gg].xm);
                 bool ok = V1.d <= 8;
@@ -424,6 +414,8 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
                     }
                 }
             }
+            sp.runs.push_back(g);
+            sp.runs.push_back(gg);
             g = gg;
         }
     }
@@ -470,40 +462,104 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c)
 }
 
 constexpr int kMaxThreads = 512;
+constexpr int kBuilders = 4;  // builder warps (A/B under ncu, config 1: 2 -> 151 us, 4 -> 141 us, 8 -> 149 us)
 
-// One CTA of (pairs in a class) / 4 threads; per group every thread applies
-// the group's matrix for its config to the 4 pairs p0 ^ span(lu0, lu1) of
-// each class this evolve can reach.  The thread -> pair map is the host's
-// table (SmallProgram::tab: first low slot | config << 16), read one item
-// ahead of use; the other slots are that slot XOR the group's constants
-// (small_slot is linear), so the per-group body is 4 matrix loads, 8
-// amplitude loads, 64 FP64, 8 stores and one barrier.  The chunk's group
-// records (for the matrix build) and slot constants sit in shared memory.
+// One CTA of nthr = (pairs in a class) / 4 compute threads plus kBuilders
+// builder warps.  Runs alternate between two shared-memory buffers: while the compute
+// warps apply run r (matrices and slot constants in buffer r & 1), the
+// builder warps prepare run r + 1 in the other buffer -- angles and meta
+// staged from global, sincos, the 8 configs' fused matrices per group -- and
+// one CTA barrier per run hands the buffers over.  Per group every compute
+// thread applies the group's matrix for its config to the 4 pairs
+// lo0 ^ span(lu0, lu1) of each class this evolve can reach; the thread ->
+// pair map is the host's table (SmallProgram::tab: first low slot | config
+// << 16), streamed kAhead items ahead through a shared-memory ring; the other
+// slots are that slot XOR the group's constants (small_slot is linear).
+// Inside a run each warp stays in its own coset, so groups are separated by
+// __syncwarp only.
 template <int NC>
-__global__ void __launch_bounds__(kMaxThreads, 1)
+__global__ void __launch_bounds__(kMaxThreads + 32 * kBuilders, 1)
 small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGroup *__restrict__ groups,
                  const int32_t *__restrict__ meta, const double *__restrict__ theta,
-                 const int32_t *__restrict__ chunks, int nchunks, const uint4 *__restrict__ xo,
-                 const uint32_t *__restrict__ tab, uint32_t cls0, uint32_t cls1)
+                 const int32_t *__restrict__ runs, int nruns, const uint4 *__restrict__ xo,
+                 const uint32_t *__restrict__ tab, uint32_t cls0, uint32_t cls1, uint32_t nthr)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t dim = 1u << n;
-    const uint32_t nthr = blockDim.x;
-    double2 *st = reinterpret_cast<double2 *>(smem_raw);  // state
-    double2 *cs = st + dim;                               // (cos, sin) of the chunk's angles
-    double2 *mt = cs + kSmallChunkRots;                   // [group][8 configs][kRow]
-    uint4 *xs = reinterpret_cast<uint4 *>(mt + 8 * kRow * kSmallChunkGroups);  // the chunk's slot XORs
-    uint32_t *ring = reinterpret_cast<uint32_t *>(xs + kSmallChunkGroups);        // [kRing][nthr] table entries
-    int32_t *ms = reinterpret_cast<int32_t *>(ring + kRing * kMaxThreads);       // the chunk's rotation meta
-    SmallGroup *gs = reinterpret_cast<SmallGroup *>(ms + kSmallChunkRots);        // the chunk's groups
+    double2 *st = reinterpret_cast<double2 *>(smem_raw);                       // state
+    double2 *mt = st + dim;                                                    // [2][group][8 configs][kRow]
+    uint4 *xs = reinterpret_cast<uint4 *>(mt + 2 * 8 * kRow * kSmallRunGroups);  // [2][group] slot XORs
+    uint32_t *ring = reinterpret_cast<uint32_t *>(xs + 2 * kSmallRunGroups);    // [kRing][nthr] table entries
+    double2 *cs = reinterpret_cast<double2 *>(ring + kRing * kMaxThreads);     // builder: (cos, sin) of a run
+    int32_t *ms = reinterpret_cast<int32_t *>(cs + kSmallRunRots);             // builder: meta of a run
+    int4 *gr = reinterpret_cast<int4 *>(ms + kSmallRunRots);                   // builder: (r0, r1, dimb) per group
     unsigned char *sb = smem_raw;
     const uint32_t tid = threadIdx.x;
-    // the (group, class) items in order; each thread streams its own table
-    // entries kAhead items ahead of use through a shared-memory ring
-    // (cp.async, one commit group per item; a thread reads only its own slots)
+    const bool builder = tid >= nthr;
+
+    // builder warps (kBuilders x 32 threads): matrices + slot constants of
+    // run r into buffer r & 1.  All global loads of a run are issued before
+    // their uses (group records into shared memory, angles two per thread per
+    // step), then the 8 configs x groups matrix chains read shared memory only.
+    const uint32_t bt = tid - nthr;  // builder thread index (builders only)
+    auto bsync = [] { asm volatile("bar.sync 1, %0;" ::"n"(kBuilders * 32) : "memory"); };
+    auto build = [&](int r) {
+        const int g0 = __ldg(runs + 2 * r), g1 = __ldg(runs + 2 * r + 1);
+        double2 *mb = mt + (r & 1) * 8 * kRow * kSmallRunGroups;
+        for (int i = (int)bt; i < g1 - g0; i += kBuilders * 32) {
+            const SmallGroup *G = groups + g0 + i;
+            gr[i] = make_int4(__ldg(&G->r0), __ldg(&G->r1), __ldg(&G->dimb), 0);
+            xs[(r & 1) * kSmallRunGroups + i] = __ldg(xo + g0 + i);
+        }
+        const int rb = __ldg(&groups[g0].r0), re = __ldg(&groups[g1 - 1].r1);
+        constexpr int kB = kBuilders * 32;
+        for (int k = rb + (int)bt; k < re; k += 2 * kB) {
+            const bool two = k + kB < re;
+            const double t0 = __ldg(theta + k), t1 = two ? __ldg(theta + k + kB) : 0.0;
+            const int32_t q0 = __ldg(meta + k), q1 = two ? __ldg(meta + k + kB) : 0;
+            double s0, c0, s1, c1;
+            sincos(0.5 * t0, &s0, &c0);
+            sincos(0.5 * t1, &s1, &c1);
+            cs[k - rb] = make_double2(c0, s0);
+            ms[k - rb] = q0;
+            if (two) {
+                cs[k + kB - rb] = make_double2(c1, s1);
+                ms[k + kB - rb] = q1;
+            }
+        }
+        bsync();
+        for (int t = (int)bt; t < (g1 - g0) * 8; t += kB) {
+            const int4 G = gr[t / 8];
+            const uint32_t cfg = (uint32_t)(t & 7);
+            if (cfg >= (1u << G.z)) continue;
+            double2 m00 = make_double2(1.0, 0.0), m01 = make_double2(0.0, 0.0);
+            double2 m10 = make_double2(0.0, 0.0), m11 = make_double2(1.0, 0.0);
+            for (int k = G.x; k < G.y; ++k) {
+                const int mk = ms[k - rb];
+                const double2 csr = cs[k - rb];
+                const double sig = (__popc((uint32_t)(mk >> 3) & cfg) & 1) ? -1.0 : 1.0;
+                // off-diagonals: b = -i s i^ny sigma (lo <- hi gets (-1)^ny more)
+                const double2 bq = ipow((mk & 3) + 3, csr.y * sig);
+                const double2 aq = (mk & 4) ? make_double2(-bq.x, -bq.y) : bq;
+                const double c = csr.x;
+                const double2 n00 = cfma(aq, m10, make_double2(c * m00.x, c * m00.y));
+                const double2 n01 = cfma(aq, m11, make_double2(c * m01.x, c * m01.y));
+                const double2 n10 = cfma(bq, m00, make_double2(c * m10.x, c * m10.y));
+                const double2 n11 = cfma(bq, m01, make_double2(c * m11.x, c * m11.y));
+                m00 = n00; m01 = n01; m10 = n10; m11 = n11;
+            }
+            double2 *row = mb + t * kRow;  // [group][config]
+            row[0] = m00; row[1] = m01; row[2] = m10; row[3] = m11;
+        }
+        bsync();  // cs / ms / gr are reused by the next build
+    };
+
+    // compute threads: the (group, class) items in order; each thread streams
+    // its own table entries kAhead items ahead of use (cp.async, one commit
+    // group per item; a thread reads only its own ring slots)
     const uint32_t ncl = cls1 - cls0;
-    const uint32_t n_items = (uint32_t)chunks[2 * nchunks - 1] * ncl;
-    const uint32_t ring_base = (uint32_t)__cvta_generic_to_shared(ring + tid);
+    const uint32_t n_items = (uint32_t)runs[2 * nruns - 1] * ncl;
+    const uint32_t ring_base = (uint32_t)__cvta_generic_to_shared(ring + (builder ? 0 : tid));
     uint32_t f_item = 0, f_g = 0, f_cl = cls0;  // next item to fetch and its (group, class)
     auto fetch = [&]() {
         if (f_item < n_items) {
@@ -518,91 +574,59 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
         ++f_item;
         asm volatile("cp.async.commit_group;\n" ::);
     };
-    for (int k = 0; k < kAhead; ++k) fetch();
-    for (uint32_t i = tid; i < dim; i += nthr)
+    if (!builder)
+        for (int k = 0; k < kAhead; ++k) fetch();
+    for (uint32_t i = tid; i < dim; i += blockDim.x)
         st[small_slot(i)] = basis != ~0ull ? make_double2(i == basis ? 1.0 : 0.0, 0.0) : psi[i];
+    if (builder) build(0);
+    __syncthreads();
     uint32_t item = 0;
-    for (int ch = 0; ch < nchunks; ++ch) {
-        const int g0 = chunks[2 * ch], g1 = chunks[2 * ch + 1];
-        const int rb = groups[g0].r0, re = groups[g1 - 1].r1;
-        for (int r = rb + (int)tid; r < re; r += nthr) {
-            double s, c;
-            sincos(0.5 * theta[r], &s, &c);
-            cs[r - rb] = make_double2(c, s);
-        }
-        {
-            const int words = (g1 - g0) * (int)(sizeof(SmallGroup) / 4);
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(groups + g0);
-            uint32_t *dst = reinterpret_cast<uint32_t *>(gs);
-            for (int i = (int)tid; i < words; i += nthr) dst[i] = src[i];
-            for (int i = (int)tid; i < g1 - g0; i += nthr) xs[i] = xo[g0 + i];
-            for (int r = rb + (int)tid; r < re; r += nthr) ms[r - rb] = meta[r];
-        }
-        __syncthreads();  // angles and groups ready; the previous chunk is done with mt
-        for (int t = (int)tid; t < (g1 - g0) * 8; t += nthr) {
-            const SmallGroup &G = gs[t / 8];
-            const uint32_t cfg = (uint32_t)(t & 7);
-            if (cfg >= (1u << G.dimb)) continue;
-            double2 m00 = make_double2(1.0, 0.0), m01 = make_double2(0.0, 0.0);
-            double2 m10 = make_double2(0.0, 0.0), m11 = make_double2(1.0, 0.0);
-            for (int r = G.r0; r < G.r1; ++r) {
-                const int mk = ms[r - rb];
-                const double2 csr = cs[r - rb];
-                const double sig = (__popc((uint32_t)(mk >> 3) & cfg) & 1) ? -1.0 : 1.0;
-                // off-diagonals: b = -i s i^ny sigma (lo <- hi gets (-1)^ny more)
-                const double2 b = ipow((mk & 3) + 3, csr.y * sig);
-                const double2 a = (mk & 4) ? make_double2(-b.x, -b.y) : b;
-                const double c = csr.x;
-                const double2 n00 = cfma(a, m10, make_double2(c * m00.x, c * m00.y));
-                const double2 n01 = cfma(a, m11, make_double2(c * m01.x, c * m01.y));
-                const double2 n10 = cfma(b, m00, make_double2(c * m10.x, c * m10.y));
-                const double2 n11 = cfma(b, m01, make_double2(c * m11.x, c * m11.y));
-                m00 = n00; m01 = n01; m10 = n10; m11 = n11;
-            }
-            double2 *row = mt + t * kRow;  // [group][config]
-            row[0] = m00; row[1] = m01; row[2] = m10; row[3] = m11;
-        }
-        __syncthreads();
-        for (int gi = 0; gi < g1 - g0; ++gi) {
-            const uint4 X = xs[gi];
-            const uint32_t xh = X.w & 0xffffu;
-            for (uint32_t c = 0; c < ncl; ++c) {  // the classes this evolve can reach
-                fetch();
-                asm volatile("cp.async.wait_group %0;\n" ::"n"(kAhead));
-                const uint32_t e = ring[(item % kRing) * nthr + tid];
-                ++item;
-                const double2 *M = mt + (gi * 8 + (int)((e >> 16) & 7u)) * kRow;
-                const uint32_t sg = (e >> 19) << 31;  // g = -1: D M D, D = diag(1, -1)
-                const double2 m00 = M[0], m11 = M[3];
-                const double2 m01 = flip_sign(M[1], sg), m10 = flip_sign(M[2], sg);
-                const uint32_t o0 = e & 0xffffu;
-                const uint32_t lo[4] = {o0, o0 ^ X.x, o0 ^ X.y, o0 ^ X.z};
-                double2 x[4], y[4];
+    for (int r = 0; r < nruns; ++r) {
+        if (builder) {
+            if (r + 1 < nruns) build(r + 1);
+        } else {
+            const int g0 = runs[2 * r], g1 = runs[2 * r + 1];
+            const double2 *mb = mt + (r & 1) * 8 * kRow * kSmallRunGroups;
+            const uint4 *xb = xs + (r & 1) * kSmallRunGroups;
+            for (int gi = 0; gi < g1 - g0; ++gi) {
+                const uint4 X = xb[gi];
+                const uint32_t xh = X.w & 0xffffu;
+                for (uint32_t c = 0; c < ncl; ++c) {  // the classes this evolve can reach
+                    fetch();
+                    asm volatile("cp.async.wait_group %0;\n" ::"n"(kAhead));
+                    const uint32_t e = ring[(item % kRing) * nthr + tid];
+                    ++item;
+                    const double2 *M = mb + (gi * 8 + (int)((e >> 16) & 7u)) * kRow;
+                    const uint32_t sg = (e >> 19) << 31;  // g = -1: D M D, D = diag(1, -1)
+                    const double2 m00 = M[0], m11 = M[3];
+                    const double2 m01 = flip_sign(M[1], sg), m10 = flip_sign(M[2], sg);
+                    const uint32_t o0 = e & 0xffffu;
+                    const uint32_t lo[4] = {o0, o0 ^ X.x, o0 ^ X.y, o0 ^ X.z};
+                    double2 x[4], y[4];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    x[a] = *reinterpret_cast<const double2 *>(sb + lo[a]);
-                    y[a] = *reinterpret_cast<const double2 *>(sb + (lo[a] ^ xh));
-                }
+                    for (int a = 0; a < 4; ++a) {
+                        x[a] = *reinterpret_cast<const double2 *>(sb + lo[a]);
+                        y[a] = *reinterpret_cast<const double2 *>(sb + (lo[a] ^ xh));
+                    }
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    *reinterpret_cast<double2 *>(sb + lo[a]) = cfma(m01, y[a], cmul(m00, x[a]));
-                    *reinterpret_cast<double2 *>(sb + (lo[a] ^ xh)) = cfma(m11, y[a], cmul(m10, x[a]));
+                    for (int a = 0; a < 4; ++a) {
+                        *reinterpret_cast<double2 *>(sb + lo[a]) = cfma(m01, y[a], cmul(m00, x[a]));
+                        *reinterpret_cast<double2 *>(sb + (lo[a] ^ xh)) = cfma(m11, y[a], cmul(m10, x[a]));
+                    }
                 }
+                // inside a run each warp owns its amplitudes: a warp barrier
+                if (gi + 1 < g1 - g0) __syncwarp();
             }
-            // inside a warp run each warp owns its amplitudes: a warp barrier
-            if (X.w & kSmallRunEnd)
-                __syncthreads();
-            else
-                __syncwarp();
         }
+        __syncthreads();  // run r applied, run r + 1 built
     }
-    for (uint32_t i = tid; i < dim; i += nthr) psi[i] = st[small_slot(i)];
+    for (uint32_t i = tid; i < dim; i += blockDim.x) psi[i] = st[small_slot(i)];
 }
 
 template <int NC>
 cudaError_t launch_nc(double2 *psi, int n, uint64_t basis, const SmallProgram &sp, const SmallGroup *groups,
-                      const int32_t *meta, const double *theta, const int32_t *chunks, const uint4 *xo,
-                      const uint32_t *tab, int nchunks, uint32_t c0, uint32_t c1, cudaStream_t st, size_t smem)
+                      const int32_t *meta, const double *theta, const int32_t *runs, const uint4 *xo,
+                      const uint32_t *tab, int nruns, uint32_t c0, uint32_t c1, cudaStream_t st, size_t smem)
 {
     static PerDeviceOnce once;
     if (cudaError_t e = once.run([&] {
@@ -610,8 +634,8 @@ cudaError_t launch_nc(double2 *psi, int n, uint64_t basis, const SmallProgram &s
                                         (int)small_smem_bytes(kSmallMaxQubits));
         }))
         return e;
-    small_rot_kernel<NC><<<1, sp.nthr, smem, st>>>(psi, n, basis, groups, meta, theta, chunks, nchunks, xo, tab,
-                                                   c0, c1);
+    small_rot_kernel<NC><<<1, sp.nthr + 32 * kBuilders, smem, st>>>(psi, n, basis, groups, meta, theta, runs, nruns, xo, tab,
+                                                        c0, c1, (uint32_t)sp.nthr);
     return cudaGetLastError();
 }
 
@@ -648,14 +672,14 @@ cudaError_t launch_embed_parity(double2 *dst, const double2 *src, int n_dst, uin
 
 size_t small_smem_bytes(int n)
 {
-    return ((size_t)16 << n) + 16 * (size_t)kSmallChunkRots + 16 * (size_t)kRow * 8 * kSmallChunkGroups +
-           16 * (size_t)kSmallChunkGroups + 4 * (size_t)kRing * kMaxThreads + 4 * (size_t)kSmallChunkRots +
-           sizeof(SmallGroup) * kSmallChunkGroups;
+    return ((size_t)16 << n) + 2 * 16 * (size_t)kRow * 8 * kSmallRunGroups + 2 * 16 * (size_t)kSmallRunGroups +
+           4 * (size_t)kRing * kMaxThreads + 16 * (size_t)kSmallRunRots + 4 * (size_t)kSmallRunRots +
+           16 * (size_t)kSmallRunGroups;
 }
 
 cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram &sp,
                          const SmallGroup *groups, const int32_t *meta, const double *theta,
-                         const int32_t *chunks, const uint32_t *xo, const uint32_t *tab, cudaStream_t st)
+                         const int32_t *runs, const uint32_t *xo, const uint32_t *tab, cudaStream_t st)
 {
     // from a basis state only its own class is ever non-zero
     uint32_t c0 = 0, c1 = 1u << sp.ncls;
@@ -664,11 +688,11 @@ cudaError_t launch_small(double2 *psi, int n, uint64_t basis, const SmallProgram
         for (int k = 0; k < sp.ncls; ++k) c0 |= (uint32_t)__builtin_parityll(basis & sp.w[k]) << k;
         c1 = c0 + 1;
     }
-    const int nchunks = (int)(sp.chunks.size() / 2);
+    const int nruns = (int)(sp.runs.size() / 2);
     const size_t smem = small_smem_bytes(n);
     const uint4 *x4 = reinterpret_cast<const uint4 *>(xo);
 #define QSV_SMALL_LAUNCH(NC) \
-    launch_nc<NC>(psi, n, basis, sp, groups, meta, theta, chunks, x4, tab, nchunks, c0, c1, st, smem)
+    launch_nc<NC>(psi, n, basis, sp, groups, meta, theta, runs, x4, tab, nruns, c0, c1, st, smem)
     switch (sp.ncls) {
         case 0: return QSV_SMALL_LAUNCH(0);
         case 1: return QSV_SMALL_LAUNCH(1);

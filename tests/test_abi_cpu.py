@@ -314,7 +314,7 @@ def test_gate_pass_blocks_bank_conflict_free():
 def test_small_program_grouping_host_side():
     """Small-state rotation programs (csrc/qsv_small.cu) are built on the
     host: config 1 is 261 same-flip groups (36 singles of 2 strings, 225
-    doubles of 8) in 4 shared-memory chunks; mixed gates, diagonal strings,
+    doubles of 8) in warp runs of <= 48 groups; mixed gates, diagonal strings,
     fewer than 8 or more than 12 qubits leave no small program (tile passes)."""
     import collections
 
@@ -326,7 +326,9 @@ def test_small_program_grouping_host_side():
     sm = _lib.debug_plan(12, k, q, v)["small"]
     assert sm["valid"] == 1 and len(sm["groups"]) == 261
     assert collections.Counter(g[2] - g[1] for g in sm["groups"]) == {8: 225, 2: 36}
-    assert sm["chunks"] == [0, 144, 144, 261]
+    runs = sm["runs"]  # warp runs: contiguous, each <= 48 groups (one CTA barrier each)
+    assert runs[0] == 0 and runs[-1] == 261 and all(runs[i] == runs[i + 1] for i in range(1, len(runs) - 1, 2))
+    assert all(0 < runs[i + 1] - runs[i] <= 48 for i in range(0, len(runs), 2)) and len(runs) // 2 <= 30
     assert all(g[3] <= 3 for g in sm["groups"])  # <= 8 sign-pattern configs per group
     rng = np.random.default_rng(2)
     strings = W.ucc_rotation_strings(10, 5)[:60]
@@ -345,7 +347,7 @@ def test_small_program_grouping_host_side():
     for n in (6, 13):
         s_n = W.ucc_rotation_strings(n, n // 2)[:40]
         assert small_valid(W.rotations_circuit(n, s_n, rng.uniform(-1, 1, len(s_n))), n) == 0
-    # one group of more than 2048 rotations does not fit a chunk's angle table
+    # one group of more than 2048 rotations does not fit a run's angle buffer
     one = PauliString(((0, "X"), (1, "Y"), (2, "Z")))
     assert small_valid(W.rotations_circuit(9, [one] * 2049, rng.uniform(-1, 1, 2049)), 9) == 0
     assert small_valid(W.rotations_circuit(9, [one] * 2048, rng.uniform(-1, 1, 2048)), 9) == 1
