@@ -149,33 +149,6 @@ class CudaEngine:
 
 
 # ---------------------------------------------------------------------------
-# peer shards mapped through CUDA IPC (cross-process relayouts)
-# ---------------------------------------------------------------------------
-
-_IPC_MAPS: "dict[tuple[int, bytes], int]" = {}
-_IPC_MAX = 16
-
-
-def _ipc_map(device: int, handle: bytes) -> int:
-    """Device pointer of a partner's shard (qsv_ipc_open), cached by handle;
-    the oldest mappings are closed beyond _IPC_MAX."""
-    from . import _lib
-
-    key = (device, handle)
-    base = _IPC_MAPS.get(key)
-    if base is None:
-        ptr = ctypes.c_void_p()
-        _lib.check(_lib.lib().qsv_ipc_open(device, handle, ctypes.byref(ptr)))
-        base = ptr.value
-        if len(_IPC_MAPS) >= _IPC_MAX:
-            (d0, _), old = next(iter(_IPC_MAPS.items()))
-            _IPC_MAPS.pop(next(iter(_IPC_MAPS)))
-            _lib.lib().qsv_ipc_close(d0, ctypes.c_void_p(old))
-        _IPC_MAPS[key] = base
-    return base
-
-
-# ---------------------------------------------------------------------------
 # communicators
 # ---------------------------------------------------------------------------
 
@@ -701,8 +674,8 @@ class DistStateVector:
 
     def _ipc_exchange(self, remote, chunk, s_value) -> None:
         """Pairwise in-place chunk swap over peer memory: every rank exports
-        its shard (qsv_ipc_get_handle), maps its partners' (qsv_ipc_open,
-        cached) and swaps its half of each pair with the swap kernel
+        its shard (qsv_ipc_get_handle), maps its partners' (qsv_ipc_open, for
+        this exchange only) and swaps its half of each pair with the swap kernel
         (qsv_swap_peer: the lower rank the first half, the higher the second),
         so each byte is read and written once per side with no staging copy
         and both directions of every link busy.  Ordering: every rank drains
@@ -720,13 +693,22 @@ class DistStateVector:
         self.comm.barrier()  # every shard's earlier work is done
         rs = s_value(r)
         half = chunk // 2
-        for c, p in remote[r]:
-            base = _ipc_map(self.engine.device, handles[p])
-            off, ln = (0, half) if p > r else (half, chunk - half)
-            _lib.check(L.qsv_swap_peer(shard.handle, c * chunk + off, ctypes.c_void_p(base),
-                                       rs * chunk + off, ln))
-            self.stats["ipc_swaps"] = self.stats.get("ipc_swaps", 0) + 1
-        shard.synchronize()
+        dev = self.engine.device
+        mapped = []
+        try:
+            for c, p in remote[r]:
+                ptr = ctypes.c_void_p()
+                _lib.check(L.qsv_ipc_open(dev, handles[p], ctypes.byref(ptr)))
+                mapped.append(ptr)
+                off, ln = (0, half) if p > r else (half, chunk - half)
+                _lib.check(L.qsv_swap_peer(shard.handle, c * chunk + off, ptr, rs * chunk + off, ln))
+                self.stats["ipc_swaps"] = self.stats.get("ipc_swaps", 0) + 1
+            shard.synchronize()
+        finally:
+            # a mapping pins the partner's allocation: unmap before the
+            # partner may free its shard (128 GiB at config 5)
+            for ptr in mapped:
+                L.qsv_ipc_close(dev, ptr)
         self.comm.barrier()  # every half of every pair is swapped
 
     def _p2p_exchange(self, views, remote, chunk):
