@@ -15,6 +15,7 @@ recognises and turns back into one direct Pauli rotation.
 
 from __future__ import annotations
 
+import contextlib
 import json
 import math
 from dataclasses import dataclass
@@ -109,11 +110,15 @@ class _BindPlan:
     offset) of every Affine parameter -- so bind is O(#params) numpy work."""
 
     __slots__ = ("n_qubits", "kinds", "qubits", "const", "slot", "index", "scale", "offset", "_pid",
-                 "__weakref__")
+                 "_scratch", "_lock", "__weakref__")
 
     def __init__(self, c):
+        import threading
+
         self.n_qubits = c.n_qubits
         self._pid = None
+        self._scratch = None  # const with one bound circuit's Affine slots, reused per call
+        self._lock = threading.Lock()
         gates = c.gates
         G = len(gates)
         codes = _lib.KIND_CODES
@@ -139,6 +144,19 @@ class _BindPlan:
         self.index = np.asarray(index, dtype=np.int64)
         self.scale = np.asarray(scale, dtype=np.float64)
         self.offset = np.asarray(offset, dtype=np.float64)
+
+    @contextlib.contextmanager
+    def values_with(self, slot_values):
+        """The full 3 x gates value array for these Affine slot values, in a
+        buffer reused across calls (held under a lock for the duration of the
+        caller's synchronous library call) -- so an energy evaluation at new
+        angles does not allocate and fill a fresh 3 x gates array."""
+        with self._lock:
+            if self._scratch is None:
+                self._scratch = self.const.copy()
+            if len(self.slot):
+                self._scratch[self.slot] = slot_values
+            yield self._scratch
 
     def program_id(self) -> int:
         """Id of this structure prepared in the library (qsv_prepare_gates):
@@ -183,27 +201,41 @@ class BoundCircuit:
     objects are only built if someone reads ``gates``.  Duck-types Circuit
     (n_qubits, gates, n_params = 0, is_bound, len)."""
 
-    __slots__ = ("n_qubits", "n_params", "_kinds", "_qubits", "_values", "_src", "_gates", "_plan",
-                 "__weakref__")
+    __slots__ = ("n_qubits", "n_params", "_kinds", "_qubits", "_values", "_slot_values", "_src", "_gates",
+                 "_plan", "__weakref__")
 
-    def __init__(self, src, kinds, qubits, values, plan=None):
+    def __init__(self, src, kinds, qubits, values, plan=None, slot_values=None):
         self.n_qubits = src.n_qubits
         self.n_params = 0
         self._src = src
         self._plan = plan
         self._kinds, self._qubits, self._values = kinds, qubits, values
+        self._slot_values = slot_values  # Affine slots only; the full array on demand
         self._gates = None
+
+    def call_values(self):
+        """Context manager yielding the full value array for ONE synchronous
+        library call: the materialised array if there is one, else the
+        plan's reused scratch filled with this circuit's slot values."""
+        if self._values is not None or self._plan is None:
+            return contextlib.nullcontext(self.flat()[2])
+        return self._plan.values_with(self._slot_values)
 
     @property
     def gates(self) -> tuple:
         if self._gates is None:
-            v = self._values
+            v = self.flat()[2]
             self._gates = tuple(
                 Gate(g.kind, g.qubits, tuple(Constant(float(v[3 * i + k])) for k in range(len(g.params))))
                 for i, g in enumerate(self._src.gates))
         return self._gates
 
     def flat(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        if self._values is None:
+            v = self._plan.const.copy()
+            if len(self._plan.slot):
+                v[self._plan.slot] = self._slot_values
+            self._values = v
         return self._kinds, self._qubits, self._values
 
     def is_bound(self) -> bool:
@@ -231,10 +263,11 @@ def bind(c, theta: Sequence[float]) -> BoundCircuit:
     if not np.all(np.isfinite(theta)):
         raise ValueError("parameter values must be finite")
     plan = _bind_plan(c)
-    values = plan.const.copy()
-    if len(plan.slot):
-        values[plan.slot] = plan.scale * theta[plan.index] + plan.offset
-    return BoundCircuit(c, plan.kinds, plan.qubits, values, plan)
+    # only the Affine slots are evaluated here; the full value array is built
+    # on demand (BoundCircuit.flat) or filled into the plan's scratch for one
+    # engine call (BoundCircuit.call_values)
+    slot_values = plan.scale * theta[plan.index] + plan.offset if len(plan.slot) else plan.scale[:0]
+    return BoundCircuit(c, plan.kinds, plan.qubits, None, plan, slot_values)
 
 
 def gate_matrix(kind: str, values: Sequence[float] = ()) -> np.ndarray:

@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 from . import symmetry as _symmetry
-from .circuit import flatten_bound
+from .circuit import BoundCircuit, flatten_bound
 from .errors import ResourceLimitError
 from .pauli import term_arrays
 
@@ -327,7 +327,16 @@ def apply_circuit_inplace(s: StateVector, c, basis: Optional[int] = None) -> Non
     L = _lib.lib()
     plan = getattr(c, "_plan", None)
     if plan is not None and plan.n_qubits == s.n_qubits:
-        values = c.flat()[2]
+        # a bind() result: its values go down for this one synchronous call
+        # (the plan's reused buffer -- no fresh 3 x gates array per evaluation)
+        with c.call_values() as values:
+            if basis is None:
+                _lib.check(L.qsv_apply_prepared(s.handle, plan.program_id(), _lib.dptr(values),
+                                                ctypes.byref(_last_stats)))
+            else:
+                _lib.check(L.qsv_evolve_basis_prepared(s.handle, basis, plan.program_id(),
+                                                       _lib.dptr(values), ctypes.byref(_last_stats)))
+        return
     else:
         kinds, qubits, values = _flat(c)
         plan = _id_cache_get(_PROG_CACHE, c)
@@ -411,12 +420,18 @@ def evolve(s: StateVector, c) -> StateVector:
     if c.n_qubits != s.n_qubits:
         raise ValueError("circuit and state qubit counts differ")
     # boundness (statevector.py:69-70) is checked by the flattening itself
-    # (RuntimeError on an unbound parameter), before any device work
-    kinds, qubits, values = _flat(c)
+    # (RuntimeError on an unbound parameter), before any device work; a
+    # bind() result is bound by construction and its value array is only
+    # built when a path below needs it
+    if isinstance(c, BoundCircuit):
+        kinds, qubits = c._kinds, c._qubits
+    else:
+        kinds, qubits, _ = _flat(c)
     _last_reduction["n_eff"] = None
     if s.basis_index is not None and s.n_qubits > 12 and _symmetry.enabled():
         red = _symmetry.reduction_for(s.n_qubits, kinds, qubits)
         if red is not None:  # the basis state's parity class, as an (n-1)-qubit state
+            values = _flat(c)[2]
             b = s.basis_index
             parity = bin(b).count("1") & 1
             half = StateVector._empty(s.n_qubits - 1, s.device)
