@@ -1317,27 +1317,71 @@ static void finish_expectation(const std::vector<double> &vals, int64_t S, const
     if (per_term) std::memcpy(per_term, vals.data(), (size_t)S * 8);
 }
 
-static int expectation_small(const qsv_state *s, DeviceCtx &c, int64_t S, const uint64_t *x, const uint64_t *y,
-                             const uint64_t *z, const double *coef_re, const double *coef_im, double *out_re,
-                             double *out_im, double *per_term, qsv_plan_stats *stats)
+// Device copies of small-state string records (flip, sign mask, ny mod 4),
+// keyed by the masks: an energy loop re-evaluates the same Hamiltonian, so
+// its records go up once (per device), not per call.
+struct SmallExpEntry {
+    uint64_t hash = 0;
+    int device = -1, n = 0;
+    std::vector<uint64_t> x, y, z;
+    uint32_t *d_rec = nullptr;
+};
+static std::list<SmallExpEntry> g_small_exp;
+
+static int small_exp_records(const qsv_state *s, int64_t S, const uint64_t *x, const uint64_t *y,
+                             const uint64_t *z, const uint32_t **d_rec)
 {
-    Blob b;
-    const size_t o_r = b.add(nullptr, (size_t)S * 16);
-    uint32_t *rec = reinterpret_cast<uint32_t *>(b.bytes.data() + o_r);
+    const uint64_t h = hash_masks(s->n, S, x, y, z);
+    for (auto it = g_small_exp.begin(); it != g_small_exp.end(); ++it)
+        if (it->hash == h && it->device == s->device && it->n == s->n && (int64_t)it->x.size() == S &&
+            std::memcmp(it->x.data(), x, S * 8) == 0 && std::memcmp(it->y.data(), y, S * 8) == 0 &&
+            std::memcmp(it->z.data(), z, S * 8) == 0) {
+            g_small_exp.splice(g_small_exp.begin(), g_small_exp, it);
+            *d_rec = g_small_exp.front().d_rec;
+            return QSV_OK;
+        }
+    std::vector<uint32_t> rec(4 * (size_t)S);
     for (int64_t t = 0; t < S; ++t) {
         rec[4 * t + 0] = (uint32_t)(x[t] | y[t]);
         rec[4 * t + 1] = (uint32_t)(y[t] | z[t]);
         rec[4 * t + 2] = (uint32_t)(__builtin_popcountll(y[t]) & 3);
         rec[4 * t + 3] = 0;
     }
-    char *d = nullptr;
-    size_t scratch = 0;
-    if (int rc = upload_blob(c, s->stream, b, (size_t)S * 8 + 256, &d, &scratch)) return rc;
-    double *d_vals = (double *)(d + scratch);
-    QSV_CUDA(launch_expect_small(s->amps, s->n, (const uint32_t *)(d + o_r), (int)S, d_vals,
-                                 num_sms(s->device), s->stream));
+    SmallExpEntry e;
+    e.hash = h;
+    e.device = s->device;
+    e.n = s->n;
+    e.x.assign(x, x + S);
+    e.y.assign(y, y + S);
+    e.z.assign(z, z + S);
+    if (cudaMalloc((void **)&e.d_rec, rec.size() * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return fail_code(QSV_ERR_NOMEM, "small expectation records: device allocation failed");
+    }
+    QSV_CUDA(cudaMemcpy(e.d_rec, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice));
+    g_small_exp.push_front(std::move(e));
+    if (g_small_exp.size() > 8) {  // cudaFree synchronises the device: only on eviction
+        SmallExpEntry &old = g_small_exp.back();
+        cudaSetDevice(old.device);
+        cudaFree(old.d_rec);
+        cudaSetDevice(s->device);
+        g_small_exp.pop_back();
+    }
+    *d_rec = g_small_exp.front().d_rec;
+    return QSV_OK;
+}
+
+static int expectation_small(const qsv_state *s, DeviceCtx &c, int64_t S, const uint64_t *x, const uint64_t *y,
+                             const uint64_t *z, const double *coef_re, const double *coef_im, double *out_re,
+                             double *out_im, double *per_term, qsv_plan_stats *stats)
+{
+    const uint32_t *d_rec = nullptr;
+    if (int rc = small_exp_records(s, S, x, y, z, &d_rec)) return rc;
+    // the kernel writes the per-term values straight into the pinned staging
+    // buffer (host memory the device addresses under UVA): no D2H copy call
     if (int rc = ensure_stage(c, (size_t)S * 8)) return rc;
-    QSV_CUDA(cudaMemcpyAsync(c.h_stage, d_vals, (size_t)S * 8, cudaMemcpyDeviceToHost, s->stream));
+    QSV_CUDA(launch_expect_small(s->amps, s->n, d_rec, (int)S, (double *)c.h_stage, num_sms(s->device),
+                                 s->stream));
     QSV_CUDA(cudaStreamSynchronize(s->stream));
     std::vector<double> vals(S);
     std::memcpy(vals.data(), c.h_stage, (size_t)S * 8);

@@ -473,17 +473,25 @@ _H_CACHE: dict = {}
 
 
 def _hamiltonian(h, n: int):
+    return _hamiltonian_entry(h, n)[0]
+
+
+def _hamiltonian_entry(h, n: int):
+    """(term arrays, their ctypes pointers) of a PauliSum, cached per object:
+    an energy loop re-evaluates the same Hamiltonian."""
     hit = _id_cache_get(_H_CACHE, h)
     if hit is not None and hit[0] == n:
         return hit[1]
     arrays = term_arrays(h, n)
-    _id_cache_put(_H_CACHE, h, (n, arrays), _FLAT_MAX)
-    return arrays
+    x, y, z, cr, ci = arrays
+    ptrs = (_lib.u64ptr(x), _lib.u64ptr(y), _lib.u64ptr(z), _lib.dptr(cr), _lib.dptr(ci))
+    _id_cache_put(_H_CACHE, h, (n, (arrays, ptrs)), _FLAT_MAX)
+    return arrays, ptrs
 
 
 def expectation_terms(s: StateVector, h) -> tuple[float, float, np.ndarray]:
     """(Re, Im residue, per-term <P_t>) of <s|H|s>; no Hermitian checks."""
-    x, y, z, cr, ci = _hamiltonian(h, s.n_qubits)
+    (x, y, z, cr, ci), ptrs = _hamiltonian_entry(h, s.n_qubits)
     re, im = ctypes.c_double(), ctypes.c_double()
     per = np.zeros(len(cr), dtype=np.float64)
     if isinstance(s, ParityReduced) and s.reduced:
@@ -499,10 +507,8 @@ def expectation_terms(s: StateVector, h) -> tuple[float, float, np.ndarray]:
         per[keep] = per2 * sign
         return re.value, im.value, per
     if len(cr):
-        _lib.check(_lib.lib().qsv_expectation(s.handle, len(cr), _lib.u64ptr(x), _lib.u64ptr(y),
-                                              _lib.u64ptr(z), _lib.dptr(cr), _lib.dptr(ci),
-                                              ctypes.byref(re), ctypes.byref(im), _lib.dptr(per),
-                                              None))
+        _lib.check(_lib.lib().qsv_expectation(s.handle, len(cr), *ptrs, ctypes.byref(re), ctypes.byref(im),
+                                              _lib.dptr(per), None))
     return re.value, im.value, per
 
 
