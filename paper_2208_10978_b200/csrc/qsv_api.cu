@@ -1909,7 +1909,8 @@ int qsv_debug_plan_json(int n, int64_t n_gates, const int32_t *kinds, const int3
         j += "]";
     }
     // the per-thread table and slot constants (small programs only: tests)
-    j += "],\"nthr\":" + std::to_string(t.small.nthr) + ",\"xo\":[";
+    j += "],\"nthr\":" + std::to_string(t.small.nthr) + ",\"swz\":[" + std::to_string(t.small.swz[0]) + "," +
+         std::to_string(t.small.swz[1]) + "," + std::to_string(t.small.swz[2]) + "],\"xo\":[";
     const bool emit_tab = t.small.tab.size() <= ((size_t)1 << 18);
     for (size_t i = 0; emit_tab && i < t.small.xo.size(); ++i) j += (i ? "," : "") + std::to_string(t.small.xo[i]);
     j += "],\"tab\":[";

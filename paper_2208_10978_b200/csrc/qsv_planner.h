@@ -130,6 +130,7 @@ struct SmallProgram {
     //   xo[4 g .. 4 g + 3] = byte-slot XORs of the other three pairs' lows
     //     (lu0, lu1, lu0 ^ lu1) and of the flip (low -> high amplitude)
     int nthr = 0;
+    uint32_t swz[3] = {8u, 8u, 8u};  // shared-memory slot map masks (qsv_small.cu: slot3)
     std::vector<uint32_t> tab;
     std::vector<uint32_t> xo;
     // device copy of the structure-only arrays (groups, meta, runs, xo,

@@ -48,6 +48,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 
 #include "qsv_internal.h"
@@ -125,6 +126,21 @@ static inline uint32_t parity32(uint32_t v) { return (uint32_t)__builtin_popcoun
 // quarter warp's 8 pairs vary once the pivot bit is skipped -- reach 8
 // distinct granules.  Linear over GF(2): slot(a ^ b) = slot(a) ^ slot(b).
 __host__ __device__ __forceinline__ uint32_t small_slot(uint32_t l) { return l ^ (((l >> 3) & 1u) * 7u); }
+
+// The program's slot map: the low 3 bits (16-B granule in a 128-B row) are
+// XOR-ed with three parities of the bits >= 3 (masks m[0..2]; small_slot is
+// m = {8, 8, 8}).  Linear and an involution; chosen per program so that every
+// group's lanes can reach 8 distinct granules per quarter warp.
+__host__ __device__ __forceinline__ uint32_t slot3(uint32_t l, uint32_t m0, uint32_t m1, uint32_t m2)
+{
+#ifdef __CUDA_ARCH__
+    const uint32_t g = (__popc(l & m0) & 1u) | ((__popc(l & m1) & 1u) << 1) | ((__popc(l & m2) & 1u) << 2);
+#else
+    const uint32_t g = (__builtin_popcount(l & m0) & 1u) | ((__builtin_popcount(l & m1) & 1u) << 1) |
+                       ((__builtin_popcount(l & m2) & 1u) << 2);
+#endif
+    return l ^ g;
+}
 
 // A GF(2) subspace of small index vectors: basis kept by descending pivot
 // (highest bit), so reduce() clears the pivots in order.
@@ -252,7 +268,9 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
         for (int k = 0; k < ncls; ++k) in &= parity32(v & W[k]) == 0;
         if (in) E.push_back(v);
     }
-    auto low3 = [](uint32_t v) { return small_slot(v) & 7u; };
+    uint32_t swz[3] = {8u, 8u, 8u};  // the slot map's masks (see slot3), chosen below
+    auto slot = [&](uint32_t v) { return slot3(v, swz[0], swz[1], swz[2]); };
+    auto low3 = [&](uint32_t v) { return slot(v) & 7u; };
     // per group: amplitude-space parity masks (bit h free: share vectors have bit h = 0)
     auto in_null = [&](const SmallGroup &G, uint32_t v) {
         if ((v >> G.h) & 1u) return false;
@@ -276,6 +294,7 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
     sp.tab.assign(entries, 0);
     sp.xo.assign(4 * sp.groups.size(), 0);
     std::vector<int> warp_of(1u << n, -1);
+    std::vector<Gf2Span> run_V;  // per run: its 8-dimensional subspace
     std::vector<uint32_t> cls_of(1u << n, 0);
     for (uint32_t i = 0; i < (1u << n); ++i)
         for (int k = 0; k < ncls; ++k) cls_of[i] |= parity32(i & W[k]) << k;
@@ -329,6 +348,69 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
                 if (best_score < 0) return false;
                 V.add(best);
             }
+            // share vectors: two independent ones of V in each group's null space
+            for (int m = g; m < gg; ++m) {
+                SmallGroup &G = sp.groups[m];
+                const Gf2Span S = share_dim(V, G);
+                if (S.d < 2) return false;
+                G.lu[0] = S.b[0];
+                G.lu[1] = S.b[1];
+            }
+            run_V.push_back(V);
+            sp.runs.push_back(g);
+            sp.runs.push_back(gg);
+            g = gg;
+        }
+    }
+    // The slot map: every group needs the low slot bits of its pair lows
+    // (V minus bit h) to span all 8 granules, so a quarter warp's 8 lanes can
+    // take distinct granules (conflict-free 128-bit accesses).  Keep the
+    // default map when it already does; else the best of a seeded random
+    // search over the masks.
+    {
+        std::vector<std::array<uint32_t, 7>> vh0(sp.groups.size());
+        for (size_t r = 0; r < run_V.size(); ++r)
+            for (int m = sp.runs[2 * r]; m < sp.runs[2 * r + 1]; ++m) {
+                const Gf2Span &V = run_V[r];
+                const int h = sp.groups[m].h;
+                int star = -1, k = 0;
+                for (int i = 0; i < V.d; ++i)
+                    if ((V.b[i] >> h) & 1u) { star = i; break; }
+                for (int i = 0; i < V.d; ++i) {
+                    if (i == star) continue;
+                    vh0[m][k++] = ((V.b[i] >> h) & 1u) ? V.b[i] ^ V.b[star] : V.b[i];
+                }
+            }
+        auto score = [&](const uint32_t msk[3]) {
+            int full = 0;
+            for (size_t m = 0; m < vh0.size(); ++m) {
+                Gf2Span L;
+                for (uint32_t v : vh0[m]) L.add(slot3(v, msk[0], msk[1], msk[2]) & 7u);
+                full += L.d == 3;
+            }
+            return full;
+        };
+        int best = score(swz);
+        uint64_t rng = 0x9e3779b97f4a7c15ull;
+        const uint32_t hi = ((1u << n) - 1u) & ~7u;
+        for (int it = 0; it < 4000 && best < (int)vh0.size(); ++it) {
+            uint32_t cand[3];
+            for (int j = 0; j < 3; ++j) {
+                rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+                cand[j] = (uint32_t)rng & hi;
+            }
+            const int sc = score(cand);
+            if (sc > best) {
+                best = sc;
+                for (int j = 0; j < 3; ++j) swz[j] = cand[j];
+            }
+        }
+        for (int j = 0; j < 3; ++j) sp.swz[j] = swz[j];
+    }
+    for (size_t r = 0; r < run_V.size(); ++r) {
+        const int g = sp.runs[2 * r], gg = sp.runs[2 * r + 1];
+        const Gf2Span &V = run_V[r];
+        {
             // warp = coset of V inside the class: enumerate the cosets from
             // each class's smallest index and a complement basis of V in E
             Gf2Span Cs = V;
@@ -349,25 +431,12 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
             }
             for (int m = g; m < gg; ++m) {
                 SmallGroup &G = sp.groups[m];
-                // share vectors: two independent ones of V in the null space,
-                // preferring no low slot bits (the lanes' low slots then spread)
-                const Gf2Span S = share_dim(V, G);
-                std::vector<uint32_t> Sel = S.elements();
-                std::stable_sort(Sel.begin(), Sel.end(),
-                                 [&](uint32_t a, uint32_t b2) { return (low3(a) != 0) < (low3(b2) != 0); });
-                uint32_t u0 = 0, u1 = 0;
-                for (uint32_t e : Sel)
-                    if (e) { u0 = e; break; }
-                for (uint32_t e : Sel)
-                    if (e && e != u0) { u1 = e; break; }
-                if (!u0 || !u1) return false;
-                G.lu[0] = u0;
-                G.lu[1] = u1;
+                const uint32_t u0 = G.lu[0], u1 = G.lu[1];
                 const uint32_t lowm = (1u << G.h) - 1u;
-                sp.xo[4 * m + 0] = small_slot(u0) << 4;
-                sp.xo[4 * m + 1] = small_slot(u1) << 4;
-                sp.xo[4 * m + 2] = small_slot(u0 ^ u1) << 4;
-                sp.xo[4 * m + 3] = (small_slot(G.xm) << 4) | (m == gg - 1 ? kSmallRunEnd : 0u);
+                sp.xo[4 * m + 0] = slot(u0) << 4;
+                sp.xo[4 * m + 1] = slot(u1) << 4;
+                sp.xo[4 * m + 2] = slot(u0 ^ u1) << 4;
+                sp.xo[4 * m + 3] = (slot(G.xm) << 4) | (m == gg - 1 ? kSmallRunEnd : 0u);
                 const uint32_t span4[4] = {0, u0, u1, u0 ^ u1};
                 for (uint32_t cl = 0; cl < (1u << ncls); ++cl) {
                     std::vector<std::vector<uint32_t>> quads(nwarps);
@@ -408,15 +477,12 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
                                 const uint32_t p0 = (lo0 & lowm) | ((lo0 >> 1) & ~lowm);
                                 const uint32_t cfg = parity32(p0 & G.pm[0]) | (parity32(p0 & G.pm[1]) << 1) |
                                                      (parity32(p0 & G.pm[2]) << 2) | (parity32(p0 & G.pm[3]) << 3);
-                                row[w * 32 + qt * 8 + j] = (small_slot(lo0) << 4) | (cfg << 16);
+                                row[w * 32 + qt * 8 + j] = (slot(lo0) << 4) | (cfg << 16);
                             }
                         }
                     }
                 }
             }
-            sp.runs.push_back(g);
-            sp.runs.push_back(gg);
-            g = gg;
         }
     }
     sp.valid = true;
@@ -482,7 +548,7 @@ __global__ void __launch_bounds__(kMaxThreads + 32 * kBuilders, 1)
 small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGroup *__restrict__ groups,
                  const int32_t *__restrict__ meta, const double *__restrict__ theta,
                  const int32_t *__restrict__ runs, int nruns, const uint4 *__restrict__ xo,
-                 const uint32_t *__restrict__ tab, uint32_t cls0, uint32_t cls1, uint32_t nthr)
+                 const uint32_t *__restrict__ tab, uint32_t cls0, uint32_t cls1, uint32_t nthr, uint4 swz)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t dim = 1u << n;
@@ -577,7 +643,7 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
     if (!builder)
         for (int k = 0; k < kAhead; ++k) fetch();
     for (uint32_t i = tid; i < dim; i += blockDim.x)
-        st[small_slot(i)] = basis != ~0ull ? make_double2(i == basis ? 1.0 : 0.0, 0.0) : psi[i];
+        st[slot3(i, swz.x, swz.y, swz.z)] = basis != ~0ull ? make_double2(i == basis ? 1.0 : 0.0, 0.0) : psi[i];
     if (builder) build(0);
     __syncthreads();
     uint32_t item = 0;
@@ -620,7 +686,7 @@ small_rot_kernel(double2 *__restrict__ psi, int n, uint64_t basis, const SmallGr
         }
         __syncthreads();  // run r applied, run r + 1 built
     }
-    for (uint32_t i = tid; i < dim; i += blockDim.x) psi[i] = st[small_slot(i)];
+    for (uint32_t i = tid; i < dim; i += blockDim.x) psi[i] = st[slot3(i, swz.x, swz.y, swz.z)];
 }
 
 template <int NC>
@@ -635,7 +701,8 @@ cudaError_t launch_nc(double2 *psi, int n, uint64_t basis, const SmallProgram &s
         }))
         return e;
     small_rot_kernel<NC><<<1, sp.nthr + 32 * kBuilders, smem, st>>>(psi, n, basis, groups, meta, theta, runs, nruns, xo, tab,
-                                                        c0, c1, (uint32_t)sp.nthr);
+                                                        c0, c1, (uint32_t)sp.nthr,
+                                                        make_uint4(sp.swz[0], sp.swz[1], sp.swz[2], 0u));
     return cudaGetLastError();
 }
 

@@ -357,9 +357,10 @@ def _popc(v):
     return bin(int(v)).count("1") & 1
 
 
-def _slot(v):
-    """small_slot (csrc/qsv_small.cu): an involution on 16-B shared-memory slots."""
-    return v ^ (7 if (v >> 3) & 1 else 0)
+def _slot(v, swz=(8, 8, 8)):
+    """slot3 (csrc/qsv_small.cu): the program's involution on 16-B shared-memory
+    slots -- the low 3 bits XOR three parities of the higher bits."""
+    return v ^ sum(_popc(v & m) << j for j, m in enumerate(swz))
 
 
 def _emulate_small(n, circ, basis):
@@ -378,7 +379,7 @@ def _emulate_small(n, circ, basis):
     spans, masks = _lib.match_rotations(n, k, q)
     R = [(int(m[0]), int(m[1]), int(m[2]), float(v[3 * int(s[2])])) for s, m in zip(spans, masks)]
     ncls, W, nthr = sm["ncls"], sm["w"], sm["nthr"]
-    tab, xo = sm["tab"], sm["xo"]
+    tab, xo, swz = sm["tab"], sm["xo"], sm["swz"]
     assert len(tab) == len(sm["groups"]) * (nthr << ncls)
     cls = sum(_popc(basis & W[j]) << j for j in range(ncls))
     psi = np.zeros(1 << n, dtype=complex)
@@ -388,18 +389,18 @@ def _emulate_small(n, circ, basis):
     for gi, g in enumerate(sm["groups"]):
         xm, r0, r1, dimb, h = g[0:5]
         pm, lu = g[5:9], g[9:11]
-        assert xo[4 * gi] >> 4 == _slot(lu[0]) and xo[4 * gi + 1] >> 4 == _slot(lu[1])
-        assert (xo[4 * gi + 3] & 0xFFFF) >> 4 == _slot(xm)
+        assert xo[4 * gi] >> 4 == _slot(lu[0], swz) and xo[4 * gi + 1] >> 4 == _slot(lu[1], swz)
+        assert (xo[4 * gi + 3] & 0xFFFF) >> 4 == _slot(xm, swz)
         rots = R[r0:r1]
         pairs_seen = set()
         lowm = (1 << h) - 1
         for t in range(nthr):
             e = tab[((gi << ncls) | cls) * nthr + t]
-            lo0 = _slot((e & 0xFFFF) >> 4)
+            lo0 = _slot((e & 0xFFFF) >> 4, swz)
             cfg0 = (e >> 16) & 15
             if t % 8 == 0:
                 granules = set()
-            granules.add(_slot(lo0) & 7)
+            granules.add(_slot(lo0, swz) & 7)
             if t % 8 == 7:
                 conflicts.append(8 - len(granules))
             for a in range(4):
@@ -443,6 +444,8 @@ def test_small_program_enumeration_emulated():
     b = int(ref_bits[::-1], 2)
     psi, sm = _emulate_small(10, circ, b)
     assert sm["ncls"] == 1 and sm["w"][0] == 1023 and sm["share"] == 2
+    # the program's slot map lets every quarter warp hit 8 distinct granules
+    assert sum(sm["conflicts"]) == 0
     ref = O.evolve(O.init_state(ref_bits), circ.gates)
     assert np.abs(psi - ref).max() <= 1e-12
     # a program with odd-weight flips has no conserved parity
