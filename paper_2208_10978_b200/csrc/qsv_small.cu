@@ -528,7 +528,7 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c)
 }
 
 constexpr int kMaxThreads = 512;
-constexpr int kBuilders = 4;  // builder warps (A/B under ncu, config 1: 2 -> 151 us, 4 -> 141 us, 8 -> 149 us)
+constexpr int kBuilders = 4;  // builder warps (A/B under ncu, config 1: 2 / 4 / 8 -> 151 / 141 / 149 us; with the slot map 4 / 6 / 8 -> 118 / 121 / 127 us)
 
 // One CTA of nthr = (pairs in a class) / 4 compute threads plus kBuilders
 // builder warps.  Runs alternate between two shared-memory buffers: while the compute
