@@ -393,7 +393,9 @@ bool build_small_program(int n, const std::vector<Rot> &R, SmallProgram &sp)
         int best = score(swz);
         uint64_t rng = 0x9e3779b97f4a7c15ull;
         const uint32_t hi = ((1u << n) - 1u) & ~7u;
-        for (int it = 0; it < 4000 && best < (int)vh0.size(); ++it) {
+        // bounded one-time search (per structure): <= ~2e7 rank evaluations
+        const int iters = (int)std::min<size_t>(4000, (size_t)20000000 / std::max<size_t>(1, 7 * vh0.size()));
+        for (int it = 0; it < iters && best < (int)vh0.size(); ++it) {
             uint32_t cand[3];
             for (int j = 0; j < 3; ++j) {
                 rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
