@@ -1016,14 +1016,19 @@ static int small_dev_copy(const SmallProgram &sp, int device, const SmallProgram
 
 static int run_small(qsv_state *s, const ProgramTemplate &t, const double *values, uint64_t basis)
 {
+    HostProfile prof("run_small");
     DeviceCtx *c = nullptr;
     if (int rc = ctx_for(s->device, &c)) return rc;
     const SmallProgram &sp = t.small;
     const SmallProgram::DevCopy *dc = nullptr;
     if (int rc = small_dev_copy(sp, s->device, &dc)) return rc;
-    Blob b;
-    const size_t o_t = b.add(nullptr, sp.src.size() * sizeof(double));
-    double *th = reinterpret_cast<double *>(b.bytes.data() + o_t);
+    prof.mark("tables");
+    // the angles go straight into the pinned staging buffer (one H2D copy)
+    const size_t bytes = sp.src.size() * sizeof(double);
+    if (int rc = ensure_work(*c, s->stream, bytes + 256)) return rc;
+    if (int rc = ensure_stage(*c, bytes)) return rc;
+    prof.mark("stage");
+    double *th = reinterpret_cast<double *>(c->h_stage);
     uint64_t bad = 0;
     for (size_t r = 0; r < sp.src.size(); ++r) {
         th[r] = values[3 * (size_t)sp.src[r]];
@@ -1032,14 +1037,17 @@ static int run_small(qsv_state *s, const ProgramTemplate &t, const double *value
         bad |= (uint64_t)(((bits >> 52) & 0x7ffu) == 0x7ffu);
     }
     if (bad) return fail_code(QSV_ERR_INVALID, "non-finite gate parameter");
-    char *d = nullptr;
-    size_t scratch = 0;
-    if (int rc = upload_blob(*c, s->stream, b, 0, &d, &scratch)) return rc;
+    prof.mark("gather");
+    QSV_CUDA(cudaMemcpyAsync(c->d_work, c->h_stage, bytes, cudaMemcpyHostToDevice, s->stream));
+    QSV_CUDA(cudaEventRecord(c->stage_ev, s->stream));
+    c->stage_pending = true;
+    prof.mark("h2d");
     const char *k = dc->base;
     QSV_CUDA(launch_small(s->amps, s->n, basis, sp, (const SmallGroup *)(k + dc->o_groups),
-                          (const int32_t *)(k + dc->o_meta), (const double *)(d + o_t),
+                          (const int32_t *)(k + dc->o_meta), (const double *)c->d_work,
                           (const int32_t *)(k + dc->o_runs), (const uint32_t *)(k + dc->o_xo),
                           (const uint32_t *)(k + dc->o_tab), s->stream));
+    prof.mark("launch");
     ++g_small_launches;
     return QSV_OK;
 }
