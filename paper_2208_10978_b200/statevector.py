@@ -642,16 +642,18 @@ def _rotation_gradient(c, theta, apply_h, s0: StateVector, prog) -> np.ndarray:
 
     x, y, z, rz = prog
     bound = bind(c, theta)
-    values = bound.flat()[2]
-    angles = np.ascontiguousarray(values[3 * rz])
+    plan = _bind_plan(c)
+    block_of_slot = np.searchsorted(3 * rz, plan.slot)
+    # the block angles straight from the bound Affine slots (no 3 x gates array)
+    angles = np.ascontiguousarray(plan.const[3 * rz])
+    if len(plan.slot):
+        angles[block_of_slot] = bound._slot_values
     psi = evolve(s0, bound)
     lam = apply_h(psi)
     g = np.zeros(len(rz), dtype=np.float64)
     _lib.check(_lib.lib().qsv_rotation_adjoint(psi.handle, lam.handle, len(rz), _lib.u64ptr(x),
                                                _lib.u64ptr(y), _lib.u64ptr(z), _lib.dptr(angles),
                                                _lib.dptr(g)))
-    plan = _bind_plan(c)
-    block_of_slot = np.searchsorted(3 * rz, plan.slot)
     grad = np.zeros(c.n_params, dtype=np.float64)
     np.add.at(grad, plan.index, plan.scale * g[block_of_slot])
     return grad
