@@ -1383,14 +1383,18 @@ static int expectation_small(const qsv_state *s, DeviceCtx &c, int64_t S, const 
                              const uint64_t *z, const double *coef_re, const double *coef_im, double *out_re,
                              double *out_im, double *per_term, qsv_plan_stats *stats)
 {
+    HostProfile prof("expectation_small");
     const uint32_t *d_rec = nullptr;
     if (int rc = small_exp_records(s, S, x, y, z, &d_rec)) return rc;
+    prof.mark("records");
     // the kernel writes the per-term values straight into the pinned staging
     // buffer (host memory the device addresses under UVA): no D2H copy call
     if (int rc = ensure_stage(c, (size_t)S * 8)) return rc;
     QSV_CUDA(launch_expect_small(s->amps, s->n, d_rec, (int)S, (double *)c.h_stage, num_sms(s->device),
                                  s->stream));
+    prof.mark("launch");
     QSV_CUDA(cudaStreamSynchronize(s->stream));
+    prof.mark("sync");
     std::vector<double> vals(S);
     std::memcpy(vals.data(), c.h_stage, (size_t)S * 8);
     finish_expectation(vals, S, coef_re, coef_im, out_re, out_im, per_term);

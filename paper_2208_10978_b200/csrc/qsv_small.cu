@@ -68,39 +68,71 @@ constexpr size_t kSmallMaxTable = (size_t)16 << 20;  // per-thread table entries
 namespace {
 
 // Small-state expectation (n <= 12: the state is <= 64 KiB and stays in L1):
-// one warp per string, <P_t> = Re sum_i conj(psi_i) i^ny (-1)^{|(i^f) & m|}
-// psi_{i^f} over all i, lanes striding i (coalesced; the partner reads are a
-// permutation inside the same lines), a fixed shuffle tree per string, so the
-// values are deterministic.  rec[t] = {flip, sign mask, ny mod 4}.  One launch
-// replaces the sweep + column-reduction pairs of the general path.
-__global__ void __launch_bounds__(512) expect_small_kernel(const double2 *__restrict__ psi, uint32_t dim,
-                                                           const uint4 *__restrict__ rec, int S,
-                                                           double *__restrict__ out)
+// one CTA of 256 threads per string (grid-stride over strings).  For a flip
+// f != 0 the pairs (i, i ^ f) contribute complex-conjugate terms (P is
+// Hermitian), so <P_t> = sum over the lows i (bit h of i = 0) of
+// 2 Re(conj(psi_i) i^ny (-1)^{|(i^f) & m|} psi_{i^f}) -- half the elements;
+// Z-only strings sum |psi_i|^2 signs over all i.  Each thread keeps two
+// independent partial sums (short dependent chains), then a fixed-order
+// block reduction (warp shuffles, 8 warp partials in order): deterministic.
+// rec[t] = {flip, sign mask, ny mod 4}.  One launch replaces the sweep +
+// column-reduction pairs of the general path.
+constexpr int kExpT = 256;
+__global__ void __launch_bounds__(kExpT) expect_small_kernel(const double2 *__restrict__ psi, uint32_t dim,
+                                                             const uint4 *__restrict__ rec, int S,
+                                                             double *__restrict__ out)
 {
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < S; t += gridDim.x * wpb) {
+    __shared__ double red[kExpT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int t = blockIdx.x; t < S; t += gridDim.x) {
         const uint4 r = __ldg(rec + t);
         const uint32_t f = r.x, m = r.y, ny = r.z;
-        double acc = 0.0;
-        if (ny & 1) {  // i^ny = +-i: the imaginary part of conj(a) b
-            for (uint32_t i = lane; i < dim; i += 32) {
-                const double2 a = __ldg(psi + i), b = __ldg(psi + (i ^ f));
-                const double q = fma(a.x, b.y, -a.y * b.x);
-                acc += (__popc((i ^ f) & m) & 1) ? -q : q;
+        double a0 = 0.0, a1 = 0.0;
+        if (f != 0) {
+            const int h = 31 - __clz(f);
+            const uint32_t lowm = (1u << h) - 1u;
+            const uint32_t npairs = dim >> 1;
+            for (uint32_t p = threadIdx.x; p < npairs; p += 2 * kExpT) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t q = p + (uint32_t)u * kExpT;
+                    if (q >= npairs) break;
+                    const uint32_t i = ((q & ~lowm) << 1) | (q & lowm), j = i ^ f;
+                    const double2 x = __ldg(psi + i), y = __ldg(psi + j);
+                    // Re(i^ny conj(x) y): P = Re conj(x) y, Q = Im conj(x) y
+                    double v = (ny & 1) ? fma(x.x, y.y, -x.y * y.x) : fma(x.x, y.x, x.y * y.y);
+                    if (ny == 1 || ny == 2) v = -v;
+                    if (__popc(j & m) & 1) v = -v;
+                    if (u == 0) a0 += v; else a1 += v;
+                }
             }
-            if (ny == 1) acc = -acc;  // Re(i (P + iQ)) = -Q, Re(-i (P + iQ)) = Q
+            a0 *= 2.0;
+            a1 *= 2.0;
         } else {
-            for (uint32_t i = lane; i < dim; i += 32) {
-                const double2 a = __ldg(psi + i), b = __ldg(psi + (i ^ f));
-                const double p = fma(a.x, b.x, a.y * b.y);
-                acc += (__popc((i ^ f) & m) & 1) ? -p : p;
+            for (uint32_t i = threadIdx.x; i < dim; i += 2 * kExpT) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t k = i + (uint32_t)u * kExpT;
+                    if (k >= dim) break;
+                    const double2 x = __ldg(psi + k);
+                    double v = fma(x.x, x.x, x.y * x.y);
+                    if (__popc(k & m) & 1) v = -v;
+                    if (u == 0) a0 += v; else a1 += v;
+                }
             }
-            if (ny == 2) acc = -acc;
         }
+        double acc = a0 + a1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) out[t] = acc;
+        if (lane == 0) red[warp] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < kExpT / 32; ++w) v += red[w];
+            out[t] = v;
+        }
+        __syncthreads();  // red is reused by the next string
     }
 }
 
@@ -110,9 +142,8 @@ cudaError_t launch_expect_small(const double2 *psi, int n, const uint32_t *rec, 
                                 cudaStream_t st)
 {
     if (S <= 0) return cudaSuccess;
-    const int warps = 16;
-    const int grid = std::max(1, std::min((S + warps - 1) / warps, 2 * sms));
-    expect_small_kernel<<<grid, 32 * warps, 0, st>>>(psi, 1u << n, reinterpret_cast<const uint4 *>(rec), S, out);
+    const int grid = std::max(1, std::min(S, 8 * sms));
+    expect_small_kernel<<<grid, kExpT, 0, st>>>(psi, 1u << n, reinterpret_cast<const uint4 *>(rec), S, out);
     return cudaGetLastError();
 }
 
