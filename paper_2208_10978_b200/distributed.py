@@ -148,6 +148,11 @@ class CudaEngine:
         return shard.amplitudes
 
 
+# CUDA IPC unavailable here (a rank could not export or map a shard): every
+# later relayout takes the NCCL path (all ranks see the same failure report)
+_IPC_BROKEN = False
+
+
 # ---------------------------------------------------------------------------
 # communicators
 # ---------------------------------------------------------------------------
@@ -638,9 +643,7 @@ class DistStateVector:
                         self._swap_local(views[r], views[p], c * chunk, rs * chunk, chunk)
                 else:
                     remote.setdefault(r, []).append((c, p))
-        if remote and self._ipc_enabled():
-            self._ipc_exchange(remote, chunk, s_value)
-        elif remote:
+        if remote and not (self._ipc_enabled() and self._ipc_exchange(remote, chunk, s_value)):
             self._p2p_exchange(views, remote, chunk)
         self._sync_after(views)
         self.stats["relayouts"] += 1
@@ -670,9 +673,9 @@ class DistStateVector:
         place over peer memory (CUDA IPC + swap kernel) instead of NCCL
         send/recv through staging.  QSV_DIST_IPC=0 keeps the NCCL path."""
         return (isinstance(self.engine, CudaEngine) and isinstance(self.comm, ProcessGroupComm)
-                and os.environ.get("QSV_DIST_IPC", "1") != "0")
+                and os.environ.get("QSV_DIST_IPC", "1") != "0" and not _IPC_BROKEN)
 
-    def _ipc_exchange(self, remote, chunk, s_value) -> None:
+    def _ipc_exchange(self, remote, chunk, s_value) -> bool:
         """Pairwise in-place chunk swap over peer memory: every rank exports
         its shard (qsv_ipc_get_handle), maps its partners' (qsv_ipc_open, for
         this exchange only) and swaps its half of each pair with the swap kernel
@@ -680,36 +683,52 @@ class DistStateVector:
         so each byte is read and written once per side with no staging copy
         and both directions of every link busy.  Ordering: every rank drains
         its stream and meets the others at a barrier before any swap, and
-        again after its own swaps -- no kernel ever waits on another rank."""
+        again after its own swaps -- no kernel ever waits on another rank.
+        Every rank reports whether it could export and map; if any could not
+        (no IPC in this environment), all return False before touching data
+        and the caller takes the NCCL path."""
         from . import _lib
 
+        global _IPC_BROKEN
         r = self.comm.rank
         shard = self.shards[r]
         L = _lib.lib()
-        h = (ctypes.c_char * 64)()
-        _lib.check(L.qsv_ipc_get_handle(shard.handle, h))
-        handles = self.comm.gather_arrays({r: bytes(h)})
-        shard.synchronize()
-        self.comm.barrier()  # every shard's earlier work is done
-        rs = s_value(r)
-        half = chunk // 2
         dev = self.engine.device
-        mapped = []
+        h = (ctypes.c_char * 64)()
+        ok = L.qsv_ipc_get_handle(shard.handle, h) == 0
+        handles = self.comm.gather_arrays({r: bytes(h) if ok else None})
+        if any(x is None for x in handles):
+            _IPC_BROKEN = True
+            return False
+        mapped = {}
         try:
+            # (test hook: QSV_DIST_IPC_FAIL=<rank> makes that rank's mapping fail)
+            fail_here = os.environ.get("QSV_DIST_IPC_FAIL") == str(r)
             for c, p in remote[r]:
                 ptr = ctypes.c_void_p()
-                _lib.check(L.qsv_ipc_open(dev, handles[p], ctypes.byref(ptr)))
-                mapped.append(ptr)
+                if fail_here or L.qsv_ipc_open(dev, handles[p], ctypes.byref(ptr)) != 0:
+                    ok = False
+                    break
+                mapped[p] = ptr
+            if not all(self.comm.gather_arrays({r: ok})):
+                _IPC_BROKEN = True
+                return False
+            shard.synchronize()
+            self.comm.barrier()  # every shard's earlier work is done
+            rs = s_value(r)
+            half = chunk // 2
+            for c, p in remote[r]:
                 off, ln = (0, half) if p > r else (half, chunk - half)
-                _lib.check(L.qsv_swap_peer(shard.handle, c * chunk + off, ptr, rs * chunk + off, ln))
+                _lib.check(L.qsv_swap_peer(shard.handle, c * chunk + off, mapped[p], rs * chunk + off, ln))
                 self.stats["ipc_swaps"] = self.stats.get("ipc_swaps", 0) + 1
             shard.synchronize()
         finally:
             # a mapping pins the partner's allocation: unmap before the
             # partner may free its shard (128 GiB at config 5)
-            for ptr in mapped:
+            for ptr in mapped.values():
                 L.qsv_ipc_close(dev, ptr)
         self.comm.barrier()  # every half of every pair is swapped
+        return True
 
     def _p2p_exchange(self, views, remote, chunk):
         """Pairwise chunk swap with the remote partners, one bounded piece at

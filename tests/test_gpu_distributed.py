@@ -76,17 +76,22 @@ def _pg_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("ipc", ["1", "0"])
+@pytest.mark.parametrize("ipc", ["1", "0", "fail"])
 def test_process_group_sharded_on_device(D, ipc, monkeypatch):
     """ProcessGroupComm + CudaEngine across 2 processes (gloo plumbing, both
     on this GPU): the multi-process sharded path against the oracle, with the
     relayout chunks swapped in place over CUDA IPC peer memory (default) or,
-    with QSV_DIST_IPC=0, sent through host staging."""
+    with QSV_DIST_IPC=0, sent through host staging; "fail": rank 1 cannot map
+    its partner, so both ranks agree to fall back to the staged path."""
     import socket
 
     import torch.multiprocessing as mp
 
-    monkeypatch.setenv("QSV_DIST_IPC", ipc)
+    if ipc == "fail":
+        monkeypatch.setenv("QSV_DIST_IPC", "1")
+        monkeypatch.setenv("QSV_DIST_IPC_FAIL", "1")
+    else:
+        monkeypatch.setenv("QSV_DIST_IPC", ipc)
 
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -111,7 +116,7 @@ def test_process_group_sharded_on_device(D, ipc, monkeypatch):
         assert np.abs(amps - ref).max() < 1e-10
         assert abs(e - e_ref) <= 1e-10 * max(1.0, abs(e_ref))
         assert nrel >= 1
-        assert (nswap > 0) == (ipc == "1")
+        assert (nswap > 0) == (ipc == "1")  # "fail": no swap kernels, the staged path ran
 
 
 @pytest.mark.parametrize("P", [2, 8])
