@@ -1428,6 +1428,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
     if (s->n <= kSmallMaxQubits && small_expect_enabled())
         return expectation_small(s, *c, S, x, y, z, coef_re, coef_im, out_re, out_im, per_term, stats);
 
+    HostProfile prof("expectation");
     const uint64_t h = hash_masks(s->n, S, x, y, z);
     const bool jit = jit_enabled(s->n);
     const std::string knobs = planner_knobs();
@@ -1472,6 +1473,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
         if (!srcs.empty() && jit_prepare(s->device, srcs, err) && getenv("QSV_JIT_VERBOSE"))
             fprintf(stderr, "qsv jit: %s\n", err.c_str());
     }
+    prof.mark("plan");
     // blob: per sweep groups / terms / map / gflip
     Blob b;
     struct Off { size_t g, t, m, f, off, comp; int rows; };
@@ -1505,6 +1507,7 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
         return rc;
     double *d_per_term = (double *)(d + scratch);
     double *d_partial = (double *)(d + scratch + per_term_bytes);
+    prof.mark("upload");
     for (size_t k = 0; k < plan->size(); ++k) {
         const SweepPlan &sp = (*plan)[k];
         const Off &o = offs[k];
@@ -1534,10 +1537,12 @@ int qsv_expectation(const qsv_state *s, int64_t S, const uint64_t *x, const uint
         QSV_CUDA(launch_reduce_columns(d_partial, rows, nterms, (const int32_t *)(d + o.m),
                                        d_per_term, s->stream));
     }
+    prof.mark("launches");
     std::vector<double> vals(S);
     if (int rc = ensure_stage(*c, (size_t)S * 8)) return rc;
     QSV_CUDA(cudaMemcpyAsync(c->h_stage, d_per_term, (size_t)S * 8, cudaMemcpyDeviceToHost, s->stream));
     QSV_CUDA(cudaStreamSynchronize(s->stream));
+    prof.mark("sync");
     std::memcpy(vals.data(), c->h_stage, (size_t)S * 8);
     finish_expectation(vals, S, coef_re, coef_im, out_re, out_im, per_term);
     qsv_plan_stats st{};
