@@ -128,6 +128,33 @@ def test_vectorised_bind_matches_per_gate_evaluation():
     assert cfg["circuit"].n_qubits == 8
 
 
+def test_lazy_bind_values_are_per_circuit():
+    """bind evaluates only the Affine slots: each BoundCircuit keeps its own
+    values (successive binds of one parametric circuit do not share a value
+    array), the full array built on demand equals the engine-call buffer
+    (call_values, the plan's reused scratch), and both equal per-gate
+    evaluation."""
+    from paper_2208_10978_b200.circuit import evolution_gates
+
+    strings = W.ucc_rotation_strings(8, 4)
+    gates = []
+    for k, st in enumerate(strings):
+        gates.extend(evolution_gates(st, Affine(k, -0.5, 0.1)))
+    c = Circuit(8, tuple(gates), len(strings))
+    rng = np.random.default_rng(1)
+    t1, t2 = rng.uniform(-1, 1, len(strings)), rng.uniform(-1, 1, len(strings))
+    b1, b2 = bind(c, t1), bind(c, t2)
+    with b2.call_values() as v:  # fills the shared scratch with b2's slots
+        v2_call = v.copy()
+    with b1.call_values() as v:  # ... then with b1's
+        v1_call = v.copy()
+    v1, v2 = b1.flat()[2], b2.flat()[2]
+    assert v1 is not v2 and np.array_equal(v1, v1_call) and np.array_equal(v2, v2_call)
+    for i, g in enumerate(c.gates):
+        for j, p in enumerate(g.params):
+            assert v1[3 * i + j] == p.evaluate(t1) and v2[3 * i + j] == p.evaluate(t2)
+
+
 def _ref_engine():
     import os
     import sys
